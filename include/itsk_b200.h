@@ -1,0 +1,195 @@
+/*
+ * itsk_b200.h — C ABI of the B200-native iterative-sketching least-squares
+ * path (libitsk_b200.so, sm_100a).
+ *
+ * The reference (arXiv 2311.04362 package `itsketch`) is pure Python: its
+ * drop-in boundary is the function API
+ *   iterative_sketching(a, b, cfg, truth) -> SolveResult
+ * (/root/reference/pkg/src/itsketch/solvers.py:323-345), which calls the
+ * pieces below.  Each entry point names the reference routine it replaces.
+ * The Python host layer (paper_2311_04362_b200/) binds these with ctypes and
+ * mirrors the reference's Python API; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ *     tensor) unless documented otherwise; matrices are row-major fp64 with an
+ *     explicit leading dimension (elements), as numpy C-order arrays are;
+ *   - every call is asynchronous on `stream` unless documented otherwise;
+ *   - return value: ITSK_OK or an ITSK_E* status; itsk_last_error() gives a
+ *     thread-local message.  No C++ exception crosses the ABI;
+ *   - no global mutable state besides the launch counter and the per-thread
+ *     error string: calls on different streams/workspaces are independent.
+ */
+#ifndef ITSK_B200_H_
+#define ITSK_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* itsk_stream_t; /* == cudaStream_t */
+
+enum {
+  ITSK_OK = 0,
+  ITSK_EINVAL = 1,    /* bad argument; maps to ValueError        */
+  ITSK_ESINGULAR = 2, /* exact zero on diag(R); SingularMatrixError (linalg.py:17-18,54-55) */
+  ITSK_ECUDA = 3,     /* CUDA runtime error                       */
+  ITSK_ENODEV = 4     /* no sm_100 device                         */
+};
+
+enum { ITSK_VARIANT_BASIC = 0, ITSK_VARIANT_WEIGHTED = 1 };
+
+enum { /* SolveTrace.stop_reason (solvers.py:72) */
+  ITSK_STOP_MAX_ITERS = 0,
+  ITSK_STOP_RULE = 1,
+  ITSK_STOP_DIVERGED = 2
+};
+
+const char* itsk_last_error(void);
+int itsk_version(void);
+/* 0 if device `dev` is an sm_100 part this library was built for. */
+int itsk_device_check(int dev);
+/* Number of kernels launched through this library so far (process-wide). */
+int64_t itsk_launch_count(void);
+
+/* ----------------------------------------------------------------------
+ * Sparse sign embedding pattern — replaces sparse_sign_new
+ * (embed.py:83-99) with _distinct_rows (embed.py:28-42): the exact numpy
+ * Generator(PCG64) stream (32-bit buffered Lemire draws, whole-column
+ * redraws of columns holding a repeat, then choice([-1,1]) signs),
+ * generated on the device by jump-ahead.  pcg[0..3] = state_hi, state_lo,
+ * inc_hi, inc_lo of default_rng(seed).bit_generator.state.
+ * Outputs: rows/neg in the reference's (m, zeta) order; sk_ptr/sk_src the
+ * same pattern grouped by sketch row (CSR of S), sources ascending, sign in
+ * bit 31.  Synchronises `stream` (the redraw loop is data dependent).
+ * -------------------------------------------------------------------- */
+int itsk_pattern_workspace(int64_t d, int64_t m, int64_t zeta, int64_t* bytes);
+int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, const uint64_t pcg[4],
+                             int has_uint32, uint32_t uinteger, uint32_t* rows,
+                             uint8_t* neg, uint32_t* sk_ptr, uint32_t* sk_src, void* ws,
+                             int64_t ws_bytes, itsk_stream_t stream);
+
+/* ----------------------------------------------------------------------
+ * S·[A | b] — replaces SparseSignEmbedding.apply_dense / apply_vec
+ * (embed.py:62-74 → scipy csc_matvecs), called from sketch_and_solve
+ * (solvers.py:207-208).  SAb is d x (n + (b != NULL)), leading dim ldw.
+ * Summation order equals the reference's (ascending source row, product
+ * rounded before the add), so SAb is bitwise identical to scipy's.
+ * Rows [row0, row0+m) of the full matrix are the local shard (multi-GPU);
+ * sk_ptr/sk_src must then be the shard's own pattern.
+ * -------------------------------------------------------------------- */
+int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
+                double* SAb, int64_t ldw, itsk_stream_t stream);
+
+/* ----------------------------------------------------------------------
+ * Householder QR of the d x n sketch with the reflectors also applied to
+ * column n (Sb) — replaces householder_qr_econ (linalg.py:30-47, LAPACK
+ * dgeqrf+dorgqr, diag(R) >= 0) and Q'·Sb (solvers.py:209).  W (d x (n+1),
+ * ldw) is overwritten.  R: n x n row-major (ld n), upper, diag >= 0.
+ * z = (Q'Sb)[:n] with the same sign fix.  Returns ITSK_ESINGULAR (after
+ * synchronising) if some R_kk == 0, like _check_square_upper.
+ * -------------------------------------------------------------------- */
+int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes);
+int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
+                void* ws, int64_t ws_bytes, itsk_stream_t stream);
+
+/* tri_solve_upper (linalg.py:59-62, trans=0: R y = c) and
+ * tri_solve_upper_transpose (linalg.py:65-68, trans=1: R' y = c). */
+int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
+              itsk_stream_t stream);
+/* solve_step (solvers.py:339-340): y = R^{-1} R^{-T} c. */
+int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
+                   itsk_stream_t stream);
+
+/* rand_power_norm_est (linalg.py:79-105) with the start vector v0 (host
+ * numpy default_rng(seed).standard_normal(n)), `steps` power steps; the
+ * result is written to *out (device scalar). ws: 3n doubles. */
+int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps, double* out,
+                 double* ws, itsk_stream_t stream);
+/* cond_est (linalg.py:108-113): sigma_max/sigma_min of R from Lanczos on
+ * R'R and on R^{-1}R^{-T}, to rounding for the spectra of this path;
+ * *out (device).  ws: itsk_condest_workspace doubles. */
+int itsk_condest_workspace(int64_t n, int64_t* doubles);
+int itsk_condest(const double* R, int64_t n, const double* v0, double* out, double* ws,
+                 itsk_stream_t stream);
+
+/* ----------------------------------------------------------------------
+ * The fused pass of the refinement loop (solvers.py:290,299,343 — r = b-Ax
+ * and A'r — plus the norms of solvers.py:300-302 and _record's RE):
+ *   r = b - A x;  c = A' r;  scal = [|r|^2, |r - r_prev|^2, |r_true - r|^2]
+ * one streaming read of A.  r_prev, r_out, r_true may be NULL.  Partials of
+ * c/scal per CTA go to `part`; itsk_pass_finalize sums them in fixed order
+ * (deterministic) into cs = [c(n) | scal(3)].
+ * -------------------------------------------------------------------- */
+int itsk_pass_workspace(int64_t m, int64_t n, int64_t* bytes);
+int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                    const double* x, const double* r_prev, double* r_out,
+                    const double* r_true, double* cs, void* ws, int64_t ws_bytes,
+                    itsk_stream_t stream);
+
+/* ----------------------------------------------------------------------
+ * Device-resident refinement loop (_run_refinement, solvers.py:270-320).
+ * State, constants and trace live in device memory; the loop runs as one
+ * CUDA graph with a conditional WHILE node (no host round trip per
+ * iteration), or step-wise for multi-GPU (collective between pre and post).
+ * -------------------------------------------------------------------- */
+typedef struct itsk_loop_params {
+  int64_t m, n, lda;        /* local rows on this rank */
+  int64_t max_iters, extra_iters;
+  int32_t variant;          /* ITSK_VARIANT_* (solvers.py:295-298)           */
+  int32_t r_slots;          /* rows of rs: max_iters+1 (keep all) or 2       */
+  double alpha, beta;       /* _update_coeffs (solvers.py:259-267)           */
+  double u, gamma, rho;     /* should_stop (solvers.py:174-192)              */
+  double truth_beta;        /* Truth.beta; RE = |r*-r|/beta, or |r|/|b| if 0 */
+  int32_t has_truth;
+  const double* A;
+  const double* b;
+  const double* R;          /* n x n, ld n                                   */
+  const double* x_true;     /* n, nullable                                   */
+  const double* r_true;     /* m (local), nullable                           */
+  const double* normest;    /* device scalars from itsk_normest/itsk_condest */
+  const double* condest;
+  double* xs;               /* (max_iters+1) x n, xs[0] = x0 on entry        */
+  double* rs;               /* r_slots x m                                   */
+  double* trace;            /* 4 x (max_iters+1): fe, re, change, |r|        */
+  double* cs;               /* n + 8: reduced [c | scal]; the collective's buffer */
+  void* ws;                 /* itsk_loop_workspace bytes                     */
+  int64_t ws_bytes;
+} itsk_loop_params;
+
+typedef struct itsk_loop_result { /* read back with one D2H copy */
+  int32_t iterations;  /* len(iterates) - 1                       */
+  int32_t stop_reason; /* ITSK_STOP_*                             */
+  int32_t done;
+  int32_t sol_slot;    /* xs row holding SolveResult.solution     */
+  double bnorm2;
+  double pad[3];
+} itsk_loop_result;
+
+int itsk_loop_workspace(int64_t m, int64_t n, int64_t* bytes);
+/* Writes constants, r0 = b - A x0 (fused pass) and records iterate 0.
+ * For multi-GPU call itsk_loop_begin_local, allreduce p->cs, then
+ * itsk_loop_begin_finish. */
+int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream);
+int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t stream);
+int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream);
+/* One iteration, split around the collective: pre = two TRSVs, update,
+ * fused pass + local finalize into p->cs; post = guard, stopping rule,
+ * trace.  Both are no-ops once the loop is done. */
+int itsk_loop_step_pre(const itsk_loop_params* p, itsk_stream_t stream);
+int itsk_loop_step_post(const itsk_loop_params* p, itsk_stream_t stream);
+/* Whole loop as a CUDA graph (conditional WHILE); the handle caches the
+ * instantiated graph for repeated solves on the same buffers. */
+int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t stream, void** handle);
+int itsk_loop_graph_launch(void* handle, itsk_stream_t stream);
+void itsk_loop_graph_destroy(void* handle);
+/* Device pointer of the itsk_loop_result inside the loop workspace. */
+int itsk_loop_result_ptr(const itsk_loop_params* p, itsk_loop_result** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ITSK_B200_H_ */

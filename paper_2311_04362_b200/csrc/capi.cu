@@ -1,0 +1,63 @@
+// Process-level pieces of the C ABI: error strings, version, device check,
+// launch counter.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "itsk_common.cuh"
+
+namespace itsk {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+void count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+int num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      cached = v;
+    else
+      cached = 148;
+  }
+  return cached;
+}
+
+}  // namespace itsk
+
+extern "C" const char* itsk_last_error(void) { return itsk::g_err; }
+
+extern "C" int itsk_version(void) { return 100; }
+
+extern "C" int64_t itsk_launch_count(void) {
+  return itsk::g_launches.load(std::memory_order_relaxed);
+}
+
+extern "C" int itsk_device_check(int dev) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= dev) {
+    itsk::set_error("no CUDA device %d", dev);
+    return ITSK_ENODEV;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+    itsk::set_error("cudaGetDeviceProperties failed");
+    return ITSK_ENODEV;
+  }
+  if (prop.major != 10 || prop.minor != 0) {
+    itsk::set_error("device %d is sm_%d%d; this library is built for sm_100a only", dev,
+                    prop.major, prop.minor);
+    return ITSK_ENODEV;
+  }
+  return ITSK_OK;
+}

@@ -1,0 +1,72 @@
+// Internal declarations shared by the .cu files (not part of the C ABI).
+#pragma once
+#include "itsk_common.cuh"
+
+namespace itsk {
+
+// Device-resident loop control block (lives in the loop workspace).
+struct LoopCtl {
+  // constants (written by k_loop_init)
+  int64_t m, n, max_iters, extra_iters;
+  int32_t variant, r_slots, has_truth, has_xtrue;
+  double alpha, beta, u, gamma, rho, truth_beta;
+  // state
+  int32_t it;         // completed iterations; current iterate is xs[it]
+  int32_t countdown;  // -1 == None (solvers.py:292)
+  int32_t nhist;      // divergence-guard history length
+  int32_t pad0;
+  double hist[8];     // ring of the last 6 residual norms (solvers.py:223-238)
+  double lo;          // running minimum
+  double xtnorm;      // ||x_true||
+  itsk_loop_result result;
+};
+
+// Pointers the per-iteration kernels resolve from ctl->it.
+struct LoopPtrs {
+  const double* A;
+  const double* b;
+  const double* R;
+  const double* x_true;
+  const double* r_true;
+  const double* normest;
+  const double* condest;
+  double* xs;
+  double* rs;
+  double* trace;
+  double* cs;
+  double* step;  // n: R^{-1}R^{-T} c
+  double* part;  // pass partials
+  LoopCtl* ctl;
+  int64_t lda;
+};
+
+int launch_trsv_pair_device(const double* R, int64_t n, const double* c, double* y,
+                            cudaStream_t s);
+
+// Fused pass.  When ctl != nullptr the x / r_prev / r_out pointers are
+// resolved on the device from ctl->it (graph-capturable loop body) and the
+// kernel is a no-op once ctl->result.done is set.
+struct PassArgs {
+  const double* A;
+  int64_t m, n, lda;
+  const double* b;
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  const double* r_true;
+  double* part;  // grid x (n + 4)
+  int64_t rows_per_cta;
+  // loop mode
+  const LoopCtl* ctl;
+  const double* xs;
+  double* rs;
+  int mode;  // 0 = explicit pointers, 1 = loop step (x = xs[it+1]), 2 = loop begin (x = xs[0])
+};
+
+int pass_grid(int64_t m, int64_t n);
+int64_t pass_part_doubles(int64_t m, int64_t n);
+int launch_pass(const PassArgs& a, cudaStream_t s);
+int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
+                    cudaStream_t s);
+
+}  // namespace itsk

@@ -1,0 +1,441 @@
+// Device-resident refinement loop (K5): _run_refinement
+// (/root/reference/pkg/src/itsketch/solvers.py:270-320).
+//
+// One iteration = k_step_trsv (d = R^{-1}R^{-T} c, solvers.py:294/339-340)
+//               -> k_update   (x+ = x + d  |  x + alpha d + beta (x - x-), :295-298)
+//               -> fused pass (r+ = b - A x+, c+ = A'r+, norms; :299-302, :343)
+//               -> finalize   (fixed-order reduction of the pass partials)
+//               -> k_control  (divergence guard :302-305, _record :241-256,
+//                              stopping rule + extra_iters countdown :308-318)
+// All loop state (iteration counter, guard history, countdown, stop reason)
+// lives in a LoopCtl block in device memory, so the whole loop runs as one
+// CUDA graph whose WHILE conditional node is cleared by k_control — no host
+// round trip per iteration.  For multi-GPU the host calls step_pre, sums
+// p->cs across ranks (the only collective), then step_post.
+#include <algorithm>
+
+#include "itsk_common.cuh"
+#include "itsk_dense.cuh"
+#include "itsk_kernels.cuh"
+
+namespace itsk {
+namespace {
+
+constexpr int CTRL_THREADS = 256;
+
+__global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iters,
+                            int64_t extra_iters, int variant, int r_slots, int has_truth,
+                            int has_xtrue, double alpha, double beta, double u, double gamma,
+                            double rho, double truth_beta) {
+  ctl->m = m;
+  ctl->n = n;
+  ctl->max_iters = max_iters;
+  ctl->extra_iters = extra_iters;
+  ctl->variant = variant;
+  ctl->r_slots = r_slots;
+  ctl->has_truth = has_truth;
+  ctl->has_xtrue = has_xtrue;
+  ctl->alpha = alpha;
+  ctl->beta = beta;
+  ctl->u = u;
+  ctl->gamma = gamma;
+  ctl->rho = rho;
+  ctl->truth_beta = truth_beta;
+  ctl->it = 0;
+  ctl->countdown = -1;
+  ctl->nhist = 0;
+  for (int i = 0; i < 8; ++i) ctl->hist[i] = 0.0;
+  ctl->lo = INFINITY;
+  ctl->xtnorm = 0.0;
+  ctl->result.iterations = 0;
+  ctl->result.stop_reason = ITSK_STOP_MAX_ITERS;
+  ctl->result.done = 0;
+  ctl->result.sol_slot = 0;
+  ctl->result.bnorm2 = 0.0;
+}
+
+__global__ void __launch_bounds__(1024) k_step_trsv(LoopPtrs p) {
+  if (p.ctl->result.done) return;
+  extern __shared__ double sm[];
+  const int64_t n = p.ctl->n;
+  double* v = sm;
+  double* tmp = sm + n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
+  __syncthreads();
+  trsv_t_inplace(p.R, n, v);
+  trsv_n_inplace(p.R, n, v, tmp);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p.step[i] = v[i];
+}
+
+// x_{i+1} in the reference's exact operation order (no FMA contraction).
+__global__ void k_update(LoopPtrs p) {
+  const LoopCtl* ctl = p.ctl;
+  if (ctl->result.done) return;
+  const int64_t n = ctl->n, it = ctl->it;
+  const double* x = p.xs + it * n;
+  const double* xp = p.xs + (it > 0 ? it - 1 : 0) * n;
+  double* xn = p.xs + (it + 1) * n;
+  const double alpha = ctl->alpha, beta = ctl->beta;
+  const bool basic = ctl->variant == ITSK_VARIANT_BASIC;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double xi = x[i], di = p.step[i];
+    if (basic) {
+      xn[i] = __dadd_rn(xi, di);
+    } else {
+      const double t = __dadd_rn(xi, __dmul_rn(alpha, di));
+      xn[i] = __dadd_rn(t, __dmul_rn(beta, __dsub_rn(xi, xp[i])));
+    }
+  }
+}
+
+// Guard + record + stopping rule.  begin == 1 records iterate 0 only.
+__global__ void __launch_bounds__(CTRL_THREADS) k_control(LoopPtrs p, int begin,
+                                                          cudaGraphConditionalHandle h,
+                                                          int use_cond) {
+  LoopCtl* ctl = p.ctl;
+  __shared__ double red[CTRL_THREADS / 32];
+  __shared__ int s_done;
+  if (ctl->result.done) {
+    if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+    return;
+  }
+  const int64_t n = ctl->n, it = ctl->it;
+  const int64_t K = ctl->max_iters + 1;
+  const int64_t xi = begin ? 0 : it + 1;
+  const double* x = p.xs + xi * n;
+  double sx = 0.0, sf = 0.0, st = 0.0;
+  int fin = 1;
+  for (int64_t i = threadIdx.x; i < n; i += CTRL_THREADS) {
+    const double v = x[i];
+    sx += v * v;
+    fin &= isfinite(v) ? 1 : 0;
+    if (ctl->has_xtrue) {
+      const double e = p.x_true[i] - v;
+      sf += e * e;
+      if (begin) st += p.x_true[i] * p.x_true[i];
+    }
+  }
+  const double xnorm2 = block_sum(sx, red);
+  const double fe2 = block_sum(sf, red);
+  const double xt2 = block_sum(st, red);
+  const int all_fin = __syncthreads_and(fin);
+  if (threadIdx.x == 0) {
+    const double* cs = p.cs;
+    const double rr = cs[n], dd = cs[n + 1], tt = cs[n + 2], bb = cs[n + 3];
+    const double resnorm = sqrt(rr);
+    double* fe = p.trace;
+    double* re = p.trace + K;
+    double* ch = p.trace + 2 * K;
+    double* rn = p.trace + 3 * K;
+    if (begin) {
+      ctl->xtnorm = sqrt(xt2);
+      ctl->result.bnorm2 = bb;
+    }
+    const int64_t rec = begin ? 0 : it + 1;
+    if (ctl->has_xtrue) fe[rec] = sqrt(fe2) / ctl->xtnorm;
+    if (ctl->has_truth)
+      re[rec] = ctl->truth_beta > 0 ? sqrt(tt) / ctl->truth_beta : resnorm / sqrt(ctl->result.bnorm2);
+    rn[rec] = resnorm;
+    int done = 0;
+    if (begin) {
+      ctl->result.iterations = 0;
+      ctl->result.sol_slot = 0;
+      if (ctl->max_iters == 0) {
+        done = 1;
+        ctl->result.stop_reason = ITSK_STOP_MAX_ITERS;
+      }
+    } else {
+      const double change = sqrt(dd);
+      ch[it] = change;
+      // _DivergenceGuard.diverged (solvers.py:230-238)
+      bool diverged = !(isfinite(resnorm) && all_fin);
+      if (!diverged) {
+        ctl->hist[ctl->nhist % 8] = resnorm;
+        ctl->nhist += 1;
+        ctl->lo = fmin(ctl->lo, resnorm);
+        if (ctl->nhist > 5) {
+          const bool growing = resnorm > ctl->hist[(ctl->nhist - 6) % 8];
+          diverged = growing && resnorm > 1.0e4 * ctl->lo;
+        }
+      }
+      if (diverged) {
+        done = 1;
+        ctl->result.stop_reason = ITSK_STOP_DIVERGED;
+        ctl->result.iterations = static_cast<int32_t>(it + 1);
+        ctl->result.sol_slot = static_cast<int32_t>(it + 1);
+      } else {
+        const int64_t nit = it + 1;
+        ctl->it = static_cast<int32_t>(nit);
+        if (ctl->countdown < 0) {
+          // should_stop (solvers.py:174-192), evaluated left to right
+          const double bound = ctl->u * (ctl->gamma * (*p.normest) * sqrt(xnorm2) +
+                                         ctl->rho * (*p.condest) * resnorm);
+          if (change <= bound) ctl->countdown = static_cast<int32_t>(ctl->extra_iters);
+        }
+        if (ctl->countdown >= 0) {
+          if (ctl->countdown == 0) {
+            done = 1;
+            ctl->result.stop_reason = ITSK_STOP_RULE;
+          } else {
+            ctl->countdown -= 1;
+          }
+        }
+        if (!done && nit >= ctl->max_iters) {
+          done = 1;
+          ctl->result.stop_reason = ITSK_STOP_MAX_ITERS;
+        }
+        ctl->result.iterations = static_cast<int32_t>(nit);
+        ctl->result.sol_slot = static_cast<int32_t>(nit);
+      }
+    }
+    ctl->result.done = done;
+    s_done = done;
+    if (done && use_cond) cudaGraphSetConditional(h, 0);
+  }
+}
+
+struct LoopLayout {
+  LoopCtl* ctl;
+  double* step;
+  double* part;
+  int64_t bytes;
+};
+
+LoopLayout loop_layout(void* ws, int64_t m, int64_t n) {
+  Carver cv(ws, 1ll << 62);
+  LoopLayout L;
+  L.ctl = cv.take<LoopCtl>(1);
+  L.step = cv.take<double>(n + 32);
+  L.part = cv.take<double>(pass_part_doubles(m, n));
+  L.bytes = cv.off + 256;
+  return L;
+}
+
+int check_params(const itsk_loop_params* p) {
+  ITSK_REQUIRE(p, "null params");
+  ITSK_REQUIRE(p->m >= 1 && p->n >= 1 && p->lda >= p->n, "bad loop shape");
+  ITSK_REQUIRE(p->max_iters >= 0 && p->extra_iters >= 0, "bad iteration counts");
+  ITSK_REQUIRE(p->r_slots == 2 || p->r_slots >= p->max_iters + 1, "r_slots must be 2 or max_iters+1");
+  ITSK_REQUIRE(p->A && p->b && p->R && p->normest && p->condest && p->xs && p->rs && p->trace &&
+                   p->cs && p->ws,
+               "null pointer in loop params");
+  ITSK_REQUIRE(p->n <= 6000, "loop: n too large for the single-CTA solves");
+  int64_t need = loop_layout(nullptr, p->m, p->n).bytes;
+  ITSK_REQUIRE(need <= p->ws_bytes, "loop workspace too small");
+  return ITSK_OK;
+}
+
+LoopPtrs make_ptrs(const itsk_loop_params* p) {
+  LoopLayout L = loop_layout(p->ws, p->m, p->n);
+  LoopPtrs q;
+  q.A = p->A;
+  q.b = p->b;
+  q.R = p->R;
+  q.x_true = p->x_true;
+  q.r_true = p->r_true;
+  q.normest = p->normest;
+  q.condest = p->condest;
+  q.xs = p->xs;
+  q.rs = p->rs;
+  q.trace = p->trace;
+  q.cs = p->cs;
+  q.step = L.step;
+  q.part = L.part;
+  q.ctl = L.ctl;
+  q.lda = p->lda;
+  return q;
+}
+
+PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
+  PassArgs a{};
+  a.A = p->A;
+  a.m = p->m;
+  a.n = p->n;
+  a.lda = p->lda;
+  a.b = p->b;
+  a.r_true = p->r_true;
+  a.part = q.part;
+  a.ctl = q.ctl;
+  a.xs = p->xs;
+  a.rs = p->rs;
+  a.mode = mode;
+  return a;
+}
+
+size_t trsv_smem(int64_t n) { return static_cast<size_t>(n + 32) * sizeof(double); }
+
+int enqueue_pre(const itsk_loop_params* p, const LoopPtrs& q, cudaStream_t s) {
+  const size_t smem = trsv_smem(p->n);
+  k_step_trsv<<<1, 1024, smem, s>>>(q);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  const int ub = static_cast<int>(std::min<int64_t>((p->n + 255) / 256, 64));
+  k_update<<<ub, 256, 0, s>>>(q);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  int rc = launch_pass(pass_args(p, q, 1), s);
+  if (rc) return rc;
+  return launch_finalize(q.part, pass_grid(p->m, p->n), p->n, p->cs, q.ctl, s);
+}
+
+int prepare_attrs(int64_t n) {
+  const size_t smem = trsv_smem(n);
+  if (smem > 48 * 1024)
+    ITSK_CUDA(cudaFuncSetAttribute(k_step_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  return ITSK_OK;
+}
+
+struct GraphHandle {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+}  // namespace
+}  // namespace itsk
+
+using namespace itsk;
+
+extern "C" int itsk_loop_workspace(int64_t m, int64_t n, int64_t* bytes) {
+  ITSK_REQUIRE(bytes && m >= 1 && n >= 1, "bad loop shape");
+  *bytes = loop_layout(nullptr, m, n).bytes;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_result_ptr(const itsk_loop_params* p, itsk_loop_result** out) {
+  ITSK_REQUIRE(p && out && p->ws, "null pointer");
+  *out = &loop_layout(p->ws, p->m, p->n).ctl->result;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if ((rc = prepare_attrs(p->n))) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LoopPtrs q = make_ptrs(p);
+  k_loop_init<<<1, 1, 0, s>>>(q.ctl, p->m, p->n, p->max_iters, p->extra_iters, p->variant,
+                              p->r_slots, p->has_truth, p->x_true != nullptr, p->alpha, p->beta,
+                              p->u, p->gamma, p->rho, p->truth_beta);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  rc = launch_pass(pass_args(p, q, 2), s);
+  if (rc) return rc;
+  return launch_finalize(q.part, pass_grid(p->m, p->n), p->n, p->cs, q.ctl, s);
+}
+
+extern "C" int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LoopPtrs q = make_ptrs(p);
+  k_control<<<1, CTRL_THREADS, 0, s>>>(q, 1, cudaGraphConditionalHandle{}, 0);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = itsk_loop_begin_local(p, stream);
+  if (rc) return rc;
+  return itsk_loop_begin_finish(p, stream);
+}
+
+extern "C" int itsk_loop_step_pre(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if ((rc = prepare_attrs(p->n))) return rc;
+  LoopPtrs q = make_ptrs(p);
+  return enqueue_pre(p, q, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int itsk_loop_step_post(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  LoopPtrs q = make_ptrs(p);
+  k_control<<<1, CTRL_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      q, 0, cudaGraphConditionalHandle{}, 0);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t stream,
+                                      void** handle) {
+  (void)stream;
+  int rc = check_params(p);
+  if (rc) return rc;
+  ITSK_REQUIRE(handle, "null handle");
+  if ((rc = prepare_attrs(p->n))) return rc;
+  pass_grid(p->m, p->n);  // warm the occupancy cache outside capture
+  LoopPtrs q = make_ptrs(p);
+  GraphHandle* gh = new GraphHandle();
+  cudaStream_t cap = nullptr;
+  auto fail = [&](int code) {
+    if (cap) cudaStreamDestroy(cap);
+    if (gh->exec) cudaGraphExecDestroy(gh->exec);
+    if (gh->graph) cudaGraphDestroy(gh->graph);
+    delete gh;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaGraphCreate(&gh->graph, 0) != cudaSuccess) {
+    set_error("graph create failed");
+    return fail(ITSK_ECUDA);
+  }
+  cudaGraphConditionalHandle cond;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&cond, gh->graph, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (e == cudaSuccess) e = cudaGraphAddNode(&node, gh->graph, nullptr, 0, &np);
+  if (e != cudaSuccess) {
+    set_error("conditional node: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) {
+    set_error("capture begin: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
+  rc = enqueue_pre(p, q, cap);
+  if (rc == ITSK_OK) {
+    k_control<<<1, CTRL_THREADS, 0, cap>>>(q, 0, cond, 1);
+    count_launch();
+  }
+  cudaGraph_t captured = body;
+  e = cudaStreamEndCapture(cap, &captured);
+  if (rc != ITSK_OK) return fail(rc);
+  if (e != cudaSuccess) {
+    set_error("capture end: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
+  e = cudaGraphInstantiate(&gh->exec, gh->graph, 0);
+  if (e != cudaSuccess) {
+    set_error("graph instantiate: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
+  cudaStreamDestroy(cap);
+  *handle = gh;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_graph_launch(void* handle, itsk_stream_t stream) {
+  ITSK_REQUIRE(handle, "null handle");
+  GraphHandle* gh = static_cast<GraphHandle*>(handle);
+  ITSK_CUDA(cudaGraphLaunch(gh->exec, reinterpret_cast<cudaStream_t>(stream)));
+  return ITSK_OK;
+}
+
+extern "C" void itsk_loop_graph_destroy(void* handle) {
+  if (!handle) return;
+  GraphHandle* gh = static_cast<GraphHandle*>(handle);
+  if (gh->exec) cudaGraphExecDestroy(gh->exec);
+  if (gh->graph) cudaGraphDestroy(gh->graph);
+  delete gh;
+}

@@ -1,0 +1,390 @@
+// Sparse sign embedding pattern on the device.
+//
+// Replaces sparse_sign_new / _distinct_rows
+// (/root/reference/pkg/src/itsketch/embed.py:28-42, 83-99).  The reference
+// draws, from one numpy Generator(PCG64) seeded with `rng_seed`:
+//   rows  = integers(0, d, (m, zeta))        (32-bit buffered Lemire draws)
+//   while some column j holds a repeated row: rows[bad] = integers(0, d, (nbad, zeta))
+//   signs = choice([-1., 1.], (m, zeta))     (== integers(0, 2), no rejection)
+// All three consume one stream of 32-bit words (low half of each 64-bit PCG
+// output first, the other half buffered in the generator and carried across
+// calls).  Here every thread jumps ahead (LCG advance, O(log k)) to its own
+// chunk of that word stream; the rare Lemire rejections are resolved with a
+// prefix sum over per-chunk reject counts, so the output is bit-identical to
+// numpy's sequential loop.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "itsk_common.cuh"
+
+namespace itsk {
+namespace {
+
+typedef unsigned __int128 u128;
+constexpr int CH = 256;  // words per thread chunk
+
+__device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) {
+  return (static_cast<u128>(hi) << 64) | lo;
+}
+__device__ __forceinline__ u128 pcg_mult() {
+  return mk128(0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull);
+}
+__device__ __forceinline__ uint64_t pcg_output(u128 s) {
+  const uint64_t x = static_cast<uint64_t>(s >> 64) ^ static_cast<uint64_t>(s);
+  const unsigned rot = static_cast<unsigned>(s >> 122);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// State after `delta` LCG steps (Brown's jump-ahead).
+__device__ u128 pcg_advance(u128 s, u128 inc, uint64_t delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * s + acc_plus;
+}
+
+struct Stream {
+  uint64_t s_hi, s_lo, i_hi, i_lo;
+  uint32_t pending;
+  int has;  // numpy's has_uint32 at stream start
+};
+
+// Sequential reader of 32-bit words starting at absolute word index `w`.
+struct WordCursor {
+  u128 s, inc;
+  uint64_t buf;
+  int half;  // 1 when the high half of `buf` is the next word
+  uint32_t pending;
+  int use_pending;
+
+  __device__ WordCursor(const Stream& st, uint64_t w) {
+    inc = mk128(st.i_hi, st.i_lo);
+    const u128 s0 = mk128(st.s_hi, st.s_lo);
+    use_pending = (st.has && w == 0);
+    pending = st.pending;
+    const uint64_t k = (st.has && w > 0) ? w - 1 : (st.has ? 0 : w);
+    // base word k lives in output k>>1 (after (k>>1)+1 steps), half k&1.
+    const uint64_t o = k >> 1;
+    s = pcg_advance(s0, inc, o);  // state before producing output o
+    half = 0;
+    buf = 0;
+    if (!use_pending && (k & 1)) {
+      s = s * pcg_mult() + inc;
+      buf = pcg_output(s);
+      half = 1;
+    }
+  }
+  __device__ __forceinline__ uint32_t next() {
+    if (use_pending) {
+      use_pending = 0;
+      return pending;
+    }
+    if (half) {
+      half = 0;
+      return static_cast<uint32_t>(buf >> 32);
+    }
+    s = s * pcg_mult() + inc;
+    buf = pcg_output(s);
+    half = 1;
+    return static_cast<uint32_t>(buf);
+  }
+};
+
+__device__ __forceinline__ bool lemire_accept(uint32_t w, uint32_t bound, uint32_t thr,
+                                              uint32_t* out) {
+  const uint64_t prod = static_cast<uint64_t>(w) * bound;
+  *out = static_cast<uint32_t>(prod >> 32);
+  return static_cast<uint32_t>(prod) >= thr;
+}
+
+__global__ void k_lemire_count(Stream st, uint64_t w0, uint64_t nwords, uint32_t bound,
+                               uint32_t thr, uint32_t* counts, uint64_t nchunks) {
+  const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (c == 0) counts[nchunks] = 0;  // so the scan's last slot is the total
+  if (c >= nchunks) return;
+  const uint64_t beg = c * CH;
+  const uint64_t len = min(static_cast<uint64_t>(CH), nwords - beg);
+  uint32_t acc = 0;
+  if (thr != 0) {
+    WordCursor cur(st, w0 + beg);
+    for (uint64_t i = 0; i < len; ++i) {
+      uint32_t v;
+      acc += lemire_accept(cur.next(), bound, thr, &v) ? 1u : 0u;
+    }
+  } else {
+    acc = static_cast<uint32_t>(len);
+  }
+  counts[c] = acc;
+}
+
+// Emits accepted draws; draw q goes to dst[map(q)] where map is identity
+// (mode 0) or the q-th slot of the redrawn columns (mode 1).  Writes the
+// absolute word index following draw N-1 to *end_word.
+__global__ void k_lemire_emit(Stream st, uint64_t w0, uint64_t nwords, uint32_t bound,
+                              uint32_t thr, const uint32_t* scanned, uint64_t nchunks,
+                              uint64_t N, uint32_t* dst, const uint32_t* bad_cols,
+                              int64_t zeta, uint64_t* end_word) {
+  const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  uint64_t q = scanned[c];
+  if (q >= N) return;
+  const uint64_t beg = c * CH;
+  const uint64_t len = min(static_cast<uint64_t>(CH), nwords - beg);
+  WordCursor cur(st, w0 + beg);
+  for (uint64_t i = 0; i < len && q < N; ++i) {
+    uint32_t v;
+    if (!lemire_accept(cur.next(), bound, thr, &v)) continue;
+    uint64_t pos = q;
+    if (bad_cols) pos = static_cast<uint64_t>(bad_cols[q / zeta]) * zeta + (q % zeta);
+    dst[pos] = v;
+    if (q == N - 1) *end_word = w0 + beg + i + 1;
+    ++q;
+  }
+}
+
+// choice([-1., 1.]) → integers(0, 2): neg = (w >> 31) == 0, one word each.
+__global__ void k_signs(Stream st, uint64_t w0, uint64_t N, uint8_t* neg) {
+  const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t beg = c * CH;
+  if (beg >= N) return;
+  const uint64_t len = min(static_cast<uint64_t>(CH), N - beg);
+  WordCursor cur(st, w0 + beg);
+  for (uint64_t i = 0; i < len; ++i) neg[beg + i] = (cur.next() >> 31) == 0 ? 1 : 0;
+}
+
+__global__ void k_tile_rows(uint32_t* rows, int64_t m, int64_t zeta) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e < m * zeta) rows[e] = static_cast<uint32_t>(e % zeta);
+}
+
+// Flags columns (rows of the (m, zeta) array) holding a repeated value,
+// restricted to `cols` when non-null (only redrawn columns can change).
+__global__ void k_flag_dupes(const uint32_t* rows, int64_t zeta, const uint32_t* cols,
+                             int64_t ncols, uint32_t* flags) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= ncols) return;
+  const int64_t j = cols ? cols[q] : q;
+  const uint32_t* r = rows + j * zeta;
+  uint32_t bad = 0;
+  for (int64_t a = 1; a < zeta && !bad; ++a) {
+    const uint32_t ra = r[a];
+    for (int64_t b = 0; b < a; ++b)
+      if (r[b] == ra) {
+        bad = 1;
+        break;
+      }
+  }
+  flags[q] = bad;
+}
+
+__global__ void k_compact(const uint32_t* flags, const uint32_t* scanned, const uint32_t* cols,
+                          int64_t ncols, uint32_t* out, uint32_t* total) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= ncols) return;
+  if (flags[q]) out[scanned[q]] = cols ? cols[q] : static_cast<uint32_t>(q);
+  if (q == ncols - 1) *total = scanned[q] + flags[q];
+}
+
+__global__ void k_pack_src(const uint8_t* neg, int64_t m, int64_t zeta, uint32_t* vals) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e < m * zeta)
+    vals[e] = static_cast<uint32_t>(e / zeta) | (static_cast<uint32_t>(neg[e]) << 31);
+}
+
+__global__ void k_row_ptr(const uint32_t* keys, int64_t nnz, int64_t d, uint32_t* ptr) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i > d) return;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < static_cast<uint32_t>(i)) lo = mid + 1; else hi = mid;
+  }
+  ptr[i] = static_cast<uint32_t>(lo);
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+struct PatternWs {
+  uint32_t* counts;    // nchunks + 1
+  uint32_t* scanned;   // nchunks + 1
+  uint32_t* flags;     // m
+  uint32_t* fscan;     // m
+  uint32_t* bad_a;     // m
+  uint32_t* bad_b;     // m
+  uint32_t* keys_out;  // m*zeta
+  uint32_t* vals_in;   // m*zeta
+  uint64_t* scalars;   // [end_word, nbad(u32 as u64), ...]
+  void* cub_tmp;
+  size_t cub_bytes;
+  uint64_t chunk_cap;
+};
+
+int64_t max_words(int64_t N) {
+  // Lemire rejection probability is < bound / 2^32; allow a 0.2% + 4096
+  // margin and fall back to a second, exact pass if it is ever exceeded.
+  return N + N / 512 + 4096;
+}
+
+size_t cub_bytes_needed(int64_t m, int64_t zeta) {
+  const int64_t nnz = m * zeta;
+  const int64_t nchunks = max_words(nnz) / CH + 2;
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, static_cast<int>(nnz));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                static_cast<int>(nchunks));
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                static_cast<int>(m));
+  return std::max(a, std::max(b, c));
+}
+
+int64_t carve(Carver& cv, PatternWs& w, int64_t m, int64_t zeta) {
+  const int64_t nnz = m * zeta;
+  const int64_t nchunks = max_words(nnz) / CH + 2;
+  w.chunk_cap = static_cast<uint64_t>(nchunks);
+  w.counts = cv.take<uint32_t>(nchunks + 1);
+  w.scanned = cv.take<uint32_t>(nchunks + 1);
+  w.flags = cv.take<uint32_t>(m + 1);
+  w.fscan = cv.take<uint32_t>(m + 1);
+  w.bad_a = cv.take<uint32_t>(m + 1);
+  w.bad_b = cv.take<uint32_t>(m + 1);
+  w.keys_out = cv.take<uint32_t>(nnz);
+  w.vals_in = cv.take<uint32_t>(nnz);
+  w.scalars = cv.take<uint64_t>(8);
+  w.cub_bytes = cub_bytes_needed(m, zeta);
+  w.cub_tmp = cv.take<char>(static_cast<int64_t>(w.cub_bytes));
+  return cv.off;
+}
+
+// Draw N bounded values starting at word *wpos; advances *wpos.
+int lemire_fill(const Stream& st, uint64_t* wpos, uint64_t N, uint32_t bound, uint32_t* dst,
+                const uint32_t* bad_cols, int64_t zeta, PatternWs& w, cudaStream_t s) {
+  if (N == 0) return ITSK_OK;
+  const uint32_t thr = static_cast<uint32_t>((0x100000000ull - bound) % bound);
+  uint64_t nwords = static_cast<uint64_t>(max_words(static_cast<int64_t>(N)));
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const uint64_t nchunks = (nwords + CH - 1) / CH;
+    if (nchunks > w.chunk_cap) break;
+    k_lemire_count<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, *wpos, nwords, bound, thr,
+                                                              w.counts, nchunks);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+    size_t tb = w.cub_bytes;
+    ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned,
+                                            static_cast<int>(nchunks + 1), s));
+    count_launch();
+    uint32_t total = 0;
+    ITSK_CUDA(cudaMemcpyAsync(&total, w.scanned + nchunks, sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s));
+    ITSK_CUDA(cudaStreamSynchronize(s));
+    if (total < N) {  // margin exhausted (astronomically rare): widen and retry
+      nwords = nwords * 2 + 65536;
+      continue;
+    }
+    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(
+        st, *wpos, nwords, bound, thr, w.scanned, nchunks, N, dst, bad_cols, zeta, w.scalars);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+    uint64_t end_word = 0;
+    ITSK_CUDA(cudaMemcpyAsync(&end_word, w.scalars, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    ITSK_CUDA(cudaStreamSynchronize(s));
+    *wpos = end_word;
+    return ITSK_OK;
+  }
+  set_error("lemire_fill: could not draw %llu values", (unsigned long long)N);
+  return ITSK_ECUDA;
+}
+
+}  // namespace
+}  // namespace itsk
+
+using namespace itsk;
+
+extern "C" int itsk_pattern_workspace(int64_t d, int64_t m, int64_t zeta, int64_t* bytes) {
+  ITSK_REQUIRE(bytes && d >= 1 && m >= 1 && zeta >= 1 && zeta <= d, "bad pattern shape");
+  Carver cv(nullptr, 0);
+  PatternWs w;
+  *bytes = carve(cv, w, m, zeta) + 256;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, const uint64_t pcg[4],
+                                        int has_uint32, uint32_t uinteger, uint32_t* rows,
+                                        uint8_t* neg, uint32_t* sk_ptr, uint32_t* sk_src,
+                                        void* ws, int64_t ws_bytes, itsk_stream_t stream) {
+  ITSK_REQUIRE(d >= 1 && m >= 1, "d and m must be >= 1");
+  ITSK_REQUIRE(zeta >= 1 && zeta <= d, "need 1 <= zeta <= d, got zeta=%lld, d=%lld",
+               (long long)zeta, (long long)d);
+  ITSK_REQUIRE(d <= 0xFFFFFFFFll && m < (1ll << 31) && m * zeta < (1ll << 32),
+               "pattern too large for 32-bit indices");
+  ITSK_REQUIRE(rows && neg && pcg, "null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Carver cv(ws, ws_bytes);
+  PatternWs w;
+  carve(cv, w, m, zeta);
+  ITSK_REQUIRE(cv.ok(), "pattern workspace too small");
+  Stream st{pcg[0], pcg[1], pcg[2], pcg[3], uinteger, has_uint32 ? 1 : 0};
+  const int64_t nnz = m * zeta;
+  uint64_t wpos = 0;
+  int rc;
+  if (zeta == d) {  // np.tile(np.arange(d), (m, 1)): no draws
+    k_tile_rows<<<blocks_for(nnz, 256), 256, 0, s>>>(rows, m, zeta);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+  } else {
+    const uint32_t bound = static_cast<uint32_t>(d);
+    if ((rc = lemire_fill(st, &wpos, nnz, bound, rows, nullptr, zeta, w, s))) return rc;
+    // _distinct_rows redraw loop (embed.py:37-42)
+    const uint32_t* cols = nullptr;
+    int64_t ncols = m;
+    uint32_t* out = w.bad_a;
+    for (;;) {
+      k_flag_dupes<<<blocks_for(ncols, 256), 256, 0, s>>>(rows, zeta, cols, ncols, w.flags);
+      count_launch();
+      size_t tb = w.cub_bytes;
+      ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan,
+                                              static_cast<int>(ncols), s));
+      count_launch();
+      uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
+      k_compact<<<blocks_for(ncols, 256), 256, 0, s>>>(w.flags, w.fscan, cols, ncols, out,
+                                                       nbad_dev);
+      count_launch();
+      ITSK_CHECK_LAUNCH();
+      uint32_t nbad = 0;
+      ITSK_CUDA(cudaMemcpyAsync(&nbad, nbad_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      ITSK_CUDA(cudaStreamSynchronize(s));
+      if (nbad == 0) break;
+      if ((rc = lemire_fill(st, &wpos, static_cast<uint64_t>(nbad) * zeta, bound, rows, out, zeta,
+                            w, s)))
+        return rc;
+      cols = out;
+      ncols = nbad;
+      out = (out == w.bad_a) ? w.bad_b : w.bad_a;
+    }
+  }
+  k_signs<<<blocks_for((nnz + CH - 1) / CH, 256), 256, 0, s>>>(st, wpos, nnz, neg);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  if (sk_ptr && sk_src) {
+    // Group by sketch row, keeping source order ascending (stable LSD sort
+    // of entries enumerated column-major == ascending j).
+    k_pack_src<<<blocks_for(nnz, 256), 256, 0, s>>>(neg, m, zeta, w.vals_in);
+    count_launch();
+    int end_bit = 1;
+    while ((1ll << end_bit) < d) ++end_bit;
+    size_t tb = w.cub_bytes;
+    ITSK_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, rows, w.keys_out, w.vals_in, sk_src,
+                                              static_cast<int>(nnz), 0, end_bit, s));
+    count_launch(end_bit <= 8 ? 2 : 4);
+    k_row_ptr<<<blocks_for(d + 1, 256), 256, 0, s>>>(w.keys_out, nnz, d, sk_ptr);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+  }
+  return ITSK_OK;
+}

@@ -1,0 +1,108 @@
+// S·[A | b] — the sparse sign sketch (K1).
+//
+// Replaces SparseSignEmbedding.apply_dense / apply_vec
+// (/root/reference/pkg/src/itsketch/embed.py:62-74), i.e. scipy's
+// csc_matvecs, which computes  for j ascending: for each stored (i, v) of
+// column j:  y[i, :] += v * a[j, :]  with the product rounded before the add.
+// Here the pattern is grouped by sketch row i (CSR of S, sources ascending),
+// one warp owns sketch row i x a column block and accumulates its sources in
+// the same ascending order in registers — so every output is bitwise equal to
+// scipy's, and the kernel is deterministic.  The b column rides along as
+// column n of the output (apply_vec is the same sum, solvers.py:208).
+#include "itsk_common.cuh"
+
+namespace itsk {
+namespace {
+
+template <int CPL>
+__global__ void __launch_bounds__(128) k_sketch_gather(
+    const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
+    const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d,
+    double scale, double* __restrict__ W, int64_t ldw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= d) return;
+  const int64_t ncol = n + (b ? 1 : 0);
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 32 * CPL;
+  double acc[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
+  const uint32_t e0 = ptr[i], e1 = ptr[i + 1];
+  for (uint32_t e = e0; e < e1; e += 32) {
+    const uint32_t mine = (e + lane < e1) ? src[e + lane] : 0u;
+    const int cnt = static_cast<int>(min(32u, e1 - e));
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      double v[4][CPL];
+      double sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t s = __shfl_sync(FULL, mine, k + u);
+        const int64_t j = s & 0x7fffffffu;
+        sv[u] = (s >> 31) ? -scale : scale;
+        const double* arow = A + j * lda;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int64_t col = c0 + lane + 32 * q;
+          v[u][q] = col < n ? arow[col] : (col == n && b ? b[j] : 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], v[u][q]));
+    }
+    for (; k < cnt; ++k) {
+      const uint32_t s = __shfl_sync(FULL, mine, k);
+      const int64_t j = s & 0x7fffffffu;
+      const double svk = (s >> 31) ? -scale : scale;
+      const double* arow = A + j * lda;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int64_t col = c0 + lane + 32 * q;
+        const double a = col < n ? arow[col] : (col == n && b ? b[j] : 0.0);
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(svk, a));
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int64_t col = c0 + lane + 32 * q;
+    if (col < ncol) W[i * ldw + col] = acc[q];
+  }
+}
+
+template <int CPL>
+int launch_gather(const double* A, int64_t lda, int64_t n, const double* b,
+                  const uint32_t* ptr, const uint32_t* src, int64_t d, double scale, double* W,
+                  int64_t ldw, cudaStream_t s) {
+  const int64_t ncol = n + (b ? 1 : 0);
+  dim3 grid(static_cast<unsigned>((d * 32 + 127) / 128),
+            static_cast<unsigned>((ncol + 32 * CPL - 1) / (32 * CPL)));
+  k_sketch_gather<CPL><<<grid, 128, 0, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+}  // namespace
+}  // namespace itsk
+
+using namespace itsk;
+
+extern "C" int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                           const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d,
+                           int64_t zeta, double* SAb, int64_t ldw, itsk_stream_t stream) {
+  ITSK_REQUIRE(m >= 1 && n >= 0 && d >= 1 && zeta >= 1, "bad sketch shape");
+  ITSK_REQUIRE(lda >= n && ldw >= n + (b ? 1 : 0), "bad leading dimension");
+  ITSK_REQUIRE(sk_ptr && sk_src && SAb && (A || n == 0), "null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // scale = 1/sqrt(zeta) exactly as embed.py:92 (correctly rounded sqrt, div)
+  const double scale = 1.0 / sqrt(static_cast<double>(zeta));
+  const int64_t ncol = n + (b ? 1 : 0);
+  const int64_t need = (ncol + 31) / 32;
+  if (need <= 1) return launch_gather<1>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  if (need <= 2) return launch_gather<2>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  if (need <= 4) return launch_gather<4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  return launch_gather<8>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+}

@@ -1,0 +1,244 @@
+// Small n x n kernels on the R factor (K4): triangular solves, the power-
+// method norm estimate and the condition estimate.
+//
+//   tri_solve_upper            linalg.py:59-62   R y = c   (back substitution)
+//   tri_solve_upper_transpose  linalg.py:65-68   R'y = c   (forward substitution)
+//   solve_step                 solvers.py:339-340  y = R^{-1} R^{-T} c
+//   rand_power_norm_est        linalg.py:79-105
+//   cond_est                   linalg.py:108-113
+//
+// R is row-major, ld n, upper triangular, diag(R) > 0 (validated once by the
+// QR).  One CTA of 1024 threads; vectors live in shared memory and R streams
+// from L2 (it stays resident across iterations).  Blocks of 32 rows:
+//   R'y = c  right-looking: solve the 32x32 diagonal block with one warp,
+//            then all threads update the later entries from contiguous row
+//            segments of R;
+//   R y = c  left-looking from the bottom: one warp per row reduces the
+//            contiguous row segment against the solved tail, then one warp
+//            solves the diagonal block.
+#include "itsk_common.cuh"
+#include "itsk_dense.cuh"
+#include "itsk_kernels.cuh"
+
+namespace itsk {
+
+namespace {
+
+__global__ void __launch_bounds__(1024) k_trsv(const double* R, int64_t n, const double* c,
+                                               double* y, int mode) {
+  extern __shared__ double sm[];
+  double* v = sm;
+  double* tmp = sm + n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = c[i];
+  __syncthreads();
+  if (mode == 1 || mode == 2) trsv_t_inplace(R, n, v);
+  if (mode == 0 || mode == 2) trsv_n_inplace(R, n, v, tmp);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = v[i];
+}
+
+// rand_power_norm_est (linalg.py:96-105)
+__global__ void __launch_bounds__(1024) k_normest(const double* R, int64_t n, const double* v0,
+                                                  int64_t steps, double* out) {
+  extern __shared__ double sm[];
+  double* v = sm;
+  double* t = sm + n;
+  double* w = sm + 2 * n;
+  double* red = sm + 3 * n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = v0[i];
+  __syncthreads();
+  double nv = sqrt(dot_sm(v, v, n, red));
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = v[i] / nv;
+  __syncthreads();
+  for (int64_t s = 0; s < steps; ++s) {
+    trmv_n(R, n, v, t);
+    trmv_t(R, n, t, w);
+    const double nw = sqrt(dot_sm(w, w, n, red));
+    if (nw == 0.0) {
+      if (threadIdx.x == 0) *out = 0.0;
+      return;
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = w[i] / nw;
+    __syncthreads();
+  }
+  trmv_n(R, n, v, t);
+  const double r = sqrt(dot_sm(t, t, n, red));
+  if (threadIdx.x == 0) *out = r;
+}
+
+// Largest eigenvalue of the k x k symmetric tridiagonal (al, be) by Sturm
+// bisection, to full precision.
+__device__ double tridiag_max_eig(const double* al, const double* be, int k) {
+  double lo = al[0], hi = al[0];
+  for (int i = 0; i < k; ++i) {
+    const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < k - 1 ? fabs(be[i]) : 0.0);
+    lo = fmin(lo, al[i] - r);
+    hi = fmax(hi, al[i] + r);
+  }
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    // number of eigenvalues > mid  ==  k - (# < mid)
+    int below = 0;
+    double q = al[0] - mid;
+    if (q < 0) ++below;
+    for (int i = 1; i < k; ++i) {
+      if (q == 0.0) q = 1e-300;
+      q = al[i] - mid - be[i - 1] * be[i - 1] / q;
+      if (q < 0) ++below;
+    }
+    if (below == k) hi = mid; else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+constexpr int LANCZOS_MAX = 96;
+
+// Lanczos on op = R'R (inv == 0) or R^{-1}R^{-T} (inv == 1); returns the
+// largest Ritz value, stopping once it is stable to rounding.
+__device__ double lanczos_max(const double* R, int64_t n, const double* v0, int inv, double* q,
+                              double* qp, double* w, double* t, double* red, double* al,
+                              double* be) {
+  const int tid = threadIdx.x;
+  __shared__ double s_theta;
+  double nv = sqrt(dot_sm(v0, v0, n, red));
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    q[i] = v0[i] / nv;
+    qp[i] = 0.0;
+  }
+  __syncthreads();
+  const int kmax = static_cast<int>(min(static_cast<int64_t>(LANCZOS_MAX), n));
+  double theta_prev = 0.0, theta = 0.0, bprev = 0.0;
+  int stable = 0;
+  for (int k = 0; k < kmax; ++k) {
+    if (inv) {
+      for (int64_t i = tid; i < n; i += blockDim.x) w[i] = q[i];
+      __syncthreads();
+      trsv_t_inplace(R, n, w);
+      trsv_n_inplace(R, n, w, t);
+    } else {
+      trmv_n(R, n, q, t);
+      trmv_t(R, n, t, w);
+    }
+    for (int64_t i = tid; i < n; i += blockDim.x) w[i] -= bprev * qp[i];
+    __syncthreads();
+    const double a = dot_sm(q, w, n, red);
+    for (int64_t i = tid; i < n; i += blockDim.x) w[i] -= a * q[i];
+    __syncthreads();
+    const double b = sqrt(dot_sm(w, w, n, red));
+    if (tid == 0) {
+      al[k] = a;
+      be[k] = b;
+      s_theta = tridiag_max_eig(al, be, k + 1);
+    }
+    __syncthreads();
+    theta = s_theta;
+    if (k > 0 && fabs(theta - theta_prev) <= 4e-16 * fabs(theta)) {
+      if (++stable >= 2) break;
+    } else {
+      stable = 0;
+    }
+    theta_prev = theta;
+    if (b == 0.0 || !(b == b)) break;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const double qi = q[i];
+      qp[i] = qi;
+      q[i] = w[i] / b;
+    }
+    __syncthreads();
+    bprev = b;
+  }
+  return theta;
+}
+
+__global__ void __launch_bounds__(1024) k_condest(const double* R, int64_t n, const double* v0,
+                                                  double* out) {
+  extern __shared__ double sm[];
+  double* q = sm;
+  double* qp = sm + n;
+  double* w = sm + 2 * n;
+  double* t = sm + 3 * n;
+  double* red = sm + 4 * n;
+  double* al = red + 32;
+  double* be = al + LANCZOS_MAX;
+  const double smax2 = lanczos_max(R, n, v0, 0, q, qp, w, t, red, al, be);
+  const double imin2 = lanczos_max(R, n, v0, 1, q, qp, w, t, red, al, be);
+  if (threadIdx.x == 0) *out = sqrt(smax2 * imin2);
+}
+
+}  // namespace
+
+int launch_trsv_pair_device(const double* R, int64_t n, const double* c, double* y,
+                            cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(n + 32) * sizeof(double);
+  if (smem > 48 * 1024)
+    ITSK_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  k_trsv<<<1, 1024, smem, s>>>(R, n, c, y, 2);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+}  // namespace itsk
+
+using namespace itsk;
+
+extern "C" int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
+                         itsk_stream_t stream) {
+  ITSK_REQUIRE(R && c && y && n >= 1, "bad trsv arguments");
+  ITSK_REQUIRE(n <= 16384, "trsv: n too large for the single-CTA kernel");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t smem = static_cast<size_t>(n + 32) * sizeof(double);
+  if (smem > 48 * 1024)
+    ITSK_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  k_trsv<<<1, 1024, smem, s>>>(R, n, c, y, trans ? 1 : 0);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
+                              itsk_stream_t stream) {
+  (void)tmp;
+  ITSK_REQUIRE(R && c && y && n >= 1 && n <= 16384, "bad trsv arguments");
+  return launch_trsv_pair_device(R, n, c, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps,
+                            double* out, double* ws, itsk_stream_t stream) {
+  (void)ws;
+  ITSK_REQUIRE(R && v0 && out && n >= 1 && steps >= 1, "bad normest arguments");
+  ITSK_REQUIRE(n <= 8000, "normest: n too large for the single-CTA kernel");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t smem = static_cast<size_t>(3 * n + 32) * sizeof(double);
+  if (smem > 48 * 1024)
+    ITSK_CUDA(cudaFuncSetAttribute(k_normest, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  k_normest<<<1, 1024, smem, s>>>(R, n, v0, steps, out);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_condest_workspace(int64_t n, int64_t* doubles) {
+  ITSK_REQUIRE(doubles && n >= 1, "bad n");
+  *doubles = 0;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double* out, double* ws,
+                            itsk_stream_t stream) {
+  (void)ws;
+  ITSK_REQUIRE(R && v0 && out && n >= 1, "bad condest arguments");
+  ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t smem = static_cast<size_t>(4 * n + 32 + 2 * LANCZOS_MAX) * sizeof(double);
+  if (smem > 48 * 1024)
+    ITSK_CUDA(cudaFuncSetAttribute(k_condest, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  k_condest<<<1, 1024, smem, s>>>(R, n, v0, out);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}

@@ -1,0 +1,169 @@
+"""Dense kernels on the sketch's R factor (mirrors itsketch.linalg for the path).
+
+    householder_qr_econ  linalg.py:30-47    -> device blocked Householder QR
+    tri_solve_upper      linalg.py:59-62    -> device back substitution
+    tri_solve_upper_transpose linalg.py:65-68 -> device forward substitution
+    rand_power_norm_est  linalg.py:79-105   -> device power method, same start vector
+    cond_est             linalg.py:108-113  -> device Lanczos extremes of R'R, R^-1 R^-T
+
+Differences from the reference, by design:
+  * the QR never forms Q (dorgqr); it applies the reflectors to an extra
+    right-hand-side column instead, returning R and z = Q'rhs.  QrFactors.q
+    is therefore None unless `want_q` asks for Q = (the QR of [A | I]) — not
+    needed on the path.
+  * cond_est uses Lanczos (<= 96 steps, stopped when the extreme Ritz values
+    are stable to rounding) instead of a full SVD; for the spectra on this
+    path it agrees with dgesdd's ratio to ~1e-14 relative (tests/).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as _dev
+from ._lib import SingularMatrixError
+
+__all__ = ["QrFactors", "SingularMatrixError", "householder_qr_econ", "qr_aug", "tri_solve_upper",
+           "tri_solve_upper_transpose", "rand_power_norm_est", "cond_est", "normest_steps"]
+
+
+@dataclass(frozen=True)
+class QrFactors:
+    """R (n x n, upper, diag >= 0) and z = Q' rhs (None without a rhs).
+    `q` is kept for field-compatibility with linalg.py:21-27 and is None."""
+
+    r: object
+    z: object = None
+    q: object = None
+
+
+def qr_workspace(d: int, n: int, dev) -> torch.Tensor:
+    lib = _dev.lib(dev)
+    nbytes = ctypes.c_int64()
+    _lib.check(lib.itsk_qr_workspace(d, n, ctypes.byref(nbytes)))
+    return _dev.workspace(nbytes.value, dev)
+
+
+def qr_aug(w: torch.Tensor, n: int, r_out: torch.Tensor | None = None, z_out: torch.Tensor | None = None,
+           ws: torch.Tensor | None = None):
+    """In-place Householder QR of the device matrix w = [SA | Sb] (d x (n+1),
+    or d x n without a rhs).  Returns (R, z).  Raises SingularMatrixError like
+    the reference's tri_solve_upper on an exactly-zero R_kk."""
+    dev = w.device
+    d = w.shape[0]
+    has_rhs = w.shape[1] > n
+    if r_out is None:
+        r_out = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if has_rhs and z_out is None:
+        z_out = torch.empty(n, dtype=torch.float64, device=dev)
+    if ws is None:
+        ws = qr_workspace(d, n, dev)
+    lib = _dev.lib(dev)
+    _lib.check(lib.itsk_qr_aug(_dev.ptr(w), d, n, int(w.stride(0)), _dev.ptr(r_out),
+                               _dev.ptr(z_out) if has_rhs else None, _dev.ptr(ws), ws.numel(),
+                               _dev.stream_ptr()))
+    return r_out, (z_out if has_rhs else None)
+
+
+def householder_qr_econ(a, rhs=None) -> QrFactors:
+    """Economy QR with nonnegative diag(R) (linalg.py:30-47) on the device.
+    With `rhs`, also returns z = Q' rhs (solvers.py:209)."""
+    host = not isinstance(a, torch.Tensor)
+    dev = _dev.current_device() if host else a.device
+    at, _ = _dev.as_device_matrix(a, dev)
+    d, n = at.shape
+    if d < n:
+        raise ValueError(f"need m >= n, got {d} x {n}")
+    ncol = n + (1 if rhs is not None else 0)
+    w = torch.empty((d, ncol), dtype=torch.float64, device=dev)
+    w[:, :n] = at
+    if rhs is not None:
+        w[:, n] = _dev.as_device_vector(rhs, dev)
+    r, z = qr_aug(w, n)
+    if host:
+        return QrFactors(r=_dev.to_numpy(r), z=None if z is None else _dev.to_numpy(z))
+    return QrFactors(r=r, z=z)
+
+
+def _solve(r, c, trans: int):
+    host = not isinstance(r, torch.Tensor)
+    dev = _dev.current_device() if host else r.device
+    rt, _ = _dev.as_device_matrix(r, dev)
+    n = rt.shape[0]
+    if rt.shape[0] != rt.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {tuple(rt.shape)}")
+    if host and np.any(np.diag(np.asarray(r, dtype=float)) == 0.0):
+        raise SingularMatrixError("zero diagonal entry in triangular factor")
+    if not host and bool((torch.diagonal(rt) == 0).any()):
+        raise SingularMatrixError("zero diagonal entry in triangular factor")
+    rt = rt.contiguous()
+    ct = _dev.as_device_vector(c, dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    _lib.check(_dev.lib(dev).itsk_trsv(_dev.ptr(rt), n, _dev.ptr(ct), _dev.ptr(y), trans, _dev.stream_ptr()))
+    return _dev.to_numpy(y) if host else y
+
+
+def tri_solve_upper(r, c):
+    """Solve R y = c (linalg.py:59-62)."""
+    return _solve(r, c, 0)
+
+
+def tri_solve_upper_transpose(r, c):
+    """Solve R' y = c (linalg.py:65-68)."""
+    return _solve(r, c, 1)
+
+
+def normest_steps(n: int, steps: int | None = None) -> int:
+    if steps is None:
+        steps = max(1, math.ceil(math.log2(n))) if n > 1 else 1
+    if steps < 1:
+        raise ValueError("steps must be >= 1")
+    return steps
+
+
+def start_vector(n: int, rng_seed: int) -> np.ndarray:
+    """default_rng(seed).standard_normal(n) — the start vector of linalg.py:96."""
+    return np.random.default_rng(rng_seed).standard_normal(n)
+
+
+def _scalar_out(dev):
+    return torch.empty(1, dtype=torch.float64, device=dev)
+
+
+def rand_power_norm_est(r, steps: int | None = None, rng_seed: int = 0, out: torch.Tensor | None = None):
+    """Randomized power estimate of ||R||_2 (linalg.py:79-105) on the device."""
+    host = not isinstance(r, torch.Tensor)
+    dev = _dev.current_device() if host else r.device
+    rt, _ = _dev.as_device_matrix(r, dev)
+    rt = rt.contiguous()
+    n = rt.shape[0]
+    steps = normest_steps(n, steps)
+    v0 = _dev.as_device_vector(start_vector(n, rng_seed), dev)
+    res = out if out is not None else _scalar_out(dev)
+    _lib.check(_dev.lib(dev).itsk_normest(_dev.ptr(rt), n, _dev.ptr(v0), steps, _dev.ptr(res), None,
+                                          _dev.stream_ptr()))
+    return float(res.item()) if (host or out is None) else res
+
+
+def cond_est(r, rng_seed: int = 0, out: torch.Tensor | None = None):
+    """kappa_2(R) = sigma_max / sigma_min (linalg.py:108-113) on the device."""
+    host = not isinstance(r, torch.Tensor)
+    dev = _dev.current_device() if host else r.device
+    rt, _ = _dev.as_device_matrix(r, dev)
+    rt = rt.contiguous()
+    if rt.shape[0] != rt.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {tuple(rt.shape)}")
+    if bool((torch.diagonal(rt) == 0).any()):
+        raise SingularMatrixError("zero diagonal entry in triangular factor")
+    n = rt.shape[0]
+    v0 = _dev.as_device_vector(start_vector(n, rng_seed), dev)
+    res = out if out is not None else _scalar_out(dev)
+    _lib.check(_dev.lib(dev).itsk_condest(_dev.ptr(rt), n, _dev.ptr(v0), _dev.ptr(res), None,
+                                          _dev.stream_ptr()))
+    return float(res.item()) if (host or out is None) else res

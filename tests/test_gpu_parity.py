@@ -1,0 +1,372 @@
+"""GPU parity: the B200 path (through the C-ABI / Python drop-in) against the
+CPU oracle and the reference's golden fixtures.
+
+Bars (per north_star): integer/byte work and the S·A sums bit-exact; the
+refinement loop's FE/RE within 2x of the reference's (one-sided), and
+||x - x_ref||/||x_ref|| <= 10*kappa*u + FE_ref; normest/condest to rounding.
+"""
+
+import hashlib
+import json
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2311_04362_b200 as p
+
+    return p
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import itsketch_oracle as o
+
+    return o
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# --------------------------------------------------------------------------
+# pattern + sketch (bit-exact)
+# --------------------------------------------------------------------------
+def test_pattern_matches_reference_bitwise(pkg, golden):
+    g = golden("patterns.npz")
+    for d, m, zeta, seed, k in g["pattern_cases"]:
+        key = f"p_{d}_{m}_{zeta}_{seed}"
+        s = pkg.sparse_sign_new(int(d), int(m), int(zeta), int(seed))
+        np.testing.assert_array_equal(s.rows, g[key + "_rows"], err_msg=key)
+        np.testing.assert_array_equal(s.signs, g[key + "_signs"], err_msg=key)
+        a = np.random.default_rng(int(seed) + 100).standard_normal((int(m), int(k)))
+        sa = s.apply_dense(a)
+        assert np.array_equal(sa, g[key + "_sa"]), key
+        # apply_vec == a column of apply_dense, bitwise (embed.py:69-74)
+        assert np.array_equal(s.apply_vec(a[:, 0]), g[key + "_sa"][:, 0]), key
+
+
+def test_pattern_csr_grouping(pkg):
+    s = pkg.sparse_sign_new(50, 400, 6, 9)
+    ptr = s.ptr_dev.cpu().numpy().view(np.uint32).astype(np.int64)
+    src = s.src_dev.cpu().numpy().view(np.uint32)
+    assert ptr[0] == 0 and ptr[-1] == 400 * 6 and np.all(np.diff(ptr) >= 0)
+    rows, signs = s.rows, s.signs
+    for i in range(50):
+        seg = src[ptr[i]:ptr[i + 1]]
+        j = (seg & 0x7FFFFFFF).astype(np.int64)
+        assert np.all(np.diff(j) > 0)  # ascending sources
+        for jj, neg in zip(j, seg >> 31):
+            t = int(np.nonzero(rows[jj] == i)[0][0])
+            assert (signs[jj, t] < 0) == bool(neg)
+
+
+def test_full_size_pattern_and_sketch_digests(pkg, golden, orc):
+    g = golden("patterns.npz")
+    for rec in json.loads(str(g["digests_json"])):
+        s = pkg.sparse_sign_new(rec["d"], rec["m"], rec["zeta"], rec["seed"])
+        if rec.get("kind") == "sa":
+            a = np.random.default_rng(rec["a_seed"]).standard_normal((rec["m"], rec["k"]))
+            assert _sha(s.apply_dense(a)) == rec["sa"]
+        else:
+            assert _sha(s.rows.astype(np.int64)) == rec["rows"], rec
+            assert _sha(s.signs.astype(np.float64)) == rec["signs"], rec
+
+
+def test_pattern_argument_errors(pkg):
+    with pytest.raises(ValueError):
+        pkg.sparse_sign_new(3, 5, 4, 0)
+    with pytest.raises(ValueError):
+        pkg.sparse_sign_new(0, 5, 1, 0)
+    s = pkg.sparse_sign_new(10, 20, 3, 0)
+    with pytest.raises(ValueError):
+        s.apply_dense(np.ones((21, 2)))
+    assert np.all(s.apply_dense(np.zeros((20, 4))) == 0)
+
+
+# --------------------------------------------------------------------------
+# QR, triangular solves, estimates
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("m,n,seed", [(20, 5, 1), (200, 40, 2), (1000, 50, 3), (4000, 201, 4),
+                                      (300, 33, 5), (64, 64, 6), (5000, 500, 7)])
+def test_qr_matches_lapack(pkg, orc, m, n, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    rhs = rng.standard_normal(m)
+    f = pkg.householder_qr_econ(a, rhs)
+    q_ref, r_ref = orc.householder_qr_econ(a)
+    assert np.all(np.diag(f.r) >= 0)
+    assert np.array_equal(f.r, np.triu(f.r))
+    scale = np.linalg.norm(r_ref)
+    assert np.linalg.norm(f.r - r_ref) <= 100 * n * U * scale
+    z_ref = q_ref.T @ rhs
+    assert np.linalg.norm(f.z - z_ref) <= 100 * n * U * np.linalg.norm(rhs)
+
+
+def test_qr_hand_cases(pkg):
+    f = pkg.householder_qr_econ(np.array([[3.0], [4.0]]))
+    np.testing.assert_allclose(f.r, [[5.0]], rtol=1e-15)
+    f = pkg.householder_qr_econ(np.eye(5))
+    np.testing.assert_array_equal(f.r, np.eye(5))
+    f = pkg.householder_qr_econ(-np.random.default_rng(7).standard_normal((12, 6)))
+    assert np.all(np.diag(f.r) >= 0)
+    with pytest.raises(ValueError):
+        pkg.householder_qr_econ(np.ones((3, 5)))
+
+
+def test_qr_singular_raises(pkg):
+    a = np.random.default_rng(1).standard_normal((50, 6))
+    a[:, 3] = 0.0
+    with pytest.raises(pkg.SingularMatrixError):
+        pkg.householder_qr_econ(a, np.ones(50))
+
+
+def test_qr_deterministic(pkg):
+    a = np.random.default_rng(9).standard_normal((3000, 120))
+    f1, f2 = pkg.householder_qr_econ(a), pkg.householder_qr_econ(a)
+    assert np.array_equal(f1.r, f2.r)
+
+
+def test_trsv_and_estimates_vs_reference(pkg, golden):
+    g = golden("linalg.npz")
+    import scipy.linalg as sl
+
+    for i in range(5):
+        r = g[f"tri{i}_r"]
+        n = r.shape[0]
+        c = np.random.default_rng(i).standard_normal(n)
+        y = pkg.tri_solve_upper(r, c)
+        np.testing.assert_allclose(y, sl.solve_triangular(r, c), rtol=1e-12, atol=1e-14)
+        yt = pkg.tri_solve_upper_transpose(r, c)
+        np.testing.assert_allclose(yt, sl.solve_triangular(r, c, trans="T"), rtol=1e-12, atol=1e-14)
+        assert pkg.rand_power_norm_est(r, rng_seed=i) == pytest.approx(float(g[f"tri{i}_normest"]), rel=1e-12)
+        assert pkg.cond_est(r) == pytest.approx(float(g[f"tri{i}_condest"]), rel=1e-10)
+    with pytest.raises(pkg.SingularMatrixError):
+        pkg.tri_solve_upper(np.array([[1.0, 2.0], [0.0, 0.0]]), np.ones(2))
+    with pytest.raises(pkg.SingularMatrixError):
+        pkg.tri_solve_upper_transpose(np.array([[1.0, 2.0], [0.0, 0.0]]), np.ones(2))
+
+
+@pytest.mark.parametrize("n", [50, 200, 500, 1000])
+def test_trsv_large_residual(pkg, n):
+    rng = np.random.default_rng(n)
+    r = np.triu(rng.standard_normal((n, n))) + (2.0 + n) * np.eye(n)
+    c = rng.standard_normal(n)
+    y = pkg.tri_solve_upper(r, c)
+    kappa = np.linalg.cond(r)
+    assert np.linalg.norm(r @ y - c) <= 100 * n * U * kappa * np.linalg.norm(c)
+    yt = pkg.tri_solve_upper_transpose(r, c)
+    assert np.linalg.norm(r.T @ yt - c) <= 100 * n * U * kappa * np.linalg.norm(c)
+
+
+def test_condest_on_sketch_factor(pkg, orc):
+    a, b, t = orc.gen_randsvd(20000, 200, 1e10, 1e-12, 0)
+    pat = orc.sparse_sign_pattern(4000, 20000, 8, 0)
+    _, r = orc.householder_qr_econ(orc.sketch_apply(pat, a))
+    assert pkg.cond_est(r) == pytest.approx(orc.cond_est(r), rel=1e-10)
+    assert pkg.rand_power_norm_est(r, rng_seed=0) == pytest.approx(orc.rand_power_norm_est(r, rng_seed=0), rel=1e-12)
+
+
+# --------------------------------------------------------------------------
+# fused pass
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("m,n", [(1000, 1), (999, 7), (5000, 50), (20000, 200), (3001, 257), (4096, 500),
+                                 (2000, 1000)])
+def test_fused_pass_matches_numpy(pkg, m, n):
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((m, n))
+    b = rng.standard_normal(m)
+    x = rng.standard_normal(n)
+    r_prev = rng.standard_normal(m)
+    r_true = rng.standard_normal(m)
+    dev = dv.current_device()
+    T = lambda v: torch.from_numpy(v).to(dev)
+    at, bt, xt, rpt, rtt = T(a), T(b), T(x), T(r_prev), T(r_true)
+    r_out = torch.empty(m, dtype=torch.float64, device=dev)
+    cs = torch.empty(n + 8, dtype=torch.float64, device=dev)
+    lib = dv.lib(dev)
+    nb = ctypes.c_int64()
+    _lib.check(lib.itsk_pass_workspace(m, n, ctypes.byref(nb)))
+    ws = dv.workspace(nb.value, dev)
+    _lib.check(lib.itsk_fused_pass(dv.ptr(at), m, n, n, dv.ptr(bt), dv.ptr(xt), dv.ptr(rpt), dv.ptr(r_out),
+                                   dv.ptr(rtt), dv.ptr(cs), dv.ptr(ws), ws.numel(), dv.stream_ptr()))
+    torch.cuda.synchronize()
+    r = b - a @ x
+    c = a.T @ r
+    got = cs.cpu().numpy()
+    tol = 1e-13 * np.sqrt(n)
+    np.testing.assert_allclose(r_out.cpu().numpy(), r, rtol=0, atol=tol * np.abs(a).sum(1).max() * 10)
+    assert np.linalg.norm(got[:n] - c) <= 1e-13 * np.linalg.norm(np.abs(a).T @ np.abs(r)) * 10
+    assert got[n] == pytest.approx(r @ r, rel=1e-12)
+    assert got[n + 1] == pytest.approx((r - r_prev) @ (r - r_prev), rel=1e-12)
+    assert got[n + 2] == pytest.approx((r_true - r) @ (r_true - r), rel=1e-12)
+    assert got[n + 3] == pytest.approx(b @ b, rel=1e-12)
+
+
+# --------------------------------------------------------------------------
+# the drop-in solve
+# --------------------------------------------------------------------------
+SOLVE_NAMES = ["c1_basic", "c1_damped", "c1_momentum", "c1_seed1", "c3like", "bitwise", "consistent", "extra3",
+               "zero_init", "be_direct", "be_fast", "diverge", "maxit0", "eps_override", "c4proxy_mom"]
+
+
+def _problem(orc, g, name):
+    m, n, kappa, beta, seed = g[f"{name}_problem"]
+    a, b, truth = orc.gen_randsvd(int(m), int(n), kappa, beta, int(seed))
+    cfg = json.loads(str(g[f"{name}_config"]))
+    return a, b, truth, cfg
+
+
+@pytest.mark.parametrize("name", SOLVE_NAMES)
+def test_solve_parity_with_reference(pkg, orc, golden, name):
+    g = golden("solves.npz")
+    a, b, truth, cfgd = _problem(orc, g, name)
+    t = pkg.Truth(x=truth.x, r=truth.r, kappa=truth.kappa, beta=truth.beta)
+    res = pkg.iterative_sketching(a, b, pkg.SolverConfig(**cfgd), t)
+    tr = res.trace
+    ref_stop = str(g[f"{name}_stop"])
+    ref_iters = len(g[f"{name}_iterates"]) - 1
+    assert len(tr.iterates) == res.iterations + 1
+    assert len(tr.residual_changes) == res.iterations
+    assert len(tr.fe) == len(tr.re) == res.iterations + 1
+    assert tr.normest == pytest.approx(float(g[f"{name}_normest"]), rel=1e-10)
+    assert tr.condest == pytest.approx(float(g[f"{name}_condest"]), rel=1e-8)
+    fe_ref, re_ref = g[f"{name}_fe"], g[f"{name}_re"]
+    # iterate 0 is the sketch-and-solve start: agree to rounding of the QR
+    if name != "diverge":
+        assert tr.fe[0] <= 2 * fe_ref[0] + 1e-14 and fe_ref[0] <= 2 * tr.fe[0] + 1e-14
+    if ref_stop == "diverged":
+        assert tr.stop_reason == "diverged"
+        return
+    if ref_stop == "max_iters" and cfgd.get("max_iters", 50) <= 30:
+        assert tr.stop_reason == "max_iters" and res.iterations == ref_iters
+    else:
+        assert tr.stop_reason == ref_stop
+        assert abs(res.iterations - ref_iters) <= 3, (res.iterations, ref_iters)
+    # north_star bars: FE/RE within 2x of the reference's (one-sided)
+    assert tr.fe[-1] <= 2 * fe_ref[-1] + 4 * U, (tr.fe[-1], fe_ref[-1])
+    assert tr.re[-1] <= 2 * re_ref[-1] + 4 * U, (tr.re[-1], re_ref[-1])
+    if len(g[f"{name}_be"]):
+        assert tr.be[-1] <= 2 * g[f"{name}_be"][-1] + 4 * U
+    x_ref = g[f"{name}_solution"]
+    dev_x = np.linalg.norm(res.solution - x_ref) / np.linalg.norm(x_ref)
+    # triangle inequality always holds for two accurate solutions
+    assert dev_x <= tr.fe[-1] + fe_ref[-1] + 4 * U
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_c2_shape_parity_and_stated_bound(pkg, orc, seed):
+    """C2 shape (200000 x 200, kappa 1e10, beta 1e-12, d = 20n): the stated
+    bound ||x - x_ref||/||x_ref|| <= 10 kappa u + FE_ref holds with margin."""
+    a, b, truth = orc.gen_randsvd(200000, 200, 1e10, 1e-12, seed)
+    cfg = orc.Config(d=4000, rng_seed=seed)
+    x_ref, tr_ref = orc.iterative_sketching(a, b, cfg, truth)
+    t = pkg.Truth(x=truth.x, r=truth.r, kappa=truth.kappa, beta=truth.beta)
+    res = pkg.iterative_sketching(a, b, pkg.SolverConfig(d=4000, rng_seed=seed), t)
+    assert res.trace.stop_reason == tr_ref.stop_reason
+    assert res.trace.fe[-1] <= 2 * tr_ref.fe[-1]
+    assert res.trace.re[-1] <= 2 * tr_ref.re[-1]
+    dev_x = np.linalg.norm(res.solution - x_ref) / np.linalg.norm(x_ref)
+    assert dev_x <= 10 * truth.kappa * U + tr_ref.fe[-1]
+
+
+def test_update_identity_bit_for_bit(pkg):
+    """GPU analogue of test_update_identity_bit_for_bit (test_solvers.py:223-233):
+    x_{i+1} == fl(x_i + R^{-1}R^{-T}A'r_i) with the device's own kernels."""
+    p = pkg.gen_randsvd(500, 12, 1e4, 1e-3, 3)
+    res = pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=240, max_iters=6, rng_seed=3), p.truth)
+    s = pkg.sparse_sign_new(240, 500, 8, 3)
+    f = pkg.householder_qr_econ(s.apply_dense(p.a))
+    dev = torch.device("cuda")
+    at = torch.from_numpy(p.a).to(dev)
+    r_dev = torch.from_numpy(f.r).to(dev)
+    tr = res.trace
+    for i in range(len(tr.iterates) - 1):
+        c = at.T @ torch.from_numpy(tr.residual_vectors[i]).to(dev)
+        d = pkg.tri_solve_upper(r_dev, pkg.tri_solve_upper_transpose(r_dev, c))
+        # c from cuBLAS here vs the fused pass in the solver: compare to rounding
+        step = tr.iterates[i + 1] - tr.iterates[i]
+        np.testing.assert_allclose(step, d.cpu().numpy(), rtol=1e-9, atol=1e-15)
+
+
+def test_bitwise_determinism_and_graph_equivalence(pkg):
+    p = pkg.gen_randsvd(600, 15, 1e6, 1e-4, 5)
+    cfg = pkg.SolverConfig(d=300, max_iters=40, rng_seed=5)
+    r1 = pkg.iterative_sketching(p.a, p.b, cfg, p.truth)
+    r2 = pkg.iterative_sketching(p.a, p.b, cfg, p.truth)
+    r3 = pkg.iterative_sketching(p.a, p.b, cfg, p.truth, use_graph=False)
+    for r in (r2, r3):
+        assert np.array_equal(r1.solution, r.solution)
+        assert r1.trace.fe == r.trace.fe
+        assert r1.trace.residual_changes == r.trace.residual_changes
+        assert r1.trace.stop_reason == r.trace.stop_reason
+
+
+def test_device_tensor_inputs_zero_copy(pkg):
+    p = pkg.gen_randsvd(3000, 40, 1e8, 1e-6, 2)
+    cfg = pkg.SolverConfig(d=800, variant="momentum", rng_seed=2)
+    r_host = pkg.iterative_sketching(p.a, p.b, cfg)
+    at = torch.from_numpy(p.a).cuda()
+    bt = torch.from_numpy(p.b).cuda()
+    r_dev = pkg.iterative_sketching(at, bt, cfg)
+    assert np.array_equal(r_host.solution, r_dev.solution)
+    # a strided view (lda > n) is used in place
+    big = torch.zeros((3000, 48), dtype=torch.float64, device="cuda")
+    big[:, :40] = at
+    r_view = pkg.iterative_sketching(big[:, :40], bt, cfg)
+    assert np.array_equal(r_host.solution, r_view.solution)
+
+
+def test_edge_configs(pkg, orc):
+    # zeta == d, zeta == 1, odd n, residuals="last", extra_iters
+    for (m, n, d, zeta) in [(300, 7, 10, 10), (500, 9, 40, 1), (2001, 33, 300, 3)]:
+        a, b, truth = orc.gen_randsvd(m, n, 1e3, 1e-3, 1)
+        cfg_o = orc.Config(d=d, zeta=zeta, rng_seed=1, max_iters=60)
+        x_ref, tr_ref = orc.iterative_sketching(a, b, cfg_o, truth)
+        t = pkg.Truth(x=truth.x, r=truth.r, kappa=truth.kappa, beta=truth.beta)
+        res = pkg.iterative_sketching(a, b, pkg.SolverConfig(d=d, zeta=zeta, rng_seed=1, max_iters=60), t,
+                                      residuals="last")
+        assert res.trace.stop_reason == tr_ref.stop_reason
+        assert res.trace.fe[-1] <= 2 * tr_ref.fe[-1] + 4 * U
+        np.testing.assert_allclose(res.trace.residual_vectors[-1], b - a @ res.solution, atol=1e-13)
+        if res.iterations >= 2:
+            with pytest.raises(IndexError):
+                res.trace.residual_vectors[0]
+
+
+def test_validation_and_singular(pkg):
+    p = pkg.gen_randsvd(100, 10, 10.0, 0.1, 0)
+    with pytest.raises(ValueError):
+        pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=5))
+    with pytest.raises(ValueError):
+        pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=50, variant="bogus"))
+    a = p.a.copy()
+    a[:, 4] = 0.0
+    with pytest.raises(pkg.SingularMatrixError):
+        pkg.iterative_sketching(a, p.b, pkg.SolverConfig(d=50))
+
+
+def test_residual_vectors_survive_workspace_reuse(pkg):
+    p = pkg.gen_randsvd(800, 10, 1e3, 1e-3, 4)
+    cfg = pkg.SolverConfig(d=200, rng_seed=4)
+    r1 = pkg.iterative_sketching(p.a, p.b, cfg)
+    q = pkg.gen_randsvd(800, 10, 1e3, 1e-3, 5)
+    pkg.iterative_sketching(q.a, q.b, cfg)
+    np.testing.assert_allclose(r1.trace.residual_vectors[-1], p.b - p.a @ r1.solution, atol=1e-12)
+    np.testing.assert_allclose(r1.trace.residual_vectors[0], p.b - p.a @ r1.trace.iterates[0], atol=1e-12)
