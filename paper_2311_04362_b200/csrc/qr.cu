@@ -27,7 +27,7 @@ struct QrArgs {
   int64_t d, n, ldw, N;  // N = n + 1 columns (last is Sb) or n
   double* R;
   double* z;
-  double* part1;  // P
+  double* part1;  // 2 x P
   double* part2;  // P x NB
   double* part3;  // P x NB x ld3
   double* Zg;     // NB x N
@@ -69,10 +69,14 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr(QrArgs a) {
         ss += v * v;
       }
       ss = block_sum(ss, red);
-      if (tid == 0) a.part1[p] = ss;
+      // part1 is double-buffered by column parity: without a barrier between
+      // B(j) and A(j+1) (tau == 0), a fast CTA must not overwrite the slot a
+      // slow CTA is still summing.
+      double* part1 = a.part1 + (j & 1) * P;
+      if (tid == 0) part1[p] = ss;
       grid_barrier(a.bar);
       double t = 0.0;
-      for (int q = tid; q < P; q += QR_THREADS) t += ldcg(a.part1 + q);
+      for (int q = tid; q < P; q += QR_THREADS) t += ldcg(part1 + q);
       const double xn2 = block_sum(t, red);
       const double alpha = ldcg(W + j * ldw + j);
       double beta, tau, scal;
@@ -123,7 +127,8 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr(QrArgs a) {
           W[r * ldw + j + 1 + cc] += v * temp;
         }
       }
-      if (tid == 0 && j >= lo && j < hi) W[j * ldw + j] = beta;
+      // W[j][j] keeps alpha (other CTAs may still be reading it when there is
+      // no barrier after B); R's diagonal comes from betas[] at the end.
       __syncthreads();
     }
     // ---------------- trailing update: W -= V T' V' W (dlarft + dlarfb) ------
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr(QrArgs a) {
     const int64_t i = idx / n, c = idx % n;
     const double bi = ldcg(a.betas + i);
     const double sg = bi < 0.0 ? -1.0 : 1.0;
-    a.R[idx] = (c < i) ? 0.0 : sg * ldcg(W + i * ldw + c);
+    a.R[idx] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * ldcg(W + i * ldw + c));
   }
   for (int64_t i = gtid; i < n; i += gstride) {
     const double bi = ldcg(a.betas + i);
@@ -269,7 +274,7 @@ QrLayout qr_layout(void* ws, int64_t d, int64_t n, int has_rhs) {
   Carver cv(ws, 1ll << 62);
   L.bar = cv.take<unsigned>(64);
   L.singular = cv.take<int>(64);
-  L.part1 = cv.take<double>(L.P);
+  L.part1 = cv.take<double>(2 * L.P);
   L.part2 = cv.take<double>(static_cast<int64_t>(L.P) * NB);
   L.part3 = cv.take<double>(static_cast<int64_t>(L.P) * NB * L.ld3);
   L.Zg = cv.take<double>(NB * N);
