@@ -71,14 +71,22 @@ int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, const uint64_t 
                              uint8_t* neg, uint32_t* sk_ptr, uint32_t* sk_src, void* ws,
                              int64_t ws_bytes, itsk_stream_t stream);
 
+/* CSR (grouped by sketch row, sources ascending) of a contiguous slice of
+ * the pattern: rows/neg point at entry row0*zeta of the full (m, zeta)
+ * arrays, m is the slice length; sources are slice-local.  Used by each rank
+ * of a row-sharded solve for its own block of columns of S. */
+int itsk_pattern_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_t zeta, int64_t d,
+                     uint32_t* sk_ptr, uint32_t* sk_src, void* ws, int64_t ws_bytes,
+                     itsk_stream_t stream);
+
 /* ----------------------------------------------------------------------
  * S·[A | b] — replaces SparseSignEmbedding.apply_dense / apply_vec
  * (embed.py:62-74 → scipy csc_matvecs), called from sketch_and_solve
  * (solvers.py:207-208).  SAb is d x (n + (b != NULL)), leading dim ldw.
  * Summation order equals the reference's (ascending source row, product
  * rounded before the add), so SAb is bitwise identical to scipy's.
- * Rows [row0, row0+m) of the full matrix are the local shard (multi-GPU);
- * sk_ptr/sk_src must then be the shard's own pattern.
+ * For a row shard (multi-GPU) pass the shard's rows and its own CSR
+ * (itsk_pattern_csr); the per-rank partial sketches are then summed.
  * -------------------------------------------------------------------- */
 int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                 const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
@@ -119,10 +127,11 @@ int itsk_condest(const double* R, int64_t n, const double* v0, double* out, doub
 /* ----------------------------------------------------------------------
  * The fused pass of the refinement loop (solvers.py:290,299,343 — r = b-Ax
  * and A'r — plus the norms of solvers.py:300-302 and _record's RE):
- *   r = b - A x;  c = A' r;  scal = [|r|^2, |r - r_prev|^2, |r_true - r|^2]
- * one streaming read of A.  r_prev, r_out, r_true may be NULL.  Partials of
- * c/scal per CTA go to `part`; itsk_pass_finalize sums them in fixed order
- * (deterministic) into cs = [c(n) | scal(3)].
+ *   r = b - A x;  c = A' r;
+ *   scal = [|r|^2, |r - r_prev|^2, |r_true - r|^2, |b|^2]
+ * in one streaming read of A.  r_prev, r_out, r_true may be NULL.  Per-CTA
+ * partials go to the workspace and are summed in a fixed order
+ * (deterministic) into cs = [c(n) | scal(4)].
  * -------------------------------------------------------------------- */
 int itsk_pass_workspace(int64_t m, int64_t n, int64_t* bytes);
 int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,

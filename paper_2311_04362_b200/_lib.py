@@ -64,6 +64,7 @@ _SIGS = {
     "itsk_sparse_sign_pattern": (ctypes.c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(ctypes.c_uint64),
                                                 ctypes.c_int, ctypes.c_uint32, c_dp, c_dp, c_dp, c_dp,
                                                 c_dp, c_i64, c_dp]),
+    "itsk_pattern_csr": (ctypes.c_int, [c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_dp]),
     "itsk_sketch": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_i64, c_dp,
                                    c_i64, c_dp]),
     "itsk_qr_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),

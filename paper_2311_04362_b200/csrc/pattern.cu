@@ -301,6 +301,25 @@ int lemire_fill(const Stream& st, uint64_t* wpos, uint64_t N, uint32_t bound, ui
   return ITSK_ECUDA;
 }
 
+// Group the (m, zeta) pattern by sketch row, keeping source order ascending
+// (stable LSD sort of entries enumerated column-major == ascending j).
+int build_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_t zeta, int64_t d,
+              uint32_t* sk_ptr, uint32_t* sk_src, PatternWs& w, cudaStream_t s) {
+  const int64_t nnz = m * zeta;
+  k_pack_src<<<blocks_for(nnz, 256), 256, 0, s>>>(neg, m, zeta, w.vals_in);
+  count_launch();
+  int end_bit = 1;
+  while ((1ll << end_bit) < d) ++end_bit;
+  size_t tb = w.cub_bytes;
+  ITSK_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, rows, w.keys_out, w.vals_in, sk_src,
+                                            static_cast<int>(nnz), 0, end_bit, s));
+  count_launch(end_bit <= 8 ? 2 : 4);
+  k_row_ptr<<<blocks_for(d + 1, 256), 256, 0, s>>>(w.keys_out, nnz, d, sk_ptr);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
 }  // namespace
 }  // namespace itsk
 
@@ -372,19 +391,21 @@ extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, cons
   count_launch();
   ITSK_CHECK_LAUNCH();
   if (sk_ptr && sk_src) {
-    // Group by sketch row, keeping source order ascending (stable LSD sort
-    // of entries enumerated column-major == ascending j).
-    k_pack_src<<<blocks_for(nnz, 256), 256, 0, s>>>(neg, m, zeta, w.vals_in);
-    count_launch();
-    int end_bit = 1;
-    while ((1ll << end_bit) < d) ++end_bit;
-    size_t tb = w.cub_bytes;
-    ITSK_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, rows, w.keys_out, w.vals_in, sk_src,
-                                              static_cast<int>(nnz), 0, end_bit, s));
-    count_launch(end_bit <= 8 ? 2 : 4);
-    k_row_ptr<<<blocks_for(d + 1, 256), 256, 0, s>>>(w.keys_out, nnz, d, sk_ptr);
-    count_launch();
-    ITSK_CHECK_LAUNCH();
+    int rc2 = build_csr(rows, neg, m, zeta, d, sk_ptr, sk_src, w, s);
+    if (rc2) return rc2;
   }
   return ITSK_OK;
+}
+
+extern "C" int itsk_pattern_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_t zeta,
+                                int64_t d, uint32_t* sk_ptr, uint32_t* sk_src, void* ws,
+                                int64_t ws_bytes, itsk_stream_t stream) {
+  ITSK_REQUIRE(rows && neg && sk_ptr && sk_src && ws, "null pointer");
+  ITSK_REQUIRE(d >= 1 && m >= 1 && zeta >= 1 && m < (1ll << 31) && m * zeta < (1ll << 31),
+               "bad pattern slice");
+  Carver cv(ws, ws_bytes);
+  PatternWs w;
+  carve(cv, w, m, zeta);
+  ITSK_REQUIRE(cv.ok(), "pattern workspace too small");
+  return build_csr(rows, neg, m, zeta, d, sk_ptr, sk_src, w, reinterpret_cast<cudaStream_t>(stream));
 }

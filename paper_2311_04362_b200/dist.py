@@ -1,0 +1,161 @@
+"""Row-sharded iterative sketching over several B200s (one process per GPU).
+
+A, b (and truth.r) are split into contiguous row blocks, rank g owning rows
+[r0_g, r1_g).  Exactness follows from the column structure of the two
+products on the path:
+
+    S·[A | b] = sum_g S[:, J_g] [A_g | b_g]        (one allreduce, d x (n+1))
+    A'r       = sum_g A_g' r_g                      (one allreduce per iteration,
+                                                     fused with the 4 norm partials)
+
+Everything else — the QR of the reduced sketch, x0, normest/condest, the two
+triangular solves, the update, the stopping rule and the divergence guard —
+is replicated: every rank holds bit-identical inputs (an allreduce returns the
+same bytes on every rank) and runs the same deterministic kernels, so the
+iterates agree bitwise across ranks without any further exchange.
+
+The collective is torch.distributed.all_reduce (NCCL over NVLink/NVSwitch on
+the GPU box) issued on the solver's stream between itsk_loop_step_pre and
+itsk_loop_step_post.  The loop driver (`run_sharded_loop`) and the shard
+arithmetic are plain host logic, tested with gloo on CPU (tests/test_dist_gloo.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as _dev
+from .embed import pcg_state
+from .linalg import normest_steps, start_vector
+from .problems import Truth
+from .solvers import (SolverConfig, _assemble, _loop_params, _read_result, _Workspace, update_coeffs)
+
+
+def shard_bounds(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced row block of `rank` (first m % world ranks get one more)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of size {world}")
+    base, extra = divmod(m, world)
+    r0 = rank * base + min(rank, extra)
+    return r0, r0 + base + (1 if rank < extra else 0)
+
+
+def run_sharded_loop(step_pre, allreduce_cs, step_post, is_done, max_iters: int, check_every: int = 4) -> int:
+    """Drive the replicated refinement loop around its one collective.
+
+    Every rank calls the same sequence; the device-side control makes the
+    per-iteration kernels no-ops once the stopping rule / guard fired, so the
+    host only polls `is_done` every `check_every` iterations (it is identical
+    on all ranks, which therefore issue the same number of collectives).
+    Returns the number of iterations issued."""
+    issued = 0
+    while issued < max_iters:
+        for _ in range(min(check_every, max_iters - issued)):
+            step_pre()
+            allreduce_cs()
+            step_post()
+            issued += 1
+        if is_done():
+            break
+    return issued
+
+
+class ShardedWorkspace(_Workspace):
+    """Workspace of one rank: full-size pattern (generated on every rank from
+    the shared seed), local CSR, local A / b / r_true, replicated sketch and R."""
+
+    def __init__(self, dev, m_total, m_local, n, d, zeta, max_iters, r_slots, with_truth):
+        super().__init__(dev, m_local, n, d, zeta, max_iters, r_slots, with_truth)
+        self.m_total = m_total
+        lib = _dev.lib(dev)
+        nnz_full = m_total * zeta
+        self.rows_full = torch.empty(nnz_full, dtype=torch.int32, device=dev)
+        self.neg_full = torch.empty(nnz_full, dtype=torch.uint8, device=dev)
+        nb = ctypes.c_int64()
+        _lib.check(lib.itsk_pattern_workspace(d, m_total, zeta, ctypes.byref(nb)))
+        self.pat_ws = _dev.workspace(nb.value, dev)
+
+
+def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
+                                truth: Truth | None = None, group=None, *, residuals: str = "last",
+                                check_every: int = 4):
+    """Row-sharded solve.  Each rank passes its own block [row0, row0+m_local)
+    of A and b (numpy or CUDA tensors); `truth.r` may be the full vector or
+    the local slice.  Returns a SolveResult whose iterates / solution / trace
+    scalars are identical on every rank; residual_vectors hold the local rows."""
+    import torch.distributed as tdist
+
+    a_shape = a_local.shape
+    m_loc, n = int(a_shape[0]), int(a_shape[1])
+    cfg.validate(n)
+    alpha, beta = update_coeffs(cfg, n)
+    if cfg.track_be:
+        raise ValueError("track_be is not supported by the sharded solver")
+    dev = _dev.current_device()
+    lib = _dev.lib(dev)
+    r_slots = cfg.max_iters + 1 if residuals == "all" else 2
+    ws = ShardedWorkspace(dev, m_total, m_loc, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots, truth is not None)
+    at, lda = _dev.as_device_matrix(a_local, dev)
+    ws.b.copy_(_dev.as_device_vector(b_local, dev))
+    if truth is not None:
+        ws.x_true.copy_(torch.from_numpy(np.asarray(truth.x, dtype=np.float64)))
+        if truth.beta > 0:
+            r = np.asarray(truth.r, dtype=np.float64)
+            r = r[row0:row0 + m_loc] if r.shape[0] == m_total else r
+            ws.r_true.copy_(torch.from_numpy(np.ascontiguousarray(r)))
+    stream_obj = torch.cuda.current_stream(dev)
+    stream = int(stream_obj.cuda_stream)
+
+    def allreduce(t: torch.Tensor):
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
+
+    # pattern of all m columns from the shared seed, CSR of this rank's block
+    words, has32, pend = pcg_state(cfg.rng_seed)
+    _lib.check(lib.itsk_sparse_sign_pattern(
+        cfg.d, m_total, cfg.zeta, words, has32, pend, _dev.ptr(ws.rows_full), _dev.ptr(ws.neg_full),
+        None, None, _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
+    off = row0 * cfg.zeta
+    _lib.check(lib.itsk_pattern_csr(
+        _dev.ptr(ws.rows_full) + 4 * off, _dev.ptr(ws.neg_full) + off, m_loc, cfg.zeta, cfg.d,
+        _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
+    _lib.check(lib.itsk_sketch(_dev.ptr(at), m_loc, n, lda, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr),
+                               _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
+    allreduce(ws.W)
+    _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
+                               _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
+    if cfg.init == "zero":
+        ws.xs[0].zero_()
+    else:
+        _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
+    ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
+    _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), _dev.ptr(ws.est),
+                                None, stream))
+    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, None, stream))
+
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=m_loc)
+    cs = ws.cs[: n + 4]
+    _lib.check(lib.itsk_loop_begin_local(ctypes.byref(p), stream))
+    allreduce(cs)
+    _lib.check(lib.itsk_loop_begin_finish(ctypes.byref(p), stream))
+    rp = ctypes.c_void_p()
+    _lib.check(lib.itsk_loop_result_ptr(ctypes.byref(p), ctypes.byref(rp)))
+    res_off = rp.value - _dev.ptr(ws.loop_ws)
+    done_dev = ws.loop_ws[res_off + 8: res_off + 12]  # itsk_loop_result.done
+
+    def is_done() -> bool:
+        return bool(done_dev.view(torch.int32).item())
+
+    run_sharded_loop(
+        lambda: _lib.check(lib.itsk_loop_step_pre(ctypes.byref(p), stream)),
+        lambda: allreduce(cs),
+        lambda: _lib.check(lib.itsk_loop_step_post(ctypes.byref(p), stream)),
+        is_done, cfg.max_iters, check_every)
+    res = _read_result(lib, ws, p, stream_obj)
+    out = _assemble(ws, res, truth, cfg, at, ws.b)
+    out._workspace = ws  # keep the local residual rows alive
+    return out

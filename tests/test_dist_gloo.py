@@ -1,0 +1,130 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the row-sharded solve's
+host logic: shard bounds, the pattern slice each rank owns, the two sums
+(sketch once, [A'r | norms] per iteration) and the loop driver
+`run_sharded_loop`.  The per-rank arithmetic is stood in by the CPU oracle;
+on the GPU box the same driver calls the C-ABI kernels."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2311_04362_b200.dist import run_sharded_loop, shard_bounds
+
+
+def test_shard_bounds_cover_rows():
+    for m in (1, 7, 100, 200000):
+        for world in (1, 2, 3, 8):
+            if world > m:
+                continue
+            spans = [shard_bounds(m, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+
+
+def test_loop_driver_polls_and_stops():
+    calls = []
+    state = {"k": 0}
+
+    def pre():
+        calls.append("pre")
+
+    def ar():
+        calls.append("ar")
+
+    def post():
+        calls.append("post")
+        state["k"] += 1
+
+    n = run_sharded_loop(pre, ar, post, lambda: state["k"] >= 6, max_iters=50, check_every=4)
+    assert n == 8 and calls[:3] == ["pre", "ar", "post"]
+    assert run_sharded_loop(pre, ar, post, lambda: False, max_iters=3, check_every=4) == 3
+    assert run_sharded_loop(pre, ar, post, lambda: False, max_iters=0) == 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import itsketch_oracle as orc
+
+        m, n, d, zeta, seed = 3000, 12, 200, 8, 4
+        a, b, truth = orc.gen_randsvd(m, n, 1e6, 1e-5, seed)
+        pat = orc.sparse_sign_pattern(d, m, zeta, seed)
+        r0, r1 = shard_bounds(m, world, rank)
+        # this rank's block of S's columns
+        local = orc.Pattern(d, r1 - r0, zeta, pat.rows[r0:r1], pat.signs[r0:r1], pat.scale)
+        sab = torch.from_numpy(orc.sketch_apply(local, np.column_stack([a[r0:r1], b[r0:r1]])))
+        dist.all_reduce(sab)
+        full = orc.sketch_apply(pat, np.column_stack([a, b]))
+        sketch_err = float(np.abs(sab.numpy() - full).max() / np.abs(full).max())
+        q, rf = orc.householder_qr_econ(sab.numpy()[:, :n])
+        x = orc.tri_solve_upper(rf, q.T @ sab.numpy()[:, n])
+        normest = orc.rand_power_norm_est(rf, rng_seed=seed)
+        condest = orc.cond_est(rf)
+        al, bl = a[r0:r1], b[r0:r1]
+        st = {"x": x, "r": bl - al @ x, "iters": 0, "done": False}
+        cs = torch.zeros(n + 2, dtype=torch.float64)
+
+        def pre():
+            if st["done"]:
+                cs.zero_()
+                return
+            c = al.T @ st["r"]
+            cs.copy_(torch.from_numpy(np.concatenate([c, [0.0, 0.0]])))
+
+        def post():
+            if st["done"]:
+                return
+            c = cs.numpy()[:n].copy()
+            step = orc.tri_solve_upper(rf, orc.tri_solve_upper_transpose(rf, c))
+            xn = st["x"] + step
+            rn = bl - al @ xn
+            sums = torch.tensor([rn @ rn, (rn - st["r"]) @ (rn - st["r"])], dtype=torch.float64)
+            dist.all_reduce(sums)
+            change, resn = float(np.sqrt(sums[1])), float(np.sqrt(sums[0]))
+            st["x"], st["r"] = xn, rn
+            st["iters"] += 1
+            bound = 2.0**-53 * (normest * np.linalg.norm(xn) + 0.04 * condest * resn)
+            if change <= bound or st["iters"] >= 40:
+                st["done"] = True
+
+        issued = run_sharded_loop(pre, lambda: dist.all_reduce(cs), post, lambda: st["done"], 40, 4)
+        x_ref, tr = orc.iterative_sketching(a, b, orc.Config(d=d, zeta=zeta, rng_seed=seed, max_iters=40), truth)
+        out[rank] = dict(sketch_err=sketch_err, x=st["x"], iters=st["iters"], issued=issued,
+                         ref_iters=len(tr.iterates) - 1, x_ref=x_ref)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_solve_gloo():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert res[0]["sketch_err"] < 1e-14 and res[1]["sketch_err"] < 1e-14
+    # replicated state: identical iterates on both ranks
+    assert np.array_equal(res[0]["x"], res[1]["x"])
+    assert res[0]["iters"] == res[1]["iters"] and res[0]["issued"] == res[1]["issued"]
+    assert abs(res[0]["iters"] - res[0]["ref_iters"]) <= 2
+    x_ref = res[0]["x_ref"]
+    assert np.linalg.norm(res[0]["x"] - x_ref) <= 1e-6 * np.linalg.norm(x_ref)
