@@ -1,6 +1,8 @@
 // Process-level pieces of the C ABI: error strings, version, device check,
 // launch counter.
 #include <atomic>
+#include <mutex>
+#include <unordered_set>
 #include <cstdarg>
 #include <cstdio>
 
@@ -19,6 +21,23 @@ void set_error(const char* fmt, ...) {
 }
 
 void count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+cudaError_t allow_max_smem(const void* func) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(func)) return cudaSuccess;
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, func);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - static_cast<int>(fa.sharedSizeBytes));
+  if (e == cudaSuccess) done.insert(func);
+  return e;
+}
 
 int num_sms() {
   static int cached = 0;

@@ -38,6 +38,10 @@ void count_launch(int64_t k = 1);
 
 int num_sms();
 
+// Raise `func`'s dynamic shared-memory limit to the device maximum (once per
+// kernel per process; cudaFuncSetAttribute is too slow to call per launch).
+cudaError_t allow_max_smem(const void* func);
+
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -65,7 +65,7 @@ struct PassArgs {
 
 int pass_grid(int64_t m, int64_t n);
 int64_t pass_part_doubles(int64_t m, int64_t n);
-int launch_pass(const PassArgs& a, cudaStream_t s);
+int launch_pass(const PassArgs& a, cudaStream_t s, int* grid_used);
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s);
 

@@ -54,16 +54,31 @@ __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iter
   ctl->result.bnorm2 = 0.0;
 }
 
-__global__ void __launch_bounds__(1024) k_step_trsv(LoopPtrs p) {
+template <bool PACKED>
+__global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
   if (p.ctl->result.done) return;
   extern __shared__ double sm[];
   const int64_t n = p.ctl->n;
-  double* v = sm;
-  double* tmp = sm + n;
+  double* v;
+  double* tmp;
+  if (PACKED) {
+    stage_packed(p.R, n, sm);
+    v = sm + packed_doubles(n);
+  } else {
+    v = sm;
+  }
+  tmp = v + n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   __syncthreads();
-  trsv_t_inplace(p.R, n, v);
-  trsv_n_inplace(p.R, n, v, tmp);
+  if (PACKED) {
+    const RPacked R{sm, n};
+    trsv_t_inplace(R, n, v);
+    trsv_n_inplace(R, n, v, tmp);
+  } else {
+    const RGlobal R{p.R, n};
+    trsv_t_inplace(R, n, v);
+    trsv_n_inplace(R, n, v, tmp);
+  }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p.step[i] = v[i];
 }
 
@@ -263,27 +278,34 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   return a;
 }
 
-size_t trsv_smem(int64_t n) { return static_cast<size_t>(n + 32) * sizeof(double); }
+bool trsv_packed(int64_t n) { return use_packed(n, n + 32); }
+
+size_t trsv_smem(int64_t n) {
+  return static_cast<size_t>((trsv_packed(n) ? packed_doubles(n) : 0) + n + 32) * sizeof(double);
+}
 
 int enqueue_pre(const itsk_loop_params* p, const LoopPtrs& q, cudaStream_t s) {
   const size_t smem = trsv_smem(p->n);
-  k_step_trsv<<<1, 1024, smem, s>>>(q);
+  if (trsv_packed(p->n))
+    k_step_trsv<true><<<1, DENSE_THREADS, smem, s>>>(q);
+  else
+    k_step_trsv<false><<<1, DENSE_THREADS, smem, s>>>(q);
   count_launch();
   ITSK_CHECK_LAUNCH();
   const int ub = static_cast<int>(std::min<int64_t>((p->n + 255) / 256, 64));
   k_update<<<ub, 256, 0, s>>>(q);
   count_launch();
   ITSK_CHECK_LAUNCH();
-  int rc = launch_pass(pass_args(p, q, 1), s);
+  int grid = 0;
+  int rc = launch_pass(pass_args(p, q, 1), s, &grid);
   if (rc) return rc;
-  return launch_finalize(q.part, pass_grid(p->m, p->n), p->n, p->cs, q.ctl, s);
+  return launch_finalize(q.part, grid, p->n, p->cs, q.ctl, s);
 }
 
 int prepare_attrs(int64_t n) {
-  const size_t smem = trsv_smem(n);
-  if (smem > 48 * 1024)
-    ITSK_CUDA(cudaFuncSetAttribute(k_step_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
+  (void)n;
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_step_trsv<true>)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_step_trsv<false>)));
   return ITSK_OK;
 }
 
@@ -320,9 +342,10 @@ extern "C" int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t st
                               p->u, p->gamma, p->rho, p->truth_beta);
   count_launch();
   ITSK_CHECK_LAUNCH();
-  rc = launch_pass(pass_args(p, q, 2), s);
+  int grid = 0;
+  rc = launch_pass(pass_args(p, q, 2), s, &grid);
   if (rc) return rc;
-  return launch_finalize(q.part, pass_grid(p->m, p->n), p->n, p->cs, q.ctl, s);
+  return launch_finalize(q.part, grid, p->n, p->cs, q.ctl, s);
 }
 
 extern "C" int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream) {

@@ -11,6 +11,8 @@
 // streaming loads; each CTA owns a contiguous row range.  Per-CTA partials
 // are summed by k_finalize in a fixed order, so c and the norms are
 // bitwise reproducible run to run.
+#include <algorithm>
+
 #include "itsk_common.cuh"
 #include "itsk_kernels.cuh"
 
@@ -137,14 +139,265 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(PassArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant (sm_100a): one producer warp streams contiguous tiles of
+// T rows (T*lda*8 bytes, one cp.async.bulk each, L2 evict-first) into an
+// S-stage shared-memory ring guarded by mbarriers; 8 consumer warps take rows
+// round-robin from the ring.  The row is read twice from shared memory (dot,
+// then c update), so registers hold only c (and x when it fits) — this keeps
+// ~S*16 KB of HBM traffic in flight per SM independent of n.
+// ---------------------------------------------------------------------------
+constexpr int TMA_MAX_CONSUMERS = 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+struct TmaShape {
+  int T;            // rows per tile (multiple of UNR)
+  int S;            // stages
+  int stage_bytes;  // T*lda*8, 128-aligned
+};
+
+// Consumer warps take batches of UNR consecutive rows (a batch never spans
+// two tiles): the UNR dot products and their shuffle reductions are
+// interleaved, so the per-row latency chain (LDS -> FMA chain -> 5 shuffles)
+// is paid once per batch.  Only A goes through the bulk-copy ring — one copy
+// per tile; per-copy cost, not bytes, limits TMA at small sizes — while lanes
+// 0..UNR-1 prefetch b / r_prev / r_true of the warp's batch two steps ahead
+// with ordinary loads.  stage_tile[s] names the tile a stage holds, so a
+// consumer never waits on an mbarrier phase that aliases an older tile.
+template <int CPL, int UNR, int NCW>
+__global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaShape sh) {
+  constexpr int THREADS = 32 * (NCW + 1);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NC = 32 * CPL;
+  constexpr bool XREG = CPL <= 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + 32;
+  int* stage_tile = reinterpret_cast<int*>(empty + 32);
+  double* xsm = reinterpret_cast<double*>(smraw + 1024);
+  unsigned char* stages = smraw + 1024 + (XREG ? 0 : NC * 8);
+  __shared__ double ssm[NCW][4];
+
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  if (a.mode == 0) {
+    x = a.x;
+    r_prev = a.r_prev;
+    r_out = a.r_out;
+  } else {
+    const LoopCtl* ctl = a.ctl;
+    if (ctl->result.done) return;
+    const int64_t S = ctl->r_slots;
+    if (a.mode == 1) {
+      const int64_t it = ctl->it;
+      x = a.xs + (it + 1) * a.n;
+      r_prev = a.rs + (it % S) * a.m;
+      r_out = a.rs + ((it + 1) % S) * a.m;
+    } else {
+      x = a.xs;
+      r_prev = nullptr;
+      r_out = a.rs;
+    }
+  }
+  const double* r_true = a.r_true;
+  const double* b = a.b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n, lda = a.lda;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
+  const int T = sh.T, S = sh.S;
+  const int ntiles = (nrows + T - 1) / T;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, T / UNR);  // one arrival per consumed batch
+      stage_tile[s] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!XREG)
+    for (int c = tid; c < NC; c += THREADS) xsm[c] = (c < n) ? x[c] : 0.0;
+  __syncthreads();
+
+  double acc[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
+
+  if (warp == NCW) {
+    // ---------------- producer: one elected lane, one bulk copy per tile ---
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t % S;
+        if (t >= S) mbar_wait(empty + s, static_cast<unsigned>(((t / S) - 1) & 1));
+        const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
+        const int rows = min(T, nrows - t * T);
+        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+        reinterpret_cast<volatile int*>(stage_tile)[s] = t;
+        mbar_expect_tx(full + s, bytes);
+        bulk_g2s(stages + static_cast<int64_t>(s) * sh.stage_bytes, a.A + row0 * lda, bytes, full + s, pol);
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    double xv[XREG ? CPL : 1];
+    if (XREG) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        xv[q] = (c < n) ? x[c] : 0.0;
+      }
+    }
+    // lane u < UNR carries row u of the batch: prefetched scalars and sums
+    double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
+    constexpr int STEP = NCW * UNR;
+    auto fetch = [&](int k, double& fb, double& fp, double& ft) {
+      const int kk = k + lane;
+      const bool ok = lane < UNR && kk < nrows;
+      const int64_t g = r_begin + kk;
+      fb = ok ? b[g] : 0.0;
+      fp = (ok && r_prev) ? r_prev[g] : 0.0;
+      ft = (ok && r_true) ? r_true[g] : 0.0;
+    };
+    double cb, cp, ct, nb, np, nt;
+    const int k_first = warp * UNR;
+    fetch(k_first, cb, cp, ct);
+    fetch(k_first + STEP, nb, np, nt);
+    for (int k0 = k_first; k0 < nrows; k0 += STEP) {
+      double fb, fp, ft;
+      fetch(k0 + 2 * STEP, fb, fp, ft);
+      const int t = k0 / T;
+      const int s = t % S;
+      while (reinterpret_cast<volatile int*>(stage_tile)[s] != t) __nanosleep(20);
+      mbar_wait(full + s, static_cast<unsigned>((t / S) & 1));
+      const double* base =
+          reinterpret_cast<const double*>(stages + static_cast<int64_t>(s) * sh.stage_bytes) +
+          static_cast<int64_t>(k0 - t * T) * lda;
+      const int nu = min(UNR, nrows - k0);
+      double dot[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) dot[u] = 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        if (c < n) {
+          const double xq = XREG ? xv[XREG ? q : 0] : xsm[c];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            if (u < nu) dot[u] = fma(base[u * lda + c], xq, dot[u]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) dot[u] += __shfl_xor_sync(FULL, dot[u], o);
+      double r[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) r[u] = __shfl_sync(FULL, cb, u) - dot[u];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        if (c < n) {
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            if (u < nu) acc[q] = fma(r[u], base[u * lda + c], acc[q]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);  // release after every read of the stage
+      if (lane < nu) {
+        double rl = r[0];
+#pragma unroll
+        for (int u = 1; u < UNR; ++u)
+          if (lane == u) rl = r[u];
+        if (r_out) r_out[r_begin + k0 + lane] = rl;
+        s_rr += rl * rl;
+        s_bb += cb * cb;
+        const double dd = rl - cp;
+        s_dd += dd * dd;
+        const double tt = ct - rl;
+        s_tt += tt * tt;
+      }
+      cb = nb; cp = np; ct = nt;
+      nb = fb; np = fp; nt = ft;
+    }
+    // fixed-order combination of the UNR lane partials
+    s_rr = warp_sum(s_rr);
+    s_dd = warp_sum(s_dd);
+    s_tt = warp_sum(s_tt);
+    s_bb = warp_sum(s_bb);
+    if (lane == 0) {
+      ssm[warp][0] = s_rr;
+      ssm[warp][1] = r_prev ? s_dd : 0.0;
+      ssm[warp][2] = r_true ? s_tt : 0.0;
+      ssm[warp][3] = s_bb;
+    }
+  }
+  __syncthreads();  // all tiles consumed: the ring is free for the reduction
+  double* csm = reinterpret_cast<double*>(stages);
+  if (warp < NCW) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) csm[warp * NC + lane + 32 * q] = acc[q];
+  }
+  __syncthreads();
+  double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
+  for (int c = tid; c < n; c += THREADS) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) sum += csm[w * NC + c];
+    out[c] = sum;
+  }
+  if (tid < 4) {
+    double sum = 0.0;
+    for (int w = 0; w < NCW; ++w) sum += ssm[w][tid];
+    out[n + tid] = sum;
+  }
+}
+
+// Fixed-order reduction of the per-CTA partials: one warp per output, lanes
+// take CTAs strided by 32, then a fixed shuffle tree.
 __global__ void k_finalize(const double* __restrict__ part, int grid, int64_t n, double* cs,
                            const LoopCtl* ctl) {
   if (ctl && ctl->result.done) return;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (c >= n + 4) return;
   double s = 0.0;
-  for (int g = 0; g < grid; ++g) s += part[static_cast<int64_t>(g) * (n + 4) + c];
-  cs[c] = s;
+  for (int g = lane; g < grid; g += 32) s += part[static_cast<int64_t>(g) * (n + 4) + c];
+  s = warp_sum(s);
+  if (lane == 0) cs[c] = s;
 }
 
 template <int CPL>
@@ -164,8 +417,7 @@ int blocks_per_sm() {
   static int cached = -1;
   if (cached < 0) {
     const size_t smem = pass_smem<CPL>();
-    cudaFuncSetAttribute(k_pass<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    allow_max_smem(reinterpret_cast<const void*>(k_pass<CPL>));
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pass<CPL>, PASS_THREADS, smem) !=
             cudaSuccess ||
@@ -197,24 +449,111 @@ int launch_cpl(const PassArgs& a, int grid, cudaStream_t s) {
   return ITSK_OK;
 }
 
+constexpr int TMA_SMEM_BUDGET = 220 * 1024;
+
+// columns per lane for the TMA path: exact multiples of 32 up to 8, then
+// powers of two (ragged lanes are predicated off)
+int tma_cpl(int64_t n) {
+  const int64_t need = (n + 31) / 32;
+  if (need <= 8) return static_cast<int>(std::max<int64_t>(1, need));
+  if (need <= 16) return 16;
+  if (need <= 32) return 32;
+  return 64;
+}
+
+bool tma_eligible(const PassArgs& a) {
+  // bulk copies need 16-byte aligned source rows
+  return reinterpret_cast<uintptr_t>(a.A) % 16 == 0 && (a.lda % 2 == 0) && a.n <= 2048;
+}
+
+TmaShape tma_shape(int64_t lda, int cpl, int unr, int ncw) {
+  TmaShape sh;
+  const int64_t row_bytes = lda * 8;
+  // ~16 KB (at least UNR rows) per bulk copy
+  int64_t T = std::max<int64_t>(1, (16384 + row_bytes - 1) / row_bytes);
+  T = ((T + unr - 1) / unr) * unr;
+  sh.T = static_cast<int>(T);
+  sh.stage_bytes = static_cast<int>(align_up(T * row_bytes, 128));
+  const int xbytes = cpl > 8 ? 32 * cpl * 8 : 0;
+  sh.S = std::min(24, (TMA_SMEM_BUDGET - 1024 - xbytes) / sh.stage_bytes);
+  const int red = ncw * 32 * cpl * 8;  // final reduction reuses the ring
+  while (sh.S * sh.stage_bytes < red) ++sh.S;
+  return sh;
+}
+
+size_t tma_smem(const TmaShape& sh, int cpl) {
+  return 1024 + (cpl > 8 ? 32 * cpl * 8 : 0) + static_cast<size_t>(sh.S) * sh.stage_bytes;
+}
+
+template <int CPL, int UNR, int NCW>
+int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
+  PassArgs a = a0;
+  const TmaShape sh = tma_shape(a.lda, CPL, UNR, NCW);
+  // Row partition depends only on (m, grid) — not on lda or the tile size —
+  // so the fixed-order reduction of c is the same for any leading dimension.
+  a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
+  const size_t smem = tma_smem(sh, CPL);
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>)));
+  k_pass_tma<CPL, UNR, NCW><<<grid, 32 * (NCW + 1), smem, s>>>(a, sh);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+// rows per consumer batch: 4 while a row is <= 16 columns per lane, then
+// fewer so c stays in registers
+template <int CPL>
+int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
+  constexpr int UNR = CPL <= 16 ? 4 : (CPL <= 32 ? 2 : 1);
+  constexpr int NCW = CPL <= 16 ? 16 : 8;  // more consumer warps while c fits in registers
+  return launch_tma_u<CPL, UNR, NCW>(a, grid, s);
+}
+
+int tma_grid(int64_t m) {
+  int64_t g = num_sms();
+  const int64_t cap = (m + 7) / 8;
+  if (g > cap) g = cap;
+  return static_cast<int>(std::max<int64_t>(1, g));
+}
+
 }  // namespace
 
-int pass_grid(int64_t m, int64_t n) {
+int pass_grid_v1(int64_t m, int64_t n) {
   const int cpl = cpl_for(n);
-  int64_t g = static_cast<int64_t>(num_sms()) * occupancy_for(cpl);
+  int64_t g = static_cast<int64_t>(num_sms()) * occupancy_for(std::min(cpl, 32));
   const int64_t cap = (m + PASS_WARPS - 1) / PASS_WARPS;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<int>(g);
 }
 
+int pass_grid(int64_t m, int64_t n) { return std::max(pass_grid_v1(m, n), tma_grid(m)); }
+
 int64_t pass_part_doubles(int64_t m, int64_t n) {
   return static_cast<int64_t>(pass_grid(m, n)) * (n + 4);
 }
 
-int launch_pass(const PassArgs& a0, cudaStream_t s) {
+int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
+  if (tma_eligible(a0)) {
+    const int grid = tma_grid(a0.m);
+    *grid_used = grid;
+    switch (tma_cpl(a0.n)) {
+      case 1: return launch_tma<1>(a0, grid, s);
+      case 2: return launch_tma<2>(a0, grid, s);
+      case 3: return launch_tma<3>(a0, grid, s);
+      case 4: return launch_tma<4>(a0, grid, s);
+      case 5: return launch_tma<5>(a0, grid, s);
+      case 6: return launch_tma<6>(a0, grid, s);
+      case 7: return launch_tma<7>(a0, grid, s);
+      case 8: return launch_tma<8>(a0, grid, s);
+      case 16: return launch_tma<16>(a0, grid, s);
+      case 32: return launch_tma<32>(a0, grid, s);
+      default: return launch_tma<64>(a0, grid, s);
+    }
+  }
   PassArgs a = a0;
-  const int grid = pass_grid(a.m, a.n);
+  const int grid = pass_grid_v1(a.m, a.n);
+  *grid_used = grid;
   a.rows_per_cta = (a.m + grid - 1) / grid;
   switch (cpl_for(a.n)) {
     case 1: return launch_cpl<1>(a, grid, s);
@@ -224,16 +563,16 @@ int launch_pass(const PassArgs& a0, cudaStream_t s) {
     case 16: return launch_cpl<16>(a, grid, s);
     case 32: return launch_cpl<32>(a, grid, s);
     default:
-      set_error("fused pass: n=%lld exceeds the register-resident row limit (1024)",
-                (long long)a.n);
+      set_error("fused pass: n=%lld with an odd leading dimension exceeds the register-resident "
+                "row limit (1024)", (long long)a.n);
       return ITSK_EINVAL;
   }
 }
 
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s) {
-  const int t = 128;
-  k_finalize<<<static_cast<unsigned>((n + 4 + t - 1) / t), t, 0, s>>>(part, grid, n, cs, ctl);
+  const int t = 256;
+  k_finalize<<<static_cast<unsigned>(((n + 4) * 32 + t - 1) / t), t, 0, s>>>(part, grid, n, cs, ctl);
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
@@ -269,7 +608,8 @@ extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t ld
   a.r_true = r_true;
   a.part = static_cast<double*>(ws);
   a.mode = 0;
-  int rc = launch_pass(a, s);
+  int grid = 0;
+  int rc = launch_pass(a, s, &grid);
   if (rc) return rc;
-  return launch_finalize(a.part, pass_grid(m, n), n, cs, nullptr, s);
+  return launch_finalize(a.part, grid, n, cs, nullptr, s);
 }

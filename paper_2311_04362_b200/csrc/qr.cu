@@ -2,181 +2,268 @@
 //
 // Replaces householder_qr_econ (/root/reference/pkg/src/itsketch/linalg.py:30-47,
 // LAPACK dgeqrf + dorgqr, then diag(R) >= 0) and the x0 right-hand side
-// Q'·Sb (solvers.py:209).  Blocked right-looking Householder (LAPACK
-// dgeqr2/dlarft/dlarfb semantics, dlarfg's beta = -sign(alpha)*||x||), run as
-// ONE cooperative kernel: every CTA owns a contiguous block of rows of W for
-// the whole factorisation; column norms and reflector products are reduced
-// across CTAs with fixed-order sums (deterministic, identical on every CTA)
-// between software grid barriers.  Q is never formed: the reflectors are
+// Q'·Sb (solvers.py:209).  Blocked right-looking Householder with LAPACK's
+// dlarfg convention (beta = -sign(alpha) ||x||) and dlarft/dlarfb compact-WY
+// trailing updates, run as ONE kernel whose CTAs each own a contiguous block
+// of rows for the whole factorisation.  Q is never formed: the reflectors are
 // applied to the Sb column like any other trailing column, which yields
-// z = (Q'Sb)[:n] directly.  The trailing update W -= V (T'(V'W)) of each
-// 32-wide panel is computed per CTA on its own rows.
+// z = (Q'Sb)[:n] directly.
+//
+// Per column there is exactly ONE cross-CTA exchange: every CTA publishes
+// [sum_{r>j} x_r^2, sum_{r>j} x_r a_rc (c in the panel)] for its rows (and
+// the owner of row j appends row j), after which every CTA forms beta, tau
+// and v'a_c = a_jc + scal * sum_{r>j} x_r a_rc locally — the quantities
+// dgeqr2 computes with two passes (dnrm2, then dlarf's dgemv).  The CTA's
+// rows of the current 32-wide panel live in shared memory.
+//
+// Two launch shapes share the code:
+//   cluster mode  one thread-block cluster of <= 16 CTAs (small d, e.g. C2
+//                 d = 4000): records are exchanged through distributed shared
+//                 memory and synchronisation is barrier.cluster;
+//   grid mode     a cooperative grid of up to 148 CTAs (large d): records in
+//                 global memory, software grid barrier.
+// All cross-CTA sums run in fixed CTA order, so R is bitwise reproducible and
+// identical on every CTA.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "itsk_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace itsk {
 namespace {
 
 constexpr int NB = 32;
-constexpr int QR_THREADS = 256;
-constexpr int YCH = 64;  // Y columns reduced per smem chunk
+constexpr int PSL = NB + 1;  // padded row stride of the panel cache: column walks are conflict-free
+constexpr int QR_THREADS = 512;
+constexpr int QR_WARPS = QR_THREADS / 32;
+constexpr int REC = 2 * NB;  // [S_c (NB) | row j of the panel (NB, owner only)]
 
 struct QrArgs {
   double* W;
-  int64_t d, n, ldw, N;  // N = n + 1 columns (last is Sb) or n
+  int64_t d, n, ldw, N;  // N = n + 1 (Sb column) or n
   double* R;
   double* z;
-  double* part1;  // 2 x P
-  double* part2;  // P x NB
-  double* part3;  // P x NB x ld3
-  double* Zg;     // NB x N
-  double* betas;  // n
-  double* taus;   // n
-  unsigned* bar;
   int* singular;
+  // grid-mode exchange buffers (global)
+  double* grec;  // 2 x P x REC
+  double* ggy;   // P x NB x (NB + N)
+  double* gz;    // NB x N
+  unsigned* bar;
   int64_t hmax;
-  int64_t ld3;
 };
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-__global__ void __launch_bounds__(QR_THREADS) k_qr(QrArgs a) {
-  extern __shared__ double sm[];
-  const int P = gridDim.x, p = blockIdx.x, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarp = QR_THREADS / 32;
+__device__ __forceinline__ int64_t split_lo(int q, int P, int64_t len) {
+  return (static_cast<int64_t>(q) * len) / P;
+}
+
+// CTA q of P owning index j of a range of length len split by split_lo.
+__device__ __forceinline__ int split_owner(int64_t j, int P, int64_t len) {
+  int q = static_cast<int>((j * P) / len);
+  while (q > 0 && split_lo(q, P, len) > j) --q;
+  while (q + 1 < P && split_lo(q + 1, P, len) <= j) ++q;
+  return q;
+}
+
+// Exchange through global memory + software grid barrier.
+struct XGrid {
+  double* rec;
+  double* gy;
+  double* z;
+  unsigned* bar;
+  int P, p;
+  int64_t ldgy, N;
+  __device__ double* rec_w(int buf) const { return rec + (static_cast<int64_t>(buf) * P + p) * REC; }
+  __device__ double rec_r(int buf, int q, int i) const {
+    return ldcg(rec + (static_cast<int64_t>(buf) * P + q) * REC + i);
+  }
+  __device__ double* gy_w() const { return gy + static_cast<int64_t>(p) * NB * ldgy; }
+  __device__ double gy_r(int q, int jj, int64_t c) const {
+    return ldcg(gy + (static_cast<int64_t>(q) * NB + jj) * ldgy + c);
+  }
+  // Z (NB x trailing columns) in global, ld N; CTA p writes its column slice.
+  __device__ double* z_slice(int64_t c_lo) const { return z + c_lo; }
+  __device__ int64_t z_ld() const { return N; }
+  __device__ void load_z(int64_t c, int64_t, int kb, double* zc) const {
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj) zc[jj] = (jj < kb) ? ldcg(z + jj * N + c) : 0.0;
+  }
+  __device__ void sync() const { grid_barrier(bar); }
+};
+
+// Exchange through distributed shared memory inside one cluster.
+struct XCluster {
+  double* rec;  // local smem, 2 x REC
+  double* gy;   // local smem, NB x ldgy
+  double* z;    // local smem, NB x zld: this CTA's column slice of Z
+  int P, p;
+  int64_t ldgy, N, zld;
+  __device__ double* rec_w(int buf) const { return rec + buf * REC; }
+  __device__ double rec_r(int buf, int q, int i) const {
+    const double* r = cg::this_cluster().map_shared_rank(rec, q);
+    return r[buf * REC + i];
+  }
+  __device__ double* gy_w() const { return gy; }
+  __device__ double gy_r(int q, int jj, int64_t c) const {
+    const double* g = cg::this_cluster().map_shared_rank(gy, q);
+    return g[jj * ldgy + c];
+  }
+  __device__ double* z_slice(int64_t) const { return z; }
+  __device__ int64_t z_ld() const { return zld; }
+  // column c (trailing-relative) of Z from the CTA whose slice holds it
+  __device__ void load_z(int64_t c, int64_t Nt, int kb, double* zc) const {
+    const int q = split_owner(c, P, Nt);
+    const int64_t qlo = split_lo(q, P, Nt);
+    const double* zq = cg::this_cluster().map_shared_rank(z, q);
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj) zc[jj] = (jj < kb) ? zq[jj * zld + (c - qlo)] : 0.0;
+  }
+  __device__ void sync() const { cg::this_cluster().sync(); }
+};
+
+template <class X>
+__device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
+  const int P = x.P, p = x.p, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int64_t d = a.d, n = a.n, ldw = a.ldw, N = a.N;
   double* W = a.W;
-  const int64_t lo = (static_cast<int64_t>(p) * d) / P;
-  const int64_t hi = (static_cast<int64_t>(p + 1) * d) / P;
-  double* Vs = sm;                   // hmax x NB
-  double* Ts = Vs + a.hmax * NB;     // NB x NB
-  double* Gs = Ts + NB * NB;         // NB x NB
-  double* red = Gs + NB * NB;        // 32
-  double* wv = red + 32;             // NB
-  double* Ys = wv + NB;              // NB x YCH
-  __shared__ double s_tau[NB];
+  const int64_t lo = split_lo(p, P, d), hi = split_lo(p + 1, P, d);
+  const int64_t h = hi - lo;
+  double* Ps = sm;                 // hmax x PSL: own rows of the current panel
+  double* Ts = Ps + a.hmax * PSL;  // NB x NB
+  double* Gs = Ts + NB * NB;      // NB x NB (also row j of the panel)
+  double* wv = Gs + NB * NB;      // NB
+  double* betas = wv + NB;        // n, identical on every CTA
+  double* taus = betas + n;       // NB, current panel
+  double* ysl = taus + NB;        // NB x 64 staging of Y
+  __shared__ double s_coef[2];
 
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(min(static_cast<int64_t>(NB), n - k0));
-    // ---------------- panel: unblocked Householder (dgeqr2) ----------------
-    for (int jj = 0; jj < kb; ++jj) {
-      const int64_t j = k0 + jj;
-      const int64_t rs = max(lo, j + 1);
-      double ss = 0.0;
-      for (int64_t r = rs + tid; r < hi; r += QR_THREADS) {
-        const double v = W[r * ldw + j];
-        ss += v * v;
-      }
-      ss = block_sum(ss, red);
-      // part1 is double-buffered by column parity: without a barrier between
-      // B(j) and A(j+1) (tau == 0), a fast CTA must not overwrite the slot a
-      // slow CTA is still summing.
-      double* part1 = a.part1 + (j & 1) * P;
-      if (tid == 0) part1[p] = ss;
-      grid_barrier(a.bar);
-      double t = 0.0;
-      for (int q = tid; q < P; q += QR_THREADS) t += ldcg(part1 + q);
-      const double xn2 = block_sum(t, red);
-      const double alpha = ldcg(W + j * ldw + j);
-      double beta, tau, scal;
-      if (xn2 == 0.0) {  // dlarfg: H = I
-        tau = 0.0;
-        beta = alpha;
-        scal = 1.0;
-      } else {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      if (tid == 0) s_tau[jj] = tau;
-      if (tid == 0 && p == 0) {
-        a.betas[j] = beta;
-        a.taus[j] = tau;
-      }
-      if (xn2 != 0.0)
-        for (int64_t r = rs + tid; r < hi; r += QR_THREADS) W[r * ldw + j] *= scal;
-      __syncthreads();
-      const int ncp = static_cast<int>(k0 + kb - j - 1);
-      if (ncp > 0 && tau != 0.0) {
-        const int64_t r0 = max(lo, j);
-        for (int cc = warp; cc < ncp; cc += nwarp) {
-          const int64_t c = j + 1 + cc;
-          double acc = 0.0;
-          for (int64_t r = r0 + lane; r < hi; r += 32) {
-            const double v = (r == j) ? 1.0 : W[r * ldw + j];
-            acc += v * W[r * ldw + c];
-          }
-          acc = warp_sum(acc);
-          if (lane == 0) a.part2[static_cast<int64_t>(p) * NB + cc] = acc;
-        }
-        grid_barrier(a.bar);
-        for (int cc = warp; cc < ncp; cc += nwarp) {
-          double s = 0.0;
-          for (int q = lane; q < P; q += 32) s += ldcg(a.part2 + static_cast<int64_t>(q) * NB + cc);
-          s = warp_sum(s);
-          if (lane == 0) wv[cc] = s;
-        }
-        __syncthreads();
-        const int64_t nr = hi > r0 ? hi - r0 : 0;
-        for (int64_t idx = tid; idx < nr * ncp; idx += QR_THREADS) {
-          const int64_t r = r0 + idx / ncp;
-          const int cc = static_cast<int>(idx % ncp);
-          const double v = (r == j) ? 1.0 : W[r * ldw + j];
-          const double temp = -tau * wv[cc];
-          W[r * ldw + j + 1 + cc] += v * temp;
-        }
-      }
-      // W[j][j] keeps alpha (other CTAs may still be reading it when there is
-      // no barrier after B); R's diagonal comes from betas[] at the end.
-      __syncthreads();
-    }
-    // ---------------- trailing update: W -= V T' V' W (dlarft + dlarfb) ------
-    const int64_t ct0 = k0 + kb;
-    const int64_t Nt = N - ct0;
-    if (Nt <= 0) continue;
-    const int64_t rlo = max(lo, k0);
-    const int64_t hv = hi > rlo ? hi - rlo : 0;
-    for (int64_t idx = tid; idx < hv * NB; idx += QR_THREADS) {
-      const int64_t rr = idx / NB;
-      const int jj = static_cast<int>(idx % NB);
-      const int64_t r = rlo + rr;
-      double v = 0.0;
-      if (jj < kb) v = (r < k0 + jj) ? 0.0 : (r == k0 + jj ? 1.0 : W[r * ldw + k0 + jj]);
-      Vs[idx] = v;
+    for (int idx = tid; idx < static_cast<int>(h) * NB; idx += QR_THREADS) {
+      const int rr = idx / NB, c = idx % NB;
+      const int64_t r = lo + rr;
+      Ps[rr * PSL + c] = (c < kb && r >= k0) ? W[r * ldw + k0 + c] : 0.0;
     }
     __syncthreads();
-    // partial [G | Y] = V_own' [V_own | W_own(:, ct0:)]
-    const int64_t ncols3 = kb + Nt;
-    for (int64_t cidx = tid; cidx < ncols3; cidx += QR_THREADS) {
+    // ---------------- panel: dgeqr2 with one exchange per column ----------------
+    for (int jj = 0; jj < kb; ++jj) {
+      const int64_t j = k0 + jj;
+      const int buf = static_cast<int>(j & 1);  // records double-buffered by parity
+      const int owner = split_owner(j, P, d);
+      double* rec = x.rec_w(buf);
+      const int ncol = kb - jj;
+      const int64_t rs = max(lo, j + 1);
+      for (int cc = warp; cc < ncol; cc += QR_WARPS) {
+        double s = 0.0;
+        for (int64_t r = rs + lane; r < hi; r += 32)
+          s += Ps[(r - lo) * PSL + jj] * Ps[(r - lo) * PSL + jj + cc];
+        s = warp_sum(s);
+        if (lane == 0) rec[cc] = s;
+      }
+      if (p == owner)
+        for (int cc = tid; cc < ncol; cc += QR_THREADS) rec[NB + cc] = Ps[(j - lo) * PSL + jj + cc];
+      x.sync();
+      for (int cc = warp; cc < ncol; cc += QR_WARPS) {
+        double s = 0.0;
+        for (int q = lane; q < P; q += 32) s += x.rec_r(buf, q, cc);
+        s = warp_sum(s);
+        if (lane == 0) wv[cc] = s;
+      }
+      if (tid < ncol) Gs[tid] = x.rec_r(buf, owner, NB + tid);
+      __syncthreads();
+      if (tid == 0) {
+        const double xn2 = wv[0];
+        const double alpha = Gs[0];
+        double beta, tau, scal;
+        if (xn2 == 0.0) {  // dlarfg: H = I
+          tau = 0.0;
+          beta = alpha;
+          scal = 1.0;
+        } else {
+          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        s_coef[0] = tau;
+        s_coef[1] = scal;
+        betas[j] = beta;
+        taus[jj] = tau;
+      }
+      __syncthreads();
+      const double tau = s_coef[0], scal = s_coef[1];
+      // temp_c = -tau * v'a_c,  v'a_c = a_jc + scal * sum_{r>j} x_r a_rc
+      if (tid > 0 && tid < ncol) wv[tid] = -tau * (Gs[tid] + scal * wv[tid]);
+      __syncthreads();
+      if (tau != 0.0) {
+        const int64_t rj = max(lo, j);
+        const int nupd = static_cast<int>(hi - rj) * ncol;
+        for (int idx = tid; idx < nupd; idx += QR_THREADS) {
+          const int rr = idx / ncol, cc = idx - rr * ncol;
+          if (cc == 0) continue;
+          const int64_t r = rj + rr;
+          double* row = Ps + (r - lo) * PSL;
+          if (r == j) row[jj + cc] += wv[cc];
+          else row[jj + cc] += (row[jj] * scal) * wv[cc];
+        }
+        __syncthreads();
+        for (int64_t r = rs + tid; r < hi; r += QR_THREADS) Ps[(r - lo) * PSL + jj] *= scal;
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < static_cast<int>(h) * NB; idx += QR_THREADS) {
+      const int rr = idx / NB, c = idx % NB;
+      const int64_t r = lo + rr;
+      if (c < kb && r >= k0) W[r * ldw + k0 + c] = Ps[rr * PSL + c];
+    }
+    // ---------------- trailing update: W -= V T' (V'W)  (dlarft + dlarfb) -----------
+    const int64_t ct0 = k0 + kb;
+    const int64_t Nt = N - ct0;
+    if (Nt <= 0) {
+      __syncthreads();
+      continue;
+    }
+    for (int idx = tid; idx < static_cast<int>(h) * NB; idx += QR_THREADS) {
+      const int rr = idx / NB, c = idx % NB;
+      const int64_t r = lo + rr;
+      if (c >= kb || r < k0 + c) Ps[rr * PSL + c] = 0.0;
+      else if (r == k0 + c) Ps[rr * PSL + c] = 1.0;
+    }
+    __syncthreads();
+    const int64_t r0 = max(lo, k0);
+    const int64_t hv = hi > r0 ? hi - r0 : 0;
+    const double* V = Ps + (r0 - lo) * PSL;
+    double* gyw = x.gy_w();
+    for (int64_t c = tid; c < kb + Nt; c += QR_THREADS) {
       double acc[NB];
 #pragma unroll
       for (int jj = 0; jj < NB; ++jj) acc[jj] = 0.0;
       for (int64_t rr = 0; rr < hv; ++rr) {
-        const double x = (cidx < kb) ? Vs[rr * NB + cidx] : W[(rlo + rr) * ldw + ct0 + cidx - kb];
-        const double* vrow = Vs + rr * NB;
+        const double xv = (c < kb) ? V[rr * PSL + c] : W[(r0 + rr) * ldw + ct0 + c - kb];
+        const double* vrow = V + rr * PSL;
 #pragma unroll
-        for (int jj = 0; jj < NB; ++jj) acc[jj] = fma(vrow[jj], x, acc[jj]);
+        for (int jj = 0; jj < NB; ++jj) acc[jj] = fma(vrow[jj], xv, acc[jj]);
       }
-      double* dst = a.part3 + static_cast<int64_t>(p) * NB * a.ld3 + cidx;
 #pragma unroll
       for (int jj = 0; jj < NB; ++jj)
-        if (jj < kb) dst[jj * a.ld3] = acc[jj];
+        if (jj < kb) gyw[jj * x.ldgy + c] = acc[jj];
     }
-    grid_barrier(a.bar);
-    // every CTA: G (fixed order) and T
+    x.sync();
     for (int idx = tid; idx < kb * kb; idx += QR_THREADS) {
       const int jj = idx / kb, kk = idx % kb;
       double s = 0.0;
-      for (int q = 0; q < P; ++q) s += ldcg(a.part3 + (static_cast<int64_t>(q) * NB + jj) * a.ld3 + kk);
+      for (int q = 0; q < P; ++q) s += x.gy_r(q, jj, kk);
       Gs[jj * NB + kk] = s;
     }
     __syncthreads();
-    if (warp == 0) {  // dlarft, forward / columnwise, lane k owns row k of T
+    if (warp == 0) {  // dlarft (forward, columnwise); lane k owns row k of T
       for (int i = 0; i < kb; ++i) {
-        const double ti = s_tau[i];
-        double g = (lane < i) ? -ti * Gs[lane * NB + i] : 0.0;
-        // T(0:i, i) = T(0:i, 0:i) * g   (upper triangular T)
+        const double ti = taus[i];
+        const double g = (lane < i) ? -ti * Gs[lane * NB + i] : 0.0;
         double acc = 0.0;
         for (int l = 0; l < i; ++l) {
           const double gl = __shfl_sync(FULL, g, l);
@@ -184,103 +271,144 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr(QrArgs a) {
         }
         if (lane < i) Ts[lane * NB + i] = (ti == 0.0) ? 0.0 : acc;
         if (lane == i) Ts[i * NB + i] = ti;
-        if (lane > i && lane < NB) Ts[lane * NB + i] = 0.0;
+        if (lane > i) Ts[lane * NB + i] = 0.0;
         __syncwarp();
       }
     }
     __syncthreads();
-    // Y slice of this CTA -> Z = T' Y  (global, NB x N)
-    const int64_t c_lo = (static_cast<int64_t>(p) * Nt) / P;
-    const int64_t c_hi = (static_cast<int64_t>(p + 1) * Nt) / P;
-    for (int64_t cb = c_lo; cb < c_hi; cb += YCH) {
-      const int w = static_cast<int>(min(static_cast<int64_t>(YCH), c_hi - cb));
+    const int64_t c_lo = split_lo(p, P, Nt), c_hi = split_lo(p + 1, P, Nt);
+    double* zw = x.z_slice(c_lo);
+    const int64_t zld = x.z_ld();
+    for (int64_t cb = c_lo; cb < c_hi; cb += 64) {
+      const int w = static_cast<int>(min(static_cast<int64_t>(64), c_hi - cb));
       for (int idx = tid; idx < kb * w; idx += QR_THREADS) {
         const int jj = idx / w, cc = idx % w;
         double s = 0.0;
-        for (int q = 0; q < P; ++q)
-          s += ldcg(a.part3 + (static_cast<int64_t>(q) * NB + jj) * a.ld3 + kb + cb + cc);
-        Ys[jj * YCH + cc] = s;
+        for (int q = 0; q < P; ++q) s += x.gy_r(q, jj, kb + cb + cc);
+        ysl[jj * 64 + cc] = s;
       }
       __syncthreads();
       for (int idx = tid; idx < kb * w; idx += QR_THREADS) {
         const int jj = idx / w, cc = idx % w;
         double s = 0.0;
-        for (int kk = 0; kk <= jj; ++kk) s += Ts[kk * NB + jj] * Ys[kk * YCH + cc];
-        a.Zg[jj * N + cb + cc] = s;
+        for (int kk = 0; kk <= jj; ++kk) s += Ts[kk * NB + jj] * ysl[kk * 64 + cc];
+        zw[jj * zld + (cb - c_lo) + cc] = s;
       }
       __syncthreads();
     }
-    grid_barrier(a.bar);
+    x.sync();
     for (int64_t c = tid; c < Nt; c += QR_THREADS) {
       double zc[NB];
-#pragma unroll
-      for (int jj = 0; jj < NB; ++jj) zc[jj] = (jj < kb) ? ldcg(a.Zg + jj * N + c) : 0.0;
+      x.load_z(c, Nt, kb, zc);
       for (int64_t rr = 0; rr < hv; ++rr) {
-        double* wp = W + (rlo + rr) * ldw + ct0 + c;
+        double* wp = W + (r0 + rr) * ldw + ct0 + c;
         double acc = *wp;
-        const double* vrow = Vs + rr * NB;
+        const double* vrow = V + rr * PSL;
 #pragma unroll
         for (int jj = 0; jj < NB; ++jj) acc = fma(-vrow[jj], zc[jj], acc);
         *wp = acc;
       }
     }
-    // The next panel's first grid barrier orders these writes before any
-    // cross-CTA read; own-row reads only need the CTA barrier.
     __syncthreads();
   }
-  grid_barrier(a.bar);
-  // R = sign-fixed upper triangle, z = sign-fixed Q'Sb (linalg.py:43-46)
-  const int64_t gtid = static_cast<int64_t>(p) * QR_THREADS + tid;
-  const int64_t gstride = static_cast<int64_t>(P) * QR_THREADS;
-  for (int64_t idx = gtid; idx < n * n; idx += gstride) {
-    const int64_t i = idx / n, c = idx % n;
-    const double bi = ldcg(a.betas + i);
+  // R (sign-fixed upper triangle) and z = sign-fixed Q'Sb for own rows < n
+  // (linalg.py:43-46); every value read here was written by this CTA.
+  const int64_t ihi = min(hi, n);
+  for (int64_t idx = tid; idx < (ihi > lo ? ihi - lo : 0) * n; idx += QR_THREADS) {
+    const int64_t i = lo + idx / n, c = idx % n;
+    const double bi = betas[i];
     const double sg = bi < 0.0 ? -1.0 : 1.0;
-    a.R[idx] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * ldcg(W + i * ldw + c));
+    a.R[i * n + c] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
   }
-  for (int64_t i = gtid; i < n; i += gstride) {
-    const double bi = ldcg(a.betas + i);
+  for (int64_t i = lo + tid; i < ihi; i += QR_THREADS) {
+    const double bi = betas[i];
     const double sg = bi < 0.0 ? -1.0 : 1.0;
-    if (a.z && N > n) a.z[i] = sg * ldcg(W + i * ldw + n);
-    if (bi == 0.0) atomicOr(a.singular, 1);
+    if (a.z && N > n) a.z[i] = sg * W[i * ldw + n];
   }
+  if (p == 0)
+    for (int64_t i = tid; i < n; i += QR_THREADS)
+      if (betas[i] == 0.0) atomicOr(a.singular, 1);
 }
 
-struct QrLayout {
+__global__ void __launch_bounds__(QR_THREADS) k_qr_grid(QrArgs a) {
+  extern __shared__ double sm[];
+  XGrid x;
+  x.rec = a.grec;
+  x.gy = a.ggy;
+  x.z = a.gz;
+  x.bar = a.bar;
+  x.P = gridDim.x;
+  x.p = blockIdx.x;
+  x.ldgy = NB + a.N;
+  x.N = a.N;
+  qr_body(a, x, sm);
+}
+
+__host__ __device__ size_t common_doubles(int64_t hmax, int64_t n) {
+  return static_cast<size_t>(hmax * PSL + 2 * NB * NB + NB + n + NB + NB * 64);
+}
+
+__global__ void __launch_bounds__(QR_THREADS) k_qr_cluster(QrArgs a) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  XCluster x;
+  x.P = static_cast<int>(cl.num_blocks());
+  x.p = static_cast<int>(cl.block_rank());
+  x.ldgy = NB + a.N;
+  x.N = a.N;
+  x.zld = (a.N + x.P - 1) / x.P + 1;
+  x.rec = sm + common_doubles(a.hmax, a.n);
+  x.gy = x.rec + 2 * REC;
+  x.z = x.gy + NB * x.ldgy;
+  cl.sync();
+  qr_body(a, x, sm);
+  cl.sync();  // keep shared memory alive until every CTA finished reading it
+}
+
+struct QrPlan {
+  bool cluster;
   int P;
-  int64_t hmax, ld3;
+  int64_t hmax;
   size_t smem;
-  int64_t bytes;
+  int64_t ws_bytes;
   unsigned* bar;
   int* singular;
-  double *part1, *part2, *part3, *Zg, *betas, *taus;
+  double *grec, *ggy, *gz;
 };
 
-int qr_grid(int64_t d) {
-  const int sms = num_sms();
-  int64_t P = (d + 15) / 16;  // >= 16 rows per CTA
-  if (P > sms) P = sms;
-  if (P < 1) P = 1;
-  return static_cast<int>(P);
-}
+constexpr size_t QR_SMEM_MAX = 220 * 1024;
 
-QrLayout qr_layout(void* ws, int64_t d, int64_t n, int has_rhs) {
-  QrLayout L;
-  L.P = qr_grid(d);
+QrPlan qr_plan(void* ws, int64_t d, int64_t n, int has_rhs) {
+  QrPlan L;
   const int64_t N = n + (has_rhs ? 1 : 0);
-  L.hmax = (d + L.P - 1) / L.P + 1;
-  L.ld3 = NB + N;
-  L.smem = static_cast<size_t>(L.hmax * NB + 2 * NB * NB + 32 + NB + NB * YCH) * sizeof(double);
+  // cluster mode: <= 16 CTAs (non-portable cluster limit); panel rows and the
+  // exchange buffers in shared memory
+  const int C = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (d + 63) / 64)));
+  const int64_t hmax_c = (d + C - 1) / C + 1;
+  const int64_t zld = (N + C - 1) / C + 1;
+  const size_t smem_cl = (common_doubles(hmax_c, n) + 2 * REC + NB * (NB + N) + NB * zld) * 8;
+  L.cluster = smem_cl <= QR_SMEM_MAX;
+  if (L.cluster) {
+    L.P = C;
+    L.hmax = hmax_c;
+    L.smem = smem_cl;
+  } else {
+    const int64_t P = std::min<int64_t>(num_sms(), std::max<int64_t>(1, (d + 31) / 32));
+    L.P = static_cast<int>(P);
+    L.hmax = (d + P - 1) / P + 1;
+    L.smem = common_doubles(L.hmax, n) * 8;
+  }
   Carver cv(ws, 1ll << 62);
   L.bar = cv.take<unsigned>(64);
   L.singular = cv.take<int>(64);
-  L.part1 = cv.take<double>(2 * L.P);
-  L.part2 = cv.take<double>(static_cast<int64_t>(L.P) * NB);
-  L.part3 = cv.take<double>(static_cast<int64_t>(L.P) * NB * L.ld3);
-  L.Zg = cv.take<double>(NB * N);
-  L.betas = cv.take<double>(n);
-  L.taus = cv.take<double>(n);
-  L.bytes = cv.off + 256;
+  if (L.cluster) {
+    L.grec = L.ggy = L.gz = nullptr;
+  } else {
+    L.grec = cv.take<double>(2ll * L.P * REC);
+    L.ggy = cv.take<double>(static_cast<int64_t>(L.P) * NB * (NB + N));
+    L.gz = cv.take<double>(NB * N);
+  }
+  L.ws_bytes = cv.off + 256;
   return L;
 }
 
@@ -291,7 +419,7 @@ using namespace itsk;
 
 extern "C" int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes) {
   ITSK_REQUIRE(bytes && d >= n && n >= 1, "need d >= n >= 1");
-  *bytes = qr_layout(nullptr, d, n, 1).bytes;
+  *bytes = std::max(qr_plan(nullptr, d, n, 1).ws_bytes, qr_plan(nullptr, d, n, 0).ws_bytes);
   return ITSK_OK;
 }
 
@@ -301,10 +429,11 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   ITSK_REQUIRE(n >= 1 && d >= n, "need m >= n, got %lld x %lld", (long long)d, (long long)n);
   const int has_rhs = z != nullptr;
   ITSK_REQUIRE(ldw >= n + has_rhs, "bad leading dimension");
-  QrLayout L = qr_layout(ws, d, n, has_rhs);
-  ITSK_REQUIRE(L.bytes <= ws_bytes, "qr workspace too small (%lld < %lld)", (long long)ws_bytes,
-               (long long)L.bytes);
-  ITSK_REQUIRE(L.smem <= 200 * 1024, "qr: too many rows per CTA");
+  QrPlan L = qr_plan(ws, d, n, has_rhs);
+  ITSK_REQUIRE(L.ws_bytes <= ws_bytes, "qr workspace too small (%lld < %lld)", (long long)ws_bytes,
+               (long long)L.ws_bytes);
+  ITSK_REQUIRE(L.smem <= QR_SMEM_MAX, "qr: too many rows per CTA (d=%lld, n=%lld)", (long long)d,
+               (long long)n);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   ITSK_CUDA(cudaMemsetAsync(L.bar, 0, 512, s));
   QrArgs a;
@@ -315,21 +444,38 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   a.N = n + has_rhs;
   a.R = R;
   a.z = z;
-  a.part1 = L.part1;
-  a.part2 = L.part2;
-  a.part3 = L.part3;
-  a.Zg = L.Zg;
-  a.betas = L.betas;
-  a.taus = L.taus;
-  a.bar = L.bar;
   a.singular = L.singular;
+  a.grec = L.grec;
+  a.ggy = L.ggy;
+  a.gz = L.gz;
+  a.bar = L.bar;
   a.hmax = L.hmax;
-  a.ld3 = L.ld3;
-  ITSK_CUDA(cudaFuncSetAttribute(k_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(L.smem)));
-  void* args[] = {&a};
-  ITSK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr), dim3(L.P),
-                                        dim3(QR_THREADS), args, L.smem, s));
+  if (L.cluster) {
+    ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_qr_cluster)));
+    static bool nonportable = false;
+    if (!nonportable) {
+      ITSK_CUDA(cudaFuncSetAttribute(k_qr_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      nonportable = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.P);
+    cfg.blockDim = dim3(QR_THREADS);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = L.P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_qr_cluster, a));
+  } else {
+    ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_qr_grid)));
+    void* args[] = {&a};
+    ITSK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_qr_grid), dim3(L.P),
+                                          dim3(QR_THREADS), args, L.smem, s));
+  }
   count_launch();
   int singular = 0;
   ITSK_CUDA(cudaMemcpyAsync(&singular, L.singular, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -24,26 +24,51 @@ namespace itsk {
 
 namespace {
 
-__global__ void __launch_bounds__(1024) k_trsv(const double* R, int64_t n, const double* c,
+// Accessor selection: PACKED stages the upper triangle in shared memory first.
+template <bool PACKED>
+struct RSel;
+template <>
+struct RSel<true> {
+  using type = RPacked;
+  __device__ static RPacked make(const double* R, int64_t n, double*& sm) {
+    stage_packed(R, n, sm);
+    RPacked a{sm, n};
+    sm += packed_doubles(n);
+    return a;
+  }
+};
+template <>
+struct RSel<false> {
+  using type = RGlobal;
+  __device__ static RGlobal make(const double* R, int64_t n, double*&) { return RGlobal{R, n}; }
+};
+
+template <bool PACKED>
+__global__ void __launch_bounds__(DENSE_THREADS) k_trsv(const double* R, int64_t n, const double* c,
                                                double* y, int mode) {
   extern __shared__ double sm[];
-  double* v = sm;
-  double* tmp = sm + n;
+  double* cur = sm;
+  const auto RA = RSel<PACKED>::make(R, n, cur);
+  double* v = cur;
+  double* tmp = cur + n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = c[i];
   __syncthreads();
-  if (mode == 1 || mode == 2) trsv_t_inplace(R, n, v);
-  if (mode == 0 || mode == 2) trsv_n_inplace(R, n, v, tmp);
+  if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v);
+  if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, tmp);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = v[i];
 }
 
 // rand_power_norm_est (linalg.py:96-105)
-__global__ void __launch_bounds__(1024) k_normest(const double* R, int64_t n, const double* v0,
+template <bool PACKED>
+__global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, int64_t n, const double* v0,
                                                   int64_t steps, double* out) {
   extern __shared__ double sm[];
-  double* v = sm;
-  double* t = sm + n;
-  double* w = sm + 2 * n;
-  double* red = sm + 3 * n;
+  double* cur = sm;
+  const auto R = RSel<PACKED>::make(R0, n, cur);
+  double* v = cur;
+  double* t = cur + n;
+  double* w = cur + 2 * n;
+  double* red = cur + 3 * n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = v0[i];
   __syncthreads();
   double nv = sqrt(dot_sm(v, v, n, red));
@@ -95,7 +120,8 @@ constexpr int LANCZOS_MAX = 96;
 
 // Lanczos on op = R'R (inv == 0) or R^{-1}R^{-T} (inv == 1); returns the
 // largest Ritz value, stopping once it is stable to rounding.
-__device__ double lanczos_max(const double* R, int64_t n, const double* v0, int inv, double* q,
+template <class RA>
+__device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv, double* q,
                               double* qp, double* w, double* t, double* red, double* al,
                               double* be) {
   const int tid = threadIdx.x;
@@ -150,14 +176,17 @@ __device__ double lanczos_max(const double* R, int64_t n, const double* v0, int 
   return theta;
 }
 
-__global__ void __launch_bounds__(1024) k_condest(const double* R, int64_t n, const double* v0,
+template <bool PACKED>
+__global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, int64_t n, const double* v0,
                                                   double* out) {
   extern __shared__ double sm[];
-  double* q = sm;
-  double* qp = sm + n;
-  double* w = sm + 2 * n;
-  double* t = sm + 3 * n;
-  double* red = sm + 4 * n;
+  double* cur = sm;
+  const auto R = RSel<PACKED>::make(R0, n, cur);
+  double* q = cur;
+  double* qp = cur + n;
+  double* w = cur + 2 * n;
+  double* t = cur + 3 * n;
+  double* red = cur + 4 * n;
   double* al = red + 32;
   double* be = al + LANCZOS_MAX;
   const double smax2 = lanczos_max(R, n, v0, 0, q, qp, w, t, red, al, be);
@@ -167,16 +196,32 @@ __global__ void __launch_bounds__(1024) k_condest(const double* R, int64_t n, co
 
 }  // namespace
 
-int launch_trsv_pair_device(const double* R, int64_t n, const double* c, double* y,
-                            cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(n + 32) * sizeof(double);
-  if (smem > 48 * 1024)
-    ITSK_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  k_trsv<<<1, 1024, smem, s>>>(R, n, c, y, 2);
+template <class K>
+int prep(K kernel, size_t smem) {
+  if (smem > 48 * 1024) ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(kernel)));
+  return ITSK_OK;
+}
+
+int launch_trsv(const double* R, int64_t n, const double* c, double* y, int mode, cudaStream_t s) {
+  const int64_t other = n + 32;
+  const bool packed = use_packed(n, other);
+  const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
+  int rc;
+  if (packed) {
+    if ((rc = prep(k_trsv<true>, smem))) return rc;
+    k_trsv<true><<<1, DENSE_THREADS, smem, s>>>(R, n, c, y, mode);
+  } else {
+    if ((rc = prep(k_trsv<false>, smem))) return rc;
+    k_trsv<false><<<1, DENSE_THREADS, smem, s>>>(R, n, c, y, mode);
+  }
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
+}
+
+int launch_trsv_pair_device(const double* R, int64_t n, const double* c, double* y,
+                            cudaStream_t s) {
+  return launch_trsv(R, n, c, y, 2, s);
 }
 
 }  // namespace itsk
@@ -187,22 +232,14 @@ extern "C" int itsk_trsv(const double* R, int64_t n, const double* c, double* y,
                          itsk_stream_t stream) {
   ITSK_REQUIRE(R && c && y && n >= 1, "bad trsv arguments");
   ITSK_REQUIRE(n <= 16384, "trsv: n too large for the single-CTA kernel");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t smem = static_cast<size_t>(n + 32) * sizeof(double);
-  if (smem > 48 * 1024)
-    ITSK_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  k_trsv<<<1, 1024, smem, s>>>(R, n, c, y, trans ? 1 : 0);
-  count_launch();
-  ITSK_CHECK_LAUNCH();
-  return ITSK_OK;
+  return launch_trsv(R, n, c, y, trans ? 1 : 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
                               itsk_stream_t stream) {
   (void)tmp;
   ITSK_REQUIRE(R && c && y && n >= 1 && n <= 16384, "bad trsv arguments");
-  return launch_trsv_pair_device(R, n, c, y, reinterpret_cast<cudaStream_t>(stream));
+  return launch_trsv(R, n, c, y, 2, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps,
@@ -211,11 +248,17 @@ extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_
   ITSK_REQUIRE(R && v0 && out && n >= 1 && steps >= 1, "bad normest arguments");
   ITSK_REQUIRE(n <= 8000, "normest: n too large for the single-CTA kernel");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t smem = static_cast<size_t>(3 * n + 32) * sizeof(double);
-  if (smem > 48 * 1024)
-    ITSK_CUDA(cudaFuncSetAttribute(k_normest, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  k_normest<<<1, 1024, smem, s>>>(R, n, v0, steps, out);
+  const int64_t other = 3 * n + 32;
+  const bool packed = use_packed(n, other);
+  const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
+  int rc;
+  if (packed) {
+    if ((rc = prep(k_normest<true>, smem))) return rc;
+    k_normest<true><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, steps, out);
+  } else {
+    if ((rc = prep(k_normest<false>, smem))) return rc;
+    k_normest<false><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, steps, out);
+  }
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
@@ -233,11 +276,17 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
   ITSK_REQUIRE(R && v0 && out && n >= 1, "bad condest arguments");
   ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t smem = static_cast<size_t>(4 * n + 32 + 2 * LANCZOS_MAX) * sizeof(double);
-  if (smem > 48 * 1024)
-    ITSK_CUDA(cudaFuncSetAttribute(k_condest, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  k_condest<<<1, 1024, smem, s>>>(R, n, v0, out);
+  const int64_t other = 4 * n + 32 + 2 * LANCZOS_MAX;
+  const bool packed = use_packed(n, other);
+  const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
+  int rc;
+  if (packed) {
+    if ((rc = prep(k_condest<true>, smem))) return rc;
+    k_condest<true><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, out);
+  } else {
+    if ((rc = prep(k_condest<false>, smem))) return rc;
+    k_condest<false><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, out);
+  }
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
