@@ -112,16 +112,21 @@ int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
 int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
                    itsk_stream_t stream);
 
+/* Packed upper triangle of R (row i holds R[i][i..n)), padded to 16 bytes:
+ * what the single-CTA R kernels bulk-copy into shared memory in one shot. */
+int itsk_pack_upper_doubles(int64_t n, int64_t* doubles);
+int itsk_pack_upper(const double* R, int64_t n, double* Rp, itsk_stream_t stream);
+
 /* rand_power_norm_est (linalg.py:79-105) with the start vector v0 (host
  * numpy default_rng(seed).standard_normal(n)), `steps` power steps; the
- * result is written to *out (device scalar). ws: 3n doubles. */
+ * result is written to *out (device scalar).  Rp: itsk_pack_upper(R) or NULL. */
 int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps, double* out,
-                 double* ws, itsk_stream_t stream);
+                 const double* Rp, itsk_stream_t stream);
 /* cond_est (linalg.py:108-113): sigma_max/sigma_min of R from Lanczos on
- * R'R and on R^{-1}R^{-T}, to rounding for the spectra of this path;
- * *out (device).  ws: itsk_condest_workspace doubles. */
+ * R'R and on R^{-1}R^{-T}, stopped when the extreme Ritz values settle to
+ * 1e-13; *out (device).  Rp: packed R or NULL. */
 int itsk_condest_workspace(int64_t n, int64_t* doubles);
-int itsk_condest(const double* R, int64_t n, const double* v0, double* out, double* ws,
+int itsk_condest(const double* R, int64_t n, const double* v0, double* out, const double* Rp,
                  itsk_stream_t stream);
 
 /* ----------------------------------------------------------------------
@@ -157,6 +162,7 @@ typedef struct itsk_loop_params {
   const double* A;
   const double* b;
   const double* R;          /* n x n, ld n                                   */
+  const double* Rp;         /* itsk_pack_upper(R) or NULL                    */
   const double* x_true;     /* n, nullable                                   */
   const double* r_true;     /* m (local), nullable                           */
   const double* normest;    /* device scalars from itsk_normest/itsk_condest */

@@ -40,7 +40,7 @@ class LoopParams(ctypes.Structure):
         ("u", ctypes.c_double), ("gamma", ctypes.c_double), ("rho", ctypes.c_double),
         ("truth_beta", ctypes.c_double),
         ("has_truth", ctypes.c_int32),
-        ("A", c_dp), ("b", c_dp), ("R", c_dp), ("x_true", c_dp), ("r_true", c_dp),
+        ("A", c_dp), ("b", c_dp), ("R", c_dp), ("Rp", c_dp), ("x_true", c_dp), ("r_true", c_dp),
         ("normest", c_dp), ("condest", c_dp),
         ("xs", c_dp), ("rs", c_dp), ("trace", c_dp), ("cs", c_dp),
         ("ws", c_dp), ("ws_bytes", c_i64),
@@ -72,6 +72,8 @@ _SIGS = {
     "itsk_trsv": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, ctypes.c_int, c_dp]),
     "itsk_trsv_pair": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, c_dp, c_dp]),
     "itsk_normest": (ctypes.c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_dp, c_dp]),
+    "itsk_pack_upper_doubles": (ctypes.c_int, [c_i64, ctypes.POINTER(c_i64)]),
+    "itsk_pack_upper": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp]),
     "itsk_condest_workspace": (ctypes.c_int, [c_i64, ctypes.POINTER(c_i64)]),
     "itsk_condest": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, c_dp, c_dp]),
     "itsk_pass_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),

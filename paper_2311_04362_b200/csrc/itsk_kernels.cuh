@@ -26,6 +26,7 @@ struct LoopPtrs {
   const double* A;
   const double* b;
   const double* R;
+  const double* Rp;  // packed upper triangle or nullptr
   const double* x_true;
   const double* r_true;
   const double* normest;

@@ -62,21 +62,22 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
   double* v;
   double* tmp;
   if (PACKED) {
-    stage_packed(p.R, n, sm);
+    if (p.Rp) stage_packed_bulk(p.Rp, n, sm); else stage_packed(p.R, n, sm);
     v = sm + packed_doubles(n);
   } else {
     v = sm;
   }
   tmp = v + n;
+  __shared__ double red_s[32 * (DENSE_THREADS / 32) + 32];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   __syncthreads();
   if (PACKED) {
-    const RPacked R{sm, n};
-    trsv_t_inplace(R, n, v);
+    const RPacked R(sm, n);
+    trsv_t_inplace(R, n, v, red_s);
     trsv_n_inplace(R, n, v, tmp);
   } else {
     const RGlobal R{p.R, n};
-    trsv_t_inplace(R, n, v);
+    trsv_t_inplace(R, n, v, red_s);
     trsv_n_inplace(R, n, v, tmp);
   }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p.step[i] = v[i];
@@ -247,6 +248,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.A = p->A;
   q.b = p->b;
   q.R = p->R;
+  q.Rp = p->Rp;
   q.x_true = p->x_true;
   q.r_true = p->r_true;
   q.normest = p->normest;

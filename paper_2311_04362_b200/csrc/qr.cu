@@ -27,6 +27,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "itsk_common.cuh"
 
@@ -77,7 +79,11 @@ struct XGrid {
   unsigned* bar;
   int P, p;
   int64_t ldgy, N;
-  __device__ double* rec_w(int buf) const { return rec + (static_cast<int64_t>(buf) * P + p) * REC; }
+  // publish this CTA's record (n entries of `local`) before the exchange sync
+  __device__ void publish(int buf, const double* local, int cnt) const {
+    double* dst = rec + (static_cast<int64_t>(buf) * P + p) * REC;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = local[i];
+  }
   __device__ double rec_r(int buf, int q, int i) const {
     return ldcg(rec + (static_cast<int64_t>(buf) * P + q) * REC + i);
   }
@@ -88,25 +94,27 @@ struct XGrid {
   // Z (NB x trailing columns) in global, ld N; CTA p writes its column slice.
   __device__ double* z_slice(int64_t c_lo) const { return z + c_lo; }
   __device__ int64_t z_ld() const { return N; }
-  __device__ void load_z(int64_t c, int64_t, int kb, double* zc) const {
-#pragma unroll
-    for (int jj = 0; jj < NB; ++jj) zc[jj] = (jj < kb) ? ldcg(z + jj * N + c) : 0.0;
-  }
+  __device__ double z_at(int jj, int64_t c, int64_t) const { return ldcg(z + jj * N + c); }
   __device__ void sync() const { grid_barrier(bar); }
 };
 
 // Exchange through distributed shared memory inside one cluster.
 struct XCluster {
-  double* rec;  // local smem, 2 x REC
+  double* rec;  // local smem inbox, 2 x P x REC: every CTA pushes its record here
   double* gy;   // local smem, NB x ldgy
   double* z;    // local smem, NB x zld: this CTA's column slice of Z
   int P, p;
   int64_t ldgy, N, zld;
-  __device__ double* rec_w(int buf) const { return rec + buf * REC; }
-  __device__ double rec_r(int buf, int q, int i) const {
-    const double* r = cg::this_cluster().map_shared_rank(rec, q);
-    return r[buf * REC + i];
+  // push model: remote stores into every CTA's inbox before the barrier, so
+  // the reads after it are local (remote loads would sit on the critical path)
+  __device__ void publish(int buf, const double* local, int cnt) const {
+    cg::cluster_group cl = cg::this_cluster();
+    for (int e = threadIdx.x; e < P * cnt; e += blockDim.x) {
+      const int q = e / cnt, i = e - q * cnt;
+      cl.map_shared_rank(rec, q)[(buf * P + p) * REC + i] = local[i];
+    }
   }
+  __device__ double rec_r(int buf, int q, int i) const { return rec[(buf * P + q) * REC + i]; }
   __device__ double* gy_w() const { return gy; }
   __device__ double gy_r(int q, int jj, int64_t c) const {
     const double* g = cg::this_cluster().map_shared_rank(gy, q);
@@ -114,33 +122,59 @@ struct XCluster {
   }
   __device__ double* z_slice(int64_t) const { return z; }
   __device__ int64_t z_ld() const { return zld; }
-  // column c (trailing-relative) of Z from the CTA whose slice holds it
-  __device__ void load_z(int64_t c, int64_t Nt, int kb, double* zc) const {
+  // Z[jj][c] (c trailing-relative) from the CTA whose slice holds column c
+  __device__ double z_at(int jj, int64_t c, int64_t Nt) const {
     const int q = split_owner(c, P, Nt);
     const int64_t qlo = split_lo(q, P, Nt);
     const double* zq = cg::this_cluster().map_shared_rank(z, q);
-#pragma unroll
-    for (int jj = 0; jj < NB; ++jj) zc[jj] = (jj < kb) ? zq[jj * zld + (c - qlo)] : 0.0;
+    return zq[jj * zld + (c - qlo)];
   }
   __device__ void sync() const { cg::this_cluster().sync(); }
 };
 
+// fp64 tensor-core tile: D(8x8) += A(8x4) * B(4x8)  (DMMA.8x8x4 on sm_100a).
+// Fragments (PTX m8n8k4 .f64): a = A[g][t], b = B[t][g], d = D[g][2t + {0,1}],
+// with g = lane / 4 and t = lane % 4.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int RT = 32;        // row tile of the trailing update
+constexpr int CB = 64;        // column chunk of the trailing update
+constexpr int CBP = CB + 4;   // padded stride of the staged tiles
+
+#ifdef ITSK_QR_PROFILE
+__device__ unsigned long long g_qr_prof[16];
+#define QPROF(i) do { __syncthreads(); if (threadIdx.x == 0 && x.p == 0) { long long _t = clock64(); _qacc[i] += _t - _qt; _qt = _t; } } while (0)
+#else
+#define QPROF(i) do { } while (0)
+#endif
+
 template <class X>
 __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
+#ifdef ITSK_QR_PROFILE
+  long long _qt = clock64();
+  long long _qacc[12] = {0};
+#endif
   const int P = x.P, p = x.p, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
   const int64_t d = a.d, n = a.n, ldw = a.ldw, N = a.N;
   double* W = a.W;
   const int64_t lo = split_lo(p, P, d), hi = split_lo(p + 1, P, d);
   const int64_t h = hi - lo;
   double* Ps = sm;                 // hmax x PSL: own rows of the current panel
   double* Ts = Ps + a.hmax * PSL;  // NB x NB
-  double* Gs = Ts + NB * NB;      // NB x NB (also row j of the panel)
-  double* wv = Gs + NB * NB;      // NB
-  double* betas = wv + NB;        // n, identical on every CTA
-  double* taus = betas + n;       // NB, current panel
-  double* ysl = taus + NB;        // NB x 64 staging of Y
+  double* Gs = Ts + NB * NB;       // NB x NB (also row j of the panel)
+  double* wv = Gs + NB * NB;       // NB
+  double* betas = wv + NB;         // n, identical on every CTA
+  double* taus = betas + n;        // NB, current panel
+  double* tile = taus + NB;        // RT x CBP: staged W tile / Y staging
+  double* Zs = tile + RT * CBP;    // NB x CBP: staged Z chunk
   __shared__ double s_coef[2];
+  int owner = 0;  // owner CTA of row j, advanced monotonically
 
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int kb = static_cast<int>(min(static_cast<int64_t>(NB), n - k0));
@@ -154,66 +188,91 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
     for (int jj = 0; jj < kb; ++jj) {
       const int64_t j = k0 + jj;
       const int buf = static_cast<int>(j & 1);  // records double-buffered by parity
-      const int owner = split_owner(j, P, d);
-      double* rec = x.rec_w(buf);
+      while (owner + 1 < P && split_lo(owner + 1, P, d) <= j) ++owner;
+      double* rec = Gs + 128;  // local staging of this CTA's record
       const int ncol = kb - jj;
       const int64_t rs = max(lo, j + 1);
-      for (int cc = warp; cc < ncol; cc += QR_WARPS) {
-        double s = 0.0;
-        for (int64_t r = rs + lane; r < hi; r += 32)
-          s += Ps[(r - lo) * PSL + jj] * Ps[(r - lo) * PSL + jj + cc];
-        s = warp_sum(s);
-        if (lane == 0) rec[cc] = s;
+      const int c0 = warp, c1 = warp + QR_WARPS;  // each warp: two panel columns
+      QPROF(0);
+      if (c0 < ncol) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int64_t r = rs + lane; r < hi; r += 32) {
+          const double* row = Ps + (r - lo) * PSL + jj;
+          const double xr = row[0];
+          s0 = fma(xr, row[c0], s0);
+          if (c1 < ncol) s1 = fma(xr, row[c1], s1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(FULL, s0, o);
+          s1 += __shfl_xor_sync(FULL, s1, o);
+        }
+        if (lane == 0) {
+          rec[c0] = s0;
+          if (c1 < ncol) rec[c1] = s1;
+        }
       }
       if (p == owner)
         for (int cc = tid; cc < ncol; cc += QR_THREADS) rec[NB + cc] = Ps[(j - lo) * PSL + jj + cc];
-      x.sync();
-      for (int cc = warp; cc < ncol; cc += QR_WARPS) {
-        double s = 0.0;
-        for (int q = lane; q < P; q += 32) s += x.rec_r(buf, q, cc);
-        s = warp_sum(s);
-        if (lane == 0) wv[cc] = s;
-      }
-      if (tid < ncol) Gs[tid] = x.rec_r(buf, owner, NB + tid);
       __syncthreads();
-      if (tid == 0) {
-        const double xn2 = wv[0];
-        const double alpha = Gs[0];
-        double beta, tau, scal;
-        if (xn2 == 0.0) {  // dlarfg: H = I
-          tau = 0.0;
-          beta = alpha;
-          scal = 1.0;
-        } else {
-          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
+      x.publish(buf, rec, p == owner ? REC : ncol);
+      QPROF(1);
+      x.sync();
+      QPROF(2);
+      if (tid >= QR_THREADS - 32 && tid - (QR_THREADS - 32) < ncol)
+        Gs[tid - (QR_THREADS - 32)] = x.rec_r(buf, owner, NB + tid - (QR_THREADS - 32));
+      if (c0 < ncol) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int q = lane; q < P; q += 32) {
+          s0 += x.rec_r(buf, q, c0);
+          if (c1 < ncol) s1 += x.rec_r(buf, q, c1);
         }
-        s_coef[0] = tau;
-        s_coef[1] = scal;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(FULL, s0, o);
+          s1 += __shfl_xor_sync(FULL, s1, o);
+        }
+        if (lane == 0) {
+          wv[c0] = s0;
+          if (c1 < ncol) wv[c1] = s1;
+        }
+      }
+      __syncthreads();
+      QPROF(3);
+      // every thread forms the same dlarfg coefficients (no broadcast needed)
+      const double xn2 = wv[0];
+      const double alpha = Gs[0];
+      double beta, tau, scal;
+      if (xn2 == 0.0) {  // dlarfg: H = I
+        tau = 0.0;
+        beta = alpha;
+        scal = 1.0;
+      } else {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (tid == 0) {
         betas[j] = beta;
         taus[jj] = tau;
       }
-      __syncthreads();
-      const double tau = s_coef[0], scal = s_coef[1];
-      // temp_c = -tau * v'a_c,  v'a_c = a_jc + scal * sum_{r>j} x_r a_rc
-      if (tid > 0 && tid < ncol) wv[tid] = -tau * (Gs[tid] + scal * wv[tid]);
-      __syncthreads();
+      QPROF(4);
       if (tau != 0.0) {
-        const int64_t rj = max(lo, j);
-        const int nupd = static_cast<int>(hi - rj) * ncol;
-        for (int idx = tid; idx < nupd; idx += QR_THREADS) {
-          const int rr = idx / ncol, cc = idx - rr * ncol;
-          if (cc == 0) continue;
-          const int64_t r = rj + rr;
-          double* row = Ps + (r - lo) * PSL;
-          if (r == j) row[jj + cc] += wv[cc];
-          else row[jj + cc] += (row[jj] * scal) * wv[cc];
+        // warp per row, lane per panel column: a_rc += v_r * temp_c with
+        // temp_c = -tau * (a_jc + scal * sum_{r>j} x_r a_rc), v_r = scal * x_r, v_j = 1
+        const int cc = lane;
+        const double temp = (cc > 0 && cc < ncol) ? -tau * (Gs[cc] + scal * wv[cc]) : 0.0;
+        for (int64_t r = max(lo, j) + warp; r < hi; r += QR_WARPS) {
+          double* row = Ps + (r - lo) * PSL + jj;
+          const double xr = row[0];
+          const double vr = (r == j) ? 1.0 : xr * scal;
+          if (cc > 0 && cc < ncol) row[cc] += vr * temp;
+          __syncwarp();
+          if (lane == 0 && r != j) row[0] = vr;
         }
-        __syncthreads();
-        for (int64_t r = rs + tid; r < hi; r += QR_THREADS) Ps[(r - lo) * PSL + jj] *= scal;
       }
       __syncthreads();
+      QPROF(5);
     }
     for (int idx = tid; idx < static_cast<int>(h) * NB; idx += QR_THREADS) {
       const int rr = idx / NB, c = idx % NB;
@@ -235,24 +294,55 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
     }
     __syncthreads();
     const int64_t r0 = max(lo, k0);
-    const int64_t hv = hi > r0 ? hi - r0 : 0;
+    const int hv = hi > r0 ? static_cast<int>(hi - r0) : 0;
     const double* V = Ps + (r0 - lo) * PSL;
+    QPROF(6);
+    // (1) partial [G | Y] = V_own' [V_own | W_own(:, ct0:)] on DMMA tiles:
+    //     M = 32 (reflectors), N = CB columns per chunk, K = own rows.
     double* gyw = x.gy_w();
-    for (int64_t c = tid; c < kb + Nt; c += QR_THREADS) {
-      double acc[NB];
+    const int ncols3 = kb + static_cast<int>(Nt);
+    for (int cb = 0; cb < ncols3; cb += CB) {
+      const int cw = min(CB, ncols3 - cb);
+      double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+      for (int rt = 0; rt < hv; rt += RT) {
+        const int rh = min(RT, hv - rt);
+        __syncthreads();
+        for (int idx = tid; idx < RT * CB; idx += QR_THREADS) {
+          const int rr = idx / CB, c = idx % CB, cg_ = cb + c;
+          double v = 0.0;
+          if (rr < rh && c < cw)
+            v = (cg_ < kb) ? V[(rt + rr) * PSL + cg_] : W[(r0 + rt + rr) * ldw + ct0 + cg_ - kb];
+          tile[rr * CBP + c] = v;
+        }
+        __syncthreads();
 #pragma unroll
-      for (int jj = 0; jj < NB; ++jj) acc[jj] = 0.0;
-      for (int64_t rr = 0; rr < hv; ++rr) {
-        const double xv = (c < kb) ? V[rr * PSL + c] : W[(r0 + rr) * ldw + ct0 + c - kb];
-        const double* vrow = V + rr * PSL;
+        for (int tt = 0; tt < 2; ++tt) {
+          const int T = warp * 2 + tt;  // 32 output tiles: 4 (M) x 8 (N)
+          const int mt = T >> 3, nt = T & 7;
 #pragma unroll
-        for (int jj = 0; jj < NB; ++jj) acc[jj] = fma(vrow[jj], xv, acc[jj]);
+          for (int k = 0; k < RT; k += 4) {
+            const int rr = k + t4;
+            const double av = (rr < rh) ? V[(rt + rr) * PSL + mt * 8 + g4] : 0.0;
+            const double bv = tile[rr * CBP + nt * 8 + g4];
+            dmma_8x8x4(d0[tt], d1[tt], av, bv);
+          }
+        }
       }
 #pragma unroll
-      for (int jj = 0; jj < NB; ++jj)
-        if (jj < kb) gyw[jj * x.ldgy + c] = acc[jj];
+      for (int tt = 0; tt < 2; ++tt) {
+        const int T = warp * 2 + tt;
+        const int mt = T >> 3, nt = T & 7;
+        const int jj = mt * 8 + g4, c = nt * 8 + t4 * 2;
+        if (jj < kb) {
+          if (c < cw) gyw[jj * x.ldgy + cb + c] = d0[tt];
+          if (c + 1 < cw) gyw[jj * x.ldgy + cb + c + 1] = d1[tt];
+        }
+      }
     }
+    QPROF(7);
     x.sync();
+    QPROF(8);
+    // (2) G = V'V (fixed CTA order) and T (dlarft, forward / columnwise), on every CTA
     for (int idx = tid; idx < kb * kb; idx += QR_THREADS) {
       const int jj = idx / kb, kk = idx % kb;
       double s = 0.0;
@@ -260,7 +350,7 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
       Gs[jj * NB + kk] = s;
     }
     __syncthreads();
-    if (warp == 0) {  // dlarft (forward, columnwise); lane k owns row k of T
+    if (warp == 0) {  // lane k owns row k of T
       for (int i = 0; i < kb; ++i) {
         const double ti = taus[i];
         const double g = (lane < i) ? -ti * Gs[lane * NB + i] : 0.0;
@@ -276,40 +366,68 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
       }
     }
     __syncthreads();
+    // (3) this CTA's column slice of Y (fixed-order sum) -> Z = T'Y
     const int64_t c_lo = split_lo(p, P, Nt), c_hi = split_lo(p + 1, P, Nt);
     double* zw = x.z_slice(c_lo);
     const int64_t zld = x.z_ld();
-    for (int64_t cb = c_lo; cb < c_hi; cb += 64) {
-      const int w = static_cast<int>(min(static_cast<int64_t>(64), c_hi - cb));
+    for (int64_t cb = c_lo; cb < c_hi; cb += CB) {
+      const int w = static_cast<int>(min(static_cast<int64_t>(CB), c_hi - cb));
       for (int idx = tid; idx < kb * w; idx += QR_THREADS) {
         const int jj = idx / w, cc = idx % w;
         double s = 0.0;
         for (int q = 0; q < P; ++q) s += x.gy_r(q, jj, kb + cb + cc);
-        ysl[jj * 64 + cc] = s;
+        tile[jj * CBP + cc] = s;
       }
       __syncthreads();
       for (int idx = tid; idx < kb * w; idx += QR_THREADS) {
         const int jj = idx / w, cc = idx % w;
         double s = 0.0;
-        for (int kk = 0; kk <= jj; ++kk) s += Ts[kk * NB + jj] * ysl[kk * 64 + cc];
+        for (int kk = 0; kk <= jj; ++kk) s += Ts[kk * NB + jj] * tile[kk * CBP + cc];
         zw[jj * zld + (cb - c_lo) + cc] = s;
       }
       __syncthreads();
     }
+    QPROF(9);
     x.sync();
-    for (int64_t c = tid; c < Nt; c += QR_THREADS) {
-      double zc[NB];
-      x.load_z(c, Nt, kb, zc);
-      for (int64_t rr = 0; rr < hv; ++rr) {
-        double* wp = W + (r0 + rr) * ldw + ct0 + c;
-        double acc = *wp;
-        const double* vrow = V + rr * PSL;
+    QPROF(10);
+    // (4) W_own(:, ct0:) -= V_own Z on DMMA tiles: M = RT rows, N = CB, K = 32.
+    for (int cb = 0; cb < Nt; cb += CB) {
+      const int cw = static_cast<int>(min(static_cast<int64_t>(CB), Nt - cb));
+      __syncthreads();
+      for (int idx = tid; idx < NB * CB; idx += QR_THREADS) {
+        const int c = idx / NB, jj = idx % NB;  // one column per 32 threads: one owner lookup
+        Zs[jj * CBP + c] = (jj < kb && c < cw) ? x.z_at(jj, cb + c, Nt) : 0.0;
+      }
+      for (int rt = 0; rt < hv; rt += RT) {
+        const int rh = min(RT, hv - rt);
+        __syncthreads();
+        for (int idx = tid; idx < RT * CB; idx += QR_THREADS) {
+          const int rr = idx / CB, c = idx % CB;
+          tile[rr * CBP + c] = (rr < rh && c < cw) ? W[(r0 + rt + rr) * ldw + ct0 + cb + c] : 0.0;
+        }
+        __syncthreads();
 #pragma unroll
-        for (int jj = 0; jj < NB; ++jj) acc = fma(-vrow[jj], zc[jj], acc);
-        *wp = acc;
+        for (int tt = 0; tt < 2; ++tt) {
+          const int T = warp * 2 + tt;  // 32 output tiles: 4 (M) x 8 (N)
+          const int mt = T >> 3, nt = T & 7;
+          const int rr = mt * 8 + g4, c = nt * 8 + t4 * 2;
+          double d0 = tile[rr * CBP + c], d1 = tile[rr * CBP + c + 1];
+#pragma unroll
+          for (int k = 0; k < NB; k += 4) {
+            const double av = (mt * 8 + g4 < rh) ? -V[(rt + mt * 8 + g4) * PSL + k + t4] : 0.0;
+            const double bv = Zs[(k + t4) * CBP + nt * 8 + g4];
+            dmma_8x8x4(d0, d1, av, bv);
+          }
+          if (rr < rh) {
+            double* wp = W + (r0 + rt + rr) * ldw + ct0 + cb + c;
+            if (c < cw) wp[0] = d0;
+            if (c + 1 < cw) wp[1] = d1;
+          }
+        }
       }
     }
     __syncthreads();
+    QPROF(11);
   }
   // R (sign-fixed upper triangle) and z = sign-fixed Q'Sb for own rows < n
   // (linalg.py:43-46); every value read here was written by this CTA.
@@ -328,9 +446,13 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
   if (p == 0)
     for (int64_t i = tid; i < n; i += QR_THREADS)
       if (betas[i] == 0.0) atomicOr(a.singular, 1);
+#ifdef ITSK_QR_PROFILE
+  if (threadIdx.x == 0 && x.p == 0)
+    for (int i = 0; i < 12; ++i) g_qr_prof[i] += _qacc[i];
+#endif
 }
 
-__global__ void __launch_bounds__(QR_THREADS) k_qr_grid(QrArgs a) {
+__global__ void __launch_bounds__(QR_THREADS, 1) k_qr_grid(QrArgs a) {
   extern __shared__ double sm[];
   XGrid x;
   x.rec = a.grec;
@@ -345,10 +467,10 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_grid(QrArgs a) {
 }
 
 __host__ __device__ size_t common_doubles(int64_t hmax, int64_t n) {
-  return static_cast<size_t>(hmax * PSL + 2 * NB * NB + NB + n + NB + NB * 64);
+  return static_cast<size_t>(hmax * PSL + 2 * NB * NB + NB + n + NB + RT * CBP + NB * CBP);
 }
 
-__global__ void __launch_bounds__(QR_THREADS) k_qr_cluster(QrArgs a) {
+__global__ void __launch_bounds__(QR_THREADS, 1) k_qr_cluster(QrArgs a) {
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
   XCluster x;
@@ -358,7 +480,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_cluster(QrArgs a) {
   x.N = a.N;
   x.zld = (a.N + x.P - 1) / x.P + 1;
   x.rec = sm + common_doubles(a.hmax, a.n);
-  x.gy = x.rec + 2 * REC;
+  x.gy = x.rec + 2 * x.P * REC;
   x.z = x.gy + NB * x.ldgy;
   cl.sync();
   qr_body(a, x, sm);
@@ -386,14 +508,20 @@ QrPlan qr_plan(void* ws, int64_t d, int64_t n, int has_rhs) {
   const int C = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (d + 63) / 64)));
   const int64_t hmax_c = (d + C - 1) / C + 1;
   const int64_t zld = (N + C - 1) / C + 1;
-  const size_t smem_cl = (common_doubles(hmax_c, n) + 2 * REC + NB * (NB + N) + NB * zld) * 8;
+  const size_t smem_cl = (common_doubles(hmax_c, n) + 2 * C * REC + NB * (NB + N) + NB * zld) * 8;
   L.cluster = smem_cl <= QR_SMEM_MAX;
+  // tuning override: ITSK_QR_MODE=grid|cluster
+  if (const char* e = getenv("ITSK_QR_MODE")) {
+    if (!strcmp(e, "grid")) L.cluster = false;
+  }
+  int grid_cap = num_sms();
+  if (const char* e = getenv("ITSK_QR_GRID")) grid_cap = std::max(1, std::min(grid_cap, atoi(e)));
   if (L.cluster) {
     L.P = C;
     L.hmax = hmax_c;
     L.smem = smem_cl;
   } else {
-    const int64_t P = std::min<int64_t>(num_sms(), std::max<int64_t>(1, (d + 31) / 32));
+    const int64_t P = std::min<int64_t>(grid_cap, std::max<int64_t>(1, (d + 31) / 32));
     L.P = static_cast<int>(P);
     L.hmax = (d + P - 1) / P + 1;
     L.smem = common_doubles(L.hmax, n) * 8;
@@ -486,3 +614,11 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   }
   return ITSK_OK;
 }
+
+#ifdef ITSK_QR_PROFILE
+extern "C" void itsk_qr_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_qr_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(itsk::g_qr_prof, z, sizeof(z));
+}
+#endif

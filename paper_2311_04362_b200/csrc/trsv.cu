@@ -16,8 +16,12 @@
 //   R y = c  left-looking from the bottom: one warp per row reduces the
 //            contiguous row segment against the solved tail, then one warp
 //            solves the diagonal block.
+#include <cooperative_groups.h>
+
 #include "itsk_common.cuh"
 #include "itsk_dense.cuh"
+
+namespace cg = cooperative_groups;
 #include "itsk_kernels.cuh"
 
 namespace itsk {
@@ -30,9 +34,9 @@ struct RSel;
 template <>
 struct RSel<true> {
   using type = RPacked;
-  __device__ static RPacked make(const double* R, int64_t n, double*& sm) {
-    stage_packed(R, n, sm);
-    RPacked a{sm, n};
+  __device__ static RPacked make(const double* R, const double* Rp, int64_t n, double*& sm) {
+    if (Rp) stage_packed_bulk(Rp, n, sm); else stage_packed(R, n, sm);
+    RPacked a(sm, n);
     sm += packed_doubles(n);
     return a;
   }
@@ -40,7 +44,9 @@ struct RSel<true> {
 template <>
 struct RSel<false> {
   using type = RGlobal;
-  __device__ static RGlobal make(const double* R, int64_t n, double*&) { return RGlobal{R, n}; }
+  __device__ static RGlobal make(const double* R, const double*, int64_t n, double*&) {
+    return RGlobal{R, n};
+  }
 };
 
 template <bool PACKED>
@@ -48,27 +54,28 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_trsv(const double* R, int64_t
                                                double* y, int mode) {
   extern __shared__ double sm[];
   double* cur = sm;
-  const auto RA = RSel<PACKED>::make(R, n, cur);
+  const auto RA = RSel<PACKED>::make(R, nullptr, n, cur);
   double* v = cur;
   double* tmp = cur + n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = c[i];
   __syncthreads();
-  if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v);
+  __shared__ double red_s[32 * (DENSE_THREADS / 32) + 32];
+  if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v, red_s);
   if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, tmp);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = v[i];
 }
 
 // rand_power_norm_est (linalg.py:96-105)
 template <bool PACKED>
-__global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, int64_t n, const double* v0,
-                                                  int64_t steps, double* out) {
+__global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, const double* Rp, int64_t n,
+                                                          const double* v0, int64_t steps, double* out) {
   extern __shared__ double sm[];
   double* cur = sm;
-  const auto R = RSel<PACKED>::make(R0, n, cur);
+  const auto R = RSel<PACKED>::make(R0, Rp, n, cur);
   double* v = cur;
   double* t = cur + n;
   double* w = cur + 2 * n;
-  double* red = cur + 3 * n;
+  __shared__ double red[32 * (DENSE_THREADS / 32) + 32];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = v0[i];
   __syncthreads();
   double nv = sqrt(dot_sm(v, v, n, red));
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, int
   __syncthreads();
   for (int64_t s = 0; s < steps; ++s) {
     trmv_n(R, n, v, t);
-    trmv_t(R, n, t, w);
+    trmv_t(R, n, t, w, red);
     const double nw = sqrt(dot_sm(w, w, n, red));
     if (nw == 0.0) {
       if (threadIdx.x == 0) *out = 0.0;
@@ -139,11 +146,11 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
     if (inv) {
       for (int64_t i = tid; i < n; i += blockDim.x) w[i] = q[i];
       __syncthreads();
-      trsv_t_inplace(R, n, w);
+      trsv_t_inplace(R, n, w, red);
       trsv_n_inplace(R, n, w, t);
     } else {
       trmv_n(R, n, q, t);
-      trmv_t(R, n, t, w);
+      trmv_t(R, n, t, w, red);
     }
     for (int64_t i = tid; i < n; i += blockDim.x) w[i] -= bprev * qp[i];
     __syncthreads();
@@ -158,7 +165,9 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
     }
     __syncthreads();
     theta = s_theta;
-    if (k > 0 && fabs(theta - theta_prev) <= 4e-16 * fabs(theta)) {
+    // stop once the extreme Ritz value has settled (two consecutive steps
+    // within 1e-12 relative — far below what the stopping rule resolves)
+    if (k > 0 && fabs(theta - theta_prev) <= 1e-12 * fabs(theta)) {
       if (++stable >= 2) break;
     } else {
       stable = 0;
@@ -177,21 +186,37 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
 }
 
 template <bool PACKED>
-__global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, int64_t n, const double* v0,
-                                                  double* out) {
+__global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, const double* Rp, int64_t n,
+                                                          const double* v0, double* out) {
   extern __shared__ double sm[];
   double* cur = sm;
-  const auto R = RSel<PACKED>::make(R0, n, cur);
+  const auto R = RSel<PACKED>::make(R0, Rp, n, cur);
   double* q = cur;
   double* qp = cur + n;
   double* w = cur + 2 * n;
   double* t = cur + 3 * n;
-  double* red = cur + 4 * n;
-  double* al = red + 32;
+  __shared__ double red[32 * (DENSE_THREADS / 32) + 32];
+  double* al = cur + 4 * n;
   double* be = al + LANCZOS_MAX;
-  const double smax2 = lanczos_max(R, n, v0, 0, q, qp, w, t, red, al, be);
-  const double imin2 = lanczos_max(R, n, v0, 1, q, qp, w, t, red, al, be);
-  if (threadIdx.x == 0) *out = sqrt(smax2 * imin2);
+  // CTA 0: largest eigenvalue of R'R; CTA 1: of (R'R)^{-1}; both at once in a
+  // 2-CTA cluster, combined through distributed shared memory.
+  __shared__ double theta;
+  const unsigned rank = cg::this_cluster().block_rank();
+  const double th = lanczos_max(R, n, v0, static_cast<int>(rank), q, qp, w, t, red, al, be);
+  if (threadIdx.x == 0) theta = th;
+  cg::this_cluster().sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    const double other = *cg::this_cluster().map_shared_rank(&theta, 1);
+    *out = sqrt(theta * other);
+  }
+  cg::this_cluster().sync();
+}
+
+__global__ void k_pack_upper(const double* __restrict__ R, int64_t n, double* __restrict__ Rp) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  if (j >= i) Rp[i * n - (i * (i - 1)) / 2 + (j - i)] = R[e];
 }
 
 }  // namespace
@@ -243,8 +268,7 @@ extern "C" int itsk_trsv_pair(const double* R, int64_t n, const double* c, doubl
 }
 
 extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps,
-                            double* out, double* ws, itsk_stream_t stream) {
-  (void)ws;
+                            double* out, const double* Rp, itsk_stream_t stream) {
   ITSK_REQUIRE(R && v0 && out && n >= 1 && steps >= 1, "bad normest arguments");
   ITSK_REQUIRE(n <= 8000, "normest: n too large for the single-CTA kernel");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -254,10 +278,10 @@ extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_
   int rc;
   if (packed) {
     if ((rc = prep(k_normest<true>, smem))) return rc;
-    k_normest<true><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, steps, out);
+    k_normest<true><<<1, DENSE_THREADS, smem, s>>>(R, Rp, n, v0, steps, out);
   } else {
     if ((rc = prep(k_normest<false>, smem))) return rc;
-    k_normest<false><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, steps, out);
+    k_normest<false><<<1, DENSE_THREADS, smem, s>>>(R, nullptr, n, v0, steps, out);
   }
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -270,9 +294,8 @@ extern "C" int itsk_condest_workspace(int64_t n, int64_t* doubles) {
   return ITSK_OK;
 }
 
-extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double* out, double* ws,
-                            itsk_stream_t stream) {
-  (void)ws;
+extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double* out,
+                            const double* Rp, itsk_stream_t stream) {
   ITSK_REQUIRE(R && v0 && out && n >= 1, "bad condest arguments");
   ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -280,13 +303,41 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
   const bool packed = use_packed(n, other);
   const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
   int rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(DENSE_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (packed) {
     if ((rc = prep(k_condest<true>, smem))) return rc;
-    k_condest<true><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, out);
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<true>, R, Rp, n, v0, out));
   } else {
     if ((rc = prep(k_condest<false>, smem))) return rc;
-    k_condest<false><<<1, DENSE_THREADS, smem, s>>>(R, n, v0, out);
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<false>, R, static_cast<const double*>(nullptr), n, v0, out));
   }
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_pack_upper_doubles(int64_t n, int64_t* doubles) {
+  ITSK_REQUIRE(doubles && n >= 1, "bad n");
+  *doubles = packed_bytes(n) / 8;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_pack_upper(const double* R, int64_t n, double* Rp, itsk_stream_t stream) {
+  ITSK_REQUIRE(R && Rp && n >= 1, "bad pack arguments");
+  const int64_t total = n * n;
+  k_pack_upper<<<static_cast<unsigned>((total + 255) / 256), 256, 0,
+                 reinterpret_cast<cudaStream_t>(stream)>>>(R, n, Rp);
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;

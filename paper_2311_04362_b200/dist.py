@@ -128,14 +128,16 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     allreduce(ws.W)
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
+    _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
         _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
     ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
     _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), _dev.ptr(ws.est),
-                                None, stream))
-    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, None, stream))
+                                _dev.ptr(ws.Rp), stream))
+    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, _dev.ptr(ws.Rp),
+                                stream))
 
     p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=m_loc)
     cs = ws.cs[: n + 4]

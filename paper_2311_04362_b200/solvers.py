@@ -207,6 +207,8 @@ class _Workspace:
         _lib.check(lib.itsk_qr_workspace(d, n, ctypes.byref(nb)))
         self.qr_ws = _dev.workspace(nb.value, dev)
         self.R = torch.empty((n, n), **f64)
+        _lib.check(lib.itsk_pack_upper_doubles(n, ctypes.byref(nb)))
+        self.Rp = torch.empty(nb.value, **f64)
         self.z = torch.empty(n, **f64)
         self.v0 = torch.empty(n, **f64)
         self.est = torch.zeros(2, **f64)  # normest, condest
@@ -286,14 +288,16 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
                                _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, stream))
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
+    _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
         _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
     ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)), non_blocking=False)
     est_ptr = _dev.ptr(ws.est)
-    _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr, None, stream))
-    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, None, stream))
+    _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
+                                _dev.ptr(ws.Rp), stream))
+    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, _dev.ptr(ws.Rp), stream))
 
 
 def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None):
@@ -312,6 +316,7 @@ def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth,
     p.A = _dev.ptr(at)
     p.b = _dev.ptr(ws.b)
     p.R = _dev.ptr(ws.R)
+    p.Rp = _dev.ptr(ws.Rp)
     p.x_true = _dev.ptr(ws.x_true) if truth is not None else None
     p.r_true = _dev.ptr(ws.r_true) if (truth is not None and truth.beta > 0) else None
     p.normest = _dev.ptr(ws.est)

@@ -151,7 +151,7 @@ def test_trsv_and_estimates_vs_reference(pkg, golden):
         yt = pkg.tri_solve_upper_transpose(r, c)
         np.testing.assert_allclose(yt, sl.solve_triangular(r, c, trans="T"), rtol=1e-12, atol=1e-14)
         assert pkg.rand_power_norm_est(r, rng_seed=i) == pytest.approx(float(g[f"tri{i}_normest"]), rel=1e-12)
-        assert pkg.cond_est(r) == pytest.approx(float(g[f"tri{i}_condest"]), rel=1e-10)
+        assert pkg.cond_est(r) == pytest.approx(float(g[f"tri{i}_condest"]), rel=1e-9)
     with pytest.raises(pkg.SingularMatrixError):
         pkg.tri_solve_upper(np.array([[1.0, 2.0], [0.0, 0.0]]), np.ones(2))
     with pytest.raises(pkg.SingularMatrixError):
@@ -174,7 +174,7 @@ def test_condest_on_sketch_factor(pkg, orc):
     a, b, t = orc.gen_randsvd(20000, 200, 1e10, 1e-12, 0)
     pat = orc.sparse_sign_pattern(4000, 20000, 8, 0)
     _, r = orc.householder_qr_econ(orc.sketch_apply(pat, a))
-    assert pkg.cond_est(r) == pytest.approx(orc.cond_est(r), rel=1e-10)
+    assert pkg.cond_est(r) == pytest.approx(orc.cond_est(r), rel=1e-9)
     assert pkg.rand_power_norm_est(r, rng_seed=0) == pytest.approx(orc.rand_power_norm_est(r, rng_seed=0), rel=1e-12)
 
 
@@ -248,7 +248,7 @@ def test_solve_parity_with_reference(pkg, orc, golden, name):
     assert tr.normest == pytest.approx(float(g[f"{name}_normest"]), rel=1e-10)
     # R differs from LAPACK's by rounding; sigma_min(R) moves by ~kappa*u relative
     kap = float(g[f"{name}_condest"])
-    assert tr.condest == pytest.approx(kap, rel=max(1e-10, 10 * kap * U))
+    assert tr.condest == pytest.approx(kap, rel=max(1e-9, 10 * kap * U))
     fe_ref, re_ref = g[f"{name}_fe"], g[f"{name}_re"]
     # iterate 0 is the sketch-and-solve start: agree to rounding of the QR
     if name != "diverge":
