@@ -61,57 +61,58 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every 5 ms while the
+    timed region runs (nvidia-smi's 100 ms floor would see ~1 sample of a
+    60 ms region)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.samples: list[tuple[float, int]] = []
+        self.smax = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self._nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                clk = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rsn = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((float(clk), int(rsn)))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if getattr(self, "thread", None) is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+        reasons = set()
+        for _, r in self.samples:
+            for bit, nm in names.items():
+                if r & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [c for c, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 5 ms"}
 
 
 def make_problem(name: str, seed: int = 0):
@@ -290,6 +291,14 @@ def run_b200(args):
     x_dev = torch.from_numpy(res.solution).to(dev)
     pass_ms = reduce_max(fused_pass_timing(lib, a_dev, b_dev, x_dev))
     peak, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "pass_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("m") == r1 - r0 and tr.get("n") == n:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     alg_bytes = 8.0 * (r1 - r0) * n
     achieved = alg_bytes / (pass_ms * 1e-3) / 1e9
     out = None
@@ -306,7 +315,7 @@ def run_b200(args):
             "e2e": {"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": int(8 * m * n + 8 * m),
                     "d2h_bytes_per_step": int(8 * ((cfg.max_iters + 1) * n + 4 * (cfg.max_iters + 1) + 2) + 48)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": "k_pass (fused r=b-Ax, c=A'r) + k_finalize",
                          "bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms},
             "gpu_launches": int(launches),

@@ -12,6 +12,7 @@
 // are summed by k_finalize in a fixed order, so c and the norms are
 // bitwise reproducible run to run.
 #include <algorithm>
+#include <cstdlib>
 
 #include "itsk_common.cuh"
 #include "itsk_kernels.cuh"
@@ -439,12 +440,20 @@ TmaShape tma_shape(int64_t lda, int cpl, int unr, int ncw) {
   TmaShape sh;
   const int64_t row_bytes = lda * 8;
   // ~16 KB (at least UNR rows) per bulk copy
-  int64_t T = std::max<int64_t>(1, (16384 + row_bytes - 1) / row_bytes);
+  static const int64_t tile_target = [] {
+    const char* e = getenv("ITSK_PASS_TILE_BYTES");  // tuning knob
+    return e ? std::max(1024L, atol(e)) : 16384L;
+  }();
+  int64_t T = std::max<int64_t>(1, (tile_target + row_bytes - 1) / row_bytes);
   T = ((T + unr - 1) / unr) * unr;
   sh.T = static_cast<int>(T);
   sh.stage_bytes = static_cast<int>(align_up(T * row_bytes, 128));
   const int xbytes = cpl > 8 ? 32 * cpl * 8 : 0;
-  sh.S = std::min(24, (TMA_SMEM_BUDGET - 1024 - xbytes) / sh.stage_bytes);
+  static const int budget = [] {
+    const char* e = getenv("ITSK_PASS_SMEM_KB");  // tuning knob
+    return e ? atoi(e) * 1024 : TMA_SMEM_BUDGET;
+  }();
+  sh.S = std::min(24, (budget - 1024 - xbytes) / sh.stage_bytes);
   const int red = ncw * 32 * cpl * 8;  // final reduction reuses the ring
   while (sh.S * sh.stage_bytes < red) ++sh.S;
   return sh;
@@ -479,7 +488,11 @@ int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
 }
 
 int tma_grid(int64_t m) {
-  int64_t g = num_sms();
+  static const int per_sm = [] {
+    const char* e = getenv("ITSK_PASS_CTAS_PER_SM");  // tuning knob
+    return e ? std::max(1, atoi(e)) : 1;
+  }();
+  int64_t g = static_cast<int64_t>(num_sms()) * per_sm;
   const int64_t cap = (m + 7) / 8;
   if (g > cap) g = cap;
   return static_cast<int>(std::max<int64_t>(1, g));
@@ -540,6 +553,13 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
 
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s) {
+  static const bool carve = [] {
+    // keep the max shared-memory carveout across the pass / finalize pair:
+    // switching the L1/shared split between back-to-back kernels drains SMs
+    cudaFuncSetAttribute(k_finalize, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
   const int t = 256;
   k_finalize<<<static_cast<unsigned>(((n + 4) * 32 + t - 1) / t), t, 0, s>>>(part, grid, n, cs, ctl);
   count_launch();
