@@ -70,4 +70,9 @@ int launch_pass(const PassArgs& a, cudaStream_t s, int* grid_used);
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s);
 
+// Communication-avoiding cluster QR (qr_tsqr.cu)
+int qr_tsqr_plan(int64_t d, int64_t n, size_t* smem);
+int launch_qr_tsqr(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
+                   int* singular, int C, size_t smem, cudaStream_t s);
+
 }  // namespace itsk

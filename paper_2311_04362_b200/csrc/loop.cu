@@ -68,17 +68,17 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
     v = sm;
   }
   tmp = v + n;
-  __shared__ double red_s[32 * (DENSE_THREADS / 32) + 32];
+  __shared__ double red_s[64 * (DENSE_THREADS / 32)];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   __syncthreads();
   if (PACKED) {
     const RPacked R(sm, n);
     trsv_t_inplace(R, n, v, red_s);
-    trsv_n_inplace(R, n, v, tmp);
+    trsv_n_inplace(R, n, v, red_s);
   } else {
-    const RGlobal R{p.R, n};
+    const RGlobal R(p.R, n);
     trsv_t_inplace(R, n, v, red_s);
-    trsv_n_inplace(R, n, v, tmp);
+    trsv_n_inplace(R, n, v, red_s);
   }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p.step[i] = v[i];
 }

@@ -21,7 +21,7 @@ namespace itsk {
 namespace {
 
 typedef unsigned __int128 u128;
-constexpr int CH = 256;  // words per thread chunk
+constexpr int CH = 64;  // words per thread chunk
 
 __device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) {
   return (static_cast<u128>(hi) << 64) | lo;
@@ -103,9 +103,10 @@ __device__ __forceinline__ bool lemire_accept(uint32_t w, uint32_t bound, uint32
   return static_cast<uint32_t>(prod) >= thr;
 }
 
-__global__ void k_lemire_count(Stream st, uint64_t w0, uint64_t nwords, uint32_t bound,
+__global__ void k_lemire_count(Stream st, const uint64_t* w0p, uint64_t nwords, uint32_t bound,
                                uint32_t thr, uint32_t* counts, uint64_t nchunks) {
   const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t w0 = *w0p;  // stream position stays on the device: no host round trip
   if (c == 0) counts[nchunks] = 0;  // so the scan's last slot is the total
   if (c >= nchunks) return;
   const uint64_t beg = c * CH;
@@ -126,11 +127,14 @@ __global__ void k_lemire_count(Stream st, uint64_t w0, uint64_t nwords, uint32_t
 // Emits accepted draws; draw q goes to dst[map(q)] where map is identity
 // (mode 0) or the q-th slot of the redrawn columns (mode 1).  Writes the
 // absolute word index following draw N-1 to *end_word.
-__global__ void k_lemire_emit(Stream st, uint64_t w0, uint64_t nwords, uint32_t bound,
+__global__ void k_lemire_emit(Stream st, const uint64_t* w0p, uint64_t nwords, uint32_t bound,
                               uint32_t thr, const uint32_t* scanned, uint64_t nchunks,
                               uint64_t N, uint32_t* dst, const uint32_t* bad_cols,
-                              int64_t zeta, uint64_t* end_word) {
+                              int64_t zeta, uint64_t* end_word, uint32_t* short_flag) {
   const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t w0 = *w0p;
+  // too few accepted words in the margin: flag it, the host redoes the draw
+  if (c == 0 && scanned[nchunks] < N) *short_flag = 1;
   if (c >= nchunks) return;
   uint64_t q = scanned[c];
   if (q >= N) return;
@@ -149,8 +153,9 @@ __global__ void k_lemire_emit(Stream st, uint64_t w0, uint64_t nwords, uint32_t 
 }
 
 // choice([-1., 1.]) → integers(0, 2): neg = (w >> 31) == 0, one word each.
-__global__ void k_signs(Stream st, uint64_t w0, uint64_t N, uint8_t* neg) {
+__global__ void k_signs(Stream st, const uint64_t* w0p, uint64_t N, uint8_t* neg) {
   const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t w0 = *w0p;
   const uint64_t beg = c * CH;
   if (beg >= N) return;
   const uint64_t len = min(static_cast<uint64_t>(CH), N - beg);
@@ -262,16 +267,29 @@ int64_t carve(Carver& cv, PatternWs& w, int64_t m, int64_t zeta) {
   return cv.off;
 }
 
-// Draw N bounded values starting at word *wpos; advances *wpos.
-int lemire_fill(const Stream& st, uint64_t* wpos, uint64_t N, uint32_t bound, uint32_t* dst,
-                const uint32_t* bad_cols, int64_t zeta, PatternWs& w, cudaStream_t s) {
+// Word position of the stream lives on the device, ping-ponged between two
+// slots (scalars[2], scalars[3]); scalars[4] is the "margin too small" flag.
+struct StreamPos {
+  uint64_t* slots;
+  int cur = 0;
+  uint64_t* in() const { return slots + cur; }
+  uint64_t* out() const { return slots + (cur ^ 1); }
+  void flip() { cur ^= 1; }
+};
+
+// Draw N bounded values starting at the device-side word position.  Fast
+// mode never synchronises (a short margin raises the device flag, checked at
+// the next natural sync); safe mode checks the margin on the host and widens.
+int lemire_fill(const Stream& st, StreamPos& pos, uint64_t N, uint32_t bound, uint32_t* dst,
+                const uint32_t* bad_cols, int64_t zeta, PatternWs& w, cudaStream_t s, bool safe) {
   if (N == 0) return ITSK_OK;
   const uint32_t thr = static_cast<uint32_t>((0x100000000ull - bound) % bound);
   uint64_t nwords = static_cast<uint64_t>(max_words(static_cast<int64_t>(N)));
+  uint32_t* short_flag = reinterpret_cast<uint32_t*>(w.scalars + 4);
   for (int attempt = 0; attempt < 8; ++attempt) {
     const uint64_t nchunks = (nwords + CH - 1) / CH;
     if (nchunks > w.chunk_cap) break;
-    k_lemire_count<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, *wpos, nwords, bound, thr,
+    k_lemire_count<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, pos.in(), nwords, bound, thr,
                                                               w.counts, nchunks);
     count_launch();
     ITSK_CHECK_LAUNCH();
@@ -279,22 +297,22 @@ int lemire_fill(const Stream& st, uint64_t* wpos, uint64_t N, uint32_t bound, ui
     ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned,
                                             static_cast<int>(nchunks + 1), s));
     count_launch();
-    uint32_t total = 0;
-    ITSK_CUDA(cudaMemcpyAsync(&total, w.scanned + nchunks, sizeof(uint32_t),
-                              cudaMemcpyDeviceToHost, s));
-    ITSK_CUDA(cudaStreamSynchronize(s));
-    if (total < N) {  // margin exhausted (astronomically rare): widen and retry
-      nwords = nwords * 2 + 65536;
-      continue;
+    if (safe) {
+      uint32_t total = 0;
+      ITSK_CUDA(cudaMemcpyAsync(&total, w.scanned + nchunks, sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, s));
+      ITSK_CUDA(cudaStreamSynchronize(s));
+      if (total < N) {
+        nwords = nwords * 2 + 65536;
+        continue;
+      }
     }
-    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(
-        st, *wpos, nwords, bound, thr, w.scanned, nchunks, N, dst, bad_cols, zeta, w.scalars);
+    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, pos.in(), nwords, bound, thr,
+                                                             w.scanned, nchunks, N, dst, bad_cols,
+                                                             zeta, pos.out(), short_flag);
     count_launch();
     ITSK_CHECK_LAUNCH();
-    uint64_t end_word = 0;
-    ITSK_CUDA(cudaMemcpyAsync(&end_word, w.scalars, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    ITSK_CUDA(cudaStreamSynchronize(s));
-    *wpos = end_word;
+    pos.flip();
     return ITSK_OK;
   }
   set_error("lemire_fill: could not draw %llu values", (unsigned long long)N);
@@ -350,46 +368,59 @@ extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, cons
   ITSK_REQUIRE(cv.ok(), "pattern workspace too small");
   Stream st{pcg[0], pcg[1], pcg[2], pcg[3], uinteger, has_uint32 ? 1 : 0};
   const int64_t nnz = m * zeta;
-  uint64_t wpos = 0;
+  StreamPos pos{w.scalars + 2};
   int rc;
-  if (zeta == d) {  // np.tile(np.arange(d), (m, 1)): no draws
-    k_tile_rows<<<blocks_for(nnz, 256), 256, 0, s>>>(rows, m, zeta);
-    count_launch();
-    ITSK_CHECK_LAUNCH();
-  } else {
-    const uint32_t bound = static_cast<uint32_t>(d);
-    if ((rc = lemire_fill(st, &wpos, nnz, bound, rows, nullptr, zeta, w, s))) return rc;
-    // _distinct_rows redraw loop (embed.py:37-42)
-    const uint32_t* cols = nullptr;
-    int64_t ncols = m;
-    uint32_t* out = w.bad_a;
-    for (;;) {
-      k_flag_dupes<<<blocks_for(ncols, 256), 256, 0, s>>>(rows, zeta, cols, ncols, w.flags);
-      count_launch();
-      size_t tb = w.cub_bytes;
-      ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan,
-                                              static_cast<int>(ncols), s));
-      count_launch();
-      uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
-      k_compact<<<blocks_for(ncols, 256), 256, 0, s>>>(w.flags, w.fscan, cols, ncols, out,
-                                                       nbad_dev);
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool safe = pass == 1;  // pass 1 only if the fast pass ran out of margin
+    ITSK_CUDA(cudaMemsetAsync(w.scalars, 0, 8 * sizeof(uint64_t), s));
+    pos.cur = 0;
+    bool redo = false;
+    if (zeta == d) {  // np.tile(np.arange(d), (m, 1)): no draws
+      k_tile_rows<<<blocks_for(nnz, 256), 256, 0, s>>>(rows, m, zeta);
       count_launch();
       ITSK_CHECK_LAUNCH();
-      uint32_t nbad = 0;
-      ITSK_CUDA(cudaMemcpyAsync(&nbad, nbad_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-      ITSK_CUDA(cudaStreamSynchronize(s));
-      if (nbad == 0) break;
-      if ((rc = lemire_fill(st, &wpos, static_cast<uint64_t>(nbad) * zeta, bound, rows, out, zeta,
-                            w, s)))
-        return rc;
-      cols = out;
-      ncols = nbad;
-      out = (out == w.bad_a) ? w.bad_b : w.bad_a;
+    } else {
+      const uint32_t bound = static_cast<uint32_t>(d);
+      if ((rc = lemire_fill(st, pos, nnz, bound, rows, nullptr, zeta, w, s, safe))) return rc;
+      // _distinct_rows redraw loop (embed.py:37-42): one host sync per round
+      const uint32_t* cols = nullptr;
+      int64_t ncols = m;
+      uint32_t* out = w.bad_a;
+      for (;;) {
+        k_flag_dupes<<<blocks_for(ncols, 256), 256, 0, s>>>(rows, zeta, cols, ncols, w.flags);
+        count_launch();
+        size_t tb = w.cub_bytes;
+        ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan,
+                                                static_cast<int>(ncols), s));
+        count_launch();
+        uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
+        k_compact<<<blocks_for(ncols, 256), 256, 0, s>>>(w.flags, w.fscan, cols, ncols, out,
+                                                         nbad_dev);
+        count_launch();
+        ITSK_CHECK_LAUNCH();
+        uint64_t hs[5];
+        ITSK_CUDA(cudaMemcpyAsync(hs, w.scalars, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        ITSK_CUDA(cudaStreamSynchronize(s));
+        const uint32_t nbad = static_cast<uint32_t>(hs[1]);
+        if (static_cast<uint32_t>(hs[4])) {  // a fast draw ran short: redo safely
+          redo = true;
+          break;
+        }
+        if (nbad == 0) break;
+        if ((rc = lemire_fill(st, pos, static_cast<uint64_t>(nbad) * zeta, bound, rows, out, zeta,
+                              w, s, safe)))
+          return rc;
+        cols = out;
+        ncols = nbad;
+        out = (out == w.bad_a) ? w.bad_b : w.bad_a;
+      }
     }
+    if (redo) continue;
+    k_signs<<<blocks_for((nnz + CH - 1) / CH, 256), 256, 0, s>>>(st, pos.in(), nnz, neg);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+    break;
   }
-  k_signs<<<blocks_for((nnz + CH - 1) / CH, 256), 256, 0, s>>>(st, wpos, nnz, neg);
-  count_launch();
-  ITSK_CHECK_LAUNCH();
   if (sk_ptr && sk_src) {
     int rc2 = build_csr(rows, neg, m, zeta, d, sk_ptr, sk_src, w, s);
     if (rc2) return rc2;

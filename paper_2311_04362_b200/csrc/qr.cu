@@ -31,6 +31,7 @@
 #include <cstring>
 
 #include "itsk_common.cuh"
+#include "itsk_kernels.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -564,6 +565,24 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
                (long long)n);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   ITSK_CUDA(cudaMemsetAsync(L.bar, 0, 512, s));
+  // Communication-avoiding cluster path (qr_tsqr.cu): correct, but its
+  // 64x32 tree QRs are not yet faster than one exchange per column, so it is
+  // opt-in (ITSK_QR_MODE=tsqr) until the small-QR primitive is tuned.
+  const char* mode = getenv("ITSK_QR_MODE");
+  size_t tsqr_smem = 0;
+  const int tsqr_c = (mode && !strcmp(mode, "tsqr")) ? qr_tsqr_plan(d, n, &tsqr_smem) : 0;
+  if (tsqr_c > 0) {
+    int rc = launch_qr_tsqr(W, d, n, ldw, n + has_rhs, R, z, L.singular, tsqr_c, tsqr_smem, s);
+    if (rc) return rc;
+    int singular = 0;
+    ITSK_CUDA(cudaMemcpyAsync(&singular, L.singular, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ITSK_CUDA(cudaStreamSynchronize(s));
+    if (singular) {
+      set_error("zero diagonal entry in triangular factor");
+      return ITSK_ESINGULAR;
+    }
+    return ITSK_OK;
+  }
   QrArgs a;
   a.W = W;
   a.d = d;

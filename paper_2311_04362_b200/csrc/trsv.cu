@@ -45,7 +45,7 @@ template <>
 struct RSel<false> {
   using type = RGlobal;
   __device__ static RGlobal make(const double* R, const double*, int64_t n, double*&) {
-    return RGlobal{R, n};
+    return RGlobal(R, n);
   }
 };
 
@@ -59,9 +59,9 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_trsv(const double* R, int64_t
   double* tmp = cur + n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = c[i];
   __syncthreads();
-  __shared__ double red_s[32 * (DENSE_THREADS / 32) + 32];
+  __shared__ double red_s[64 * (DENSE_THREADS / 32)];
   if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v, red_s);
-  if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, tmp);
+  if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, red_s);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = v[i];
 }
 
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, con
   double* v = cur;
   double* t = cur + n;
   double* w = cur + 2 * n;
-  __shared__ double red[32 * (DENSE_THREADS / 32) + 32];
+  __shared__ double red[64 * (DENSE_THREADS / 32)];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = v0[i];
   __syncthreads();
   double nv = sqrt(dot_sm(v, v, n, red));
@@ -147,7 +147,7 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
       for (int64_t i = tid; i < n; i += blockDim.x) w[i] = q[i];
       __syncthreads();
       trsv_t_inplace(R, n, w, red);
-      trsv_n_inplace(R, n, w, t);
+      trsv_n_inplace(R, n, w, red);
     } else {
       trmv_n(R, n, q, t);
       trmv_t(R, n, t, w, red);
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, con
   double* qp = cur + n;
   double* w = cur + 2 * n;
   double* t = cur + 3 * n;
-  __shared__ double red[32 * (DENSE_THREADS / 32) + 32];
+  __shared__ double red[64 * (DENSE_THREADS / 32)];
   double* al = cur + 4 * n;
   double* be = al + LANCZOS_MAX;
   // CTA 0: largest eigenvalue of R'R; CTA 1: of (R'R)^{-1}; both at once in a

@@ -2,13 +2,14 @@
 #include <cstdio>
 #include <vector>
 #include <cmath>
+#define ITSK_DENSE_PROBE
 #include "itsk_dense.cuh"
 using namespace itsk;
 namespace itsk { void set_error(const char*, ...) {} void count_launch(int64_t) {} int num_sms() { return 148; } cudaError_t allow_max_smem(const void*) { return cudaSuccess; } }
 
 __global__ void __launch_bounds__(512) probe(const double* Rp, int n, double* y, long long* cyc) {
   extern __shared__ double sm[];
-  __shared__ double red[32 * 16 + 32];
+  __shared__ double red[64 * 16];
   long long t0 = clock64();
   stage_packed_bulk(Rp, n, sm);
   long long t1 = clock64();
@@ -20,7 +21,7 @@ __global__ void __launch_bounds__(512) probe(const double* Rp, int n, double* y,
   long long t2 = clock64();
   trsv_t_inplace(R, n, v, red);
   long long t3 = clock64();
-  trsv_n_inplace(R, n, v, tmp);
+  trsv_n_inplace(R, n, v, red);
   long long t4 = clock64();
   trmv_n(R, n, v, tmp);
   long long t5 = clock64();
@@ -46,6 +47,8 @@ int main() {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0); for (int it = 0; it < 20; ++it) probe<<<1, 512, smem>>>(dP, n, dy, dc); cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
+    long long gp[8]; cudaMemcpyFromSymbol(gp, g_probe, 64); long long z8[8] = {0}; cudaMemcpyToSymbol(g_probe, z8, 64);
+    printf("   per-call (23 calls) prep %lld chain %lld\n", gp[0] / 23, gp[1] / 23);
     printf("n=%d stage %lld  trsv_t %lld  trsv_n %lld  trmv_n %lld  trmv_t %lld cycles ; kernel %.1f us  (%s)\n", n, c[0], c[1], c[2], c[3], c[4], ms * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
   }
   long long* dc; cudaMalloc(&dc, 64);
