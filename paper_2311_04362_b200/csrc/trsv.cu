@@ -223,7 +223,9 @@ __global__ void k_pack_upper(const double* __restrict__ R, int64_t n, double* __
 
 template <class K>
 int prep(K kernel, size_t smem) {
-  if (smem > 48 * 1024) ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(kernel)));
+  // dynamic + static (the kernels' reduction arrays) may cross the 48 KB
+  // default even when `smem` alone does not; the opt-in is cached per kernel
+  if (smem > 16 * 1024) ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(kernel)));
   return ITSK_OK;
 }
 

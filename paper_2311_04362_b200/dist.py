@@ -103,11 +103,11 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     at, lda = _dev.as_device_matrix(a_local, dev)
     ws.b.copy_(_dev.as_device_vector(b_local, dev))
     if truth is not None:
-        ws.x_true.copy_(torch.from_numpy(np.asarray(truth.x, dtype=np.float64)))
+        ws.x_true.copy_(_dev.as_device_vector(truth.x, dev))
         if truth.beta > 0:
-            r = np.asarray(truth.r, dtype=np.float64)
+            r = truth.r
             r = r[row0:row0 + m_loc] if r.shape[0] == m_total else r
-            ws.r_true.copy_(torch.from_numpy(np.ascontiguousarray(r)))
+            ws.r_true.copy_(_dev.as_device_vector(r, dev))
     stream_obj = torch.cuda.current_stream(dev)
     stream = int(stream_obj.cuda_stream)
 

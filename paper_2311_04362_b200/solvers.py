@@ -430,9 +430,9 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
         raise ValueError(f"b has {bsrc.shape[0]} entries, A has {m} rows")
     ws.b.copy_(bsrc, non_blocking=True)
     if truth is not None:
-        ws.x_true.copy_(torch.from_numpy(np.asarray(truth.x, dtype=np.float64)), non_blocking=True)
+        ws.x_true.copy_(_dev.as_device_vector(truth.x, dev))
         if truth.beta > 0:
-            ws.r_true.copy_(torch.from_numpy(np.asarray(truth.r, dtype=np.float64)), non_blocking=True)
+            ws.r_true.copy_(_dev.as_device_vector(truth.r, dev))
     stream_obj = torch.cuda.current_stream(dev)
     stream = int(stream_obj.cuda_stream)
     _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream)

@@ -10,12 +10,17 @@ from paper_2311_04362_b200.linalg import start_vector, normest_steps
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 variant = sys.argv[2] if len(sys.argv) > 2 else "basic"
-from bench import CONFIGS
+gen = sys.argv[3] if len(sys.argv) > 3 else None
+from bench import CONFIGS, make_problem
 m, n, kappa, beta, d, zeta = CONFIGS[cfgname]
-p = itsk.gen_randsvd(m, n, kappa, beta, 0)
+t0 = time.perf_counter()
+p, _, _ = make_problem(cfgname, 0, gen)
+torch.cuda.synchronize()
+print(f"generate {time.perf_counter() - t0:.1f} s", flush=True)
 dev = torch.device("cuda")
 lib = _lib.lib_for_device(0)
-at = torch.from_numpy(p.a).to(dev); bt = torch.from_numpy(p.b).to(dev)
+at = p.a if isinstance(p.a, torch.Tensor) else torch.from_numpy(p.a).to(dev)
+bt = p.b if isinstance(p.b, torch.Tensor) else torch.from_numpy(p.b).to(dev)
 cfg = itsk.SolverConfig(d=d, zeta=zeta, variant=variant)
 for _ in range(3):
     res = itsk.iterative_sketching(at, bt, cfg, residuals="last")
@@ -48,6 +53,8 @@ out["loop(graph)"] = T(loop)
 out["loop(steps)"] = T(lambda: solvers.run_loop(lib, ws, p_, False, s))
 out["trsv_pair"] = T(lambda: _lib.check(lib.itsk_trsv_pair(dv.ptr(ws.R), n, dv.ptr(ws.cs), dv.ptr(ws.z), None, s)))
 out["full_solve"] = T(lambda: itsk.iterative_sketching(at, bt, cfg, residuals="last"))
-print(f"{cfgname} {variant} iters={res.iterations}")
+res = itsk.iterative_sketching(at, bt, cfg, p.truth, residuals="last")
+print(f"{cfgname} {variant} iters={res.iterations} stop={res.trace.stop_reason} "
+      f"fe={res.trace.fe[-1]:.3e} re={res.trace.re[-1]:.3e} normest={res.trace.normest:.4e} condest={res.trace.condest:.4e}")
 for k, (g, w) in out.items():
     print(f"{k:14s} device {g:9.3f} ms   wall {w:9.3f} ms")
