@@ -112,8 +112,12 @@ int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
 int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
                    itsk_stream_t stream);
 
-/* Packed upper triangle of R (row i holds R[i][i..n)), padded to 16 bytes:
- * what the single-CTA R kernels bulk-copy into shared memory in one shot. */
+/* Packed form of R for the single-CTA R kernels, which bulk-copy it into
+ * shared memory in one shot: the upper triangle by rows (row i holds
+ * R[i][i..n), padded to 16 bytes), then the inverses of the 32x32 diagonal
+ * blocks (packed the same way) and each block's 1-norm condition number.
+ * The substitutions multiply by a block inverse when that block is well
+ * conditioned (kappa_1 <= 1e4) and run the scalar chain otherwise. */
 int itsk_pack_upper_doubles(int64_t n, int64_t* doubles);
 int itsk_pack_upper(const double* R, int64_t n, double* Rp, itsk_stream_t stream);
 

@@ -25,6 +25,10 @@ struct RGlobal {
   int nn;
   __device__ __forceinline__ RGlobal(const double* r, int64_t n) : R(r), nn(static_cast<int>(n)) {}
   __device__ __forceinline__ double operator()(int i, int j) const { return R[i * nn + j]; }
+  // incremental addressing: element index; (i, j) -> (i + 1, j) adds rstep(i)
+  __device__ __forceinline__ int addr(int i, int j) const { return i * nn + j; }
+  __device__ __forceinline__ int rstep(int) const { return nn; }
+  __device__ __forceinline__ double ld(int a) const { return R[a]; }
 };
 
 // upper triangle packed by rows: row i holds R[i][i..n) starting at
@@ -38,6 +42,17 @@ struct RPacked {
     const uint32_t off = static_cast<uint32_t>(i * nn - ((i * (i - 1)) >> 1) + (j - i));
     double v;
     asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + off * 8u));  // read-only data: no volatile
+    return v;
+  }
+  // incremental addressing: shared-window byte address; (i, j) -> (i + 1, j)
+  // adds rstep(i) = (n - i - 1) * 8
+  __device__ __forceinline__ uint32_t addr(int i, int j) const {
+    return base + static_cast<uint32_t>(i * nn - ((i * (i - 1)) >> 1) + (j - i)) * 8u;
+  }
+  __device__ __forceinline__ uint32_t rstep(int i) const { return static_cast<uint32_t>(nn - i - 1) * 8u; }
+  __device__ __forceinline__ double ld(uint32_t a) const {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
   }
 };
@@ -63,12 +78,50 @@ __host__ __device__ __forceinline__ int64_t packed_bytes(int64_t n) {
   return (packed_doubles(n) * 8 + 15) / 16 * 16;
 }
 
-__device__ __forceinline__ void stage_packed_bulk(const double* Rp, int64_t n, double* P) {
+// Extended packed layout written by itsk_pack_upper (all offsets in doubles):
+//   [0, P0)          upper triangle packed by rows, P0 = packed_bytes(n)/8
+//   [P0, P0 + XD)    inverses of the 32x32 diagonal blocks, block B at
+//                    P0 + 528 B, packed by rows like the triangle (a partial
+//                    last block holds bs(bs+1)/2 entries)
+//   [P0 + XD, +nblk) kappa_1 of each diagonal block (||D||_1 ||D^-1||_1)
+// A kernel may stage the whole layout or only its first P0 doubles.
+constexpr int DIAG_BLK_PACKED = 528;  // 32 * 33 / 2
+// Blocks whose 1-norm condition number exceeds this use the substitution
+// chain; better-conditioned ones multiply by the stored inverse (forward
+// error kappa(D) u either way, and R's diagonal blocks of the sketched
+// problems are well conditioned: kappa(D_B) ~ kappa(R)^(32/n)).
+constexpr double INVD_COND_MAX = 1.0e4;
+
+__host__ __device__ __forceinline__ int64_t invd_doubles(int64_t n) {
+  const int64_t rem = n % 32;
+  return (n / 32) * DIAG_BLK_PACKED + rem * (rem + 1) / 2;
+}
+__host__ __device__ __forceinline__ int64_t nblocks32(int64_t n) { return (n + 31) / 32; }
+__host__ __device__ __forceinline__ int64_t rp_doubles(int64_t n) {
+  return (packed_bytes(n) / 8 + invd_doubles(n) + nblocks32(n) + 1) / 2 * 2;
+}
+
+// Diagonal-block inverses in shared memory (X == nullptr: not available).
+struct DiagInv {
+  const double* X;
+  const double* kap;
+  __device__ __forceinline__ bool use(int B) const { return X != nullptr && kap[B] <= INVD_COND_MAX; }
+  __device__ __forceinline__ const double* blk(int B) const { return X + B * DIAG_BLK_PACKED; }
+};
+
+__device__ __forceinline__ DiagInv diag_inv_at(const double* P, int64_t n, bool with_inv) {
+  DiagInv d;
+  d.X = with_inv ? P + packed_bytes(n) / 8 : nullptr;
+  d.kap = with_inv ? d.X + invd_doubles(n) : nullptr;
+  return d;
+}
+
+__device__ __forceinline__ void stage_packed_bulk(const double* Rp, int64_t n, double* P, bool with_inv = false) {
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const unsigned bytes = static_cast<unsigned>(packed_bytes(n));
+    const unsigned bytes = static_cast<unsigned>(with_inv ? rp_doubles(n) * 8 : packed_bytes(n));
     mbar_expect_tx(&bar, bytes);
     bulk_g2s_plain(P, Rp, bytes, &bar);
   }
@@ -90,7 +143,8 @@ __device__ __forceinline__ void stage_packed_bulk(const double* Rp, int64_t n, d
 
 // y := R^{-T} y   (forward substitution)
 template <class RA>
-__device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, double* red) {
+__device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, double* red,
+                                               DiagInv inv = DiagInv{nullptr, nullptr}) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = static_cast<int>(n64);
   const int nw = blockDim.x >> 5, nh = nw - 1;  // helper warps 1..nw-1
@@ -110,33 +164,67 @@ __device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, 
         for (int w = 1; w < nw; ++w) s += pb[w * 32 + lane];
       }
       if (I >= 1) {
+        // block I-1's rows (final) into block I: 4 independent chains,
+        // incremental row addressing
         const int pb0 = b0 - 32;
-        double p2 = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) p2 = fma(R(pb0 + k, jl), y[pb0 + k], p2);
-        s += p2;
-      }
-      double col[32];
+        auto ad = R.addr(pb0, jl);
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double v = R(min(b0 + k, n - 1), jl);
-        col[k] = (k < lane && lane < bs) ? v : 0.0;
+        for (int k = 0; k < 32; k += 4) {
+          const double r0 = R.ld(ad);
+          ad += R.rstep(pb0 + k);
+          const double r1 = R.ld(ad);
+          ad += R.rstep(pb0 + k + 1);
+          const double r2 = R.ld(ad);
+          ad += R.rstep(pb0 + k + 2);
+          const double r3 = R.ld(ad);
+          ad += R.rstep(pb0 + k + 3);
+          q0 = fma(r0, y[pb0 + k], q0);
+          q1 = fma(r1, y[pb0 + k + 1], q1);
+          q2 = fma(r2, y[pb0 + k + 2], q2);
+          q3 = fma(r3, y[pb0 + k + 3], q3);
+        }
+        s += (q0 + q1) + (q2 + q3);
       }
-      const double dg = R(jl, jl);
-      const double rinv = (lane < bs) ? 1.0 / dg : 0.0;
       const double yv = y[jl];
       double yi = (lane < bs) ? yv - s : 0.0;
 #ifdef ITSK_DENSE_PROBE
-      __syncwarp();
       long long _c1 = clock64();
 #endif
-      // straight-line chain: for k >= bs the step is a no-op (lane k holds 0,
-      // col[k] == 0), so no per-step branch / reconvergence is needed
+      if (inv.use(I)) {
+        // y_B = X' t with X = D^-1 packed by rows: lane i sums X[k][i] t_k, k <= i
+        const double* X = inv.blk(I);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int off = lane;  // X[k][lane] at off(k) + lane - k, off(k+1) - off(k) = bs - k
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        if (lane == k) yi *= rinv;
-        const double yk = __shfl_sync(FULL, yi, k);
-        yi = fma(-col[k], yk, yi);  // col[k] == 0 for lanes <= k
+        for (int k = 0; k < 32; k += 4) {
+          const double t0 = __shfl_sync(FULL, yi, k), t1 = __shfl_sync(FULL, yi, k + 1);
+          const double t2 = __shfl_sync(FULL, yi, k + 2), t3 = __shfl_sync(FULL, yi, k + 3);
+          const int o0 = off, o1 = o0 + bs - k - 1, o2 = o1 + bs - k - 2, o3 = o2 + bs - k - 3;
+          off = o3 + bs - k - 4;
+          if (k < lane + 1 && lane < bs) a0 = fma(X[o0], t0, a0);
+          if (k + 1 < lane + 1 && lane < bs) a1 = fma(X[o1], t1, a1);
+          if (k + 2 < lane + 1 && lane < bs) a2 = fma(X[o2], t2, a2);
+          if (k + 3 < lane + 1 && lane < bs) a3 = fma(X[o3], t3, a3);
+        }
+        yi = (a0 + a1) + (a2 + a3);
+      } else {
+        double col[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double v = R(min(b0 + k, n - 1), jl);
+          col[k] = (k < lane && lane < bs) ? v : 0.0;
+        }
+        const double dg = R(jl, jl);
+        const double rinv = (lane < bs) ? 1.0 / dg : 0.0;
+        // straight-line chain: for k >= bs the step is a no-op (lane k holds 0,
+        // col[k] == 0), so no per-step branch / reconvergence is needed
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          if (lane == k) yi *= rinv;
+          const double yk = __shfl_sync(FULL, yi, k);
+          yi = fma(-col[k], yk, yi);  // col[k] == 0 for lanes <= k
+        }
       }
 #ifdef ITSK_DENSE_PROBE
       __syncwarp();
@@ -159,7 +247,8 @@ __device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, 
 
 // x := R^{-1} x   (back substitution, blocks from the bottom)
 template <class RA>
-__device__ __forceinline__ void trsv_n_inplace(const RA& R, int n64, double* x, double* red) {
+__device__ __forceinline__ void trsv_n_inplace(const RA& R, int n64, double* x, double* red,
+                                               DiagInv inv = DiagInv{nullptr, nullptr}) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = static_cast<int>(n64);
   const int nw = blockDim.x >> 5, nh = nw - 1;
@@ -175,29 +264,45 @@ __device__ __forceinline__ void trsv_n_inplace(const RA& R, int n64, double* x, 
       if (I + 1 < nblk) {  // block I+1's contribution: row il, columns [be, be+32)
         const int cb = be;
         const int cw = static_cast<int>(min(32, n - cb));
-        double p2 = 0.0;
-#pragma unroll 8
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
         for (int k = 0; k < 32; ++k) {
           const double rv = R(il, min(cb + k, n - 1));
-          p2 = fma(k < cw ? rv : 0.0, x[min(cb + k, n - 1)], p2);
+          q[k & 3] = fma(k < cw ? rv : 0.0, x[min(cb + k, n - 1)], q[k & 3]);
         }
-        s += p2;
+        s += (q[0] + q[1]) + (q[2] + q[3]);
       }
-      double row[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double v = R(il, min(b0 + k, n - 1));
-        row[k] = (k > lane && k < bs) ? v : 0.0;
-      }
-      const double dg = R(il, il);
-      const double rinv = (lane < bs) ? 1.0 / dg : 0.0;
       const double xv = x[il];
       double t = (lane < bs) ? xv - s : 0.0;
+      if (inv.use(I)) {
+        // x_B = X t: lane i sums X[i][k] t_k over k >= i (row i of the packed block)
+        const double* Xr = inv.blk(I) + (lane * bs - ((lane * (lane - 1)) >> 1)) - lane;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-      for (int k = 31; k >= 0; --k) {  // no-op steps for k >= bs (see trsv_t_inplace)
-        if (lane == k) t *= rinv;
-        const double xk = __shfl_sync(FULL, t, k);
-        t = fma(-row[k], xk, t);  // row[k] == 0 for lanes >= k
+        for (int k = 0; k < 32; k += 4) {
+          const double t0 = __shfl_sync(FULL, t, k), t1 = __shfl_sync(FULL, t, k + 1);
+          const double t2 = __shfl_sync(FULL, t, k + 2), t3 = __shfl_sync(FULL, t, k + 3);
+          if (k >= lane && k < bs) a0 = fma(Xr[k], t0, a0);
+          if (k + 1 >= lane && k + 1 < bs) a1 = fma(Xr[k + 1], t1, a1);
+          if (k + 2 >= lane && k + 2 < bs) a2 = fma(Xr[k + 2], t2, a2);
+          if (k + 3 >= lane && k + 3 < bs) a3 = fma(Xr[k + 3], t3, a3);
+        }
+        t = (lane < bs) ? (a0 + a1) + (a2 + a3) : 0.0;
+      } else {
+        double row[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double v = R(il, min(b0 + k, n - 1));
+          row[k] = (k > lane && k < bs) ? v : 0.0;
+        }
+        const double dg = R(il, il);
+        const double rinv = (lane < bs) ? 1.0 / dg : 0.0;
+#pragma unroll
+        for (int k = 31; k >= 0; --k) {  // no-op steps for k >= bs (see trsv_t_inplace)
+          if (lane == k) t *= rinv;
+          const double xk = __shfl_sync(FULL, t, k);
+          t = fma(-row[k], xk, t);  // row[k] == 0 for lanes >= k
+        }
       }
       if (lane < bs) x[b0 + lane] = t;
     } else if (I >= 1 && nh > 0) {
@@ -286,6 +391,11 @@ constexpr int64_t DENSE_SMEM_BUDGET = 200 * 1024;
 
 __host__ __device__ __forceinline__ bool use_packed(int64_t n, int64_t other_doubles) {
   return (packed_doubles(n) + other_doubles) * 8 <= DENSE_SMEM_BUDGET;
+}
+
+// the extended layout (triangle + diagonal-block inverses) fits as well
+__host__ __device__ __forceinline__ bool use_packed_inv(int64_t n, int64_t other_doubles) {
+  return (rp_doubles(n) + other_doubles) * 8 <= DENSE_SMEM_BUDGET;
 }
 
 }  // namespace itsk

@@ -39,6 +39,7 @@ struct LoopPtrs {
   double* part;  // pass partials
   LoopCtl* ctl;
   int64_t lda;
+  int rp_inv;  // Rp carries the diagonal-block inverses and the TRSV kernel stages them
 };
 
 int launch_trsv_pair_device(const double* R, int64_t n, const double* c, double* y,

@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
   double* v;
   double* tmp;
   if (PACKED) {
-    if (p.Rp) stage_packed_bulk(p.Rp, n, sm); else stage_packed(p.R, n, sm);
-    v = sm + packed_doubles(n);
+    if (p.Rp) stage_packed_bulk(p.Rp, n, sm, p.rp_inv != 0); else stage_packed(p.R, n, sm);
+    v = sm + (p.rp_inv ? rp_doubles(n) : packed_doubles(n));
   } else {
     v = sm;
   }
@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
   __syncthreads();
   if (PACKED) {
     const RPacked R(sm, n);
-    trsv_t_inplace(R, n, v, red_s);
-    trsv_n_inplace(R, n, v, red_s);
+    const DiagInv inv = diag_inv_at(sm, n, p.rp_inv != 0);
+    trsv_t_inplace(R, n, v, red_s, inv);
+    trsv_n_inplace(R, n, v, red_s, inv);
   } else {
     const RGlobal R(p.R, n);
     trsv_t_inplace(R, n, v, red_s);
@@ -261,6 +262,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.part = L.part;
   q.ctl = L.ctl;
   q.lda = p->lda;
+  q.rp_inv = (p->Rp != nullptr && use_packed_inv(p->n, p->n + 32)) ? 1 : 0;
   return q;
 }
 
@@ -283,7 +285,9 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
 bool trsv_packed(int64_t n) { return use_packed(n, n + 32); }
 
 size_t trsv_smem(int64_t n) {
-  return static_cast<size_t>((trsv_packed(n) ? packed_doubles(n) : 0) + n + 32) * sizeof(double);
+  // sized for the extended layout when it fits (k_step_trsv stages it iff Rp is set)
+  const int64_t tri = use_packed_inv(n, n + 32) ? rp_doubles(n) : packed_doubles(n);
+  return static_cast<size_t>((trsv_packed(n) ? tri : 0) + n + 32) * sizeof(double);
 }
 
 int enqueue_pre(const itsk_loop_params* p, const LoopPtrs& q, cudaStream_t s) {

@@ -9,12 +9,15 @@
 // the same ascending order in registers — so every output is bitwise equal to
 // scipy's, and the kernel is deterministic.  The b column rides along as
 // column n of the output (apply_vec is the same sum, solvers.py:208).
+#include <algorithm>
+#include <cstdlib>
+
 #include "itsk_common.cuh"
 
 namespace itsk {
 namespace {
 
-template <int CPL>
+template <int CPL, int UNR>
 __global__ void __launch_bounds__(128) k_sketch_gather(
     const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
     const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d,
@@ -24,6 +27,14 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   if (i >= d) return;
   const int64_t ncol = n + (b ? 1 : 0);
   const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 32 * CPL;
+  // per column slot: 0 = A column, 1 = the b column, 2 = none
+  int kind[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int64_t col = c0 + lane + 32 * q;
+    kind[q] = col < n ? 0 : (col == n && b ? 1 : 2);
+  }
+  const double* Ac = A + c0 + lane;
   double acc[CPL];
 #pragma unroll
   for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
@@ -32,23 +43,21 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
     const uint32_t mine = (e + lane < e1) ? src[e + lane] : 0u;
     const int cnt = static_cast<int>(min(32u, e1 - e));
     int k = 0;
-    for (; k + 4 <= cnt; k += 4) {
-      double v[4][CPL];
-      double sv[4];
+    for (; k + UNR <= cnt; k += UNR) {
+      double v[UNR][CPL];
+      double sv[UNR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         const uint32_t s = __shfl_sync(FULL, mine, k + u);
         const int64_t j = s & 0x7fffffffu;
         sv[u] = (s >> 31) ? -scale : scale;
-        const double* arow = A + j * lda;
+        const double* arow = Ac + j * lda;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const int64_t col = c0 + lane + 32 * q;
-          v[u][q] = col < n ? arow[col] : (col == n && b ? b[j] : 0.0);
-        }
+        for (int q = 0; q < CPL; ++q)
+          v[u][q] = kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < UNR; ++u)
 #pragma unroll
         for (int q = 0; q < CPL; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], v[u][q]));
     }
@@ -56,11 +65,10 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
       const uint32_t s = __shfl_sync(FULL, mine, k);
       const int64_t j = s & 0x7fffffffu;
       const double svk = (s >> 31) ? -scale : scale;
-      const double* arow = A + j * lda;
+      const double* arow = Ac + j * lda;
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
-        const int64_t col = c0 + lane + 32 * q;
-        const double a = col < n ? arow[col] : (col == n && b ? b[j] : 0.0);
+        const double a = kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0);
         acc[q] = __dadd_rn(acc[q], __dmul_rn(svk, a));
       }
     }
@@ -72,14 +80,26 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   }
 }
 
-template <int CPL>
+// Tuning knobs (read per call so tests can sweep the variants in-process).
+struct SketchTune {
+  int gcpl = 0;       // register gather: cap on columns-per-lane (more column blocks)
+  int unr = 0;        // register gather: sources per unrolled group (0 = heuristic)
+  SketchTune() {
+    if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
+    if (const char* e = getenv("ITSK_SKETCH_UNR")) unr = atoi(e);
+  }
+};
+
+SketchTune sketch_tune() { return SketchTune(); }
+
+template <int CPL, int UNR>
 int launch_gather(const double* A, int64_t lda, int64_t n, const double* b,
                   const uint32_t* ptr, const uint32_t* src, int64_t d, double scale, double* W,
                   int64_t ldw, cudaStream_t s) {
   const int64_t ncol = n + (b ? 1 : 0);
   dim3 grid(static_cast<unsigned>((d * 32 + 127) / 128),
             static_cast<unsigned>((ncol + 32 * CPL - 1) / (32 * CPL)));
-  k_sketch_gather<CPL><<<grid, 128, 0, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw);
+  k_sketch_gather<CPL, UNR><<<grid, 128, 0, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw);
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
@@ -100,9 +120,26 @@ extern "C" int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, c
   // scale = 1/sqrt(zeta) exactly as embed.py:92 (correctly rounded sqrt, div)
   const double scale = 1.0 / sqrt(static_cast<double>(zeta));
   const int64_t ncol = n + (b ? 1 : 0);
-  const int64_t need = (ncol + 31) / 32;
-  if (need <= 1) return launch_gather<1>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
-  if (need <= 2) return launch_gather<2>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
-  if (need <= 4) return launch_gather<4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
-  return launch_gather<8>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  const SketchTune tu = sketch_tune();
+  // columns per lane: at most 4 (4 columns x 4 sources = 16 loads in flight
+  // per lane at ~70 registers; 8 columns needs ~110 registers and halves the
+  // resident warps — 25% slower at C2), fewer when d is small so that the grid
+  // still has >= ~6000 warps (the chains are sequential per output, so
+  // parallelism comes only from d x column blocks).  A TMA-staged variant
+  // (per-warp ring of bulk-copied row segments) measured 1.8-5x slower: the
+  // per-copy cost of 0.25-2 KB bulk copies dominates.
+  int64_t need = (ncol + 31) / 32;
+  int64_t cap = 4;
+  while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 6000) cap >>= 1;
+  if (tu.gcpl > 0) cap = tu.gcpl;
+  if (need > cap) need = cap;
+  const int unr = tu.unr > 0 ? tu.unr : (need <= 2 ? 8 : 4);
+#define ITSK_G(CPLV, UNRV) \
+  if (unr == UNRV) return launch_gather<CPLV, UNRV>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  if (need <= 1) { ITSK_G(1, 8) ITSK_G(1, 2) return launch_gather<1, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
+  if (need <= 2) { ITSK_G(2, 8) ITSK_G(2, 2) return launch_gather<2, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
+  if (need <= 4) { ITSK_G(4, 8) ITSK_G(4, 2) return launch_gather<4, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
+  ITSK_G(8, 8) ITSK_G(8, 2)
+#undef ITSK_G
+  return launch_gather<8, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
 }

@@ -18,6 +18,8 @@
 //            solves the diagonal block.
 #include <cooperative_groups.h>
 
+#include <cfloat>
+
 #include "itsk_common.cuh"
 #include "itsk_dense.cuh"
 
@@ -34,17 +36,24 @@ struct RSel;
 template <>
 struct RSel<true> {
   using type = RPacked;
-  __device__ static RPacked make(const double* R, const double* Rp, int64_t n, double*& sm) {
-    if (Rp) stage_packed_bulk(Rp, n, sm); else stage_packed(R, n, sm);
+  // with_inv: Rp carries the diagonal-block inverses (extended layout) and
+  // the kernel's shared memory was sized for all of it
+  __device__ static RPacked make(const double* R, const double* Rp, int64_t n, double*& sm,
+                                 DiagInv* inv = nullptr, bool with_inv = false) {
+    with_inv = with_inv && Rp != nullptr;
+    if (Rp) stage_packed_bulk(Rp, n, sm, with_inv); else stage_packed(R, n, sm);
     RPacked a(sm, n);
-    sm += packed_doubles(n);
+    if (inv) *inv = diag_inv_at(sm, n, with_inv);
+    sm += with_inv ? rp_doubles(n) : packed_doubles(n);
     return a;
   }
 };
 template <>
 struct RSel<false> {
   using type = RGlobal;
-  __device__ static RGlobal make(const double* R, const double*, int64_t n, double*&) {
+  __device__ static RGlobal make(const double* R, const double*, int64_t n, double*&,
+                                 DiagInv* inv = nullptr, bool = false) {
+    if (inv) *inv = DiagInv{nullptr, nullptr};
     return RGlobal(R, n);
   }
 };
@@ -97,30 +106,63 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_normest(const double* R0, con
   if (threadIdx.x == 0) *out = r;
 }
 
-// Largest eigenvalue of the k x k symmetric tridiagonal (al, be) by Sturm
-// bisection, to full precision.
-__device__ double tridiag_max_eig(const double* al, const double* be, int k) {
-  double lo = al[0], hi = al[0];
-  for (int i = 0; i < k; ++i) {
-    const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < k - 1 ? fabs(be[i]) : 0.0);
-    lo = fmin(lo, al[i] - r);
-    hi = fmax(hi, al[i] + r);
-  }
-  for (int it = 0; it < 200; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    if (mid <= lo || mid >= hi) break;
-    // number of eigenvalues > mid  ==  k - (# < mid)
-    int below = 0;
-    double q = al[0] - mid;
+// Number of eigenvalues of the k x k symmetric tridiagonal (al, be) below x
+// (Sturm count through the LDL' recurrence).
+__device__ __forceinline__ int sturm_below(const double* al, const double* be, int k, double x) {
+  int below = 0;
+  double q = al[0] - x;
+  if (q < 0) ++below;
+  for (int i = 1; i < k; ++i) {
+    if (q == 0.0) q = 1e-300;
+    q = al[i] - x - be[i - 1] * be[i - 1] / q;
     if (q < 0) ++below;
-    for (int i = 1; i < k; ++i) {
-      if (q == 0.0) q = 1e-300;
-      q = al[i] - mid - be[i - 1] * be[i - 1] / q;
-      if (q < 0) ++below;
-    }
-    if (below == k) hi = mid; else lo = mid;
   }
-  return 0.5 * (lo + hi);
+  return below;
+}
+
+// Largest eigenvalue of the k x k symmetric tridiagonal (al, be), to full
+// precision, by parallel multisection: each round the CTA's T threads test T
+// shifts spread over the current bracket [lo, hi] and keep the sub-interval
+// holding the top eigenvalue — log2(T+1) ~ 9 bits per round instead of one
+// per (sequential, divide-bound) bisection step.  Called by all threads;
+// returns the same value on every thread.
+__device__ double tridiag_max_eig(const double* al, const double* be, int k) {
+  __shared__ double s_lo, s_hi;
+  __shared__ int s_best;
+  const int tid = threadIdx.x, T = blockDim.x;
+  if (tid == 0) {
+    double lo = al[0], hi = al[0];
+    for (int i = 0; i < k; ++i) {
+      const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i < k - 1 ? fabs(be[i]) : 0.0);
+      lo = fmin(lo, al[i] - r);
+      hi = fmax(hi, al[i] + r);
+    }
+    s_lo = lo;
+    s_hi = hi;
+  }
+  __syncthreads();
+  for (int round = 0; round < 16; ++round) {
+    const double lo = s_lo, hi = s_hi;
+    const double w = hi - lo;
+    if (!(w > 0.0)) break;
+    const double x = lo + w * (static_cast<double>(tid + 1) / (T + 1));
+    // an eigenvalue lies above x  <=>  fewer than k lie below x
+    const int above = (x > lo && x < hi && sturm_below(al, be, k, x) < k) ? tid : -1;
+    if (tid == 0) s_best = -1;
+    __syncthreads();
+    if (above >= 0) atomicMax(&s_best, above);
+    __syncthreads();
+    if (tid == 0) {
+      const int t = s_best;
+      const double nlo = t >= 0 ? lo + w * (static_cast<double>(t + 1) / (T + 1)) : lo;
+      const double nhi = t + 1 < T ? lo + w * (static_cast<double>(t + 2) / (T + 1)) : hi;
+      s_lo = nlo;
+      s_hi = fmax(nhi, nlo);
+    }
+    __syncthreads();
+    if (s_hi - s_lo <= 2.0 * DBL_EPSILON * fmax(fabs(s_lo), fabs(s_hi))) break;
+  }
+  return 0.5 * (s_lo + s_hi);
 }
 
 constexpr int LANCZOS_MAX = 96;
@@ -130,9 +172,8 @@ constexpr int LANCZOS_MAX = 96;
 template <class RA>
 __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv, double* q,
                               double* qp, double* w, double* t, double* red, double* al,
-                              double* be) {
+                              double* be, DiagInv dinv) {
   const int tid = threadIdx.x;
-  __shared__ double s_theta;
   double nv = sqrt(dot_sm(v0, v0, n, red));
   for (int64_t i = tid; i < n; i += blockDim.x) {
     q[i] = v0[i] / nv;
@@ -146,8 +187,8 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
     if (inv) {
       for (int64_t i = tid; i < n; i += blockDim.x) w[i] = q[i];
       __syncthreads();
-      trsv_t_inplace(R, n, w, red);
-      trsv_n_inplace(R, n, w, red);
+      trsv_t_inplace(R, n, w, red, dinv);
+      trsv_n_inplace(R, n, w, red, dinv);
     } else {
       trmv_n(R, n, q, t);
       trmv_t(R, n, t, w, red);
@@ -161,10 +202,9 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
     if (tid == 0) {
       al[k] = a;
       be[k] = b;
-      s_theta = tridiag_max_eig(al, be, k + 1);
     }
     __syncthreads();
-    theta = s_theta;
+    theta = tridiag_max_eig(al, be, k + 1);
     // stop once the extreme Ritz value has settled (two consecutive steps
     // within 1e-12 relative — far below what the stopping rule resolves)
     if (k > 0 && fabs(theta - theta_prev) <= 1e-12 * fabs(theta)) {
@@ -187,10 +227,11 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
 
 template <bool PACKED>
 __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, const double* Rp, int64_t n,
-                                                          const double* v0, double* out) {
+                                                          const double* v0, double* out, int with_inv) {
   extern __shared__ double sm[];
   double* cur = sm;
-  const auto R = RSel<PACKED>::make(R0, Rp, n, cur);
+  DiagInv dinv;
+  const auto R = RSel<PACKED>::make(R0, Rp, n, cur, &dinv, with_inv != 0);
   double* q = cur;
   double* qp = cur + n;
   double* w = cur + 2 * n;
@@ -202,7 +243,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, con
   // 2-CTA cluster, combined through distributed shared memory.
   __shared__ double theta;
   const unsigned rank = cg::this_cluster().block_rank();
-  const double th = lanczos_max(R, n, v0, static_cast<int>(rank), q, qp, w, t, red, al, be);
+  const double th = lanczos_max(R, n, v0, static_cast<int>(rank), q, qp, w, t, red, al, be, dinv);
   if (threadIdx.x == 0) theta = th;
   cg::this_cluster().sync();
   if (rank == 0 && threadIdx.x == 0) {
@@ -217,6 +258,56 @@ __global__ void k_pack_upper(const double* __restrict__ R, int64_t n, double* __
   if (e >= n * n) return;
   const int64_t i = e / n, j = e - i * n;
   if (j >= i) Rp[i * n - (i * (i - 1)) / 2 + (j - i)] = R[e];
+}
+
+// Inverse of diagonal block B (warp per block, lane j = column j) into the
+// extended packed layout, plus its 1-norm condition number.  Column j of
+// D^-1 by back substitution: x_j = 1/D_jj, x_k = -(sum_{l=k+1..j} D_kl x_l)/D_kk.
+__global__ void __launch_bounds__(32) k_invert_diag(const double* __restrict__ R, int64_t n64,
+                                                   double* __restrict__ X, double* __restrict__ kap) {
+  const int n = static_cast<int>(n64);
+  const int B = blockIdx.x, lane = threadIdx.x;
+  const int b0 = 32 * B, bs = min(32, n - b0);
+  __shared__ double D[32][33];
+  for (int k = 0; k < 32; ++k)
+    D[k][lane] = (k < bs && lane < bs && lane >= k) ? R[static_cast<int64_t>(b0 + k) * n + b0 + lane] : 0.0;
+  __syncwarp();
+  double x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = 0.0;
+  if (lane < bs) {
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      if (k == lane) {
+        x[k] = 1.0 / D[k][k];
+      } else if (k < lane) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = k + 1; l < 32; ++l)
+          if (l <= lane) s = fma(D[k][l], x[l], s);
+        x[k] = -s / D[k][k];
+      }
+    }
+  }
+  double* Xb = X + static_cast<int64_t>(B) * DIAG_BLK_PACKED;
+  double cx = 0.0, cd = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k <= lane && lane < bs) {
+      Xb[k * bs - ((k * (k - 1)) >> 1) + (lane - k)] = x[k];
+      cx += fabs(x[k]);
+      cd += fabs(D[k][lane]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cx = fmax(cx, __shfl_xor_sync(FULL, cx, o));
+    cd = fmax(cd, __shfl_xor_sync(FULL, cd, o));
+  }
+  if (lane == 0) {
+    const double k1 = cx * cd;
+    kap[B] = (k1 == k1) ? k1 : INFINITY;  // a zero pivot gives inf/nan: use the chain
+  }
 }
 
 }  // namespace
@@ -303,7 +394,9 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t other = 4 * n + 32 + 2 * LANCZOS_MAX;
   const bool packed = use_packed(n, other);
-  const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
+  const int with_inv = Rp != nullptr && use_packed_inv(n, other);
+  const size_t smem =
+      static_cast<size_t>((packed ? (with_inv ? rp_doubles(n) : packed_doubles(n)) : 0) + other) * sizeof(double);
   int rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2);
@@ -319,10 +412,10 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
   cfg.numAttrs = 1;
   if (packed) {
     if ((rc = prep(k_condest<true>, smem))) return rc;
-    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<true>, R, Rp, n, v0, out));
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<true>, R, Rp, n, v0, out, with_inv));
   } else {
     if ((rc = prep(k_condest<false>, smem))) return rc;
-    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<false>, R, static_cast<const double*>(nullptr), n, v0, out));
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<false>, R, static_cast<const double*>(nullptr), n, v0, out, 0));
   }
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -331,15 +424,20 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
 
 extern "C" int itsk_pack_upper_doubles(int64_t n, int64_t* doubles) {
   ITSK_REQUIRE(doubles && n >= 1, "bad n");
-  *doubles = packed_bytes(n) / 8;
+  *doubles = rp_doubles(n);
   return ITSK_OK;
 }
 
 extern "C" int itsk_pack_upper(const double* R, int64_t n, double* Rp, itsk_stream_t stream) {
   ITSK_REQUIRE(R && Rp && n >= 1, "bad pack arguments");
+  ITSK_REQUIRE(n <= 46340, "pack: n too large");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t total = n * n;
-  k_pack_upper<<<static_cast<unsigned>((total + 255) / 256), 256, 0,
-                 reinterpret_cast<cudaStream_t>(stream)>>>(R, n, Rp);
+  k_pack_upper<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(R, n, Rp);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  double* X = Rp + packed_bytes(n) / 8;
+  k_invert_diag<<<static_cast<unsigned>(nblocks32(n)), 32, 0, s>>>(R, n, X, X + invd_doubles(n));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;

@@ -84,6 +84,36 @@ def test_full_size_pattern_and_sketch_digests(pkg, golden, orc):
             assert _sha(s.signs.astype(np.float64)) == rec["signs"], rec
 
 
+SKETCH_VARIANTS = [
+    {}, {"ITSK_SKETCH_UNR": "8"}, {"ITSK_SKETCH_UNR": "2"}, {"ITSK_SKETCH_GCPL": "2", "ITSK_SKETCH_UNR": "8"},
+    {"ITSK_SKETCH_GCPL": "8", "ITSK_SKETCH_UNR": "4"},
+    {"ITSK_SKETCH_GCPL": "4"}, {"ITSK_SKETCH_GCPL": "1"},
+]
+
+
+@pytest.mark.parametrize("variant", SKETCH_VARIANTS)
+def test_sketch_kernel_variants_bitwise(pkg, orc, monkeypatch, variant):
+    """Every sketch kernel variant (register gather with 1..8 columns per lane
+    and 2/4/8-source groups) equals scipy's order bitwise, for even and odd n,
+    a padded leading dimension, and the fused b column."""
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11)
+    for d, m, n, zeta in [(300, 5000, 40, 8), (64, 3000, 257, 4), (500, 2000, 3, 16), (40, 6000, 100, 8)]:
+        pat = orc.sparse_sign_pattern(d, m, zeta, 2)
+        s = pkg.sparse_sign_new(d, m, zeta, 2)
+        a = rng.standard_normal((m, n))
+        b = rng.standard_normal(m)
+        ref = orc.sketch_apply(pat, np.column_stack([a, b]))
+        dev = torch.device("cuda")
+        lda = n + (n % 2) + 2                       # even, padded
+        buf = torch.zeros((m, lda), dtype=torch.float64, device=dev)
+        buf[:, :n] = torch.from_numpy(a).to(dev)
+        got = s.apply_dense(buf[:, :n], torch.from_numpy(b).to(dev)).cpu().numpy()
+        assert np.array_equal(got, ref), (variant, d, m, n, zeta)
+        assert np.array_equal(s.apply_dense(a), ref[:, :n]), (variant, d, m, n, zeta)
+
+
 def test_pattern_argument_errors(pkg):
     with pytest.raises(ValueError):
         pkg.sparse_sign_new(3, 5, 4, 0)
