@@ -72,6 +72,19 @@ int launch_finalize(const double* part, int grid, int64_t n, double* cs, const L
                     cudaStream_t s);
 
 // Communication-avoiding cluster QR (qr_tsqr.cu)
+// Panel / update split QR (qr2.cu), the default path of itsk_qr_aug.
+struct QrV2Plan {
+  int C;             // cluster size of the panel kernel
+  int NB;            // panel width (32, or 16 when 32 does not fit), 0 = unusable
+  int64_t hmax;      // rows per CTA bound
+  size_t smem;       // panel kernel dynamic shared memory
+  int64_t ldy;       // leading dimension of the partial Y buffers
+  int64_t ws_doubles;
+};
+QrV2Plan qr_v2_plan(int64_t d, int64_t n);
+int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
+                 int* singular, double* ws, const QrV2Plan& P, cudaStream_t s);
+
 int qr_tsqr_plan(int64_t d, int64_t n, size_t* smem);
 int launch_qr_tsqr(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
                    int* singular, int C, size_t smem, cudaStream_t s);

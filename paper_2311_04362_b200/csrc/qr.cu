@@ -546,9 +546,12 @@ QrPlan qr_plan(void* ws, int64_t d, int64_t n, int has_rhs) {
 
 using namespace itsk;
 
+constexpr int64_t V2_WS_OFFSET = 1024;  // bytes: [0,512) barrier, [512,1024) singular flag
+
 extern "C" int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes) {
   ITSK_REQUIRE(bytes && d >= n && n >= 1, "need d >= n >= 1");
   *bytes = std::max(qr_plan(nullptr, d, n, 1).ws_bytes, qr_plan(nullptr, d, n, 0).ws_bytes);
+  *bytes = std::max<int64_t>(*bytes, V2_WS_OFFSET + 8 * qr_v2_plan(d, n).ws_doubles);
   return ITSK_OK;
 }
 
@@ -564,11 +567,27 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   ITSK_REQUIRE(L.smem <= QR_SMEM_MAX, "qr: too many rows per CTA (d=%lld, n=%lld)", (long long)d,
                (long long)n);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const char* mode = getenv("ITSK_QR_MODE");
+  const QrV2Plan V2 = qr_v2_plan(d, n);
+  if (V2.NB > 0 && !(mode && (!strcmp(mode, "v1") || !strcmp(mode, "grid") || !strcmp(mode, "tsqr")))) {
+    ITSK_REQUIRE(V2_WS_OFFSET + 8 * V2.ws_doubles <= ws_bytes, "qr workspace too small");
+    int* sing = reinterpret_cast<int*>(static_cast<char*>(ws) + 512);
+    double* wsd = reinterpret_cast<double*>(static_cast<char*>(ws) + V2_WS_OFFSET);
+    int rc = launch_qr_v2(W, d, n, ldw, n + has_rhs, R, z, sing, wsd, V2, s);
+    if (rc) return rc;
+    int singular = 0;
+    ITSK_CUDA(cudaMemcpyAsync(&singular, sing, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ITSK_CUDA(cudaStreamSynchronize(s));
+    if (singular) {
+      set_error("zero diagonal entry in triangular factor");
+      return ITSK_ESINGULAR;
+    }
+    return ITSK_OK;
+  }
   ITSK_CUDA(cudaMemsetAsync(L.bar, 0, 512, s));
   // Communication-avoiding cluster path (qr_tsqr.cu): correct, but its
   // 64x32 tree QRs are not yet faster than one exchange per column, so it is
   // opt-in (ITSK_QR_MODE=tsqr) until the small-QR primitive is tuned.
-  const char* mode = getenv("ITSK_QR_MODE");
   size_t tsqr_smem = 0;
   const int tsqr_c = (mode && !strcmp(mode, "tsqr")) ? qr_tsqr_plan(d, n, &tsqr_smem) : 0;
   if (tsqr_c > 0) {

@@ -1,0 +1,616 @@
+// Householder QR of the augmented sketch [SA | Sb] (K2), panel / update split.
+//
+// Same algorithm and conventions as qr.cu (LAPACK dgeqr2 + dlarfb with the
+// compact-WY factor of dlarft, dlarfg's beta = -sign(alpha) ||x||;
+// /root/reference/pkg/src/itsketch/linalg.py:30-47 via dgeqrf), restructured
+// for latency:
+//
+//   k_qr_panel   one thread-block cluster (<= 16 CTAs) factors the NB-wide
+//                panel.  The CTAs' rows of the panel stay in shared memory;
+//                each column costs ONE fused sweep over the rows (apply
+//                reflector j and accumulate the partial sums of column j+1 in
+//                the same pass), one __syncthreads and ONE cluster barrier
+//                (each CTA pushes its record into every inbox through
+//                distributed shared memory).  The panel ends with G = V'V on
+//                DMMA tiles, summed over the cluster in rank order.
+//   k_qr_y       Y_s = V_s' W2_s over the trailing columns: (column block x
+//                row split) CTAs, cp.async double-buffered row chunks, DMMA.
+//   k_qr_z       Z = T'Y without forming T: (T')^{-1} = diag(1/tau) +
+//                strict_lower(G'), so z_i = tau_i (y_i - sum_{k<i} G_ki z_k)
+//                (tau_i = 0 gives z_i = 0, as dlarft's zero column of T).
+//   k_qr_apply   W2 -= V Z on (row block x column block) CTAs, DMMA.
+//   k_qr_finish  R with diag(R) >= 0 (linalg.py:43-46) and z = (Q'Sb)[:n].
+//
+// Every cross-CTA sum runs in a fixed order: R is bitwise reproducible.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "itsk_common.cuh"
+#include "itsk_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace itsk {
+namespace {
+
+constexpr int QP_THREADS = 512;
+constexpr int QP_WARPS = QP_THREADS / 32;
+constexpr int UT = 64;        // update tile: 64 columns (and 64 rows in k_qr_apply)
+constexpr int UTP = UT + 4;   // padded stride
+constexpr int YRT = 32;       // row chunk of k_qr_y
+constexpr int MAX_SPLIT = 16; // row splits of k_qr_y (partials summed by k_qr_z)
+constexpr int MAX_C = 16;     // cluster size bound
+
+__device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
+__device__ __forceinline__ int64_t lo_of(int q, int P, int64_t len) {
+  return (static_cast<int64_t>(q) * len) / P;
+}
+// D(8x8) += A(8x4) * B(4x8); fragments: a = A[g][t], b = B[t][g],
+// d = D[g][2t + {0, 1}], g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int nbytes = valid ? 8 : 0;  // 0: zero-fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// V(r, c) of the panel starting at row k0: unit lower trapezoidal.
+__device__ __forceinline__ double vval(double stored, int64_t r, int64_t k0, int c) {
+  const int64_t jr = k0 + c;
+  return r < jr ? 0.0 : (r == jr ? 1.0 : stored);
+}
+
+struct PanelArgs {
+  double* W;
+  int64_t d, ldw;
+  int64_t k0;
+  int kb;
+  int64_t hmax;
+  double* betas;  // global, n: R diagonal before the sign fix
+  double* taus;   // global, n
+  double* Gp;     // global, MAX_C x NB x NB: per-CTA partial V'V
+  double* G;      // global, NB x NB: V'V of this panel
+};
+
+#ifdef ITSK_QR2_PROFILE
+__device__ unsigned long long g_qr2_prof[8];
+#define Q2P(i) do { if (threadIdx.x == 0 && q == 0) { long long _t = clock64(); _qa[i] += _t - _qt; _qt = _t; } } while (0)
+#else
+#define Q2P(i) do { } while (0)
+#endif
+
+template <int NB>
+__global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
+  constexpr int PS = NB + 1;   // padded row stride: row walks are bank-conflict free
+  constexpr int REC = 2 * NB;  // [partial sums (NB) | owner's next pivot row (NB)]
+  extern __shared__ __align__(16) double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), q = static_cast<int>(cl.block_rank());
+#ifdef ITSK_QR2_PROFILE
+  long long _qt = clock64();
+  long long _qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = a.k0, ldw = a.ldw;
+  const int kb = a.kb;
+  const int64_t len = a.d - k0;
+  const int64_t lo = k0 + lo_of(q, C, len), hi = k0 + lo_of(q + 1, C, len);
+  const int h = static_cast<int>(hi - lo);
+  double* Ps = sm;                   // h x PS
+  double* inbox = Ps + a.hmax * PS;  // 2 x C x REC (parity-buffered)
+  double* red = inbox + 2 * C * REC; // QP_WARPS x NB
+  double* taus = red + QP_WARPS * NB;
+  double* betl = taus + NB;
+  __shared__ int bnd[MAX_C + 1];  // row split of [k0, d) relative to k0 (no 64-bit divides later)
+  if (tid <= C) bnd[tid] = static_cast<int>(lo_of(tid, C, len));
+  const int cl_lane = lane < NB ? lane : NB - 1;  // NB = 16: upper half-warp mirrors
+
+  for (int idx = tid; idx < h * NB; idx += QP_THREADS) {
+    const int rr = idx / NB, c = idx - rr * NB;
+    Ps[rr * PS + c] = c < kb ? a.W[(lo + rr) * ldw + k0 + c] : 0.0;
+  }
+  __syncthreads();
+
+  // One sweep over the own rows (4 per step): apply reflector jj when `apply`
+  // (lane c > jj: a_rc += v_r temp_c; lane jj stores v_r) and accumulate lane
+  // c's partial sum_{r > j+1} a_{r,jj+1} a_{r,c} for the next column; then
+  // every CTA's record goes to every inbox and the cluster synchronises.
+  auto sweep = [&](int jj, bool apply, double scal, double temp) {
+    const int jn = jj + 1;
+    const int jl = static_cast<int>(k0 + jj - lo);  // local index of row j (may be outside [0,h))
+    const int jnl = jl + 1;
+    // lane predicates are loop-invariant: lanes with temp == 0 rewrite their
+    // value unchanged, lanes < jn accumulate partials nobody reads
+    const bool l_v = apply && lane == jj;
+    const bool l_st = lane < NB;
+    const int jsrc = jn < NB ? jn : 0;
+    const int jcol = jj < 0 ? 0 : jj;
+    // rows j and j+1: updated, not part of the next column's sums
+    if (apply) {
+#pragma unroll
+      for (int sr0 = 0; sr0 < 2; ++sr0) {
+        const int sr = jl + sr0;
+        if (sr >= 0 && sr < h && (sr & (QP_WARPS - 1)) == warp) {
+          double* row = Ps + sr * PS;
+          const double v = row[cl_lane];
+          const double vr = sr0 == 0 ? 1.0 : row[jcol] * scal;
+          double v2 = fma(vr, temp, v);
+          if (l_v && sr0 == 1) v2 = vr;
+          if (l_st) row[lane] = v2;
+        }
+      }
+    }
+    // bulk rows r > j+1 owned by this warp (rr = warp mod QP_WARPS)
+    const int start = jnl + 1 > 0 ? jnl + 1 : 0;
+    int rr = start + ((warp - start) & (QP_WARPS - 1));
+    double p0 = 0.0, p1 = 0.0;
+    if (apply) {
+      for (; rr + 3 * QP_WARPS < h; rr += 4 * QP_WARPS) {
+        double v[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* row = Ps + (rr + u * QP_WARPS) * PS;
+          v[u] = row[cl_lane];
+          x[u] = row[jcol];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double vr = x[u] * scal;
+          double v2 = fma(vr, temp, v[u]);
+          v2 = l_v ? vr : v2;
+          if (l_st) Ps[(rr + u * QP_WARPS) * PS + lane] = v2;
+          const double xn = __shfl_sync(FULL, v2, jsrc);
+          if (u & 1) p1 = fma(xn, v2, p1); else p0 = fma(xn, v2, p0);
+        }
+      }
+      for (; rr < h; rr += QP_WARPS) {
+        double* row = Ps + rr * PS;
+        const double vr = row[jcol] * scal;
+        double v2 = fma(vr, temp, row[cl_lane]);
+        v2 = l_v ? vr : v2;
+        if (l_st) row[lane] = v2;
+        const double xn = __shfl_sync(FULL, v2, jsrc);
+        p0 = fma(xn, v2, p0);
+      }
+    } else {
+      for (; rr + 3 * QP_WARPS < h; rr += 4 * QP_WARPS) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double v = Ps[(rr + u * QP_WARPS) * PS + cl_lane];
+          const double xn = __shfl_sync(FULL, v, jsrc);
+          if (u & 1) p1 = fma(xn, v, p1); else p0 = fma(xn, v, p0);
+        }
+      }
+      for (; rr < h; rr += QP_WARPS) {
+        const double v = Ps[rr * PS + cl_lane];
+        const double xn = __shfl_sync(FULL, v, jsrc);
+        p0 = fma(xn, v, p0);
+      }
+    }
+    Q2P(0);
+    if (jn >= kb) return;  // last column: no record to exchange
+    if (lane < NB) red[warp * NB + lane] = p0 + p1;
+    __syncthreads();
+    Q2P(1);
+    if (warp < C) {  // warp w delivers this CTA's record to CTA w
+      const int buf = jn & 1;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (lane < kb) {
+#pragma unroll
+        for (int w = 0; w < QP_WARPS; w += 4) {
+          s0 += red[w * NB + lane];
+          s1 += red[(w + 1) * NB + lane];
+          s2 += red[(w + 2) * NB + lane];
+          s3 += red[(w + 3) * NB + lane];
+        }
+      }
+      const int64_t jrn = k0 + jn;
+      const bool own_next = jrn >= lo && jrn < hi;
+      if (lane >= jn && lane < kb) {
+        double* ib = cl.map_shared_rank(inbox, warp) + (buf * C + q) * REC;
+        ib[lane] = (s0 + s1) + (s2 + s3);
+        if (own_next) ib[NB + lane] = Ps[(jrn - lo) * PS + lane];
+      }
+    }
+    Q2P(2);
+    cl.sync();
+    Q2P(3);
+  };
+
+  __syncthreads();  // bnd
+  sweep(-1, false, 0.0, 0.0);  // partial sums of column 0
+  int own = 0;
+  for (int jj = 0; jj < kb; ++jj) {
+    const int buf = jj & 1;
+    while (own + 1 < C && bnd[own + 1] <= jj) ++own;  // owner of row k0 + jj
+    // every warp forms the same dlarfg coefficients from the inbox (fixed order)
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
+    const double* ib = inbox + buf * C * REC + cl_lane;
+#pragma unroll
+    for (int t = 0; t < MAX_C; t += 4) {
+      if (t < C) S0 += ib[t * REC];
+      if (t + 1 < C) S1 += ib[(t + 1) * REC];
+      if (t + 2 < C) S2 += ib[(t + 2) * REC];
+      if (t + 3 < C) S3 += ib[(t + 3) * REC];
+    }
+    const double S = (S0 + S1) + (S2 + S3);
+    const double arow = ib[own * REC + NB];
+    const double xn2 = __shfl_sync(FULL, S, jj);
+    const double alpha = __shfl_sync(FULL, arow, jj);
+    double beta, tau, scal;
+    if (xn2 == 0.0) {  // dlarfg: H = I
+      tau = 0.0;
+      beta = alpha;
+      scal = 1.0;
+    } else {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) {
+      taus[jj] = tau;
+      betl[jj] = beta;
+    }
+    const double temp = (lane > jj && lane < kb) ? -tau * (arow + scal * S) : 0.0;
+    Q2P(4);
+    sweep(jj, tau != 0.0, scal, temp);
+  }
+  __syncthreads();
+  Q2P(5);
+  // write the panel back (R rows above the diagonal, v below), betas, taus
+  for (int idx = tid; idx < h * NB; idx += QP_THREADS) {
+    const int rr = idx / NB, c = idx - rr * NB;
+    if (c < kb) a.W[(lo + rr) * ldw + k0 + c] = Ps[rr * PS + c];
+  }
+  if (q == 0)
+    for (int c = tid; c < kb; c += QP_THREADS) {
+      a.betas[k0 + c] = betl[c];
+      a.taus[k0 + c] = taus[c];
+    }
+  // G_q = V_own' V_own on DMMA tiles (one 8x8 tile per warp), to global
+  constexpr int GT = NB / 8;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  if (warp < GT * GT) {
+    const int mt = warp / GT, nt = warp - mt * GT;
+    const int ci = mt * 8 + g4, ck = nt * 8 + g4;
+    double d0 = 0.0, d1 = 0.0;
+    for (int r0 = 0; r0 < h; r0 += 4) {
+      const int r = r0 + t4;
+      const bool ok = r < h;
+      const double av = ok ? vval(Ps[r * PS + ci], lo + r, k0, ci) : 0.0;
+      const double bv = ok ? vval(Ps[r * PS + ck], lo + r, k0, ck) : 0.0;
+      dmma(d0, d1, av, bv);
+    }
+    double* gp = a.Gp + static_cast<int64_t>(q) * NB * NB;
+    gp[ci * NB + nt * 8 + 2 * t4] = d0;
+    gp[ci * NB + nt * 8 + 2 * t4 + 1] = d1;
+  }
+  cl.sync();
+  // G = sum_t G_t in rank order; element e summed by CTA e % C
+  for (int e = q + C * tid; e < NB * NB; e += C * QP_THREADS) {
+    double s = 0.0;
+    for (int t = 0; t < C; ++t) s += __ldcg(a.Gp + static_cast<int64_t>(t) * NB * NB + e);
+    a.G[e] = s;
+  }
+  Q2P(6);
+#ifdef ITSK_QR2_PROFILE
+  if (threadIdx.x == 0 && q == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_qr2_prof[i], static_cast<unsigned long long>(_qa[i]));
+#endif
+}
+
+struct UpdArgs {
+  double* W;
+  int64_t d, ldw, k0;
+  int kb;
+  int64_t c0, Nt;     // trailing columns [c0, c0 + Nt)
+  double* Yp;         // S x NB x ldy partial Y
+  double* Z;          // NB x ldy
+  int64_t ldy;
+  int S;
+  const double* G;    // NB x NB
+  const double* taus; // global, indexed k0 + i
+};
+
+// Y_s = V_s' W2_s  (M = NB reflectors, N = UT columns, K = rows of split s)
+template <int NB>
+__global__ void __launch_bounds__(256) k_qr_y(UpdArgs a) {
+  constexpr int MT = NB / 8, NT = UT / 8;
+  constexpr int TPW = (MT * NT + 7) / 8;  // tiles per warp (8 warps)
+  constexpr int VS = NB + 1;              // strides (8-byte cp.async: any alignment)
+  constexpr int WS = UT + 1;
+  extern __shared__ __align__(16) double ysm[];
+  double* Vt = ysm;                  // 2 x YRT x VS
+  double* Wt = Vt + 2 * YRT * VS;    // 2 x YRT x WS
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int64_t cb = static_cast<int64_t>(blockIdx.x) * UT;
+  const int cw = static_cast<int>(imin64(UT, a.Nt - cb));
+  const int64_t len = a.d - a.k0;
+  const int64_t rlo = a.k0 + lo_of(blockIdx.y, a.S, len), rhi = a.k0 + lo_of(blockIdx.y + 1, a.S, len);
+  const int nchunks = static_cast<int>((rhi - rlo + YRT - 1) / YRT);
+  auto load = [&](int ch, int st) {
+    const int64_t r0 = rlo + static_cast<int64_t>(ch) * YRT;
+    double* vt = Vt + st * YRT * VS;
+    double* wt = Wt + st * YRT * WS;
+    for (int idx = tid; idx < YRT * NB; idx += 256) {
+      const int rr = idx / NB, c = idx - rr * NB;
+      const int64_t r = r0 + rr;
+      const bool ok = r < rhi && c < a.kb;
+      cp_async8(vt + rr * VS + c, a.W + (ok ? r * a.ldw + a.k0 + c : 0), ok);
+    }
+    for (int idx = tid; idx < YRT * UT; idx += 256) {
+      const int rr = idx / UT, c = idx - rr * UT;
+      const int64_t r = r0 + rr;
+      const bool ok = r < rhi && c < cw;
+      cp_async8(wt + rr * WS + c, a.W + (ok ? r * a.ldw + a.c0 + cb + c : 0), ok);
+    }
+    cp_commit();
+  };
+  double d0[TPW], d1[TPW];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) d0[u] = d1[u] = 0.0;
+  if (nchunks > 0) load(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch & 1;
+    if (ch + 1 < nchunks) {
+      load(ch + 1, st ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int64_t r0 = rlo + static_cast<int64_t>(ch) * YRT;
+    const double* vt = Vt + st * YRT * VS;
+    const double* wt = Wt + st * YRT * WS;
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int T = warp * TPW + u;
+      if (T < MT * NT) {
+        const int mt = T / NT, nt = T - mt * NT;
+        const int ci = mt * 8 + g4;
+#pragma unroll
+        for (int k = 0; k < YRT; k += 4) {
+          const double av = vval(vt[(k + t4) * VS + ci], r0 + k + t4, a.k0, ci);
+          dmma(d0[u], d1[u], av, wt[(k + t4) * WS + nt * 8 + g4]);
+        }
+      }
+    }
+    __syncthreads();  // stage st is refilled by the next iteration's load
+  }
+  double* Y = a.Yp + static_cast<int64_t>(blockIdx.y) * NB * a.ldy;
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int T = warp * TPW + u;
+    if (T < MT * NT) {
+      const int mt = T / NT, nt = T - mt * NT;
+      const int i = mt * 8 + g4, c = nt * 8 + t4 * 2;
+      if (c < cw) Y[i * a.ldy + cb + c] = d0[u];
+      if (c + 1 < cw) Y[i * a.ldy + cb + c + 1] = d1[u];
+    }
+  }
+}
+
+// Z = T' sum_s Y_s for UT columns: z_i = tau_i (y_i - sum_{k<i} G_ki z_k)
+template <int NB>
+__global__ void __launch_bounds__(256) k_qr_z(UpdArgs a) {
+  __shared__ double Ys[NB][UT + 1];
+  __shared__ double Gs[NB][NB + 1];
+  __shared__ double ts[NB];
+  const int tid = threadIdx.x;
+  const int64_t cb = static_cast<int64_t>(blockIdx.x) * UT;
+  const int cw = static_cast<int>(imin64(UT, a.Nt - cb));
+  for (int idx = tid; idx < NB * UT; idx += 256) {
+    const int i = idx / UT, c = idx - i * UT;
+    double s = 0.0;
+    if (i < a.kb && c < cw)
+      for (int sp = 0; sp < a.S; ++sp) s += a.Yp[(static_cast<int64_t>(sp) * NB + i) * a.ldy + cb + c];
+    Ys[i][c] = s;
+  }
+  for (int idx = tid; idx < NB * NB; idx += 256) Gs[idx / NB][idx % NB] = a.G[idx];
+  if (tid < NB) ts[tid] = tid < a.kb ? a.taus[a.k0 + tid] : 0.0;
+  __syncthreads();
+  if (tid < cw) {
+    const int c = tid;
+    for (int i = 0; i < a.kb; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+      int k = 0;
+      for (; k + 1 < i; k += 2) {
+        s0 = fma(Gs[k][i], Ys[k][c], s0);
+        s1 = fma(Gs[k + 1][i], Ys[k + 1][c], s1);
+      }
+      if (k < i) s0 = fma(Gs[k][i], Ys[k][c], s0);
+      Ys[i][c] = ts[i] * (Ys[i][c] - (s0 + s1));  // row i of Z overwrites row i of Y
+    }
+    for (int i = 0; i < a.kb; ++i) a.Z[i * a.ldy + cb + c] = Ys[i][c];
+  }
+}
+
+// W2 -= V Z on a 64-row x 64-column tile
+template <int NB>
+__global__ void __launch_bounds__(256) k_qr_apply(UpdArgs a) {
+  constexpr int NT = UT / 8;  // 64 output tiles, 8 per warp
+  __shared__ double Zs[NB][UTP];
+  __shared__ double Vs[UT][NB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int64_t r0 = a.k0 + static_cast<int64_t>(blockIdx.x) * UT;
+  const int rh = static_cast<int>(imin64(UT, a.d - r0));
+  const int64_t cb = static_cast<int64_t>(blockIdx.y) * UT;
+  const int cw = static_cast<int>(imin64(UT, a.Nt - cb));
+  for (int idx = tid; idx < NB * UT; idx += 256) {
+    const int i = idx / UT, c = idx - i * UT;
+    Zs[i][c] = (i < a.kb && c < cw) ? a.Z[i * a.ldy + cb + c] : 0.0;
+  }
+  for (int idx = tid; idx < UT * NB; idx += 256) {
+    const int rr = idx / NB, c = idx - rr * NB;
+    const int64_t r = r0 + rr;
+    Vs[rr][c] = (rr < rh && c < a.kb) ? vval(a.W[r * a.ldw + a.k0 + c], r, a.k0, c) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int T = warp * 8 + u;
+    const int mt = T / NT, nt = T - mt * NT;
+    const int rr = mt * 8 + g4, c = nt * 8 + t4 * 2;
+    double* wp = a.W + (r0 + rr) * a.ldw + a.c0 + cb + c;
+    const bool rok = rr < rh;
+    double d0 = (rok && c < cw) ? wp[0] : 0.0;
+    double d1 = (rok && c + 1 < cw) ? wp[1] : 0.0;
+#pragma unroll
+    for (int k = 0; k < NB; k += 4) dmma(d0, d1, -Vs[mt * 8 + g4][k + t4], Zs[k + t4][nt * 8 + g4]);
+    if (rok) {
+      if (c < cw) wp[0] = d0;
+      if (c + 1 < cw) wp[1] = d1;
+    }
+  }
+}
+
+// R (sign-fixed upper triangle) and z = sign-fixed Q'Sb (linalg.py:43-46).
+__global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, const double* betas,
+                            double* R, double* z, int* singular) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int64_t i = e / n, c = e - i * n;
+  const double bi = betas[i];
+  const double sg = bi < 0.0 ? -1.0 : 1.0;
+  R[e] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
+  if (c == 0) {
+    if (z && N > n) z[i] = sg * W[i * ldw + n];
+    if (bi == 0.0) atomicOr(singular, 1);
+  }
+}
+
+size_t y_smem(int nb) { return static_cast<size_t>(2 * YRT * (nb + 1) + 2 * YRT * (UT + 1)) * 8; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
+  QrV2Plan p{};
+  p.C = static_cast<int>(std::min<int64_t>(MAX_C, std::max<int64_t>(1, d / 64)));
+  p.hmax = (d + p.C - 1) / p.C + 1;
+  const int64_t N = n + 1;
+  for (int nb : {32, 16}) {
+    const int64_t doubles = p.hmax * (nb + 1) + 2 * p.C * 2 * nb + QP_WARPS * nb + 2 * nb;
+    if (doubles * 8 <= 220 * 1024) {
+      p.NB = nb;
+      p.smem = static_cast<size_t>(doubles * 8);
+      break;
+    }
+  }
+  p.ldy = N;
+  // Yp (MAX_SPLIT x 32 x N) | Z (32 x N) | betas (n) | taus (n) | Gp (MAX_C x 32 x 32) | G (32 x 32)
+  p.ws_doubles = static_cast<int64_t>(MAX_SPLIT + 1) * 32 * N + 2 * n + (MAX_C + 1) * 32 * 32 + 64;
+  return p;
+}
+
+int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
+                 int* singular, double* ws, const QrV2Plan& P, cudaStream_t s) {
+  double* Yp = ws;
+  double* Z = Yp + static_cast<int64_t>(MAX_SPLIT) * 32 * N;
+  double* betas = Z + 32 * N;
+  double* taus = betas + n;
+  double* Gp = taus + n;
+  double* G = Gp + MAX_C * 32 * 32;
+  ITSK_CUDA(cudaMemsetAsync(singular, 0, sizeof(int), s));
+  const void* kp = P.NB == 32 ? reinterpret_cast<const void*>(k_qr_panel<32>)
+                              : reinterpret_cast<const void*>(k_qr_panel<16>);
+  const void* ky = P.NB == 32 ? reinterpret_cast<const void*>(k_qr_y<32>)
+                              : reinterpret_cast<const void*>(k_qr_y<16>);
+  ITSK_CUDA(allow_max_smem(kp));
+  ITSK_CUDA(allow_max_smem(ky));
+  ITSK_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int nsm = num_sms();
+  const size_t ysm = y_smem(P.NB);
+  for (int64_t k0 = 0; k0 < n; k0 += P.NB) {
+    const int kb = static_cast<int>(std::min<int64_t>(P.NB, n - k0));
+    PanelArgs pa;
+    pa.W = W;
+    pa.d = d;
+    pa.ldw = ldw;
+    pa.k0 = k0;
+    pa.kb = kb;
+    pa.hmax = P.hmax;
+    pa.betas = betas;
+    pa.taus = taus;
+    pa.Gp = Gp;
+    pa.G = G;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.C);
+    cfg.blockDim = dim3(QP_THREADS);
+    cfg.dynamicSmemBytes = P.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (P.NB == 32)
+      ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_qr_panel<32>, pa));
+    else
+      ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_qr_panel<16>, pa));
+    count_launch();
+    const int64_t c0 = k0 + kb, Nt = N - c0;
+    if (Nt <= 0) continue;
+    UpdArgs ua;
+    ua.W = W;
+    ua.d = d;
+    ua.ldw = ldw;
+    ua.k0 = k0;
+    ua.kb = kb;
+    ua.c0 = c0;
+    ua.Nt = Nt;
+    ua.Yp = Yp;
+    ua.Z = Z;
+    ua.ldy = P.ldy;
+    ua.G = G;
+    ua.taus = taus;
+    const int64_t ncb = (Nt + UT - 1) / UT;
+    const int64_t rows = d - k0;
+    int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(MAX_SPLIT, (2 * nsm) / ncb)));
+    S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, rows / (2 * YRT))));
+    ua.S = S;
+    dim3 gy(static_cast<unsigned>(ncb), static_cast<unsigned>(S));
+    dim3 ga(static_cast<unsigned>((rows + UT - 1) / UT), static_cast<unsigned>(ncb));
+    if (P.NB == 32) {
+      k_qr_y<32><<<gy, 256, ysm, s>>>(ua);
+      k_qr_z<32><<<static_cast<unsigned>(ncb), 256, 0, s>>>(ua);
+      k_qr_apply<32><<<ga, 256, 0, s>>>(ua);
+    } else {
+      k_qr_y<16><<<gy, 256, ysm, s>>>(ua);
+      k_qr_z<16><<<static_cast<unsigned>(ncb), 256, 0, s>>>(ua);
+      k_qr_apply<16><<<ga, 256, 0, s>>>(ua);
+    }
+    count_launch(3);
+    ITSK_CHECK_LAUNCH();
+  }
+  k_qr_finish<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, s>>>(W, n, ldw, N, betas, R, z, singular);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+}  // namespace itsk
+
+#ifdef ITSK_QR2_PROFILE
+extern "C" void itsk_qr2_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_qr2_prof, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(itsk::g_qr2_prof, z, sizeof(z));
+}
+#endif
