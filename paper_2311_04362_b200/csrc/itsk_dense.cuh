@@ -147,8 +147,15 @@ __device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, 
                                                DiagInv inv = DiagInv{nullptr, nullptr}) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = static_cast<int>(n64);
-  const int nw = blockDim.x >> 5, nh = nw - 1;  // helper warps 1..nw-1
+  // helper warps: those not sharing warp 0's scheduler (warp % 4 != 0), so
+  // the sequential block chain of warp 0 issues without competition
+  const int nw = blockDim.x >> 5, nh = nw - (nw >> 2);
+  const int hidx = warp - (warp >> 2) - 1;
   const int nblk = static_cast<int>((n + 31) / 32);
+  // vectors, partials and block inverses all live in shared memory: let the
+  // compiler emit LDS/STS instead of generic loads
+  if (!__isShared(y) || !__isShared(red)) __builtin_unreachable();
+  if (inv.X != nullptr && !__isShared(inv.X)) __builtin_unreachable();
   for (int I = 0; I < nblk; ++I) {
     const int b0 = 32 * I;
     if (warp == 0) {
@@ -158,38 +165,53 @@ __device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, 
       const int bs = static_cast<int>(min(32, n - b0));
       const int jl = min(b0 + lane, n - 1);
       // contributions of blocks < I-1 (helpers, previous step) and of block I-1
-      double s = 0.0;
+      // contributions of blocks < I-1 (helper partials, fixed order)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (I >= 2) {
-        const double* pb = red + (I & 1) * 32 * nw;
-        for (int w = 1; w < nw; ++w) s += pb[w * 32 + lane];
+        const double* pb = red + (I & 1) * 32 * nw + lane;
+#pragma unroll
+        for (int w = 1; w < DENSE_THREADS / 32; w += 4) {
+          s1 += pb[w * 32];
+          if (w + 1 < DENSE_THREADS / 32) s2 += pb[(w + 1) * 32];
+          if (w + 2 < DENSE_THREADS / 32) s3 += pb[(w + 2) * 32];
+          if (w + 3 < DENSE_THREADS / 32) s0 += pb[(w + 3) * 32];
+        }
       }
+#ifdef ITSK_DENSE_PROBE
+      const double _sdep = s0 + s1 + s2 + s3;
+      __syncwarp();
+      long long _ca = clock64() + (_sdep == 12345.0 ? 1 : 0);
+#endif
       if (I >= 1) {
-        // block I-1's rows (final) into block I: 4 independent chains,
-        // incremental row addressing
+        // block I-1's rows (final) into block I, two rounds of 16 independent
+        // loads feeding 4 FMA chains
         const int pb0 = b0 - 32;
         auto ad = R.addr(pb0, jl);
-        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          const double r0 = R.ld(ad);
-          ad += R.rstep(pb0 + k);
-          const double r1 = R.ld(ad);
-          ad += R.rstep(pb0 + k + 1);
-          const double r2 = R.ld(ad);
-          ad += R.rstep(pb0 + k + 2);
-          const double r3 = R.ld(ad);
-          ad += R.rstep(pb0 + k + 3);
-          q0 = fma(r0, y[pb0 + k], q0);
-          q1 = fma(r1, y[pb0 + k + 1], q1);
-          q2 = fma(r2, y[pb0 + k + 2], q2);
-          q3 = fma(r3, y[pb0 + k + 3], q3);
+        for (int h2 = 0; h2 < 32; h2 += 16) {
+          double rv[16], yv[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            rv[k] = R.ld(ad);
+            ad += R.rstep(pb0 + h2 + k);
+            yv[k] = y[pb0 + h2 + k];
+          }
+#pragma unroll
+          for (int k = 0; k < 16; k += 4) {
+            s0 = fma(rv[k], yv[k], s0);
+            s1 = fma(rv[k + 1], yv[k + 1], s1);
+            s2 = fma(rv[k + 2], yv[k + 2], s2);
+            s3 = fma(rv[k + 3], yv[k + 3], s3);
+          }
         }
-        s += (q0 + q1) + (q2 + q3);
       }
+      const double s = (s0 + s1) + (s2 + s3);
       const double yv = y[jl];
       double yi = (lane < bs) ? yv - s : 0.0;
 #ifdef ITSK_DENSE_PROBE
-      long long _c1 = clock64();
+      __syncwarp();
+      long long _c1 = clock64() + (yi == 12345.0 ? 1 : 0);
+      if (lane == 0) { g_probe[2] += _ca - _c0; g_probe[3] += _c1 - _ca; }
 #endif
       if (inv.use(I)) {
         // y_B = X' t with X = D^-1 packed by rows: lane i sums X[k][i] t_k, k <= i
@@ -232,13 +254,15 @@ __device__ __forceinline__ void trsv_t_inplace(const RA& R, int n64, double* y, 
       if (lane == 0) { g_probe[0] += _c1 - _c0; g_probe[1] += _c2 - _c1; }
 #endif
       if (lane < bs) y[b0 + lane] = yi;
-    } else if (I + 1 < nblk && nh > 0) {
+    } else if (I + 1 < nblk) {
       // helpers: rows [0, b0) (blocks < I, final) into block I+1
-      const int t0 = b0 + 32;
-      const int jl = min(t0 + lane, n - 1);
-      const int k_lo = (b0 * (warp - 1)) / nh, k_hi = (b0 * warp) / nh;
       double acc = 0.0;
-      for (int k = k_lo; k < k_hi; ++k) acc = fma(R(k, jl), y[k], acc);
+      if (warp & 3) {
+        const int t0 = b0 + 32;
+        const int jl = min(t0 + lane, n - 1);
+        const int k_lo = (b0 * hidx) / nh, k_hi = (b0 * (hidx + 1)) / nh;
+        for (int k = k_lo; k < k_hi; ++k) acc = fma(R(k, jl), y[k], acc);
+      }
       red[((I + 1) & 1) * 32 * nw + warp * 32 + lane] = acc;
     }
     __syncthreads();
@@ -251,27 +275,42 @@ __device__ __forceinline__ void trsv_n_inplace(const RA& R, int n64, double* x, 
                                                DiagInv inv = DiagInv{nullptr, nullptr}) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = static_cast<int>(n64);
-  const int nw = blockDim.x >> 5, nh = nw - 1;
+  const int nw = blockDim.x >> 5, nh = nw - (nw >> 2);  // helpers: warp % 4 != 0 (see trsv_t_inplace)
+  const int hidx = warp - (warp >> 2) - 1;
   const int nblk = static_cast<int>((n + 31) / 32);
+  if (!__isShared(x) || !__isShared(red)) __builtin_unreachable();
+  if (inv.X != nullptr && !__isShared(inv.X)) __builtin_unreachable();
   for (int I = nblk - 1; I >= 0; --I) {
     const int b0 = 32 * I;
     const int be = min(b0 + 32, n);
     const int bs = static_cast<int>(be - b0);
     if (warp == 0) {
       const int il = min(b0 + lane, n - 1);
-      double s = 0.0;
-      if (I + 1 < nblk) s = red[(I & 1) * 32 * nw + lane];  // columns beyond block I+1 (helpers)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (I + 1 < nblk) s0 = red[(I & 1) * 32 * nw + lane];  // columns beyond block I+1 (helpers)
       if (I + 1 < nblk) {  // block I+1's contribution: row il, columns [be, be+32)
         const int cb = be;
         const int cw = static_cast<int>(min(32, n - cb));
-        double q[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const double rv = R(il, min(cb + k, n - 1));
-          q[k & 3] = fma(k < cw ? rv : 0.0, x[min(cb + k, n - 1)], q[k & 3]);
+        for (int h2 = 0; h2 < 32; h2 += 16) {
+          double rv[16], xv[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int kk = h2 + k;
+            const int cc = min(cb + kk, n - 1);
+            rv[k] = kk < cw ? R(il, cc) : 0.0;
+            xv[k] = x[cc];
+          }
+#pragma unroll
+          for (int k = 0; k < 16; k += 4) {
+            s1 = fma(rv[k], xv[k], s1);
+            s2 = fma(rv[k + 1], xv[k + 1], s2);
+            s3 = fma(rv[k + 2], xv[k + 2], s3);
+            s0 = fma(rv[k + 3], xv[k + 3], s0);
+          }
         }
-        s += (q[0] + q[1]) + (q[2] + q[3]);
       }
+      const double s = (s0 + s1) + (s2 + s3);
       const double xv = x[il];
       double t = (lane < bs) ? xv - s : 0.0;
       if (inv.use(I)) {
@@ -305,11 +344,11 @@ __device__ __forceinline__ void trsv_n_inplace(const RA& R, int n64, double* x, 
         }
       }
       if (lane < bs) x[b0 + lane] = t;
-    } else if (I >= 1 && nh > 0) {
+    } else if (I >= 1 && (warp & 3)) {
       // helpers: columns [be + 32, n) (blocks > I+1, final) into the rows of block I-1
       const int tb0 = b0 - 32;
       const int c0 = be;  // blocks > I are final
-      for (int rr = warp - 1; rr < 32; rr += nh) {
+      for (int rr = hidx; rr < 32; rr += nh) {
         const int i = tb0 + rr;
         double acc = 0.0;
         for (int j = c0 + lane; j < n; j += 32) acc = fma(R(i, j), x[j], acc);

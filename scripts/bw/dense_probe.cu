@@ -66,8 +66,8 @@ int main() {
       long long gp[8]; cudaMemcpyFromSymbol(gp, g_probe, 64);
       std::vector<double> y(n); cudaMemcpy(y.data(), dy, n * 8, cudaMemcpyDeviceToHost);
       double cs = 0; for (double v : y) cs += v;
-      printf("n=%d inv=%d stage %lld trsv_t %lld trsv_n %lld trmv_n %lld trmv_t %lld cycles; kernel %.1f us; t-blocks prep %lld chain %lld; checksum %.15e (%s)\n",
-             n, with_inv, c[0], c[1], c[2], c[3], c[4], ms * 1e3 / 20, gp[0] / 20, gp[1] / 20, cs, cudaGetErrorString(cudaGetLastError()));
+      printf("n=%d inv=%d stage %lld trsv_t %lld trsv_n %lld trmv_n %lld trmv_t %lld cycles; kernel %.1f us; t-blocks prep %lld (red %lld p2 %lld) chain %lld; checksum %.15e (%s)\n",
+             n, with_inv, c[0], c[1], c[2], c[3], c[4], ms * 1e3 / 20, gp[0] / 20, gp[2] / 20, gp[3] / 20, gp[1] / 20, cs, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
