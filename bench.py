@@ -391,8 +391,8 @@ def run_b200(args):
             solve(a_pin.numpy(), b_pin.numpy())
         t_e2e, res_e2e = timed(a_pin.numpy(), b_pin.numpy(), args.steps)
     iters = res.iterations
-    # graph-body kernels (trsv, update, pass, finalize, control) run per iteration
-    launches = (l1 - l0) + args.steps * 5 * iters if not dist_on else (l1 - l0)
+    # graph-body kernels (fused pass, tail) run once per iteration
+    launches = (l1 - l0) + args.steps * 2 * iters if not dist_on else (l1 - l0)
 
     def reduce_max(v):
         if not dist_on:

@@ -189,15 +189,16 @@ typedef struct itsk_loop_result { /* read back with one D2H copy */
 } itsk_loop_result;
 
 int itsk_loop_workspace(int64_t m, int64_t n, int64_t* bytes);
-/* Writes constants, r0 = b - A x0 (fused pass) and records iterate 0.
- * For multi-GPU call itsk_loop_begin_local, allreduce p->cs, then
- * itsk_loop_begin_finish. */
+/* Writes constants, r0 = b - A x0 (fused pass), records iterate 0 and
+ * forms x1.  For multi-GPU call itsk_loop_begin_local, allreduce p->cs,
+ * then itsk_loop_begin_finish. */
 int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream);
 int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t stream);
 int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream);
-/* One iteration, split around the collective: pre = two TRSVs, update,
- * fused pass + local finalize into p->cs; post = guard, stopping rule,
- * trace.  Both are no-ops once the loop is done. */
+/* One iteration, split around the collective: pre = fused pass over the
+ * local rows + partial sums into p->cs; post = guard, stopping rule, trace
+ * and (unless stopped) the next iterate (two TRSVs + update).  Both are
+ * no-ops once the loop is done. */
 int itsk_loop_step_pre(const itsk_loop_params* p, itsk_stream_t stream);
 int itsk_loop_step_post(const itsk_loop_params* p, itsk_stream_t stream);
 /* Whole loop as a CUDA graph (conditional WHILE); the handle caches the

@@ -63,7 +63,18 @@ struct PassArgs {
   const double* xs;
   double* rs;
   int mode;  // 0 = explicit pointers, 1 = loop step (x = xs[it+1]), 2 = loop begin (x = xs[0])
+  // in-kernel reduction (optional): when `tickets` is set the pass itself
+  // sums the per-CTA partials into `cs` — the last CTA of each group of
+  // `group` CTAs sums its group into gpart, the last group sums the groups,
+  // both in CTA / group order (deterministic); tickets self-reset.
+  unsigned* tickets;  // ceil(grid / group) + 1 counters, zero before first use
+  double* gpart;      // ceil(grid / group) x (n + 4)
+  double* cs;         // n + 4
+  int group;
 };
+
+// counters / group partials needed by the in-kernel reduction of a pass
+int pass_groups(int64_t m, int64_t n, int* group);
 
 int pass_grid(int64_t m, int64_t n);
 int64_t pass_part_doubles(int64_t m, int64_t n);

@@ -1,17 +1,21 @@
 // Device-resident refinement loop (K5): _run_refinement
 // (/root/reference/pkg/src/itsketch/solvers.py:270-320).
 //
-// One iteration = k_step_trsv (d = R^{-1}R^{-T} c, solvers.py:294/339-340)
-//               -> k_update   (x+ = x + d  |  x + alpha d + beta (x - x-), :295-298)
-//               -> fused pass (r+ = b - A x+, c+ = A'r+, norms; :299-302, :343)
-//               -> finalize   (fixed-order reduction of the pass partials)
-//               -> k_control  (divergence guard :302-305, _record :241-256,
-//                              stopping rule + extra_iters countdown :308-318)
+// One iteration = two kernels:
+//   fused pass  r = b - A x, c = A'r and the norms (solvers.py:299-302,
+//               :343); the pass also sums its per-CTA partials (last CTA of
+//               each group, then the last group, in a fixed order: PassArgs)
+//   k_tail      one CTA: the control step (divergence guard :302-305,
+//               _record :241-256, stopping rule + extra_iters countdown
+//               :308-318) and, unless the loop stopped, the next iterate:
+//               d = R^{-1}R^{-T} c (:294, :339-340) and
+//               x+ = x + d | x + alpha d + beta (x - x-) (:295-298).
 // All loop state (iteration counter, guard history, countdown, stop reason)
 // lives in a LoopCtl block in device memory, so the whole loop runs as one
-// CUDA graph whose WHILE conditional node is cleared by k_control — no host
-// round trip per iteration.  For multi-GPU the host calls step_pre, sums
-// p->cs across ranks (the only collective), then step_post.
+// CUDA graph whose WHILE conditional node is cleared by k_tail — no host
+// round trip per iteration.  For multi-GPU the host calls step_pre (pass +
+// local partial sums), sums p->cs across ranks (the only collective), then
+// step_post (control + next iterate, replicated).
 #include <algorithm>
 
 #include "itsk_common.cuh"
@@ -21,7 +25,6 @@
 namespace itsk {
 namespace {
 
-constexpr int CTRL_THREADS = 256;
 
 __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iters,
                             int64_t extra_iters, int variant, int r_slots, int has_truth,
@@ -54,76 +57,19 @@ __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iter
   ctl->result.bnorm2 = 0.0;
 }
 
-template <bool PACKED>
-__global__ void __launch_bounds__(DENSE_THREADS) k_step_trsv(LoopPtrs p) {
-  if (p.ctl->result.done) return;
-  extern __shared__ double sm[];
-  const int64_t n = p.ctl->n;
-  double* v;
-  double* tmp;
-  if (PACKED) {
-    if (p.Rp) stage_packed_bulk(p.Rp, n, sm, p.rp_inv != 0); else stage_packed(p.R, n, sm);
-    v = sm + (p.rp_inv ? rp_doubles(n) : packed_doubles(n));
-  } else {
-    v = sm;
-  }
-  tmp = v + n;
-  __shared__ double red_s[64 * (DENSE_THREADS / 32)];
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
-  __syncthreads();
-  if (PACKED) {
-    const RPacked R(sm, n);
-    const DiagInv inv = diag_inv_at(sm, n, p.rp_inv != 0);
-    trsv_t_inplace(R, n, v, red_s, inv);
-    trsv_n_inplace(R, n, v, red_s, inv);
-  } else {
-    const RGlobal R(p.R, n);
-    trsv_t_inplace(R, n, v, red_s);
-    trsv_n_inplace(R, n, v, red_s);
-  }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p.step[i] = v[i];
-}
-
-// x_{i+1} in the reference's exact operation order (no FMA contraction).
-__global__ void k_update(LoopPtrs p) {
-  const LoopCtl* ctl = p.ctl;
-  if (ctl->result.done) return;
-  const int64_t n = ctl->n, it = ctl->it;
-  const double* x = p.xs + it * n;
-  const double* xp = p.xs + (it > 0 ? it - 1 : 0) * n;
-  double* xn = p.xs + (it + 1) * n;
-  const double alpha = ctl->alpha, beta = ctl->beta;
-  const bool basic = ctl->variant == ITSK_VARIANT_BASIC;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double xi = x[i], di = p.step[i];
-    if (basic) {
-      xn[i] = __dadd_rn(xi, di);
-    } else {
-      const double t = __dadd_rn(xi, __dmul_rn(alpha, di));
-      xn[i] = __dadd_rn(t, __dmul_rn(beta, __dsub_rn(xi, xp[i])));
-    }
-  }
-}
-
 // Guard + record + stopping rule.  begin == 1 records iterate 0 only.
-__global__ void __launch_bounds__(CTRL_THREADS) k_control(LoopPtrs p, int begin,
-                                                          cudaGraphConditionalHandle h,
-                                                          int use_cond) {
-  LoopCtl* ctl = p.ctl;
-  __shared__ double red[CTRL_THREADS / 32];
+// Called by every thread of the tail CTA with `ctl` a shared-memory copy of
+// the loop state; returns the (CTA-uniform) done flag.
+__device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
+  __shared__ double red[DENSE_THREADS / 32];
   __shared__ int s_done;
-  if (ctl->result.done) {
-    if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
-    return;
-  }
   const int64_t n = ctl->n, it = ctl->it;
   const int64_t K = ctl->max_iters + 1;
   const int64_t xi = begin ? 0 : it + 1;
   const double* x = p.xs + xi * n;
   double sx = 0.0, sf = 0.0, st = 0.0;
   int fin = 1;
-  for (int64_t i = threadIdx.x; i < n; i += CTRL_THREADS) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const double v = x[i];
     sx += v * v;
     fin &= isfinite(v) ? 1 : 0;
@@ -208,14 +154,108 @@ __global__ void __launch_bounds__(CTRL_THREADS) k_control(LoopPtrs p, int begin,
     }
     ctl->result.done = done;
     s_done = done;
-    if (done && use_cond) cudaGraphSetConditional(h, 0);
   }
+  __syncthreads();
+  return s_done;
+}
+
+
+enum : int { TAIL_CONTROL = 2, TAIL_STEP = 4, TAIL_BEGIN = 8 };
+
+// The serial tail of an iteration on one CTA (see the file comment).
+#ifdef ITSK_TAIL_PROBE
+__device__ unsigned long long g_tail_prof[16];
+#define TP(i) do { if (threadIdx.x == 0) { long long _t = clock64(); atomicAdd(&g_tail_prof[i], (unsigned long long)(_t - _tp)); _tp = _t; } } while (0)
+#else
+#define TP(i) do { } while (0)
+#endif
+
+template <bool PACKED>
+__global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, int grid,
+                                                        cudaGraphConditionalHandle h, int use_cond) {
+#ifdef ITSK_TAIL_PROBE
+  long long _tp = clock64();
+  if (threadIdx.x == 0) atomicAdd(&g_tail_prof[15], 1ull);
+#endif
+  // the loop state in shared memory: the control step's scalar bookkeeping
+  // would otherwise be a chain of dependent L2 round trips
+  constexpr int CTL_WORDS = sizeof(LoopCtl) / 8;
+  static_assert(sizeof(LoopCtl) % 8 == 0 && CTL_WORDS <= DENSE_THREADS, "LoopCtl copy");
+  __shared__ LoopCtl s_ctl;
+  if (threadIdx.x < CTL_WORDS)
+    reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
+  __syncthreads();
+  LoopCtl* ctl = &s_ctl;
+  TP(0);
+  if (ctl->result.done) {
+    if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+    return;
+  }
+  const int64_t n = ctl->n;
+  if (flags & TAIL_CONTROL) {
+    const int done = control_step(p, ctl, (flags & TAIL_BEGIN) ? 1 : 0);
+    TP(2);
+    if (threadIdx.x < CTL_WORDS)
+      reinterpret_cast<uint64_t*>(p.ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(&s_ctl)[threadIdx.x];
+    if (done) {
+      if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+      return;
+    }
+  }
+  if (!(flags & TAIL_STEP)) return;
+  // d = R^{-1} R^{-T} c in shared memory, then x_{it+1}
+  extern __shared__ double sm[];
+  double* v;
+  if (PACKED) {
+    if (p.Rp) stage_packed_bulk(p.Rp, n, sm, p.rp_inv != 0); else stage_packed(p.R, n, sm);
+    v = sm + (p.rp_inv ? rp_doubles(n) : packed_doubles(n));
+  } else {
+    v = sm;
+  }
+  __shared__ double red_s[64 * (DENSE_THREADS / 32)];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
+  __syncthreads();
+  TP(3);
+  if (PACKED) {
+    const RPacked R(sm, n);
+    const DiagInv inv = diag_inv_at(sm, n, p.rp_inv != 0);
+    trsv_t_inplace(R, n, v, red_s, inv);
+    TP(4);
+    trsv_n_inplace(R, n, v, red_s, inv);
+    TP(5);
+  } else {
+    const RGlobal R(p.R, n);
+    trsv_t_inplace(R, n, v, red_s);
+    trsv_n_inplace(R, n, v, red_s);
+  }
+  // x_{i+1} in the reference's exact operation order (no FMA contraction)
+  const int64_t it = ctl->it;
+  const double* x = p.xs + it * n;
+  const double* xp = p.xs + (it > 0 ? it - 1 : 0) * n;
+  double* xn = p.xs + (it + 1) * n;
+  const double alpha = ctl->alpha, beta = ctl->beta;
+  const bool basic = ctl->variant == ITSK_VARIANT_BASIC;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double xi = x[i], di = v[i];
+    if (basic) {
+      xn[i] = __dadd_rn(xi, di);
+    } else {
+      const double t = __dadd_rn(xi, __dmul_rn(alpha, di));
+      xn[i] = __dadd_rn(t, __dmul_rn(beta, __dsub_rn(xi, xp[i])));
+    }
+  }
+  __syncthreads();
+  TP(6);
 }
 
 struct LoopLayout {
   LoopCtl* ctl;
   double* step;
   double* part;
+  double* gpart;
+  unsigned* tickets;
+  int ntickets;
+  int group;
   int64_t bytes;
 };
 
@@ -225,6 +265,10 @@ LoopLayout loop_layout(void* ws, int64_t m, int64_t n) {
   L.ctl = cv.take<LoopCtl>(1);
   L.step = cv.take<double>(n + 32);
   L.part = cv.take<double>(pass_part_doubles(m, n));
+  const int ng = pass_groups(m, n, &L.group);
+  L.gpart = cv.take<double>(static_cast<int64_t>(ng) * (n + 4));
+  L.ntickets = ng + 1;
+  L.tickets = cv.take<unsigned>(L.ntickets);
   L.bytes = cv.off + 256;
   return L;
 }
@@ -279,7 +323,19 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   a.xs = p->xs;
   a.rs = p->rs;
   a.mode = mode;
+  // the pass reduces its partials into p->cs itself
+  const LoopLayout L = loop_layout(p->ws, p->m, p->n);
+  a.tickets = L.tickets;
+  a.gpart = L.gpart;
+  a.cs = p->cs;
+  a.group = L.group;
   return a;
+}
+
+int reset_tickets(const itsk_loop_params* p, cudaStream_t s) {
+  const LoopLayout L = loop_layout(p->ws, p->m, p->n);
+  ITSK_CUDA(cudaMemsetAsync(L.tickets, 0, sizeof(unsigned) * L.ntickets, s));
+  return ITSK_OK;
 }
 
 bool trsv_packed(int64_t n) { return use_packed(n, n + 32); }
@@ -290,28 +346,22 @@ size_t trsv_smem(int64_t n) {
   return static_cast<size_t>((trsv_packed(n) ? tri : 0) + n + 32) * sizeof(double);
 }
 
-int enqueue_pre(const itsk_loop_params* p, const LoopPtrs& q, cudaStream_t s) {
-  const size_t smem = trsv_smem(p->n);
+int enqueue_tail(const itsk_loop_params* p, const LoopPtrs& q, int flags, int grid, cudaStream_t s,
+                 cudaGraphConditionalHandle cond = cudaGraphConditionalHandle{}, int use_cond = 0) {
+  const size_t smem = (flags & TAIL_STEP) ? trsv_smem(p->n) : 0;
   if (trsv_packed(p->n))
-    k_step_trsv<true><<<1, DENSE_THREADS, smem, s>>>(q);
+    k_tail<true><<<1, DENSE_THREADS, smem, s>>>(q, flags, grid, cond, use_cond);
   else
-    k_step_trsv<false><<<1, DENSE_THREADS, smem, s>>>(q);
+    k_tail<false><<<1, DENSE_THREADS, smem, s>>>(q, flags, grid, cond, use_cond);
   count_launch();
   ITSK_CHECK_LAUNCH();
-  const int ub = static_cast<int>(std::min<int64_t>((p->n + 255) / 256, 64));
-  k_update<<<ub, 256, 0, s>>>(q);
-  count_launch();
-  ITSK_CHECK_LAUNCH();
-  int grid = 0;
-  int rc = launch_pass(pass_args(p, q, 1), s, &grid);
-  if (rc) return rc;
-  return launch_finalize(q.part, grid, p->n, p->cs, q.ctl, s);
+  return ITSK_OK;
 }
 
 int prepare_attrs(int64_t n) {
   (void)n;
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_step_trsv<true>)));
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_step_trsv<false>)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_tail<true>)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_tail<false>)));
   return ITSK_OK;
 }
 
@@ -324,6 +374,14 @@ struct GraphHandle {
 }  // namespace itsk
 
 using namespace itsk;
+
+#ifdef ITSK_TAIL_PROBE
+extern "C" void itsk_tail_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_tail_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(itsk::g_tail_prof, z, sizeof(z));
+}
+#endif
 
 extern "C" int itsk_loop_workspace(int64_t m, int64_t n, int64_t* bytes) {
   ITSK_REQUIRE(bytes && m >= 1 && n >= 1, "bad loop shape");
@@ -348,46 +406,55 @@ extern "C" int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t st
                               p->u, p->gamma, p->rho, p->truth_beta);
   count_launch();
   ITSK_CHECK_LAUNCH();
+  if ((rc = reset_tickets(p, s))) return rc;
   int grid = 0;
-  rc = launch_pass(pass_args(p, q, 2), s, &grid);
-  if (rc) return rc;
-  return launch_finalize(q.part, grid, p->n, p->cs, q.ctl, s);
+  return launch_pass(pass_args(p, q, 2), s, &grid);
 }
 
 extern "C" int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream) {
   int rc = check_params(p);
   if (rc) return rc;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = prepare_attrs(p->n))) return rc;
   LoopPtrs q = make_ptrs(p);
-  k_control<<<1, CTRL_THREADS, 0, s>>>(q, 1, cudaGraphConditionalHandle{}, 0);
-  count_launch();
-  ITSK_CHECK_LAUNCH();
-  return ITSK_OK;
+  return enqueue_tail(p, q, TAIL_CONTROL | TAIL_BEGIN | TAIL_STEP, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream) {
-  int rc = itsk_loop_begin_local(p, stream);
+  int rc = check_params(p);
   if (rc) return rc;
-  return itsk_loop_begin_finish(p, stream);
+  if ((rc = prepare_attrs(p->n))) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LoopPtrs q = make_ptrs(p);
+  k_loop_init<<<1, 1, 0, s>>>(q.ctl, p->m, p->n, p->max_iters, p->extra_iters, p->variant,
+                              p->r_slots, p->has_truth, p->x_true != nullptr, p->alpha, p->beta,
+                              p->u, p->gamma, p->rho, p->truth_beta);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  if ((rc = reset_tickets(p, s))) return rc;
+  int grid = 0;
+  rc = launch_pass(pass_args(p, q, 2), s, &grid);
+  if (rc) return rc;
+  return enqueue_tail(p, q, TAIL_CONTROL | TAIL_BEGIN | TAIL_STEP, grid, s);
 }
 
+// local half of an iteration: the pass over this rank's rows and its partial sums
 extern "C" int itsk_loop_step_pre(const itsk_loop_params* p, itsk_stream_t stream) {
   int rc = check_params(p);
   if (rc) return rc;
   if ((rc = prepare_attrs(p->n))) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   LoopPtrs q = make_ptrs(p);
-  return enqueue_pre(p, q, reinterpret_cast<cudaStream_t>(stream));
+  int grid = 0;
+  return launch_pass(pass_args(p, q, 1), s, &grid);
 }
 
+// replicated half: control step and the next iterate
 extern "C" int itsk_loop_step_post(const itsk_loop_params* p, itsk_stream_t stream) {
   int rc = check_params(p);
   if (rc) return rc;
+  if ((rc = prepare_attrs(p->n))) return rc;
   LoopPtrs q = make_ptrs(p);
-  k_control<<<1, CTRL_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      q, 0, cudaGraphConditionalHandle{}, 0);
-  count_launch();
-  ITSK_CHECK_LAUNCH();
-  return ITSK_OK;
+  return enqueue_tail(p, q, TAIL_CONTROL | TAIL_STEP, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t stream,
@@ -432,11 +499,9 @@ extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t s
     set_error("capture begin: %s", cudaGetErrorString(e));
     return fail(ITSK_ECUDA);
   }
-  rc = enqueue_pre(p, q, cap);
-  if (rc == ITSK_OK) {
-    k_control<<<1, CTRL_THREADS, 0, cap>>>(q, 0, cond, 1);
-    count_launch();
-  }
+  int grid = 0;
+  rc = launch_pass(pass_args(p, q, 1), cap, &grid);
+  if (rc == ITSK_OK) rc = enqueue_tail(p, q, TAIL_CONTROL | TAIL_STEP, grid, cap, cond, 1);
   cudaGraph_t captured = body;
   e = cudaStreamEndCapture(cap, &captured);
   if (rc != ITSK_OK) return fail(rc);

@@ -164,6 +164,47 @@ struct TmaShape {
 // 0..UNR-1 prefetch b / r_prev / r_true of the warp's batch two steps ahead
 // with ordinary loads.  stage_tile[s] names the tile a stage holds, so a
 // consumer never waits on an mbarrier phase that aliases an older tile.
+// Two-level "last CTA" reduction of the per-CTA partials (see PassArgs):
+// the partial of this CTA is in a.part[blockIdx.x]; the last arriver of each
+// group sums its group in CTA order, the last group sums the groups in group
+// order, so the result does not depend on which CTA finishes last.
+__device__ void group_reduce(const PassArgs& a, int64_t n) {
+  __shared__ int s_last;
+  const int64_t w = n + 4;
+  const int G = a.group, gi = static_cast<int>(blockIdx.x) / G;
+  const int gsz = min(G, static_cast<int>(gridDim.x) - gi * G);
+  const int ng = (static_cast<int>(gridDim.x) + G - 1) / G;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[gi], 1u) == static_cast<unsigned>(gsz - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) a.tickets[gi] = 0;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < gsz; ++k) s += __ldcg(a.part + static_cast<int64_t>(gi * G + k) * w + c);
+    a.gpart[static_cast<int64_t>(gi) * w + c] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[ng], 1u) == static_cast<unsigned>(ng - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) a.tickets[ng] = 0;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0;
+    int g = 0;
+    for (; g + 1 < ng; g += 2) {
+      s0 += __ldcg(a.gpart + static_cast<int64_t>(g) * w + c);
+      s1 += __ldcg(a.gpart + static_cast<int64_t>(g + 1) * w + c);
+    }
+    if (g < ng) s0 += __ldcg(a.gpart + static_cast<int64_t>(g) * w + c);
+    a.cs[c] = s0 + s1;
+  }
+}
+
 template <int CPL, int UNR, int NCW>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaShape sh) {
   constexpr int THREADS = 32 * (NCW + 1);
@@ -354,6 +395,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
     for (int w = 0; w < NCW; ++w) sum += ssm[w][tid];
     out[n + tid] = sum;
   }
+  if (a.tickets) group_reduce(a, n);
 }
 
 // Fixed-order reduction of the per-CTA partials: one warp per output, lanes
@@ -534,21 +576,33 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
     }
   }
   PassArgs a = a0;
+  a.tickets = nullptr;  // the LDG variant leaves partials: finalize below when asked
   const int grid = pass_grid_v1(a.m, a.n);
   *grid_used = grid;
   a.rows_per_cta = (a.m + grid - 1) / grid;
+  int rc;
   switch (cpl_for(a.n)) {
-    case 1: return launch_cpl<1>(a, grid, s);
-    case 2: return launch_cpl<2>(a, grid, s);
-    case 4: return launch_cpl<4>(a, grid, s);
-    case 8: return launch_cpl<8>(a, grid, s);
-    case 16: return launch_cpl<16>(a, grid, s);
-    case 32: return launch_cpl<32>(a, grid, s);
+    case 1: rc = launch_cpl<1>(a, grid, s); break;
+    case 2: rc = launch_cpl<2>(a, grid, s); break;
+    case 4: rc = launch_cpl<4>(a, grid, s); break;
+    case 8: rc = launch_cpl<8>(a, grid, s); break;
+    case 16: rc = launch_cpl<16>(a, grid, s); break;
+    case 32: rc = launch_cpl<32>(a, grid, s); break;
     default:
       set_error("fused pass: n=%lld with an odd leading dimension exceeds the register-resident "
                 "row limit (1024)", (long long)a.n);
       return ITSK_EINVAL;
   }
+  if (rc == ITSK_OK && a0.tickets) rc = launch_finalize(a0.part, grid, a0.n, a0.cs, a0.ctl, s);
+  return rc;
+}
+
+int pass_groups(int64_t m, int64_t n, int* group) {
+  const int grid = pass_grid(m, n);
+  int G = 1;
+  while (G * G < grid) ++G;  // ~sqrt(grid): both levels read ~G partials per column
+  if (group) *group = G;
+  return (grid + G - 1) / G;
 }
 
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,

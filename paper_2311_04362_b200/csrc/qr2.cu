@@ -415,8 +415,16 @@ __global__ void __launch_bounds__(256) k_qr_z(UpdArgs a) {
   for (int idx = tid; idx < NB * UT; idx += 256) {
     const int i = idx / UT, c = idx - i * UT;
     double s = 0.0;
-    if (i < a.kb && c < cw)
-      for (int sp = 0; sp < a.S; ++sp) s += a.Yp[(static_cast<int64_t>(sp) * NB + i) * a.ldy + cb + c];
+    if (i < a.kb && c < cw) {
+      // all S partial loads in flight at once, summed in split order
+      const double* yp = a.Yp + static_cast<int64_t>(i) * a.ldy + cb + c;
+      const int64_t stride = static_cast<int64_t>(NB) * a.ldy;
+      double v[MAX_SPLIT];
+#pragma unroll
+      for (int sp = 0; sp < MAX_SPLIT; ++sp) v[sp] = sp < a.S ? yp[sp * stride] : 0.0;
+#pragma unroll
+      for (int sp = 0; sp < MAX_SPLIT; ++sp) s += v[sp];
+    }
     Ys[i][c] = s;
   }
   for (int idx = tid; idx < NB * NB; idx += 256) Gs[idx / NB][idx % NB] = a.G[idx];

@@ -269,8 +269,15 @@ __global__ void __launch_bounds__(32) k_invert_diag(const double* __restrict__ R
   const int B = blockIdx.x, lane = threadIdx.x;
   const int b0 = 32 * B, bs = min(32, n - b0);
   __shared__ double D[32][33];
-  for (int k = 0; k < 32; ++k)
-    D[k][lane] = (k < bs && lane < bs && lane >= k) ? R[static_cast<int64_t>(b0 + k) * n + b0 + lane] : 0.0;
+  __shared__ double rinv[32];
+  double dv[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k)  // all 32 loads in flight
+    dv[k] = (k < bs && lane < bs && lane >= k) ? R[static_cast<int64_t>(b0 + k) * n + b0 + lane] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) D[k][lane] = dv[k];
+  __syncwarp();
+  rinv[lane] = lane < bs ? 1.0 / D[lane][lane] : 0.0;
   __syncwarp();
   double x[32];
 #pragma unroll
@@ -279,13 +286,15 @@ __global__ void __launch_bounds__(32) k_invert_diag(const double* __restrict__ R
 #pragma unroll
     for (int k = 31; k >= 0; --k) {
       if (k == lane) {
-        x[k] = 1.0 / D[k][k];
+        x[k] = rinv[k];
       } else if (k < lane) {
-        double s = 0.0;
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int l = k + 1; l < 32; ++l)
-          if (l <= lane) s = fma(D[k][l], x[l], s);
-        x[k] = -s / D[k][k];
+          if (l <= lane) {
+            if (l & 1) s1 = fma(D[k][l], x[l], s1); else s0 = fma(D[k][l], x[l], s0);
+          }
+        x[k] = -(s0 + s1) * rinv[k];
       }
     }
   }
