@@ -435,7 +435,7 @@ def run_b200(args):
                                     "skipped": "host RAM below 2x A for the pinned copy"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-                         "kernel": "k_pass (fused r=b-Ax, c=A'r) + k_finalize",
+                         "kernel": "k_pass_tma (fused r=b-Ax, c=A'r, norms, in-kernel partial reduction)",
                          "bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms},
             "gpu_launches": int(launches),
             "iterations": iters, "stop_reason": res.trace.stop_reason, "fe": fe,

@@ -625,9 +625,31 @@ int launch_finalize(const double* part, int grid, int64_t n, double* cs, const L
 
 using namespace itsk;
 
+namespace {
+// workspace of the stand-alone pass: partials | group partials | tickets
+struct PassWs {
+  double* part;
+  double* gpart;
+  unsigned* tickets;
+  int ntickets, group;
+  int64_t bytes;
+};
+PassWs pass_ws(void* ws, int64_t m, int64_t n) {
+  Carver cv(ws, 1ll << 62);
+  PassWs w;
+  w.part = cv.take<double>(pass_part_doubles(m, n));
+  const int ng = pass_groups(m, n, &w.group);
+  w.gpart = cv.take<double>(static_cast<int64_t>(ng) * (n + 4));
+  w.ntickets = ng + 1;
+  w.tickets = cv.take<unsigned>(w.ntickets);
+  w.bytes = cv.off + 256;
+  return w;
+}
+}  // namespace
+
 extern "C" int itsk_pass_workspace(int64_t m, int64_t n, int64_t* bytes) {
   ITSK_REQUIRE(bytes && m >= 1 && n >= 1, "bad pass shape");
-  *bytes = pass_part_doubles(m, n) * static_cast<int64_t>(sizeof(double)) + 256;
+  *bytes = pass_ws(nullptr, m, n).bytes;
   return ITSK_OK;
 }
 
@@ -637,7 +659,8 @@ extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t ld
                                itsk_stream_t stream) {
   ITSK_REQUIRE(A && b && x && cs && ws, "null pointer");
   ITSK_REQUIRE(m >= 1 && n >= 1 && lda >= n, "bad pass shape");
-  ITSK_REQUIRE(pass_part_doubles(m, n) * 8 <= ws_bytes, "pass workspace too small");
+  const PassWs w = pass_ws(ws, m, n);
+  ITSK_REQUIRE(w.bytes <= ws_bytes, "pass workspace too small");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   PassArgs a{};
   a.A = A;
@@ -649,10 +672,15 @@ extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t ld
   a.r_prev = r_prev;
   a.r_out = r_out;
   a.r_true = r_true;
-  a.part = static_cast<double*>(ws);
+  a.part = w.part;
   a.mode = 0;
+  // the same in-kernel reduction as the loop; the caller's workspace is not
+  // known to be zeroed, so the 4-byte counters are reset here
+  a.tickets = w.tickets;
+  a.gpart = w.gpart;
+  a.cs = cs;
+  a.group = w.group;
+  ITSK_CUDA(cudaMemsetAsync(w.tickets, 0, sizeof(unsigned) * w.ntickets, s));
   int grid = 0;
-  int rc = launch_pass(a, s, &grid);
-  if (rc) return rc;
-  return launch_finalize(a.part, grid, n, cs, nullptr, s);
+  return launch_pass(a, s, &grid);
 }

@@ -66,6 +66,28 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Distributed-shared-memory transactions: a remote 8-byte store that
+// completes `bytes` on the destination CTA's mbarrier (no cluster barrier).
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // V(r, c) of the panel starting at row k0: unit lower trapezoidal.
 __device__ __forceinline__ double vval(double stored, int64_t r, int64_t k0, int c) {
   const int64_t jr = k0 + c;
@@ -114,7 +136,13 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   double* taus = red + QP_WARPS * NB;
   double* betl = taus + NB;
   __shared__ int bnd[MAX_C + 1];  // row split of [k0, d) relative to k0 (no 64-bit divides later)
+  __shared__ __align__(8) uint64_t mb[2];  // record arrivals, one mbarrier per inbox parity
   if (tid <= C) bnd[tid] = static_cast<int>(lo_of(tid, C, len));
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int cl_lane = lane < NB ? lane : NB - 1;  // NB = 16: upper half-warp mirrors
 
   for (int idx = tid; idx < h * NB; idx += QP_THREADS) {
@@ -137,6 +165,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     const bool l_st = lane < NB;
     const int jsrc = jn < NB ? jn : 0;
     const int jcol = jj < 0 ? 0 : jj;
+    double p0 = 0.0, p1 = 0.0;
     // rows j and j+1: updated, not part of the next column's sums
     if (apply) {
 #pragma unroll
@@ -155,7 +184,6 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     // bulk rows r > j+1 owned by this warp (rr = warp mod QP_WARPS)
     const int start = jnl + 1 > 0 ? jnl + 1 : 0;
     int rr = start + ((warp - start) & (QP_WARPS - 1));
-    double p0 = 0.0, p1 = 0.0;
     if (apply) {
       for (; rr + 3 * QP_WARPS < h; rr += 4 * QP_WARPS) {
         double v[4], x[4];
@@ -204,8 +232,10 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     if (lane < NB) red[warp * NB + lane] = p0 + p1;
     __syncthreads();
     Q2P(1);
+    const int buf = jn & 1;
+    if (tid == 0)  // this CTA expects C records of (kb - jn) sums plus the owner's row
+      mbar_expect_tx(&mb[buf], static_cast<unsigned>((C + 1) * (kb - jn) * 8));
     if (warp < C) {  // warp w delivers this CTA's record to CTA w
-      const int buf = jn & 1;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (lane < kb) {
 #pragma unroll
@@ -219,51 +249,63 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
       const int64_t jrn = k0 + jn;
       const bool own_next = jrn >= lo && jrn < hi;
       if (lane >= jn && lane < kb) {
-        double* ib = cl.map_shared_rank(inbox, warp) + (buf * C + q) * REC;
-        ib[lane] = (s0 + s1) + (s2 + s3);
-        if (own_next) ib[NB + lane] = Ps[(jrn - lo) * PS + lane];
+        const uint32_t ib = mapa_u32(smem_u32(inbox + (buf * C + q) * REC + lane), warp);
+        const uint32_t rb = mapa_u32(smem_u32(&mb[buf]), warp);
+        st_async_f64(ib, (s0 + s1) + (s2 + s3), rb);
+        if (own_next) st_async_f64(ib + NB * 8, Ps[(jrn - lo) * PS + lane], rb);
       }
     }
     Q2P(2);
-    cl.sync();
+    mbar_wait_cluster(&mb[buf], static_cast<unsigned>((jn >> 1) & 1));
     Q2P(3);
   };
 
-  __syncthreads();  // bnd
+  cl.sync();  // bnd, and every CTA's mbarriers initialised before any remote transaction
   sweep(-1, false, 0.0, 0.0);  // partial sums of column 0
   int own = 0;
   for (int jj = 0; jj < kb; ++jj) {
     const int buf = jj & 1;
     while (own + 1 < C && bnd[own + 1] <= jj) ++own;  // owner of row k0 + jj
-    // every warp forms the same dlarfg coefficients from the inbox (fixed order)
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
-    const double* ib = inbox + buf * C * REC + cl_lane;
+    // warp 0 forms the dlarfg coefficients from the inbox (fixed order) and
+    // publishes tau, scal and temp_c; the other warps wait at the barrier
+    // (sixteen redundant copies of the sqrt/divide chain were slower)
+    __shared__ double s_coef[2];
+    __shared__ double s_temp[32];
+    if (warp == 0) {
+      double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
+      const double* ib = inbox + buf * C * REC + cl_lane;
 #pragma unroll
-    for (int t = 0; t < MAX_C; t += 4) {
-      if (t < C) S0 += ib[t * REC];
-      if (t + 1 < C) S1 += ib[(t + 1) * REC];
-      if (t + 2 < C) S2 += ib[(t + 2) * REC];
-      if (t + 3 < C) S3 += ib[(t + 3) * REC];
+      for (int t = 0; t < MAX_C; t += 4) {
+        if (t < C) S0 += ib[t * REC];
+        if (t + 1 < C) S1 += ib[(t + 1) * REC];
+        if (t + 2 < C) S2 += ib[(t + 2) * REC];
+        if (t + 3 < C) S3 += ib[(t + 3) * REC];
+      }
+      const double S = (S0 + S1) + (S2 + S3);
+      const double arow = ib[own * REC + NB];
+      const double xn2 = __shfl_sync(FULL, S, jj);
+      const double alpha = __shfl_sync(FULL, arow, jj);
+      double beta, tau, scal;
+      if (xn2 == 0.0) {  // dlarfg: H = I
+        tau = 0.0;
+        beta = alpha;
+        scal = 1.0;
+      } else {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      s_temp[lane] = (lane > jj && lane < kb) ? -tau * (arow + scal * S) : 0.0;
+      if (lane == 0) {
+        taus[jj] = tau;
+        betl[jj] = beta;
+        s_coef[0] = tau;
+        s_coef[1] = scal;
+      }
     }
-    const double S = (S0 + S1) + (S2 + S3);
-    const double arow = ib[own * REC + NB];
-    const double xn2 = __shfl_sync(FULL, S, jj);
-    const double alpha = __shfl_sync(FULL, arow, jj);
-    double beta, tau, scal;
-    if (xn2 == 0.0) {  // dlarfg: H = I
-      tau = 0.0;
-      beta = alpha;
-      scal = 1.0;
-    } else {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (tid == 0) {
-      taus[jj] = tau;
-      betl[jj] = beta;
-    }
-    const double temp = (lane > jj && lane < kb) ? -tau * (arow + scal * S) : 0.0;
+    __syncthreads();
+    const double tau = s_coef[0], scal = s_coef[1];
+    const double temp = s_temp[lane];
     Q2P(4);
     sweep(jj, tau != 0.0, scal, temp);
   }
@@ -501,6 +543,16 @@ __global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, 
   }
 }
 
+// kernel-argument array for cudaLaunchKernelExC (one by-value struct)
+struct ArgPack {
+  void* p[1];
+};
+inline void** args_of(PanelArgs& pa) {
+  static thread_local ArgPack ap;
+  ap.p[0] = &pa;
+  return ap.p;
+}
+
 size_t y_smem(int nb) { return static_cast<size_t>(2 * YRT * (nb + 1) + 2 * YRT * (UT + 1)) * 8; }
 
 }  // namespace
@@ -568,10 +620,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (P.NB == 32)
-      ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_qr_panel<32>, pa));
-    else
-      ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_qr_panel<16>, pa));
+    ITSK_CUDA(cudaLaunchKernelExC(&cfg, kp, args_of(pa)));
     count_launch();
     const int64_t c0 = k0 + kb, Nt = N - c0;
     if (Nt <= 0) continue;
