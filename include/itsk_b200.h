@@ -147,6 +147,13 @@ int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t lda, const do
                     const double* x, const double* r_prev, double* r_out,
                     const double* r_true, double* cs, void* ws, int64_t ws_bytes,
                     itsk_stream_t stream);
+/* The same pass with r = bscale * b - A x: one LSQR bidiagonalisation step
+ * beta' u' = A R^{-1} v - alpha u in one sweep over A (b = beta u, x = -R^{-1} v,
+ * bscale = -alpha / beta), c = A' (beta' u') alongside (solvers.py:455-461). */
+int itsk_fused_pass_scaled(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                           double bscale, const double* x, const double* r_prev, double* r_out,
+                           const double* r_true, double* cs, void* ws, int64_t ws_bytes,
+                           itsk_stream_t stream);
 
 /* ----------------------------------------------------------------------
  * Device-resident refinement loop (_run_refinement, solvers.py:270-320).

@@ -16,6 +16,7 @@ from .linalg import (
     tri_solve_upper,
     tri_solve_upper_transpose,
 )
+from .lsqr import lsqr, sketch_and_precondition
 from .problems import LsProblem, Truth, gen_randsvd
 from .solvers import (
     SolveResult,
@@ -34,5 +35,5 @@ __all__ = [
     "QrFactors", "cond_est", "householder_qr_econ", "rand_power_norm_est", "tri_solve_upper",
     "tri_solve_upper_transpose", "LsProblem", "Truth", "gen_randsvd", "SolveResult", "SolverConfig",
     "SolveTrace", "damping_params", "iterative_sketching", "momentum_params", "release_workspaces",
-    "should_stop", "sketch_and_solve",
+    "should_stop", "sketch_and_solve", "lsqr", "sketch_and_precondition",
 ]

@@ -79,6 +79,8 @@ _SIGS = {
     "itsk_pass_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_fused_pass": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp,
                                        c_dp, c_i64, c_dp]),
+    "itsk_fused_pass_scaled": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.c_double, c_dp, c_dp,
+                                              c_dp, c_dp, c_dp, c_dp, c_i64, c_dp]),
     "itsk_loop_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_loop_begin": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
     "itsk_loop_begin_local": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),

@@ -71,6 +71,7 @@ struct PassArgs {
   double* gpart;      // ceil(grid / group) x (n + 4)
   double* cs;         // n + 4
   int group;
+  double bscale = 1.0;  // r = bscale * b - A x (LSQR: u_{k+1} beta = A y - alpha u_k)
 };
 
 // counters / group partials needed by the in-kernel reduction of a pass

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(PassArgs a) {
         dot = fma(av[u][q], XREG ? xv[XREG ? q : 0] : xsm[lane + 32 * q], dot);
       dot = warp_sum(dot);
       const double bj = b[row];
-      const double r = bj - dot;
+      const double r = (a.bscale == 1.0 ? bj : a.bscale * bj) - dot;
 #pragma unroll
       for (int q = 0; q < CPL; ++q) acc[q] = fma(r, av[u][q], acc[q]);
       if (lane == 0) {
@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
   }
   const double* r_true = a.r_true;
   const double* b = a.b;
+  const double bscale = a.bscale;  // 1.0 except in LSQR's bidiagonalisation
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n, lda = a.lda;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
         for (int u = 0; u < UNR; ++u) dot[u] += __shfl_xor_sync(FULL, dot[u], o);
       double r[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) r[u] = __shfl_sync(FULL, cb, u) - dot[u];
+      for (int u = 0; u < UNR; ++u) r[u] = bscale * __shfl_sync(FULL, cb, u) - dot[u];
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const int c = lane + 32 * q;
@@ -657,6 +658,13 @@ extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t ld
                                const double* x, const double* r_prev, double* r_out,
                                const double* r_true, double* cs, void* ws, int64_t ws_bytes,
                                itsk_stream_t stream) {
+  return itsk_fused_pass_scaled(A, m, n, lda, b, 1.0, x, r_prev, r_out, r_true, cs, ws, ws_bytes, stream);
+}
+
+extern "C" int itsk_fused_pass_scaled(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                                      double bscale, const double* x, const double* r_prev, double* r_out,
+                                      const double* r_true, double* cs, void* ws, int64_t ws_bytes,
+                                      itsk_stream_t stream) {
   ITSK_REQUIRE(A && b && x && cs && ws, "null pointer");
   ITSK_REQUIRE(m >= 1 && n >= 1 && lda >= n, "bad pass shape");
   const PassWs w = pass_ws(ws, m, n);
@@ -674,6 +682,7 @@ extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t ld
   a.r_true = r_true;
   a.part = w.part;
   a.mode = 0;
+  a.bscale = bscale;
   // the same in-kernel reduction as the loop; the caller's workspace is not
   // known to be zeroed, so the 4-byte counters are reset here
   a.tickets = w.tickets;

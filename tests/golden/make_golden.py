@@ -19,6 +19,8 @@ $ITSKETCH_REF) and records its outputs on seeded inputs:
                   zero init, extra_iters, consistent systems, track_be and a
                   diverging configuration.
   linalg.npz    — householder_qr_econ R factors, normest / condest values.
+  lsqr.npz      — sketch_and_precondition traces (solvers.py:485-525) and
+                  lsqr (solvers.py:411-482) solutions / iteration counts.
 """
 
 from __future__ import annotations
@@ -36,7 +38,7 @@ sys.path.insert(0, REF)
 from itsketch.embed import sparse_sign_new  # noqa: E402
 from itsketch.linalg import cond_est, householder_qr_econ, rand_power_norm_est  # noqa: E402
 from itsketch.problems import gen_randsvd  # noqa: E402
-from itsketch.solvers import SolverConfig, iterative_sketching  # noqa: E402
+from itsketch.solvers import SolverConfig, iterative_sketching, lsqr, sketch_and_precondition  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -176,7 +178,64 @@ def make_linalg():
     np.savez_compressed(os.path.join(HERE, "linalg.npz"), **out)
 
 
+SAP_CASES = [
+    # name, (m, n, kappa, beta, seed), SolverConfig kwargs
+    ("sap_hard", (4000, 50, 1e10, 1e-6, 0), dict(d=1000, max_iters=60)),
+    ("sap_zero", (4000, 50, 1e10, 1e-6, 0), dict(d=1000, init="zero", max_iters=60)),
+    ("sap_consistent", (400, 15, 1e4, 0.0, 0), dict(d=300, max_iters=50)),
+    ("sap_consistent_zero", (400, 15, 1e4, 0.0, 0), dict(d=300, init="zero", max_iters=50)),
+    ("sap_small", (300, 10, 1e2, 1e-3, 1), dict(d=200, max_iters=30)),
+    ("sap_c3like", (4000, 50, 1e15, 1e-3, 1), dict(d=1000, max_iters=100, rng_seed=1)),
+    ("sap_maxit", (4000, 50, 1e10, 1e-6, 2), dict(d=1000, max_iters=5, rng_seed=2)),
+]
+
+
+def make_lsqr():
+    out = {}
+    names = []
+    for name, (m, n, kappa, beta, seed), kw in SAP_CASES:
+        p = gen_randsvd(m, n, kappa, beta, seed)
+        res = sketch_and_precondition(p.a, p.b, SolverConfig(**kw), p.truth)
+        tr = res.trace
+        out[f"{name}_problem"] = np.array([m, n, kappa, beta, seed], dtype=np.float64)
+        out[f"{name}_config"] = np.array(json.dumps(kw))
+        out[f"{name}_iterates"] = np.array(tr.iterates)
+        out[f"{name}_fe"] = np.array(tr.fe)
+        out[f"{name}_re"] = np.array(tr.re)
+        out[f"{name}_changes"] = np.array(tr.residual_changes)
+        out[f"{name}_stop"] = np.array(tr.stop_reason)
+        out[f"{name}_normest"] = np.array(tr.normest)
+        out[f"{name}_condest"] = np.array(tr.condest)
+        out[f"{name}_solution"] = res.solution
+        names.append(name)
+        print(f"{name}: iters={res.iterations} stop={tr.stop_reason} fe={tr.fe[-1]:.3e}")
+    out["names"] = np.array(names)
+    # lsqr with the exact QR preconditioner on Gaussian problems (acceptance C10)
+    for seed in range(5):
+        rng = np.random.default_rng(seed)
+        a = rng.standard_normal((200, 20))
+        b = rng.standard_normal(200)
+        r_fac = householder_qr_econ(a).r
+        x, iters = lsqr(a, b, np.zeros(20), r_fac, max_iters=3)
+        out[f"c10_{seed}_a"], out[f"c10_{seed}_b"], out[f"c10_{seed}_r"] = a, b, r_fac
+        out[f"c10_{seed}_x"], out[f"c10_{seed}_iters"] = x, np.array(iters)
+    # lsqr with a sketched preconditioner (test_sketch_preconditioner_matches_dense)
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((200, 20))
+    b = rng.standard_normal(200)
+    r_fac = householder_qr_econ(sparse_sign_new(100, 200, 8, 2).apply_dense(a)).r
+    x, iters = lsqr(a, b, np.zeros(20), r_fac, max_iters=100)
+    out["sk_a"], out["sk_b"], out["sk_r"], out["sk_x"], out["sk_iters"] = a, b, r_fac, x, np.array(iters)
+    np.savez_compressed(os.path.join(HERE, "lsqr.npz"), **out)
+
+
 if __name__ == "__main__":
-    make_patterns()
-    make_linalg()
-    make_solves()
+    which = sys.argv[1:] or ["patterns", "linalg", "solves", "lsqr"]
+    if "patterns" in which:
+        make_patterns()
+    if "linalg" in which:
+        make_linalg()
+    if "solves" in which:
+        make_solves()
+    if "lsqr" in which:
+        make_lsqr()
