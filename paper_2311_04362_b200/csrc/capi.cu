@@ -1,5 +1,6 @@
 // Process-level pieces of the C ABI: error strings, version, device check,
 // launch counter.
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <unordered_set>
@@ -37,6 +38,14 @@ cudaError_t allow_max_smem(const void* func) {
                              optin - static_cast<int>(fa.sharedSizeBytes));
   if (e == cudaSuccess) done.insert(func);
   return e;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ITSK_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
 }
 
 int num_sms() {

@@ -108,6 +108,33 @@ __device__ __forceinline__ double ldg_stream(const double* p, uint64_t pol) {
   return v;
 }
 
+// ---- programmatic dependent launch ----
+// griddepcontrol.wait: block until the preceding kernel in the stream has
+// completed and its memory is visible; launch_dependents: let the next kernel
+// start its prologue.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch `func` with programmatic stream serialisation allowed (kernels that
+// call pdl_wait() before touching their predecessor's output).  ITSK_NO_PDL=1
+// launches without the attribute.
+bool pdl_enabled();
+template <class... Args>
+cudaError_t launch_pdl(const void* func, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  void* ptrs[] = {static_cast<void*>(&args)...};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, func, ptrs);
+}
+
 // ---- mbarrier + 1D bulk copy (TMA) helpers ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -39,6 +39,7 @@ struct LoopPtrs {
   double* part;  // pass partials
   LoopCtl* ctl;
   int64_t lda;
+  int64_t n;
   int rp_inv;  // Rp carries the diagonal-block inverses and the TRSV kernel stages them
 };
 

@@ -177,6 +177,18 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   long long _tp = clock64();
   if (threadIdx.x == 0) atomicAdd(&g_tail_prof[15], 1ull);
 #endif
+  // Programmatic dependent launch: let the next pass start streaming A, and
+  // stage R (written long before) while the preceding pass finishes; the
+  // pass's outputs and the loop state are read after griddepcontrol.wait.
+  pdl_trigger();
+  extern __shared__ double sm[];
+  const int64_t n = p.n;
+  double* v = sm;
+  if (PACKED && (flags & TAIL_STEP)) {
+    if (p.Rp) stage_packed_bulk(p.Rp, n, sm, p.rp_inv != 0); else stage_packed(p.R, n, sm);
+    v = sm + (p.rp_inv ? rp_doubles(n) : packed_doubles(n));
+  }
+  pdl_wait();
   // the loop state in shared memory: the control step's scalar bookkeeping
   // would otherwise be a chain of dependent L2 round trips
   constexpr int CTL_WORDS = sizeof(LoopCtl) / 8;
@@ -191,7 +203,6 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
     return;
   }
-  const int64_t n = ctl->n;
   if (flags & TAIL_CONTROL) {
     const int done = control_step(p, ctl, (flags & TAIL_BEGIN) ? 1 : 0);
     TP(2);
@@ -203,15 +214,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     }
   }
   if (!(flags & TAIL_STEP)) return;
-  // d = R^{-1} R^{-T} c in shared memory, then x_{it+1}
-  extern __shared__ double sm[];
-  double* v;
-  if (PACKED) {
-    if (p.Rp) stage_packed_bulk(p.Rp, n, sm, p.rp_inv != 0); else stage_packed(p.R, n, sm);
-    v = sm + (p.rp_inv ? rp_doubles(n) : packed_doubles(n));
-  } else {
-    v = sm;
-  }
+  // d = R^{-1} R^{-T} c in shared memory (R staged above), then x_{it+1}
   __shared__ double red_s[64 * (DENSE_THREADS / 32)];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   __syncthreads();
@@ -306,6 +309,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.part = L.part;
   q.ctl = L.ctl;
   q.lda = p->lda;
+  q.n = p->n;
   q.rp_inv = (p->Rp != nullptr && use_packed_inv(p->n, p->n + 32)) ? 1 : 0;
   return q;
 }
@@ -349,10 +353,9 @@ size_t trsv_smem(int64_t n) {
 int enqueue_tail(const itsk_loop_params* p, const LoopPtrs& q, int flags, int grid, cudaStream_t s,
                  cudaGraphConditionalHandle cond = cudaGraphConditionalHandle{}, int use_cond = 0) {
   const size_t smem = (flags & TAIL_STEP) ? trsv_smem(p->n) : 0;
-  if (trsv_packed(p->n))
-    k_tail<true><<<1, DENSE_THREADS, smem, s>>>(q, flags, grid, cond, use_cond);
-  else
-    k_tail<false><<<1, DENSE_THREADS, smem, s>>>(q, flags, grid, cond, use_cond);
+  const void* fn = trsv_packed(p->n) ? reinterpret_cast<const void*>(k_tail<true>)
+                                     : reinterpret_cast<const void*>(k_tail<false>);
+  ITSK_CUDA(launch_pdl(fn, dim3(1), dim3(DENSE_THREADS), smem, s, q, flags, grid, cond, use_cond));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;

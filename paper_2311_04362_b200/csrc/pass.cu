@@ -217,6 +217,46 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
   double* xsm = reinterpret_cast<double*>(smraw + 1024);
   unsigned char* stages = smraw + 1024 + (XREG ? 0 : NC * 8);
   __shared__ double ssm[NCW][4];
+  __shared__ int s_done;
+
+  const double* r_true = a.r_true;
+  const double* b = a.b;
+  const double bscale = a.bscale;  // 1.0 except in LSQR's bidiagonalisation
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n, lda = a.lda;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
+  const int T = sh.T, S = sh.S;
+  const int ntiles = (nrows + T - 1) / T;
+  const int npre = min(S, ntiles);  // tiles issued before the dependency wait
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, T / UNR);  // one arrival per consumed batch
+      stage_tile[s] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // Programmatic dependent launch: A does not depend on the previous kernel,
+  // so the producer fills the ring while that kernel (the loop tail) still
+  // runs; everything the previous kernel writes (x, the loop state) is read
+  // after griddepcontrol.wait.
+  pdl_trigger();
+  if (warp == NCW && lane == 0) {
+    const uint64_t pol = evict_first_policy();
+    for (int t = 0; t < npre; ++t) {
+      const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
+      const int rows = min(T, nrows - t * T);
+      const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+      reinterpret_cast<volatile int*>(stage_tile)[t] = t;
+      mbar_expect_tx(full + t, bytes);
+      bulk_g2s(stages + static_cast<int64_t>(t) * sh.stage_bytes, a.A + row0 * lda, bytes, full + t, pol);
+    }
+  }
+  pdl_wait();
 
   const double* x;
   const double* r_prev;
@@ -227,7 +267,14 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
     r_out = a.r_out;
   } else {
     const LoopCtl* ctl = a.ctl;
-    if (ctl->result.done) return;
+    if (tid == 0) s_done = ctl->result.done;
+    __syncthreads();
+    if (s_done) {
+      // loop finished: drain the prefetched copies before the CTA exits
+      if (warp == NCW && lane == 0)
+        for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
+      return;
+    }
     const int64_t S = ctl->r_slots;
     if (a.mode == 1) {
       const int64_t it = ctl->it;
@@ -239,25 +286,6 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
       r_prev = nullptr;
       r_out = a.rs;
     }
-  }
-  const double* r_true = a.r_true;
-  const double* b = a.b;
-  const double bscale = a.bscale;  // 1.0 except in LSQR's bidiagonalisation
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n = a.n, lda = a.lda;
-  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
-  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
-  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
-  const int T = sh.T, S = sh.S;
-  const int ntiles = (nrows + T - 1) / T;
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, T / UNR);  // one arrival per consumed batch
-      stage_tile[s] = -1;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!XREG)
     for (int c = tid; c < NC; c += THREADS) xsm[c] = (c < n) ? x[c] : 0.0;
@@ -271,7 +299,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
     // ---------------- producer: one elected lane, one bulk copy per tile ---
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = npre; t < ntiles; ++t) {
         const int s = t % S;
         if (t >= S) mbar_wait(empty + s, static_cast<unsigned>(((t / S) - 1) & 1));
         const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
@@ -515,7 +543,8 @@ int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
   a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
   const size_t smem = tma_smem(sh, CPL);
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>)));
-  k_pass_tma<CPL, UNR, NCW><<<grid, 32 * (NCW + 1), smem, s>>>(a, sh);
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>), dim3(grid), dim3(32 * (NCW + 1)),
+                       smem, s, a, sh));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
