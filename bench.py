@@ -289,10 +289,12 @@ def fused_pass_timing(lib, at, bt, x, n_launch=30):
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         sp = int(stream.cuda_stream)
+        _lib.check(lib.itsk_pass_workspace_init(dv.ptr(ws), m, n, sp))
 
         def launch():
-            _lib.check(lib.itsk_fused_pass(dv.ptr(at), m, n, int(at.stride(0)), dv.ptr(bt), dv.ptr(x), dv.ptr(r_prev),
-                                           dv.ptr(r_out), None, dv.ptr(cs), dv.ptr(ws), ws.numel(), sp))
+            _lib.check(lib.itsk_fused_pass_ex(dv.ptr(at), m, n, int(at.stride(0)), dv.ptr(bt), 1.0, dv.ptr(x),
+                                              dv.ptr(r_prev), dv.ptr(r_out), None, dv.ptr(cs), dv.ptr(ws),
+                                              ws.numel(), _lib.PASS_WS_READY, sp))
 
         for _ in range(5):
             launch()

@@ -155,6 +155,17 @@ int itsk_fused_pass_scaled(const double* A, int64_t m, int64_t n, int64_t lda, c
                            const double* r_true, double* cs, void* ws, int64_t ws_bytes,
                            itsk_stream_t stream);
 
+/* Pass flags.  ITSK_PASS_WS_READY: the workspace's reduction counters are
+ * zero — set by itsk_pass_workspace_init once, and left so by every pass that
+ * completes — so the per-call reset (a memset on the stream, which also stops
+ * a programmatic-dependent-launch overlap with the previous pass) is skipped. */
+#define ITSK_PASS_WS_READY 1u
+int itsk_pass_workspace_init(void* ws, int64_t m, int64_t n, itsk_stream_t stream);
+int itsk_fused_pass_ex(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                       double bscale, const double* x, const double* r_prev, double* r_out,
+                       const double* r_true, double* cs, void* ws, int64_t ws_bytes,
+                       unsigned flags, itsk_stream_t stream);
+
 /* ----------------------------------------------------------------------
  * Device-resident refinement loop (_run_refinement, solvers.py:270-320).
  * State, constants and trace live in device memory; the loop runs as one

@@ -81,6 +81,9 @@ _SIGS = {
                                        c_dp, c_i64, c_dp]),
     "itsk_fused_pass_scaled": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.c_double, c_dp, c_dp,
                                               c_dp, c_dp, c_dp, c_dp, c_i64, c_dp]),
+    "itsk_pass_workspace_init": (ctypes.c_int, [c_dp, c_i64, c_i64, c_dp]),
+    "itsk_fused_pass_ex": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.c_double, c_dp, c_dp,
+                                          c_dp, c_dp, c_dp, c_dp, c_i64, ctypes.c_uint, c_dp]),
     "itsk_loop_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_loop_begin": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
     "itsk_loop_begin_local": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
@@ -92,6 +95,8 @@ _SIGS = {
     "itsk_loop_graph_destroy": (None, [c_dp]),
     "itsk_loop_result_ptr": (ctypes.c_int, [ctypes.POINTER(LoopParams), ctypes.POINTER(c_dp)]),
 }
+
+PASS_WS_READY = 1  # include/itsk_b200.h ITSK_PASS_WS_READY
 
 _lock = threading.Lock()
 _lib = None

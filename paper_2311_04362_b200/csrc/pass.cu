@@ -167,7 +167,25 @@ struct TmaShape {
 // Two-level "last CTA" reduction of the per-CTA partials (see PassArgs):
 // the partial of this CTA is in a.part[blockIdx.x]; the last arriver of each
 // group sums its group in CTA order, the last group sums the groups in group
-// order, so the result does not depend on which CTA finishes last.
+// order, so the result does not depend on which CTA finishes last.  The
+// partials are L2 reads: each level issues a whole chunk of them before the
+// first add (RCH loads in flight per column) — a dependent load per partial
+// was ~12 serialised L2 round trips at 148 CTAs, most of the pass's fixed
+// cost at C2.  The adds keep the sequential order of the index.
+constexpr int RCH = 16;
+
+__device__ __forceinline__ double sum_strided(const double* p, int64_t stride, int cnt, double s) {
+  for (int k0 = 0; k0 < cnt; k0 += RCH) {
+    double v[RCH];
+#pragma unroll
+    for (int k = 0; k < RCH; ++k) v[k] = (k0 + k < cnt) ? __ldcg(p + (k0 + k) * stride) : 0.0;
+#pragma unroll
+    for (int k = 0; k < RCH; ++k)
+      if (k0 + k < cnt) s += v[k];
+  }
+  return s;
+}
+
 __device__ void group_reduce(const PassArgs& a, int64_t n) {
   __shared__ int s_last;
   const int64_t w = n + 4;
@@ -181,11 +199,8 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) a.tickets[gi] = 0;
-  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < gsz; ++k) s += __ldcg(a.part + static_cast<int64_t>(gi * G + k) * w + c);
-    a.gpart[static_cast<int64_t>(gi) * w + c] = s;
-  }
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x)
+    a.gpart[static_cast<int64_t>(gi) * w + c] = sum_strided(a.part + static_cast<int64_t>(gi) * G * w + c, w, gsz, 0.0);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[ng], 1u) == static_cast<unsigned>(ng - 1);
@@ -193,14 +208,11 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) a.tickets[ng] = 0;
+  // even groups into s0, odd groups into s1, then s0 + s1
+  const int ne = (ng + 1) / 2, no = ng / 2;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0;
-    int g = 0;
-    for (; g + 1 < ng; g += 2) {
-      s0 += __ldcg(a.gpart + static_cast<int64_t>(g) * w + c);
-      s1 += __ldcg(a.gpart + static_cast<int64_t>(g + 1) * w + c);
-    }
-    if (g < ng) s0 += __ldcg(a.gpart + static_cast<int64_t>(g) * w + c);
+    const double s0 = sum_strided(a.gpart + c, 2 * w, ne, 0.0);
+    const double s1 = sum_strided(a.gpart + w + c, 2 * w, no, 0.0);
     a.cs[c] = s0 + s1;
   }
 }
@@ -919,19 +931,34 @@ extern "C" int itsk_pass_workspace(int64_t m, int64_t n, int64_t* bytes) {
   return ITSK_OK;
 }
 
+extern "C" int itsk_pass_workspace_init(void* ws, int64_t m, int64_t n, itsk_stream_t stream) {
+  ITSK_REQUIRE(ws && m >= 1 && n >= 1, "bad pass shape");
+  const PassWs w = pass_ws(ws, m, n);
+  ITSK_CUDA(cudaMemsetAsync(w.tickets, 0, sizeof(unsigned) * w.ntickets, reinterpret_cast<cudaStream_t>(stream)));
+  return ITSK_OK;
+}
+
 extern "C" int itsk_fused_pass(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                                const double* x, const double* r_prev, double* r_out,
                                const double* r_true, double* cs, void* ws, int64_t ws_bytes,
                                itsk_stream_t stream) {
-  return itsk_fused_pass_scaled(A, m, n, lda, b, 1.0, x, r_prev, r_out, r_true, cs, ws, ws_bytes, stream);
+  return itsk_fused_pass_ex(A, m, n, lda, b, 1.0, x, r_prev, r_out, r_true, cs, ws, ws_bytes, 0u, stream);
 }
 
 extern "C" int itsk_fused_pass_scaled(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                                       double bscale, const double* x, const double* r_prev, double* r_out,
                                       const double* r_true, double* cs, void* ws, int64_t ws_bytes,
                                       itsk_stream_t stream) {
+  return itsk_fused_pass_ex(A, m, n, lda, b, bscale, x, r_prev, r_out, r_true, cs, ws, ws_bytes, 0u, stream);
+}
+
+extern "C" int itsk_fused_pass_ex(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                                  double bscale, const double* x, const double* r_prev, double* r_out,
+                                  const double* r_true, double* cs, void* ws, int64_t ws_bytes,
+                                  unsigned flags, itsk_stream_t stream) {
   ITSK_REQUIRE(A && b && x && cs && ws, "null pointer");
   ITSK_REQUIRE(m >= 1 && n >= 1 && lda >= n, "bad pass shape");
+  ITSK_REQUIRE((flags & ~ITSK_PASS_WS_READY) == 0, "unknown pass flags");
   const PassWs w = pass_ws(ws, m, n);
   ITSK_REQUIRE(w.bytes <= ws_bytes, "pass workspace too small");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -948,13 +975,14 @@ extern "C" int itsk_fused_pass_scaled(const double* A, int64_t m, int64_t n, int
   a.part = w.part;
   a.mode = 0;
   a.bscale = bscale;
-  // the same in-kernel reduction as the loop; the caller's workspace is not
-  // known to be zeroed, so the 4-byte counters are reset here
+  // the same in-kernel reduction as the loop; its counters reset themselves,
+  // so only a workspace not known to be initialised is cleared here
   a.tickets = w.tickets;
   a.gpart = w.gpart;
   a.cs = cs;
   a.group = w.group;
-  ITSK_CUDA(cudaMemsetAsync(w.tickets, 0, sizeof(unsigned) * w.ntickets, s));
+  if (!(flags & ITSK_PASS_WS_READY))
+    ITSK_CUDA(cudaMemsetAsync(w.tickets, 0, sizeof(unsigned) * w.ntickets, s));
   int grid = 0;
   return launch_pass(a, s, &grid);
 }

@@ -48,6 +48,8 @@ class _DeviceLs:
         nb = ctypes.c_int64()
         _lib.check(self.lib.itsk_pass_workspace(self.m, self.n, ctypes.byref(nb)))
         self.pws = _dev.workspace(nb.value, self.dev)
+        # counters zeroed once; every pass leaves them zero (ITSK_PASS_WS_READY)
+        _lib.check(self.lib.itsk_pass_workspace_init(_dev.ptr(self.pws), self.m, self.n, self.stream))
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.cs = torch.empty(self.n + 8, **f64)
         self.U = torch.empty((2, self.m), **f64)  # unnormalised u ring
@@ -68,11 +70,11 @@ class _DeviceLs:
         """r = bscale * b - A x into r_out, c = A'r; returns (c or None, [||r||^2,
         ||r - r_prev||^2, ||r - r_true||^2, ||b||^2])."""
         self.xd.copy_(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)))
-        _lib.check(self.lib.itsk_fused_pass_scaled(
+        _lib.check(self.lib.itsk_fused_pass_ex(
             _dev.ptr(self.at), self.m, self.n, self.lda, b_ptr, float(bscale), _dev.ptr(self.xd),
             _dev.ptr(r_prev) if r_prev is not None else None, _dev.ptr(r_out) if r_out is not None else None,
             _dev.ptr(r_true) if r_true is not None else None, _dev.ptr(self.cs), _dev.ptr(self.pws),
-            self.pws.numel(), self.stream))
+            self.pws.numel(), _lib.PASS_WS_READY, self.stream))
         if want_c:
             self.host.copy_(self.cs)
             h = self.host.numpy()

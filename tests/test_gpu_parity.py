@@ -264,6 +264,41 @@ def test_fused_pass_matches_numpy(pkg, m, n):
     assert got[n + 3] == pytest.approx(b @ b, rel=1e-12)
 
 
+@pytest.mark.parametrize("m,n", [(200000, 200), (40000, 2000), (5000, 50)])
+def test_fused_pass_ws_ready_is_bitwise_stable(pkg, m, n):
+    """itsk_pass_workspace_init once, then repeated itsk_fused_pass_ex with
+    ITSK_PASS_WS_READY (no per-call reset): every call returns the bytes of
+    the resetting entry point — the counters do reset themselves."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    dev = dv.current_device()
+    g = torch.Generator(device=dev).manual_seed(m + n)
+    a = torch.randn(m, n, dtype=torch.float64, device=dev, generator=g)
+    b = torch.randn(m, dtype=torch.float64, device=dev, generator=g)
+    x = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
+    lib = dv.lib(dev)
+    nb = ctypes.c_int64()
+    _lib.check(lib.itsk_pass_workspace(m, n, ctypes.byref(nb)))
+    ws = dv.workspace(nb.value, dev)
+    ws.fill_(255)  # garbage counters: the init must clear them
+    s = dv.stream_ptr()
+    ref = torch.empty(n + 8, dtype=torch.float64, device=dev)
+    _lib.check(lib.itsk_fused_pass(dv.ptr(a), m, n, n, dv.ptr(b), dv.ptr(x), None, None, None, dv.ptr(ref),
+                                   dv.ptr(ws), ws.numel(), s))
+    ws.fill_(255)
+    _lib.check(lib.itsk_pass_workspace_init(dv.ptr(ws), m, n, s))
+    for _ in range(4):
+        cs = torch.full((n + 8,), float("nan"), dtype=torch.float64, device=dev)
+        _lib.check(lib.itsk_fused_pass_ex(dv.ptr(a), m, n, n, dv.ptr(b), 1.0, dv.ptr(x), None, None, None,
+                                          dv.ptr(cs), dv.ptr(ws), ws.numel(), _lib.PASS_WS_READY, s))
+        assert torch.equal(cs[: n + 4], ref[: n + 4])
+    assert lib.itsk_fused_pass_ex(dv.ptr(a), m, n, n, dv.ptr(b), 1.0, dv.ptr(x), None, None, None, dv.ptr(cs),
+                                  dv.ptr(ws), ws.numel(), 6, s) == _lib.ITSK_EINVAL
+
+
 # --------------------------------------------------------------------------
 # the drop-in solve
 # --------------------------------------------------------------------------
