@@ -167,6 +167,27 @@ int itsk_fused_pass_ex(const double* A, int64_t m, int64_t n, int64_t lda, const
                        unsigned flags, itsk_stream_t stream);
 
 /* ----------------------------------------------------------------------
+ * Sparse CSR A (embed.py:76-80 apply_sparse; solvers.py:195-196 and the
+ * loop's a @ x / a.T @ r on a scipy CSR matrix, section 3.5).
+ * A plan keeps the caller's CSR arrays (row_ptr m+1, col nnz, val nnz; device
+ * pointers that must outlive the plan) and builds, once, the CSC copy and
+ * the chunk table of the A'r pass.  itsk_csr_sketch is bitwise scipy's S·A;
+ * itsk_csr_pass writes cs = [A'r | |r|^2, |r - r_prev|^2, |r_true - r|^2,
+ * |b|^2] like itsk_fused_pass (r = bscale*b - A x bitwise scipy's).
+ * -------------------------------------------------------------------- */
+typedef struct itsk_csr_plan itsk_csr_plan;
+int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m,
+                         int64_t n, int64_t nnz, itsk_stream_t stream, itsk_csr_plan** plan);
+void itsk_csr_plan_destroy(itsk_csr_plan* plan);
+int itsk_csr_shape(const itsk_csr_plan* plan, int64_t* m, int64_t* n, int64_t* nnz);
+int itsk_csr_sketch(const itsk_csr_plan* plan, const double* b, const uint32_t* sk_ptr,
+                    const uint32_t* sk_src, int64_t d, int64_t zeta, double* SAb, int64_t ldw,
+                    itsk_stream_t stream);
+int itsk_csr_pass(const itsk_csr_plan* plan, const double* b, double bscale, const double* x,
+                  const double* r_prev, double* r_out, const double* r_true, double* cs,
+                  itsk_stream_t stream);
+
+/* ----------------------------------------------------------------------
  * Device-resident refinement loop (_run_refinement, solvers.py:270-320).
  * State, constants and trace live in device memory; the loop runs as one
  * CUDA graph with a conditional WHILE node (no host round trip per
@@ -195,6 +216,7 @@ typedef struct itsk_loop_params {
   double* cs;               /* n + 8: reduced [c | scal]; the collective's buffer */
   void* ws;                 /* itsk_loop_workspace bytes                     */
   int64_t ws_bytes;
+  const struct itsk_csr_plan* csr; /* sparse A (A, lda unused) or NULL        */
 } itsk_loop_params;
 
 typedef struct itsk_loop_result { /* read back with one D2H copy */

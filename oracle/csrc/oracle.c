@@ -6,6 +6,10 @@
  *   the d x m CSC matrix S in ascending order and each of its zeta stored
  *   entries, y[row, :] += val * x[j, :], product rounded before the add.
  *   Built with -ffp-contract=off so no FMA changes the rounding.
+ * oracle_sketch_apply_csr: the same for a CSR A — scipy's S_csc @ A.tocsc()
+ *   (embed.py:76-80, csr_matmat on the transposes) adds, per output entry,
+ *   fl(s * a_jc) over the sources j ascending (stored order inside a row),
+ *   i.e. the dense sum with the zero entries of A skipped.
  * oracle_pcg64_words: the 32-bit word stream numpy's Generator(PCG64) feeds
  *   its bounded-integer sampler (embed.py:89-91), for pinning the GPU stream.
  */
@@ -21,6 +25,20 @@ void oracle_sketch_apply(int64_t m, int64_t k, int64_t zeta, const int64_t* rows
       for (int64_t c = 0; c < k; ++c) {
         double prod = v * xj[c];
         yi[c] = yi[c] + prod;
+      }
+    }
+  }
+}
+
+void oracle_sketch_apply_csr(int64_t m, int64_t n, int64_t zeta, const int64_t* rows, const double* vals,
+                             const int64_t* row_ptr, const int32_t* col, const double* val, double* y) {
+  for (int64_t j = 0; j < m; ++j) {
+    for (int64_t t = 0; t < zeta; ++t) {
+      const double v = vals[j * zeta + t];
+      double* yi = y + rows[j * zeta + t] * n;
+      for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) {
+        double prod = val[e] * v;
+        yi[col[e]] = yi[col[e]] + prod;
       }
     }
   }

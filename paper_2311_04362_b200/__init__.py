@@ -17,7 +17,8 @@ from .linalg import (
     tri_solve_upper_transpose,
 )
 from .lsqr import lsqr, sketch_and_precondition
-from .problems import LsProblem, Truth, gen_randsvd
+from .problems import LsProblem, Truth, gen_randsvd, gen_sparse
+from .sparse import CsrMatrix
 from .solvers import (
     SolveResult,
     SolverConfig,
@@ -35,5 +36,5 @@ __all__ = [
     "QrFactors", "cond_est", "householder_qr_econ", "rand_power_norm_est", "tri_solve_upper",
     "tri_solve_upper_transpose", "LsProblem", "Truth", "gen_randsvd", "SolveResult", "SolverConfig",
     "SolveTrace", "damping_params", "iterative_sketching", "momentum_params", "release_workspaces",
-    "should_stop", "sketch_and_solve", "lsqr", "sketch_and_precondition",
+    "should_stop", "sketch_and_solve", "lsqr", "sketch_and_precondition", "gen_sparse", "CsrMatrix",
 ]

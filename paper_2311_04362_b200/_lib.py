@@ -44,6 +44,7 @@ class LoopParams(ctypes.Structure):
         ("normest", c_dp), ("condest", c_dp),
         ("xs", c_dp), ("rs", c_dp), ("trace", c_dp), ("cs", c_dp),
         ("ws", c_dp), ("ws_bytes", c_i64),
+        ("csr", c_dp),
     ]
 
 
@@ -84,6 +85,11 @@ _SIGS = {
     "itsk_pass_workspace_init": (ctypes.c_int, [c_dp, c_i64, c_i64, c_dp]),
     "itsk_fused_pass_ex": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.c_double, c_dp, c_dp,
                                           c_dp, c_dp, c_dp, c_dp, c_i64, ctypes.c_uint, c_dp]),
+    "itsk_csr_plan_create": (ctypes.c_int, [c_dp, c_dp, c_dp, c_i64, c_i64, c_i64, c_dp, ctypes.POINTER(c_dp)]),
+    "itsk_csr_plan_destroy": (None, [c_dp]),
+    "itsk_csr_shape": (ctypes.c_int, [c_dp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "itsk_csr_sketch": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_i64, c_i64, c_dp, c_i64, c_dp]),
+    "itsk_csr_pass": (ctypes.c_int, [c_dp, c_dp, ctypes.c_double, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp]),
     "itsk_loop_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_loop_begin": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
     "itsk_loop_begin_local": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),

@@ -84,6 +84,13 @@ int launch_pass(const PassArgs& a, cudaStream_t s, int* grid_used);
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s);
 
+// Sparse CSR A (sparse.cu): the pass over a plan, explicit pointers (mode 0)
+// or loop mode (x / r slots from ctl, as PassArgs)
+struct CsrPlan;
+int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const double* x, const double* r_prev,
+                    double* r_out, const double* r_true, double* cs, const LoopCtl* ctl, const double* xs,
+                    double* rs, int mode, cudaStream_t s);
+
 // Communication-avoiding cluster QR (qr_tsqr.cu)
 // Panel / update split QR (qr2.cu), the default path of itsk_qr_aug.
 struct QrV2Plan {

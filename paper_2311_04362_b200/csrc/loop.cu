@@ -278,10 +278,10 @@ LoopLayout loop_layout(void* ws, int64_t m, int64_t n) {
 
 int check_params(const itsk_loop_params* p) {
   ITSK_REQUIRE(p, "null params");
-  ITSK_REQUIRE(p->m >= 1 && p->n >= 1 && p->lda >= p->n, "bad loop shape");
+  ITSK_REQUIRE(p->m >= 1 && p->n >= 1 && (p->csr || p->lda >= p->n), "bad loop shape");
   ITSK_REQUIRE(p->max_iters >= 0 && p->extra_iters >= 0, "bad iteration counts");
   ITSK_REQUIRE(p->r_slots == 2 || p->r_slots >= p->max_iters + 1, "r_slots must be 2 or max_iters+1");
-  ITSK_REQUIRE(p->A && p->b && p->R && p->normest && p->condest && p->xs && p->rs && p->trace &&
+  ITSK_REQUIRE((p->A || p->csr) && p->b && p->R && p->normest && p->condest && p->xs && p->rs && p->trace &&
                    p->cs && p->ws,
                "null pointer in loop params");
   ITSK_REQUIRE(p->n <= 6000, "loop: n too large for the single-CTA solves");
@@ -334,6 +334,16 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   a.cs = p->cs;
   a.group = L.group;
   return a;
+}
+
+// the loop's pass: the dense fused pass, or the CSR row / CSC chunk passes
+int loop_pass(const itsk_loop_params* p, const LoopPtrs& q, int mode, cudaStream_t s, int* grid) {
+  if (p->csr) {
+    *grid = 0;
+    return launch_csr_pass(reinterpret_cast<const CsrPlan*>(p->csr), p->b, 1.0, nullptr, nullptr, nullptr,
+                           p->r_true, p->cs, q.ctl, p->xs, p->rs, mode, s);
+  }
+  return launch_pass(pass_args(p, q, mode), s, grid);
 }
 
 int reset_tickets(const itsk_loop_params* p, cudaStream_t s) {
@@ -411,7 +421,7 @@ extern "C" int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t st
   ITSK_CHECK_LAUNCH();
   if ((rc = reset_tickets(p, s))) return rc;
   int grid = 0;
-  return launch_pass(pass_args(p, q, 2), s, &grid);
+  return loop_pass(p, q, 2, s, &grid);
 }
 
 extern "C" int itsk_loop_begin_finish(const itsk_loop_params* p, itsk_stream_t stream) {
@@ -435,7 +445,7 @@ extern "C" int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream) 
   ITSK_CHECK_LAUNCH();
   if ((rc = reset_tickets(p, s))) return rc;
   int grid = 0;
-  rc = launch_pass(pass_args(p, q, 2), s, &grid);
+  rc = loop_pass(p, q, 2, s, &grid);
   if (rc) return rc;
   return enqueue_tail(p, q, TAIL_CONTROL | TAIL_BEGIN | TAIL_STEP, grid, s);
 }
@@ -448,7 +458,7 @@ extern "C" int itsk_loop_step_pre(const itsk_loop_params* p, itsk_stream_t strea
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   LoopPtrs q = make_ptrs(p);
   int grid = 0;
-  return launch_pass(pass_args(p, q, 1), s, &grid);
+  return loop_pass(p, q, 1, s, &grid);
 }
 
 // replicated half: control step and the next iterate
@@ -503,7 +513,7 @@ extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t s
     return fail(ITSK_ECUDA);
   }
   int grid = 0;
-  rc = launch_pass(pass_args(p, q, 1), cap, &grid);
+  rc = loop_pass(p, q, 1, cap, &grid);
   if (rc == ITSK_OK) rc = enqueue_tail(p, q, TAIL_CONTROL | TAIL_STEP, grid, cap, cond, 1);
   cudaGraph_t captured = body;
   e = cudaStreamEndCapture(cap, &captured);

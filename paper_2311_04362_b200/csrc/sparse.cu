@@ -1,0 +1,557 @@
+// Sparse CSR A (§3.5).
+//
+// The reference accepts a scipy sparse A on the same path:
+//   S·A      embed.py:76-80  (S_csc @ A.tocsc()).todense() — per output entry
+//            SA[k, i] = sum over the sources j of S's row k, ascending, with
+//            A[j, i] != 0 of fl(s_kj * A[j, i]), added sequentially from 0
+//            (scipy csr_matmat on the transposes)
+//   r        solvers.py:290,299  b - a @ x   (csr_matvec: a sequential row sum)
+//   c        solvers.py:343      a.T @ r     (csc_matvec over rows ascending)
+// Here:
+//   k_sketch_csr  one warp per sketch row: its sources (CSR of S, ascending)
+//                 in batches of 32, each lane prefetching the first entries
+//                 of one source row; the batch is then applied source by
+//                 source to a shared-memory accumulator row — the same
+//                 per-entry operation sequence as scipy, so S·A is bitwise
+//                 equal to the reference (b rides along as column n).
+//   k_csr_rows    r_j = b_j - sum_t fl(A_jt x_t) in stored order (bitwise
+//                 csr_matvec), r written, the four norm partials per CTA.
+//   k_csc_chunks  c = A'r over the CSC copy of A built once per plan (stable
+//                 radix sort of the entries by column): every column is cut
+//                 into fixed chunks of CHUNK entries, a warp sums a chunk in a
+//                 fixed lane/tree order.
+//   k_csr_finish  per column the chunk partials in chunk order, and the norm
+//                 partials in CTA order, into cs = [c | 4 norms] — the layout
+//                 of the dense fused pass, so the loop's tail kernel is shared.
+// Deterministic run to run; r is bitwise the reference's, c differs from the
+// reference's sequential sum by rounding only.
+#include <algorithm>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "itsk_common.cuh"
+#include "itsk_kernels.cuh"
+
+namespace itsk {
+namespace {
+
+constexpr int CSR_THREADS = 256;
+constexpr int CHUNK = 1024;      // CSC entries per warp chunk
+constexpr int SK_PREF = 4;       // entries of a source row prefetched per lane
+
+__global__ void k_entry_rows(const int64_t* __restrict__ row_ptr, int64_t m, uint32_t* __restrict__ erow) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (int64_t e = row_ptr[j]; e < row_ptr[j + 1]; ++e) erow[e] = static_cast<uint32_t>(j);
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, int64_t nnz) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < nnz) v[e] = static_cast<uint32_t>(e);
+}
+
+__global__ void k_csc_gather(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ erow,
+                             const double* __restrict__ val, int64_t nnz, int32_t* __restrict__ crow,
+                             double* __restrict__ cval) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const uint32_t e = perm[p];
+  crow[p] = static_cast<int32_t>(erow[e]);
+  cval[p] = val[e];
+}
+
+// col_ptr[k] = first position of key >= k in the sorted column keys
+__global__ void k_col_ptr(const uint32_t* __restrict__ keys, int64_t nnz, int64_t n, int64_t* __restrict__ col_ptr) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k > n) return;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < static_cast<uint32_t>(k)) lo = mid + 1; else hi = mid;
+  }
+  col_ptr[k] = lo;
+}
+
+__global__ void k_check_csr(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t m,
+                            int64_t n, int64_t nnz, int* __restrict__ bad) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j > m) return;
+  const int64_t p = row_ptr[j];
+  if (p < 0 || p > nnz || (j == 0 && p != 0) || (j == m && p != nnz) || (j > 0 && row_ptr[j - 1] > p)) {
+    atomicOr(bad, 1);
+    return;
+  }
+  if (j < m)
+    for (int64_t e = p; e < row_ptr[j + 1] && e < nnz; ++e)
+      if (col[e] < 0 || col[e] >= n) atomicOr(bad, 2);
+}
+
+// ---------------------------------------------------------------------------
+// S·[A | b] for CSR A
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sketch_csr(
+    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const double* __restrict__ val,
+    int64_t n, const double* __restrict__ b, const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src,
+    int64_t d, double scale, double* __restrict__ W, int64_t ldw, int smem_acc) {
+  extern __shared__ double sacc[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (i >= d) return;
+  const int64_t ncol = n + (b ? 1 : 0);
+  // the accumulator row: shared memory when it fits, else the output row itself
+  double* acc = smem_acc ? sacc + static_cast<int64_t>(warp) * ncol : W + i * ldw;
+  for (int64_t c = lane; c < ncol; c += 32) acc[c] = 0.0;
+  __syncwarp();
+  const uint32_t e0 = ptr[i], e1 = ptr[i + 1];
+  for (uint32_t e = e0; e < e1; e += 32) {
+    const int cnt = static_cast<int>(min(32u, e1 - e));
+    // lane l: metadata and the first SK_PREF entries of source e + l
+    uint32_t s = 0;
+    int64_t p0 = 0;
+    int len = 0;
+    double sv = 0.0, bj = 0.0;
+    int pc[SK_PREF];
+    double pv[SK_PREF];
+    if (lane < cnt) {
+      s = src[e + lane];
+      const int64_t j = s & 0x7fffffffu;
+      sv = (s >> 31) ? -scale : scale;
+      p0 = row_ptr[j];
+      len = static_cast<int>(row_ptr[j + 1] - p0);
+      if (b) bj = b[j];
+    }
+#pragma unroll
+    for (int t = 0; t < SK_PREF; ++t) {
+      pc[t] = t < len ? col[p0 + t] : -1;
+      pv[t] = t < len ? val[p0 + t] : 0.0;
+    }
+    for (int k = 0; k < cnt; ++k) {
+      const double svk = __shfl_sync(FULL, sv, k);
+      const int lk = __shfl_sync(FULL, len, k);
+      const int64_t pk = __shfl_sync(FULL, p0, k);
+      // entries of source k, 32 at a time, lane t takes entry t
+      for (int t0 = 0; t0 < lk; t0 += 32) {
+        int c = -1;
+        double v = 0.0;
+        if (t0 == 0) {
+#pragma unroll
+          for (int t = 0; t < SK_PREF; ++t) {
+            const int ct = __shfl_sync(FULL, pc[t], k);
+            const double vt = __shfl_sync(FULL, pv[t], k);
+            if (lane == t) { c = ct; v = vt; }
+          }
+        }
+        const int t = t0 + lane;
+        if (t < lk && (t0 > 0 || lane >= SK_PREF)) {
+          c = col[pk + t];
+          v = val[pk + t];
+        }
+        const bool act = t < lk;
+        // a repeated column inside one row (non-canonical CSR) is applied in
+        // stored order, like scipy's sequential loop
+        const unsigned peers = __match_any_sync(FULL, act ? c : -1 - lane);
+        if (!__any_sync(FULL, act && __popc(peers) > 1)) {
+          if (act) acc[c] = __dadd_rn(acc[c], __dmul_rn(v, svk));
+        } else {
+          for (int q = 0; q < 32; ++q) {
+            if (lane == q && act) acc[c] = __dadd_rn(acc[c], __dmul_rn(v, svk));
+            __syncwarp();
+          }
+        }
+        __syncwarp();
+      }
+      const double bk = __shfl_sync(FULL, bj, k);
+      if (b && lane == 0) acc[n] = __dadd_rn(acc[n], __dmul_rn(bk, svk));
+      __syncwarp();
+    }
+  }
+  if (smem_acc)
+    for (int64_t c = lane; c < ncol; c += 32) W[i * ldw + c] = acc[c];
+}
+
+// ---------------------------------------------------------------------------
+// The pass: r = bscale*b - A x (rows), c = A'r (CSC chunks), finish
+// ---------------------------------------------------------------------------
+struct CsrPassArgs {
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+  const int64_t* col_ptr;
+  const int32_t* crow;
+  const double* cval;
+  const int32_t* chunk_col;
+  const int64_t* chunk_ptr;
+  double* chunk_part;
+  double* row_part;  // g1 x 4
+  int64_t m, n, nchunks, rows_per_cta;
+  int g1;
+  const double* b;
+  double bscale;
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  const double* r_true;
+  double* cs;
+  // loop mode (as PassArgs): x / r_prev / r_out from ctl->it
+  const LoopCtl* ctl;
+  const double* xs;
+  double* rs;
+  int mode;
+};
+
+__device__ __forceinline__ bool resolve(const CsrPassArgs& a, const double*& x, const double*& r_prev,
+                                        double*& r_out) {
+  if (a.mode == 0) {
+    x = a.x;
+    r_prev = a.r_prev;
+    r_out = a.r_out;
+    return true;
+  }
+  const LoopCtl* ctl = a.ctl;
+  if (ctl->result.done) return false;
+  const int64_t S = ctl->r_slots;
+  if (a.mode == 1) {
+    const int64_t it = ctl->it;
+    x = a.xs + (it + 1) * a.n;
+    r_prev = a.rs + (it % S) * a.m;
+    r_out = a.rs + ((it + 1) % S) * a.m;
+  } else {
+    x = a.xs;
+    r_prev = nullptr;
+    r_out = a.rs;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(CSR_THREADS) k_csr_rows(CsrPassArgs a) {
+  __shared__ double red[CSR_THREADS / 32];
+  pdl_wait();
+  const double *x, *r_prev;
+  double* r_out;
+  if (!resolve(a, x, r_prev, r_out)) return;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r1 = min(a.m, r0 + a.rows_per_cta);
+  double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
+  for (int64_t j = r0 + threadIdx.x; j < r1; j += CSR_THREADS) {
+    double dot = 0.0;
+    const int64_t p1 = a.row_ptr[j + 1];
+    for (int64_t e = a.row_ptr[j]; e < p1; ++e) dot = __dadd_rn(dot, __dmul_rn(a.val[e], __ldg(x + a.col[e])));
+    const double bj = a.b[j];
+    const double r = __dsub_rn(a.bscale == 1.0 ? bj : __dmul_rn(a.bscale, bj), dot);
+    r_out[j] = r;
+    s_rr += r * r;
+    s_bb += bj * bj;
+    if (r_prev) {
+      const double dd = r - r_prev[j];
+      s_dd += dd * dd;
+    }
+    if (a.r_true) {
+      const double tt = a.r_true[j] - r;
+      s_tt += tt * tt;
+    }
+  }
+  s_rr = block_sum(s_rr, red);
+  s_dd = block_sum(s_dd, red);
+  s_tt = block_sum(s_tt, red);
+  s_bb = block_sum(s_bb, red);
+  if (threadIdx.x == 0) {
+    double* o = a.row_part + 4 * static_cast<int64_t>(blockIdx.x);
+    o[0] = s_rr;
+    o[1] = r_prev ? s_dd : 0.0;
+    o[2] = a.r_true ? s_tt : 0.0;
+    o[3] = s_bb;
+  }
+}
+
+__global__ void __launch_bounds__(CSR_THREADS) k_csc_chunks(CsrPassArgs a) {
+  pdl_wait();
+  const double *x, *r_prev;
+  double* r;
+  if (!resolve(a, x, r_prev, r)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * (CSR_THREADS / 32) + (threadIdx.x >> 5);
+  if (q >= a.nchunks) return;
+  const int k = a.chunk_col[q];
+  const int64_t lo = a.col_ptr[k] + (q - a.chunk_ptr[k]) * CHUNK;
+  const int64_t hi = min(lo + CHUNK, a.col_ptr[k + 1]);
+  double s = 0.0;
+  for (int64_t p = lo + lane; p < hi; p += 32) s = fma(a.cval[p], r[a.crow[p]], s);
+  s = warp_sum(s);
+  if (lane == 0) a.chunk_part[q] = s;
+}
+
+__global__ void __launch_bounds__(CSR_THREADS) k_csr_finish(CsrPassArgs a) {
+  pdl_wait();
+  if (a.mode != 0 && a.ctl->result.done) return;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < a.n) {
+    double s = 0.0;
+    for (int64_t q = a.chunk_ptr[t]; q < a.chunk_ptr[t + 1]; ++q) s += a.chunk_part[q];
+    a.cs[t] = s;
+  } else if (t < a.n + 4) {
+    const int w = static_cast<int>(t - a.n);
+    double s = 0.0;
+    for (int g = 0; g < a.g1; ++g) s += a.row_part[4 * static_cast<int64_t>(g) + w];
+    a.cs[t] = s;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan: the CSC copy, chunk table and partial buffers (one device allocation)
+// ---------------------------------------------------------------------------
+struct CsrPlan {
+  int64_t m, n, nnz;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+  int64_t* col_ptr;
+  int32_t* crow;
+  double* cval;
+  int32_t* chunk_col;
+  int64_t* chunk_ptr;
+  double* chunk_part;
+  double* row_part;
+  double* r_tmp;
+  int64_t nchunks;
+  int g1;
+  int64_t rows_per_cta;
+  void* pool;
+};
+
+int csr_rows_grid(int64_t m) {
+  int64_t g = (m + CSR_THREADS - 1) / CSR_THREADS;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(std::max<int64_t>(1, std::min(g, cap)));
+}
+
+int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const double* x, const double* r_prev,
+                    double* r_out, const double* r_true, double* cs, const LoopCtl* ctl, const double* xs,
+                    double* rs, int mode, cudaStream_t s) {
+  CsrPassArgs a{};
+  a.row_ptr = P->row_ptr;
+  a.col = P->col;
+  a.val = P->val;
+  a.col_ptr = P->col_ptr;
+  a.crow = P->crow;
+  a.cval = P->cval;
+  a.chunk_col = P->chunk_col;
+  a.chunk_ptr = P->chunk_ptr;
+  a.chunk_part = P->chunk_part;
+  a.row_part = P->row_part;
+  a.m = P->m;
+  a.n = P->n;
+  a.nchunks = P->nchunks;
+  a.rows_per_cta = P->rows_per_cta;
+  a.g1 = P->g1;
+  a.b = b;
+  a.bscale = bscale;
+  a.x = x;
+  a.r_prev = r_prev;
+  a.r_out = (mode == 0 && !r_out) ? P->r_tmp : r_out;
+  a.r_true = r_true;
+  a.cs = cs;
+  a.ctl = ctl;
+  a.xs = xs;
+  a.rs = rs;
+  a.mode = mode;
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_rows), dim3(P->g1), dim3(CSR_THREADS), 0, s, a));
+  count_launch();
+  if (P->nchunks > 0) {
+    const unsigned g2 = static_cast<unsigned>((P->nchunks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32));
+    ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csc_chunks), dim3(g2), dim3(CSR_THREADS), 0, s, a));
+    count_launch();
+  }
+  const unsigned g3 = static_cast<unsigned>((P->n + 4 + CSR_THREADS - 1) / CSR_THREADS);
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_finish), dim3(g3), dim3(CSR_THREADS), 0, s, a));
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+}  // namespace itsk
+
+using namespace itsk;
+
+extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m,
+                                    int64_t n, int64_t nnz, itsk_stream_t stream, itsk_csr_plan** plan) {
+  ITSK_REQUIRE(plan && row_ptr && (nnz == 0 || (col && val)), "null pointer");
+  ITSK_REQUIRE(m >= 1 && n >= 1 && nnz >= 0, "bad CSR shape");
+  ITSK_REQUIRE(nnz < (1ll << 31) && m < (1ll << 31) && n < (1ll << 31), "CSR too large (nnz, m, n < 2^31)");
+  *plan = nullptr;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // validate the structure on the device (monotone row_ptr, columns in range)
+  int* bad = nullptr;
+  ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s));
+  ITSK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  k_check_csr<<<static_cast<unsigned>((m + 1 + 255) / 256), 256, 0, s>>>(row_ptr, col, m, n, nnz, bad);
+  count_launch();
+  int hbad = 0;
+  ITSK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ITSK_CUDA(cudaStreamSynchronize(s));
+  ITSK_CUDA(cudaFreeAsync(bad, s));
+  ITSK_REQUIRE(hbad == 0, "invalid CSR structure (%s)", (hbad & 1) ? "row_ptr" : "column index out of range");
+
+  // sort scratch (freed before return)
+  const int bits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(n)));
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, static_cast<int>(std::max<int64_t>(nnz, 1)),
+                                  0, bits, s);
+  Carver sc(nullptr, 1ll << 62);
+  sc.take<uint32_t>(nnz);  // keys out
+  sc.take<uint32_t>(nnz);  // iota
+  sc.take<uint32_t>(nnz);  // perm
+  sc.take<uint32_t>(nnz);  // entry rows
+  sc.take<char>(static_cast<int64_t>(cub_bytes));
+  void* scratch = nullptr;
+  ITSK_CUDA(cudaMallocAsync(&scratch, std::max<int64_t>(sc.off, 256), s));
+  Carver c2(scratch, 1ll << 62);
+  uint32_t* keys = c2.take<uint32_t>(nnz);
+  uint32_t* iota = c2.take<uint32_t>(nnz);
+  uint32_t* perm = c2.take<uint32_t>(nnz);
+  uint32_t* erow = c2.take<uint32_t>(nnz);
+  void* cub_tmp = c2.take<char>(static_cast<int64_t>(cub_bytes));
+
+  CsrPlan* P = new CsrPlan();
+  P->m = m;
+  P->n = n;
+  P->nnz = nnz;
+  P->row_ptr = row_ptr;
+  P->col = col;
+  P->val = val;
+  P->g1 = csr_rows_grid(m);
+  P->rows_per_cta = (m + P->g1 - 1) / P->g1;
+  std::vector<int64_t> hptr(n + 1, 0);
+  auto fail = [&](int code) {
+    cudaFreeAsync(scratch, s);
+    if (P->pool) cudaFree(P->pool);
+    delete P;
+    return code;
+  };
+  // CSC: stable sort of the entry ids by column (entries are in row order)
+  int64_t* col_ptr_tmp = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&col_ptr_tmp), sizeof(int64_t) * (n + 1), s) != cudaSuccess) {
+    set_error("csr plan: allocation failed");
+    return fail(ITSK_ECUDA);
+  }
+  if (nnz > 0) {
+    k_entry_rows<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(row_ptr, m, erow);
+    k_iota<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(iota, nnz);
+    count_launch(2);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, reinterpret_cast<const uint32_t*>(col), keys, iota, perm,
+                                    static_cast<int>(nnz), 0, bits, s);
+    k_col_ptr<<<static_cast<unsigned>((n + 1 + 255) / 256), 256, 0, s>>>(keys, nnz, n, col_ptr_tmp);
+    count_launch(2);
+  } else {
+    cudaMemsetAsync(col_ptr_tmp, 0, sizeof(int64_t) * (n + 1), s);
+  }
+  if (cudaMemcpyAsync(hptr.data(), col_ptr_tmp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    set_error("csr plan: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaFreeAsync(col_ptr_tmp, s);
+    return fail(ITSK_ECUDA);
+  }
+  // chunk table (host; one-time)
+  std::vector<int64_t> cptr(n + 1, 0);
+  for (int64_t k = 0; k < n; ++k) cptr[k + 1] = cptr[k] + (hptr[k + 1] - hptr[k] + CHUNK - 1) / CHUNK;
+  P->nchunks = cptr[n];
+  std::vector<int32_t> ccol(std::max<int64_t>(P->nchunks, 1));
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t q = cptr[k]; q < cptr[k + 1]; ++q) ccol[q] = static_cast<int32_t>(k);
+  Carver pc(nullptr, 1ll << 62);
+  pc.take<int64_t>(n + 1);
+  pc.take<int32_t>(nnz);
+  pc.take<double>(nnz);
+  pc.take<int32_t>(std::max<int64_t>(P->nchunks, 1));
+  pc.take<int64_t>(n + 1);
+  pc.take<double>(std::max<int64_t>(P->nchunks, 1));
+  pc.take<double>(4 * static_cast<int64_t>(P->g1));
+  pc.take<double>(m);
+  if (cudaMalloc(&P->pool, pc.off + 256) != cudaSuccess) {
+    set_error("csr plan: device allocation of %lld bytes failed", (long long)pc.off);
+    cudaFreeAsync(col_ptr_tmp, s);
+    return fail(ITSK_ECUDA);
+  }
+  Carver pv(P->pool, 1ll << 62);
+  P->col_ptr = pv.take<int64_t>(n + 1);
+  P->crow = pv.take<int32_t>(nnz);
+  P->cval = pv.take<double>(nnz);
+  P->chunk_col = pv.take<int32_t>(std::max<int64_t>(P->nchunks, 1));
+  P->chunk_ptr = pv.take<int64_t>(n + 1);
+  P->chunk_part = pv.take<double>(std::max<int64_t>(P->nchunks, 1));
+  P->row_part = pv.take<double>(4 * static_cast<int64_t>(P->g1));
+  P->r_tmp = pv.take<double>(m);
+  cudaError_t e = cudaMemcpyAsync(P->col_ptr, col_ptr_tmp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(P->chunk_col, ccol.data(), sizeof(int32_t) * ccol.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(P->chunk_ptr, cptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) {
+    k_csc_gather<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm, erow, val, nnz, P->crow, P->cval);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+  cudaFreeAsync(col_ptr_tmp, s);
+  if (e != cudaSuccess) {
+    set_error("csr plan: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
+  cudaFreeAsync(scratch, s);
+  *plan = reinterpret_cast<itsk_csr_plan*>(P);
+  return ITSK_OK;
+}
+
+extern "C" void itsk_csr_plan_destroy(itsk_csr_plan* plan) {
+  if (!plan) return;
+  CsrPlan* P = reinterpret_cast<CsrPlan*>(plan);
+  cudaDeviceSynchronize();
+  if (P->pool) cudaFree(P->pool);
+  delete P;
+}
+
+extern "C" int itsk_csr_shape(const itsk_csr_plan* plan, int64_t* m, int64_t* n, int64_t* nnz) {
+  ITSK_REQUIRE(plan, "null plan");
+  const CsrPlan* P = reinterpret_cast<const CsrPlan*>(plan);
+  if (m) *m = P->m;
+  if (n) *n = P->n;
+  if (nnz) *nnz = P->nnz;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_csr_sketch(const itsk_csr_plan* plan, const double* b, const uint32_t* sk_ptr,
+                               const uint32_t* sk_src, int64_t d, int64_t zeta, double* SAb, int64_t ldw,
+                               itsk_stream_t stream) {
+  ITSK_REQUIRE(plan && sk_ptr && sk_src && SAb, "null pointer");
+  const CsrPlan* P = reinterpret_cast<const CsrPlan*>(plan);
+  ITSK_REQUIRE(d >= 1 && zeta >= 1 && ldw >= P->n + (b ? 1 : 0), "bad sketch shape");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const double scale = 1.0 / sqrt(static_cast<double>(zeta));  // embed.py:92
+  const int64_t ncol = P->n + (b ? 1 : 0);
+  static const bool attr = [] {
+    return allow_max_smem(reinterpret_cast<const void*>(k_sketch_csr)) == cudaSuccess;
+  }();
+  (void)attr;
+  const int64_t budget = 200 * 1024;
+  int warps = static_cast<int>(std::min<int64_t>(8, budget / (ncol * 8)));
+  const int smem_acc = warps >= 1 ? 1 : 0;
+  if (!smem_acc) warps = 8;
+  const size_t smem = smem_acc ? static_cast<size_t>(warps) * ncol * 8 : 0;
+  const unsigned grid = static_cast<unsigned>((d + warps - 1) / warps);
+  k_sketch_csr<<<grid, 32 * warps, smem, s>>>(P->row_ptr, P->col, P->val, P->n, b, sk_ptr, sk_src, d, scale, SAb,
+                                              ldw, smem_acc);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_csr_pass(const itsk_csr_plan* plan, const double* b, double bscale, const double* x,
+                             const double* r_prev, double* r_out, const double* r_true, double* cs,
+                             itsk_stream_t stream) {
+  ITSK_REQUIRE(plan && b && x && cs, "null pointer");
+  return launch_csr_pass(reinterpret_cast<const CsrPlan*>(plan), b, bscale, x, r_prev, r_out, r_true, cs, nullptr,
+                         nullptr, nullptr, 0, reinterpret_cast<cudaStream_t>(stream));
+}

@@ -105,6 +105,21 @@ class SparseSignEmbedding:
             raise ValueError("apply_vec expects a vector")
         return self.apply_dense(v)
 
+    def apply_sparse(self, a, b=None):
+        """S @ a for a sparse m x n matrix, dense result (embed.py:76-80) —
+        bitwise scipy's (S_csc @ a.tocsc()).todense().  `a` is a scipy sparse
+        matrix (numpy result) or a sparse.CsrMatrix (device result); with `b`,
+        S @ [a | b]."""
+        from .sparse import CsrMatrix, as_csr_matrix
+
+        dev = self.rows_dev.device
+        A = as_csr_matrix(a, dev)
+        if A.shape[0] != self.m:
+            raise ValueError(f"dimension mismatch: S is {self.d}x{self.m}, input has {A.shape[0]} rows")
+        bt = None if b is None else _dev.as_device_vector(b, dev)
+        res = A.sketch(self, bt)
+        return res if isinstance(a, CsrMatrix) else _dev.to_numpy(res)
+
     def _sketch(self, at, n, lda, bt, out):
         dev = self.rows_dev.device
         ncol = n + (1 if bt is not None else 0)

@@ -13,6 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+import scipy.sparse as sp
 
 
 @dataclass
@@ -69,3 +70,24 @@ def gen_randsvd(m: int, n: int, kappa: float, beta: float, seed: int) -> LsProbl
     r = beta * p / np.linalg.norm(p)
     b = a @ x + r
     return LsProblem(a=a, b=b, truth=Truth(x=x, r=r, kappa=float(kappa), beta=float(beta)))
+
+
+def gen_sparse(m: int, n: int, seed: int) -> LsProblem:
+    """Sparse +-1 instance (problems.py:92-110; section 3.5): three
+    distinct uniform column positions per row — rows with a repeated position
+    are redrawn whole, in stream order, until none is left — values +-1,
+    Gaussian b, no ground truth.  CSR with sorted column indices."""
+    if not (m >= n >= 3):
+        raise ValueError(f"need m >= n >= 3, got m={m}, n={n}")
+    rng = np.random.default_rng(seed)
+    cols = rng.integers(0, n, size=(m, 3))
+    while True:
+        s = np.sort(cols, axis=1)
+        dup = (s[:, 1:] == s[:, :-1]).any(axis=1)
+        if not dup.any():
+            break
+        cols[dup] = rng.integers(0, n, size=(int(dup.sum()), 3))
+    vals = rng.choice(np.array([-1.0, 1.0]), size=(m, 3))
+    a = sp.csr_matrix((vals.ravel(), cols.ravel(), 3 * np.arange(m + 1)), shape=(m, n))
+    a.sort_indices()
+    return LsProblem(a=a, b=rng.standard_normal(m), truth=None)

@@ -33,6 +33,7 @@ from . import device as _dev
 from .embed import default_distortion, pcg_state, SparseSignEmbedding
 from .linalg import SingularMatrixError, normest_steps, start_vector
 from .problems import Truth
+from .sparse import as_csr_matrix, is_sparse
 
 __all__ = ["SolverConfig", "SolveTrace", "SolveResult", "iterative_sketching", "sketch_and_solve",
            "damping_params", "momentum_params", "should_stop", "SingularMatrixError",
@@ -277,15 +278,20 @@ def release_workspaces() -> None:
 # ---------------------------------------------------------------------------
 # The solve
 # ---------------------------------------------------------------------------
-def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int):
-    """Pattern, S·[A|b], QR, x0, normest, condest — solvers.py:332-337."""
+def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None):
+    """Pattern, S·[A|b], QR, x0, normest, condest — solvers.py:332-337
+    (S·A by apply_sparse for a CSR A, solvers.py:195-196)."""
     m, n, d, zeta = ws.m, ws.n, ws.d, ws.zeta
     words, has32, pend = pcg_state(cfg.rng_seed)
     _lib.check(lib.itsk_sparse_sign_pattern(
         d, m, zeta, words, has32, pend, _dev.ptr(ws.rows), _dev.ptr(ws.neg), _dev.ptr(ws.sk_ptr),
         _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
-    _lib.check(lib.itsk_sketch(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
-                               _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, stream))
+    if csr is not None:
+        _lib.check(lib.itsk_csr_sketch(csr.plan, _dev.ptr(bt), _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), d, zeta,
+                                       _dev.ptr(ws.W), n + 1, stream))
+    else:
+        _lib.check(lib.itsk_sketch(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
+                                   _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, stream))
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
@@ -300,8 +306,9 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
     _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, _dev.ptr(ws.Rp), stream))
 
 
-def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None):
+def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None, csr=None):
     p = _lib.LoopParams()
+    p.csr = csr.plan if csr is not None else None
     p.m = ws.m if m_local is None else m_local
     p.n = ws.n
     p.lda = lda
@@ -313,7 +320,7 @@ def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth,
     p.u, p.gamma, p.rho = float(cfg.unit_roundoff), float(cfg.stop_gamma), float(cfg.stop_rho)
     p.has_truth = 1 if truth is not None else 0
     p.truth_beta = float(truth.beta) if truth is not None else 0.0
-    p.A = _dev.ptr(at)
+    p.A = _dev.ptr(at) if csr is None else None
     p.b = _dev.ptr(ws.b)
     p.R = _dev.ptr(ws.R)
     p.Rp = _dev.ptr(ws.Rp)
@@ -417,7 +424,14 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
         raise ValueError(f"backward_error capped at m <= 4000, got m = {m}")
     r_slots = cfg.max_iters + 1 if residuals == "all" else 2
     ws = _workspace(dev, m, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots, truth is not None)
-    if isinstance(a, torch.Tensor) and a.is_cuda:
+    csr = None
+    if is_sparse(a):
+        # sparse A (solvers.py:195-196; section 3.5): CSR pass + CSC copy
+        if cfg.track_be:
+            raise ValueError("track_be is not supported for a sparse A on the B200 path")
+        csr = as_csr_matrix(a, dev)
+        at, lda = None, 0
+    elif isinstance(a, torch.Tensor) and a.is_cuda:
         at, lda = _dev.as_device_matrix(a, dev)
     else:
         arr = np.asarray(a, dtype=np.float64)
@@ -435,8 +449,8 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
             ws.r_true.copy_(_dev.as_device_vector(truth.r, dev))
     stream_obj = torch.cuda.current_stream(dev)
     stream = int(stream_obj.cuda_stream)
-    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream)
-    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth)
+    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr)
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr)
     run_loop(lib, ws, p, use_graph, stream)
     res = _read_result(lib, ws, p, stream_obj)
     return _assemble(ws, res, truth, cfg, at, ws.b)
