@@ -9,11 +9,10 @@
 //   c        solvers.py:343      a.T @ r     (csc_matvec over rows ascending)
 // Here:
 //   k_sketch_csr  one warp per sketch row: its sources (CSR of S, ascending)
-//                 in batches of 32, each lane prefetching the first entries
-//                 of one source row; the batch is then applied source by
-//                 source to a shared-memory accumulator row — the same
-//                 per-entry operation sequence as scipy, so S·A is bitwise
-//                 equal to the reference (b rides along as column n).
+//                 in batches of 32, their entries applied in rank waves to a
+//                 shared-memory accumulator row — every column receives its
+//                 products in source order, so S·A is bitwise the
+//                 reference's (b: the dense gather kernel, column n).
 //   k_csr_rows    r_j = b_j - sum_t fl(A_jt x_t) in stored order (bitwise
 //                 csr_matvec), r written, the four norm partials per CTA.
 //   k_csc_chunks  c = A'r over the CSC copy of A built once per plan (stable
@@ -88,86 +87,99 @@ __global__ void k_check_csr(const int64_t* __restrict__ row_ptr, const int32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// S·[A | b] for CSR A
+// S·A for CSR A
+//
+// A warp owns sketch row k and walks its sources in ascending order, 32 at a
+// time.  The batch's entries (source-major, stored order inside a row) are
+// taken 32 per round; inside a round, an entry's rank = the number of earlier
+// entries of the round with the same column (__match_any_sync), and the
+// round is applied in waves of equal rank — entries of one wave touch
+// distinct columns, and every column still receives its products in source
+// order, so each output is the same sequential sum as scipy's.  Rounds of a
+// batch are loaded together (RND x 2 loads in flight per lane).  S·b (the
+// b column) is one more sequential chain per row: the dense gather kernel
+// computes it (itsk_sketch with n = 0).
 // ---------------------------------------------------------------------------
+constexpr int SK_RND = 4;  // rounds of 32 entries loaded per batch step
+
 __global__ void __launch_bounds__(256) k_sketch_csr(
     const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const double* __restrict__ val,
-    int64_t n, const double* __restrict__ b, const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src,
-    int64_t d, double scale, double* __restrict__ W, int64_t ldw, int smem_acc) {
+    int64_t n, const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
+    double* __restrict__ W, int64_t ldw, int smem_acc) {
   extern __shared__ double sacc[];
+  __shared__ int soff[8][33];
+  __shared__ int64_t sp0[8][32];
+  __shared__ double ssv[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
   if (i >= d) return;
-  const int64_t ncol = n + (b ? 1 : 0);
   // the accumulator row: shared memory when it fits, else the output row itself
-  double* acc = smem_acc ? sacc + static_cast<int64_t>(warp) * ncol : W + i * ldw;
-  for (int64_t c = lane; c < ncol; c += 32) acc[c] = 0.0;
-  __syncwarp();
+  double* acc = smem_acc ? sacc + static_cast<int64_t>(warp) * n : W + i * ldw;
+  for (int64_t c = lane; c < n; c += 32) acc[c] = 0.0;
+  const unsigned lt = (1u << lane) - 1u;
   const uint32_t e0 = ptr[i], e1 = ptr[i + 1];
   for (uint32_t e = e0; e < e1; e += 32) {
     const int cnt = static_cast<int>(min(32u, e1 - e));
-    // lane l: metadata and the first SK_PREF entries of source e + l
-    uint32_t s = 0;
-    int64_t p0 = 0;
     int len = 0;
-    double sv = 0.0, bj = 0.0;
-    int pc[SK_PREF];
-    double pv[SK_PREF];
+    int64_t p0 = 0;
+    double sv = 0.0;
     if (lane < cnt) {
-      s = src[e + lane];
-      const int64_t j = s & 0x7fffffffu;
-      sv = (s >> 31) ? -scale : scale;
+      const uint32_t sj = src[e + lane];
+      const int64_t j = sj & 0x7fffffffu;
+      sv = (sj >> 31) ? -scale : scale;
       p0 = row_ptr[j];
       len = static_cast<int>(row_ptr[j + 1] - p0);
-      if (b) bj = b[j];
     }
+    int inc = len;
 #pragma unroll
-    for (int t = 0; t < SK_PREF; ++t) {
-      pc[t] = t < len ? col[p0 + t] : -1;
-      pv[t] = t < len ? val[p0 + t] : 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
     }
-    for (int k = 0; k < cnt; ++k) {
-      const double svk = __shfl_sync(FULL, sv, k);
-      const int lk = __shfl_sync(FULL, len, k);
-      const int64_t pk = __shfl_sync(FULL, p0, k);
-      // entries of source k, 32 at a time, lane t takes entry t
-      for (int t0 = 0; t0 < lk; t0 += 32) {
-        int c = -1;
-        double v = 0.0;
-        if (t0 == 0) {
+    const int T = __shfl_sync(FULL, inc, 31);
+    __syncwarp();
+    soff[warp][lane] = inc - len;
+    if (lane == 31) soff[warp][32] = T;
+    sp0[warp][lane] = p0;
+    ssv[warp][lane] = sv;
+    __syncwarp();
+    for (int t0 = 0; t0 < T; t0 += 32 * SK_RND) {
+      int cr[SK_RND];
+      double pr[SK_RND];
 #pragma unroll
-          for (int t = 0; t < SK_PREF; ++t) {
-            const int ct = __shfl_sync(FULL, pc[t], k);
-            const double vt = __shfl_sync(FULL, pv[t], k);
-            if (lane == t) { c = ct; v = vt; }
+      for (int u = 0; u < SK_RND; ++u) {
+        const int t = t0 + 32 * u + lane;
+        cr[u] = -1 - lane;
+        pr[u] = 0.0;
+        if (t < T) {
+          // source of entry t: the last q with soff[q] <= t
+          int lo = 0, hi = cnt - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (soff[warp][mid] <= t) lo = mid; else hi = mid - 1;
           }
+          const int64_t ei = sp0[warp][lo] + (t - soff[warp][lo]);
+          cr[u] = col[ei];
+          pr[u] = __dmul_rn(val[ei], ssv[warp][lo]);
         }
-        const int t = t0 + lane;
-        if (t < lk && (t0 > 0 || lane >= SK_PREF)) {
-          c = col[pk + t];
-          v = val[pk + t];
-        }
-        const bool act = t < lk;
-        // a repeated column inside one row (non-canonical CSR) is applied in
-        // stored order, like scipy's sequential loop
-        const unsigned peers = __match_any_sync(FULL, act ? c : -1 - lane);
-        if (!__any_sync(FULL, act && __popc(peers) > 1)) {
-          if (act) acc[c] = __dadd_rn(acc[c], __dmul_rn(v, svk));
-        } else {
-          for (int q = 0; q < 32; ++q) {
-            if (lane == q && act) acc[c] = __dadd_rn(acc[c], __dmul_rn(v, svk));
-            __syncwarp();
-          }
-        }
-        __syncwarp();
       }
-      const double bk = __shfl_sync(FULL, bj, k);
-      if (b && lane == 0) acc[n] = __dadd_rn(acc[n], __dmul_rn(bk, svk));
-      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < SK_RND; ++u) {
+        if (t0 + 32 * u >= T) break;
+        const bool act = cr[u] >= 0;
+        const unsigned peers = __match_any_sync(FULL, cr[u]);
+        const int rank = __popc(peers & lt);
+        const int waves = __reduce_max_sync(FULL, act ? rank : 0);
+        for (int w = 0; w <= waves; ++w) {
+          if (act && rank == w) acc[cr[u]] = __dadd_rn(acc[cr[u]], pr[u]);
+          __syncwarp();
+        }
+      }
     }
+    __syncwarp();
   }
   if (smem_acc)
-    for (int64_t c = lane; c < ncol; c += 32) W[i * ldw + c] = acc[c];
+    for (int64_t c = lane; c < n; c += 32) W[i * ldw + c] = acc[c];
 }
 
 // ---------------------------------------------------------------------------
@@ -224,32 +236,89 @@ __device__ __forceinline__ bool resolve(const CsrPassArgs& a, const double*& x, 
   return true;
 }
 
+// Rows: a warp takes RPL*32 consecutive rows at a time (lane l owns rows
+// l, l+32, ...); all their row pointers / b / r_prev loads are issued
+// together, then the batch's entries (one contiguous CSR range) are staged in
+// shared memory with coalesced, independent loads, and each lane sums its
+// rows in stored order (the bitwise csr_matvec order).  x is staged per CTA
+// when it fits.  A batch with more entries than the stage uses direct loads.
+constexpr int RPL = 1;            // rows per lane per batch
+constexpr int ROW_STAGE = 256;    // staged entries per warp (8 per row on average at RPL 1)
+constexpr int X_STAGE = 8192;     // x staged in shared memory up to this n
+
 __global__ void __launch_bounds__(CSR_THREADS) k_csr_rows(CsrPassArgs a) {
   __shared__ double red[CSR_THREADS / 32];
+  // dynamic: staged values | staged columns | x (when n <= X_STAGE)
+  extern __shared__ double dsm[];
+  double(*sval)[ROW_STAGE] = reinterpret_cast<double(*)[ROW_STAGE]>(dsm);
+  int(*scol)[ROW_STAGE] = reinterpret_cast<int(*)[ROW_STAGE]>(dsm + (CSR_THREADS / 32) * ROW_STAGE);
+  double* xsm = dsm + (CSR_THREADS / 32) * ROW_STAGE * 3 / 2;
   pdl_wait();
   const double *x, *r_prev;
   double* r_out;
   if (!resolve(a, x, r_prev, r_out)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool xs = a.n <= X_STAGE;
+  if (xs)
+    for (int64_t c = threadIdx.x; c < a.n; c += CSR_THREADS) xsm[c] = x[c];
+  __syncthreads();
+  const double* xv = xs ? xsm : x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
   const int64_t r1 = min(a.m, r0 + a.rows_per_cta);
+  constexpr int BATCH = 32 * RPL;
   double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
-  for (int64_t j = r0 + threadIdx.x; j < r1; j += CSR_THREADS) {
-    double dot = 0.0;
-    const int64_t p1 = a.row_ptr[j + 1];
-    for (int64_t e = a.row_ptr[j]; e < p1; ++e) dot = __dadd_rn(dot, __dmul_rn(a.val[e], __ldg(x + a.col[e])));
-    const double bj = a.b[j];
-    const double r = __dsub_rn(a.bscale == 1.0 ? bj : __dmul_rn(a.bscale, bj), dot);
-    r_out[j] = r;
-    s_rr += r * r;
-    s_bb += bj * bj;
-    if (r_prev) {
-      const double dd = r - r_prev[j];
-      s_dd += dd * dd;
+  for (int64_t j0 = r0 + BATCH * warp; j0 < r1; j0 += BATCH * (CSR_THREADS / 32)) {
+    int64_t plo[RPL], phi[RPL];
+    double bj[RPL], rp[RPL], rt[RPL];
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int64_t j = j0 + lane + 32 * u;
+      const bool ok = j < r1;
+      plo[u] = ok ? a.row_ptr[j] : 0;
+      phi[u] = ok ? a.row_ptr[j + 1] : 0;
+      bj[u] = ok ? a.b[j] : 0.0;
+      rp[u] = (ok && r_prev) ? r_prev[j] : 0.0;
+      rt[u] = (ok && a.r_true) ? a.r_true[j] : 0.0;
     }
-    if (a.r_true) {
-      const double tt = a.r_true[j] - r;
+    const int nrow = static_cast<int>(r1 - j0 < BATCH ? r1 - j0 : BATCH);
+    const int last = nrow - 1;
+    const int64_t base = __shfl_sync(FULL, plo[0], 0);
+    int64_t end = 0;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int64_t e = __shfl_sync(FULL, phi[u], last & 31);
+      if (u == (last >> 5)) end = e;
+    }
+    const int64_t total = end - base;
+    const bool staged = total <= ROW_STAGE;
+    if (staged) {
+      for (int t = lane; t < total; t += 32) {
+        scol[warp][t] = a.col[base + t];
+        sval[warp][t] = a.val[base + t];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int64_t j = j0 + lane + 32 * u;
+      if (j >= r1) continue;
+      double dot = 0.0;
+      if (staged) {
+        for (int64_t e = plo[u] - base; e < phi[u] - base; ++e)
+          dot = __dadd_rn(dot, __dmul_rn(sval[warp][e], xv[scol[warp][e]]));
+      } else {
+        for (int64_t e = plo[u]; e < phi[u]; ++e) dot = __dadd_rn(dot, __dmul_rn(a.val[e], xv[a.col[e]]));
+      }
+      const double r = __dsub_rn(a.bscale == 1.0 ? bj[u] : __dmul_rn(a.bscale, bj[u]), dot);
+      r_out[j] = r;
+      s_rr += r * r;
+      s_bb += bj[u] * bj[u];
+      const double dd = r - rp[u];
+      s_dd += dd * dd;
+      const double tt = rt[u] - r;
       s_tt += tt * tt;
     }
+    __syncwarp();
   }
   s_rr = block_sum(s_rr, red);
   s_dd = block_sum(s_dd, red);
@@ -264,6 +333,9 @@ __global__ void __launch_bounds__(CSR_THREADS) k_csr_rows(CsrPassArgs a) {
   }
 }
 
+// A'r: a warp per chunk of CHUNK CSC entries (one column); lane l sums
+// entries l, l+32, ... into 4 interleaved accumulators (8 loads in flight),
+// combined in a fixed order, then a fixed shuffle tree.
 __global__ void __launch_bounds__(CSR_THREADS) k_csc_chunks(CsrPassArgs a) {
   pdl_wait();
   const double *x, *r_prev;
@@ -275,25 +347,48 @@ __global__ void __launch_bounds__(CSR_THREADS) k_csc_chunks(CsrPassArgs a) {
   const int k = a.chunk_col[q];
   const int64_t lo = a.col_ptr[k] + (q - a.chunk_ptr[k]) * CHUNK;
   const int64_t hi = min(lo + CHUNK, a.col_ptr[k + 1]);
-  double s = 0.0;
-  for (int64_t p = lo + lane; p < hi; p += 32) s = fma(a.cval[p], r[a.crow[p]], s);
-  s = warp_sum(s);
+  constexpr int U = 8;  // accumulators: 16 loads in flight per lane, then 8 gathers
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  int64_t p = lo + lane;
+  for (; p + 32 * (U - 1) < hi; p += 32 * U) {
+    int ri[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ri[u] = a.crow[p + 32 * u];
+      v[u] = a.cval[p + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = fma(v[u], r[ri[u]], acc[u]);
+  }
+  for (; p < hi; p += 32) acc[0] = fma(a.cval[p], r[a.crow[p]], acc[0]);
+  double t = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) t += acc[u];
+  const double s = warp_sum(t);
   if (lane == 0) a.chunk_part[q] = s;
 }
 
+// Finish: warp w of the grid sums column w's chunk partials (lane-strided,
+// fixed tree); the last 4 warps sum the row kernel's norm partials.
 __global__ void __launch_bounds__(CSR_THREADS) k_csr_finish(CsrPassArgs a) {
   pdl_wait();
   if (a.mode != 0 && a.ctl->result.done) return;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < a.n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * (CSR_THREADS / 32) + (threadIdx.x >> 5);
+  if (w < a.n) {
     double s = 0.0;
-    for (int64_t q = a.chunk_ptr[t]; q < a.chunk_ptr[t + 1]; ++q) s += a.chunk_part[q];
-    a.cs[t] = s;
-  } else if (t < a.n + 4) {
-    const int w = static_cast<int>(t - a.n);
+    for (int64_t q = a.chunk_ptr[w] + lane; q < a.chunk_ptr[w + 1]; q += 32) s += a.chunk_part[q];
+    s = warp_sum(s);
+    if (lane == 0) a.cs[w] = s;
+  } else if (w < a.n + 4) {
+    const int k = static_cast<int>(w - a.n);
     double s = 0.0;
-    for (int g = 0; g < a.g1; ++g) s += a.row_part[4 * static_cast<int64_t>(g) + w];
-    a.cs[t] = s;
+    for (int g = lane; g < a.g1; g += 32) s += a.row_part[4 * static_cast<int64_t>(g) + k];
+    s = warp_sum(s);
+    if (lane == 0) a.cs[w] = s;
   }
 }
 
@@ -322,7 +417,7 @@ struct CsrPlan {
 };
 
 int csr_rows_grid(int64_t m) {
-  int64_t g = (m + CSR_THREADS - 1) / CSR_THREADS;
+  int64_t g = (m + 2 * RPL * CSR_THREADS - 1) / (2 * RPL * CSR_THREADS);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   return static_cast<int>(std::max<int64_t>(1, std::min(g, cap)));
 }
@@ -357,14 +452,19 @@ int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const doub
   a.xs = xs;
   a.rs = rs;
   a.mode = mode;
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_rows), dim3(P->g1), dim3(CSR_THREADS), 0, s, a));
+  static const bool attr = [] {
+    return allow_max_smem(reinterpret_cast<const void*>(k_csr_rows)) == cudaSuccess;
+  }();
+  (void)attr;
+  const size_t xsmem = (CSR_THREADS / 32) * ROW_STAGE * 12 + (P->n <= X_STAGE ? static_cast<size_t>(P->n) * 8 : 0);
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_rows), dim3(P->g1), dim3(CSR_THREADS), xsmem, s, a));
   count_launch();
   if (P->nchunks > 0) {
     const unsigned g2 = static_cast<unsigned>((P->nchunks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32));
     ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csc_chunks), dim3(g2), dim3(CSR_THREADS), 0, s, a));
     count_launch();
   }
-  const unsigned g3 = static_cast<unsigned>((P->n + 4 + CSR_THREADS - 1) / CSR_THREADS);
+  const unsigned g3 = static_cast<unsigned>((P->n + 4 + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32));
   ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_finish), dim3(g3), dim3(CSR_THREADS), 0, s, a));
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -423,7 +523,7 @@ extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, 
   P->col = col;
   P->val = val;
   P->g1 = csr_rows_grid(m);
-  P->rows_per_cta = (m + P->g1 - 1) / P->g1;
+  P->rows_per_cta = align_up((m + P->g1 - 1) / P->g1, 32 * RPL);
   std::vector<int64_t> hptr(n + 1, 0);
   auto fail = [&](int code) {
     cudaFreeAsync(scratch, s);
@@ -530,21 +630,23 @@ extern "C" int itsk_csr_sketch(const itsk_csr_plan* plan, const double* b, const
   ITSK_REQUIRE(d >= 1 && zeta >= 1 && ldw >= P->n + (b ? 1 : 0), "bad sketch shape");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const double scale = 1.0 / sqrt(static_cast<double>(zeta));  // embed.py:92
-  const int64_t ncol = P->n + (b ? 1 : 0);
   static const bool attr = [] {
     return allow_max_smem(reinterpret_cast<const void*>(k_sketch_csr)) == cudaSuccess;
   }();
   (void)attr;
-  const int64_t budget = 200 * 1024;
-  int warps = static_cast<int>(std::min<int64_t>(8, budget / (ncol * 8)));
+  const int64_t n = P->n;
+  const int64_t budget = 180 * 1024;
+  int warps = static_cast<int>(std::min<int64_t>(8, budget / (n * 8)));
   const int smem_acc = warps >= 1 ? 1 : 0;
   if (!smem_acc) warps = 8;
-  const size_t smem = smem_acc ? static_cast<size_t>(warps) * ncol * 8 : 0;
+  const size_t smem = smem_acc ? static_cast<size_t>(warps) * n * 8 : 0;
   const unsigned grid = static_cast<unsigned>((d + warps - 1) / warps);
-  k_sketch_csr<<<grid, 32 * warps, smem, s>>>(P->row_ptr, P->col, P->val, P->n, b, sk_ptr, sk_src, d, scale, SAb,
-                                              ldw, smem_acc);
+  k_sketch_csr<<<grid, 32 * warps, smem, s>>>(P->row_ptr, P->col, P->val, n, sk_ptr, sk_src, d, scale, SAb, ldw,
+                                              smem_acc);
   count_launch();
   ITSK_CHECK_LAUNCH();
+  // S·b into column n: the dense gather with no A columns (apply_vec's sum)
+  if (b) return itsk_sketch(nullptr, P->m, 0, 0, b, sk_ptr, sk_src, d, zeta, SAb + n, ldw, stream);
   return ITSK_OK;
 }
 
