@@ -25,9 +25,9 @@
 // Deterministic run to run; r is bitwise the reference's, c differs from the
 // reference's sequential sum by rounding only.
 #include <algorithm>
-#include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "itsk_common.cuh"
 #include "itsk_kernels.cuh"
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(CSR_THREADS) k_csc_chunks(CsrPassArgs a) {
   if (!resolve(a, x, r_prev, r)) return;
   const int lane = threadIdx.x & 31;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * (CSR_THREADS / 32) + (threadIdx.x >> 5);
-  if (q >= a.nchunks) return;
+  if (q >= a.chunk_ptr[a.n]) return;  // a.nchunks bounds the grid
   const int k = a.chunk_col[q];
   const int64_t lo = a.col_ptr[k] + (q - a.chunk_ptr[k]) * CHUNK;
   const int64_t hi = min(lo + CHUNK, a.col_ptr[k + 1]);
@@ -475,6 +475,36 @@ int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const doub
 
 using namespace itsk;
 
+namespace itsk {
+namespace {
+// chunks per column, then (after the scan) the chunk -> column map
+__global__ void k_chunk_count(const int64_t* __restrict__ col_ptr, int64_t n, int64_t* __restrict__ cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) cnt[k] = (col_ptr[k + 1] - col_ptr[k] + CHUNK - 1) / CHUNK;
+}
+__global__ void k_chunk_fill(const int64_t* __restrict__ chunk_ptr, int64_t n, int32_t* __restrict__ chunk_col) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  for (int64_t q = chunk_ptr[k]; q < chunk_ptr[k + 1]; ++q) chunk_col[q] = static_cast<int32_t>(k);
+}
+
+// keep freed stream-ordered allocations in the device pool (plans are made
+// per solve; returning the memory to the driver each time costs milliseconds)
+void retain_pool_memory() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+}  // namespace
+}  // namespace itsk
+
 extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t m,
                                     int64_t n, int64_t nnz, itsk_stream_t stream, itsk_csr_plan** plan) {
   ITSK_REQUIRE(plan && row_ptr && (nnz == 0 || (col && val)), "null pointer");
@@ -482,39 +512,7 @@ extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, 
   ITSK_REQUIRE(nnz < (1ll << 31) && m < (1ll << 31) && n < (1ll << 31), "CSR too large (nnz, m, n < 2^31)");
   *plan = nullptr;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // validate the structure on the device (monotone row_ptr, columns in range)
-  int* bad = nullptr;
-  ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s));
-  ITSK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  k_check_csr<<<static_cast<unsigned>((m + 1 + 255) / 256), 256, 0, s>>>(row_ptr, col, m, n, nnz, bad);
-  count_launch();
-  int hbad = 0;
-  ITSK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  ITSK_CUDA(cudaStreamSynchronize(s));
-  ITSK_CUDA(cudaFreeAsync(bad, s));
-  ITSK_REQUIRE(hbad == 0, "invalid CSR structure (%s)", (hbad & 1) ? "row_ptr" : "column index out of range");
-
-  // sort scratch (freed before return)
-  const int bits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(n)));
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, static_cast<int>(std::max<int64_t>(nnz, 1)),
-                                  0, bits, s);
-  Carver sc(nullptr, 1ll << 62);
-  sc.take<uint32_t>(nnz);  // keys out
-  sc.take<uint32_t>(nnz);  // iota
-  sc.take<uint32_t>(nnz);  // perm
-  sc.take<uint32_t>(nnz);  // entry rows
-  sc.take<char>(static_cast<int64_t>(cub_bytes));
-  void* scratch = nullptr;
-  ITSK_CUDA(cudaMallocAsync(&scratch, std::max<int64_t>(sc.off, 256), s));
-  Carver c2(scratch, 1ll << 62);
-  uint32_t* keys = c2.take<uint32_t>(nnz);
-  uint32_t* iota = c2.take<uint32_t>(nnz);
-  uint32_t* perm = c2.take<uint32_t>(nnz);
-  uint32_t* erow = c2.take<uint32_t>(nnz);
-  void* cub_tmp = c2.take<char>(static_cast<int64_t>(cub_bytes));
-
+  retain_pool_memory();
   CsrPlan* P = new CsrPlan();
   P->m = m;
   P->n = n;
@@ -524,83 +522,98 @@ extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, 
   P->val = val;
   P->g1 = csr_rows_grid(m);
   P->rows_per_cta = align_up((m + P->g1 - 1) / P->g1, 32 * RPL);
-  std::vector<int64_t> hptr(n + 1, 0);
+  P->nchunks = n + (nnz + CHUNK - 1) / CHUNK;  // upper bound; the count is chunk_ptr[n]
+  const int bits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(n)));
+  const int nsort = static_cast<int>(std::max<int64_t>(nnz, 1));
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, nsort, 0, bits, s);
+  cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                static_cast<int>(n), s);
+  // one stream-ordered allocation: the plan's arrays, then creation scratch
+  Carver cv(nullptr, 1ll << 62);
+  auto layout = [&](Carver& c, bool assign) {
+    int64_t* a0 = c.take<int64_t>(n + 1);
+    int32_t* a1 = c.take<int32_t>(nnz);
+    double* a2 = c.take<double>(nnz);
+    int32_t* a3 = c.take<int32_t>(P->nchunks);
+    int64_t* a4 = c.take<int64_t>(n + 1);
+    double* a5 = c.take<double>(P->nchunks);
+    double* a6 = c.take<double>(4 * static_cast<int64_t>(P->g1));
+    double* a7 = c.take<double>(m);
+    int* a8 = c.take<int>(1);
+    if (assign) {
+      P->col_ptr = a0; P->crow = a1; P->cval = a2; P->chunk_col = a3;
+      P->chunk_ptr = a4; P->chunk_part = a5; P->row_part = a6; P->r_tmp = a7;
+    }
+    return a8;
+  };
+  layout(cv, false);
+  const int64_t keep = cv.off;
+  cv.take<uint32_t>(nnz);  // sorted keys
+  cv.take<uint32_t>(nnz);  // iota
+  cv.take<uint32_t>(nnz);  // permutation
+  cv.take<uint32_t>(nnz);  // entry rows
+  cv.take<int64_t>(n);     // chunk counts
+  cv.take<char>(static_cast<int64_t>(std::max(sort_bytes, scan_bytes)));
   auto fail = [&](int code) {
-    cudaFreeAsync(scratch, s);
-    if (P->pool) cudaFree(P->pool);
+    if (P->pool) cudaFreeAsync(P->pool, s);
     delete P;
     return code;
   };
-  // CSC: stable sort of the entry ids by column (entries are in row order)
-  int64_t* col_ptr_tmp = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&col_ptr_tmp), sizeof(int64_t) * (n + 1), s) != cudaSuccess) {
-    set_error("csr plan: allocation failed");
-    return fail(ITSK_ECUDA);
+  if (cudaMallocAsync(&P->pool, cv.off + 256, s) != cudaSuccess) {
+    set_error("csr plan: device allocation of %lld bytes failed", (long long)cv.off);
+    cudaGetLastError();
+    delete P;
+    return ITSK_ECUDA;
   }
-  if (nnz > 0) {
-    k_entry_rows<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(row_ptr, m, erow);
-    k_iota<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(iota, nnz);
-    count_launch(2);
-    cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, reinterpret_cast<const uint32_t*>(col), keys, iota, perm,
-                                    static_cast<int>(nnz), 0, bits, s);
-    k_col_ptr<<<static_cast<unsigned>((n + 1 + 255) / 256), 256, 0, s>>>(keys, nnz, n, col_ptr_tmp);
-    count_launch(2);
-  } else {
-    cudaMemsetAsync(col_ptr_tmp, 0, sizeof(int64_t) * (n + 1), s);
-  }
-  if (cudaMemcpyAsync(hptr.data(), col_ptr_tmp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess) {
-    set_error("csr plan: %s", cudaGetErrorString(cudaGetLastError()));
-    cudaFreeAsync(col_ptr_tmp, s);
-    return fail(ITSK_ECUDA);
-  }
-  // chunk table (host; one-time)
-  std::vector<int64_t> cptr(n + 1, 0);
-  for (int64_t k = 0; k < n; ++k) cptr[k + 1] = cptr[k] + (hptr[k + 1] - hptr[k] + CHUNK - 1) / CHUNK;
-  P->nchunks = cptr[n];
-  std::vector<int32_t> ccol(std::max<int64_t>(P->nchunks, 1));
-  for (int64_t k = 0; k < n; ++k)
-    for (int64_t q = cptr[k]; q < cptr[k + 1]; ++q) ccol[q] = static_cast<int32_t>(k);
-  Carver pc(nullptr, 1ll << 62);
-  pc.take<int64_t>(n + 1);
-  pc.take<int32_t>(nnz);
-  pc.take<double>(nnz);
-  pc.take<int32_t>(std::max<int64_t>(P->nchunks, 1));
-  pc.take<int64_t>(n + 1);
-  pc.take<double>(std::max<int64_t>(P->nchunks, 1));
-  pc.take<double>(4 * static_cast<int64_t>(P->g1));
-  pc.take<double>(m);
-  if (cudaMalloc(&P->pool, pc.off + 256) != cudaSuccess) {
-    set_error("csr plan: device allocation of %lld bytes failed", (long long)pc.off);
-    cudaFreeAsync(col_ptr_tmp, s);
-    return fail(ITSK_ECUDA);
-  }
-  Carver pv(P->pool, 1ll << 62);
-  P->col_ptr = pv.take<int64_t>(n + 1);
-  P->crow = pv.take<int32_t>(nnz);
-  P->cval = pv.take<double>(nnz);
-  P->chunk_col = pv.take<int32_t>(std::max<int64_t>(P->nchunks, 1));
-  P->chunk_ptr = pv.take<int64_t>(n + 1);
-  P->chunk_part = pv.take<double>(std::max<int64_t>(P->nchunks, 1));
-  P->row_part = pv.take<double>(4 * static_cast<int64_t>(P->g1));
-  P->r_tmp = pv.take<double>(m);
-  cudaError_t e = cudaMemcpyAsync(P->col_ptr, col_ptr_tmp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(P->chunk_col, ccol.data(), sizeof(int32_t) * ccol.size(), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(P->chunk_ptr, cptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && nnz > 0) {
-    k_csc_gather<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm, erow, val, nnz, P->crow, P->cval);
-    count_launch();
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
-  cudaFreeAsync(col_ptr_tmp, s);
+  Carver c2(P->pool, 1ll << 62);
+  int* bad = layout(c2, true);
+  uint32_t* keys = c2.take<uint32_t>(nnz);
+  uint32_t* iota = c2.take<uint32_t>(nnz);
+  uint32_t* perm = c2.take<uint32_t>(nnz);
+  uint32_t* erow = c2.take<uint32_t>(nnz);
+  int64_t* ccnt = c2.take<int64_t>(n);
+  void* tmp = c2.take<char>(static_cast<int64_t>(std::max(sort_bytes, scan_bytes)));
+  (void)keep;
+  // validate the structure (monotone row_ptr, columns in range): the one sync
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+  k_check_csr<<<static_cast<unsigned>((m + 1 + 255) / 256), 256, 0, s>>>(row_ptr, col, m, n, nnz, bad);
+  count_launch();
+  int hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     set_error("csr plan: %s", cudaGetErrorString(e));
     return fail(ITSK_ECUDA);
   }
-  cudaFreeAsync(scratch, s);
+  if (hbad) {
+    set_error("invalid CSR structure (%s)", (hbad & 1) ? "row_ptr" : "column index out of range");
+    return fail(ITSK_EINVAL);
+  }
+  // CSC: stable radix sort of the entry ids by column (entries are in row order)
+  if (nnz > 0) {
+    k_entry_rows<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(row_ptr, m, erow);
+    k_iota<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(iota, nnz);
+    cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, reinterpret_cast<const uint32_t*>(col), keys, iota, perm,
+                                    static_cast<int>(nnz), 0, bits, s);
+    k_col_ptr<<<static_cast<unsigned>((n + 1 + 255) / 256), 256, 0, s>>>(keys, nnz, n, P->col_ptr);
+    k_csc_gather<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm, erow, val, nnz, P->crow, P->cval);
+    count_launch(5);
+  } else {
+    cudaMemsetAsync(P->col_ptr, 0, sizeof(int64_t) * (n + 1), s);
+  }
+  // chunk table on the device: counts, inclusive scan into chunk_ptr[1..n], fill
+  k_chunk_count<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P->col_ptr, n, ccnt);
+  cudaMemsetAsync(P->chunk_ptr, 0, sizeof(int64_t), s);
+  cub::DeviceScan::InclusiveSum(tmp, scan_bytes, ccnt, P->chunk_ptr + 1, static_cast<int>(n), s);
+  k_chunk_fill<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(P->chunk_ptr, n, P->chunk_col);
+  count_launch(3);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("csr plan: %s", cudaGetErrorString(e));
+    return fail(ITSK_ECUDA);
+  }
   *plan = reinterpret_cast<itsk_csr_plan*>(P);
   return ITSK_OK;
 }
@@ -608,8 +621,8 @@ extern "C" int itsk_csr_plan_create(const int64_t* row_ptr, const int32_t* col, 
 extern "C" void itsk_csr_plan_destroy(itsk_csr_plan* plan) {
   if (!plan) return;
   CsrPlan* P = reinterpret_cast<CsrPlan*>(plan);
-  cudaDeviceSynchronize();
-  if (P->pool) cudaFree(P->pool);
+  cudaDeviceSynchronize();  // no stream still reads the plan
+  if (P->pool) cudaFreeAsync(P->pool, 0);
   delete P;
 }
 
