@@ -91,6 +91,15 @@ int itsk_pattern_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_
 int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                 const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
                 double* SAb, int64_t ldw, itsk_stream_t stream);
+/* The same sum restricted to the source rows [row0, row1), continuing from
+ * SAb's current values when `accumulate` is set: windows taken in row order
+ * give the bitwise result of one itsk_sketch call, so A can be sketched
+ * chunk by chunk while it is still being copied to the device. A points to
+ * row 0 (only rows row0..row1-1 are read). */
+int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                     const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
+                     double* SAb, int64_t ldw, int64_t row0, int64_t row1, int accumulate,
+                     itsk_stream_t stream);
 
 /* ----------------------------------------------------------------------
  * Householder QR of the d x n sketch with the reflectors also applied to

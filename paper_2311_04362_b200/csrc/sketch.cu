@@ -17,11 +17,30 @@
 namespace itsk {
 namespace {
 
+// Source-row window of one launch: only sources j in [j0, j1) are summed,
+// continuing from W's current value when `accum` is set.  Sources are
+// ascending in each sketch row's list, so consecutive windows in row order
+// add the same terms in the same order as one launch over all rows — the
+// upload pipeline sketches A chunk by chunk as it arrives, bitwise the same.
+struct SkRange {
+  uint32_t j0, j1;
+  int accum;
+};
+
+__device__ __forceinline__ uint32_t lower_src(const uint32_t* __restrict__ src, uint32_t lo, uint32_t hi,
+                                              uint32_t key) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((src[mid] & 0x7fffffffu) < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 template <int CPL, int UNR>
 __global__ void __launch_bounds__(128) k_sketch_gather(
     const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
     const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d,
-    double scale, double* __restrict__ W, int64_t ldw) {
+    double scale, double* __restrict__ W, int64_t ldw, SkRange rg) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (i >= d) return;
@@ -37,8 +56,13 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   const double* Ac = A + c0 + lane;
   double acc[CPL];
 #pragma unroll
-  for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
-  const uint32_t e0 = ptr[i], e1 = ptr[i + 1];
+  for (int q = 0; q < CPL; ++q) {
+    const int64_t col = c0 + lane + 32 * q;
+    acc[q] = (rg.accum && col < ncol) ? W[i * ldw + col] : 0.0;
+  }
+  uint32_t e0 = ptr[i], e1 = ptr[i + 1];
+  if (rg.j0 > 0) e0 = lower_src(src, e0, e1, rg.j0);
+  if (rg.j1 != 0xffffffffu) e1 = lower_src(src, e0, e1, rg.j1);
   for (uint32_t e = e0; e < e1; e += 32) {
     const uint32_t mine = (e + lane < e1) ? src[e + lane] : 0u;
     const int cnt = static_cast<int>(min(32u, e1 - e));
@@ -95,11 +119,11 @@ SketchTune sketch_tune() { return SketchTune(); }
 template <int CPL, int UNR>
 int launch_gather(const double* A, int64_t lda, int64_t n, const double* b,
                   const uint32_t* ptr, const uint32_t* src, int64_t d, double scale, double* W,
-                  int64_t ldw, cudaStream_t s) {
+                  int64_t ldw, SkRange rg, cudaStream_t s) {
   const int64_t ncol = n + (b ? 1 : 0);
   dim3 grid(static_cast<unsigned>((d * 32 + 127) / 128),
             static_cast<unsigned>((ncol + 32 * CPL - 1) / (32 * CPL)));
-  k_sketch_gather<CPL, UNR><<<grid, 128, 0, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw);
+  k_sketch_gather<CPL, UNR><<<grid, 128, 0, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw, rg);
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
@@ -113,7 +137,19 @@ using namespace itsk;
 extern "C" int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                            const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d,
                            int64_t zeta, double* SAb, int64_t ldw, itsk_stream_t stream) {
+  return itsk_sketch_rows(A, m, n, lda, b, sk_ptr, sk_src, d, zeta, SAb, ldw, 0, m, 0, stream);
+}
+
+extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                                const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
+                                double* SAb, int64_t ldw, int64_t row0, int64_t row1, int accumulate,
+                                itsk_stream_t stream) {
   ITSK_REQUIRE(m >= 1 && n >= 0 && d >= 1 && zeta >= 1, "bad sketch shape");
+  ITSK_REQUIRE(0 <= row0 && row0 <= row1 && row1 <= m && m < (1ll << 31), "bad source-row window");
+  SkRange rg;
+  rg.j0 = static_cast<uint32_t>(row0);
+  rg.j1 = row1 >= m ? 0xffffffffu : static_cast<uint32_t>(row1);
+  rg.accum = accumulate ? 1 : 0;
   ITSK_REQUIRE(lda >= n && ldw >= n + (b ? 1 : 0), "bad leading dimension");
   ITSK_REQUIRE(sk_ptr && sk_src && SAb && (A || n == 0), "null pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -135,11 +171,11 @@ extern "C" int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, c
   if (need > cap) need = cap;
   const int unr = tu.unr > 0 ? tu.unr : (need <= 2 ? 8 : 4);
 #define ITSK_G(CPLV, UNRV) \
-  if (unr == UNRV) return launch_gather<CPLV, UNRV>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
-  if (need <= 1) { ITSK_G(1, 8) ITSK_G(1, 2) return launch_gather<1, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
-  if (need <= 2) { ITSK_G(2, 8) ITSK_G(2, 2) return launch_gather<2, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
-  if (need <= 4) { ITSK_G(4, 8) ITSK_G(4, 2) return launch_gather<4, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s); }
+  if (unr == UNRV) return launch_gather<CPLV, UNRV>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
+  if (need <= 1) { ITSK_G(1, 8) ITSK_G(1, 2) return launch_gather<1, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s); }
+  if (need <= 2) { ITSK_G(2, 8) ITSK_G(2, 2) return launch_gather<2, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s); }
+  if (need <= 4) { ITSK_G(4, 8) ITSK_G(4, 2) return launch_gather<4, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s); }
   ITSK_G(8, 8) ITSK_G(8, 2)
 #undef ITSK_G
-  return launch_gather<8, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, s);
+  return launch_gather<8, 4>(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
 }

@@ -223,6 +223,7 @@ class _Workspace:
         self.x_true = torch.empty(n, **f64) if with_truth else None
         self.r_true = torch.empty(m, **f64) if with_truth else None
         self.A = None  # upload buffer for host A (allocated on demand)
+        self.copy_stream = None  # side stream of the chunked upload
         self.graph = None
         self.graph_key = None
         self.last_residuals = None
@@ -278,15 +279,46 @@ def release_workspaces() -> None:
 # ---------------------------------------------------------------------------
 # The solve
 # ---------------------------------------------------------------------------
-def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None):
+_PIPE_MIN_BYTES = 32 << 20   # host A at least this large is uploaded in chunks
+_PIPE_CHUNK_BYTES = 48 << 20
+
+
+def _upload_chunks(m: int, n: int) -> list[tuple[int, int]]:
+    k = max(2, min(8, -(-8 * m * n // _PIPE_CHUNK_BYTES)))
+    step = -(-m // k)
+    return [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
+
+
+def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None, upload=None):
     """Pattern, S·[A|b], QR, x0, normest, condest — solvers.py:332-337
-    (S·A by apply_sparse for a CSR A, solvers.py:195-196)."""
+    (S·A by apply_sparse for a CSR A, solvers.py:195-196).
+
+    upload: a host matrix still to be copied into `at` (= ws.A).  The copy
+    runs on a side stream in row chunks; the pattern is drawn while the first
+    chunk is in flight and each chunk is sketched as soon as it lands
+    (itsk_sketch_rows continues every sum in source order, so S·[A|b] is
+    bitwise the one-shot result)."""
     m, n, d, zeta = ws.m, ws.n, ws.d, ws.zeta
+    compute = torch.cuda.current_stream(ws.dev)
+    if upload is not None:
+        if ws.copy_stream is None:
+            ws.copy_stream = torch.cuda.Stream(ws.dev)
+        ws.copy_stream.wait_stream(compute)  # earlier work on this stream still reads ws.A
     words, has32, pend = pcg_state(cfg.rng_seed)
     _lib.check(lib.itsk_sparse_sign_pattern(
         d, m, zeta, words, has32, pend, _dev.ptr(ws.rows), _dev.ptr(ws.neg), _dev.ptr(ws.sk_ptr),
         _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
-    if csr is not None:
+    if upload is not None:
+        for k, (r0, r1) in enumerate(_upload_chunks(m, n)):
+            with torch.cuda.stream(ws.copy_stream):
+                at[r0:r1].copy_(upload[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(ws.copy_stream)
+            compute.wait_event(ev)
+            _lib.check(lib.itsk_sketch_rows(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
+                                            _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, r0, r1,
+                                            1 if k else 0, stream))
+    elif csr is not None:
         _lib.check(lib.itsk_csr_sketch(csr.plan, _dev.ptr(bt), _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), d, zeta,
                                        _dev.ptr(ws.W), n + 1, stream))
     else:
@@ -425,6 +457,7 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
     r_slots = cfg.max_iters + 1 if residuals == "all" else 2
     ws = _workspace(dev, m, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots, truth is not None)
     csr = None
+    upload = None
     if is_sparse(a):
         # sparse A (solvers.py:195-196; section 3.5): CSR pass + CSC copy
         if cfg.track_be:
@@ -437,7 +470,11 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
         arr = np.asarray(a, dtype=np.float64)
         if ws.A is None:
             ws.A = torch.empty((m, n), dtype=torch.float64, device=dev)
-        ws.A.copy_(torch.from_numpy(np.ascontiguousarray(arr)), non_blocking=True)
+        host_a = torch.from_numpy(np.ascontiguousarray(arr))
+        if 8 * m * n >= _PIPE_MIN_BYTES:
+            upload = host_a  # copied chunk by chunk under the pattern and the sketch
+        else:
+            ws.A.copy_(host_a, non_blocking=True)
         at, lda = ws.A, n
     bsrc = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(b, dtype=np.float64)))
     if bsrc.shape[0] != m:
@@ -449,7 +486,7 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
             ws.r_true.copy_(_dev.as_device_vector(truth.r, dev))
     stream_obj = torch.cuda.current_stream(dev)
     stream = int(stream_obj.cuda_stream)
-    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr)
+    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr, upload)
     p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr)
     run_loop(lib, ws, p, use_graph, stream)
     res = _read_result(lib, ws, p, stream_obj)

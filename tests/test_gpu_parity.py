@@ -444,6 +444,45 @@ def test_device_tensor_inputs_zero_copy(pkg):
     assert np.array_equal(r_host.solution, r_view.solution)
 
 
+def test_chunked_upload_and_sketch_windows_bitwise(pkg, orc):
+    """A host A >= 32 MB is uploaded in row chunks and sketched window by
+    window as it lands (itsk_sketch_rows): the solve is bitwise the one from
+    the device-resident A, and any row windows taken in order reproduce the
+    one-shot sketch bit for bit."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    m, n = 40000, 120  # 38 MB -> the pipelined path
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((m, n)) / np.sqrt(m)
+    b = rng.standard_normal(m)
+    cfg = pkg.SolverConfig(d=2400, max_iters=12, rng_seed=7)
+    pinned = torch.from_numpy(a).pin_memory()
+    r_host = pkg.iterative_sketching(pinned.numpy(), b, cfg)
+    r_page = pkg.iterative_sketching(a, b, cfg)
+    r_dev = pkg.iterative_sketching(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg)
+    assert np.array_equal(r_host.solution, r_dev.solution)
+    assert np.array_equal(r_page.solution, r_dev.solution)
+    # windows
+    s = pkg.sparse_sign_new(500, 3000, 8, 3)
+    a2 = torch.from_numpy(rng.standard_normal((3000, 37))).cuda()
+    b2 = torch.from_numpy(rng.standard_normal(3000)).cuda()
+    ref = s.apply_dense(a2, b2)
+    lib = dv.lib(a2.device)
+    for cuts in ([0, 3000], [0, 1, 1500, 1501, 3000], [0, 700, 700, 2999, 3000]):
+        w = torch.full((500, 38), float("nan"), dtype=torch.float64, device=a2.device)
+        for k in range(len(cuts) - 1):
+            _lib.check(lib.itsk_sketch_rows(dv.ptr(a2), 3000, 37, 37, dv.ptr(b2), dv.ptr(s.ptr_dev), dv.ptr(s.src_dev),
+                                            500, 8, dv.ptr(w), 38, cuts[k], cuts[k + 1], 1 if k else 0,
+                                            dv.stream_ptr()))
+        assert torch.equal(w, ref), cuts
+    assert lib.itsk_sketch_rows(dv.ptr(a2), 3000, 37, 37, dv.ptr(b2), dv.ptr(s.ptr_dev), dv.ptr(s.src_dev), 500, 8,
+                                dv.ptr(w), 38, 10, 5, 0, dv.stream_ptr()) == _lib.ITSK_EINVAL
+    del ctypes
+
+
 def test_edge_configs(pkg, orc):
     # zeta == d, zeta == 1, odd n, residuals="last", extra_iters
     for (m, n, d, zeta) in [(300, 7, 10, 10), (500, 9, 40, 1), (2001, 33, 300, 3)]:
