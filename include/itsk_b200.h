@@ -112,6 +112,11 @@ int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t lda, const d
 int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes);
 int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
                 void* ws, int64_t ws_bytes, itsk_stream_t stream);
+/* The same without the host round trip: the "exact zero on diag(R)" flag
+ * (1/0) is copied to the device int *singular on the stream; the caller
+ * raises SingularMatrixError when it reads the flag with its results. */
+int itsk_qr_aug_async(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z, void* ws,
+                      int64_t ws_bytes, int* singular, itsk_stream_t stream);
 
 /* tri_solve_upper (linalg.py:59-62, trans=0: R y = c) and
  * tri_solve_upper_transpose (linalg.py:65-68, trans=1: R' y = c). */

@@ -555,8 +555,11 @@ extern "C" int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes) {
   return ITSK_OK;
 }
 
-extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
-                           void* ws, int64_t ws_bytes, itsk_stream_t stream) {
+namespace {
+// Launches the factorisation; *flag receives the device address of the
+// "exact zero on diag(R)" flag (read by the caller, synchronously or not).
+int qr_aug_core(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z, void* ws, int64_t ws_bytes,
+                itsk_stream_t stream, int** flag) {
   ITSK_REQUIRE(W && R && ws, "null pointer");
   ITSK_REQUIRE(n >= 1 && d >= n, "need m >= n, got %lld x %lld", (long long)d, (long long)n);
   const int has_rhs = z != nullptr;
@@ -575,13 +578,7 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
     double* wsd = reinterpret_cast<double*>(static_cast<char*>(ws) + V2_WS_OFFSET);
     int rc = launch_qr_v2(W, d, n, ldw, n + has_rhs, R, z, sing, wsd, V2, s);
     if (rc) return rc;
-    int singular = 0;
-    ITSK_CUDA(cudaMemcpyAsync(&singular, sing, sizeof(int), cudaMemcpyDeviceToHost, s));
-    ITSK_CUDA(cudaStreamSynchronize(s));
-    if (singular) {
-      set_error("zero diagonal entry in triangular factor");
-      return ITSK_ESINGULAR;
-    }
+    *flag = sing;
     return ITSK_OK;
   }
   ITSK_CUDA(cudaMemsetAsync(L.bar, 0, 512, s));
@@ -593,13 +590,7 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   if (tsqr_c > 0) {
     int rc = launch_qr_tsqr(W, d, n, ldw, n + has_rhs, R, z, L.singular, tsqr_c, tsqr_smem, s);
     if (rc) return rc;
-    int singular = 0;
-    ITSK_CUDA(cudaMemcpyAsync(&singular, L.singular, sizeof(int), cudaMemcpyDeviceToHost, s));
-    ITSK_CUDA(cudaStreamSynchronize(s));
-    if (singular) {
-      set_error("zero diagonal entry in triangular factor");
-      return ITSK_ESINGULAR;
-    }
+    *flag = L.singular;
     return ITSK_OK;
   }
   QrArgs a;
@@ -643,13 +634,36 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
                                           dim3(QR_THREADS), args, L.smem, s));
   }
   count_launch();
+  *flag = L.singular;
+  return ITSK_OK;
+}
+}  // namespace
+
+
+extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
+                           void* ws, int64_t ws_bytes, itsk_stream_t stream) {
+  int* flag = nullptr;
+  int rc = qr_aug_core(W, d, n, ldw, R, z, ws, ws_bytes, stream, &flag);
+  if (rc) return rc;
   int singular = 0;
-  ITSK_CUDA(cudaMemcpyAsync(&singular, L.singular, sizeof(int), cudaMemcpyDeviceToHost, s));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  ITSK_CUDA(cudaMemcpyAsync(&singular, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   ITSK_CUDA(cudaStreamSynchronize(s));
   if (singular) {
     set_error("zero diagonal entry in triangular factor");
     return ITSK_ESINGULAR;
   }
+  return ITSK_OK;
+}
+
+extern "C" int itsk_qr_aug_async(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z, void* ws,
+                                 int64_t ws_bytes, int* singular, itsk_stream_t stream) {
+  ITSK_REQUIRE(singular, "null singular flag");
+  int* flag = nullptr;
+  int rc = qr_aug_core(W, d, n, ldw, R, z, ws, ws_bytes, stream, &flag);
+  if (rc) return rc;
+  ITSK_CUDA(cudaMemcpyAsync(singular, flag, sizeof(int), cudaMemcpyDeviceToDevice,
+                            reinterpret_cast<cudaStream_t>(stream)));
   return ITSK_OK;
 }
 

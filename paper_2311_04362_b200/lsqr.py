@@ -33,7 +33,8 @@ import torch
 from . import _lib
 from . import device as _dev
 from .problems import Truth
-from .solvers import (DeviceResiduals, SolverConfig, SolveResult, SolveTrace, _sketch_qr_x0, _workspace)
+from .solvers import (DeviceResiduals, SolverConfig, SolveResult, SolveTrace, _sketch_qr_x0, _workspace,
+                      check_singular)
 
 
 class _DeviceLs:
@@ -170,6 +171,8 @@ def sketch_and_precondition(a, b, cfg: SolverConfig, truth: Truth | None = None,
     stream = _dev.stream_ptr()
     _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream)
     est = ws.est.cpu().numpy()
+    ws.sing_host.copy_(ws.sing)
+    check_singular(ws)
     trace = SolveTrace(normest=float(est[0]), condest=float(est[1]))
     x0 = ws.xs[0].cpu().numpy()
     r_true = None

@@ -224,6 +224,11 @@ class _Workspace:
         self.r_true = torch.empty(m, **f64) if with_truth else None
         self.A = None  # upload buffer for host A (allocated on demand)
         self.copy_stream = None  # side stream of the chunked upload
+        self.est_stream = None   # side stream of condest
+        self.sing = torch.zeros(1, dtype=torch.int32, device=dev)  # QR zero-pivot flag
+        self.sing_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.v0_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        self.v0_seed = None
         self.graph = None
         self.graph_key = None
         self.last_residuals = None
@@ -304,6 +309,11 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
         if ws.copy_stream is None:
             ws.copy_stream = torch.cuda.Stream(ws.dev)
         ws.copy_stream.wait_stream(compute)  # earlier work on this stream still reads ws.A
+    # normest / condest start vector (linalg.py:96): host draw, pinned, async
+    if ws.v0_seed != cfg.rng_seed:
+        ws.v0_host.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
+        ws.v0_seed = cfg.rng_seed
+    ws.v0.copy_(ws.v0_host, non_blocking=True)
     words, has32, pend = pcg_state(cfg.rng_seed)
     _lib.check(lib.itsk_sparse_sign_pattern(
         d, m, zeta, words, has32, pend, _dev.ptr(ws.rows), _dev.ptr(ws.neg), _dev.ptr(ws.sk_ptr),
@@ -324,18 +334,33 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
     else:
         _lib.check(lib.itsk_sketch(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
                                    _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, stream))
-    _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
-                               _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
+    # no host round trip: the zero-pivot flag is read with the results
+    _lib.check(lib.itsk_qr_aug_async(_dev.ptr(ws.W), d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
+                                     _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), _dev.ptr(ws.sing), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
+    # condest (a 2-CTA cluster, the longest of the three) runs beside x0 and
+    # normest (one CTA each) on a side stream
+    if ws.est_stream is None:
+        ws.est_stream = torch.cuda.Stream(ws.dev)
+    ws.est_stream.wait_stream(compute)
+    est_ptr = _dev.ptr(ws.est)
+    with torch.cuda.stream(ws.est_stream):
+        _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, _dev.ptr(ws.Rp),
+                                    int(ws.est_stream.cuda_stream)))
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
         _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
-    ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)), non_blocking=False)
-    est_ptr = _dev.ptr(ws.est)
     _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
                                 _dev.ptr(ws.Rp), stream))
-    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, _dev.ptr(ws.Rp), stream))
+    compute.wait_stream(ws.est_stream)
+
+
+def check_singular(ws: _Workspace) -> None:
+    """The QR's zero-pivot flag (itsk_qr_aug_async) -> SingularMatrixError,
+    as tri_solve_upper raises it in sketch_and_solve (linalg.py:54-55)."""
+    if int(ws.sing_host[0]) != 0:
+        raise SingularMatrixError("zero diagonal entry in triangular factor")
 
 
 def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None, csr=None):
@@ -386,7 +411,9 @@ def _read_result(lib, ws: _Workspace, p, stream_obj) -> _lib.LoopResult:
     hb[:nxs].copy_(ws.xs.view(-1), non_blocking=True)
     hb[nxs:nxs + ws.trace.numel()].copy_(ws.trace.view(-1), non_blocking=True)
     hb[nxs + ws.trace.numel():nxs + ws.trace.numel() + 2].copy_(ws.est, non_blocking=True)
+    ws.sing_host.copy_(ws.sing, non_blocking=True)
     stream_obj.synchronize()
+    check_singular(ws)
     return _lib.LoopResult.from_buffer_copy(bytes(host.numpy()))
 
 
