@@ -146,6 +146,11 @@ int itsk_normest(const double* R, int64_t n, const double* v0, int64_t steps, do
 int itsk_condest_workspace(int64_t n, int64_t* doubles);
 int itsk_condest(const double* R, int64_t n, const double* v0, double* out, const double* Rp,
                  itsk_stream_t stream);
+/* The same estimate with the (R'R)^{-1} Lanczos run on X = R^{-1} (formed
+ * once into ws, itsk_condest_workspace doubles) by matrix-vector products
+ * instead of two triangular solves per step. */
+int itsk_condest_ws(const double* R, int64_t n, const double* v0, double* out, const double* Rp,
+                    double* ws, int64_t ws_doubles, itsk_stream_t stream);
 
 /* ----------------------------------------------------------------------
  * The fused pass of the refinement loop (solvers.py:290,299,343 — r = b-Ax

@@ -80,6 +80,7 @@ _SIGS = {
     "itsk_pack_upper": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp]),
     "itsk_condest_workspace": (ctypes.c_int, [c_i64, ctypes.POINTER(c_i64)]),
     "itsk_condest": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, c_dp, c_dp]),
+    "itsk_condest_ws": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, c_dp, c_dp, c_i64, c_dp]),
     "itsk_pass_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_fused_pass": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp,
                                        c_dp, c_i64, c_dp]),

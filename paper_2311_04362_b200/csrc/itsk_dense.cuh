@@ -390,33 +390,33 @@ __device__ __forceinline__ void trmv_n(const RA& R, int n64, const double* v, do
   __syncthreads();
 }
 
-// out := R' v : per 32-column block, warps split the i-range, lanes the
-// columns (contiguous row segments); fixed-order sum of the warp partials
+// out := R' v : a warp owns a 32-column block (lane = column j) and runs the
+// rows i <= j of that block down two interleaved chains (even / odd i), so
+// there is no cross-warp reduction and one barrier at the end.  Row segments
+// are contiguous (conflict-free), v[i] is a broadcast.
 template <class RA>
 __device__ __forceinline__ void trmv_t(const RA& R, int n64, const double* v, double* out,
                                        double* red) {
+  (void)red;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = static_cast<int>(n64);
   const int nw = blockDim.x >> 5;
-  for (int b0 = 0; b0 < n; b0 += 32) {
-    const int bs = static_cast<int>(min(32, n - b0));
-    const int top = b0 + bs;  // rows i < top contribute to this block
-    const int k_lo = (top * warp) / nw, k_hi = (top * (warp + 1)) / nw;
-    double acc = 0.0;
-    const int j = min(b0 + lane, n - 1);
-    for (int i = k_lo; i < k_hi; ++i) {
-      const double rv = R(i, j);
-      acc = fma(i <= j ? rv : 0.0, v[i], acc);
+  const int nblk = (n + 31) / 32;
+  // heaviest blocks (the last ones) first
+  for (int bb = warp; bb < nblk; bb += nw) {
+    const int b = nblk - 1 - bb;
+    const int j = 32 * b + lane;
+    const int jj = min(j, n - 1);
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+    for (; i + 1 <= jj; i += 2) {
+      a0 = fma(R(i, jj), v[i], a0);
+      a1 = fma(R(i + 1, jj), v[i + 1], a1);
     }
-    red[warp * 32 + lane] = (lane < bs) ? acc : 0.0;
-    __syncthreads();
-    if (warp == 0 && lane < bs) {
-      double sum = 0.0;
-      for (int w = 0; w < nw; ++w) sum += red[w * 32 + lane];
-      out[b0 + lane] = sum;
-    }
-    __syncthreads();
+    if (i == jj) a0 = fma(R(i, jj), v[i], a0);
+    if (j < n) out[j] = a0 + a1;
   }
+  __syncthreads();
 }
 
 __device__ __forceinline__ double dot_sm(const double* a, const double* b, int64_t n, double* red) {

