@@ -371,8 +371,8 @@ template <int NB>
 __global__ void __launch_bounds__(256) k_qr_y(UpdArgs a) {
   constexpr int MT = NB / 8, NT = UT / 8;
   constexpr int TPW = (MT * NT + 7) / 8;  // tiles per warp (8 warps)
-  constexpr int VS = NB + 1;              // strides (8-byte cp.async: any alignment)
-  constexpr int WS = UT + 1;
+  constexpr int VS = NB + 4;              // strides = 4 mod 16: conflict-free DMMA fragments
+  constexpr int WS = UT + 4;
   extern __shared__ __align__(16) double ysm[];
   double* Vt = ysm;                  // 2 x YRT x VS
   double* Wt = Vt + 2 * YRT * VS;    // 2 x YRT x WS
@@ -493,7 +493,7 @@ template <int NB>
 __global__ void __launch_bounds__(256) k_qr_apply(UpdArgs a) {
   constexpr int NT = UT / 8;  // 64 output tiles, 8 per warp
   __shared__ double Zs[NB][UTP];
-  __shared__ double Vs[UT][NB + 1];
+  __shared__ double Vs[UT][NB + 4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g4 = lane >> 2, t4 = lane & 3;
   const int64_t r0 = a.k0 + static_cast<int64_t>(blockIdx.x) * UT;
@@ -528,6 +528,188 @@ __global__ void __launch_bounds__(256) k_qr_apply(UpdArgs a) {
   }
 }
 
+// Look-ahead update of the NEXT panel's columns [c0, c0 + nb2) by the
+// panel just factored, in one cluster launch (the same row split as
+// k_qr_panel): each CTA stages its rows of V and of the block, forms its
+// partial Y = V'W2 on DMMA tiles, the partials are summed through distributed
+// shared memory in rank order (every CTA redundantly, so all hold the same
+// Y), Z = T'Y by substitution with G and tau, and W2 -= V Z.  The rest of
+// the trailing matrix is updated by k_qr_y / k_qr_z / k_qr_apply on a side
+// stream while the next panel is factored.
+#ifdef ITSK_QRNEXT_PROBE
+__device__ unsigned long long g_qn_prof[8];
+#define QNP(i) do { if (threadIdx.x == 0 && q == 0) { long long _t = clock64(); atomicAdd(&g_qn_prof[i], (unsigned long long)(_t - _qt)); _qt = _t; } } while (0)
+#else
+#define QNP(i) do { } while (0)
+#endif
+
+// DMMA fragments read a[g][t] / b[t][g] from row-major shared tiles: a row
+// stride = 4 (mod 16) doubles puts the 16 lanes of each half-warp (g, t in
+// 0..3) on 16 distinct 8-byte banks (a +1 pad gives 4-way conflicts).
+template <int NB>
+__global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next(UpdArgs a, int64_t hmax) {
+  constexpr int VS = NB + 4, BS = 36;
+#ifdef ITSK_QRNEXT_PROBE
+  long long _qt = clock64();
+#endif
+  extern __shared__ __align__(16) double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), q = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int64_t k0 = a.k0, ldw = a.ldw;
+  const int64_t len = a.d - k0;
+  const int64_t lo = k0 + lo_of(q, C, len), hi = k0 + lo_of(q + 1, C, len);
+  const int h = static_cast<int>(hi - lo);
+  const int hp = (h + 7) & ~7;
+  const int hz = (h + 15) & ~15;           // rows staged (zero-filled past h)
+  const int nb2 = static_cast<int>(a.Nt);  // <= 32
+  double* Vs = sm;                      // (hmax + 16) x VS
+  double* Bs = Vs + (hmax + 16) * VS;   // (hmax + 16) x BS
+  double* Yq = Bs + (hmax + 16) * BS;   // 32 x BS: this CTA's partial
+  double* Ys = Yq + 32 * BS;            // 32 x BS: the sum, then Z
+  double* Gs = Ys + 32 * BS;            // NB x VS
+  double* ts = Gs + NB * VS;            // NB
+  double* Yo = ts + NB;                 // NB x 32: the elements this CTA owns, summed
+  // rows staged with cp.async (all loads in flight; zero-fill past h / kb /
+  // nb2), then V's unit lower trapezoid fixed up on the rows k0 .. k0+kb-1
+  for (int idx = tid; idx < hz * 32; idx += QP_THREADS) {
+    const int rr = idx >> 5, c = idx & 31;
+    const int64_t r = lo + rr;
+    if (c < NB) {
+      const bool ok = rr < h && c < a.kb;
+      cp_async8(Vs + rr * VS + c, a.W + (ok ? r * ldw + k0 + c : 0), ok);
+    }
+    const bool okb = rr < h && c < nb2;
+    cp_async8(Bs + rr * BS + c, a.W + (okb ? r * ldw + a.c0 + c : 0), okb);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  if (lo < k0 + a.kb)
+    for (int idx = tid; idx < NB * NB; idx += QP_THREADS) {
+      const int rr = idx / NB, c = idx - rr * NB;
+      const int64_t r = lo + rr;
+      if (rr < h && c < a.kb && r <= k0 + c) Vs[rr * VS + c] = (r == k0 + c) ? 1.0 : 0.0;
+    }
+  for (int idx = tid; idx < NB * NB; idx += QP_THREADS) Gs[(idx / NB) * VS + idx % NB] = a.G[idx];
+  if (tid < NB) ts[tid] = tid < a.kb ? a.taus[k0 + tid] : 0.0;
+  __syncthreads();
+  QNP(0);
+  // partial Y (NB x 32): warp -> 8x8 tile (NB/8 x 4 tiles over 16 warps);
+  // the row sum runs in 4 interleaved DMMA chains (a dependent DMMA costs
+  // ~300 cycles: one chain over all rows was most of this kernel's time)
+  constexpr int MT = NB / 8;
+  if (warp < MT * 4) {
+    const int mt = warp >> 2, nt = warp & 3;
+    double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+    const int hp16 = (hp + 15) & ~15;  // rows beyond hp are zero-filled below
+    for (int k = 0; k < hp16; k += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = k + 4 * u + t4;
+        dmma(d0[u], d1[u], Vs[kk * VS + mt * 8 + g4], Bs[kk * BS + nt * 8 + g4]);
+      }
+    }
+    Yq[(mt * 8 + g4) * BS + nt * 8 + 2 * t4] = (d0[0] + d0[1]) + (d0[2] + d0[3]);
+    Yq[(mt * 8 + g4) * BS + nt * 8 + 2 * t4 + 1] = (d1[0] + d1[1]) + (d1[2] + d1[3]);
+  }
+  QNP(1);
+  cl.sync();
+  QNP(5);
+  // sum of the C partials in rank order: reduce-scatter (CTA q sums the
+  // elements e = q (mod C) over all ranks, all remote loads in flight), then
+  // all-gather from the owners
+  for (int e = q + C * tid; e < NB * 32; e += C * QP_THREADS) {
+    const uint32_t la = smem_u32(Yq + (e >> 5) * BS + (e & 31));
+    double v[MAX_C];
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t) {
+      v[t] = 0.0;
+      if (t < C) asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[t]) : "r"(mapa_u32(la, t)) : "memory");
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t)
+      if (t < C) sum += v[t];
+    Yo[e] = sum;
+  }
+  cl.sync();
+  for (int e = tid; e < NB * 32; e += QP_THREADS) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(mapa_u32(smem_u32(Yo + e), e % C)) : "memory");
+    Ys[(e >> 5) * BS + (e & 31)] = v;
+  }
+  __syncthreads();
+  QNP(2);
+  // Z = T'Y: z_i = tau_i (y_i - sum_{k<i} G_ki z_k).  Warp per column, lane
+  // j carries t_j = y_j - sum_{k<i} G_kj z_k; step i: z_i = tau_i t_i (lane
+  // i), broadcast, lanes j > i subtract G_ij z_i.
+  // two columns per warp, their chains interleaved
+  for (int c = warp; c < nb2; c += 2 * QP_WARPS) {
+    const int c2 = c + QP_WARPS;
+    const bool two = c2 < nb2;
+    double t = lane < a.kb ? Ys[lane * BS + c] : 0.0;
+    double u = (two && lane < a.kb) ? Ys[lane * BS + c2] : 0.0;
+    for (int i = 0; i < a.kb; ++i) {
+      const double g = Gs[i * VS + (lane < NB ? lane : 0)];
+      const double zi = __shfl_sync(FULL, ts[i] * t, i);
+      const double wi = __shfl_sync(FULL, ts[i] * u, i);
+      if (lane == i) {
+        t = zi;
+        u = wi;
+      } else if (lane > i) {
+        t = fma(-g, zi, t);
+        u = fma(-g, wi, u);
+      }
+    }
+    Ys[lane * BS + c] = lane < a.kb ? t : 0.0;
+    if (two) Ys[lane * BS + c2] = lane < a.kb ? u : 0.0;
+  }
+  __syncthreads();
+  QNP(3);
+  // W2 -= V Z: (hp/8) x 4 tiles of 8x8; a warp's tiles advance together
+  // through k so their DMMA chains interleave
+  const int ntile = (hp >> 3) * 4;
+  constexpr int TW = 8;  // tiles per warp per round
+  for (int T0 = warp * TW; T0 < ntile; T0 += QP_WARPS * TW) {
+    double d0[TW], d1[TW];
+#pragma unroll
+    for (int u = 0; u < TW; ++u) {
+      const int T = T0 + u;
+      const int rr = (T >> 2) * 8 + g4, c = (T & 3) * 8 + 2 * t4;
+      d0[u] = T < ntile ? Bs[rr * BS + c] : 0.0;
+      d1[u] = T < ntile ? Bs[rr * BS + c + 1] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NB; k += 4) {
+#pragma unroll
+      for (int u = 0; u < TW; ++u) {
+        const int T = T0 + u < ntile ? T0 + u : 0;
+        const int rr = (T >> 2) * 8 + g4;
+        dmma(d0[u], d1[u], -Vs[rr * VS + k + t4], Ys[(k + t4) * BS + (T & 3) * 8 + g4]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < TW; ++u) {
+      const int T = T0 + u;
+      const int rr = (T >> 2) * 8 + g4, c = (T & 3) * 8 + 2 * t4;
+      if (T < ntile && rr < h) {
+        double* wp = a.W + (lo + rr) * ldw + a.c0 + c;
+        if (c < nb2) wp[0] = d0[u];
+        if (c + 1 < nb2) wp[1] = d1[u];
+      }
+    }
+  }
+  cl.sync();  // no CTA exits while another may still read its Yo
+  QNP(4);
+}
+
+size_t next_smem(int64_t hmax, int nb) {
+  return static_cast<size_t>((hmax + 16) * (nb + 4) + (hmax + 16) * 36 + 2 * 32 * 36 + nb * (nb + 4) + nb +
+                             nb * 32) * 8;
+}
+
 // R (sign-fixed upper triangle) and z = sign-fixed Q'Sb (linalg.py:43-46).
 __global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, const double* betas,
                             double* R, double* z, int* singular) {
@@ -543,6 +725,38 @@ __global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, 
   }
 }
 
+// Side stream and events of the look-ahead (per device, created once).
+bool lookahead_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ITSK_QR_LOOKAHEAD");  // tuning knob: 0 = update all columns on the main stream
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+int side_stream(cudaStream_t* out) {
+  static cudaStream_t st[64] = {};
+  int dev = 0;
+  ITSK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return ITSK_EINVAL;
+  if (!st[dev]) ITSK_CUDA(cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking));
+  *out = st[dev];
+  return ITSK_OK;
+}
+
+cudaError_t pooled_event(int which, cudaEvent_t* out) {
+  static cudaEvent_t ev[64][2] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!ev[dev][which]) {
+    e = cudaEventCreateWithFlags(&ev[dev][which], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *out = ev[dev][which];
+  return cudaSuccess;
+}
+
 // kernel-argument array for cudaLaunchKernelExC (one by-value struct)
 struct ArgPack {
   void* p[1];
@@ -553,7 +767,7 @@ inline void** args_of(PanelArgs& pa) {
   return ap.p;
 }
 
-size_t y_smem(int nb) { return static_cast<size_t>(2 * YRT * (nb + 1) + 2 * YRT * (UT + 1)) * 8; }
+size_t y_smem(int nb) { return static_cast<size_t>(2 * YRT * (nb + 4) + 2 * YRT * (UT + 4)) * 8; }
 
 }  // namespace
 
@@ -572,8 +786,10 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
     }
   }
   p.ldy = N;
-  // Yp (MAX_SPLIT x 32 x N) | Z (32 x N) | betas (n) | taus (n) | Gp (MAX_C x 32 x 32) | G (32 x 32)
-  p.ws_doubles = static_cast<int64_t>(MAX_SPLIT + 1) * 32 * N + 2 * n + (MAX_C + 1) * 32 * 32 + 64;
+  // Yp (MAX_SPLIT x 32 x N) | Z (32 x N) | betas (n) | taus (n) | Gp (MAX_C x 32 x 32) | G (32 x 32 per panel:
+  // the side-stream update of panel k reads its G while panel k+1 writes its own)
+  const int64_t npan = (n + 15) / 16;
+  p.ws_doubles = static_cast<int64_t>(MAX_SPLIT + 1) * 32 * N + 2 * n + (MAX_C + npan) * 32 * 32 + 64;
   return p;
 }
 
@@ -590,13 +806,37 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
                               : reinterpret_cast<const void*>(k_qr_panel<16>);
   const void* ky = P.NB == 32 ? reinterpret_cast<const void*>(k_qr_y<32>)
                               : reinterpret_cast<const void*>(k_qr_y<16>);
+  const void* kn = P.NB == 32 ? reinterpret_cast<const void*>(k_qr_next<32>)
+                              : reinterpret_cast<const void*>(k_qr_next<16>);
   ITSK_CUDA(allow_max_smem(kp));
   ITSK_CUDA(allow_max_smem(ky));
+  ITSK_CUDA(allow_max_smem(kn));
   ITSK_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ITSK_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int nsm = num_sms();
   const size_t ysm = y_smem(P.NB);
+  const size_t nsmem = next_smem(P.hmax, P.NB);
+  // look-ahead: the next panel's columns are updated right after the panel
+  // (k_qr_next, critical path); the rest of the trailing matrix on a side
+  // stream, overlapping the next panel.  Ordering: rest(k) before next(k+1)
+  // (which updates columns rest(k) covered), rest(k) after panel(k).
+  const bool ahead = nsmem <= 220 * 1024 && lookahead_enabled();
+  cudaStream_t side = nullptr;
+  if (ahead) {
+    int rc = side_stream(&side);
+    if (rc) return rc;
+  }
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+  if (ahead) {
+    ITSK_CUDA(pooled_event(0, &ev_main));
+    ITSK_CUDA(pooled_event(1, &ev_side));
+    ITSK_CUDA(cudaEventRecord(ev_main, s));  // the side stream starts after prior work on s
+    ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
+  }
+  bool side_busy = false;
   for (int64_t k0 = 0; k0 < n; k0 += P.NB) {
     const int kb = static_cast<int>(std::min<int64_t>(P.NB, n - k0));
+    double* Gk = G + (k0 / P.NB) * 32 * 32;
     PanelArgs pa;
     pa.W = W;
     pa.d = d;
@@ -607,7 +847,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     pa.betas = betas;
     pa.taus = taus;
     pa.Gp = Gp;
-    pa.G = G;
+    pa.G = Gk;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P.C);
     cfg.blockDim = dim3(QP_THREADS);
@@ -635,27 +875,52 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     ua.Yp = Yp;
     ua.Z = Z;
     ua.ldy = P.ldy;
-    ua.G = G;
+    ua.G = Gk;
     ua.taus = taus;
-    const int64_t ncb = (Nt + UT - 1) / UT;
     const int64_t rows = d - k0;
+    cudaStream_t us = s;  // stream of the bulk update
+    if (ahead) {
+      ITSK_CUDA(cudaEventRecord(ev_main, s));  // panel(k) done
+      // the next panel's block on s (after rest(k-1) finished on the side stream)
+      if (side_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
+      UpdArgs un = ua;
+      const int64_t nb2 = std::min<int64_t>(P.NB, Nt);
+      un.Nt = nb2;
+      cudaLaunchConfig_t nc = cfg;
+      nc.dynamicSmemBytes = nsmem;
+      void* nargs[] = {&un, const_cast<int64_t*>(&P.hmax)};
+      ITSK_CUDA(cudaLaunchKernelExC(&nc, kn, nargs));
+      count_launch();
+      if (Nt == nb2) continue;
+      ua.c0 = c0 + nb2;
+      ua.Nt = Nt - nb2;
+      // rest(k) on the side stream once panel(k) is done (beside next(k))
+      ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
+      us = side;
+    }
+    const int64_t ncb = (ua.Nt + UT - 1) / UT;
     int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(MAX_SPLIT, (2 * nsm) / ncb)));
     S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, rows / (2 * YRT))));
     ua.S = S;
     dim3 gy(static_cast<unsigned>(ncb), static_cast<unsigned>(S));
     dim3 ga(static_cast<unsigned>((rows + UT - 1) / UT), static_cast<unsigned>(ncb));
     if (P.NB == 32) {
-      k_qr_y<32><<<gy, 256, ysm, s>>>(ua);
-      k_qr_z<32><<<static_cast<unsigned>(ncb), 256, 0, s>>>(ua);
-      k_qr_apply<32><<<ga, 256, 0, s>>>(ua);
+      k_qr_y<32><<<gy, 256, ysm, us>>>(ua);
+      k_qr_z<32><<<static_cast<unsigned>(ncb), 256, 0, us>>>(ua);
+      k_qr_apply<32><<<ga, 256, 0, us>>>(ua);
     } else {
-      k_qr_y<16><<<gy, 256, ysm, s>>>(ua);
-      k_qr_z<16><<<static_cast<unsigned>(ncb), 256, 0, s>>>(ua);
-      k_qr_apply<16><<<ga, 256, 0, s>>>(ua);
+      k_qr_y<16><<<gy, 256, ysm, us>>>(ua);
+      k_qr_z<16><<<static_cast<unsigned>(ncb), 256, 0, us>>>(ua);
+      k_qr_apply<16><<<ga, 256, 0, us>>>(ua);
     }
     count_launch(3);
     ITSK_CHECK_LAUNCH();
+    if (ahead) {
+      ITSK_CUDA(cudaEventRecord(ev_side, side));
+      side_busy = true;
+    }
   }
+  if (ahead && side_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
   k_qr_finish<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, s>>>(W, n, ldw, N, betas, R, z, singular);
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -663,6 +928,12 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
 }
 
 }  // namespace itsk
+
+#ifdef ITSK_QRNEXT_PROBE
+extern "C" void itsk_qrnext_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_qn_prof, sizeof(unsigned long long) * 8);
+}
+#endif
 
 #ifdef ITSK_QR2_PROFILE
 extern "C" void itsk_qr2_profile_read(unsigned long long* out) {

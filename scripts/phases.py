@@ -46,7 +46,8 @@ out["copyW"] = T(lambda: ws.W.copy_(W0))
 out["trsv_x0"] = T(lambda: _lib.check(lib.itsk_trsv(dv.ptr(ws.R), n, dv.ptr(ws.z), dv.ptr(ws.xs[0]), 0, s)))
 out["normest"] = T(lambda: _lib.check(lib.itsk_normest(dv.ptr(ws.R), n, dv.ptr(ws.v0), normest_steps(n), dv.ptr(ws.est), None, s)))
 out["condest"] = T(lambda: _lib.check(lib.itsk_condest(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, None, s)))
-out["condest_ws"] = T(lambda: _lib.check(lib.itsk_condest_ws(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, dv.ptr(ws.Rp), dv.ptr(ws.cond_ws), ws.cond_ws.numel(), s)))
+cond_ws = torch.empty(n * n, dtype=torch.float64, device=dev)
+out["condest_ws"] = T(lambda: _lib.check(lib.itsk_condest_ws(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, dv.ptr(ws.Rp), dv.ptr(cond_ws), cond_ws.numel(), s)))
 out["condest_Rp"] = T(lambda: _lib.check(lib.itsk_condest(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, dv.ptr(ws.Rp), s)))
 out["normest_Rp"] = T(lambda: _lib.check(lib.itsk_normest(dv.ptr(ws.R), n, dv.ptr(ws.v0), normest_steps(n), dv.ptr(ws.est), dv.ptr(ws.Rp), s)))
 p_ = solvers._loop_params(ws, at, n, cfg, 1.0, 0.0, None)
