@@ -115,7 +115,7 @@ __device__ unsigned long long g_qr2_prof[8];
 
 template <int NB>
 __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
-  constexpr int PS = NB + 1;   // padded row stride: row walks are bank-conflict free
+  constexpr int PS = NB + 1;   // padded row stride (a wider pad would push C4's 1500-row panels out of shared memory)
   constexpr int REC = 2 * NB;  // [partial sums (NB) | owner's next pivot row (NB)]
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -327,17 +327,21 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   if (warp < GT * GT) {
     const int mt = warp / GT, nt = warp - mt * GT;
     const int ci = mt * 8 + g4, ck = nt * 8 + g4;
-    double d0 = 0.0, d1 = 0.0;
-    for (int r0 = 0; r0 < h; r0 += 4) {
-      const int r = r0 + t4;
-      const bool ok = r < h;
-      const double av = ok ? vval(Ps[r * PS + ci], lo + r, k0, ci) : 0.0;
-      const double bv = ok ? vval(Ps[r * PS + ck], lo + r, k0, ck) : 0.0;
-      dmma(d0, d1, av, bv);
+    // 4 interleaved DMMA chains (a dependent DMMA costs ~300 cycles)
+    double e0[4] = {0.0, 0.0, 0.0, 0.0}, e1[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r0 = 0; r0 < h; r0 += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 4 * u + t4;
+        const bool ok = r < h;
+        const double av = ok ? vval(Ps[r * PS + ci], lo + r, k0, ci) : 0.0;
+        const double bv = ok ? vval(Ps[r * PS + ck], lo + r, k0, ck) : 0.0;
+        dmma(e0[u], e1[u], av, bv);
+      }
     }
     double* gp = a.Gp + static_cast<int64_t>(q) * NB * NB;
-    gp[ci * NB + nt * 8 + 2 * t4] = d0;
-    gp[ci * NB + nt * 8 + 2 * t4 + 1] = d1;
+    gp[ci * NB + nt * 8 + 2 * t4] = (e0[0] + e0[1]) + (e0[2] + e0[3]);
+    gp[ci * NB + nt * 8 + 2 * t4 + 1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
   }
   cl.sync();
   // G = sum_t G_t in rank order; element e summed by CTA e % C
