@@ -314,17 +314,32 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
         ws.v0_host.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
         ws.v0_seed = cfg.rng_seed
     ws.v0.copy_(ws.v0_host, non_blocking=True)
+    events = []
+
+    def copy_chunk(r0, r1):
+        with torch.cuda.stream(ws.copy_stream):
+            at[r0:r1].copy_(upload[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(ws.copy_stream)
+        events.append(ev)
+
+    chunks = _upload_chunks(m, n) if upload is not None else []
+    # pinned host memory: every chunk copy is queued before the pattern (whose
+    # redraw rounds wait on the host), so the copy engine never idles; a
+    # pageable copy blocks the host, so those are interleaved with the sketches
+    early = upload is not None and upload.is_pinned()
+    if early:
+        for r0, r1 in chunks:
+            copy_chunk(r0, r1)
     words, has32, pend = pcg_state(cfg.rng_seed)
     _lib.check(lib.itsk_sparse_sign_pattern(
         d, m, zeta, words, has32, pend, _dev.ptr(ws.rows), _dev.ptr(ws.neg), _dev.ptr(ws.sk_ptr),
         _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
     if upload is not None:
-        for k, (r0, r1) in enumerate(_upload_chunks(m, n)):
-            with torch.cuda.stream(ws.copy_stream):
-                at[r0:r1].copy_(upload[r0:r1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(ws.copy_stream)
-            compute.wait_event(ev)
+        for k, (r0, r1) in enumerate(chunks):
+            if not early:
+                copy_chunk(r0, r1)
+            compute.wait_event(events[k])
             _lib.check(lib.itsk_sketch_rows(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
                                             _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, r0, r1,
                                             1 if k else 0, stream))
