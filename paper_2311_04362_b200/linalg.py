@@ -164,7 +164,9 @@ def cond_est(r, rng_seed: int = 0, out: torch.Tensor | None = None):
     n = rt.shape[0]
     v0 = _dev.as_device_vector(start_vector(n, rng_seed), dev)
     res = out if out is not None else _scalar_out(dev)
-    ws = torch.empty(n * n, dtype=torch.float64, device=dev)
+    nws = ctypes.c_int64()
+    _lib.check(_dev.lib(dev).itsk_condest_workspace(n, ctypes.byref(nws)))
+    ws = torch.empty(nws.value, dtype=torch.float64, device=dev)
     _lib.check(_dev.lib(dev).itsk_condest_ws(_dev.ptr(rt), n, _dev.ptr(v0), _dev.ptr(res), None, _dev.ptr(ws),
-                                             n * n, _dev.stream_ptr()))
+                                             ws.numel(), _dev.stream_ptr()))
     return float(res.item()) if (host or out is None) else res

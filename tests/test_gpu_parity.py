@@ -464,19 +464,29 @@ def test_condest_inverse_operator_matches_trsv_operator(pkg, orc, m, n, kappa, d
     v0 = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).to(dev)
     o1 = torch.empty(1, dtype=torch.float64, device=dev)
     o2 = torch.empty(1, dtype=torch.float64, device=dev)
-    ws = torch.empty(n * n, dtype=torch.float64, device=dev)
+    import ctypes
+
+    nws = ctypes_i64()
+    lib.itsk_condest_workspace(n, ctypes.byref(nws))
+    ws = torch.empty(nws.value, dtype=torch.float64, device=dev)
     rp = torch.empty(_rp_len(lib, n), dtype=torch.float64, device=dev)
     _lib.check(lib.itsk_pack_upper(dv.ptr(rt), n, dv.ptr(rp), dv.stream_ptr()))
     _lib.check(lib.itsk_condest(dv.ptr(rt), n, dv.ptr(v0), dv.ptr(o1), dv.ptr(rp), dv.stream_ptr()))
-    _lib.check(lib.itsk_condest_ws(dv.ptr(rt), n, dv.ptr(v0), dv.ptr(o2), dv.ptr(rp), dv.ptr(ws), n * n,
+    _lib.check(lib.itsk_condest_ws(dv.ptr(rt), n, dv.ptr(v0), dv.ptr(o2), dv.ptr(rp), dv.ptr(ws), ws.numel(),
                                    dv.stream_ptr()))
     c1, c2 = float(o1.item()), float(o2.item())
     exact = orc.cond_est(r)
     assert c2 == pytest.approx(c1, rel=1e-10)
     assert c2 == pytest.approx(exact, rel=1e-9)
     # X really is R^-1 (upper triangle)
-    x = np.triu(ws.view(n, n).cpu().numpy())
+    x = np.triu(ws[: n * n].view(n, n).cpu().numpy())
     assert np.linalg.norm(x @ r - np.eye(n)) <= 1e3 * n * U * np.linalg.norm(x) * np.linalg.norm(r)
+
+
+def ctypes_i64():
+    import ctypes
+
+    return ctypes.c_int64()
 
 
 def _rp_len(lib, n):
