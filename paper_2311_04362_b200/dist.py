@@ -86,9 +86,12 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
                                 check_every: int = 4):
     """Row-sharded solve.  Each rank passes its own block [row0, row0+m_local)
     of A and b (numpy or CUDA tensors); `truth.r` may be the full vector or
-    the local slice.  Returns a SolveResult whose iterates / solution / trace
+    the local slice.  A sparse block (scipy sparse / CsrMatrix) runs the CSR
+    pass of sparse.cu on the rank's rows.  Returns a SolveResult whose iterates / solution / trace
     scalars are identical on every rank; residual_vectors hold the local rows."""
     import torch.distributed as tdist
+
+    from .sparse import as_csr_matrix, is_sparse
 
     a_shape = a_local.shape
     m_loc, n = int(a_shape[0]), int(a_shape[1])
@@ -100,7 +103,12 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     lib = _dev.lib(dev)
     r_slots = cfg.max_iters + 1 if residuals == "all" else 2
     ws = ShardedWorkspace(dev, m_total, m_loc, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots, truth is not None)
-    at, lda = _dev.as_device_matrix(a_local, dev)
+    csr = None
+    if is_sparse(a_local):  # a row block of a sparse A (solvers.py:195-196)
+        csr = as_csr_matrix(a_local, dev)
+        at, lda = None, 0
+    else:
+        at, lda = _dev.as_device_matrix(a_local, dev)
     ws.b.copy_(_dev.as_device_vector(b_local, dev))
     if truth is not None:
         ws.x_true.copy_(_dev.as_device_vector(truth.x, dev))
@@ -123,8 +131,12 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     _lib.check(lib.itsk_pattern_csr(
         _dev.ptr(ws.rows_full) + 4 * off, _dev.ptr(ws.neg_full) + off, m_loc, cfg.zeta, cfg.d,
         _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
-    _lib.check(lib.itsk_sketch(_dev.ptr(at), m_loc, n, lda, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr),
-                               _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
+    if csr is not None:
+        _lib.check(lib.itsk_csr_sketch(csr.plan, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), cfg.d,
+                                       cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
+    else:
+        _lib.check(lib.itsk_sketch(_dev.ptr(at), m_loc, n, lda, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr),
+                                   _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
     allreduce(ws.W)
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
@@ -139,7 +151,7 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, _dev.ptr(ws.Rp),
                                 stream))
 
-    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=m_loc)
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=m_loc, csr=csr)
     cs = ws.cs[: n + 4]
     _lib.check(lib.itsk_loop_begin_local(ctypes.byref(p), stream))
     allreduce(cs)
@@ -160,4 +172,5 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     res = _read_result(lib, ws, p, stream_obj)
     out = _assemble(ws, res, truth, cfg, at, ws.b)
     out._workspace = ws  # keep the local residual rows alive
+    out._csr = csr       # and the local CSR plan the trace's residuals came from
     return out

@@ -128,3 +128,45 @@ def test_two_rank_sharded_solve_gloo():
     assert abs(res[0]["iters"] - res[0]["ref_iters"]) <= 2
     x_ref = res[0]["x_ref"]
     assert np.linalg.norm(res[0]["x"] - x_ref) <= 1e-6 * np.linalg.norm(x_ref)
+
+
+def _sparse_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import itsketch_oracle as orc
+        from paper_2311_04362_b200.problems import gen_sparse
+
+        m, n, d, zeta, seed = 5000, 30, 300, 8, 6
+        p = gen_sparse(m, n, seed)
+        pat = orc.sparse_sign_pattern(d, m, zeta, seed)
+        r0, r1 = shard_bounds(m, world, rank)
+        local = orc.Pattern(d, r1 - r0, zeta, pat.rows[r0:r1], pat.signs[r0:r1], pat.scale)
+        # the rank's CSR row block and its slice of S's columns (dist.py, sparse branch)
+        sa = torch.from_numpy(orc.sketch_apply_sparse(local, p.a[r0:r1]))
+        dist.all_reduce(sa)
+        full = orc.sketch_apply_sparse(pat, p.a)
+        x = np.random.default_rng(rank).standard_normal(n)
+        dist.broadcast(t := torch.from_numpy(x), src=0)
+        r_loc = p.b[r0:r1] - p.a[r0:r1] @ t.numpy()
+        c = torch.from_numpy(p.a[r0:r1].T @ r_loc)
+        dist.all_reduce(c)
+        c_full = p.a.T @ (p.b - p.a @ t.numpy())
+        out[rank] = dict(sk=float(np.abs(sa.numpy() - full).max() / np.abs(full).max()),
+                         c=float(np.abs(c.numpy() - c_full).max() / np.abs(c_full).max()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sparse_sums_gloo():
+    """The sparse branch's two sums over row blocks (S·A once, A'r per
+    iteration) equal the single-block results to rounding."""
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_sparse_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    for r in range(world):
+        assert res[r]["sk"] < 1e-14 and res[r]["c"] < 1e-13
