@@ -144,6 +144,24 @@ def test_qr_matches_lapack(pkg, orc, m, n, seed):
     assert np.linalg.norm(f.z - z_ref) <= 100 * n * U * np.linalg.norm(rhs)
 
 
+@pytest.mark.parametrize("mode", ["v1", "grid", "tsqr"])
+@pytest.mark.parametrize("m,n,seed", [(200, 40, 2), (4000, 201, 4), (5000, 500, 7)])
+def test_qr_alternate_paths_match_lapack(pkg, orc, monkeypatch, mode, m, n, seed):
+    """The QR paths selected by ITSK_QR_MODE (the round-1 cluster kernel, its
+    grid-barrier form, the communication-avoiding cluster TSQR) against LAPACK
+    with the default path's bar; the default (panel / update split) is
+    covered by test_qr_matches_lapack."""
+    monkeypatch.setenv("ITSK_QR_MODE", mode)
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    rhs = rng.standard_normal(m)
+    f = pkg.householder_qr_econ(a, rhs)
+    q_ref, r_ref = orc.householder_qr_econ(a)
+    assert np.all(np.diag(f.r) >= 0)
+    assert np.linalg.norm(f.r - r_ref) <= 100 * n * U * np.linalg.norm(r_ref)
+    assert np.linalg.norm(f.z - q_ref.T @ rhs) <= 100 * n * U * np.linalg.norm(rhs)
+
+
 def test_qr_hand_cases(pkg):
     f = pkg.householder_qr_econ(np.array([[3.0], [4.0]]))
     np.testing.assert_allclose(f.r, [[5.0]], rtol=1e-15)
