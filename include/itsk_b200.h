@@ -236,6 +236,15 @@ typedef struct itsk_loop_params {
   void* ws;                 /* itsk_loop_workspace bytes                     */
   int64_t ws_bytes;
   const struct itsk_csr_plan* csr; /* sparse A (A, lda unused) or NULL        */
+  /* Deferred estimates (nullable).  When set, normest/condest may still be
+   * running on another stream while the loop starts: the tail evaluates the
+   * stopping rule only once *est_ready != 0 (store it with itsk_flag_store
+   * after both estimates, on their stream), replaying the rule over the
+   * iterations already recorded; itsk_loop_finish, enqueued after the
+   * estimates, settles a loop that ended (guard / max_iters) before they
+   * were ready.  Requires r_slots == max_iters + 1 (the stop may move back
+   * to an earlier, still-held iterate). */
+  const uint64_t* est_ready;
 } itsk_loop_params;
 
 typedef struct itsk_loop_result { /* read back with one D2H copy */
@@ -265,6 +274,13 @@ int itsk_loop_step_post(const itsk_loop_params* p, itsk_stream_t stream);
 int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t stream, void** handle);
 int itsk_loop_graph_launch(void* handle, itsk_stream_t stream);
 void itsk_loop_graph_destroy(void* handle);
+/* Settles the deferred stopping rule (est_ready set): replays the rule over
+ * the iterations the loop ran before the estimates were ready and moves the
+ * stop back to where the reference would have stopped (solvers.py:306-316).
+ * A no-op otherwise.  Enqueue after the loop and after the estimates. */
+int itsk_loop_finish(const itsk_loop_params* p, itsk_stream_t stream);
+/* *flag = value with release semantics (the estimates' ready flag). */
+int itsk_flag_store(uint64_t* flag, uint64_t value, itsk_stream_t stream);
 /* Device pointer of the itsk_loop_result inside the loop workspace. */
 int itsk_loop_result_ptr(const itsk_loop_params* p, itsk_loop_result** out);
 

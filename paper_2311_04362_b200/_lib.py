@@ -45,6 +45,7 @@ class LoopParams(ctypes.Structure):
         ("xs", c_dp), ("rs", c_dp), ("trace", c_dp), ("cs", c_dp),
         ("ws", c_dp), ("ws_bytes", c_i64),
         ("csr", c_dp),
+        ("est_ready", c_dp),
     ]
 
 
@@ -103,6 +104,8 @@ _SIGS = {
     "itsk_loop_graph_create": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp, ctypes.POINTER(c_dp)]),
     "itsk_loop_graph_launch": (ctypes.c_int, [c_dp, c_dp]),
     "itsk_loop_graph_destroy": (None, [c_dp]),
+"itsk_loop_finish": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
+    "itsk_flag_store": (ctypes.c_int, [c_dp, ctypes.c_uint64, c_dp]),
     "itsk_loop_result_ptr": (ctypes.c_int, [ctypes.POINTER(LoopParams), ctypes.POINTER(c_dp)]),
 }
 

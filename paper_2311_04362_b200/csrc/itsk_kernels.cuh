@@ -14,10 +14,12 @@ struct LoopCtl {
   int32_t it;         // completed iterations; current iterate is xs[it]
   int32_t countdown;  // -1 == None (solvers.py:292)
   int32_t nhist;      // divergence-guard history length
-  int32_t pad0;
+  int32_t eval_next;  // first iterate whose stopping rule is not yet evaluated (deferred estimates)
   double hist[8];     // ring of the last 6 residual norms (solvers.py:223-238)
   double lo;          // running minimum
   double xtnorm;      // ||x_true||
+  int32_t resolve;    // loop ended before the deferred estimates were ready
+  int32_t pad1;
   itsk_loop_result result;
 };
 
@@ -31,6 +33,7 @@ struct LoopPtrs {
   const double* r_true;
   const double* normest;
   const double* condest;
+  const uint64_t* est_ready;  // nullptr: the estimates are ready
   double* xs;
   double* rs;
   double* trace;
@@ -73,6 +76,7 @@ struct PassArgs {
   double* cs;         // n + 4
   int group;
   double bscale = 1.0;  // r = bscale * b - A x (LSQR: u_{k+1} beta = A y - alpha u_k)
+  int sm_reserve = 0;   // SMs left free for kernels running beside the pass (the loop's estimates and tail)
 };
 
 // counters / group partials needed by the in-kernel reduction of a pass

@@ -47,6 +47,8 @@ __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iter
   ctl->it = 0;
   ctl->countdown = -1;
   ctl->nhist = 0;
+  ctl->eval_next = 1;
+  ctl->resolve = 0;
   for (int i = 0; i < 8; ++i) ctl->hist[i] = 0.0;
   ctl->lo = INFINITY;
   ctl->xtnorm = 0.0;
@@ -57,12 +59,65 @@ __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iter
   ctl->result.bnorm2 = 0.0;
 }
 
+// ||x||^2 with the per-thread order of control_step's fused loop (explicit
+// FMA), so a replayed rule sees the same bits as a live one.
+__device__ double xnorm2_of(const double* x, int64_t n, double* red) {
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = __fma_rn(x[i], x[i], s);
+  return block_sum(s, red);
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// should_stop (solvers.py:174-192, evaluated left to right) and the
+// extra_iters countdown (:306-316) for the iterates k = ctl->eval_next..last
+// in order.  Called by every thread of the CTA (the norms of earlier iterates
+// are block sums); the iterate `last` uses the caller's values.  Returns the
+// iterate the reference stops at, or -1.
+__device__ int64_t replay_rule(const LoopPtrs& p, LoopCtl* ctl, int64_t last, double last_xnorm2,
+                               double last_change, double last_resnorm, double* red) {
+  __shared__ int64_t s_stop;
+  const int64_t n = ctl->n, K = ctl->max_iters + 1;
+  const double normest = __ldcg(p.normest), condest = __ldcg(p.condest);
+  if (threadIdx.x == 0) s_stop = -1;
+  __syncthreads();
+  for (int64_t k = ctl->eval_next; k <= last; ++k) {
+    const double xn2 = (k == last) ? last_xnorm2 : xnorm2_of(p.xs + k * n, n, red);
+    if (threadIdx.x == 0) {
+      const double change = (k == last) ? last_change : p.trace[2 * K + k - 1];
+      const double resnorm = (k == last) ? last_resnorm : p.trace[3 * K + k];
+      if (ctl->countdown < 0) {
+        const double bound = ctl->u * (ctl->gamma * normest * sqrt(xn2) + ctl->rho * condest * resnorm);
+        if (change <= bound) ctl->countdown = static_cast<int32_t>(ctl->extra_iters);
+      }
+      if (ctl->countdown >= 0) {
+        if (ctl->countdown == 0) s_stop = k;
+        else ctl->countdown -= 1;
+      }
+    }
+    __syncthreads();
+    if (s_stop >= 0) break;
+  }
+  if (threadIdx.x == 0) ctl->eval_next = static_cast<int32_t>(last + 1);
+  const int64_t r = s_stop;
+  __syncthreads();
+  return r;
+}
+
 // Guard + record + stopping rule.  begin == 1 records iterate 0 only.
 // Called by every thread of the tail CTA with `ctl` a shared-memory copy of
-// the loop state; returns the (CTA-uniform) done flag.
+// the loop state; returns the (CTA-uniform) done flag.  With deferred
+// estimates (p.est_ready) the rule is evaluated only once they are ready,
+// replaying the iterates recorded meanwhile (replay_rule); a loop that ends
+// first (guard, max_iters) is settled by k_loop_finish.
 __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
   __shared__ double red[DENSE_THREADS / 32];
-  __shared__ int s_done;
+  __shared__ int s_done, s_eval;
+  __shared__ double s_change, s_resnorm;
   const int64_t n = ctl->n, it = ctl->it;
   const int64_t K = ctl->max_iters + 1;
   const int64_t xi = begin ? 0 : it + 1;
@@ -71,7 +126,7 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
   int fin = 1;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const double v = x[i];
-    sx += v * v;
+    sx = __fma_rn(v, v, sx);
     fin &= isfinite(v) ? 1 : 0;
     if (ctl->has_xtrue) {
       const double e = p.x_true[i] - v;
@@ -100,7 +155,8 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
     if (ctl->has_truth)
       re[rec] = ctl->truth_beta > 0 ? sqrt(tt) / ctl->truth_beta : resnorm / sqrt(ctl->result.bnorm2);
     rn[rec] = resnorm;
-    int done = 0;
+    int done = 0, eval = 0;
+    const bool ready = p.est_ready == nullptr || ld_acquire_u64(p.est_ready) != 0;
     if (begin) {
       ctl->result.iterations = 0;
       ctl->result.sol_slot = 0;
@@ -127,29 +183,36 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
         ctl->result.stop_reason = ITSK_STOP_DIVERGED;
         ctl->result.iterations = static_cast<int32_t>(it + 1);
         ctl->result.sol_slot = static_cast<int32_t>(it + 1);
+        if (!ready) ctl->resolve = 1;
       } else {
-        const int64_t nit = it + 1;
-        ctl->it = static_cast<int32_t>(nit);
-        if (ctl->countdown < 0) {
-          // should_stop (solvers.py:174-192), evaluated left to right
-          const double bound = ctl->u * (ctl->gamma * (*p.normest) * sqrt(xnorm2) +
-                                         ctl->rho * (*p.condest) * resnorm);
-          if (change <= bound) ctl->countdown = static_cast<int32_t>(ctl->extra_iters);
-        }
-        if (ctl->countdown >= 0) {
-          if (ctl->countdown == 0) {
-            done = 1;
-            ctl->result.stop_reason = ITSK_STOP_RULE;
-          } else {
-            ctl->countdown -= 1;
-          }
-        }
-        if (!done && nit >= ctl->max_iters) {
-          done = 1;
-          ctl->result.stop_reason = ITSK_STOP_MAX_ITERS;
-        }
-        ctl->result.iterations = static_cast<int32_t>(nit);
-        ctl->result.sol_slot = static_cast<int32_t>(nit);
+        ctl->it = static_cast<int32_t>(it + 1);
+        eval = ready ? 1 : 0;
+        s_change = change;
+        s_resnorm = resnorm;
+      }
+    }
+    ctl->result.done = done;
+    s_done = done;
+    s_eval = eval;
+  }
+  __syncthreads();
+  if (begin || s_done) return s_done;
+  const int64_t nit = it + 1;
+  const int64_t stop = s_eval ? replay_rule(p, ctl, nit, xnorm2, s_change, s_resnorm, red) : -1;
+  if (threadIdx.x == 0) {
+    int done = 0;
+    if (stop >= 0) {
+      done = 1;
+      ctl->result.stop_reason = ITSK_STOP_RULE;
+      ctl->result.iterations = static_cast<int32_t>(stop);
+      ctl->result.sol_slot = static_cast<int32_t>(stop);
+    } else {
+      ctl->result.iterations = static_cast<int32_t>(nit);
+      ctl->result.sol_slot = static_cast<int32_t>(nit);
+      if (nit >= ctl->max_iters) {
+        done = 1;
+        ctl->result.stop_reason = ITSK_STOP_MAX_ITERS;
+        if (!s_eval) ctl->resolve = 1;
       }
     }
     ctl->result.done = done;
@@ -159,6 +222,42 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
   return s_done;
 }
 
+// Settles a loop that ended before its deferred estimates were ready
+// (itsk_loop_finish; stream-ordered after the estimates): the rule replayed
+// over the iterates it did not see; a stop it finds comes before the guard's
+// or max_iters' (solvers.py:300-318: the rule of iterate k is checked before
+// iterate k+1 runs, and at max_iters before the loop exits).
+__global__ void __launch_bounds__(DENSE_THREADS) k_loop_finish(LoopPtrs p) {
+  __shared__ double red[DENSE_THREADS / 32];
+  constexpr int CTL_WORDS = sizeof(LoopCtl) / 8;
+  __shared__ LoopCtl s_ctl;
+  if (threadIdx.x < CTL_WORDS)
+    reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
+  __syncthreads();
+  LoopCtl* ctl = &s_ctl;
+  if (!ctl->resolve) return;
+  const int64_t n = ctl->n, K = ctl->max_iters + 1;
+  const int64_t last = ctl->it;  // the last iterate that passed the guard
+  const double xn2 = xnorm2_of(p.xs + last * n, n, red);
+  const int64_t stop = last >= ctl->eval_next
+                           ? replay_rule(p, ctl, last, xn2, p.trace[2 * K + last - 1], p.trace[3 * K + last], red)
+                           : -1;
+  if (threadIdx.x == 0) {
+    if (stop >= 0) {
+      ctl->result.stop_reason = ITSK_STOP_RULE;
+      ctl->result.iterations = static_cast<int32_t>(stop);
+      ctl->result.sol_slot = static_cast<int32_t>(stop);
+    }
+    ctl->resolve = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < CTL_WORDS)
+    reinterpret_cast<uint64_t*>(p.ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(&s_ctl)[threadIdx.x];
+}
+
+__global__ void k_flag_store(uint64_t* flag, uint64_t value) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
 
 enum : int { TAIL_CONTROL = 2, TAIL_STEP = 4, TAIL_BEGIN = 8 };
 
@@ -285,6 +384,8 @@ int check_params(const itsk_loop_params* p) {
                    p->cs && p->ws,
                "null pointer in loop params");
   ITSK_REQUIRE(p->n <= 6000, "loop: n too large for the single-CTA solves");
+  ITSK_REQUIRE(!p->est_ready || p->r_slots == p->max_iters + 1,
+               "deferred estimates need every residual kept (r_slots == max_iters + 1)");
   int64_t need = loop_layout(nullptr, p->m, p->n).bytes;
   ITSK_REQUIRE(need <= p->ws_bytes, "loop workspace too small");
   return ITSK_OK;
@@ -301,6 +402,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.r_true = p->r_true;
   q.normest = p->normest;
   q.condest = p->condest;
+  q.est_ready = p->est_ready;
   q.xs = p->xs;
   q.rs = p->rs;
   q.trace = p->trace;
@@ -312,6 +414,18 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.n = p->n;
   q.rp_inv = (p->Rp != nullptr && use_packed_inv(p->n, p->n + 32)) ? 1 : 0;
   return q;
+}
+
+// SMs the loop's passes leave free: the tail CTA (which the next pass
+// overlaps under programmatic dependent launch) and the deferred estimates
+// (condest's 2-CTA cluster, normest) running beside the first iterations.
+// A pass CTA that finds no free SM would wait for them.
+int loop_sm_reserve() {
+  static const int r = [] {
+    const char* e = getenv("ITSK_LOOP_SM_RESERVE");  // tuning knob
+    return e ? std::max(0, atoi(e)) : 4;
+  }();
+  return r;
 }
 
 PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
@@ -333,6 +447,7 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   a.gpart = L.gpart;
   a.cs = p->cs;
   a.group = L.group;
+  a.sm_reserve = loop_sm_reserve();
   return a;
 }
 
@@ -529,6 +644,25 @@ extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t s
   }
   cudaStreamDestroy(cap);
   *handle = gh;
+  return ITSK_OK;
+}
+
+extern "C" int itsk_loop_finish(const itsk_loop_params* p, itsk_stream_t stream) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (!p->est_ready) return ITSK_OK;
+  LoopPtrs q = make_ptrs(p);
+  k_loop_finish<<<1, DENSE_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(q);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_flag_store(uint64_t* flag, uint64_t value, itsk_stream_t stream) {
+  ITSK_REQUIRE(flag, "null flag");
+  k_flag_store<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, value);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
   return ITSK_OK;
 }
 

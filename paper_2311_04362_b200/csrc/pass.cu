@@ -807,12 +807,12 @@ int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
   return launch_tma_u<CPL, UNR, NCW>(a, grid, s);
 }
 
-int tma_grid(int64_t m) {
+int tma_grid(int64_t m, int reserve = 0) {
   static const int per_sm = [] {
     const char* e = getenv("ITSK_PASS_CTAS_PER_SM");  // tuning knob
     return e ? std::max(1, atoi(e)) : 1;
   }();
-  int64_t g = static_cast<int64_t>(num_sms()) * per_sm;
+  int64_t g = static_cast<int64_t>(std::max(1, num_sms() - reserve)) * per_sm;
   const int64_t cap = (m + 7) / 8;
   if (g > cap) g = cap;
   return static_cast<int>(std::max<int64_t>(1, g));
@@ -837,7 +837,7 @@ int64_t pass_part_doubles(int64_t m, int64_t n) {
 
 int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
   if (tma_eligible(a0)) {
-    const int grid = tma_grid(a0.m);
+    const int grid = tma_grid(a0.m, a0.sm_reserve);
     *grid_used = grid;
     switch (tma_cpl(a0.n)) {
       case 1: return launch_tma<1>(a0, grid, s);

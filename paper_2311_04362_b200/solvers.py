@@ -212,7 +212,7 @@ class _Workspace:
         self.Rp = torch.empty(nb.value, **f64)
         self.z = torch.empty(n, **f64)
         self.v0 = torch.empty(n, **f64)
-        self.est = torch.zeros(2, **f64)  # normest, condest
+        self.est = torch.zeros(3, **f64)  # normest, condest, ready flag (deferred estimates)
         self.xs = torch.empty((max_iters + 1, n), **f64)
         self.rs = torch.empty((r_slots, m), **f64)
         self.trace = torch.empty((4, max_iters + 1), **f64)
@@ -225,6 +225,7 @@ class _Workspace:
         self.A = None  # upload buffer for host A (allocated on demand)
         self.copy_stream = None  # side stream of the chunked upload
         self.est_stream = None   # side stream of condest
+        self.est_stream2 = None  # side stream of normest (deferred estimates)
         self.sing = torch.zeros(1, dtype=torch.int32, device=dev)  # QR zero-pivot flag
         self.sing_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.v0_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -294,7 +295,8 @@ def _upload_chunks(m: int, n: int) -> list[tuple[int, int]]:
     return [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
 
 
-def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None, upload=None):
+def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None, upload=None,
+                  defer: bool = False):
     """Pattern, S·[A|b], QR, x0, normest, condest — solvers.py:332-337
     (S·A by apply_sparse for a CSR A, solvers.py:195-196).
 
@@ -302,7 +304,13 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
     runs on a side stream in row chunks; the pattern is drawn while the first
     chunk is in flight and each chunk is sketched as soon as it lands
     (itsk_sketch_rows continues every sum in source order, so S·[A|b] is
-    bitwise the one-shot result)."""
+    bitwise the one-shot result).
+
+    defer: normest and condest run on side streams beside the start of the
+    loop instead of before it; they enter only the stopping rule, which the
+    loop evaluates once the ready flag (ws.est[2]) is set, replaying the
+    iterates recorded meanwhile (itsk_loop_params.est_ready).  The caller
+    joins ws.est_stream and calls itsk_loop_finish after the loop."""
     m, n, d, zeta = ws.m, ws.n, ws.d, ws.zeta
     compute = torch.cuda.current_stream(ws.dev)
     if upload is not None:
@@ -354,21 +362,34 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
                                      _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), _dev.ptr(ws.sing), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     # condest (a 2-CTA cluster, the longest of the three) runs beside x0 and
-    # normest (one CTA each) on a side stream
+    # normest (one CTA each) on a side stream; deferred, both run beside the
+    # loop's first iterations
     if ws.est_stream is None:
         ws.est_stream = torch.cuda.Stream(ws.dev)
-    ws.est_stream.wait_stream(compute)
     est_ptr = _dev.ptr(ws.est)
+    if defer:
+        if ws.est_stream2 is None:
+            ws.est_stream2 = torch.cuda.Stream(ws.dev)
+        _lib.check(lib.itsk_flag_store(est_ptr + 16, 0, stream))
+        ws.est_stream2.wait_stream(compute)
+    ws.est_stream.wait_stream(compute)
     with torch.cuda.stream(ws.est_stream):
         _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est_ptr + 8, _dev.ptr(ws.Rp),
                                     int(ws.est_stream.cuda_stream)))
+    if defer:
+        s2 = int(ws.est_stream2.cuda_stream)
+        _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
+                                    _dev.ptr(ws.Rp), s2))
+        ws.est_stream.wait_stream(ws.est_stream2)
+        _lib.check(lib.itsk_flag_store(est_ptr + 16, 1, int(ws.est_stream.cuda_stream)))
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
         _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
-    _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
-                                _dev.ptr(ws.Rp), stream))
-    compute.wait_stream(ws.est_stream)
+    if not defer:
+        _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
+                                    _dev.ptr(ws.Rp), stream))
+        compute.wait_stream(ws.est_stream)
 
 
 def check_singular(ws: _Workspace) -> None:
@@ -378,7 +399,8 @@ def check_singular(ws: _Workspace) -> None:
         raise SingularMatrixError("zero diagonal entry in triangular factor")
 
 
-def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None, csr=None):
+def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None, csr=None,
+                 defer: bool = False):
     p = _lib.LoopParams()
     p.csr = csr.plan if csr is not None else None
     p.m = ws.m if m_local is None else m_local
@@ -406,6 +428,7 @@ def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth,
     p.cs = _dev.ptr(ws.cs)
     p.ws = _dev.ptr(ws.loop_ws)
     p.ws_bytes = ws.loop_ws.numel()
+    p.est_ready = _dev.ptr(ws.est) + 16 if defer else None
     return p
 
 
@@ -425,7 +448,7 @@ def _read_result(lib, ws: _Workspace, p, stream_obj) -> _lib.LoopResult:
     hb = ws.host_buf
     hb[:nxs].copy_(ws.xs.view(-1), non_blocking=True)
     hb[nxs:nxs + ws.trace.numel()].copy_(ws.trace.view(-1), non_blocking=True)
-    hb[nxs + ws.trace.numel():nxs + ws.trace.numel() + 2].copy_(ws.est, non_blocking=True)
+    hb[nxs + ws.trace.numel():nxs + ws.trace.numel() + 2].copy_(ws.est[:2], non_blocking=True)
     ws.sing_host.copy_(ws.sing, non_blocking=True)
     stream_obj.synchronize()
     check_singular(ws)
@@ -528,9 +551,15 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
             ws.r_true.copy_(_dev.as_device_vector(truth.r, dev))
     stream_obj = torch.cuda.current_stream(dev)
     stream = int(stream_obj.cuda_stream)
-    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr, upload)
-    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr)
+    # estimates beside the loop (needs every residual kept: the stop may move
+    # back to an iterate recorded before they were ready)
+    defer = ws.r_slots == cfg.max_iters + 1 and cfg.max_iters > 0
+    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr, upload, defer=defer)
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr, defer=defer)
     run_loop(lib, ws, p, use_graph, stream)
+    if defer:
+        stream_obj.wait_stream(ws.est_stream)
+        _lib.check(lib.itsk_loop_finish(ctypes.byref(p), stream))
     res = _read_result(lib, ws, p, stream_obj)
     return _assemble(ws, res, truth, cfg, at, ws.b)
 

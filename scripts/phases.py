@@ -57,6 +57,8 @@ out["loop(graph)"] = T(loop)
 out["loop(steps)"] = T(lambda: solvers.run_loop(lib, ws, p_, False, s))
 out["trsv_pair"] = T(lambda: _lib.check(lib.itsk_trsv_pair(dv.ptr(ws.R), n, dv.ptr(ws.cs), dv.ptr(ws.z), None, s)))
 out["full_solve"] = T(lambda: itsk.iterative_sketching(at, bt, cfg, residuals="last"))
+# residuals="all": normest / condest deferred beside the loop's first iterations
+out["full_solve_all"] = T(lambda: itsk.iterative_sketching(at, bt, cfg, residuals="all"))
 res = itsk.iterative_sketching(at, bt, cfg, p.truth, residuals="last")
 print(f"{cfgname} {variant} iters={res.iterations} stop={res.trace.stop_reason} "
       f"fe={res.trace.fe[-1]:.3e} re={res.trace.re[-1]:.3e} normest={res.trace.normest:.4e} condest={res.trace.condest:.4e}")
