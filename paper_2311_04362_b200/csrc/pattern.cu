@@ -12,6 +12,9 @@
 // chunk of that word stream; the rare Lemire rejections are resolved with a
 // prefix sum over per-chunk reject counts, so the output is bit-identical to
 // numpy's sequential loop.
+#include <algorithm>
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -130,11 +133,10 @@ __global__ void k_lemire_count(Stream st, const uint64_t* w0p, uint64_t nwords, 
 __global__ void k_lemire_emit(Stream st, const uint64_t* w0p, uint64_t nwords, uint32_t bound,
                               uint32_t thr, const uint32_t* scanned, uint64_t nchunks,
                               uint64_t N, uint32_t* dst, const uint32_t* bad_cols,
-                              int64_t zeta, uint64_t* end_word, uint32_t* short_flag) {
+                              int64_t zeta, uint64_t* end_word) {
   const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t w0 = *w0p;
-  // too few accepted words in the margin: flag it, the host redoes the draw
-  if (c == 0 && scanned[nchunks] < N) *short_flag = 1;
+  // too few accepted words in the margin: k_redraw draws the rest
   if (c >= nchunks) return;
   uint64_t q = scanned[c];
   if (q >= N) return;
@@ -194,6 +196,154 @@ __global__ void k_compact(const uint32_t* flags, const uint32_t* scanned, const 
   if (q >= ncols) return;
   if (flags[q]) out[scanned[q]] = cols ? cols[q] : static_cast<uint32_t>(q);
   if (q == ncols - 1) *total = scanned[q] + flags[q];
+}
+
+// ---------------------------------------------------------------------------
+// Redraw rounds on one CTA (no host round trip).  After the parallel first
+// draw and the parallel duplicate scan of all m columns, the reference's
+// while loop (embed.py:37-42) redraws only the bad columns, in ascending
+// column order, each round from the stream position where the previous one
+// ended; after the first round a few hundred or thousand columns remain, so
+// one CTA runs every further round: words drawn in tiles (thread t takes
+// RD_W consecutive words, a block scan of the accept counts places the
+// draws in stream order), then the redrawn columns re-checked and compacted
+// in order.  The same code finishes the first draw if its word margin ran
+// short (draws total..N-1, then a full duplicate scan).
+constexpr int RD_T = 1024;
+constexpr int RD_W = 4;
+
+// Exclusive prefix sum over the CTA in thread order; *tot = the CTA total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tot) {
+  __shared__ uint32_t wsum[RD_T / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = wsum[lane];
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    wsum[lane] = wi - w;
+    if (lane == 31) *tot = wi;
+  }
+  __syncthreads();
+  const uint32_t r = wsum[warp] + inc - v;
+  __syncthreads();  // wsum is reused by the next call
+  return r;
+}
+
+// Draws `count` Lemire values from word position `pos` on; draw q goes to
+// rows[q0 + q] (cols == nullptr) or to column cols[q / zeta], slot q % zeta.
+// Returns (every thread) the position after the last accepted word.
+__device__ uint64_t draw_seq(const Stream& st, uint64_t pos, uint64_t count, uint32_t bound, uint32_t thr,
+                             uint32_t* rows, uint64_t q0, const uint32_t* cols, int64_t zeta) {
+  __shared__ uint32_t s_tot;
+  __shared__ uint64_t s_end;
+  uint64_t done = 0;
+  while (done < count) {
+    const uint64_t base = pos + static_cast<uint64_t>(threadIdx.x) * RD_W;
+    WordCursor cur(st, base);
+    uint32_t v[RD_W];
+    unsigned acc = 0, cnt = 0;
+#pragma unroll
+    for (int i = 0; i < RD_W; ++i) {
+      if (lemire_accept(cur.next(), bound, thr, &v[i])) {
+        acc |= 1u << i;
+        ++cnt;
+      }
+    }
+    const uint32_t ex = block_excl_scan(cnt, &s_tot);
+    uint64_t q = done + ex;
+#pragma unroll
+    for (int i = 0; i < RD_W; ++i) {
+      if (!(acc >> i & 1u)) continue;
+      if (q < count) {
+        const uint64_t at = cols ? static_cast<uint64_t>(cols[q / zeta]) * zeta + (q % zeta) : q0 + q;
+        rows[at] = v[i];
+        if (q == count - 1) s_end = base + i + 1;
+      }
+      ++q;
+    }
+    __syncthreads();
+    const uint64_t tot = s_tot;
+    if (done + tot >= count) {
+      pos = s_end;
+      done = count;
+    } else {
+      pos += static_cast<uint64_t>(RD_T) * RD_W;
+      done += tot;
+    }
+    __syncthreads();
+  }
+  return pos;
+}
+
+// Columns of `in` (all columns 0..nin-1 when in == nullptr) holding a
+// repeated row, compacted in order into `out`; returns their number.
+__device__ uint32_t flag_compact(const uint32_t* rows, int64_t zeta, const uint32_t* in, uint32_t nin,
+                                 uint32_t* out) {
+  __shared__ uint32_t s_tot;
+  uint32_t nout = 0;
+  for (uint32_t c0 = 0; c0 < nin; c0 += RD_T) {
+    const uint32_t q = c0 + threadIdx.x;
+    uint32_t j = 0, bad = 0;
+    if (q < nin) {
+      j = in ? in[q] : q;
+      const uint32_t* r = rows + static_cast<int64_t>(j) * zeta;
+      for (int64_t a = 1; a < zeta && !bad; ++a) {
+        const uint32_t ra = r[a];
+        for (int64_t b = 0; b < a; ++b)
+          if (r[b] == ra) {
+            bad = 1;
+            break;
+          }
+      }
+    }
+    const uint32_t ex = block_excl_scan(bad, &s_tot);
+    if (bad) out[nout + ex] = j;
+    nout += s_tot;
+  }
+  return nout;
+}
+
+__global__ void __launch_bounds__(RD_T, 1) k_redraw(Stream st, uint32_t bound, uint32_t thr, uint64_t N,
+                                                    uint32_t* rows, int64_t m, int64_t zeta,
+                                                    const uint32_t* scanned1, uint64_t nchunks1,
+                                                    uint64_t nwords1, uint64_t* slots, uint32_t* bad_a,
+                                                    uint32_t* bad_b, const uint32_t* nbad1) {
+  // slots[0]: position before the first draw, slots[1]: after it (written by
+  // k_lemire_emit unless its margin ran short); the final position goes to
+  // slots[0] for k_signs
+  const uint64_t total1 = scanned1[nchunks1];
+  uint64_t pos;
+  uint32_t nbad;
+  uint32_t* cur = bad_a;
+  uint32_t* nxt = bad_b;
+  if (total1 < N) {
+    pos = draw_seq(st, slots[0] + nwords1, N - total1, bound, thr, rows, total1, nullptr, zeta);
+    nbad = flag_compact(rows, zeta, nullptr, static_cast<uint32_t>(m), cur);
+  } else {
+    pos = slots[1];
+    nbad = *nbad1;
+  }
+  while (nbad > 0) {
+    pos = draw_seq(st, pos, static_cast<uint64_t>(nbad) * zeta, bound, thr, rows, 0, cur, zeta);
+    nbad = flag_compact(rows, zeta, cur, nbad, nxt);
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) slots[0] = pos;
 }
 
 __global__ void k_pack_src(const uint8_t* neg, int64_t m, int64_t zeta, uint32_t* vals) {
@@ -267,58 +417,6 @@ int64_t carve(Carver& cv, PatternWs& w, int64_t m, int64_t zeta) {
   return cv.off;
 }
 
-// Word position of the stream lives on the device, ping-ponged between two
-// slots (scalars[2], scalars[3]); scalars[4] is the "margin too small" flag.
-struct StreamPos {
-  uint64_t* slots;
-  int cur = 0;
-  uint64_t* in() const { return slots + cur; }
-  uint64_t* out() const { return slots + (cur ^ 1); }
-  void flip() { cur ^= 1; }
-};
-
-// Draw N bounded values starting at the device-side word position.  Fast
-// mode never synchronises (a short margin raises the device flag, checked at
-// the next natural sync); safe mode checks the margin on the host and widens.
-int lemire_fill(const Stream& st, StreamPos& pos, uint64_t N, uint32_t bound, uint32_t* dst,
-                const uint32_t* bad_cols, int64_t zeta, PatternWs& w, cudaStream_t s, bool safe) {
-  if (N == 0) return ITSK_OK;
-  const uint32_t thr = static_cast<uint32_t>((0x100000000ull - bound) % bound);
-  uint64_t nwords = static_cast<uint64_t>(max_words(static_cast<int64_t>(N)));
-  uint32_t* short_flag = reinterpret_cast<uint32_t*>(w.scalars + 4);
-  for (int attempt = 0; attempt < 8; ++attempt) {
-    const uint64_t nchunks = (nwords + CH - 1) / CH;
-    if (nchunks > w.chunk_cap) break;
-    k_lemire_count<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, pos.in(), nwords, bound, thr,
-                                                              w.counts, nchunks);
-    count_launch();
-    ITSK_CHECK_LAUNCH();
-    size_t tb = w.cub_bytes;
-    ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned,
-                                            static_cast<int>(nchunks + 1), s));
-    count_launch();
-    if (safe) {
-      uint32_t total = 0;
-      ITSK_CUDA(cudaMemcpyAsync(&total, w.scanned + nchunks, sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, s));
-      ITSK_CUDA(cudaStreamSynchronize(s));
-      if (total < N) {
-        nwords = nwords * 2 + 65536;
-        continue;
-      }
-    }
-    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, pos.in(), nwords, bound, thr,
-                                                             w.scanned, nchunks, N, dst, bad_cols,
-                                                             zeta, pos.out(), short_flag);
-    count_launch();
-    ITSK_CHECK_LAUNCH();
-    pos.flip();
-    return ITSK_OK;
-  }
-  set_error("lemire_fill: could not draw %llu values", (unsigned long long)N);
-  return ITSK_ECUDA;
-}
-
 // Group the (m, zeta) pattern by sketch row, keeping source order ascending
 // (stable LSD sort of entries enumerated column-major == ascending j).
 int build_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_t zeta, int64_t d,
@@ -368,59 +466,50 @@ extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, cons
   ITSK_REQUIRE(cv.ok(), "pattern workspace too small");
   Stream st{pcg[0], pcg[1], pcg[2], pcg[3], uinteger, has_uint32 ? 1 : 0};
   const int64_t nnz = m * zeta;
-  StreamPos pos{w.scalars + 2};
-  int rc;
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool safe = pass == 1;  // pass 1 only if the fast pass ran out of margin
-    ITSK_CUDA(cudaMemsetAsync(w.scalars, 0, 8 * sizeof(uint64_t), s));
-    pos.cur = 0;
-    bool redo = false;
-    if (zeta == d) {  // np.tile(np.arange(d), (m, 1)): no draws
-      k_tile_rows<<<blocks_for(nnz, 256), 256, 0, s>>>(rows, m, zeta);
-      count_launch();
-      ITSK_CHECK_LAUNCH();
-    } else {
-      const uint32_t bound = static_cast<uint32_t>(d);
-      if ((rc = lemire_fill(st, pos, nnz, bound, rows, nullptr, zeta, w, s, safe))) return rc;
-      // _distinct_rows redraw loop (embed.py:37-42): one host sync per round
-      const uint32_t* cols = nullptr;
-      int64_t ncols = m;
-      uint32_t* out = w.bad_a;
-      for (;;) {
-        k_flag_dupes<<<blocks_for(ncols, 256), 256, 0, s>>>(rows, zeta, cols, ncols, w.flags);
-        count_launch();
-        size_t tb = w.cub_bytes;
-        ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan,
-                                                static_cast<int>(ncols), s));
-        count_launch();
-        uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
-        k_compact<<<blocks_for(ncols, 256), 256, 0, s>>>(w.flags, w.fscan, cols, ncols, out,
-                                                         nbad_dev);
-        count_launch();
-        ITSK_CHECK_LAUNCH();
-        uint64_t hs[5];
-        ITSK_CUDA(cudaMemcpyAsync(hs, w.scalars, sizeof(hs), cudaMemcpyDeviceToHost, s));
-        ITSK_CUDA(cudaStreamSynchronize(s));
-        const uint32_t nbad = static_cast<uint32_t>(hs[1]);
-        if (static_cast<uint32_t>(hs[4])) {  // a fast draw ran short: redo safely
-          redo = true;
-          break;
-        }
-        if (nbad == 0) break;
-        if ((rc = lemire_fill(st, pos, static_cast<uint64_t>(nbad) * zeta, bound, rows, out, zeta,
-                              w, s, safe)))
-          return rc;
-        cols = out;
-        ncols = nbad;
-        out = (out == w.bad_a) ? w.bad_b : w.bad_a;
-      }
-    }
-    if (redo) continue;
-    k_signs<<<blocks_for((nnz + CH - 1) / CH, 256), 256, 0, s>>>(st, pos.in(), nnz, neg);
+  // stream position on the device: slots[0] before / after all row draws,
+  // slots[1] after the first draw (the host never waits on the pattern)
+  uint64_t* slots = w.scalars + 2;
+  ITSK_CUDA(cudaMemsetAsync(w.scalars, 0, 8 * sizeof(uint64_t), s));
+  if (zeta == d) {  // np.tile(np.arange(d), (m, 1)): no draws
+    k_tile_rows<<<blocks_for(nnz, 256), 256, 0, s>>>(rows, m, zeta);
     count_launch();
     ITSK_CHECK_LAUNCH();
-    break;
+  } else {
+    // first draw, all m*zeta values in parallel (embed.py:36): per-chunk
+    // accept counts, their scan, emission in stream order
+    const uint32_t bound = static_cast<uint32_t>(d);
+    const uint32_t thr = static_cast<uint32_t>((0x100000000ull - bound) % bound);
+    uint64_t nwords = static_cast<uint64_t>(max_words(nnz));
+    // test hook: a short first-draw margin exercises k_redraw's completion path
+    if (const char* e = getenv("ITSK_PATTERN_WORDS_DIV")) nwords = std::max<uint64_t>(1, nwords / std::max(1, atoi(e)));
+    const uint64_t nchunks = (nwords + CH - 1) / CH;
+    k_lemire_count<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, slots, nwords, bound, thr, w.counts, nchunks);
+    count_launch();
+    size_t tb = w.cub_bytes;
+    ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned, static_cast<int>(nchunks + 1), s));
+    count_launch();
+    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, slots, nwords, bound, thr, w.scanned, nchunks,
+                                                             static_cast<uint64_t>(nnz), rows, nullptr, zeta,
+                                                             slots + 1);
+    count_launch();
+    // duplicate scan of every column, compacted in column order (embed.py:38-40)
+    k_flag_dupes<<<blocks_for(m, 256), 256, 0, s>>>(rows, zeta, nullptr, m, w.flags);
+    count_launch();
+    tb = w.cub_bytes;
+    ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan, static_cast<int>(m), s));
+    count_launch();
+    uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
+    k_compact<<<blocks_for(m, 256), 256, 0, s>>>(w.flags, w.fscan, nullptr, m, w.bad_a, nbad_dev);
+    count_launch();
+    // every further round (embed.py:41) on one CTA
+    k_redraw<<<1, RD_T, 0, s>>>(st, bound, thr, static_cast<uint64_t>(nnz), rows, m, zeta, w.scanned, nchunks,
+                                nwords, slots, w.bad_a, w.bad_b, nbad_dev);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
   }
+  k_signs<<<blocks_for((nnz + CH - 1) / CH, 256), 256, 0, s>>>(st, slots, nnz, neg);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
   if (sk_ptr && sk_src) {
     int rc2 = build_csr(rows, neg, m, zeta, d, sk_ptr, sk_src, w, s);
     if (rc2) return rc2;

@@ -57,6 +57,22 @@ def test_pattern_matches_reference_bitwise(pkg, golden):
         assert np.array_equal(s.apply_vec(a[:, 0]), g[key + "_sa"][:, 0]), key
 
 
+@pytest.mark.parametrize("div", ["2", "1000000"])
+def test_pattern_short_first_draw_bitwise(pkg, golden, monkeypatch, div):
+    """The first parallel draw given too few words (test hook): the one-CTA
+    redraw kernel finishes it in stream order, then runs the redraw rounds;
+    the pattern is still the reference's, bit for bit."""
+    monkeypatch.setenv("ITSK_PATTERN_WORDS_DIV", div)
+    g = golden("patterns.npz")
+    for d, m, zeta, seed, k in g["pattern_cases"]:
+        if int(m) * int(zeta) > 2_000_000:
+            continue
+        key = f"p_{d}_{m}_{zeta}_{seed}"
+        s = pkg.sparse_sign_new(int(d), int(m), int(zeta), int(seed))
+        np.testing.assert_array_equal(s.rows, g[key + "_rows"], err_msg=key)
+        np.testing.assert_array_equal(s.signs, g[key + "_signs"], err_msg=key)
+
+
 def test_pattern_csr_grouping(pkg):
     s = pkg.sparse_sign_new(50, 400, 6, 9)
     ptr = s.ptr_dev.cpu().numpy().view(np.uint32).astype(np.int64)
