@@ -26,9 +26,14 @@ def _stale(out: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
+def build(verbose: bool = False, jobs: int | None = None, probe: str | None = None) -> str:
+    """probe="timeline": a diagnostic variant (libitsk_b200_timeline.so,
+    -DITSK_TIMELINE: %globaltimer stamps of the loop's kernels) for
+    scripts/loop_timeline.py; the product library is unchanged."""
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if probe is None else f"build_{probe}")
+    lib_out = LIB if probe is None else os.path.join(HERE, f"libitsk_b200_{probe}.so")
+    extra = [] if probe is None else [f"-DITSK_{probe.upper()}"]
     os.makedirs(objdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "itsk_b200.h")]
     objs, procs = [], []
@@ -37,7 +42,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if _stale(o, [s] + hdrs):
-            cmd = [nvcc, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
             procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -51,13 +56,13 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    if _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    if _stale(lib_out, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib_out, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, probe="timeline" if "--timeline" in sys.argv else None))

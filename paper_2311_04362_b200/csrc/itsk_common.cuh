@@ -194,4 +194,14 @@ struct Carver {
   bool ok() const { return off <= cap; }
 };
 
+#ifdef ITSK_TIMELINE
+// Diagnostic build only (build.py probe="timeline"): %globaltimer in ns.
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int TL_SLOTS = 64;
+#endif
+
 }  // namespace itsk

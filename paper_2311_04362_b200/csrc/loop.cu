@@ -269,9 +269,22 @@ __device__ unsigned long long g_tail_prof[16];
 #define TP(i) do { } while (0)
 #endif
 
+#ifdef ITSK_TIMELINE
+// [slot][0] entry, [1] after the dependency wait, [2] after control, [3] after
+// R'y = c, [4] after R x = y, [5] end
+__device__ unsigned long long g_tail_tl[TL_SLOTS][8];
+#define TL(i) do { if (threadIdx.x == 0 && tl_slot >= 0 && tl_slot < TL_SLOTS) g_tail_tl[tl_slot][i] = gtime(); } while (0)
+#else
+#define TL(i) do { } while (0)
+#endif
+
 template <bool PACKED>
 __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, int grid,
                                                         cudaGraphConditionalHandle h, int use_cond) {
+#ifdef ITSK_TIMELINE
+  const unsigned long long tl_t0 = gtime();
+  int tl_slot = -1;
+#endif
 #ifdef ITSK_TAIL_PROBE
   long long _tp = clock64();
   if (threadIdx.x == 0) atomicAdd(&g_tail_prof[15], 1ull);
@@ -298,6 +311,11 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   __syncthreads();
   LoopCtl* ctl = &s_ctl;
   TP(0);
+#ifdef ITSK_TIMELINE
+  tl_slot = (flags & TAIL_BEGIN) ? 0 : static_cast<int>(ctl->it) + 1;
+  if (threadIdx.x == 0 && tl_slot < TL_SLOTS) g_tail_tl[tl_slot][0] = tl_t0;
+#endif
+  TL(1);
   if (ctl->result.done) {
     if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
     return;
@@ -305,6 +323,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   if (flags & TAIL_CONTROL) {
     const int done = control_step(p, ctl, (flags & TAIL_BEGIN) ? 1 : 0);
     TP(2);
+    TL(2);
     if (threadIdx.x < CTL_WORDS)
       reinterpret_cast<uint64_t*>(p.ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(&s_ctl)[threadIdx.x];
     if (done) {
@@ -323,8 +342,10 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     const DiagInv inv = diag_inv_at(sm, n, p.rp_inv != 0);
     trsv_t_inplace(R, n, v, red_s, inv);
     TP(4);
+    TL(3);
     trsv_n_inplace(R, n, v, red_s, inv);
     TP(5);
+    TL(4);
   } else {
     const RGlobal R(p.R, n);
     trsv_t_inplace(R, n, v, red_s);
@@ -348,6 +369,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   }
   __syncthreads();
   TP(6);
+  TL(5);
 }
 
 struct LoopLayout {
@@ -493,6 +515,14 @@ int prepare_attrs(int64_t n) {
   return ITSK_OK;
 }
 
+int loop_unroll() {
+  static const int u = [] {
+    const char* e = getenv("ITSK_LOOP_UNROLL");  // tuning knob
+    return e ? std::max(1, std::min(8, atoi(e))) : 2;
+  }();
+  return u;
+}
+
 struct GraphHandle {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -502,6 +532,14 @@ struct GraphHandle {
 }  // namespace itsk
 
 using namespace itsk;
+
+#ifdef ITSK_TIMELINE
+extern "C" void itsk_tail_timeline_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_tail_tl, sizeof(itsk::g_tail_tl));
+  unsigned long long z[itsk::TL_SLOTS][8] = {};
+  cudaMemcpyToSymbol(itsk::g_tail_tl, z, sizeof(z));
+}
+#endif
 
 #ifdef ITSK_TAIL_PROBE
 extern "C" void itsk_tail_profile_read(unsigned long long* out) {
@@ -627,9 +665,15 @@ extern "C" int itsk_loop_graph_create(const itsk_loop_params* p, itsk_stream_t s
     set_error("capture begin: %s", cudaGetErrorString(e));
     return fail(ITSK_ECUDA);
   }
+  // The body holds `unroll` iterations: a kernel boundary inside the body
+  // keeps programmatic dependent launch (the next pass streams A while the
+  // tail runs), the WHILE node's re-launch between bodies does not.  Once the
+  // loop is done the remaining kernels of the body are no-ops.
   int grid = 0;
-  rc = loop_pass(p, q, 1, cap, &grid);
-  if (rc == ITSK_OK) rc = enqueue_tail(p, q, TAIL_CONTROL | TAIL_STEP, grid, cap, cond, 1);
+  for (int u = 0; u < loop_unroll() && rc == ITSK_OK; ++u) {
+    rc = loop_pass(p, q, 1, cap, &grid);
+    if (rc == ITSK_OK) rc = enqueue_tail(p, q, TAIL_CONTROL | TAIL_STEP, grid, cap, cond, 1);
+  }
   cudaGraph_t captured = body;
   e = cudaStreamEndCapture(cap, &captured);
   if (rc != ITSK_OK) return fail(rc);

@@ -217,9 +217,18 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   }
 }
 
+#ifdef ITSK_TIMELINE
+// [slot][0] first CTA start, [1] last CTA end of streaming, [2] last CTA end
+__device__ unsigned long long g_pass_tl[TL_SLOTS][4];
+#endif
+
 template <int CPL, int UNR, int NCW>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaShape sh) {
   constexpr int THREADS = 32 * (NCW + 1);
+#ifdef ITSK_TIMELINE
+  const unsigned long long tl_t0 = gtime();
+  int tl_slot = -1;
+#endif
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int NC = 32 * CPL;
   constexpr bool XREG = CPL <= 8;
@@ -288,6 +297,9 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
       return;
     }
     const int64_t S = ctl->r_slots;
+#ifdef ITSK_TIMELINE
+    tl_slot = a.mode == 1 ? static_cast<int>(ctl->it) + 1 : 0;
+#endif
     if (a.mode == 1) {
       const int64_t it = ctl->it;
       x = a.xs + (it + 1) * a.n;
@@ -436,7 +448,16 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
     for (int w = 0; w < NCW; ++w) sum += ssm[w][tid];
     out[n + tid] = sum;
   }
+#ifdef ITSK_TIMELINE
+  if (tid == 0 && tl_slot >= 0 && tl_slot < TL_SLOTS) {
+    atomicMin(&g_pass_tl[tl_slot][0], tl_t0);
+    atomicMax(&g_pass_tl[tl_slot][1], gtime());
+  }
+#endif
   if (a.tickets) group_reduce(a, n);
+#ifdef ITSK_TIMELINE
+  if (tid == 0 && tl_slot >= 0 && tl_slot < TL_SLOTS) atomicMax(&g_pass_tl[tl_slot][2], gtime());
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -986,3 +1007,15 @@ extern "C" int itsk_fused_pass_ex(const double* A, int64_t m, int64_t n, int64_t
   int grid = 0;
   return launch_pass(a, s, &grid);
 }
+
+#ifdef ITSK_TIMELINE
+extern "C" void itsk_pass_timeline_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_pass_tl, sizeof(itsk::g_pass_tl));
+  unsigned long long z[itsk::TL_SLOTS][4];
+  for (int i = 0; i < itsk::TL_SLOTS; ++i) {
+    z[i][0] = ~0ull;
+    z[i][1] = z[i][2] = z[i][3] = 0;
+  }
+  cudaMemcpyToSymbol(itsk::g_pass_tl, z, sizeof(z));
+}
+#endif
