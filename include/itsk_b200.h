@@ -123,6 +123,11 @@ int itsk_qr_aug_async(double* W, int64_t d, int64_t n, int64_t ldw, double* R, d
 int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
               itsk_stream_t stream);
 /* solve_step (solvers.py:339-340): y = R^{-1} R^{-T} c. */
+/* itsk_trsv with R staged from itsk_pack_upper's layout Rp (one bulk copy;
+ * the diagonal-block inverses applied where well conditioned — the loop
+ * tail's arithmetic).  Used for x0 = R^-1 z and LSQR's solves. */
+int itsk_trsv_rp(const double* R, const double* Rp, int64_t n, const double* c, double* y, int trans,
+                 itsk_stream_t stream);
 int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
                    itsk_stream_t stream);
 

@@ -58,19 +58,21 @@ struct RSel<false> {
   }
 };
 
+// Rp (nullable): itsk_pack_upper's layout, staged with one bulk copy;
+// with_inv: it carries the diagonal-block inverses (the loop tail's solves).
 template <bool PACKED>
-__global__ void __launch_bounds__(DENSE_THREADS) k_trsv(const double* R, int64_t n, const double* c,
-                                               double* y, int mode) {
+__global__ void __launch_bounds__(DENSE_THREADS) k_trsv(const double* R, const double* Rp, int64_t n,
+                                                        const double* c, double* y, int mode, int with_inv) {
   extern __shared__ double sm[];
   double* cur = sm;
-  const auto RA = RSel<PACKED>::make(R, nullptr, n, cur);
+  DiagInv inv{nullptr, nullptr};
+  const auto RA = RSel<PACKED>::make(R, Rp, n, cur, &inv, with_inv != 0);
   double* v = cur;
-  double* tmp = cur + n;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = c[i];
   __syncthreads();
   __shared__ double red_s[64 * (DENSE_THREADS / 32)];
-  if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v, red_s);
-  if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, red_s);
+  if (mode == 1 || mode == 2) trsv_t_inplace(RA, n, v, red_s, inv);
+  if (mode == 0 || mode == 2) trsv_n_inplace(RA, n, v, red_s, inv);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = v[i];
 }
 
@@ -372,17 +374,20 @@ int prep(K kernel, size_t smem) {
   return ITSK_OK;
 }
 
-int launch_trsv(const double* R, int64_t n, const double* c, double* y, int mode, cudaStream_t s) {
+int launch_trsv(const double* R, int64_t n, const double* c, double* y, int mode, cudaStream_t s,
+                const double* Rp = nullptr) {
   const int64_t other = n + 32;
   const bool packed = use_packed(n, other);
-  const size_t smem = static_cast<size_t>((packed ? packed_doubles(n) : 0) + other) * sizeof(double);
+  const bool with_inv = packed && Rp != nullptr && use_packed_inv(n, other);
+  const int64_t tri = with_inv ? rp_doubles(n) : (packed ? packed_doubles(n) : 0);
+  const size_t smem = static_cast<size_t>(tri + other) * sizeof(double);
   int rc;
   if (packed) {
     if ((rc = prep(k_trsv<true>, smem))) return rc;
-    k_trsv<true><<<1, DENSE_THREADS, smem, s>>>(R, n, c, y, mode);
+    k_trsv<true><<<1, DENSE_THREADS, smem, s>>>(R, Rp, n, c, y, mode, with_inv ? 1 : 0);
   } else {
     if ((rc = prep(k_trsv<false>, smem))) return rc;
-    k_trsv<false><<<1, DENSE_THREADS, smem, s>>>(R, n, c, y, mode);
+    k_trsv<false><<<1, DENSE_THREADS, smem, s>>>(R, nullptr, n, c, y, mode, 0);
   }
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -403,6 +408,13 @@ extern "C" int itsk_trsv(const double* R, int64_t n, const double* c, double* y,
   ITSK_REQUIRE(R && c && y && n >= 1, "bad trsv arguments");
   ITSK_REQUIRE(n <= 16384, "trsv: n too large for the single-CTA kernel");
   return launch_trsv(R, n, c, y, trans ? 1 : 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int itsk_trsv_rp(const double* R, const double* Rp, int64_t n, const double* c, double* y,
+                            int trans, itsk_stream_t stream) {
+  ITSK_REQUIRE(R && Rp && c && y && n >= 1, "bad trsv arguments");
+  ITSK_REQUIRE(n <= 16384, "trsv: n too large for the single-CTA kernel");
+  return launch_trsv(R, n, c, y, trans ? 1 : 0, reinterpret_cast<cudaStream_t>(stream), Rp);
 }
 
 extern "C" int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,

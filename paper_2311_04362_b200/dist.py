@@ -144,7 +144,8 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
-        _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
+        _lib.check(lib.itsk_trsv_rp(_dev.ptr(ws.R), _dev.ptr(ws.Rp), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0,
+                                    stream))
     ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
     _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), _dev.ptr(ws.est),
                                 _dev.ptr(ws.Rp), stream))

@@ -40,8 +40,9 @@ from .solvers import (DeviceResiduals, SolverConfig, SolveResult, SolveTrace, _s
 class _DeviceLs:
     """A, b and R on the device plus the fused-pass and TRSV plumbing."""
 
-    def __init__(self, at: torch.Tensor, lda: int, bt: torch.Tensor, r_dev: torch.Tensor):
-        self.at, self.lda, self.bt, self.R = at, lda, bt, r_dev
+    def __init__(self, at: torch.Tensor, lda: int, bt: torch.Tensor, r_dev: torch.Tensor,
+                 rp_dev: torch.Tensor | None = None):
+        self.at, self.lda, self.bt, self.R, self.Rp = at, lda, bt, r_dev, rp_dev
         self.m, self.n = int(at.shape[0]), int(at.shape[1])
         self.dev = at.device
         self.lib = _dev.lib(self.dev)
@@ -62,8 +63,12 @@ class _DeviceLs:
     def rsolve(self, v: np.ndarray, trans: int) -> np.ndarray:
         """R^-1 v (trans = 0) or R^-T v (trans = 1) on the device."""
         self.vin.copy_(torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)))
-        _lib.check(self.lib.itsk_trsv(_dev.ptr(self.R), self.n, _dev.ptr(self.vin), _dev.ptr(self.vout), trans,
-                                      self.stream))
+        if self.Rp is not None:  # R staged from the packed layout (itsk_pack_upper)
+            _lib.check(self.lib.itsk_trsv_rp(_dev.ptr(self.R), _dev.ptr(self.Rp), self.n, _dev.ptr(self.vin),
+                                             _dev.ptr(self.vout), trans, self.stream))
+        else:
+            _lib.check(self.lib.itsk_trsv(_dev.ptr(self.R), self.n, _dev.ptr(self.vin), _dev.ptr(self.vout),
+                                          trans, self.stream))
         return self.vout.cpu().numpy()
 
     def pass_(self, b_ptr: int, bscale: float, x: np.ndarray, r_out: torch.Tensor | None,
@@ -182,7 +187,7 @@ def sketch_and_precondition(a, b, cfg: SolverConfig, truth: Truth | None = None,
         if truth.beta > 0:
             ws.r_true.copy_(_dev.as_device_vector(truth.r, dev))
             r_true = ws.r_true
-    ops = _DeviceLs(at, lda, ws.b, ws.R)
+    ops = _DeviceLs(at, lda, ws.b, ws.R, ws.Rp)
     rs = ws.rs
     count = [0]
     bnorm = [None]

@@ -385,7 +385,8 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
     if cfg.init == "zero":
         ws.xs[0].zero_()
     else:
-        _lib.check(lib.itsk_trsv(_dev.ptr(ws.R), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0, stream))
+        _lib.check(lib.itsk_trsv_rp(_dev.ptr(ws.R), _dev.ptr(ws.Rp), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0,
+                                    stream))
     if not defer:
         _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est_ptr,
                                     _dev.ptr(ws.Rp), stream))

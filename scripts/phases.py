@@ -44,6 +44,7 @@ def qr():
 out["qr(+copy)"] = T(qr)
 out["copyW"] = T(lambda: ws.W.copy_(W0))
 out["trsv_x0"] = T(lambda: _lib.check(lib.itsk_trsv(dv.ptr(ws.R), n, dv.ptr(ws.z), dv.ptr(ws.xs[0]), 0, s)))
+out["trsv_rp_x0"] = T(lambda: _lib.check(lib.itsk_trsv_rp(dv.ptr(ws.R), dv.ptr(ws.Rp), n, dv.ptr(ws.z), dv.ptr(ws.xs[0]), 0, s)))
 out["normest"] = T(lambda: _lib.check(lib.itsk_normest(dv.ptr(ws.R), n, dv.ptr(ws.v0), normest_steps(n), dv.ptr(ws.est), None, s)))
 out["condest"] = T(lambda: _lib.check(lib.itsk_condest(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, None, s)))
 cond_ws = torch.empty(n * n, dtype=torch.float64, device=dev)

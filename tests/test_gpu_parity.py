@@ -6,6 +6,7 @@ refinement loop's FE/RE within 2x of the reference's (one-sided), and
 ||x - x_ref||/||x_ref|| <= 10*kappa*u + FE_ref; normest/condest to rounding.
 """
 
+import ctypes
 import hashlib
 import json
 import math
@@ -232,6 +233,39 @@ def test_trsv_large_residual(pkg, n):
     assert np.linalg.norm(r @ y - c) <= 100 * n * U * kappa * np.linalg.norm(c)
     yt = pkg.tri_solve_upper_transpose(r, c)
     assert np.linalg.norm(r.T @ yt - c) <= 100 * n * U * kappa * np.linalg.norm(c)
+
+
+@pytest.mark.parametrize("n,kappa", [(50, 1e10), (200, 1e10), (200, 1e15), (257, 1e6), (33, 1e3), (500, 1e8)])
+def test_trsv_rp_packed_layout(pkg, orc, n, kappa):
+    """itsk_trsv_rp (R staged from itsk_pack_upper's layout, the diagonal-block
+    inverses where kappa_1 <= 1e4: the loop tail's arithmetic; x0 and LSQR use
+    it) on sketched R factors: residual bound of a backward-stable solve, and
+    agreement with the substitution path (itsk_trsv) to kappa * u."""
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    a, _, _ = orc.gen_randsvd(max(4 * n, 400), n, kappa, 1e-6, n)
+    _, r = orc.householder_qr_econ(orc.sketch_apply(orc.sparse_sign_pattern(2 * n, a.shape[0], 8, n), a))
+    dev = dv.current_device()
+    lib = dv.lib(dev)
+    rt = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
+    nb = ctypes.c_int64()
+    _lib.check(lib.itsk_pack_upper_doubles(n, ctypes.byref(nb)))
+    rp = torch.empty(nb.value, dtype=torch.float64, device=dev)
+    s = dv.stream_ptr()
+    _lib.check(lib.itsk_pack_upper(dv.ptr(rt), n, dv.ptr(rp), s))
+    c = np.random.default_rng(n).standard_normal(n)
+    ct = torch.from_numpy(c).to(dev)
+    kap = np.linalg.cond(r)
+    for trans in (0, 1):
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        y0 = torch.empty(n, dtype=torch.float64, device=dev)
+        _lib.check(lib.itsk_trsv_rp(dv.ptr(rt), dv.ptr(rp), n, dv.ptr(ct), dv.ptr(y), trans, s))
+        _lib.check(lib.itsk_trsv(dv.ptr(rt), n, dv.ptr(ct), dv.ptr(y0), trans, s))
+        y, y0 = y.cpu().numpy(), y0.cpu().numpy()
+        m_ = r.T if trans else r
+        assert np.linalg.norm(m_ @ y - c) <= 100 * n * U * np.linalg.norm(r) * np.linalg.norm(y), trans
+        assert np.linalg.norm(y - y0) <= 100 * n * U * kap * np.linalg.norm(y0), trans
 
 
 @pytest.mark.parametrize("n", [1500, 2000])
