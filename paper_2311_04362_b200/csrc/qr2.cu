@@ -344,10 +344,16 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     gp[ci * NB + nt * 8 + 2 * t4 + 1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
   }
   cl.sync();
-  // G = sum_t G_t in rank order; element e summed by CTA e % C
+  // G = sum_t G_t in rank order; element e summed by CTA e % C (all C
+  // partial loads in flight before the adds: one L2 round trip, not C)
   for (int e = q + C * tid; e < NB * NB; e += C * QP_THREADS) {
+    double v[MAX_C];
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t) v[t] = t < C ? __ldcg(a.Gp + static_cast<int64_t>(t) * NB * NB + e) : 0.0;
     double s = 0.0;
-    for (int t = 0; t < C; ++t) s += __ldcg(a.Gp + static_cast<int64_t>(t) * NB * NB + e);
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t)
+      if (t < C) s += v[t];
     a.G[e] = s;
   }
   Q2P(6);
