@@ -211,6 +211,7 @@ __global__ void k_compact(const uint32_t* flags, const uint32_t* scanned, const 
 // short (draws total..N-1, then a full duplicate scan).
 constexpr int RD_T = 1024;
 constexpr int RD_W = 4;
+constexpr double RD_PAR_MIN = 65536.0;  // redraw rounds with more draws run as parallel kernels
 
 // Exclusive prefix sum over the CTA in thread order; *tot = the CTA total.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tot) {
@@ -315,15 +316,18 @@ __device__ uint32_t flag_compact(const uint32_t* rows, int64_t zeta, const uint3
   return nout;
 }
 
+// first != 0: continues from the parallel first draw (slots[0] = position
+// before it, *pos_in = after it unless its margin ran short, which this
+// kernel then completes); first == 0: continues after host-driven parallel
+// rounds (*pos_in = position, bad_a = the current bad list).  The final
+// position goes to slots[0] for k_signs.
 __global__ void __launch_bounds__(RD_T, 1) k_redraw(Stream st, uint32_t bound, uint32_t thr, uint64_t N,
                                                     uint32_t* rows, int64_t m, int64_t zeta,
                                                     const uint32_t* scanned1, uint64_t nchunks1,
-                                                    uint64_t nwords1, uint64_t* slots, uint32_t* bad_a,
-                                                    uint32_t* bad_b, const uint32_t* nbad1) {
-  // slots[0]: position before the first draw, slots[1]: after it (written by
-  // k_lemire_emit unless its margin ran short); the final position goes to
-  // slots[0] for k_signs
-  const uint64_t total1 = scanned1[nchunks1];
+                                                    uint64_t nwords1, uint64_t* slots, const uint64_t* pos_in,
+                                                    uint32_t* bad_a, uint32_t* bad_b, const uint32_t* nbad1,
+                                                    int first) {
+  const uint64_t total1 = first ? scanned1[nchunks1] : N;
   uint64_t pos;
   uint32_t nbad;
   uint32_t* cur = bad_a;
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(RD_T, 1) k_redraw(Stream st, uint32_t bound, u
     pos = draw_seq(st, slots[0] + nwords1, N - total1, bound, thr, rows, total1, nullptr, zeta);
     nbad = flag_compact(rows, zeta, nullptr, static_cast<uint32_t>(m), cur);
   } else {
-    pos = slots[1];
+    pos = *pos_in;
     nbad = *nbad1;
   }
   while (nbad > 0) {
@@ -501,9 +505,65 @@ extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, cons
     uint32_t* nbad_dev = reinterpret_cast<uint32_t*>(w.scalars + 1);
     k_compact<<<blocks_for(m, 256), 256, 0, s>>>(w.flags, w.fscan, nullptr, m, w.bad_a, nbad_dev);
     count_launch();
-    // every further round (embed.py:41) on one CTA
+    // Further rounds (embed.py:41).  When many columns are expected to hold a
+    // repeat (small d, large zeta: C5's d = 4n points redraw a quarter of the
+    // columns), the big rounds run as parallel draws with the host reading
+    // each round's count; the tail of small rounds — all of them at C1..C4 —
+    // runs on one CTA with no host round trip.
+    uint32_t* cur = w.bad_a;
+    uint32_t* nxt = w.bad_b;
+    uint64_t* pin = slots + 1;
+    uint64_t* pout = slots + 2;
+    int first = 1;
+    double keep = 1.0;  // expected fraction of columns without a repeat
+    for (int64_t k = 1; k < zeta; ++k) keep *= 1.0 - static_cast<double>(k) / static_cast<double>(d);
+    if (static_cast<double>(m) * (1.0 - keep) * static_cast<double>(zeta) > RD_PAR_MIN) {
+      uint64_t hs[2];
+      uint32_t tot1 = 0;
+      ITSK_CUDA(cudaMemcpyAsync(&tot1, w.scanned + nchunks, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      ITSK_CUDA(cudaMemcpyAsync(hs, w.scalars, sizeof(hs), cudaMemcpyDeviceToHost, s));
+      ITSK_CUDA(cudaStreamSynchronize(s));
+      uint32_t nbad = static_cast<uint32_t>(hs[1]);
+      if (tot1 >= static_cast<uint64_t>(nnz)) {  // else k_redraw completes the short first draw
+        first = 0;
+        while (static_cast<uint64_t>(nbad) * zeta > RD_PAR_MIN) {
+          const uint64_t N = static_cast<uint64_t>(nbad) * zeta;
+          uint64_t nw = static_cast<uint64_t>(max_words(static_cast<int64_t>(N)));
+          for (;;) {  // a short margin (never seen in practice) retries with more words
+            const uint64_t nch = (nw + CH - 1) / CH;
+            ITSK_REQUIRE(nch <= w.chunk_cap, "pattern: redraw margin exceeds the workspace");
+            k_lemire_count<<<blocks_for(nch, 256), 256, 0, s>>>(st, pin, nw, bound, thr, w.counts, nch);
+            count_launch();
+            tb = w.cub_bytes;
+            ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned, static_cast<int>(nch + 1), s));
+            count_launch();
+            k_lemire_emit<<<blocks_for(nch, 256), 256, 0, s>>>(st, pin, nw, bound, thr, w.scanned, nch, N, rows,
+                                                                 cur, zeta, pout);
+            count_launch();
+            uint32_t tot = 0;
+            ITSK_CUDA(cudaMemcpyAsync(&tot, w.scanned + nch, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ITSK_CUDA(cudaStreamSynchronize(s));
+            if (tot >= N) break;
+            nw = nw * 2 + 65536;
+          }
+          k_flag_dupes<<<blocks_for(nbad, 256), 256, 0, s>>>(rows, zeta, cur, nbad, w.flags);
+          count_launch();
+          tb = w.cub_bytes;
+          ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.flags, w.fscan, static_cast<int>(nbad), s));
+          count_launch();
+          k_compact<<<blocks_for(nbad, 256), 256, 0, s>>>(w.flags, w.fscan, cur, nbad, nxt, nbad_dev);
+          count_launch();
+          ITSK_CHECK_LAUNCH();
+          ITSK_CUDA(cudaMemcpyAsync(hs, w.scalars, sizeof(hs), cudaMemcpyDeviceToHost, s));
+          ITSK_CUDA(cudaStreamSynchronize(s));
+          nbad = static_cast<uint32_t>(hs[1]);
+          std::swap(cur, nxt);
+          std::swap(pin, pout);
+        }
+      }
+    }
     k_redraw<<<1, RD_T, 0, s>>>(st, bound, thr, static_cast<uint64_t>(nnz), rows, m, zeta, w.scanned, nchunks,
-                                nwords, slots, w.bad_a, w.bad_b, nbad_dev);
+                                nwords, slots, pin, cur, nxt, nbad_dev, first);
     count_launch();
     ITSK_CHECK_LAUNCH();
   }

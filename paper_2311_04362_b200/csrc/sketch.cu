@@ -104,11 +104,139 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   }
 }
 
+// Ring variant: warp per (sketch row, 32-column block), one column per lane,
+// each lane streaming its element of the next RG_DEPTH source rows into a
+// per-warp shared-memory ring with cp.async (8 bytes per lane per source,
+// commit groups of RG_G sources) while it adds the landed ones in source
+// order.  The register gather keeps only UNR sources in flight per warp,
+// which starves the memory system when d x column blocks is small (few
+// warps, long sequential chains: C5's d = 4n points); here ~RG_DEPTH are.
+// Same sums in the same order: bitwise equal to the register gather.
+constexpr int RG_DEPTH = 64;
+constexpr int RG_G = 8;
+constexpr int RG_NG = RG_DEPTH / RG_G;
+constexpr int RG_WARPS = 4;
+
+__device__ __forceinline__ void cp_async8_ring(double* dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int nbytes = valid ? 8 : 0;  // 0: zero-fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit_ring() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_n() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_wait_ring(int pending) {
+  // pending groups allowed to stay in flight (an immediate operand)
+  switch (pending < RG_NG - 1 ? pending : RG_NG - 1) {
+    case 0: cp_wait_n<0>(); break;
+    case 1: cp_wait_n<1>(); break;
+    case 2: cp_wait_n<2>(); break;
+    case 3: cp_wait_n<3>(); break;
+    case 4: cp_wait_n<4>(); break;
+    case 5: cp_wait_n<5>(); break;
+    case 6: cp_wait_n<6>(); break;
+    default: cp_wait_n<7>(); break;
+  }
+}
+
+// Source words reach the issuing lanes as a 32-word register block (one
+// coalesced load, the next block prefetched) and the consumer through a small
+// shared-memory ring written at issue time: no dependent global load sits
+// between consuming a group and issuing its refill.
+__global__ void __launch_bounds__(32 * RG_WARPS) k_sketch_ring(
+    const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
+    const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d,
+    double scale, double* __restrict__ W, int64_t ldw, SkRange rg) {
+  static_assert(RG_NG <= 8 && 32 % RG_G == 0, "ring shape");
+  extern __shared__ __align__(16) double ring_sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ring = ring_sm + static_cast<int64_t>(warp) * RG_DEPTH * 32;
+  uint32_t* rsrc = reinterpret_cast<uint32_t*>(ring_sm + RG_WARPS * RG_DEPTH * 32) + warp * RG_DEPTH;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * RG_WARPS + warp;
+  if (i >= d) return;  // no CTA-wide barriers below
+  const int64_t ncol = n + (b ? 1 : 0);
+  const int64_t col = static_cast<int64_t>(blockIdx.y) * 32 + lane;
+  const int kind = col < n ? 0 : (col == n && b ? 1 : 2);
+  const double* base = kind == 0 ? A + col : (kind == 1 ? b : A);
+  const int64_t stride = kind == 0 ? lda : (kind == 1 ? 1 : 0);
+  double acc = (rg.accum && col < ncol) ? W[i * ldw + col] : 0.0;
+  uint32_t e0 = ptr[i], e1 = ptr[i + 1];
+  if (rg.j0 > 0) e0 = lower_src(src, e0, e1, rg.j0);
+  if (rg.j1 != 0xffffffffu) e1 = lower_src(src, e0, e1, rg.j1);
+  const uint32_t total = e1 - e0;
+  const uint32_t ngroups = (total + RG_G - 1) / RG_G;
+  double* my = ring + lane;
+  // issue side: src words of the 32-block holding the next group, and the block after
+  uint32_t blk = 0;
+  uint32_t wcur = lane < total ? __ldg(src + e0 + lane) : 0u;
+  uint32_t wnxt = 32 + lane < total ? __ldg(src + e0 + 32 + lane) : 0u;
+  auto issue_group = [&](uint32_t g) {
+    const uint32_t q0 = g * RG_G;
+    if ((q0 >> 5) != blk) {  // next 32-block (uniform): rotate and prefetch the one after
+      blk = q0 >> 5;
+      wcur = wnxt;
+      const uint32_t qn = (blk + 1) * 32 + lane;
+      wnxt = qn < total ? __ldg(src + e0 + qn) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < RG_G; ++u) {
+      const uint32_t q = q0 + u;
+      const uint32_t w = __shfl_sync(FULL, wcur, (q0 & 31) + u);
+      if (q < total) cp_async8_ring(my + (q % RG_DEPTH) * 32, base + static_cast<int64_t>(w & 0x7fffffffu) * stride,
+                                    kind != 2);
+    }
+    const uint32_t wv = __shfl_sync(FULL, wcur, (q0 & 31) + (lane & (RG_G - 1)));
+    if (lane < RG_G) rsrc[(q0 + lane) % RG_DEPTH] = wv;
+    cp_commit_ring();
+  };
+  const uint32_t npro = ngroups < static_cast<uint32_t>(RG_NG) ? ngroups : static_cast<uint32_t>(RG_NG);
+  for (uint32_t g = 0; g < npro; ++g) issue_group(g);
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    const uint32_t left = ngroups - g - 1;
+    cp_wait_ring(static_cast<int>(left));
+    __syncwarp();  // rsrc entries written by other lanes
+    double v[RG_G];
+    uint32_t sw[RG_G];
+#pragma unroll
+    for (int u = 0; u < RG_G; ++u) {
+      const uint32_t q = g * RG_G + u;
+      sw[u] = rsrc[q % RG_DEPTH];
+      v[u] = my[(q % RG_DEPTH) * 32];
+    }
+#pragma unroll
+    for (int u = 0; u < RG_G; ++u) {
+      const uint32_t q = g * RG_G + u;
+      if (q < total) acc = __dadd_rn(acc, __dmul_rn((sw[u] >> 31) ? -scale : scale, v[u]));
+    }
+    __syncwarp();  // every lane has read the group's rsrc slots before they are rewritten
+    // the slots just read are free: refill them with group g + RG_NG
+    if (g + RG_NG < ngroups) issue_group(g + RG_NG);
+  }
+  if (col < ncol) W[i * ldw + col] = acc;
+}
+
+int launch_ring(const double* A, int64_t lda, int64_t n, const double* b, const uint32_t* ptr,
+                const uint32_t* src, int64_t d, double scale, double* W, int64_t ldw, SkRange rg,
+                cudaStream_t s) {
+  const int64_t ncol = n + (b ? 1 : 0);
+  dim3 grid(static_cast<unsigned>((d + RG_WARPS - 1) / RG_WARPS), static_cast<unsigned>((ncol + 31) / 32));
+  const size_t smem = RG_WARPS * RG_DEPTH * (32 * sizeof(double) + sizeof(uint32_t));
+  ITSK_CUDA(cudaFuncSetAttribute(k_sketch_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k_sketch_ring<<<grid, 32 * RG_WARPS, smem, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw, rg);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
 // Tuning knobs (read per call so tests can sweep the variants in-process).
 struct SketchTune {
+  int ring = -1;      // 1: cp.async ring variant, 0: register gather, -1: by shape
   int gcpl = 0;       // register gather: cap on columns-per-lane (more column blocks)
   int unr = 0;        // register gather: sources per unrolled group (0 = heuristic)
   SketchTune() {
+    if (const char* e = getenv("ITSK_SKETCH_RING")) ring = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_UNR")) unr = atoi(e);
   }
@@ -164,6 +292,13 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   // parallelism comes only from d x column blocks).  A TMA-staged variant
   // (per-warp ring of bulk-copied row segments) measured 1.8-5x slower: the
   // per-copy cost of 0.25-2 KB bulk copies dominates.
+  // few (sketch row x 32-column) chains — about one wave or less — leave the
+  // register gather with too few loads in flight: the cp.async ring keeps 64
+  // sources per warp in flight (C5 d = 400, n = 100: 1.4x; from d x blocks ~
+  // 5000 up the gather wins, profiles/r04_sketch_ring_vs_gather.txt)
+  const bool ring = tu.ring >= 0 ? tu.ring == 1
+                                 : (tu.gcpl == 0 && tu.unr == 0 && d * ((ncol + 31) / 32) <= 2048);
+  if (ring) return launch_ring(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
   int64_t need = (ncol + 31) / 32;
   int64_t cap = 4;
   while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 6000) cap >>= 1;

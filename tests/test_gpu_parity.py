@@ -74,6 +74,17 @@ def test_pattern_short_first_draw_bitwise(pkg, golden, monkeypatch, div):
         np.testing.assert_array_equal(s.signs, g[key + "_signs"], err_msg=key)
 
 
+@pytest.mark.parametrize("d,m,zeta,seed", [(50, 20000, 8, 4), (400, 200000, 16, 5), (120, 60000, 12, 6)])
+def test_pattern_many_redraws_bitwise(pkg, orc, d, m, zeta, seed):
+    """Small d, large zeta: a large share of the columns repeats a row, so the
+    first redraw rounds run as host-driven parallel draws before the one-CTA
+    kernel takes the tail; the pattern is still numpy's, bit for bit."""
+    s = pkg.sparse_sign_new(d, m, zeta, seed)
+    p = orc.sparse_sign_pattern(d, m, zeta, seed)
+    np.testing.assert_array_equal(s.rows, p.rows)
+    np.testing.assert_array_equal(s.signs, p.signs)
+
+
 def test_pattern_csr_grouping(pkg):
     s = pkg.sparse_sign_new(50, 400, 6, 9)
     ptr = s.ptr_dev.cpu().numpy().view(np.uint32).astype(np.int64)
@@ -104,7 +115,8 @@ def test_full_size_pattern_and_sketch_digests(pkg, golden, orc):
 SKETCH_VARIANTS = [
     {}, {"ITSK_SKETCH_UNR": "8"}, {"ITSK_SKETCH_UNR": "2"}, {"ITSK_SKETCH_GCPL": "2", "ITSK_SKETCH_UNR": "8"},
     {"ITSK_SKETCH_GCPL": "8", "ITSK_SKETCH_UNR": "4"},
-    {"ITSK_SKETCH_GCPL": "4"}, {"ITSK_SKETCH_GCPL": "1"},
+    {"ITSK_SKETCH_GCPL": "4"}, {"ITSK_SKETCH_GCPL": "1"}, {"ITSK_SKETCH_RING": "1"},
+    {"ITSK_SKETCH_RING": "0"},
 ]
 
 
