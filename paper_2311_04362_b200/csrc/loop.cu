@@ -122,6 +122,15 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
   const int64_t K = ctl->max_iters + 1;
   const int64_t xi = begin ? 0 : it + 1;
   const double* x = p.xs + xi * n;
+  // the pass's scalars, loaded before the block sums (one L2 round trip
+  // overlapped with them instead of after)
+  double rr = 0.0, dd = 0.0, tt = 0.0, bb = 0.0;
+  if (threadIdx.x == 0) {
+    rr = p.cs[n];
+    dd = p.cs[n + 1];
+    tt = p.cs[n + 2];
+    bb = p.cs[n + 3];
+  }
   double sx = 0.0, sf = 0.0, st = 0.0;
   int fin = 1;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -139,8 +148,6 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
   const double xt2 = block_sum(st, red);
   const int all_fin = __syncthreads_and(fin);
   if (threadIdx.x == 0) {
-    const double* cs = p.cs;
-    const double rr = cs[n], dd = cs[n + 1], tt = cs[n + 2], bb = cs[n + 3];
     const double resnorm = sqrt(rr);
     double* fe = p.trace;
     double* re = p.trace + K;
@@ -310,6 +317,9 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
   __syncthreads();
   LoopCtl* ctl = &s_ctl;
+  // c for the solves, staged now: its loads overlap the control step
+  if ((flags & TAIL_STEP) && !ctl->result.done)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   TP(0);
 #ifdef ITSK_TIMELINE
   tl_slot = (flags & TAIL_BEGIN) ? 0 : static_cast<int>(ctl->it) + 1;
@@ -334,7 +344,6 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   if (!(flags & TAIL_STEP)) return;
   // d = R^{-1} R^{-T} c in shared memory (R staged above), then x_{it+1}
   __shared__ double red_s[64 * (DENSE_THREADS / 32)];
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
   __syncthreads();
   TP(3);
   if (PACKED) {

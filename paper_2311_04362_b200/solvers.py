@@ -290,9 +290,16 @@ _PIPE_CHUNK_BYTES = 48 << 20
 
 
 def _upload_chunks(m: int, n: int) -> list[tuple[int, int]]:
+    """Row chunks of the host upload.  The sketch of the last chunk sits
+    between the end of the copy and the QR, so the tail is cut finer: the last
+    standard chunk is split into quarters."""
     k = max(2, min(8, -(-8 * m * n // _PIPE_CHUNK_BYTES)))
     step = -(-m // k)
-    return [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
+    chunks = [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
+    r0, r1 = chunks.pop()
+    q = max(1, -(-(r1 - r0) // 4))
+    chunks += [(a, min(r1, a + q)) for a in range(r0, r1, q)]
+    return chunks
 
 
 def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: int, csr=None, upload=None,

@@ -60,5 +60,5 @@ for i in range(K):
           + " ".join(f"{v:6.1f}" for v in r))
 med = np.median(np.array(rows[1:-1]), axis=0)
 print("median (slots 1..K-2): pass %.1f reduce %.1f gap %.1f ctl %.1f Rty %.1f Rx %.1f upd %.1f us" % tuple(med))
-print(f"iteration period (pass start to pass start): "
-      f"{np.median(np.diff([us(P[i, 0]) for i in range(1, K)])):.1f} us")
+print(f"iteration period (tail end to tail end): "
+      f"{np.median(np.diff([us(T[i, 5]) for i in range(1, K - 1)])):.1f} us")
