@@ -186,27 +186,34 @@ __device__ __forceinline__ double sum_strided(const double* p, int64_t stride, i
   return s;
 }
 
+// Ticket increment with acquire-release semantics at GPU scope, by one
+// thread after a CTA barrier: the barrier orders the CTA's partial writes
+// before the release, and the acquire orders the last arriver's loads of
+// the other CTAs' partials after it (one fence per CTA instead of one per
+// thread).
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ void group_reduce(const PassArgs& a, int64_t n) {
   __shared__ int s_last;
   const int64_t w = n + 4;
   const int G = a.group, gi = static_cast<int>(blockIdx.x) / G;
   const int gsz = min(G, static_cast<int>(gridDim.x) - gi * G);
   const int ng = (static_cast<int>(gridDim.x) + G - 1) / G;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[gi], 1u) == static_cast<unsigned>(gsz - 1);
+  if (threadIdx.x == 0) s_last = ticket_acq_rel(&a.tickets[gi]) == static_cast<unsigned>(gsz - 1);
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   if (threadIdx.x == 0) a.tickets[gi] = 0;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x)
     a.gpart[static_cast<int64_t>(gi) * w + c] = sum_strided(a.part + static_cast<int64_t>(gi) * G * w + c, w, gsz, 0.0);
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[ng], 1u) == static_cast<unsigned>(ng - 1);
+  if (threadIdx.x == 0) s_last = ticket_acq_rel(&a.tickets[ng]) == static_cast<unsigned>(ng - 1);
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   if (threadIdx.x == 0) a.tickets[ng] = 0;
   // even groups into s0, odd groups into s1, then s0 + s1
   const int ne = (ng + 1) / 2, no = ng / 2;
