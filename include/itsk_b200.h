@@ -217,6 +217,24 @@ int itsk_csr_pass(const itsk_csr_plan* plan, const double* b, double bscale, con
  * CUDA graph with a conditional WHILE node (no host round trip per
  * iteration), or step-wise for multi-GPU (collective between pre and post).
  * -------------------------------------------------------------------- */
+/* Peer-memory exchange of the loop's per-iteration partial sums (the
+ * allreduce of [c | norms] over NVLink without NCCL): each rank's pass, after
+ * its in-kernel reduction, stores its partial into every rank's receive
+ * buffer (peer-mapped pointers, e.g. torch symmetric memory) and raises its
+ * flag there with the exchange's epoch; each rank's tail waits for all flags
+ * of that epoch and sums the partials in rank order — the same bytes on
+ * every rank.  recv[r]: rank r's buffer of 2 x size x (n+4) doubles (epoch
+ * parity x source rank); flags[r]: rank r's size uint64 flags, zero before
+ * the first exchange.  Exchanges of one loop use epochs epoch_base ..
+ * epoch_base + max_iters; the next loop on the same buffers starts above. */
+#define ITSK_MAX_PEERS 8
+typedef struct itsk_peer_params {
+  int32_t rank, size;
+  int64_t epoch_base;
+  double* recv[ITSK_MAX_PEERS];
+  uint64_t* flags[ITSK_MAX_PEERS];
+} itsk_peer_params;
+
 typedef struct itsk_loop_params {
   int64_t m, n, lda;        /* local rows on this rank */
   int64_t max_iters, extra_iters;
@@ -250,6 +268,9 @@ typedef struct itsk_loop_params {
    * were ready.  Requires r_slots == max_iters + 1 (the stop may move back
    * to an earlier, still-held iterate). */
   const uint64_t* est_ready;
+  /* Peer-memory exchange (nullable): with it the sharded loop needs no host
+   * collective — itsk_loop_begin / the loop graph run it end to end. */
+  const itsk_peer_params* peer;
 } itsk_loop_params;
 
 typedef struct itsk_loop_result { /* read back with one D2H copy */

@@ -46,6 +46,19 @@ class LoopParams(ctypes.Structure):
         ("ws", c_dp), ("ws_bytes", c_i64),
         ("csr", c_dp),
         ("est_ready", c_dp),
+        ("peer", c_dp),
+    ]
+
+
+MAX_PEERS = 8  # include/itsk_b200.h ITSK_MAX_PEERS
+
+
+class PeerParams(ctypes.Structure):
+    """itsk_peer_params (include/itsk_b200.h)."""
+
+    _fields_ = [
+        ("rank", ctypes.c_int32), ("size", ctypes.c_int32), ("epoch_base", c_i64),
+        ("recv", c_dp * MAX_PEERS), ("flags", c_dp * MAX_PEERS),
     ]
 
 

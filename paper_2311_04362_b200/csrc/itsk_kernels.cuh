@@ -20,7 +20,16 @@ struct LoopCtl {
   double xtnorm;      // ||x_true||
   int32_t resolve;    // loop ended before the deferred estimates were ready
   int32_t pad1;
+  int64_t epoch_base; // peer exchange: epoch of the begin pass (written per loop, read by the graph's kernels)
   itsk_loop_result result;
+};
+
+// Peer exchange of the loop's partial sums (itsk_peer_params); size == 0: off.
+struct PeerArgs {
+  int rank = 0, size = 0;
+  int64_t epoch_base = 0;
+  double* recv[ITSK_MAX_PEERS] = {};
+  uint64_t* flags[ITSK_MAX_PEERS] = {};
 };
 
 // Pointers the per-iteration kernels resolve from ctl->it.
@@ -34,6 +43,7 @@ struct LoopPtrs {
   const double* normest;
   const double* condest;
   const uint64_t* est_ready;  // nullptr: the estimates are ready
+  PeerArgs peer;
   double* xs;
   double* rs;
   double* trace;
@@ -77,6 +87,7 @@ struct PassArgs {
   int group;
   double bscale = 1.0;  // r = bscale * b - A x (LSQR: u_{k+1} beta = A y - alpha u_k)
   int sm_reserve = 0;   // SMs left free for kernels running beside the pass (the loop's estimates and tail)
+  PeerArgs peer;        // loop mode: send the reduced partial to every rank
 };
 
 // counters / group partials needed by the in-kernel reduction of a pass

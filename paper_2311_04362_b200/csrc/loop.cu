@@ -29,7 +29,7 @@ namespace {
 __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iters,
                             int64_t extra_iters, int variant, int r_slots, int has_truth,
                             int has_xtrue, double alpha, double beta, double u, double gamma,
-                            double rho, double truth_beta) {
+                            double rho, double truth_beta, int64_t epoch_base) {
   ctl->m = m;
   ctl->n = n;
   ctl->max_iters = max_iters;
@@ -49,6 +49,7 @@ __global__ void k_loop_init(LoopCtl* ctl, int64_t m, int64_t n, int64_t max_iter
   ctl->nhist = 0;
   ctl->eval_next = 1;
   ctl->resolve = 0;
+  ctl->epoch_base = epoch_base;
   for (int i = 0; i < 8; ++i) ctl->hist[i] = 0.0;
   ctl->lo = INFINITY;
   ctl->xtnorm = 0.0;
@@ -266,6 +267,41 @@ __global__ void k_flag_store(uint64_t* flag, uint64_t value) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
 
+// Peer exchange, receiving side (itsk_peer_params): wait until every rank's
+// partial of this epoch has landed, then p.cs = sum over ranks in rank order
+// (identical bytes on every rank).  A rank that never arrives (a failed peer)
+// traps after 60 s instead of hanging the GPU.
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void peer_gather(const LoopPtrs& p, int64_t epoch_base, int64_t it_epoch) {
+  const PeerArgs& pe = p.peer;
+  const uint64_t epoch = static_cast<uint64_t>(epoch_base + it_epoch);
+  const uint64_t* fl = pe.flags[pe.rank];
+  if (static_cast<int>(threadIdx.x) < pe.size) {
+    uint64_t t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys_u64(fl + threadIdx.x) < epoch) {
+      __nanosleep(64);
+      uint64_t t = 0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60ull * 1000000000ull) asm volatile("trap;");
+    }
+  }
+  __syncthreads();
+  const int64_t w = p.n + 4;
+  const double* rv = pe.recv[pe.rank] + (epoch & 1) * pe.size * w;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    double s = __ldcg(rv + c);
+    for (int r = 1; r < pe.size; ++r) s += __ldcg(rv + r * w + c);
+    p.cs[c] = s;
+  }
+  __syncthreads();
+}
+
 enum : int { TAIL_CONTROL = 2, TAIL_STEP = 4, TAIL_BEGIN = 8 };
 
 // The serial tail of an iteration on one CTA (see the file comment).
@@ -317,6 +353,8 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
   __syncthreads();
   LoopCtl* ctl = &s_ctl;
+  if (p.peer.size > 0 && !ctl->result.done)
+    peer_gather(p, ctl->epoch_base, (flags & TAIL_BEGIN) ? 0 : ctl->it + 1);
   // c for the solves, staged now: its loads overlap the control step
   if ((flags & TAIL_STEP) && !ctl->result.done)
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = p.cs[i];
@@ -415,11 +453,33 @@ int check_params(const itsk_loop_params* p) {
                    p->cs && p->ws,
                "null pointer in loop params");
   ITSK_REQUIRE(p->n <= 6000, "loop: n too large for the single-CTA solves");
+  if (p->peer) {
+    const itsk_peer_params* g = p->peer;
+    ITSK_REQUIRE(g->size >= 1 && g->size <= ITSK_MAX_PEERS && g->rank >= 0 && g->rank < g->size &&
+                     g->epoch_base >= 1,
+                 "bad peer params (size %d, rank %d, epoch_base %lld)", g->size, g->rank,
+                 (long long)g->epoch_base);
+    for (int r = 0; r < g->size; ++r) ITSK_REQUIRE(g->recv[r] && g->flags[r], "null peer buffer of rank %d", r);
+    ITSK_REQUIRE(!p->csr, "peer exchange: dense A only");
+  }
   ITSK_REQUIRE(!p->est_ready || p->r_slots == p->max_iters + 1,
                "deferred estimates need every residual kept (r_slots == max_iters + 1)");
   int64_t need = loop_layout(nullptr, p->m, p->n).bytes;
   ITSK_REQUIRE(need <= p->ws_bytes, "loop workspace too small");
   return ITSK_OK;
+}
+
+PeerArgs peer_args(const itsk_loop_params* p) {
+  PeerArgs g;
+  if (!p->peer) return g;
+  g.rank = p->peer->rank;
+  g.size = p->peer->size;
+  g.epoch_base = p->peer->epoch_base;
+  for (int r = 0; r < ITSK_MAX_PEERS; ++r) {
+    g.recv[r] = p->peer->recv[r];
+    g.flags[r] = p->peer->flags[r];
+  }
+  return g;
 }
 
 LoopPtrs make_ptrs(const itsk_loop_params* p) {
@@ -434,6 +494,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.normest = p->normest;
   q.condest = p->condest;
   q.est_ready = p->est_ready;
+  q.peer = peer_args(p);
   q.xs = p->xs;
   q.rs = p->rs;
   q.trace = p->trace;
@@ -479,6 +540,7 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   a.cs = p->cs;
   a.group = L.group;
   a.sm_reserve = loop_sm_reserve();
+  a.peer = q.peer;
   return a;
 }
 
@@ -578,7 +640,7 @@ extern "C" int itsk_loop_begin_local(const itsk_loop_params* p, itsk_stream_t st
   LoopPtrs q = make_ptrs(p);
   k_loop_init<<<1, 1, 0, s>>>(q.ctl, p->m, p->n, p->max_iters, p->extra_iters, p->variant,
                               p->r_slots, p->has_truth, p->x_true != nullptr, p->alpha, p->beta,
-                              p->u, p->gamma, p->rho, p->truth_beta);
+                              p->u, p->gamma, p->rho, p->truth_beta, p->peer ? p->peer->epoch_base : 0);
   count_launch();
   ITSK_CHECK_LAUNCH();
   if ((rc = reset_tickets(p, s))) return rc;
@@ -602,7 +664,7 @@ extern "C" int itsk_loop_begin(const itsk_loop_params* p, itsk_stream_t stream) 
   LoopPtrs q = make_ptrs(p);
   k_loop_init<<<1, 1, 0, s>>>(q.ctl, p->m, p->n, p->max_iters, p->extra_iters, p->variant,
                               p->r_slots, p->has_truth, p->x_true != nullptr, p->alpha, p->beta,
-                              p->u, p->gamma, p->rho, p->truth_beta);
+                              p->u, p->gamma, p->rho, p->truth_beta, p->peer ? p->peer->epoch_base : 0);
   count_launch();
   ITSK_CHECK_LAUNCH();
   if ((rc = reset_tickets(p, s))) return rc;

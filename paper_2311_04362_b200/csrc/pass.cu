@@ -217,10 +217,26 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   if (threadIdx.x == 0) a.tickets[ng] = 0;
   // even groups into s0, odd groups into s1, then s0 + s1
   const int ne = (ng + 1) / 2, no = ng / 2;
+  const PeerArgs& pe = a.peer;
+  const bool send = pe.size > 0 && a.ctl != nullptr;
+  const int64_t epoch = send ? a.ctl->epoch_base + (a.mode == 2 ? 0 : a.ctl->it + 1) : 0;
+  const int64_t slot = ((epoch & 1) * pe.size + pe.rank) * w;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
     const double s0 = sum_strided(a.gpart + c, 2 * w, ne, 0.0);
     const double s1 = sum_strided(a.gpart + w + c, 2 * w, no, 0.0);
-    a.cs[c] = s0 + s1;
+    const double v = s0 + s1;
+    a.cs[c] = v;
+    // peer exchange: this rank's partial into every rank's receive buffer
+    if (send)
+      for (int r = 0; r < pe.size; ++r) pe.recv[r][slot + c] = v;
+  }
+  if (send) {
+    __threadfence_system();
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < pe.size)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pe.flags[threadIdx.x] + pe.rank),
+                   "l"(static_cast<unsigned long long>(epoch))
+                   : "memory");
   }
 }
 
@@ -686,6 +702,25 @@ __global__ void k_finalize(const double* __restrict__ part, int grid, int64_t n,
   if (lane == 0) cs[c] = s;
 }
 
+// Peer send for the passes without the in-kernel reduction (k_pass +
+// k_finalize, rows not 16-byte aligned): the reduced partial, complete when
+// this kernel starts, to every rank's receive buffer, then the flags.
+__global__ void k_peer_send(const double* __restrict__ cs, int64_t w, const LoopCtl* ctl, int mode, PeerArgs pe) {
+  if (ctl->result.done) return;
+  const int64_t epoch = ctl->epoch_base + (mode == 2 ? 0 : ctl->it + 1);
+  const int64_t slot = ((epoch & 1) * pe.size + pe.rank) * w;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    const double v = cs[c];
+    for (int r = 0; r < pe.size; ++r) pe.recv[r][slot + c] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (static_cast<int>(threadIdx.x) < pe.size)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pe.flags[threadIdx.x] + pe.rank),
+                 "l"(static_cast<unsigned long long>(epoch))
+                 : "memory");
+}
+
 template <int CPL>
 size_t pass_smem() {
   return static_cast<size_t>(32 * CPL) * (1 + PASS_WARPS) * sizeof(double);
@@ -900,6 +935,11 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
       return ITSK_EINVAL;
   }
   if (rc == ITSK_OK && a0.tickets) rc = launch_finalize(a0.part, grid, a0.n, a0.cs, a0.ctl, s);
+  if (rc == ITSK_OK && a0.peer.size > 0 && a0.ctl) {
+    k_peer_send<<<1, 256, 0, s>>>(a0.cs, a0.n + 4, a0.ctl, a0.mode, a0.peer);
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+  }
   return rc;
 }
 

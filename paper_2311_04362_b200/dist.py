@@ -81,22 +81,90 @@ class ShardedWorkspace(_Workspace):
         self.pat_ws = _dev.workspace(nb.value, dev)
 
 
-def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
-                                truth: Truth | None = None, group=None, *, residuals: str = "last",
-                                check_every: int = 4):
-    """Row-sharded solve.  Each rank passes its own block [row0, row0+m_local)
-    of A and b (numpy or CUDA tensors); `truth.r` may be the full vector or
-    the local slice.  A sparse block (scipy sparse / CsrMatrix) runs the CSR
-    pass of sparse.cu on the rank's rows.  Returns a SolveResult whose iterates / solution / trace
-    scalars are identical on every rank; residual_vectors hold the local rows."""
+class PeerExchange:
+    """Buffers of the loop's peer-memory exchange (itsk_peer_params): every
+    rank's pass stores its reduced [c | norms] partial into every rank's
+    receive buffer over NVLink and raises a flag there; every rank's tail
+    waits for the flags and sums the partials in rank order.  No host
+    collective per iteration, so the sharded loop runs as one CUDA graph.
+
+    recv_ptrs / flag_ptrs are the device addresses of each rank's receive
+    buffer (2 x world x (n+4) float64) and flags (world uint64, zero at
+    start) as seen from this rank — torch symmetric memory peers on the GPU
+    box, or plain tensors of one device in the single-process tests."""
+
+    def __init__(self, rank: int, world: int, recv_ptrs, flag_ptrs, keep=()):
+        if not 1 <= world <= _lib.MAX_PEERS or not 0 <= rank < world:
+            raise ValueError(f"peer exchange: rank {rank} of {world} (at most {_lib.MAX_PEERS} ranks)")
+        if len(recv_ptrs) != world or len(flag_ptrs) != world:
+            raise ValueError("peer exchange: one receive buffer and one flag array per rank")
+        self.rank, self.world = rank, world
+        self.recv_ptrs, self.flag_ptrs = [int(p) for p in recv_ptrs], [int(p) for p in flag_ptrs]
+        self._keep = keep  # the tensors / handles behind the pointers
+        self.next_epoch = 1
+
+    @staticmethod
+    def buffers(n: int, world: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
+        return (torch.zeros(2 * world * (n + 4), dtype=torch.float64, device=dev),
+                torch.zeros(world, dtype=torch.int64, device=dev))
+
+    def params(self, max_iters: int) -> _lib.PeerParams:
+        """Parameters of one loop; its exchanges use epochs epoch_base ..
+        epoch_base + max_iters, the next loop starts above them (every rank
+        runs the same sequence of solves, so the epochs agree)."""
+        pp = _lib.PeerParams()
+        pp.rank, pp.size = self.rank, self.world
+        pp.epoch_base = self.next_epoch
+        self.next_epoch += max_iters + 2
+        for r in range(self.world):
+            pp.recv[r] = self.recv_ptrs[r]
+            pp.flags[r] = self.flag_ptrs[r]
+        return pp
+
+
+_PEERS: dict = {}
+
+
+def peer_exchange(n: int, dev, group=None) -> PeerExchange | None:
+    """The rank's PeerExchange for loops with n columns on `group`, set up once
+    through torch symmetric memory (IPC-mapped peer buffers over NVLink); None
+    when symmetric memory is unavailable (the caller falls back to NCCL)."""
     import torch.distributed as tdist
 
+    world = tdist.get_world_size(group)
+    rank = tdist.get_rank(group)
+    key = (id(group), dev.index, n, world)
+    if key in _PEERS:
+        return _PEERS[key]
+    if world > _lib.MAX_PEERS:
+        return None
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        g = group if group is not None else tdist.group.WORLD
+        recv = symm_mem.empty(2 * world * (n + 4), dtype=torch.float64, device=dev)
+        flags = symm_mem.empty(world, dtype=torch.int64, device=dev)
+        recv.zero_()
+        flags.zero_()
+        torch.cuda.synchronize(dev)
+        hr = symm_mem.rendezvous(recv, g)
+        hf = symm_mem.rendezvous(flags, g)
+        tdist.barrier(group=group)  # every rank's flags are zero before any rank writes
+        px = PeerExchange(rank, world, list(hr.buffer_ptrs), list(hf.buffer_ptrs), keep=(recv, flags, hr, hf))
+    except Exception:  # noqa: BLE001 - no symmetric memory on this setup: NCCL path
+        px = None
+    _PEERS[key] = px
+    return px
+
+
+def _shard_prepare(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int, truth, residuals: str):
+    """Per-rank setup up to the partial sketch: workspace, local A / b /
+    r_true, the full pattern from the shared seed, the CSR of this rank's
+    columns of S and S[:, J_g][A_g | b_g] in ws.W (still to be summed)."""
     from .sparse import as_csr_matrix, is_sparse
 
-    a_shape = a_local.shape
-    m_loc, n = int(a_shape[0]), int(a_shape[1])
+    m_loc, n = int(a_local.shape[0]), int(a_local.shape[1])
     cfg.validate(n)
-    alpha, beta = update_coeffs(cfg, n)
     if cfg.track_be:
         raise ValueError("track_be is not supported by the sharded solver")
     dev = _dev.current_device()
@@ -116,13 +184,7 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
             r = truth.r
             r = r[row0:row0 + m_loc] if r.shape[0] == m_total else r
             ws.r_true.copy_(_dev.as_device_vector(r, dev))
-    stream_obj = torch.cuda.current_stream(dev)
-    stream = int(stream_obj.cuda_stream)
-
-    def allreduce(t: torch.Tensor):
-        tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
-
-    # pattern of all m columns from the shared seed, CSR of this rank's block
+    stream = _dev.stream_ptr()
     words, has32, pend = pcg_state(cfg.rng_seed)
     _lib.check(lib.itsk_sparse_sign_pattern(
         cfg.d, m_total, cfg.zeta, words, has32, pend, _dev.ptr(ws.rows_full), _dev.ptr(ws.neg_full),
@@ -137,7 +199,15 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     else:
         _lib.check(lib.itsk_sketch(_dev.ptr(at), m_loc, n, lda, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr),
                                    _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
-    allreduce(ws.W)
+    return ws, at, lda, csr
+
+
+def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange | None = None):
+    """Replicated part after the summed sketch: QR, x0, normest, condest and
+    the loop parameters (with the peer exchange when given)."""
+    lib = _dev.lib(ws.dev)
+    n = ws.n
+    stream = _dev.stream_ptr()
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
@@ -151,27 +221,69 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
                                 _dev.ptr(ws.Rp), stream))
     _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, _dev.ptr(ws.Rp),
                                 stream))
+    alpha, beta = update_coeffs(cfg, n)
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=ws.m, csr=csr)
+    if peer is not None:
+        ws.peer_params = peer.params(cfg.max_iters)  # kept alive with the workspace
+        p.peer = ctypes.addressof(ws.peer_params)
+    return p
 
-    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=m_loc, csr=csr)
-    cs = ws.cs[: n + 4]
-    _lib.check(lib.itsk_loop_begin_local(ctypes.byref(p), stream))
-    allreduce(cs)
-    _lib.check(lib.itsk_loop_begin_finish(ctypes.byref(p), stream))
-    rp = ctypes.c_void_p()
-    _lib.check(lib.itsk_loop_result_ptr(ctypes.byref(p), ctypes.byref(rp)))
-    res_off = rp.value - _dev.ptr(ws.loop_ws)
-    done_dev = ws.loop_ws[res_off + 8: res_off + 12]  # itsk_loop_result.done
 
-    def is_done() -> bool:
-        return bool(done_dev.view(torch.int32).item())
+def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
+                                truth: Truth | None = None, group=None, *, residuals: str = "last",
+                                check_every: int = 4, peer: str = "auto"):
+    """Row-sharded solve.  Each rank passes its own block [row0, row0+m_local)
+    of A and b (numpy or CUDA tensors); `truth.r` may be the full vector or
+    the local slice.  A sparse block (scipy sparse / CsrMatrix) runs the CSR
+    pass of sparse.cu on the rank's rows.  Returns a SolveResult whose iterates / solution / trace
+    scalars are identical on every rank; residual_vectors hold the local rows.
 
-    run_sharded_loop(
-        lambda: _lib.check(lib.itsk_loop_step_pre(ctypes.byref(p), stream)),
-        lambda: allreduce(cs),
-        lambda: _lib.check(lib.itsk_loop_step_post(ctypes.byref(p), stream)),
-        is_done, cfg.max_iters, check_every)
+    peer: "auto" sums the loop's per-iteration partials through the
+    peer-memory exchange (PeerExchange: the pass stores to every rank over
+    NVLink, the tail gathers; the whole loop is one CUDA graph) when
+    symmetric memory is available and A is dense, else with NCCL allreduce
+    between the two halves of each iteration; "nccl" forces the latter."""
+    import torch.distributed as tdist
+
+    if peer not in ("auto", "nccl"):
+        raise ValueError("peer must be 'auto' or 'nccl'")
+    ws, at, lda, csr = _shard_prepare(a_local, b_local, cfg, m_total, row0, truth, residuals)
+    lib = _dev.lib(ws.dev)
+    n = ws.n
+    stream_obj = torch.cuda.current_stream(ws.dev)
+    stream = int(stream_obj.cuda_stream)
+
+    def allreduce(t: torch.Tensor):
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
+
+    allreduce(ws.W)
+    px = peer_exchange(n, ws.dev, group) if (peer == "auto" and csr is None) else None
+    p = _shard_factor(ws, at, lda, csr, cfg, truth, px)
+    if px is not None:
+        from .solvers import run_loop
+
+        run_loop(lib, ws, p, True, stream)
+    else:
+        cs = ws.cs[: n + 4]
+        _lib.check(lib.itsk_loop_begin_local(ctypes.byref(p), stream))
+        allreduce(cs)
+        _lib.check(lib.itsk_loop_begin_finish(ctypes.byref(p), stream))
+        rp = ctypes.c_void_p()
+        _lib.check(lib.itsk_loop_result_ptr(ctypes.byref(p), ctypes.byref(rp)))
+        res_off = rp.value - _dev.ptr(ws.loop_ws)
+        done_dev = ws.loop_ws[res_off + 8: res_off + 12]  # itsk_loop_result.done
+
+        def is_done() -> bool:
+            return bool(done_dev.view(torch.int32).item())
+
+        run_sharded_loop(
+            lambda: _lib.check(lib.itsk_loop_step_pre(ctypes.byref(p), stream)),
+            lambda: allreduce(cs),
+            lambda: _lib.check(lib.itsk_loop_step_post(ctypes.byref(p), stream)),
+            is_done, cfg.max_iters, check_every)
     res = _read_result(lib, ws, p, stream_obj)
     out = _assemble(ws, res, truth, cfg, at, ws.b)
     out._workspace = ws  # keep the local residual rows alive
     out._csr = csr       # and the local CSR plan the trace's residuals came from
+    out.peer_exchange = px is not None
     return out

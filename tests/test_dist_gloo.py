@@ -170,3 +170,35 @@ def test_two_rank_sparse_sums_gloo():
         res = dict(out)
     for r in range(world):
         assert res[r]["sk"] < 1e-14 and res[r]["c"] < 1e-13
+
+
+def test_peer_exchange_params_host_logic():
+    """PeerExchange (dist.py): one receive buffer and flag array per rank, at
+    most ITSK_MAX_PEERS ranks, and epochs that never repeat across solves —
+    every rank runs the same sequence of solves, so the sequences agree."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200.dist import PeerExchange
+
+    # the ctypes mirror of itsk_peer_params: two int32, one int64, 2 x 8 pointers
+    assert ctypes.sizeof(_lib.PeerParams) == 8 + 8 + 2 * 8 * _lib.MAX_PEERS
+    assert _lib.LoopParams._fields_[-1][0] == "peer"
+    ranks = [PeerExchange(r, 3, [100, 200, 300], [10, 20, 30]) for r in range(3)]
+    seqs = [[], [], []]
+    for max_iters in (50, 0, 7, 50):
+        for r, px in enumerate(ranks):
+            pp = px.params(max_iters)
+            assert pp.rank == r and pp.size == 3
+            assert list(pp.recv)[:3] == [100, 200, 300] and list(pp.flags)[:3] == [10, 20, 30]
+            seqs[r].append((pp.epoch_base, max_iters))
+    assert seqs[0] == seqs[1] == seqs[2]
+    # a loop uses epochs base .. base + max_iters; the next one starts above
+    for (b0, k0), (b1, _) in zip(seqs[0], seqs[0][1:]):
+        assert b0 >= 1 and b1 > b0 + k0
+    with pytest.raises(ValueError):
+        PeerExchange(0, 9, list(range(9)), list(range(9)))
+    with pytest.raises(ValueError):
+        PeerExchange(2, 2, [1, 2], [1, 2])
+    with pytest.raises(ValueError):
+        PeerExchange(0, 2, [1], [1, 2])

@@ -33,22 +33,112 @@ def nccl_group():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("peer", ["nccl", "auto"])
 @pytest.mark.parametrize("m,n,kappa,beta,d,variant", [(20000, 60, 1e8, 1e-6, 1200, "basic"),
                                                         (50000, 200, 1e10, 1e-10, 4000, "momentum"),
                                                         (3001, 17, 1e4, 1e-3, 340, "damped")])
-def test_sharded_solve_matches_single_gpu(nccl_group, m, n, kappa, beta, d, variant):
+def test_sharded_solve_matches_single_gpu(nccl_group, m, n, kappa, beta, d, variant, peer):
+    """peer="auto": the per-iteration sums go through the peer-memory exchange
+    (torch symmetric memory, one rank) and the loop is one CUDA graph;
+    peer="nccl": NCCL allreduce between the halves of each iteration."""
     import paper_2311_04362_b200 as itsk
     from paper_2311_04362_b200.dist import iterative_sketching_sharded
 
     p = itsk.gen_randsvd(m, n, kappa, beta, 3)
     cfg = itsk.SolverConfig(d=d, variant=variant, rng_seed=3)
     ref = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals="last")
-    got = iterative_sketching_sharded(p.a, p.b, itsk.SolverConfig(d=d, variant=variant, rng_seed=3), m, 0, p.truth)
+    for rep in range(2):  # the second solve reuses the exchange buffers (next epochs)
+        got = iterative_sketching_sharded(p.a, p.b, itsk.SolverConfig(d=d, variant=variant, rng_seed=3), m, 0,
+                                          p.truth, peer=peer)
+        if peer == "auto":
+            assert got.peer_exchange, "symmetric memory unavailable: peer exchange not exercised"
+        _same_solve(got, ref)
+
+
+def _same_solve(got, ref):
     assert got.trace.stop_reason == ref.trace.stop_reason
     assert got.iterations == ref.iterations
     assert np.array_equal(got.solution, ref.solution)
     assert got.trace.fe == ref.trace.fe and got.trace.re == ref.trace.re
     assert got.trace.normest == ref.trace.normest and got.trace.condest == ref.trace.condest
+
+
+@pytest.mark.parametrize("m,n,d,variant,world", [(30000, 60, 1200, "basic", 2), (40001, 120, 2400, "momentum", 3),
+                                                  (9001, 17, 340, "damped", 2)])
+def test_peer_exchange_ranks_in_one_process(m, n, d, variant, world):
+    """The peer exchange's kernels for `world` ranks, all on this one GPU and
+    in one process (each rank's buffers are plain device tensors, the peers'
+    pointers point at the other ranks' tensors).  Kernels never wait on work
+    that has not been issued yet: per iteration every rank's pass (which
+    stores its partial to all ranks and raises its flags) runs before any
+    rank's tail (which waits for the flags and sums in rank order).  Every
+    rank must hold the same iterates, equal bit for bit to the same sharded
+    solve with the per-iteration sums formed on the host in rank order."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import ctypes
+
+    import paper_2311_04362_b200 as itsk
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+    from paper_2311_04362_b200.dist import PeerExchange, _shard_factor, _shard_prepare, shard_bounds
+    from paper_2311_04362_b200.solvers import _assemble, _read_result
+
+    p = itsk.gen_randsvd(m, n, 1e8, 1e-6, 4)
+    dev = dv.current_device()
+    lib = dv.lib(dev)
+    so = torch.cuda.current_stream(dev)
+    s = int(so.cuda_stream)
+
+    def solve(peered: bool):
+        cfg = itsk.SolverConfig(d=d, variant=variant, rng_seed=4)
+        ranks = []
+        for r in range(world):
+            r0, r1 = shard_bounds(m, world, r)
+            ranks.append(_shard_prepare(p.a[r0:r1], p.b[r0:r1], cfg, m, r0, None, "last"))
+        W = ranks[0][0].W.clone()
+        for ws, *_ in ranks[1:]:
+            W += ws.W
+        for ws, *_ in ranks:
+            ws.W.copy_(W)
+        bufs = [PeerExchange.buffers(n, world, dev) for _ in range(world)]
+        pxs = [PeerExchange(r, world, [b[0].data_ptr() for b in bufs], [b[1].data_ptr() for b in bufs], keep=bufs)
+               for r in range(world)] if peered else [None] * world
+        ps = [_shard_factor(ws, at, lda, csr, cfg, None, px) for (ws, at, lda, csr), px in zip(ranks, pxs)]
+        cs = [ws.cs[: n + 4] for ws, *_ in ranks]
+
+        def host_sum():
+            tot = cs[0].clone()
+            for c in cs[1:]:
+                tot += c
+            for c in cs:
+                c.copy_(tot)
+
+        for r in range(world):
+            _lib.check(lib.itsk_loop_begin_local(ctypes.byref(ps[r]), s))
+        if not peered:
+            host_sum()
+        for r in range(world):
+            _lib.check(lib.itsk_loop_begin_finish(ctypes.byref(ps[r]), s))
+        for _ in range(cfg.max_iters):
+            for r in range(world):
+                _lib.check(lib.itsk_loop_step_pre(ctypes.byref(ps[r]), s))
+            if not peered:
+                host_sum()
+            for r in range(world):
+                _lib.check(lib.itsk_loop_step_post(ctypes.byref(ps[r]), s))
+        outs = []
+        for (ws, at, lda, csr), pr in zip(ranks, ps):
+            res = _read_result(lib, ws, pr, so)
+            outs.append(_assemble(ws, res, None, cfg, at, ws.b))
+        return outs
+
+    ref = solve(False)
+    got = solve(True)
+    for r in range(world):
+        assert np.array_equal(ref[r].solution, ref[0].solution)
+        _same_solve(got[r], ref[r])
+        assert got[r].trace.residual_changes == ref[r].trace.residual_changes
 
 
 def test_sharded_sparse_solve_matches_single_gpu(nccl_group):
