@@ -357,7 +357,7 @@ def run_b200(args):
 
     def solve(a_in, b_in):
         if dist_on:
-            return iterative_sketching_sharded(a_in, b_in, cfg, m, r0, residuals="last")
+            return iterative_sketching_sharded(a_in, b_in, cfg, m, r0, residuals="all")
         # the reference keeps every residual (solvers.py:245-246); that also lets
         # normest / condest run beside the first iterations (deferred estimates)
         return itsk.iterative_sketching(a_in, b_in, cfg, residuals="all")

@@ -202,9 +202,12 @@ def _shard_prepare(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
     return ws, at, lda, csr
 
 
-def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange | None = None):
+def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange | None = None,
+                  defer: bool = False):
     """Replicated part after the summed sketch: QR, x0, normest, condest and
-    the loop parameters (with the peer exchange when given)."""
+    the loop parameters (with the peer exchange when given).  defer: the
+    estimates run beside the loop (itsk_loop_params.est_ready); the caller
+    joins ws.est_stream and calls itsk_loop_finish after the loop."""
     lib = _dev.lib(ws.dev)
     n = ws.n
     stream = _dev.stream_ptr()
@@ -217,12 +220,29 @@ def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange
         _lib.check(lib.itsk_trsv_rp(_dev.ptr(ws.R), _dev.ptr(ws.Rp), n, _dev.ptr(ws.z), _dev.ptr(ws.xs[0]), 0,
                                     stream))
     ws.v0.copy_(torch.from_numpy(start_vector(n, cfg.rng_seed)))
-    _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), _dev.ptr(ws.est),
-                                _dev.ptr(ws.Rp), stream))
-    _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), _dev.ptr(ws.est) + 8, _dev.ptr(ws.Rp),
-                                stream))
+    est = _dev.ptr(ws.est)
+    if defer:
+        # normest / condest beside the loop's first iterations, as on one GPU
+        # (solvers._sketch_qr_x0): the ready flag is raised after both
+        compute = torch.cuda.current_stream(ws.dev)
+        if ws.est_stream is None:
+            ws.est_stream = torch.cuda.Stream(ws.dev)
+            ws.est_stream2 = torch.cuda.Stream(ws.dev)
+        _lib.check(lib.itsk_flag_store(est + 16, 0, stream))
+        ws.est_stream.wait_stream(compute)
+        ws.est_stream2.wait_stream(compute)
+        _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est + 8, _dev.ptr(ws.Rp),
+                                    int(ws.est_stream.cuda_stream)))
+        _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est, _dev.ptr(ws.Rp),
+                                    int(ws.est_stream2.cuda_stream)))
+        ws.est_stream.wait_stream(ws.est_stream2)
+        _lib.check(lib.itsk_flag_store(est + 16, 1, int(ws.est_stream.cuda_stream)))
+    else:
+        _lib.check(lib.itsk_normest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), normest_steps(n), est, _dev.ptr(ws.Rp),
+                                    stream))
+        _lib.check(lib.itsk_condest(_dev.ptr(ws.R), n, _dev.ptr(ws.v0), est + 8, _dev.ptr(ws.Rp), stream))
     alpha, beta = update_coeffs(cfg, n)
-    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=ws.m, csr=csr)
+    p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=ws.m, csr=csr, defer=defer)
     if peer is not None:
         ws.peer_params = peer.params(cfg.max_iters)  # kept alive with the workspace
         p.peer = ctypes.addressof(ws.peer_params)
@@ -258,7 +278,8 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
 
     allreduce(ws.W)
     px = peer_exchange(n, ws.dev, group) if (peer == "auto" and csr is None) else None
-    p = _shard_factor(ws, at, lda, csr, cfg, truth, px)
+    defer = ws.r_slots == cfg.max_iters + 1 and cfg.max_iters > 0
+    p = _shard_factor(ws, at, lda, csr, cfg, truth, px, defer=defer)
     if px is not None:
         from .solvers import run_loop
 
@@ -281,6 +302,9 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
             lambda: allreduce(cs),
             lambda: _lib.check(lib.itsk_loop_step_post(ctypes.byref(p), stream)),
             is_done, cfg.max_iters, check_every)
+    if defer:
+        stream_obj.wait_stream(ws.est_stream)
+        _lib.check(lib.itsk_loop_finish(ctypes.byref(p), stream))
     res = _read_result(lib, ws, p, stream_obj)
     out = _assemble(ws, res, truth, cfg, at, ws.b)
     out._workspace = ws  # keep the local residual rows alive

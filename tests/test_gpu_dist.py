@@ -48,8 +48,9 @@ def test_sharded_solve_matches_single_gpu(nccl_group, m, n, kappa, beta, d, vari
     cfg = itsk.SolverConfig(d=d, variant=variant, rng_seed=3)
     ref = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals="last")
     for rep in range(2):  # the second solve reuses the exchange buffers (next epochs)
+        # rep 1 keeps every residual: the estimates then run beside the loop
         got = iterative_sketching_sharded(p.a, p.b, itsk.SolverConfig(d=d, variant=variant, rng_seed=3), m, 0,
-                                          p.truth, peer=peer)
+                                          p.truth, peer=peer, residuals="last" if rep == 0 else "all")
         if peer == "auto":
             assert got.peer_exchange, "symmetric memory unavailable: peer exchange not exercised"
         _same_solve(got, ref)
