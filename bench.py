@@ -317,7 +317,9 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist_on = world > 1
+    # --sharded: the row-sharded path even at N = 1 (checks the N > 1 code
+    # path on one GPU; needs the torchrun environment)
+    dist_on = world > 1 or args.sharded
     if dist_on:
         import torch.distributed as tdist
 
@@ -396,7 +398,9 @@ def run_b200(args):
         t_e2e, res_e2e = timed(a_pin.numpy(), b_pin.numpy(), args.steps)
     iters = res.iterations
     # graph-body kernels (fused pass, tail) run once per iteration
-    launches = (l1 - l0) + args.steps * 2 * iters if not dist_on else (l1 - l0)
+    # (the sharded loop is one graph too when the peer exchange carries its sums)
+    graph_loop = (not dist_on) or bool(getattr(res, "peer_exchange", False))
+    launches = (l1 - l0) + args.steps * 2 * iters if graph_loop else (l1 - l0)
 
     def reduce_max(v):
         if not dist_on:
@@ -430,6 +434,9 @@ def run_b200(args):
             "config": {"workload": f"{args.config}: iterative_sketching m={m} n={n} d={d} zeta={zeta} "
                                    f"variant={args.variant} max_iters={cfg.max_iters}",
                        "global_rows": m, "cols": n, "parallelism": f"row-shard x{world}",
+                       "loop_exchange": (None if not dist_on else
+                                         "peer memory (pass stores to every rank, tail sums; one CUDA graph)"
+                                         if graph_loop else "nccl allreduce per iteration"),
                        "generator": GEN[args.config],
                        "l2": f"A ({a_bytes / 2**20:.0f} MiB per GPU) > L2 (126 MB): every pass streams from HBM, "
                              "no flush needed"},
@@ -473,6 +480,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default=None, choices=["basic", "damped", "momentum"])
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded (multi-GPU) path even with one rank (under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.variant is None:

@@ -22,6 +22,7 @@ arithmetic are plain host logic, tested with gloo on CPU (tests/test_dist_gloo.p
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import math
 
@@ -157,6 +158,29 @@ def peer_exchange(n: int, dev, group=None) -> PeerExchange | None:
     return px
 
 
+_SWS: "collections.OrderedDict[tuple, ShardedWorkspace]" = collections.OrderedDict()
+
+
+def _sharded_workspace(dev, m_total, row0, m_loc, n, d, zeta, max_iters, r_slots,
+                       with_truth) -> ShardedWorkspace:
+    """Per-rank workspaces (buffers, the instantiated loop graph, the peer
+    parameters) reused across solves of the same shape, as on one GPU."""
+    key = (dev.index, m_total, row0, m_loc, n, d, zeta, max_iters, r_slots, with_truth)
+    ws = _SWS.get(key)
+    if ws is None:
+        ws = ShardedWorkspace(dev, m_total, m_loc, n, d, zeta, max_iters, r_slots, with_truth)
+        _SWS[key] = ws
+        while len(_SWS) > 2:
+            _SWS.popitem(last=False)[1].release()
+    else:
+        _SWS.move_to_end(key)
+        lr = ws.last_residuals() if ws.last_residuals is not None else None
+        if lr is not None:
+            lr._detach()  # an earlier result still refers to the residual rows
+        ws.last_residuals = None
+    return ws
+
+
 def _shard_prepare(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int, truth, residuals: str):
     """Per-rank setup up to the partial sketch: workspace, local A / b /
     r_true, the full pattern from the shared seed, the CSR of this rank's
@@ -170,7 +194,8 @@ def _shard_prepare(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
     dev = _dev.current_device()
     lib = _dev.lib(dev)
     r_slots = cfg.max_iters + 1 if residuals == "all" else 2
-    ws = ShardedWorkspace(dev, m_total, m_loc, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots, truth is not None)
+    ws = _sharded_workspace(dev, m_total, row0, m_loc, n, cfg.d, cfg.zeta, cfg.max_iters, r_slots,
+                            truth is not None)
     csr = None
     if is_sparse(a_local):  # a row block of a sparse A (solvers.py:195-196)
         csr = as_csr_matrix(a_local, dev)
@@ -244,7 +269,13 @@ def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange
     alpha, beta = update_coeffs(cfg, n)
     p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, m_local=ws.m, csr=csr, defer=defer)
     if peer is not None:
-        ws.peer_params = peer.params(cfg.max_iters)  # kept alive with the workspace
+        # one PeerParams per workspace, updated in place: its address is part
+        # of the cached graph's key, the epoch base is read on the device
+        pp = peer.params(cfg.max_iters)
+        if getattr(ws, "peer_params", None) is None:
+            ws.peer_params = pp
+        else:
+            ctypes.memmove(ctypes.addressof(ws.peer_params), ctypes.addressof(pp), ctypes.sizeof(pp))
         p.peer = ctypes.addressof(ws.peer_params)
     return p
 
