@@ -52,6 +52,24 @@ __device__ u128 pcg_advance(u128 s, u128 inc, uint64_t delta) {
   return acc_mult * s + acc_plus;
 }
 
+// The affine map of `delta` LCG steps: state -> mult * state + plus.
+struct Jump {
+  u128 mult, plus;
+};
+__device__ Jump pcg_jump(u128 inc, uint64_t delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return Jump{acc_mult, acc_plus};
+}
+
 struct Stream {
   uint64_t s_hi, s_lo, i_hi, i_lo;
   uint32_t pending;
@@ -78,6 +96,18 @@ struct WordCursor {
     half = 0;
     buf = 0;
     if (!use_pending && (k & 1)) {
+      s = s * pcg_mult() + inc;
+      buf = pcg_output(s);
+      half = 1;
+    }
+  }
+  // From the state before output k >> 1 (k = the word index, has_uint32
+  // already accounted for): no jump-ahead here.
+  __device__ WordCursor(u128 s_before, u128 inc_, uint64_t k) : inc(inc_), pending(0), use_pending(0) {
+    s = s_before;
+    half = 0;
+    buf = 0;
+    if (k & 1) {
       s = s * pcg_mult() + inc;
       buf = pcg_output(s);
       half = 1;
@@ -245,14 +275,38 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tot) {
 // Draws `count` Lemire values from word position `pos` on; draw q goes to
 // rows[q0 + q] (cols == nullptr) or to column cols[q / zeta], slot q % zeta.
 // Returns (every thread) the position after the last accepted word.
-__device__ uint64_t draw_seq(const Stream& st, uint64_t pos, uint64_t count, uint32_t bound, uint32_t thr,
-                             uint32_t* rows, uint64_t q0, const uint32_t* cols, int64_t zeta) {
+// Per-thread jump-ahead, set up once per kernel: a thread's words of a tile
+// start RD_W * tid words (2 * tid outputs, RD_W even) after the tile's, and
+// consecutive tiles are RD_T * RD_W words apart — so only the first tile of
+// each call needs a (one-thread) jump from the stream origin, every other
+// cursor is one affine step from a shared base state (the full per-thread
+// 128-bit jump-ahead per tile was most of this kernel's time).
+struct RedrawJumps {
+  Jump mine;  // 2 * tid outputs
+  Jump tile;  // RD_T * RD_W / 2 outputs
+};
+
+__device__ uint64_t draw_seq(const Stream& st, const RedrawJumps& jp, uint64_t pos, uint64_t count,
+                             uint32_t bound, uint32_t thr, uint32_t* rows, uint64_t q0, const uint32_t* cols,
+                             int64_t zeta) {
+  static_assert(RD_W % 2 == 0, "thread word offsets must keep the tile's word parity");
   __shared__ uint32_t s_tot;
   __shared__ uint64_t s_end;
+  __shared__ uint64_t s_base[2];
+  const u128 inc = mk128(st.i_hi, st.i_lo);
+  // word index k of `pos` (numpy's buffered half-word consumed first when has)
+  const uint64_t k0 = st.has ? pos - 1 : pos;  // pos > 0 in every call
+  if (threadIdx.x == 0) {
+    const u128 b = pcg_advance(mk128(st.s_hi, st.s_lo), inc, k0 >> 1);  // state before output k0 >> 1
+    s_base[0] = static_cast<uint64_t>(b >> 64);
+    s_base[1] = static_cast<uint64_t>(b);
+  }
+  __syncthreads();
+  u128 base_state = mk128(s_base[0], s_base[1]);
   uint64_t done = 0;
   while (done < count) {
     const uint64_t base = pos + static_cast<uint64_t>(threadIdx.x) * RD_W;
-    WordCursor cur(st, base);
+    WordCursor cur(jp.mine.mult * base_state + jp.mine.plus, inc, (st.has ? base - 1 : base));
     uint32_t v[RD_W];
     unsigned acc = 0, cnt = 0;
 #pragma unroll
@@ -282,6 +336,7 @@ __device__ uint64_t draw_seq(const Stream& st, uint64_t pos, uint64_t count, uin
     } else {
       pos += static_cast<uint64_t>(RD_T) * RD_W;
       done += tot;
+      base_state = jp.tile.mult * base_state + jp.tile.plus;
     }
     __syncthreads();
   }
@@ -327,20 +382,24 @@ __global__ void __launch_bounds__(RD_T, 1) k_redraw(Stream st, uint32_t bound, u
                                                     uint64_t nwords1, uint64_t* slots, const uint64_t* pos_in,
                                                     uint32_t* bad_a, uint32_t* bad_b, const uint32_t* nbad1,
                                                     int first) {
+  const u128 inc = mk128(st.i_hi, st.i_lo);
+  RedrawJumps jp;
+  jp.mine = pcg_jump(inc, static_cast<uint64_t>(threadIdx.x) * (RD_W / 2));
+  jp.tile = pcg_jump(inc, static_cast<uint64_t>(RD_T) * RD_W / 2);
   const uint64_t total1 = first ? scanned1[nchunks1] : N;
   uint64_t pos;
   uint32_t nbad;
   uint32_t* cur = bad_a;
   uint32_t* nxt = bad_b;
   if (total1 < N) {
-    pos = draw_seq(st, slots[0] + nwords1, N - total1, bound, thr, rows, total1, nullptr, zeta);
+    pos = draw_seq(st, jp, slots[0] + nwords1, N - total1, bound, thr, rows, total1, nullptr, zeta);
     nbad = flag_compact(rows, zeta, nullptr, static_cast<uint32_t>(m), cur);
   } else {
     pos = *pos_in;
     nbad = *nbad1;
   }
   while (nbad > 0) {
-    pos = draw_seq(st, pos, static_cast<uint64_t>(nbad) * zeta, bound, thr, rows, 0, cur, zeta);
+    pos = draw_seq(st, jp, pos, static_cast<uint64_t>(nbad) * zeta, bound, thr, rows, 0, cur, zeta);
     nbad = flag_compact(rows, zeta, cur, nbad, nxt);
     uint32_t* t = cur;
     cur = nxt;

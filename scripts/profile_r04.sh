@@ -15,3 +15,9 @@ python scripts/micro_pass.py 200000 200 3 > $OUT/r04_pass_plain.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_pass_tma -s 3 -c 1 \
     -o $OUT/r04_pass_full python scripts/micro_pass.py 200000 200 2 > $OUT/r04_pass_ncu.log 2>&1
 echo done
+# round-4 additions: other configs, the loop's critical path, the sharded path at one rank
+python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/r04_prof_bench_c3.json 2>/dev/null
+python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > $OUT/r04_prof_bench_c4.json 2>/dev/null
+python scripts/loop_timeline.py c2 > $OUT/r04_prof_timeline_c2.txt 2>&1
+python scripts/phases.py c4 momentum > $OUT/r04_prof_phases_c4.txt 2>&1
+echo done2
