@@ -184,6 +184,43 @@ __global__ void k_lemire_emit(Stream st, const uint64_t* w0p, uint64_t nwords, u
   }
 }
 
+// The first draw (dst[q] = draw q): a warp's 32 chunks emit one contiguous
+// range of draws, so they are staged in shared memory and written out
+// coalesced (each lane's own draws are 64 consecutive words, strided 64
+// apart across the warp, when stored directly).
+constexpr int EM_WARPS = 4;
+__global__ void __launch_bounds__(32 * EM_WARPS) k_lemire_emit_first(
+    Stream st, const uint64_t* w0p, uint64_t nwords, uint32_t bound, uint32_t thr, const uint32_t* scanned,
+    uint64_t nchunks, uint64_t N, uint32_t* dst, uint64_t* end_word) {
+  __shared__ uint32_t stage[EM_WARPS][32 * CH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t w0 = *w0p;
+  const uint64_t cw0 = c - lane;  // first chunk of the warp
+  if (cw0 >= nchunks) return;     // warp-uniform
+  const uint64_t cw1 = min(cw0 + 32, nchunks);
+  const uint64_t qw0 = scanned[cw0];
+  const uint64_t qw1 = min(static_cast<uint64_t>(scanned[cw1]), N);  // scanned[nchunks] = total
+  uint32_t* sg = stage[warp];
+  if (c < nchunks) {
+    uint64_t q = scanned[c];
+    if (q < N) {
+      const uint64_t beg = c * CH;
+      const uint64_t len = min(static_cast<uint64_t>(CH), nwords - beg);
+      WordCursor cur(st, w0 + beg);
+      for (uint64_t i = 0; i < len && q < N; ++i) {
+        uint32_t v;
+        if (!lemire_accept(cur.next(), bound, thr, &v)) continue;
+        sg[q - qw0] = v;
+        if (q == N - 1) *end_word = w0 + beg + i + 1;
+        ++q;
+      }
+    }
+  }
+  __syncwarp();
+  for (uint64_t q = qw0 + lane; q < qw1; q += 32) dst[q] = sg[q - qw0];
+}
+
 // choice([-1., 1.]) → integers(0, 2): neg = (w >> 31) == 0, one word each.
 __global__ void k_signs(Stream st, const uint64_t* w0p, uint64_t N, uint8_t* neg) {
   const uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -192,6 +229,25 @@ __global__ void k_signs(Stream st, const uint64_t* w0p, uint64_t N, uint8_t* neg
   if (beg >= N) return;
   const uint64_t len = min(static_cast<uint64_t>(CH), N - beg);
   WordCursor cur(st, w0 + beg);
+  if (len == CH && (reinterpret_cast<uintptr_t>(neg) & 15) == 0) {
+    // a full chunk: the 64 sign bytes packed in registers, four 16-byte stores
+    // (byte stores strided 64 bytes across the warp were most of the time)
+    static_assert(CH == 64, "k_signs packs 64 bytes");
+    uint64_t pk[8];
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) {
+      uint64_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v |= static_cast<uint64_t>((cur.next() >> 31) == 0 ? 1 : 0) << (8 * b);
+      pk[w8] = v;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(neg + beg);  // beg % 64 == 0; neg is 16-byte aligned
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      dst[q] = make_uint4(static_cast<uint32_t>(pk[2 * q]), static_cast<uint32_t>(pk[2 * q] >> 32),
+                          static_cast<uint32_t>(pk[2 * q + 1]), static_cast<uint32_t>(pk[2 * q + 1] >> 32));
+    return;
+  }
   for (uint64_t i = 0; i < len; ++i) neg[beg + i] = (cur.next() >> 31) == 0 ? 1 : 0;
 }
 
@@ -551,9 +607,8 @@ extern "C" int itsk_sparse_sign_pattern(int64_t d, int64_t m, int64_t zeta, cons
     size_t tb = w.cub_bytes;
     ITSK_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.counts, w.scanned, static_cast<int>(nchunks + 1), s));
     count_launch();
-    k_lemire_emit<<<blocks_for(nchunks, 256), 256, 0, s>>>(st, slots, nwords, bound, thr, w.scanned, nchunks,
-                                                             static_cast<uint64_t>(nnz), rows, nullptr, zeta,
-                                                             slots + 1);
+    k_lemire_emit_first<<<blocks_for(nchunks, 32 * EM_WARPS), 32 * EM_WARPS, 0, s>>>(
+        st, slots, nwords, bound, thr, w.scanned, nchunks, static_cast<uint64_t>(nnz), rows, slots + 1);
     count_launch();
     // duplicate scan of every column, compacted in column order (embed.py:38-40)
     k_flag_dupes<<<blocks_for(m, 256), 256, 0, s>>>(rows, zeta, nullptr, m, w.flags);
