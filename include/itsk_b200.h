@@ -271,7 +271,12 @@ typedef struct itsk_loop_params {
   /* Peer-memory exchange (nullable): with it the sharded loop needs no host
    * collective — itsk_loop_begin / the loop graph run it end to end. */
   const itsk_peer_params* peer;
+  /* ITSK_LOOP_TAIL_SUMS: the pass leaves the last level of its [c | norms]
+   * reduction to the tail kernel (cs is complete only after the tail: not
+   * with a host collective between step_pre and step_post). */
+  uint32_t opts;
 } itsk_loop_params;
+#define ITSK_LOOP_TAIL_SUMS 1u
 
 typedef struct itsk_loop_result { /* read back with one D2H copy */
   int32_t iterations;  /* len(iterates) - 1                       */
@@ -307,6 +312,9 @@ void itsk_loop_graph_destroy(void* handle);
 int itsk_loop_finish(const itsk_loop_params* p, itsk_stream_t stream);
 /* *flag = value with release semantics (the estimates' ready flag). */
 int itsk_flag_store(uint64_t* flag, uint64_t value, itsk_stream_t stream);
+/* sizeof(itsk_loop_params) (0), sizeof(itsk_loop_result) (1),
+ * sizeof(itsk_peer_params) (2) as compiled into the library; -1 otherwise. */
+int64_t itsk_struct_size(int which);
 /* Device pointer of the itsk_loop_result inside the loop workspace. */
 int itsk_loop_result_ptr(const itsk_loop_params* p, itsk_loop_result** out);
 

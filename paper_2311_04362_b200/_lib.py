@@ -47,6 +47,7 @@ class LoopParams(ctypes.Structure):
         ("csr", c_dp),
         ("est_ready", c_dp),
         ("peer", c_dp),
+        ("opts", ctypes.c_uint32),
     ]
 
 
@@ -118,12 +119,14 @@ _SIGS = {
     "itsk_loop_graph_create": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp, ctypes.POINTER(c_dp)]),
     "itsk_loop_graph_launch": (ctypes.c_int, [c_dp, c_dp]),
     "itsk_loop_graph_destroy": (None, [c_dp]),
-"itsk_loop_finish": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
+    "itsk_struct_size": (c_i64, [ctypes.c_int]),
+    "itsk_loop_finish": (ctypes.c_int, [ctypes.POINTER(LoopParams), c_dp]),
     "itsk_flag_store": (ctypes.c_int, [c_dp, ctypes.c_uint64, c_dp]),
     "itsk_loop_result_ptr": (ctypes.c_int, [ctypes.POINTER(LoopParams), ctypes.POINTER(c_dp)]),
 }
 
 PASS_WS_READY = 1  # include/itsk_b200.h ITSK_PASS_WS_READY
+LOOP_TAIL_SUMS = 1  # include/itsk_b200.h ITSK_LOOP_TAIL_SUMS
 
 _lock = threading.Lock()
 _lib = None

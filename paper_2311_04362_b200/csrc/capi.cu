@@ -89,3 +89,14 @@ extern "C" int itsk_device_check(int dev) {
   }
   return ITSK_OK;
 }
+
+// ABI check for bindings: sizes of the parameter structs as compiled here
+// (tests/test_capi.py compares them with the ctypes mirrors).
+extern "C" int64_t itsk_struct_size(int which) {
+  switch (which) {
+    case 0: return static_cast<int64_t>(sizeof(itsk_loop_params));
+    case 1: return static_cast<int64_t>(sizeof(itsk_loop_result));
+    case 2: return static_cast<int64_t>(sizeof(itsk_peer_params));
+    default: return -1;
+  }
+}

@@ -44,6 +44,8 @@ struct LoopPtrs {
   const double* condest;
   const uint64_t* est_ready;  // nullptr: the estimates are ready
   PeerArgs peer;
+  const double* gpart;  // tail_sums: the pass's group partials (ng x (n+4)), summed by the tail
+  int ng;               // 0: the pass reduced into cs itself
   double* xs;
   double* rs;
   double* trace;
@@ -87,11 +89,13 @@ struct PassArgs {
   int group;
   double bscale = 1.0;  // r = bscale * b - A x (LSQR: u_{k+1} beta = A y - alpha u_k)
   int sm_reserve = 0;   // SMs left free for kernels running beside the pass (the loop's estimates and tail)
+  int tail_sums = 0;    // loop: stop after the group level; the tail sums the groups (ITSK_LOOP_TAIL_SUMS)
   PeerArgs peer;        // loop mode: send the reduced partial to every rank
 };
 
 // counters / group partials needed by the in-kernel reduction of a pass
 int pass_groups(int64_t m, int64_t n, int* group);
+int pass_tail_groups(const double* A, int64_t m, int64_t n, int64_t lda, int reserve);
 
 int pass_grid(int64_t m, int64_t n);
 int64_t pass_part_doubles(int64_t m, int64_t n);

@@ -302,6 +302,34 @@ __device__ void peer_gather(const LoopPtrs& p, int64_t epoch_base, int64_t it_ep
   __syncthreads();
 }
 
+// ITSK_LOOP_TAIL_SUMS: the last level of the pass's reduction, moved here
+// (the pass's grid has completed): even groups into s0, odd groups into s1,
+// then s0 + s1 — group_reduce's order, so cs has the same bits.
+__device__ void tail_group_sum(const LoopPtrs& p) {
+  const int64_t w = p.n + 4;
+  const int ne = (p.ng + 1) / 2, no = p.ng / 2;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    double v[16];
+    double s0 = 0.0, s1 = 0.0;
+    for (int g0 = 0; g0 < ne; g0 += 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = g0 + k < ne ? __ldcg(p.gpart + (2 * (g0 + k)) * w + c) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (g0 + k < ne) s0 += v[k];
+    }
+    for (int g0 = 0; g0 < no; g0 += 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = g0 + k < no ? __ldcg(p.gpart + (2 * (g0 + k) + 1) * w + c) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (g0 + k < no) s1 += v[k];
+    }
+    p.cs[c] = s0 + s1;
+  }
+  __syncthreads();
+}
+
 enum : int { TAIL_CONTROL = 2, TAIL_STEP = 4, TAIL_BEGIN = 8 };
 
 // The serial tail of an iteration on one CTA (see the file comment).
@@ -353,6 +381,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
     reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
   __syncthreads();
   LoopCtl* ctl = &s_ctl;
+  if (p.ng > 0 && !ctl->result.done) tail_group_sum(p);
   if (p.peer.size > 0 && !ctl->result.done)
     peer_gather(p, ctl->epoch_base, (flags & TAIL_BEGIN) ? 0 : ctl->it + 1);
   // c for the solves, staged now: its loads overlap the control step
@@ -469,6 +498,8 @@ int check_params(const itsk_loop_params* p) {
   return ITSK_OK;
 }
 
+int loop_sm_reserve();
+
 PeerArgs peer_args(const itsk_loop_params* p) {
   PeerArgs g;
   if (!p->peer) return g;
@@ -495,6 +526,14 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
   q.condest = p->condest;
   q.est_ready = p->est_ready;
   q.peer = peer_args(p);
+  {
+    const LoopLayout L = loop_layout(p->ws, p->m, p->n);
+    const int ng = ((p->opts & ITSK_LOOP_TAIL_SUMS) && !p->peer && !p->csr)
+                       ? pass_tail_groups(p->A, p->m, p->n, p->lda, loop_sm_reserve())
+                       : 0;
+    q.gpart = ng > 0 ? L.gpart : nullptr;
+    q.ng = ng;
+  }
   q.xs = p->xs;
   q.rs = p->rs;
   q.trace = p->trace;
@@ -541,6 +580,7 @@ PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   a.group = L.group;
   a.sm_reserve = loop_sm_reserve();
   a.peer = q.peer;
+  a.tail_sums = q.ng > 0 ? 1 : 0;
   return a;
 }
 

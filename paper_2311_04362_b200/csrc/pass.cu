@@ -210,6 +210,7 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   if (threadIdx.x == 0) a.tickets[gi] = 0;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x)
     a.gpart[static_cast<int64_t>(gi) * w + c] = sum_strided(a.part + static_cast<int64_t>(gi) * G * w + c, w, gsz, 0.0);
+  if (a.tail_sums) return;  // the loop's tail sums the groups (tail_group_sum, same order)
   __syncthreads();
   if (threadIdx.x == 0) s_last = ticket_acq_rel(&a.tickets[ng]) == static_cast<unsigned>(ng - 1);
   __syncthreads();
@@ -941,6 +942,21 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
     ITSK_CHECK_LAUNCH();
   }
   return rc;
+}
+
+// Groups of the in-kernel reduction of a loop pass (grid with `reserve` SMs
+// left free), or 0 when the pass reduces through k_finalize instead (rows
+// not 16-byte aligned, n > 2048): ITSK_LOOP_TAIL_SUMS needs the former.
+int pass_tail_groups(const double* A, int64_t m, int64_t n, int64_t lda, int reserve) {
+  PassArgs a{};
+  a.A = A;
+  a.n = n;
+  a.lda = lda;
+  if (!tma_eligible(a)) return 0;
+  const int grid = tma_grid(m, reserve);
+  int G = 0;
+  pass_groups(m, n, &G);
+  return (grid + G - 1) / G;
 }
 
 int pass_groups(int64_t m, int64_t n, int* group) {

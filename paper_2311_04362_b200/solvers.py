@@ -437,6 +437,9 @@ def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth,
     p.ws = _dev.ptr(ws.loop_ws)
     p.ws_bytes = ws.loop_ws.numel()
     p.est_ready = _dev.ptr(ws.est) + 16 if defer else None
+    # the pass's last reduction level in the tail: only without a host
+    # collective between the two halves of an iteration (not the NCCL path)
+    p.opts = _lib.LOOP_TAIL_SUMS if m_local is None else 0
     return p
 
 

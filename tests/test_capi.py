@@ -82,3 +82,18 @@ def test_workspace_queries_without_device():
     assert lib.itsk_qr_workspace(4000, 200, ctypes.byref(b)) == 0 and b.value > 0
     assert lib.itsk_pattern_workspace(3, 10, 4, ctypes.byref(b)) == _lib.ITSK_EINVAL
     assert b"zeta" in lib.itsk_last_error() or lib.itsk_last_error()
+
+
+def test_ctypes_structs_match_the_compiled_abi():
+    """The ctypes mirrors of the parameter structs have the sizes the library
+    was compiled with (a field added on one side only would shift every
+    later field)."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.itsk_struct_size(0) == ctypes.sizeof(_lib.LoopParams)
+    assert lib.itsk_struct_size(1) == ctypes.sizeof(_lib.LoopResult)
+    assert lib.itsk_struct_size(2) == ctypes.sizeof(_lib.PeerParams)
+    assert lib.itsk_struct_size(7) == -1
