@@ -78,11 +78,14 @@ __device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t m
                "l"(__double_as_longlong(v)), "r"(mbar)
                : "memory");
 }
+// The records land in this CTA's own shared memory (st.async with
+// complete_tx on this CTA's mbarrier), so a CTA-scope acquire suffices; a
+// cluster-scope acquire also invalidates L1 (CCTL.IVALL) at every column.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");

@@ -4,7 +4,7 @@
     -o ../../scripts/bw/libqrnext.so capi.cu qr.cu qr2.cu qr_tsqr.cu trsv.cu pass.cu loop.cu pattern.cu sketch.cu sparse.cu \\
     -lcudart_static -lrt -ldl -lpthread"""
 import ctypes, sys, os, torch
-lib = ctypes.CDLL(os.path.abspath("scripts/bw/libqrnext.so"))
+lib = ctypes.CDLL(os.path.abspath(sys.argv[3] if len(sys.argv) > 3 else "scripts/bw/libqrnext.so"))
 d, n = int(sys.argv[1]), int(sys.argv[2])
 W0 = torch.randn(d, n + 1, dtype=torch.float64, device="cuda"); W = W0.clone()
 R = torch.empty(n, n, dtype=torch.float64, device="cuda"); z = torch.empty(n, dtype=torch.float64, device="cuda")
