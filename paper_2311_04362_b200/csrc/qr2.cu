@@ -659,15 +659,23 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next(UpdArgs a, int64_t hm
   // j carries t_j = y_j - sum_{k<i} G_kj z_k; step i: z_i = tau_i t_i (lane
   // i), broadcast, lanes j > i subtract G_ij z_i.
   // two columns per warp, their chains interleaved
+  // lane j's column of G and its tau in registers: the chain is shuffle +
+  // FMA only (the same products: lane i forms tau_i t_i)
+  double gcol[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) gcol[i] = Gs[i * VS + (lane < NB ? lane : 0)];
+  const double mytau = ts[lane < NB ? lane : 0];
   for (int c = warp; c < nb2; c += 2 * QP_WARPS) {
     const int c2 = c + QP_WARPS;
     const bool two = c2 < nb2;
     double t = lane < a.kb ? Ys[lane * BS + c] : 0.0;
     double u = (two && lane < a.kb) ? Ys[lane * BS + c2] : 0.0;
-    for (int i = 0; i < a.kb; ++i) {
-      const double g = Gs[i * VS + (lane < NB ? lane : 0)];
-      const double zi = __shfl_sync(FULL, ts[i] * t, i);
-      const double wi = __shfl_sync(FULL, ts[i] * u, i);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (i >= a.kb) break;
+      const double g = gcol[i];
+      const double zi = __shfl_sync(FULL, mytau * t, i);
+      const double wi = __shfl_sync(FULL, mytau * u, i);
       if (lane == i) {
         t = zi;
         u = wi;

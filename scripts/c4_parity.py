@@ -14,6 +14,7 @@ from oracle import itsketch_oracle as orc
 
 variant = sys.argv[1] if len(sys.argv) > 1 else "momentum"
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+residuals = sys.argv[3] if len(sys.argv) > 3 else "all"  # "all": estimates deferred beside the loop
 m, n, kappa, beta, d = 4_000_000, 2000, 1e8, 1e-6, 24000
 U = 2.0 ** -53
 t0 = time.time()
@@ -21,13 +22,13 @@ p = gen_randsvd_device(m, n, kappa, beta, seed)
 torch.cuda.synchronize()
 t_gen = time.time() - t0
 cfg = itsk.SolverConfig(d=d, variant=variant, rng_seed=seed)
-res = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals="last")
+res = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals=residuals)
 torch.cuda.synchronize()
 t0 = time.time()
-res = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals="last")
+res = itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals=residuals)
 torch.cuda.synchronize()
 t_gpu = time.time() - t0
-out = {"config": "c4", "m": m, "n": n, "kappa": kappa, "beta": beta, "d": d, "zeta": 8, "variant": variant,
+out = {"config": "c4", "residuals": residuals, "m": m, "n": n, "kappa": kappa, "beta": beta, "d": d, "zeta": 8, "variant": variant,
        "seed": seed, "generate_s": t_gen, "gpu_solve_wall_s": t_gpu,
        "gpu": {"iterations": res.iterations, "stop": res.trace.stop_reason, "fe": res.trace.fe[-1],
                "re": res.trace.re[-1], "normest": res.trace.normest, "condest": res.trace.condest}}
