@@ -212,10 +212,14 @@ class _Workspace:
         self.Rp = torch.empty(nb.value, **f64)
         self.z = torch.empty(n, **f64)
         self.v0 = torch.empty(n, **f64)
-        self.est = torch.zeros(3, **f64)  # normest, condest, ready flag (deferred estimates)
-        self.xs = torch.empty((max_iters + 1, n), **f64)
+        # iterates, trace and estimates are views of one buffer: the result is
+        # read back with one device-to-host copy
+        K = max_iters + 1
+        self.out = torch.zeros(K * n + 4 * K + 4, **f64)
+        self.xs = self.out[:K * n].view(K, n)
+        self.trace = self.out[K * n:K * n + 4 * K].view(4, K)
+        self.est = self.out[K * n + 4 * K:K * n + 4 * K + 3]  # normest, condest, ready flag (deferred estimates)
         self.rs = torch.empty((r_slots, m), **f64)
-        self.trace = torch.empty((4, max_iters + 1), **f64)
         self.cs = torch.zeros(n + 8, **f64)
         _lib.check(lib.itsk_loop_workspace(m, n, ctypes.byref(nb)))
         self.loop_ws = _dev.workspace(nb.value, dev)
@@ -455,11 +459,7 @@ def _read_result(lib, ws: _Workspace, p, stream_obj) -> _lib.LoopResult:
     raw = ws.loop_ws[off:off + ctypes.sizeof(_lib.LoopResult)]
     host = ws.res_host.view(torch.uint8)[:ctypes.sizeof(_lib.LoopResult)]
     host.copy_(raw, non_blocking=True)
-    nxs = (ws.max_iters + 1) * ws.n
-    hb = ws.host_buf
-    hb[:nxs].copy_(ws.xs.view(-1), non_blocking=True)
-    hb[nxs:nxs + ws.trace.numel()].copy_(ws.trace.view(-1), non_blocking=True)
-    hb[nxs + ws.trace.numel():nxs + ws.trace.numel() + 2].copy_(ws.est[:2], non_blocking=True)
+    ws.host_buf[:ws.out.numel()].copy_(ws.out, non_blocking=True)  # iterates, trace, estimates
     ws.sing_host.copy_(ws.sing, non_blocking=True)
     stream_obj.synchronize()
     check_singular(ws)
