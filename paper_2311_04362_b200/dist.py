@@ -174,10 +174,7 @@ def _sharded_workspace(dev, m_total, row0, m_loc, n, d, zeta, max_iters, r_slots
             _SWS.popitem(last=False)[1].release()
     else:
         _SWS.move_to_end(key)
-        lr = ws.last_residuals() if ws.last_residuals is not None else None
-        if lr is not None:
-            lr._detach()  # an earlier result still refers to the residual rows
-        ws.last_residuals = None
+    ws.claim_residual_rows()
     return ws
 
 

@@ -234,21 +234,48 @@ class _Workspace:
         self.sing_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.v0_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
         self.v0_seed = None
-        self.graph = None
-        self.graph_key = None
+        self.graphs: dict = {}  # loop params key -> instantiated loop graph
+        # residual rows: a second buffer is allocated the first time a solve
+        # starts while an earlier result still refers to the rows, so results
+        # kept by the caller are not copied out (two alive: the older is)
+        self.rs_pool = [self.rs]
+        self.rs_refs = [None]
         self.last_residuals = None
         self.host_buf = torch.empty(((max_iters + 1) * n + 4 * (max_iters + 1) + 8,),
                                     dtype=torch.float64, pin_memory=True)
         self.res_host = torch.empty(8, dtype=torch.float64, pin_memory=True)
+
+    def claim_residual_rows(self) -> None:
+        """Point self.rs at a residual buffer no live result refers to."""
+        cur = next(i for i, t in enumerate(self.rs_pool) if t is self.rs)
+        if self.last_residuals is not None:
+            self.rs_refs[cur] = self.last_residuals
+            self.last_residuals = None
+        for i, ref in enumerate(self.rs_refs):
+            if ref is None or ref() is None:
+                self.rs_refs[i] = None
+                self.rs = self.rs_pool[i]
+                return
+        if len(self.rs_pool) < 2:
+            self.rs_pool.append(torch.empty_like(self.rs_pool[0]))
+            self.rs_refs.append(None)
+            self.rs = self.rs_pool[-1]
+            return
+        old = 1 - cur  # both in use: copy out the rows of the older result
+        lr = self.rs_refs[old]()
+        if lr is not None:
+            lr._detach()
+        self.rs_refs[old] = None
+        self.rs = self.rs_pool[old]
 
     def embedding(self, scale) -> SparseSignEmbedding:
         return SparseSignEmbedding(d=self.d, m=self.m, zeta=self.zeta, scale=scale, rows_dev=self.rows,
                                    neg_dev=self.neg, ptr_dev=self.sk_ptr, src_dev=self.sk_src)
 
     def release(self):
-        if self.graph is not None:
-            _lib.load().itsk_loop_graph_destroy(self.graph)
-            self.graph = None
+        for h in self.graphs.values():
+            _lib.load().itsk_loop_graph_destroy(h)
+        self.graphs = {}
 
     def __del__(self):
         try:
@@ -272,11 +299,7 @@ def _workspace(dev, m, n, d, zeta, max_iters, r_slots, with_truth) -> _Workspace
         _WS[key] = ws
     else:
         _WS.move_to_end(key)
-    if ws.last_residuals is not None:
-        lr = ws.last_residuals()
-        if lr is not None:
-            lr._detach()
-        ws.last_residuals = None
+    ws.claim_residual_rows()
     return ws
 
 
@@ -472,14 +495,16 @@ def run_loop(lib, ws: _Workspace, p, use_graph: bool, stream: int) -> None:
         return
     if use_graph:
         key = _params_key(p)
-        if ws.graph is None or ws.graph_key != key:
-            if ws.graph is not None:
-                lib.itsk_loop_graph_destroy(ws.graph)
-                ws.graph = None
+        h = ws.graphs.get(key)
+        if h is None:
+            if len(ws.graphs) >= 4:
+                for g in ws.graphs.values():
+                    lib.itsk_loop_graph_destroy(g)
+                ws.graphs = {}
             h = ctypes.c_void_p()
             _lib.check(lib.itsk_loop_graph_create(ctypes.byref(p), stream, ctypes.byref(h)))
-            ws.graph, ws.graph_key = h, key
-        _lib.check(lib.itsk_loop_graph_launch(ws.graph, stream))
+            ws.graphs[key] = h
+        _lib.check(lib.itsk_loop_graph_launch(h, stream))
     else:
         for _ in range(p.max_iters):
             _lib.check(lib.itsk_loop_step_pre(ctypes.byref(p), stream))

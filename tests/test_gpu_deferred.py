@@ -126,3 +126,18 @@ def test_rule_replayed_short_max_iters(pkg):
             r_late = _solve_flag_held(pkg, p.a, p.b, cfg, None, True)
             _same(r_late, r_sync)
             assert r_sync.trace.stop_reason == ("stopped_by_rule" if mi >= k else "max_iters")
+
+
+def test_kept_results_keep_their_residual_rows(pkg):
+    """Results kept by the caller keep valid residual vectors while the
+    workspace is reused (a second buffer rotates in; with two results alive
+    the older one's rows are copied out)."""
+    p = pkg.gen_randsvd(20000, 40, 1e6, 1e-6, 7)
+    kept = []
+    for seed in (1, 2, 3, 4):
+        cfg = pkg.SolverConfig(d=800, rng_seed=seed)
+        kept.append(pkg.iterative_sketching(p.a, p.b, cfg, residuals="all"))
+    for r in kept:
+        for i in (0, len(r.trace.residual_vectors) - 1):
+            want = p.b - p.a @ r.trace.iterates[i]
+            np.testing.assert_allclose(r.trace.residual_vectors[i], want, rtol=0, atol=1e-12 * np.linalg.norm(p.b))
