@@ -580,7 +580,12 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
     bsrc = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(b, dtype=np.float64)))
     if bsrc.shape[0] != m:
         raise ValueError(f"b has {bsrc.shape[0]} entries, A has {m} rows")
-    ws.b.copy_(bsrc, non_blocking=True)
+    if (bsrc.is_cuda and bsrc.device == dev and bsrc.dtype == torch.float64 and bsrc.dim() == 1
+            and bsrc.is_contiguous()):
+        bt = bsrc  # read in place, like A (the solver never writes b)
+    else:
+        ws.b.copy_(bsrc, non_blocking=True)
+        bt = ws.b
     if truth is not None:
         ws.x_true.copy_(_dev.as_device_vector(truth.x, dev))
         if truth.beta > 0:
@@ -590,14 +595,15 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
     # estimates beside the loop (needs every residual kept: the stop may move
     # back to an iterate recorded before they were ready)
     defer = ws.r_slots == cfg.max_iters + 1 and cfg.max_iters > 0
-    _sketch_qr_x0(lib, ws, at, lda, ws.b, cfg, stream, csr, upload, defer=defer)
+    _sketch_qr_x0(lib, ws, at, lda, bt, cfg, stream, csr, upload, defer=defer)
     p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr, defer=defer)
+    p.b = _dev.ptr(bt)
     run_loop(lib, ws, p, use_graph, stream)
     if defer:
         stream_obj.wait_stream(ws.est_stream)
         _lib.check(lib.itsk_loop_finish(ctypes.byref(p), stream))
     res = _read_result(lib, ws, p, stream_obj)
-    return _assemble(ws, res, truth, cfg, at, ws.b)
+    return _assemble(ws, res, truth, cfg, at, bt)
 
 
 def sketch_and_solve(a, b, s: SparseSignEmbedding):
