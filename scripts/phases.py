@@ -52,6 +52,7 @@ out["condest_ws"] = T(lambda: _lib.check(lib.itsk_condest_ws(dv.ptr(ws.R), n, dv
 out["condest_Rp"] = T(lambda: _lib.check(lib.itsk_condest(dv.ptr(ws.R), n, dv.ptr(ws.v0), dv.ptr(ws.est)+8, dv.ptr(ws.Rp), s)))
 out["normest_Rp"] = T(lambda: _lib.check(lib.itsk_normest(dv.ptr(ws.R), n, dv.ptr(ws.v0), normest_steps(n), dv.ptr(ws.est), dv.ptr(ws.Rp), s)))
 p_ = solvers._loop_params(ws, at, n, cfg, 1.0, 0.0, None)
+p_.b = dv.ptr(bt)  # the solver reads a device b in place (ws.b is not filled)
 def loop():
     solvers.run_loop(lib, ws, p_, True, s)
 out["loop(graph)"] = T(loop)
