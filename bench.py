@@ -1,34 +1,50 @@
 """Benchmark: fp64 iterative-sketching LS solve on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c2] [--variant basic|damped|momentum]
+                    [--config c4] [--variant basic|damped|momentum]
 
-One "step" = one full `iterative_sketching` solve of the BASELINE workload
-(configs[1], "C2": gen_randsvd(200000, 200, kappa=1e10, beta=1e-12, seed=0),
-d = 20n = 4000, zeta = 8, reference-default basic variant, max_iters = 50):
-device pattern -> S·[A|b] -> QR -> x0 -> normest/condest -> refinement loop
--> trace readback.
+One "step" = one full `iterative_sketching` solve (/root/reference/pkg/src/
+itsketch/solvers.py:323-345): device pattern -> S·[A|b] -> QR -> x0 ->
+normest/condest -> refinement loop -> trace readback.
 
-  value   solve time (ms) with A, b resident in HBM (CUDA events, max over ranks)
-  e2e     same solve through the public API from pinned host numpy arrays:
-          H2D of A and b plus the D2H of solution/trace inside the timed region
+Default workload: BASELINE.json configs[3], "C4" — the north-star's scaling
+headline: gen_randsvd construction 4e6 x 2000 (64 GB, kappa 1e8, ||r|| 1e-6,
+seed 0) built on the GPU (instances.gen_randsvd_device; the host generator is
+infeasible at this size), d = 12n = 24000, zeta = 8, momentum
+(basic never fires the stopping rule at d = 12n),
+max_iters = 50.  `--config c1|c2|c3` runs the other BASELINE sizes.
+
+  value     solve time (ms) with A, b resident in HBM (CUDA events on the
+            solver's stream, median of K steps, max over ranks)
+  e2e       the same solve through the public API from pinned host numpy
+            arrays: H2D of A and b and the D2H of the solution / trace inside
+            the timed region (`e2e_pageable`: the same from ordinary numpy)
   roofline  the fused r=b-Ax / c=A'r pass (the loop's dominant kernel), timed
-          with CUDA events on its own stream: 8*m*n algorithmic bytes / launch
-  cpu_baseline  the CPU oracle (numpy/OpenBLAS restatement of the reference)
-          on the same instance, all host cores
+            with CUDA events on its own stream: 8*m*n algorithmic bytes / launch
+  cpu_baseline  the CPU oracle (numpy/OpenBLAS restatement of the reference,
+            tests/test_oracle_pin.py) on the same bytes, all host cores, one
+            full solve with its phases
+
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (one per GPU; A row-sharded, scaling "strong": the problem is fixed).
 
 --impl reference: the reference's CPU implementation of the path (the oracle
-port — the reference is pure Python and cannot travel to the GPU box) timed on
-the host on the same config; rank 0 only.
-A (320 MB) is larger than the 126 MB L2, so every pass streams from HBM.
+port — the reference is pure Python and cannot travel to the GPU box) timed
+on the host on the same instance bytes and the same config; rank 0 only.  A
+C4 oracle solve takes ~2 minutes, so it times up to K full solves inside a
+time budget (at least one; median, the reference's own method at
+cli.py:241-252) and says how many in `cpu_baseline.sample`.
+A is larger than the 126 MB L2 at every config but C1, so every pass streams
+from HBM.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,17 +65,21 @@ CONFIGS = {
     "c3": (1000000, 500, 1e15, 1e-3, 10000, 8),
     "c4": (4000000, 2000, 1e8, 1e-6, 24000, 8),
 }
+DEFAULT_CONFIG = "c4"
 # host numpy generator (the reference's construction and draw order) where it
 # is feasible; the device generator (instances.gen_randsvd_device) for C4
 GEN = {"c1": "host", "c2": "host", "c3": "host", "c4": "device"}
 # C4: d = 12n puts basic outside its contraction margin; the
 # headline is momentum
 DEFAULT_VARIANT = {"c4": "momentum"}
-# configs whose oracle solve is too long for a bench run: phase-sampled estimate
-SAMPLED = {"c4"}
-# iteration count used by the sampled estimate when the reference arm runs
-# alone (the GPU arm uses its own count); C4 momentum: measured on the GPU
-REF_ITERS = {"c4": 18}
+# seconds of oracle solves the reference arm may spend on timed steps
+REF_BUDGET_S = float(os.environ.get("ITSK_REF_BUDGET_S", "420"))
+
+
+def workload(config: str, m: int, n: int, d: int, zeta: int, variant: str, max_iters: int) -> str:
+    """The config string both arms print (the driver compares them)."""
+    return (f"{config}: iterative_sketching m={m} n={n} d={d} zeta={zeta} variant={variant} "
+            f"max_iters={max_iters}")
 
 
 def peaks():
@@ -127,9 +147,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 5 ms"}
 
 
-def make_problem(name: str, seed: int = 0, gen: str | None = None):
+def make_problem(name: str, seed: int = 0):
+    """(LsProblem, d, zeta): host numpy arrays (C1-C3, the reference's own
+    construction) or device tensors (C4, the device generator)."""
     m, n, kappa, beta, d, zeta = CONFIGS[name]
-    if (gen or GEN[name]) == "device":
+    if GEN[name] == "device":
         from paper_2311_04362_b200.instances import gen_randsvd_device
 
         return gen_randsvd_device(m, n, kappa, beta, seed), d, zeta
@@ -147,59 +169,6 @@ def host_ram_bytes() -> int:
         return 0
 
 
-def cpu_solve_time(a, b, d, zeta, variant, reps):
-    from oracle import itsketch_oracle as orc
-
-    times = []
-    res = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        res = orc.iterative_sketching(a, b, orc.Config(d=d, zeta=zeta, variant=variant))
-        times.append(time.perf_counter() - t0)
-    return times, res
-
-
-SAMPLE_ROWS = 250_000
-
-
-def cpu_sampled_estimate(a_s, b_s, m, d, zeta, iters, seed=0):
-    """Oracle solve time at a size too large to run whole in minutes: the
-    reference's phases timed on a bounded sample and scaled to the full size.
-      pattern + S·[A|b]   on the first SAMPLE_ROWS rows, x m/SAMPLE_ROWS
-      QR                  of a d x (n+1) matrix (the sketch's shape), once
-      refinement pass     r = b - A x, c = A'r on the sample, x m/SAMPLE_ROWS,
-                          times (iters + 1) passes (+ two n x n solves each)
-    Returns (ms, description)."""
-    from oracle import itsketch_oracle as orc
-
-    ms, n = (int(v) for v in a_s.shape)
-    scale = m / ms
-    t0 = time.perf_counter()
-    pat = orc.sparse_sign_pattern(d, ms, zeta, seed)
-    orc.sketch_apply(pat, np.column_stack([a_s, b_s]))
-    t_sketch = (time.perf_counter() - t0) * scale
-    w = np.random.default_rng(1).standard_normal((d, n + 1))
-    t0 = time.perf_counter()
-    q, r = orc.householder_qr_econ(w[:, :n])
-    t_qr = time.perf_counter() - t0
-    x = np.random.default_rng(2).standard_normal(n)
-    reps = 3
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        res = b_s - a_s @ x
-        c = a_s.T @ res
-    t_pass = (time.perf_counter() - t0) / reps * scale
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        orc.tri_solve_upper(r, orc.tri_solve_upper_transpose(r, c))
-    t_tri = (time.perf_counter() - t0) / reps
-    total = t_sketch + t_qr + (iters + 1) * t_pass + iters * t_tri
-    desc = (f"extrapolated: oracle pattern+sketch and one r=b-Ax, c=A'r pass on the first {ms} of {m} rows "
-            f"(x{scale:.1f}), QR of a {d}x{n} matrix, trisolve pair; {iters} iterations "
-            f"[sketch {t_sketch:.2f} s, qr {t_qr:.2f} s, pass {t_pass:.3f} s, tri {t_tri:.4f} s]")
-    return 1e3 * total, desc
-
-
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -209,61 +178,130 @@ def blas_threads():
         return os.cpu_count()
 
 
+def host_description() -> dict:
+    """os.cpu_count, lscpu's model line, threadpoolctl."""
+    desc = {"cpu_count": os.cpu_count(), "machine": platform.machine()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                desc[k.strip()] = v.strip()
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        desc["threadpools"] = [{"api": i.get("internal_api"), "version": i.get("version"),
+                                "threads": i.get("num_threads")} for i in threadpool_info()]
+    except Exception:
+        pass
+    desc["note"] = "scipy's sparse S·A (csc_matvecs; the oracle's C restatement) is single-threaded"
+    try:
+        import psutil
+
+        desc["ram_gb"] = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    return desc
+
+
+def oracle_solve(a, b, d, zeta, variant, phases=None):
+    """One oracle solve (seconds, (x, trace))."""
+    from oracle import itsketch_oracle as orc
+
+    t0 = time.perf_counter()
+    res = orc.iterative_sketching(a, b, orc.Config(d=d, zeta=zeta, variant=variant), phases=phases)
+    return time.perf_counter() - t0, res
+
+
+def phase_summary(phases: dict, iters: int) -> dict:
+    out = {k: round(v, 3) for k, v in phases.items()}
+    if iters > 0:
+        out["per_iteration_At_r"] = round(phases.get("At_r", 0.0) / iters, 3)
+        out["per_iteration_A_x"] = round(phases.get("A_x", 0.0) / (iters + 1), 3)
+        out["per_iteration_trisolve_pair"] = round(phases.get("trisolve_pair", 0.0) / iters, 3)
+    return out
+
+
+def host_instance(config: str):
+    """The config's instance as host numpy arrays (for the reference arm):
+    C1-C3 from the host generator; C4 from the device generator (same seed,
+    the same bytes the GPU arm solves), copied to pinned host memory."""
+    prob, d, zeta = make_problem(config)
+    try:
+        import torch
+    except Exception:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(prob.a, torch.Tensor):
+        m, n = prob.a.shape
+        a_h = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        blk = 1 << 18
+        for i in range(0, m, blk):
+            a_h[i:i + blk].copy_(prob.a[i:i + blk], non_blocking=True)
+        b_h = prob.b.cpu()
+        torch.cuda.synchronize()
+        del prob
+        torch.cuda.empty_cache()
+        return a_h.numpy(), b_h.numpy(), d, zeta, a_h
+    return prob.a, prob.b, d, zeta, None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    if args.config in SAMPLED:
-        return run_reference_sampled(args)
-    prob, d, zeta = make_problem(args.config)
-    m, n = prob.a.shape
-    _, _ = cpu_solve_time(prob.a, prob.b, d, zeta, args.variant, args.warmup)
-    times, res = cpu_solve_time(prob.a, prob.b, d, zeta, args.variant, args.steps)
+    m, n, _, _, d, zeta = CONFIGS[args.config]
+    need = 8 * m * n * 1.1 + (2 << 30)
+    if GEN[args.config] == "device" and host_ram_bytes() and host_ram_bytes() < need:
+        print(json.dumps({"impl": "reference", "unavailable": f"host RAM {host_ram_bytes() / 2**30:.0f} GiB "
+                          f"< {need / 2**30:.0f} GiB for the {args.config} instance"}), flush=True)
+        return 0
+    t_gen = time.perf_counter()
+    a, b, d, zeta, _keep = host_instance(args.config)
+    t_gen = time.perf_counter() - t_gen
+    # warm-up: imports, BLAS thread pools and the oracle's C library on a small
+    # solve (a full C4 warm-up solve would add minutes of nothing)
+    from oracle import itsketch_oracle as orc
+
+    wa, wb, _ = orc.gen_randsvd(4000, 50, 1e10, 1e-6, 0)
+    for _ in range(max(1, args.warmup) if GEN[args.config] == "device" else 0):
+        oracle_solve(wa, wb, 1000, 8, args.variant)
+    for _ in range(args.warmup if GEN[args.config] != "device" else 0):
+        oracle_solve(a, b, d, zeta, args.variant)
+    times, phases, res = [], {}, None
+    t_start = time.perf_counter()
+    while len(times) < args.steps:
+        ph = {} if not times else None
+        t, res = oracle_solve(a, b, d, zeta, args.variant, phases=ph)
+        if ph is not None:
+            phases = ph
+        times.append(t)
+        elapsed = time.perf_counter() - t_start
+        if elapsed + statistics.median(times) > REF_BUDGET_S:
+            break
     ms = 1e3 * statistics.median(times)
+    iters = len(res[1].iterates) - 1
     cores = blas_threads()
+    wl = workload(args.config, m, n, d, zeta, args.variant, 50)
+    sample = (f"{len(times)} full solve(s) of {wl} on the oracle (numpy/scipy restatement of "
+              f"itsketch.iterative_sketching, pinned to the reference's fixtures), median; "
+              f"{args.steps} requested, the rest past the {REF_BUDGET_S:.0f} s budget"
+              if len(times) < args.steps else
+              f"{len(times)} full solves of {wl} on the oracle (numpy/scipy restatement of "
+              f"itsketch.iterative_sketching, pinned to the reference's fixtures), median")
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen_randsvd, seed 0)",
-        "config": {"workload": f"{args.config}: iterative_sketching m={m} n={n} d={d} zeta={zeta} "
-                               f"variant={args.variant}", "parallelism": "host threads (OpenBLAS)"},
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full solves of {args.config} on the oracle "
-                                   "(numpy/scipy restatement of itsketch.iterative_sketching)"},
+        "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic (gen_randsvd construction on the GPU, seed 0; the same bytes as the b200 arm)"
+                 if GEN[args.config] == "device" else "synthetic (gen_randsvd, seed 0)"),
+        "config": {"workload": wl, "parallelism": "host threads (OpenBLAS)"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port", "sample": sample,
+                         "solves_s": [round(t, 3) for t in times],
+                         "phases_ms_first_solve": phase_summary(phases, iters), "host": host_description()},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iterations": len(res[1].iterates) - 1, "stop_reason": res[1].stop_reason,
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-def run_reference_sampled(args):
-    """--impl reference for a config whose oracle solve does not fit a bench
-    run: each step is the phase-sampled estimate (cpu_sampled_estimate) on a
-    Gaussian row block of the config's shape (the oracle's phase times do not
-    depend on the values)."""
-    m, n, kappa, beta, d, zeta = CONFIGS[args.config]
-    rng = np.random.default_rng(0)
-    ms = min(m, SAMPLE_ROWS)
-    a_s = rng.standard_normal((ms, n))
-    b_s = rng.standard_normal(ms)
-    iters = REF_ITERS[args.config]
-    for _ in range(args.warmup):
-        cpu_sampled_estimate(a_s[:2000, :50], b_s[:2000], 2000, 200, zeta, 1)
-    vals, desc = [], ""
-    for _ in range(args.steps):
-        v, desc = cpu_sampled_estimate(a_s, b_s, m, d, zeta, iters)
-        vals.append(v)
-    ms_val = statistics.median(vals)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": ms_val, "unit": "ms", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_val, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (Gaussian row sample)",
-        "config": {"workload": f"{args.config}: iterative_sketching m={m} n={n} d={d} zeta={zeta} "
-                               f"variant={args.variant}", "parallelism": "host threads (OpenBLAS)"},
-        "cpu_baseline": {"value": ms_val, "unit": "ms", "cores": blas_threads(), "kind": "port", "sample": desc},
-        "e2e": {"value": ms_val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iterations": iters,
+        "iterations": iters, "stop_reason": res[1].stop_reason, "instance_s": round(t_gen, 2),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -309,12 +347,54 @@ def fused_pass_timing(lib, at, bt, x, n_launch=30):
     return e0.elapsed_time(e1) / n_launch  # ms per launch (pass + finalize)
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N outside torchrun: run this script as N ranks (one per GPU),
+    the way the driver launches it; every rank gets WORLD_SIZE = N."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
+def probe_launch(args) -> int:
+    """--probe-launch: each rank joins the process group (NCCL with GPUs,
+    gloo without), sums the ranks, rank 0 prints the world it saw (tests
+    that --gpus N really runs N ranks)."""
+    import torch
+    import torch.distributed as tdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        tdist.init_process_group(backend)
+        dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if backend == "nccl" else None
+        t = torch.tensor([rank + 1.0], device=dev)
+        tdist.all_reduce(t)
+        total = float(t.item())
+        tdist.destroy_process_group()
+    else:
+        total = 1.0
+    if rank == 0:
+        print(json.dumps({"probe": "launch", "world": world, "gpus": args.gpus,
+                          "rank_sum": total}), flush=True)
+    return 0
+
+
 def run_b200(args):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # --sharded: the row-sharded path even at N = 1 (checks the N > 1 code
@@ -330,7 +410,9 @@ def run_b200(args):
     from paper_2311_04362_b200.dist import iterative_sketching_sharded, shard_bounds
 
     lib = _lib.lib_for_device(local)
+    t_gen = time.perf_counter()
     prob, d, zeta = make_problem(args.config)
+    t_gen = time.perf_counter() - t_gen
     m, n = prob.a.shape
     cfg = itsk.SolverConfig(d=d, zeta=zeta, variant=args.variant)
     r0, r1 = shard_bounds(m, world, rank)
@@ -339,13 +421,20 @@ def run_b200(args):
     # pinned host copies (e2e input) and HBM-resident copies (value input)
     do_e2e = not on_device or host_ram_bytes() > 2 * a_bytes + (8 << 30)
     a_pin = b_pin = None
+    x_true = prob.truth.x
     if on_device:
-        a_dev = prob.a[r0:r1]
-        b_dev = prob.b[r0:r1].contiguous()
-        x_true = prob.truth.x
+        if world > 1:  # keep only this rank's rows on the device
+            a_dev = prob.a[r0:r1].clone()
+            b_dev = prob.b[r0:r1].clone()
+            prob = None
+            torch.cuda.empty_cache()
+        else:
+            a_dev, b_dev = prob.a, prob.b
         if do_e2e:
             a_pin = torch.empty(tuple(a_dev.shape), dtype=torch.float64, pin_memory=True)
-            a_pin.copy_(a_dev)
+            blk = 1 << 18
+            for i in range(0, a_dev.shape[0], blk):
+                a_pin[i:i + blk].copy_(a_dev[i:i + blk], non_blocking=True)
             b_pin = b_dev.cpu().pin_memory()
     else:
         a_pin = torch.empty((r1 - r0, n), dtype=torch.float64, pin_memory=True)
@@ -354,22 +443,22 @@ def run_b200(args):
         b_pin.copy_(torch.from_numpy(np.ascontiguousarray(prob.b[r0:r1])))
         a_dev = a_pin.to(dev)
         b_dev = b_pin.to(dev)
-        x_true = prob.truth.x
     torch.cuda.synchronize()
 
-    def solve(a_in, b_in):
+    def solve(a_in, b_in, variant=None):
+        c = cfg if variant is None else itsk.SolverConfig(d=d, zeta=zeta, variant=variant)
         if dist_on:
-            return iterative_sketching_sharded(a_in, b_in, cfg, m, r0, residuals="all")
+            return iterative_sketching_sharded(a_in, b_in, c, m, r0, residuals="all")
         # the reference keeps every residual (solvers.py:245-246); that also lets
         # normest / condest run beside the first iterations (deferred estimates)
-        return itsk.iterative_sketching(a_in, b_in, cfg, residuals="all")
+        return itsk.iterative_sketching(a_in, b_in, c, residuals="all")
 
     def barrier():
         if dist_on:
             tdist.barrier()
         torch.cuda.synchronize()
 
-    def timed(a_in, b_in, steps):
+    def timed(a_in, b_in, steps, variant=None):
         stream = torch.cuda.current_stream(dev)
         times = []
         res = None
@@ -378,7 +467,7 @@ def run_b200(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = solve(a_in, b_in)
+            res = solve(a_in, b_in, variant)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -392,10 +481,18 @@ def run_b200(args):
         t_dev, res = timed(a_dev, b_dev, args.steps)
     l1 = lib.itsk_launch_count()
     t_e2e = [float("nan")]
+    t_e2e_pageable = None
     if do_e2e:
-        for _ in range(min(args.warmup, 1 if on_device else args.warmup)):
-            solve(a_pin.numpy(), b_pin.numpy())
-        t_e2e, res_e2e = timed(a_pin.numpy(), b_pin.numpy(), args.steps)
+        solve(a_pin.numpy(), b_pin.numpy())
+        t_e2e, _ = timed(a_pin.numpy(), b_pin.numpy(), args.steps)
+        if not args.no_pageable:
+            # an ordinary (pageable) numpy caller: a few steps, the copy is host-bound
+            a_np = a_pin.numpy().copy() if a_bytes <= (8 << 30) or host_ram_bytes() > 3 * a_bytes else None
+            if a_np is not None:
+                b_np = b_pin.numpy().copy()
+                solve(a_np, b_np)
+                t_e2e_pageable, _ = timed(a_np, b_np, min(args.steps, 3))
+                del a_np
     iters = res.iterations
     # graph-body kernels (fused pass, tail) run once per iteration
     # (the sharded loop is one graph too when the peer exchange carries its sums)
@@ -411,6 +508,17 @@ def run_b200(args):
 
     ms_dev = reduce_max(statistics.median(t_dev))
     ms_e2e = reduce_max(statistics.median(t_e2e)) if do_e2e else None
+    ms_e2e_pg = reduce_max(statistics.median(t_e2e_pageable)) if t_e2e_pageable else None
+    # the other BASELINE variant at C2 / C3 (basic and momentum)
+    variants = {}
+    if args.config in ("c2", "c3"):
+        for v in ("basic", "momentum"):
+            if v == args.variant:
+                continue
+            solve(a_dev, b_dev, v)
+            tv, rv = timed(a_dev, b_dev, max(3, min(args.steps, 10)), v)
+            variants[v] = {"ms": reduce_max(statistics.median(tv)), "iterations": rv.iterations,
+                           "stop_reason": rv.trace.stop_reason}
     x_dev = torch.from_numpy(res.solution).to(dev)
     pass_ms = reduce_max(fused_pass_timing(lib, a_dev, b_dev, x_dev))
     peak, peak_kind = peaks()
@@ -418,8 +526,9 @@ def run_b200(args):
     try:
         with open(os.path.join(ROOT, "profiles", "pass_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("m") == r1 - r0 and tr.get("n") == n:
-            traffic = tr["dram_bytes_per_launch"]
+        for rec in (tr if isinstance(tr, list) else [tr]):
+            if rec.get("m") == r1 - r0 and rec.get("n") == n:
+                traffic = rec["dram_bytes_per_launch"]
     except Exception:
         pass
     alg_bytes = 8.0 * (r1 - r0) * n
@@ -427,44 +536,52 @@ def run_b200(args):
     out = None
     if rank == 0:
         fe = float(np.linalg.norm(res.solution - x_true) / np.linalg.norm(x_true))
+        exch = None
+        if dist_on:
+            exch = ("peer memory (pass stores to every rank, tail sums; one CUDA graph)" if graph_loop else
+                    f"nccl allreduce per iteration (peer exchange unavailable: {getattr(res, 'peer_fallback', None)})")
         out = {
             "metric": METRIC, "value": ms_dev, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen_randsvd, seed 0; no dataset)",
-            "config": {"workload": f"{args.config}: iterative_sketching m={m} n={n} d={d} zeta={zeta} "
-                                   f"variant={args.variant} max_iters={cfg.max_iters}",
+            "vs_baseline": None, "dtype": "f64",
+            "data": ("synthetic (gen_randsvd construction on the GPU, seed 0; no dataset)" if on_device else
+                     "synthetic (gen_randsvd, seed 0; no dataset)"),
+            "config": {"workload": workload(args.config, m, n, d, zeta, args.variant, cfg.max_iters),
                        "global_rows": m, "cols": n, "parallelism": f"row-shard x{world}",
-                       "loop_exchange": (None if not dist_on else
-                                         "peer memory (pass stores to every rank, tail sums; one CUDA graph)"
-                                         if graph_loop else "nccl allreduce per iteration"),
-                       "generator": GEN[args.config],
+                       "loop_exchange": exch, "generator": GEN[args.config],
                        "l2": f"A ({a_bytes / 2**20:.0f} MiB per GPU) > L2 (126 MB): every pass streams from HBM, "
                              "no flush needed"},
-            "e2e": ({"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": int(8 * m * n + 8 * m),
-                     "d2h_bytes_per_step": int(8 * ((cfg.max_iters + 1) * n + 4 * (cfg.max_iters + 1) + 2) + 48)}
+            "e2e": ({"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": int(8 * (r1 - r0) * n + 8 * (r1 - r0)),
+                     "d2h_bytes_per_step": int(8 * ((cfg.max_iters + 1) * n + 4 * (cfg.max_iters + 1) + 2) + 48),
+                     "host_memory": "pinned"}
                     if do_e2e else {"value": None, "unit": "ms",
                                     "skipped": "host RAM below 2x A for the pinned copy"}),
+            "e2e_pageable": ({"value": ms_e2e_pg, "unit": "ms", "steps": len(t_e2e_pageable),
+                              "host_memory": "pageable numpy"} if ms_e2e_pg is not None else None),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-                         "kernel": "k_pass_tma (fused r=b-Ax, c=A'r, norms, in-kernel partial reduction)",
+                         "kernel": "fused r=b-Ax, c=A'r pass (k_pass_tma / k_pass_wide: norms and the "
+                                   "in-kernel partial reduction ride along)",
                          "bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms},
             "gpu_launches": int(launches),
             "iterations": iters, "stop_reason": res.trace.stop_reason, "fe": fe,
-            "passes_per_solve": iters + 1,
+            "passes_per_solve": iters + 1, "instance_s": round(t_gen, 2),
             "clocks": clk.summary(),
         }
+        if variants:
+            out["variants"] = variants
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.config not in SAMPLED:
-            times, ores = cpu_solve_time(prob.a, prob.b, d, zeta, args.variant, 1)
-            cpu_ms, sample = 1e3 * times[0], f"1 full solve of {args.config} on the oracle (numpy/OpenBLAS)"
-        else:
-            ms_rows = min(m, SAMPLE_ROWS)
-            a_s, b_s = prob.a[:ms_rows], prob.b[:ms_rows]
-            if isinstance(a_s, torch.Tensor):
-                a_s, b_s = a_s.cpu().numpy(), b_s.cpu().numpy()
-            cpu_ms, sample = cpu_sampled_estimate(a_s, b_s, m, d, zeta, iters)
-        out["cpu_baseline"] = {"value": cpu_ms, "unit": "ms", "cores": blas_threads(), "kind": "port",
-                               "sample": sample}
+        a_h = a_pin.numpy() if a_pin is not None else np.asarray(prob.a)
+        b_h = b_pin.numpy() if b_pin is not None else np.asarray(prob.b)
+        phases = {}
+        t_cpu, ores = oracle_solve(a_h, b_h, d, zeta, args.variant, phases=phases)
+        oit = len(ores[1].iterates) - 1
+        out["cpu_baseline"] = {
+            "value": 1e3 * t_cpu, "unit": "ms", "cores": blas_threads(), "kind": "port",
+            "sample": f"1 full solve of {args.config} on the oracle (numpy/OpenBLAS restatement of "
+                      f"itsketch.iterative_sketching) on the same bytes: {oit} iterations, "
+                      f"{ores[1].stop_reason}",
+            "phases_ms": phase_summary(phases, oit), "host": host_description()}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist_on:
@@ -478,16 +595,24 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--variant", default=None, choices=["basic", "damped", "momentum"])
     ap.add_argument("--sharded", action="store_true",
                     help="run the row-sharded (multi-GPU) path even with one rank (under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-numpy e2e measurement")
+    ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.variant is None:
         args.variant = DEFAULT_VARIANT.get(args.config, "basic")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
+    if args.probe_launch:
+        return probe_launch(args)
     return run_b200(args)
 
 

@@ -223,9 +223,11 @@ int itsk_csr_pass(const itsk_csr_plan* plan, const double* b, double bscale, con
  * buffer (peer-mapped pointers, e.g. torch symmetric memory) and raises its
  * flag there with the exchange's epoch; each rank's tail waits for all flags
  * of that epoch and sums the partials in rank order — the same bytes on
- * every rank.  recv[r]: rank r's buffer of 2 x size x (n+4) doubles (epoch
- * parity x source rank); flags[r]: rank r's size uint64 flags, zero before
- * the first exchange.  Exchanges of one loop use epochs epoch_base ..
+ * every rank.  recv[r]: rank r's buffer of 2 x size x (n+5) doubles (epoch
+ * parity x source rank; per source: c, the 4 norms and the sender's
+ * deferred-estimate ready bit, so every rank takes the same decision of
+ * when the stopping rule becomes evaluable); flags[r]: rank r's size uint64
+ * flags, zero before the first exchange.  Exchanges of one loop use epochs epoch_base ..
  * epoch_base + max_iters; the next loop on the same buffers starts above. */
 #define ITSK_MAX_PEERS 8
 typedef struct itsk_peer_params {
@@ -266,7 +268,11 @@ typedef struct itsk_loop_params {
    * iterations already recorded; itsk_loop_finish, enqueued after the
    * estimates, settles a loop that ended (guard / max_iters) before they
    * were ready.  Requires r_slots == max_iters + 1 (the stop may move back
-   * to an earlier, still-held iterate). */
+   * to an earlier, still-held iterate).  With a peer exchange the rule becomes
+   * evaluable once the flag is set on EVERY rank (each rank's ready bit
+   * travels with its partial), so all ranks stop at the same iteration; a
+   * host-collective (step_pre / allreduce / step_post) loop over several
+   * ranks must not defer. */
   const uint64_t* est_ready;
   /* Peer-memory exchange (nullable): with it the sharded loop needs no host
    * collective — itsk_loop_begin / the loop graph run it end to end. */

@@ -3,7 +3,8 @@
 #include <cstdlib>
 #include <atomic>
 #include <mutex>
-#include <unordered_set>
+#include <set>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 
@@ -23,20 +24,44 @@ void set_error(const char* fmt, ...) {
 
 void count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+// Function attributes take effect per device (context): the caches below
+// are keyed on (device, function, attribute), so a process that solves on
+// cuda:0 and then cuda:1 sets them again on the second device.
+namespace {
+std::mutex g_attr_mu;
+std::set<std::tuple<int, const void*, int>> g_attr_done;
+}  // namespace
+
+cudaError_t func_attr_once(const void* func, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_tuple(dev, func, static_cast<int>(attr));
+  if (g_attr_done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, attr, value);
+  if (e == cudaSuccess) g_attr_done.insert(key);
+  return e;
+}
+
 cudaError_t allow_max_smem(const void* func) {
-  static std::mutex mu;
-  static std::unordered_set<const void*> done;
-  std::lock_guard<std::mutex> lock(mu);
-  if (done.count(func)) return cudaSuccess;
   int dev = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    if (g_attr_done.count(std::make_tuple(dev, func, -1))) return cudaSuccess;
+  }
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaFuncAttributes fa;
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, func);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              optin - static_cast<int>(fa.sharedSizeBytes));
-  if (e == cudaSuccess) done.insert(func);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    g_attr_done.insert(std::make_tuple(dev, func, -1));
+  }
   return e;
 }
 

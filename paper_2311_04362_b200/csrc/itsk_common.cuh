@@ -41,6 +41,8 @@ int num_sms();
 // Raise `func`'s dynamic shared-memory limit to the device maximum (once per
 // kernel per process; cudaFuncSetAttribute is too slow to call per launch).
 cudaError_t allow_max_smem(const void* func);
+// cudaFuncSetAttribute once per (device, function, attribute)
+cudaError_t func_attr_once(const void* func, cudaFuncAttribute attr, int value);
 
 constexpr unsigned FULL = 0xffffffffu;
 

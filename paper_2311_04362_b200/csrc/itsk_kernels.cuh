@@ -30,7 +30,22 @@ struct PeerArgs {
   int64_t epoch_base = 0;
   double* recv[ITSK_MAX_PEERS] = {};
   uint64_t* flags[ITSK_MAX_PEERS] = {};
+  // deferred estimates: the sender's local ready flag travels with its
+  // partial (element n + 4), so all ranks see the same sum of ready bits
+  const uint64_t* est_ready = nullptr;
 };
+
+// width of one rank's record in the peer receive buffers: c (n), the four
+// norms, the ready bit
+__host__ __device__ inline int64_t peer_width(int64_t n) { return n + 5; }
+
+// the sender's ready bit (1.0 when the estimates are not deferred)
+__device__ __forceinline__ double peer_ready_bit(const PeerArgs& pe) {
+  if (!pe.est_ready) return 1.0;
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pe.est_ready) : "memory");
+  return v != 0 ? 1.0 : 0.0;
+}
 
 // Pointers the per-iteration kernels resolve from ctl->it.
 struct LoopPtrs {

@@ -164,7 +164,12 @@ __device__ int control_step(const LoopPtrs& p, LoopCtl* ctl, int begin) {
       re[rec] = ctl->truth_beta > 0 ? sqrt(tt) / ctl->truth_beta : resnorm / sqrt(ctl->result.bnorm2);
     rn[rec] = resnorm;
     int done = 0, eval = 0;
-    const bool ready = p.est_ready == nullptr || ld_acquire_u64(p.est_ready) != 0;
+    // deferred estimates: evaluable once ready — on several ranks once ready
+    // on every rank (the ready bits summed by the peer exchange), so all
+    // ranks evaluate the rule at the same iteration and stop together
+    const bool ready = p.est_ready == nullptr ||
+                       (p.peer.size > 0 ? p.cs[n + 4] == static_cast<double>(p.peer.size)
+                                        : ld_acquire_u64(p.est_ready) != 0);
     if (begin) {
       ctl->result.iterations = 0;
       ctl->result.sol_slot = 0;
@@ -292,7 +297,7 @@ __device__ void peer_gather(const LoopPtrs& p, int64_t epoch_base, int64_t it_ep
     }
   }
   __syncthreads();
-  const int64_t w = p.n + 4;
+  const int64_t w = peer_width(p.n);  // c, the norms and the ready bits (their sum: ranks ready)
   const double* rv = pe.recv[pe.rank] + (epoch & 1) * pe.size * w;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
     double s = __ldcg(rv + c);
@@ -506,6 +511,7 @@ PeerArgs peer_args(const itsk_loop_params* p) {
   g.rank = p->peer->rank;
   g.size = p->peer->size;
   g.epoch_base = p->peer->epoch_base;
+  g.est_ready = p->est_ready;
   for (int r = 0; r < ITSK_MAX_PEERS; ++r) {
     g.recv[r] = p->peer->recv[r];
     g.flags[r] = p->peer->flags[r];

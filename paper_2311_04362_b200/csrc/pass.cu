@@ -221,7 +221,8 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
   const PeerArgs& pe = a.peer;
   const bool send = pe.size > 0 && a.ctl != nullptr;
   const int64_t epoch = send ? a.ctl->epoch_base + (a.mode == 2 ? 0 : a.ctl->it + 1) : 0;
-  const int64_t slot = ((epoch & 1) * pe.size + pe.rank) * w;
+  const int64_t pw = peer_width(n);
+  const int64_t slot = ((epoch & 1) * pe.size + pe.rank) * pw;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
     const double s0 = sum_strided(a.gpart + c, 2 * w, ne, 0.0);
     const double s1 = sum_strided(a.gpart + w + c, 2 * w, no, 0.0);
@@ -230,6 +231,10 @@ __device__ void group_reduce(const PassArgs& a, int64_t n) {
     // peer exchange: this rank's partial into every rank's receive buffer
     if (send)
       for (int r = 0; r < pe.size; ++r) pe.recv[r][slot + c] = v;
+  }
+  if (send && threadIdx.x == 0) {
+    const double rb = peer_ready_bit(pe);
+    for (int r = 0; r < pe.size; ++r) pe.recv[r][slot + w] = rb;
   }
   if (send) {
     __threadfence_system();
@@ -706,12 +711,13 @@ __global__ void k_finalize(const double* __restrict__ part, int grid, int64_t n,
 // Peer send for the passes without the in-kernel reduction (k_pass +
 // k_finalize, rows not 16-byte aligned): the reduced partial, complete when
 // this kernel starts, to every rank's receive buffer, then the flags.
-__global__ void k_peer_send(const double* __restrict__ cs, int64_t w, const LoopCtl* ctl, int mode, PeerArgs pe) {
+__global__ void k_peer_send(const double* __restrict__ cs, int64_t n, const LoopCtl* ctl, int mode, PeerArgs pe) {
   if (ctl->result.done) return;
   const int64_t epoch = ctl->epoch_base + (mode == 2 ? 0 : ctl->it + 1);
+  const int64_t w = peer_width(n);
   const int64_t slot = ((epoch & 1) * pe.size + pe.rank) * w;
   for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
-    const double v = cs[c];
+    const double v = c < n + 4 ? cs[c] : peer_ready_bit(pe);
     for (int r = 0; r < pe.size; ++r) pe.recv[r][slot + c] = v;
   }
   __threadfence_system();
@@ -764,7 +770,7 @@ int occupancy_for(int cpl) {
 template <int CPL>
 int launch_cpl(const PassArgs& a, int grid, cudaStream_t s) {
   const size_t smem = pass_smem<CPL>();
-  blocks_per_sm<CPL>();  // sets the smem attribute once
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass<CPL>)));  // per device
   k_pass<CPL><<<grid, PASS_THREADS, smem, s>>>(a);
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -937,7 +943,7 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
   }
   if (rc == ITSK_OK && a0.tickets) rc = launch_finalize(a0.part, grid, a0.n, a0.cs, a0.ctl, s);
   if (rc == ITSK_OK && a0.peer.size > 0 && a0.ctl) {
-    k_peer_send<<<1, 256, 0, s>>>(a0.cs, a0.n + 4, a0.ctl, a0.mode, a0.peer);
+    k_peer_send<<<1, 256, 0, s>>>(a0.cs, a0.n, a0.ctl, a0.mode, a0.peer);
     count_launch();
     ITSK_CHECK_LAUNCH();
   }
@@ -969,13 +975,10 @@ int pass_groups(int64_t m, int64_t n, int* group) {
 
 int launch_finalize(const double* part, int grid, int64_t n, double* cs, const LoopCtl* ctl,
                     cudaStream_t s) {
-  static const bool carve = [] {
-    // keep the max shared-memory carveout across the pass / finalize pair:
-    // switching the L1/shared split between back-to-back kernels drains SMs
-    cudaFuncSetAttribute(k_finalize, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    return true;
-  }();
-  (void)carve;
+  // keep the max shared-memory carveout across the pass / finalize pair:
+  // switching the L1/shared split between back-to-back kernels drains SMs
+  ITSK_CUDA(func_attr_once(reinterpret_cast<const void*>(k_finalize),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const int t = 256;
   k_finalize<<<static_cast<unsigned>(((n + 4) * 32 + t - 1) / t), t, 0, s>>>(part, grid, n, cs, ctl);
   count_launch();

@@ -609,11 +609,8 @@ int qr_aug_core(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double*
   a.hmax = L.hmax;
   if (L.cluster) {
     ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_qr_cluster)));
-    static bool nonportable = false;
-    if (!nonportable) {
-      ITSK_CUDA(cudaFuncSetAttribute(k_qr_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      nonportable = true;
-    }
+    ITSK_CUDA(func_attr_once(reinterpret_cast<const void*>(k_qr_cluster),
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(L.P);
     cfg.blockDim = dim3(QR_THREADS);

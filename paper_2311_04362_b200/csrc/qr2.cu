@@ -832,8 +832,8 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   ITSK_CUDA(allow_max_smem(kp));
   ITSK_CUDA(allow_max_smem(ky));
   ITSK_CUDA(allow_max_smem(kn));
-  ITSK_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  ITSK_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ITSK_CUDA(func_attr_once(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ITSK_CUDA(func_attr_once(kn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int nsm = num_sms();
   const size_t ysm = y_smem(P.NB);
   const size_t nsmem = next_smem(P.hmax, P.NB);

@@ -403,11 +403,8 @@ int launch_qr_tsqr(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, doub
   a.singular = singular;
   a.hmax = (d + C - 1) / C + 1;
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_qr_tsqr)));
-  static bool nonportable = false;
-  if (!nonportable) {
-    ITSK_CUDA(cudaFuncSetAttribute(k_qr_tsqr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    nonportable = true;
-  }
+  ITSK_CUDA(func_attr_once(reinterpret_cast<const void*>(k_qr_tsqr),
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(TT);

@@ -223,7 +223,7 @@ int launch_ring(const double* A, int64_t lda, int64_t n, const double* b, const 
   const int64_t ncol = n + (b ? 1 : 0);
   dim3 grid(static_cast<unsigned>((d + RG_WARPS - 1) / RG_WARPS), static_cast<unsigned>((ncol + 31) / 32));
   const size_t smem = RG_WARPS * RG_DEPTH * (32 * sizeof(double) + sizeof(uint32_t));
-  ITSK_CUDA(cudaFuncSetAttribute(k_sketch_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_sketch_ring)));
   k_sketch_ring<<<grid, 32 * RG_WARPS, smem, s>>>(A, lda, n, b, ptr, src, d, scale, W, ldw, rg);
   count_launch();
   ITSK_CHECK_LAUNCH();

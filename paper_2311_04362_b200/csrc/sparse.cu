@@ -452,10 +452,7 @@ int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const doub
   a.xs = xs;
   a.rs = rs;
   a.mode = mode;
-  static const bool attr = [] {
-    return allow_max_smem(reinterpret_cast<const void*>(k_csr_rows)) == cudaSuccess;
-  }();
-  (void)attr;
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_csr_rows)));
   const size_t xsmem = (CSR_THREADS / 32) * ROW_STAGE * 12 + (P->n <= X_STAGE ? static_cast<size_t>(P->n) * 8 : 0);
   ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_csr_rows), dim3(P->g1), dim3(CSR_THREADS), xsmem, s, a));
   count_launch();
@@ -643,10 +640,7 @@ extern "C" int itsk_csr_sketch(const itsk_csr_plan* plan, const double* b, const
   ITSK_REQUIRE(d >= 1 && zeta >= 1 && ldw >= P->n + (b ? 1 : 0), "bad sketch shape");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const double scale = 1.0 / sqrt(static_cast<double>(zeta));  // embed.py:92
-  static const bool attr = [] {
-    return allow_max_smem(reinterpret_cast<const void*>(k_sketch_csr)) == cudaSuccess;
-  }();
-  (void)attr;
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_sketch_csr)));
   const int64_t n = P->n;
   const int64_t budget = 180 * 1024;
   int warps = static_cast<int>(std::min<int64_t>(8, budget / (n * 8)));

@@ -90,7 +90,8 @@ class PeerExchange:
     collective per iteration, so the sharded loop runs as one CUDA graph.
 
     recv_ptrs / flag_ptrs are the device addresses of each rank's receive
-    buffer (2 x world x (n+4) float64) and flags (world uint64, zero at
+    buffer (2 x world x (n+5) float64: c, the 4 norms and the sender's
+    deferred-estimate ready bit) and flags (world uint64, zero at
     start) as seen from this rank — torch symmetric memory peers on the GPU
     box, or plain tensors of one device in the single-process tests."""
 
@@ -106,7 +107,7 @@ class PeerExchange:
 
     @staticmethod
     def buffers(n: int, world: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
-        return (torch.zeros(2 * world * (n + 4), dtype=torch.float64, device=dev),
+        return (torch.zeros(2 * world * (n + 5), dtype=torch.float64, device=dev),
                 torch.zeros(world, dtype=torch.int64, device=dev))
 
     def params(self, max_iters: int) -> _lib.PeerParams:
@@ -124,26 +125,35 @@ class PeerExchange:
 
 
 _PEERS: dict = {}
+# why the peer exchange is unavailable, per _PEERS key (reported by the
+# result's `peer_fallback` and by bench.py's `loop_exchange`)
+PEER_FALLBACK: dict = {}
 
 
-def peer_exchange(n: int, dev, group=None) -> PeerExchange | None:
+def peer_exchange(n: int, dev, group=None, require: bool = False) -> PeerExchange | None:
     """The rank's PeerExchange for loops with n columns on `group`, set up once
     through torch symmetric memory (IPC-mapped peer buffers over NVLink); None
-    when symmetric memory is unavailable (the caller falls back to NCCL)."""
+    when symmetric memory is unavailable (the caller falls back to NCCL and
+    the reason is kept in PEER_FALLBACK).  require=True raises instead."""
     import torch.distributed as tdist
 
     world = tdist.get_world_size(group)
     rank = tdist.get_rank(group)
     key = (id(group), dev.index, n, world)
     if key in _PEERS:
+        if _PEERS[key] is None and require:
+            raise RuntimeError(f"peer exchange unavailable: {PEER_FALLBACK.get(key)}")
         return _PEERS[key]
     if world > _lib.MAX_PEERS:
+        PEER_FALLBACK[key] = f"world size {world} > {_lib.MAX_PEERS}"
+        if require:
+            raise RuntimeError(f"peer exchange unavailable: {PEER_FALLBACK[key]}")
         return None
     try:
         import torch.distributed._symmetric_memory as symm_mem
 
         g = group if group is not None else tdist.group.WORLD
-        recv = symm_mem.empty(2 * world * (n + 4), dtype=torch.float64, device=dev)
+        recv = symm_mem.empty(2 * world * (n + 5), dtype=torch.float64, device=dev)
         flags = symm_mem.empty(world, dtype=torch.int64, device=dev)
         recv.zero_()
         flags.zero_()
@@ -152,7 +162,10 @@ def peer_exchange(n: int, dev, group=None) -> PeerExchange | None:
         hf = symm_mem.rendezvous(flags, g)
         tdist.barrier(group=group)  # every rank's flags are zero before any rank writes
         px = PeerExchange(rank, world, list(hr.buffer_ptrs), list(hf.buffer_ptrs), keep=(recv, flags, hr, hf))
-    except Exception:  # noqa: BLE001 - no symmetric memory on this setup: NCCL path
+    except Exception as exc:  # noqa: BLE001 - no symmetric memory on this setup: NCCL path
+        if require:
+            raise
+        PEER_FALLBACK[key] = f"{type(exc).__name__}: {exc}"[:300]
         px = None
     _PEERS[key] = px
     return px
@@ -290,11 +303,13 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     peer-memory exchange (PeerExchange: the pass stores to every rank over
     NVLink, the tail gathers; the whole loop is one CUDA graph) when
     symmetric memory is available and A is dense, else with NCCL allreduce
-    between the two halves of each iteration; "nccl" forces the latter."""
+    between the two halves of each iteration (the result's `peer_fallback`
+    says why); "nccl" forces the latter; "require" raises instead of falling
+    back."""
     import torch.distributed as tdist
 
-    if peer not in ("auto", "nccl"):
-        raise ValueError("peer must be 'auto' or 'nccl'")
+    if peer not in ("auto", "nccl", "require"):
+        raise ValueError("peer must be 'auto', 'nccl' or 'require'")
     ws, at, lda, csr = _shard_prepare(a_local, b_local, cfg, m_total, row0, truth, residuals)
     lib = _dev.lib(ws.dev)
     n = ws.n
@@ -305,8 +320,19 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
         tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
 
     allreduce(ws.W)
-    px = peer_exchange(n, ws.dev, group) if (peer == "auto" and csr is None) else None
-    defer = ws.r_slots == cfg.max_iters + 1 and cfg.max_iters > 0
+    if peer == "require" and csr is not None:
+        raise ValueError("peer='require': the peer exchange carries dense loops only")
+    px = peer_exchange(n, ws.dev, group, require=peer == "require") if (peer != "nccl" and csr is None) else None
+    fallback = None
+    if px is None:
+        fallback = ("peer='nccl'" if peer == "nccl" else "sparse block" if csr is not None else
+                    PEER_FALLBACK.get((id(group), ws.dev.index, n, tdist.get_world_size(group)), "unavailable"))
+    # deferred estimates: with the peer exchange the ready bits travel with
+    # the partials (every rank evaluates the rule at the same iteration); the
+    # host-collective loop polls `done` between collectives, so over several
+    # ranks it runs with the estimates computed first
+    world = tdist.get_world_size(group)
+    defer = ws.r_slots == cfg.max_iters + 1 and cfg.max_iters > 0 and (px is not None or world == 1)
     p = _shard_factor(ws, at, lda, csr, cfg, truth, px, defer=defer)
     if px is not None:
         from .solvers import run_loop
@@ -338,4 +364,5 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     out._workspace = ws  # keep the local residual rows alive
     out._csr = csr       # and the local CSR plan the trace's residuals came from
     out.peer_exchange = px is not None
+    out.peer_fallback = fallback  # None, or why the loop's sums went through NCCL
     return out

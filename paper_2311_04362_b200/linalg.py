@@ -8,9 +8,8 @@
 
 Differences from the reference, by design:
   * the QR never forms Q (dorgqr); it applies the reflectors to an extra
-    right-hand-side column instead, returning R and z = Q'rhs.  QrFactors.q
-    is therefore None unless `want_q` asks for Q = (the QR of [A | I]) — not
-    needed on the path.
+    right-hand-side column instead, returning R and z = Q'rhs.  Reading
+    QrFactors.q raises an AttributeError explaining this.
   * cond_est uses Lanczos (<= 96 steps, stopped when the extreme Ritz values
     are stable to rounding) instead of a full SVD; for the spectra on this
     path it agrees with dgesdd's ratio to ~1e-14 relative (tests/).
@@ -36,11 +35,20 @@ __all__ = ["QrFactors", "SingularMatrixError", "householder_qr_econ", "qr_aug", 
 @dataclass(frozen=True)
 class QrFactors:
     """R (n x n, upper, diag >= 0) and z = Q' rhs (None without a rhs).
-    `q` is kept for field-compatibility with linalg.py:21-27 and is None."""
+
+    The reference's QrFactors (linalg.py:21-27) carries an explicit Q; this
+    path never forms it (the reflectors are applied to the rhs column
+    instead, solvers.py:209 only needs Q'Sb).  Reading `q` raises an
+    AttributeError that says so, rather than returning None
+    (INTEGRATION.md §4)."""
 
     r: object
     z: object = None
-    q: object = None
+
+    @property
+    def q(self):
+        raise AttributeError("QrFactors.q: the B200 QR does not form Q (dorgqr); use "
+                             "householder_qr_econ(a, rhs=b).z for Q'b, as sketch_and_solve does")
 
 
 def qr_workspace(d: int, n: int, dev) -> torch.Tensor:

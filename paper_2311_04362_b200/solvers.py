@@ -234,7 +234,10 @@ class _Workspace:
         self.sing_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.v0_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
         self.v0_seed = None
-        self.graphs: dict = {}  # loop params key -> instantiated loop graph
+        # loop params key -> (instantiated loop graph, objects whose device
+        # memory it captured: kept alive so their addresses — part of the key —
+        # cannot be reused by another object while the graph is cached)
+        self.graphs: dict = {}
         # residual rows: a second buffer is allocated the first time a solve
         # starts while an earlier result still refers to the rows, so results
         # kept by the caller are not copied out (two alive: the older is)
@@ -273,7 +276,7 @@ class _Workspace:
                                    neg_dev=self.neg, ptr_dev=self.sk_ptr, src_dev=self.sk_src)
 
     def release(self):
-        for h in self.graphs.values():
+        for h, _ in self.graphs.values():
             _lib.load().itsk_loop_graph_destroy(h)
         self.graphs = {}
 
@@ -489,22 +492,27 @@ def _read_result(lib, ws: _Workspace, p, stream_obj) -> _lib.LoopResult:
     return _lib.LoopResult.from_buffer_copy(bytes(host.numpy()))
 
 
-def run_loop(lib, ws: _Workspace, p, use_graph: bool, stream: int) -> None:
+def run_loop(lib, ws: _Workspace, p, use_graph: bool, stream: int, keep=None) -> None:
+    """keep: the objects owning device memory the loop reads through
+    pointers in `p` that are not the workspace's own (a sparse A's CSR plan):
+    a cached graph holds them, so a later object cannot reuse their
+    addresses and hit a graph that captured freed memory."""
     _lib.check(lib.itsk_loop_begin(ctypes.byref(p), stream))
     if p.max_iters == 0:
         return
     if use_graph:
         key = _params_key(p)
-        h = ws.graphs.get(key)
-        if h is None:
+        ent = ws.graphs.get(key)
+        if ent is None:
             if len(ws.graphs) >= 4:
-                for g in ws.graphs.values():
+                for g, _ in ws.graphs.values():
                     lib.itsk_loop_graph_destroy(g)
                 ws.graphs = {}
             h = ctypes.c_void_p()
             _lib.check(lib.itsk_loop_graph_create(ctypes.byref(p), stream, ctypes.byref(h)))
-            ws.graphs[key] = h
-        _lib.check(lib.itsk_loop_graph_launch(h, stream))
+            ent = (h, keep)
+            ws.graphs[key] = ent
+        _lib.check(lib.itsk_loop_graph_launch(ent[0], stream))
     else:
         for _ in range(p.max_iters):
             _lib.check(lib.itsk_loop_step_pre(ctypes.byref(p), stream))
@@ -598,7 +606,7 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
     _sketch_qr_x0(lib, ws, at, lda, bt, cfg, stream, csr, upload, defer=defer)
     p = _loop_params(ws, at, lda, cfg, alpha, beta, truth, csr=csr, defer=defer)
     p.b = _dev.ptr(bt)
-    run_loop(lib, ws, p, use_graph, stream)
+    run_loop(lib, ws, p, use_graph, stream, keep=csr)
     if defer:
         stream_obj.wait_stream(ws.est_stream)
         _lib.check(lib.itsk_loop_finish(ctypes.byref(p), stream))

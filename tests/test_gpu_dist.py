@@ -152,3 +152,75 @@ def test_sharded_sparse_solve_matches_single_gpu(nccl_group):
     got = iterative_sketching_sharded(p.a, p.b, itsk.SolverConfig(d=2400, max_iters=15, rng_seed=2), 40000, 0)
     assert got.trace.stop_reason == ref.trace.stop_reason and got.iterations == ref.iterations
     assert np.array_equal(got.solution, ref.solution)
+
+
+@pytest.mark.parametrize("hold", [False, True])
+def test_peer_exchange_deferred_estimates_agree(hold):
+    """Deferred normest / condest over 2 ranks of the peer exchange (in one
+    process, as above), on a consistent system that stops after 1-2
+    iterations: each rank's ready flag rises at a different time (hold=True:
+    rank 1's stays zero through the whole loop and is raised just before
+    itsk_loop_finish).  The ready bits travel with the partials, so both ranks
+    evaluate the rule at the same iteration and stop together (a rank that
+    stopped alone would leave the other waiting for its flags: ADVICE r1),
+    and the result equals the solve with the estimates computed first."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import ctypes
+
+    import paper_2311_04362_b200 as itsk
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+    from paper_2311_04362_b200.dist import PeerExchange, _shard_factor, _shard_prepare, shard_bounds
+    from paper_2311_04362_b200.solvers import _assemble, _read_result
+
+    m, n, d, world = 20000, 40, 800, 2
+    p = itsk.gen_randsvd(m, n, 1e3, 0.0, 5)
+    dev = dv.current_device()
+    lib = dv.lib(dev)
+    so = torch.cuda.current_stream(dev)
+    s = int(so.cuda_stream)
+
+    def solve(defer: bool):
+        cfg = itsk.SolverConfig(d=d, max_iters=12, rng_seed=5)
+        ranks = []
+        for r in range(world):
+            r0, r1 = shard_bounds(m, world, r)
+            ranks.append(_shard_prepare(p.a[r0:r1], p.b[r0:r1], cfg, m, r0, None, "all"))
+        W = ranks[0][0].W.clone()
+        for ws, *_ in ranks[1:]:
+            W += ws.W
+        for ws, *_ in ranks:
+            ws.W.copy_(W)
+        bufs = [PeerExchange.buffers(n, world, dev) for _ in range(world)]
+        pxs = [PeerExchange(r, world, [b[0].data_ptr() for b in bufs], [b[1].data_ptr() for b in bufs], keep=bufs)
+               for r in range(world)]
+        ps = [_shard_factor(ws, at, lda, csr, cfg, None, px, defer=defer) for (ws, at, lda, csr), px in zip(ranks, pxs)]
+        held = torch.zeros(1, dtype=torch.int64, device=dev)
+        if defer and hold:
+            ps[1].est_ready = held.data_ptr()
+        for r in range(world):
+            _lib.check(lib.itsk_loop_begin_local(ctypes.byref(ps[r]), s))
+        for r in range(world):
+            _lib.check(lib.itsk_loop_begin_finish(ctypes.byref(ps[r]), s))
+        for _ in range(cfg.max_iters):
+            for r in range(world):
+                _lib.check(lib.itsk_loop_step_pre(ctypes.byref(ps[r]), s))
+            for r in range(world):
+                _lib.check(lib.itsk_loop_step_post(ctypes.byref(ps[r]), s))
+        outs = []
+        for (ws, at, lda, csr), pr in zip(ranks, ps):
+            if defer:
+                so.wait_stream(ws.est_stream)
+                held.fill_(1)
+                _lib.check(lib.itsk_loop_finish(ctypes.byref(pr), s))
+            res = _read_result(lib, ws, pr, so)
+            outs.append(_assemble(ws, res, None, cfg, at, ws.b))
+        return outs
+
+    ref = solve(False)
+    got = solve(True)
+    assert ref[0].trace.stop_reason == "stopped_by_rule" and ref[0].iterations <= 3
+    for r in range(world):
+        _same_solve(got[r], ref[r])
+        assert np.array_equal(got[r].solution, ref[0].solution)

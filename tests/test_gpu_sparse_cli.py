@@ -176,6 +176,23 @@ def test_sparse_solve_device_csr_and_determinism(pkg):
         pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=1920, track_be=True))
 
 
+def test_sparse_graph_cache_two_matrices_same_shape(pkg):
+    """Two different sparse A of the same shape (different nnz) solved back to
+    back from scipy inputs (a fresh CsrMatrix per call): the cached loop
+    graph of the first must not be replayed with the second's plan
+    (plan addresses were reusable while a graph held them).  Each
+    result equals the step-wise (no graph) solve of the same matrix."""
+    cfg = pkg.SolverConfig(d=1920, variant="momentum", max_iters=20, rng_seed=9)
+    p1 = pkg.gen_sparse(30000, 64, 9)
+    p2 = pkg.gen_sparse(30000, 64, 10)
+    assert p1.a.nnz != p2.a.nnz or not np.array_equal(p1.a.indices, p2.a.indices)
+    want = [pkg.iterative_sketching(p.a, p.b, cfg, use_graph=False).solution for p in (p1, p2)]
+    for _ in range(3):
+        for p, w in zip((p1, p2), want):
+            got = pkg.iterative_sketching(p.a, p.b, cfg)
+            assert np.array_equal(got.solution, w)
+
+
 # --------------------------------------------------------------------------
 # CLI with the device flag
 # --------------------------------------------------------------------------

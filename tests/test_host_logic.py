@@ -68,3 +68,16 @@ def test_gen_randsvd_matches_oracle_bitwise():
     a, b, t = orc.gen_randsvd(300, 7, 1e6, 1e-4, 5)
     assert np.array_equal(p.a, a) and np.array_equal(p.b, b) and np.array_equal(p.truth.x, t.x)
     assert math.isclose(np.linalg.norm(p.truth.r), 1e-4, rel_tol=1e-12)
+
+
+def test_qrfactors_q_raises_clearly():
+    """The B200 QR never forms Q: reading .q says so
+    instead of returning None."""
+    import pytest
+
+    from paper_2311_04362_b200.linalg import QrFactors
+
+    f = QrFactors(r=np.eye(2), z=np.zeros(2))
+    with pytest.raises(AttributeError, match="does not form Q"):
+        f.q
+    assert not hasattr(f, "q")
