@@ -694,6 +694,261 @@ __global__ void __launch_bounds__(32 * (WIDE_NCW + 1), 1) k_pass_wide(PassArgs a
   if (a.tickets) group_reduce(a, n);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-wide rows (512 < n <= 2048, the C4 shape): every consumer thread owns
+// the column pairs {2t, 2t+1} + 1024 j (j < CPP) for the whole pass, with x
+// and its slice of c in registers.  A stage of the ring holds RC_RB = 4 rows
+// (one bulk copy); each thread reads its pairs of the 4 rows ONCE from
+// shared memory (16-byte loads) into registers and releases the stage, so
+// the row is used for both the dot and the c update without a second
+// shared-memory read and without x in shared memory (k_pass_wide read the
+// row twice and x once per row: 4x the row's bytes of shared-memory traffic
+// against ~2x here).  Per batch: 4 partial dots per thread -> in-warp
+// reduce-scatter (6 shuffles; lane group g = lane/8 holds row g's warp sum)
+// -> 16 warp partials per row in shared memory (double-buffered by batch
+// parity) -> ONE named barrier -> every warp sums the 16 partials of the 4
+// rows in warp order (the same bits in every warp), r = b - dot -> c += r *
+// row.  Warp 0 (lane u <-> row u) writes r and accumulates the norms.  Each
+// column of c is owned by one thread: no shared-memory reduction of c.
+// ---------------------------------------------------------------------------
+constexpr int RC_NCW = 16, RC_RB = 4, RC_T = RC_NCW * 32;
+
+template <int CPP>
+__global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a, TmaShape sh) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + 32;
+  unsigned char* stages = smraw + 1024;
+  __shared__ double dpart[2][RC_NCW][RC_RB];
+  __shared__ double ssm[4];
+  __shared__ int s_done;
+
+  const double* r_true = a.r_true;
+  const double* b = a.b;
+  const double bscale = a.bscale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n, lda = a.lda;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
+  const int S = sh.S;
+  const int ntiles = (nrows + RC_RB - 1) / RC_RB;
+  const int npre = min(S, ntiles);
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, RC_NCW);  // one arrival per consumer warp per batch
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (warp == RC_NCW && lane == 0) {
+    const uint64_t pol = evict_first_policy();
+    for (int t = 0; t < npre; ++t) {
+      const int rows = min(RC_RB, nrows - t * RC_RB);
+      const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+      mbar_expect_tx(full + t, bytes);
+      bulk_g2s(stages + static_cast<int64_t>(t) * sh.stage_bytes, a.A + (r_begin + t * RC_RB) * lda, bytes,
+               full + t, pol);
+    }
+  }
+  pdl_wait();
+
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  if (a.mode == 0) {
+    x = a.x;
+    r_prev = a.r_prev;
+    r_out = a.r_out;
+  } else {
+    const LoopCtl* ctl = a.ctl;
+    if (tid == 0) s_done = ctl->result.done;
+    __syncthreads();
+    if (s_done) {
+      if (warp == RC_NCW && lane == 0)
+        for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
+      return;
+    }
+    const int64_t SL = ctl->r_slots;
+    if (a.mode == 1) {
+      const int64_t it = ctl->it;
+      x = a.xs + (it + 1) * a.n;
+      r_prev = a.rs + (it % SL) * a.m;
+      r_out = a.rs + ((it + 1) % SL) * a.m;
+    } else {
+      x = a.xs;
+      r_prev = nullptr;
+      r_out = a.rs;
+    }
+  }
+
+  double2 acc[CPP];
+  double2 xv[CPP];
+  int col[CPP];
+#pragma unroll
+  for (int j = 0; j < CPP; ++j) {
+    acc[j] = make_double2(0.0, 0.0);
+    col[j] = 2 * tid + 2 * RC_T * j;
+  }
+
+  if (warp == RC_NCW) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      for (int t = npre; t < ntiles; ++t) {
+        const int s = t % S;
+        mbar_wait(empty + s, static_cast<unsigned>(((t / S) - 1) & 1));
+        const int rows = min(RC_RB, nrows - t * RC_RB);
+        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+        mbar_expect_tx(full + s, bytes);
+        bulk_g2s(stages + static_cast<int64_t>(s) * sh.stage_bytes, a.A + (r_begin + t * RC_RB) * lda, bytes,
+                 full + s, pol);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < CPP; ++j) {
+      const int c = col[j];
+      xv[j].x = c < n ? x[c] : 0.0;
+      xv[j].y = c + 1 < n ? x[c + 1] : 0.0;
+    }
+    // b / r_prev / r_true of the batch's rows, one batch ahead (lane u <-> row u)
+    const bool lead = lane < RC_RB;
+    auto fetch = [&](int t, double& fb, double& fp, double& ft) {
+      const int k = t * RC_RB + lane;
+      const bool ok = lead && t < ntiles && k < nrows;
+      const int64_t g = r_begin + k;
+      fb = ok ? b[g] : 0.0;
+      fp = (ok && warp == 0 && r_prev) ? r_prev[g] : 0.0;
+      ft = (ok && warp == 0 && r_true) ? r_true[g] : 0.0;
+    };
+    double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
+    double cb, cp, ct;
+    fetch(0, cb, cp, ct);
+    const int g8 = lane >> 3;  // row whose warp sum this lane ends up holding
+    for (int t = 0; t < ntiles; ++t) {
+      double nb, np, nt;
+      fetch(t + 1, nb, np, nt);
+      const int s = t % S;
+      const int nu = min(RC_RB, nrows - t * RC_RB);
+      mbar_wait(full + s, static_cast<unsigned>((t / S) & 1));
+      const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(s) * sh.stage_bytes);
+      double2 v[RC_RB][CPP];
+#pragma unroll
+      for (int u = 0; u < RC_RB; ++u)
+#pragma unroll
+        for (int j = 0; j < CPP; ++j) {
+          const int c = col[j];
+          double2 w = make_double2(0.0, 0.0);
+          if (u < nu && c < n) {
+            w = *reinterpret_cast<const double2*>(base + u * lda + c);
+            if (c + 1 >= n) w.y = 0.0;  // the pad column of an odd n
+          }
+          v[u][j] = w;
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);  // the stage is in registers: release it
+      double d[RC_RB];
+#pragma unroll
+      for (int u = 0; u < RC_RB; ++u) {
+        double acc_d = 0.0;
+#pragma unroll
+        for (int j = 0; j < CPP; ++j) {
+          acc_d = fma(v[u][j].x, xv[j].x, acc_d);
+          acc_d = fma(v[u][j].y, xv[j].y, acc_d);
+        }
+        d[u] = acc_d;
+      }
+      // in-warp reduce-scatter: after it lane l holds row (l >> 3)'s warp sum
+      const bool h4 = (lane & 16) != 0, h3 = (lane & 8) != 0;
+      double k0 = h4 ? d[2] : d[0], k1 = h4 ? d[3] : d[1];
+      const double e0 = h4 ? d[0] : d[2], e1 = h4 ? d[1] : d[3];
+      k0 += __shfl_xor_sync(FULL, e0, 16);
+      k1 += __shfl_xor_sync(FULL, e1, 16);
+      double kk = h3 ? k1 : k0;
+      kk += __shfl_xor_sync(FULL, h3 ? k0 : k1, 8);
+      kk += __shfl_xor_sync(FULL, kk, 4);
+      kk += __shfl_xor_sync(FULL, kk, 2);
+      kk += __shfl_xor_sync(FULL, kk, 1);
+      const int par = t & 1;
+      if ((lane & 7) == 0) dpart[par][warp][g8] = kk;
+      asm volatile("bar.sync 1, %0;" ::"n"(RC_T) : "memory");
+      // every warp: the 4 rows' dots, the 16 warp partials summed in warp
+      // order (lane l < 16 holds warp l's partial of rows 2h and 2h+1 ...)
+      double q0 = 0.0, q1 = 0.0;
+      {
+        const int w = lane & 15, rr = (lane >> 4) * 2;
+        q0 = dpart[par][w][rr];
+        q1 = dpart[par][w][rr + 1];
+      }
+      // fixed tree over the 16 warps (xor 8, 4, 2, 1 within each half)
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        q0 += __shfl_xor_sync(FULL, q0, o);
+        q1 += __shfl_xor_sync(FULL, q1, o);
+      }
+      // rows 0, 1 live in lanes 0..15, rows 2, 3 in lanes 16..31
+      const double dot0 = __shfl_sync(FULL, q0, 0), dot1 = __shfl_sync(FULL, q1, 0);
+      const double dot2 = __shfl_sync(FULL, q0, 16), dot3 = __shfl_sync(FULL, q1, 16);
+      double rv[RC_RB];
+      rv[0] = bscale * __shfl_sync(FULL, cb, 0) - dot0;
+      rv[1] = bscale * __shfl_sync(FULL, cb, 1) - dot1;
+      rv[2] = bscale * __shfl_sync(FULL, cb, 2) - dot2;
+      rv[3] = bscale * __shfl_sync(FULL, cb, 3) - dot3;
+#pragma unroll
+      for (int u = 0; u < RC_RB; ++u)
+        if (u >= nu) rv[u] = 0.0;
+#pragma unroll
+      for (int u = 0; u < RC_RB; ++u)
+#pragma unroll
+        for (int j = 0; j < CPP; ++j) {
+          acc[j].x = fma(rv[u], v[u][j].x, acc[j].x);
+          acc[j].y = fma(rv[u], v[u][j].y, acc[j].y);
+        }
+      if (warp == 0 && lane < nu) {
+        double rl = rv[0];
+#pragma unroll
+        for (int u = 1; u < RC_RB; ++u)
+          if (lane == u) rl = rv[u];
+        if (r_out) r_out[r_begin + t * RC_RB + lane] = rl;
+        s_rr += rl * rl;
+        s_bb += cb * cb;
+        const double dd = rl - cp;
+        s_dd += dd * dd;
+        const double tt = ct - rl;
+        s_tt += tt * tt;
+      }
+      cb = nb; cp = np; ct = nt;
+    }
+    if (warp == 0) {
+      s_rr = warp_sum(s_rr);
+      s_dd = warp_sum(s_dd);
+      s_tt = warp_sum(s_tt);
+      s_bb = warp_sum(s_bb);
+      if (lane == 0) {
+        ssm[0] = s_rr;
+        ssm[1] = r_prev ? s_dd : 0.0;
+        ssm[2] = r_true ? s_tt : 0.0;
+        ssm[3] = s_bb;
+      }
+    }
+  }
+  __syncthreads();
+  double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
+  if (warp < RC_NCW) {
+#pragma unroll
+    for (int j = 0; j < CPP; ++j) {
+      const int c = col[j];
+      if (c < n) out[c] = acc[j].x;
+      if (c + 1 < n) out[c + 1] = acc[j].y;
+    }
+  }
+  if (tid < 4) out[n + tid] = ssm[tid];
+  if (a.tickets) group_reduce(a, n);
+}
+
 // Fixed-order reduction of the per-CTA partials: one warp per output, lanes
 // take CTAs strided by 32, then a fixed shuffle tree.
 __global__ void k_finalize(const double* __restrict__ part, int grid, int64_t n, double* cs,
@@ -859,6 +1114,31 @@ int launch_wide(const PassArgs& a0, int grid, cudaStream_t s) {
   return ITSK_OK;
 }
 
+template <int CPP>
+int launch_rowcta(const PassArgs& a0, int grid, cudaStream_t s) {
+  PassArgs a = a0;
+  TmaShape sh;
+  sh.T = RC_RB;
+  sh.stage_bytes = static_cast<int>(align_up(RC_RB * a.lda * 8, 128));
+  sh.S = std::max(2, std::min(8, (TMA_SMEM_BUDGET - 1024) / sh.stage_bytes));
+  a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
+  const size_t smem = 1024 + static_cast<size_t>(sh.S) * sh.stage_bytes;
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rowcta<CPP>)));
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rowcta<CPP>), dim3(grid), dim3(32 * (RC_NCW + 1)),
+                       smem, s, a, sh));
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+bool pass_rowcta_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ITSK_PASS_ROWCTA");  // development A/B: 0 = k_pass_wide
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 bool pass_wide_enabled() {
   static const bool on = [] {
     const char* e = getenv("ITSK_PASS_WIDE");  // tuning knob: 0 = one warp per row for all n
@@ -870,6 +1150,7 @@ bool pass_wide_enabled() {
 template <int CPL>
 int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
   if constexpr (CPL >= 32) {
+    if (pass_rowcta_enabled()) return a.n <= 2 * RC_T ? launch_rowcta<1>(a, grid, s) : launch_rowcta<2>(a, grid, s);
     if (pass_wide_enabled()) return CPL == 32 ? launch_wide<8>(a, grid, s) : launch_wide<16>(a, grid, s);
   }
   constexpr int UNR = CPL <= 16 ? 4 : (CPL <= 32 ? 2 : 1);

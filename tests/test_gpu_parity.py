@@ -344,6 +344,48 @@ def test_fused_pass_matches_numpy(pkg, m, n):
     assert got[n + 3] == pytest.approx(b @ b, rel=1e-12)
 
 
+@pytest.mark.parametrize("m,n", [(5003, 513), (4099, 1025), (6001, 2047), (777, 1500), (9, 2000)])
+def test_fused_pass_wide_padded_rows(pkg, m, n):
+    """Wide rows (512 < n <= 2048: the CTA-wide-row kernel) with an odd n
+    stored at an even leading dimension whose pad column holds NaN: the pad
+    must never enter r, c or the norms; batches of 4 rows with a ragged
+    last batch (m not a multiple of 4 per CTA)."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    rng = np.random.default_rng(m * n)
+    lda = n + (n & 1)
+    a = rng.standard_normal((m, n))
+    b = rng.standard_normal(m)
+    x = rng.standard_normal(n)
+    r_prev = rng.standard_normal(m)
+    dev = dv.current_device()
+    store = torch.full((m, lda), float("nan"), dtype=torch.float64, device=dev)
+    store[:, :n] = torch.from_numpy(a).to(dev)
+    bt, xt, rpt = (torch.from_numpy(v).to(dev) for v in (b, x, r_prev))
+    r_out = torch.empty(m, dtype=torch.float64, device=dev)
+    cs = torch.empty(n + 8, dtype=torch.float64, device=dev)
+    lib = dv.lib(dev)
+    nb = ctypes.c_int64()
+    _lib.check(lib.itsk_pass_workspace(m, n, ctypes.byref(nb)))
+    ws = dv.workspace(nb.value, dev)
+    _lib.check(lib.itsk_fused_pass(dv.ptr(store), m, n, lda, dv.ptr(bt), dv.ptr(xt), dv.ptr(rpt), dv.ptr(r_out),
+                                   None, dv.ptr(cs), dv.ptr(ws), ws.numel(), dv.stream_ptr()))
+    torch.cuda.synchronize()
+    r = b - a @ x
+    c = a.T @ r
+    got = cs.cpu().numpy()
+    assert np.isfinite(got[: n + 4]).all() and np.isfinite(r_out.cpu().numpy()).all()
+    np.testing.assert_allclose(r_out.cpu().numpy(), r, rtol=0, atol=1e-13 * np.sqrt(n) * np.abs(a).sum(1).max() * 10)
+    assert np.linalg.norm(got[:n] - c) <= 1e-13 * np.linalg.norm(np.abs(a).T @ np.abs(r)) * 10
+    assert got[n] == pytest.approx(r @ r, rel=1e-12)
+    assert got[n + 1] == pytest.approx((r - r_prev) @ (r - r_prev), rel=1e-12)
+    assert got[n + 2] == 0.0
+    assert got[n + 3] == pytest.approx(b @ b, rel=1e-12)
+
+
 @pytest.mark.parametrize("m,n", [(200000, 200), (40000, 2000), (5000, 50)])
 def test_fused_pass_ws_ready_is_bitwise_stable(pkg, m, n):
     """itsk_pass_workspace_init once, then repeated itsk_fused_pass_ex with
@@ -393,6 +435,22 @@ def _problem(orc, g, name):
     return a, b, truth, cfg
 
 
+# Golden cases held to a different bar than the strict 2x (the measured
+# per-case ratios are in profiles/r2_strict_bar.txt, scripts/strict_bar.py):
+STRICT_EXCEPTIONS = {
+    # zero init is the paper's deliberately unstable "bad_init" baseline
+    # (solvers.py:364-365): its forward-error plateau is set by early rounding
+    # errors; reordering only the reference's own matvec sums moves its FE
+    # 12-40x (1.9e-7 -> 2.3e-6..7.5e-6), so the 2x bar does not apply.  The
+    # same order of magnitude as that spread is required (measured: 22x).
+    "zero_init": ("order_of_magnitude",),
+    # beta = 0: both runs end at the rounding floor (FE 6.5e-15 vs 2.4e-15,
+    # kappa = 1e3, kappa*u = 1.1e-13); a 2x bar on rounding noise below the
+    # floor is not meaningful, the bar is max(2x reference, 10 kappa u).
+    "consistent": ("rounding_floor",),
+}
+
+
 @pytest.mark.parametrize("name", SOLVE_NAMES)
 def test_solve_parity_with_reference(pkg, orc, golden, name):
     g = golden("solves.npz")
@@ -422,37 +480,19 @@ def test_solve_parity_with_reference(pkg, orc, golden, name):
         assert tr.stop_reason == ref_stop
         # rounding moves the stop iteration by a few (survey §8c: C1 24-30 vs 26-29)
         assert abs(res.iterations - ref_iters) <= max(3, 0.15 * ref_iters), (res.iterations, ref_iters)
-    if cfgd.get("init") == "zero":
-        # zero init is the paper's deliberately unstable "bad_init" baseline
-        # (solvers.py:364-365): its forward-error plateau is set by early
-        # rounding errors; reordering only the reference's own matvec sums
-        # moves its FE 12-40x (1.9e-7 -> 2.3e-6..7.5e-6), so the 2x bar does
-        # not apply.  Require the same order of magnitude as that spread.
-        assert tr.fe[-1] <= 50 * fe_ref[-1], (tr.fe[-1], fe_ref[-1])
+    if name in STRICT_EXCEPTIONS:
+        kind = STRICT_EXCEPTIONS[name][0]
+        if kind == "order_of_magnitude":
+            assert tr.fe[-1] <= 50 * fe_ref[-1], (tr.fe[-1], fe_ref[-1])
+        else:  # "rounding_floor": both runs at kappa*u; the bar is the floor
+            floor = 10 * truth.kappa * U
+            assert tr.fe[-1] <= max(2 * fe_ref[-1], floor), (tr.fe[-1], fe_ref[-1], floor)
+            assert tr.re[-1] <= max(2 * re_ref[-1], floor), (tr.re[-1], re_ref[-1], floor)
         return
-    # north_star bar: FE/RE within 2x of the reference's (one-sided).  At a
-    # rounding plateau (C1: FE ~ kappa^2 u beta) the reference's own final FE
-    # jitters 0.1-1.5x under summation reordering, so the comparison level
-    # is max(reference, Householder-QR solve) — the forward-stability yardstick
-    # of the paper and of the reference's acceptance test C01.
-    q, rq = orc.householder_qr_econ(a)
-    x_qr = orc.tri_solve_upper(rq, q.T @ b)
-    fe_qr = orc.forward_error(truth.x, x_qr)
-    re_qr = (np.linalg.norm(truth.r - (b - a @ x_qr)) / truth.beta) if truth.beta > 0 else 0.0
-    if truth.kappa * U >= 1e-3:
-        # kappa u >= 1e-3 (the C3 stress regime, kappa = 1e15): the
-        # reference's own final FE/RE moves ~10x under a mere column
-        # permutation of A (3.5e8 .. 3.8e9 on this case, same algorithm, same
-        # data up to ordering), so one reference run is not a 2x yardstick.
-        # Use the largest of the reference's runs on 3 column orders.
-        for k in range(3):
-            perm = np.random.default_rng(100 + k).permutation(a.shape[1])
-            tp = orc.Truth(x=truth.x[perm], r=truth.r, kappa=truth.kappa, beta=truth.beta)
-            _, trp = orc.iterative_sketching(np.ascontiguousarray(a[:, perm]), b, orc.Config(**cfgd), tp)
-            fe_qr = max(fe_qr, trp.fe[-1])
-            re_qr = max(re_qr, trp.re[-1])
-    assert tr.fe[-1] <= 2 * max(fe_ref[-1], fe_qr) + 4 * U, (tr.fe[-1], fe_ref[-1], fe_qr)
-    assert tr.re[-1] <= 2 * max(re_ref[-1], re_qr) + 4 * U, (tr.re[-1], re_ref[-1], re_qr)
+    # the north-star bar, strict: FE and RE within 2x of the reference's own
+    # final values (one-sided; + a few u of absolute slack for u-level errors)
+    assert tr.fe[-1] <= 2 * fe_ref[-1] + 4 * U, (tr.fe[-1], fe_ref[-1])
+    assert tr.re[-1] <= 2 * re_ref[-1] + 4 * U, (tr.re[-1], re_ref[-1])
     if len(g[f"{name}_be"]):
         assert tr.be[-1] <= 2 * g[f"{name}_be"][-1] + 4 * U
     x_ref = g[f"{name}_solution"]
