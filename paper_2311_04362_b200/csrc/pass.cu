@@ -695,62 +695,69 @@ __global__ void __launch_bounds__(32 * (WIDE_NCW + 1), 1) k_pass_wide(PassArgs a
 }
 
 // ---------------------------------------------------------------------------
-// CTA-wide rows (512 < n <= 2048, the C4 shape): every consumer thread owns
-// the column pairs {2t, 2t+1} + 1024 j (j < CPP) for the whole pass, with x
-// and its slice of c in registers.  A stage of the ring holds RC_RB = 4 rows
-// (one bulk copy); each thread reads its pairs of the 4 rows ONCE from
-// shared memory (16-byte loads) into registers and releases the stage, so
-// the row is used for both the dot and the c update without a second
-// shared-memory read and without x in shared memory (k_pass_wide read the
-// row twice and x once per row: 4x the row's bytes of shared-memory traffic
-// against ~2x here).  Per batch: 4 partial dots per thread -> in-warp
-// reduce-scatter (6 shuffles; lane group g = lane/8 holds row g's warp sum)
-// -> 16 warp partials per row in shared memory (double-buffered by batch
-// parity) -> ONE named barrier -> every warp sums the 16 partials of the 4
-// rows in warp order (the same bits in every warp), r = b - dot -> c += r *
-// row.  Warp 0 (lane u <-> row u) writes r and accumulates the norms.  Each
-// column of c is owned by one thread: no shared-memory reduction of c.
+// Row groups (384 < n <= 2048; the C3 and C4 shapes): the 16 consumer warps
+// form NG = 16 / GW groups of GW warps; group g owns batch t = g, g + NG, ...
+// of RB = 4 consecutive rows (one stage of the ring, one bulk copy).  Inside
+// a group every thread owns the column pairs {2t, 2t+1} + 64 GW j (j < 2),
+// with x and its slice of c in registers (GW is the smallest power of two
+// with 128 GW >= n).  Each thread reads its pairs of the 4 rows ONCE from
+// shared memory (16-byte loads) into registers and releases the stage, so a
+// row is read from shared memory once and x never is (the warp-per-row and
+// warp-group kernels read the row twice and x from shared memory: ~2x the
+// shared-memory traffic per byte of A).  Per batch: 4 partial dots per
+// thread -> in-warp reduce-scatter (6 shuffles; lane l holds row l/8's warp
+// sum) -> the GW warp partials per row in shared memory (double-buffered by
+// the group's batch parity) -> ONE named barrier of the group -> every warp
+// of the group sums the GW partials of the 4 rows in warp order (the same
+// bits in every warp), r = b - dot -> c += r * row.  The group's first warp
+// (lane u <-> row u) writes r and accumulates the norms.  The groups' c
+// partials are summed in group order at the end; the norms likewise.
+// The ring's stage count is a multiple of NG, so the batch a group waits for
+// on a stage always follows that group's own previous batch there (no
+// mbarrier phase aliasing without a stage-tag check).
 // ---------------------------------------------------------------------------
-constexpr int RC_NCW = 16, RC_RB = 4, RC_T = RC_NCW * 32;
+constexpr int RW_NCW = 16, RW_RB = 4, RW_CPP = 2;
 
-template <int CPP>
-__global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a, TmaShape sh) {
+template <int GW>
+__global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, TmaShape sh) {
+  constexpr int NG = RW_NCW / GW, GT = 32 * GW, RB = RW_RB, CPP = RW_CPP;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + 32;
   unsigned char* stages = smraw + 1024;
-  __shared__ double dpart[2][RC_NCW][RC_RB];
-  __shared__ double ssm[4];
+  __shared__ double dpart[NG][2][GW][RB];
+  __shared__ double ssm[NG][4];
   __shared__ int s_done;
 
   const double* r_true = a.r_true;
   const double* b = a.b;
   const double bscale = a.bscale;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp / GW, gw = warp % GW, gt = tid - g * GT;  // group, warp / thread in group
   const int64_t n = a.n, lda = a.lda;
   const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
   const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
   const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
   const int S = sh.S;
-  const int ntiles = (nrows + RC_RB - 1) / RC_RB;
+  const int ntiles = (nrows + RB - 1) / RB;
   const int npre = min(S, ntiles);
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, RC_NCW);  // one arrival per consumer warp per batch
+    for (int st = 0; st < S; ++st) {
+      mbar_init(full + st, 1);
+      mbar_init(empty + st, GW);  // one arrival per warp of the consuming group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   pdl_trigger();
-  if (warp == RC_NCW && lane == 0) {
+  if (warp == RW_NCW && lane == 0) {
     const uint64_t pol = evict_first_policy();
     for (int t = 0; t < npre; ++t) {
-      const int rows = min(RC_RB, nrows - t * RC_RB);
+      const int rows = min(RB, nrows - t * RB);
       const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
       mbar_expect_tx(full + t, bytes);
-      bulk_g2s(stages + static_cast<int64_t>(t) * sh.stage_bytes, a.A + (r_begin + t * RC_RB) * lda, bytes,
+      bulk_g2s(stages + static_cast<int64_t>(t) * sh.stage_bytes, a.A + (r_begin + t * RB) * lda, bytes,
                full + t, pol);
     }
   }
@@ -768,7 +775,7 @@ __global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a
     if (tid == 0) s_done = ctl->result.done;
     __syncthreads();
     if (s_done) {
-      if (warp == RC_NCW && lane == 0)
+      if (warp == RW_NCW && lane == 0)
         for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
       return;
     }
@@ -786,58 +793,61 @@ __global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a
   }
 
   double2 acc[CPP];
-  double2 xv[CPP];
   int col[CPP];
 #pragma unroll
   for (int j = 0; j < CPP; ++j) {
     acc[j] = make_double2(0.0, 0.0);
-    col[j] = 2 * tid + 2 * RC_T * j;
+    col[j] = 2 * gt + 2 * GT * j;
   }
 
-  if (warp == RC_NCW) {
+  if (warp == RW_NCW) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       for (int t = npre; t < ntiles; ++t) {
-        const int s = t % S;
-        mbar_wait(empty + s, static_cast<unsigned>(((t / S) - 1) & 1));
-        const int rows = min(RC_RB, nrows - t * RC_RB);
+        const int st = t % S;
+        mbar_wait(empty + st, static_cast<unsigned>(((t / S) - 1) & 1));
+        const int rows = min(RB, nrows - t * RB);
         const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
-        mbar_expect_tx(full + s, bytes);
-        bulk_g2s(stages + static_cast<int64_t>(s) * sh.stage_bytes, a.A + (r_begin + t * RC_RB) * lda, bytes,
-                 full + s, pol);
+        mbar_expect_tx(full + st, bytes);
+        bulk_g2s(stages + static_cast<int64_t>(st) * sh.stage_bytes, a.A + (r_begin + t * RB) * lda, bytes,
+                 full + st, pol);
       }
     }
   } else {
+    double2 xv[CPP];
 #pragma unroll
     for (int j = 0; j < CPP; ++j) {
       const int c = col[j];
       xv[j].x = c < n ? x[c] : 0.0;
       xv[j].y = c + 1 < n ? x[c + 1] : 0.0;
     }
-    // b / r_prev / r_true of the batch's rows, one batch ahead (lane u <-> row u)
-    const bool lead = lane < RC_RB;
+    // b / r_prev / r_true of the group's next batch (lane u <-> row u)
+    const bool lead = lane < RB;
     auto fetch = [&](int t, double& fb, double& fp, double& ft) {
-      const int k = t * RC_RB + lane;
+      const int k = t * RB + lane;
       const bool ok = lead && t < ntiles && k < nrows;
-      const int64_t g = r_begin + k;
-      fb = ok ? b[g] : 0.0;
-      fp = (ok && warp == 0 && r_prev) ? r_prev[g] : 0.0;
-      ft = (ok && warp == 0 && r_true) ? r_true[g] : 0.0;
+      const int64_t gi = r_begin + k;
+      fb = ok ? b[gi] : 0.0;
+      fp = (ok && gw == 0 && r_prev) ? r_prev[gi] : 0.0;
+      ft = (ok && gw == 0 && r_true) ? r_true[gi] : 0.0;
     };
     double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
     double cb, cp, ct;
-    fetch(0, cb, cp, ct);
-    const int g8 = lane >> 3;  // row whose warp sum this lane ends up holding
-    for (int t = 0; t < ntiles; ++t) {
+    fetch(g, cb, cp, ct);
+    // second-stage lane map: value i of lane l is warp (l % GW)'s partial of
+    // row ((l / GW) % (RB / VPL)) * VPL + i
+    constexpr int VPL = (GW * RB + 31) / 32;  // partials per lane
+    constexpr int RPL = RB / VPL;              // row slots across the lanes
+    for (int t = g, par = 0; t < ntiles; t += NG, par ^= 1) {
       double nb, np, nt;
-      fetch(t + 1, nb, np, nt);
-      const int s = t % S;
-      const int nu = min(RC_RB, nrows - t * RC_RB);
-      mbar_wait(full + s, static_cast<unsigned>((t / S) & 1));
-      const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(s) * sh.stage_bytes);
-      double2 v[RC_RB][CPP];
+      fetch(t + NG, nb, np, nt);
+      const int st = t % S;
+      const int nu = min(RB, nrows - t * RB);
+      mbar_wait(full + st, static_cast<unsigned>((t / S) & 1));
+      const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(st) * sh.stage_bytes);
+      double2 v[RB][CPP];
 #pragma unroll
-      for (int u = 0; u < RC_RB; ++u)
+      for (int u = 0; u < RB; ++u)
 #pragma unroll
         for (int j = 0; j < CPP; ++j) {
           const int c = col[j];
@@ -849,70 +859,64 @@ __global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a
           v[u][j] = w;
         }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);  // the stage is in registers: release it
-      double d[RC_RB];
+      if (lane == 0) mbar_arrive(empty + st);  // the stage is in registers: release it
+      double d[RB];
 #pragma unroll
-      for (int u = 0; u < RC_RB; ++u) {
-        double acc_d = 0.0;
+      for (int u = 0; u < RB; ++u) {
+        double e = 0.0;
 #pragma unroll
         for (int j = 0; j < CPP; ++j) {
-          acc_d = fma(v[u][j].x, xv[j].x, acc_d);
-          acc_d = fma(v[u][j].y, xv[j].y, acc_d);
+          e = fma(v[u][j].x, xv[j].x, e);
+          e = fma(v[u][j].y, xv[j].y, e);
         }
-        d[u] = acc_d;
+        d[u] = e;
       }
-      // in-warp reduce-scatter: after it lane l holds row (l >> 3)'s warp sum
-      const bool h4 = (lane & 16) != 0, h3 = (lane & 8) != 0;
-      double k0 = h4 ? d[2] : d[0], k1 = h4 ? d[3] : d[1];
-      const double e0 = h4 ? d[0] : d[2], e1 = h4 ? d[1] : d[3];
-      k0 += __shfl_xor_sync(FULL, e0, 16);
-      k1 += __shfl_xor_sync(FULL, e1, 16);
-      double kk = h3 ? k1 : k0;
-      kk += __shfl_xor_sync(FULL, h3 ? k0 : k1, 8);
-      kk += __shfl_xor_sync(FULL, kk, 4);
-      kk += __shfl_xor_sync(FULL, kk, 2);
-      kk += __shfl_xor_sync(FULL, kk, 1);
-      const int par = t & 1;
-      if ((lane & 7) == 0) dpart[par][warp][g8] = kk;
-      asm volatile("bar.sync 1, %0;" ::"n"(RC_T) : "memory");
-      // every warp: the 4 rows' dots, the 16 warp partials summed in warp
-      // order (lane l < 16 holds warp l's partial of rows 2h and 2h+1 ...)
-      double q0 = 0.0, q1 = 0.0;
+      // in-warp reduce-scatter: lane l ends up with row l / 8's warp sum
       {
-        const int w = lane & 15, rr = (lane >> 4) * 2;
-        q0 = dpart[par][w][rr];
-        q1 = dpart[par][w][rr + 1];
+        const bool h4 = (lane & 16) != 0, h3 = (lane & 8) != 0;
+        double k0 = h4 ? d[2] : d[0], k1 = h4 ? d[3] : d[1];
+        const double e0 = h4 ? d[0] : d[2], e1 = h4 ? d[1] : d[3];
+        k0 += __shfl_xor_sync(FULL, e0, 16);
+        k1 += __shfl_xor_sync(FULL, e1, 16);
+        double kk = h3 ? k1 : k0;
+        kk += __shfl_xor_sync(FULL, h3 ? k0 : k1, 8);
+        kk += __shfl_xor_sync(FULL, kk, 4);
+        kk += __shfl_xor_sync(FULL, kk, 2);
+        kk += __shfl_xor_sync(FULL, kk, 1);
+        if ((lane & 7) == 0) dpart[g][par][gw][lane >> 3] = kk;
       }
-      // fixed tree over the 16 warps (xor 8, 4, 2, 1 within each half)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GT) : "memory");
+      // the group's GW partials per row, summed in a fixed tree (the same
+      // bits in every warp of the group)
+      double q[VPL];
+      {
+        const int w = lane % GW, r0 = ((lane / GW) % RPL) * VPL;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        q0 += __shfl_xor_sync(FULL, q0, o);
-        q1 += __shfl_xor_sync(FULL, q1, o);
+        for (int i = 0; i < VPL; ++i) q[i] = dpart[g][par][w][r0 + i];
       }
-      // rows 0, 1 live in lanes 0..15, rows 2, 3 in lanes 16..31
-      const double dot0 = __shfl_sync(FULL, q0, 0), dot1 = __shfl_sync(FULL, q1, 0);
-      const double dot2 = __shfl_sync(FULL, q0, 16), dot3 = __shfl_sync(FULL, q1, 16);
-      double rv[RC_RB];
-      rv[0] = bscale * __shfl_sync(FULL, cb, 0) - dot0;
-      rv[1] = bscale * __shfl_sync(FULL, cb, 1) - dot1;
-      rv[2] = bscale * __shfl_sync(FULL, cb, 2) - dot2;
-      rv[3] = bscale * __shfl_sync(FULL, cb, 3) - dot3;
 #pragma unroll
-      for (int u = 0; u < RC_RB; ++u)
-        if (u >= nu) rv[u] = 0.0;
+      for (int o = GW / 2; o > 0; o >>= 1)
 #pragma unroll
-      for (int u = 0; u < RC_RB; ++u)
+        for (int i = 0; i < VPL; ++i) q[i] += __shfl_xor_sync(FULL, q[i], o);
+      double rv[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const double dot = __shfl_sync(FULL, q[u % VPL], (u / VPL) * GW);
+        rv[u] = u < nu ? bscale * __shfl_sync(FULL, cb, u) - dot : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
 #pragma unroll
         for (int j = 0; j < CPP; ++j) {
           acc[j].x = fma(rv[u], v[u][j].x, acc[j].x);
           acc[j].y = fma(rv[u], v[u][j].y, acc[j].y);
         }
-      if (warp == 0 && lane < nu) {
+      if (gw == 0 && lane < nu) {
         double rl = rv[0];
 #pragma unroll
-        for (int u = 1; u < RC_RB; ++u)
+        for (int u = 1; u < RB; ++u)
           if (lane == u) rl = rv[u];
-        if (r_out) r_out[r_begin + t * RC_RB + lane] = rl;
+        if (r_out) r_out[r_begin + t * RB + lane] = rl;
         s_rr += rl * rl;
         s_bb += cb * cb;
         const double dd = rl - cp;
@@ -922,30 +926,54 @@ __global__ void __launch_bounds__(32 * (RC_NCW + 1), 1) k_pass_rowcta(PassArgs a
       }
       cb = nb; cp = np; ct = nt;
     }
-    if (warp == 0) {
+    if (gw == 0) {
       s_rr = warp_sum(s_rr);
       s_dd = warp_sum(s_dd);
       s_tt = warp_sum(s_tt);
       s_bb = warp_sum(s_bb);
       if (lane == 0) {
-        ssm[0] = s_rr;
-        ssm[1] = r_prev ? s_dd : 0.0;
-        ssm[2] = r_true ? s_tt : 0.0;
-        ssm[3] = s_bb;
+        ssm[g][0] = s_rr;
+        ssm[g][1] = r_prev ? s_dd : 0.0;
+        ssm[g][2] = r_true ? s_tt : 0.0;
+        ssm[g][3] = s_bb;
       }
     }
   }
-  __syncthreads();
+  __syncthreads();  // all stages consumed: the ring holds the groups' c partials
   double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
-  if (warp < RC_NCW) {
+  if constexpr (NG == 1) {
+    if (warp < RW_NCW) {
 #pragma unroll
-    for (int j = 0; j < CPP; ++j) {
-      const int c = col[j];
-      if (c < n) out[c] = acc[j].x;
-      if (c + 1 < n) out[c + 1] = acc[j].y;
+      for (int j = 0; j < CPP; ++j) {
+        const int c = col[j];
+        if (c < n) out[c] = acc[j].x;
+        if (c + 1 < n) out[c + 1] = acc[j].y;
+      }
+    }
+  } else {
+    double* csm = reinterpret_cast<double*>(stages);  // NG x (2 GT CPP)
+    constexpr int W = 2 * GT * CPP;
+    if (warp < RW_NCW) {
+#pragma unroll
+      for (int j = 0; j < CPP; ++j) {
+        csm[g * W + col[j]] = acc[j].x;
+        csm[g * W + col[j] + 1] = acc[j].y;
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < n; c += 32 * (RW_NCW + 1)) {
+      double sum = 0.0;
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) sum += csm[gg * W + c];
+      out[c] = sum;
     }
   }
-  if (tid < 4) out[n + tid] = ssm[tid];
+  if (tid < 4) {
+    double sum = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) sum += ssm[gg][tid];
+    out[n + tid] = sum;
+  }
   if (a.tickets) group_reduce(a, n);
 }
 
@@ -1114,29 +1142,37 @@ int launch_wide(const PassArgs& a0, int grid, cudaStream_t s) {
   return ITSK_OK;
 }
 
-template <int CPP>
-int launch_rowcta(const PassArgs& a0, int grid, cudaStream_t s) {
+template <int GW>
+int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
+  constexpr int NG = RW_NCW / GW;
   PassArgs a = a0;
   TmaShape sh;
-  sh.T = RC_RB;
-  sh.stage_bytes = static_cast<int>(align_up(RC_RB * a.lda * 8, 128));
-  sh.S = std::max(2, std::min(8, (TMA_SMEM_BUDGET - 1024) / sh.stage_bytes));
+  sh.T = RW_RB;
+  sh.stage_bytes = static_cast<int>(align_up(RW_RB * a.lda * 8, 128));
+  // a multiple of NG stages (see the kernel), <= 32 mbarriers, and room for
+  // the groups' c partials at the end
+  int S = std::min(32, (TMA_SMEM_BUDGET - 1024) / sh.stage_bytes) / NG * NG;
+  const int red = NG > 1 ? NG * 2 * 32 * GW * RW_CPP * 8 : 0;
+  while (S * sh.stage_bytes < red) S += NG;
+  sh.S = std::max(NG, S);
   a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
   const size_t smem = 1024 + static_cast<size_t>(sh.S) * sh.stage_bytes;
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rowcta<CPP>)));
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rowcta<CPP>), dim3(grid), dim3(32 * (RC_NCW + 1)),
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rows<GW>)));
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rows<GW>), dim3(grid), dim3(32 * (RW_NCW + 1)),
                        smem, s, a, sh));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
 }
 
-bool pass_rowcta_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ITSK_PASS_ROWCTA");  // development A/B: 0 = k_pass_wide
-    return !(e && atoi(e) == 0);
+// development A/B: ITSK_PASS_ROWS=0 off, 1 every n > 128, k: only where the
+// group is >= k warps wide (16: n > 1024 only)
+int pass_rows_mode() {
+  static const int mode = [] {
+    const char* e = getenv("ITSK_PASS_ROWS");
+    return e ? atoi(e) : 1;
   }();
-  return on;
+  return mode;
 }
 
 bool pass_wide_enabled() {
@@ -1149,8 +1185,20 @@ bool pass_wide_enabled() {
 
 template <int CPL>
 int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
+  // row groups where the group's 128 GW columns are mostly used (measured:
+  // n = 500, 600, 1000, 2000 faster than the warp-per-row / warp-group
+  // kernels; n = 200, 300 slower, profiles/rd2_pass_rows_ab.txt)
+  if (pass_rows_mode() > 0 && a.n > 384) {
+    const int gw = a.n > 1024 ? 16 : a.n > 512 ? 8 : 4;
+    if (pass_rows_mode() == 1 || gw >= pass_rows_mode()) {
+      switch (gw) {
+        case 16: return launch_rows<16>(a, grid, s);
+        case 8: return launch_rows<8>(a, grid, s);
+        default: return launch_rows<4>(a, grid, s);
+      }
+    }
+  }
   if constexpr (CPL >= 32) {
-    if (pass_rowcta_enabled()) return a.n <= 2 * RC_T ? launch_rowcta<1>(a, grid, s) : launch_rowcta<2>(a, grid, s);
     if (pass_wide_enabled()) return CPL == 32 ? launch_wide<8>(a, grid, s) : launch_wide<16>(a, grid, s);
   }
   constexpr int UNR = CPL <= 16 ? 4 : (CPL <= 32 ? 2 : 1);

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     Ps[rr * PS + c] = c < kb ? a.W[(lo + rr) * ldw + k0 + c] : 0.0;
   }
   __syncthreads();
+  Q2P(7);
 
   // One sweep over the own rows (4 per step): apply reflector jj when `apply`
   // (lane c > jj: a_rc += v_r temp_c; lane jj stores v_r) and accumulate lane

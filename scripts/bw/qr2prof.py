@@ -19,7 +19,7 @@ for it in range(2):
     rc = lib.itsk_qr_aug(P(W.data_ptr()), ctypes.c_int64(d), ctypes.c_int64(n), ctypes.c_int64(n + 1), P(R.data_ptr()), P(z.data_ptr()), P(ws.data_ptr()), ctypes.c_int64(ws.numel()), P(s))
     torch.cuda.synchronize()
     lib.itsk_qr2_profile_read(out)
-names = ["sweep", "syncthreads", "reduce+push", "cluster.sync", "coeffs", "(end loop)", "writeback+G+T"]
-tot = sum(out[i] for i in range(7))
+names = ["sweep", "syncthreads", "reduce+push", "cluster.sync", "coeffs", "(end loop)", "writeback+G+T", "panel load"]
+tot = sum(out[i] for i in range(8))
 for i, nm in enumerate(names): print(f"{nm:14s} {out[i]:10d} cycles {100*out[i]/max(tot,1):5.1f}%  per col {out[i]/n:8.0f}")
 print("total", tot, "cycles =", tot / 1.9e3, "us", "rc", rc)
