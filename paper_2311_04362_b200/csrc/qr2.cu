@@ -40,8 +40,9 @@ constexpr int QP_WARPS = QP_THREADS / 32;
 constexpr int UT = 64;        // update tile: 64 columns (and 64 rows in k_qr_apply)
 constexpr int UTP = UT + 4;   // padded stride
 constexpr int YRT = 32;       // row chunk of k_qr_y
-constexpr int MAX_SPLIT = 16; // row splits of k_qr_y (partials summed by k_qr_z)
+constexpr int MAX_SPLIT = 48; // row splits of k_qr_y (partials summed by k_qr_z)
 constexpr int MAX_C = 16;     // cluster size bound
+constexpr int QP_RPT = 4;     // panel rows per thread bound (rows per CTA <= QP_RPT * QP_THREADS)
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
 __device__ __forceinline__ int64_t lo_of(int q, int P, int64_t len) {
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   double* red = inbox + 2 * C * REC; // QP_WARPS x NB
   double* taus = red + QP_WARPS * NB;
   double* betl = taus + NB;
+  double* gbuf = betl + NB;  // (16 / (NB/8)^2) x NB x NB: G's row-split partials
   __shared__ int bnd[MAX_C + 1];  // row split of [k0, d) relative to k0 (no 64-bit divides later)
   __shared__ __align__(8) uint64_t mb[2];  // record arrivals, one mbarrier per inbox parity
   if (tid <= C) bnd[tid] = static_cast<int>(lo_of(tid, C, len));
@@ -148,18 +150,142 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   }
   const int cl_lane = lane < NB ? lane : NB - 1;  // NB = 16: upper half-warp mirrors
 
+  // the panel's rows, all loads in flight (zero-filled past kb)
   for (int idx = tid; idx < h * NB; idx += QP_THREADS) {
     const int rr = idx / NB, c = idx - rr * NB;
-    Ps[rr * PS + c] = c < kb ? a.W[(lo + rr) * ldw + k0 + c] : 0.0;
+    const bool ok = c < kb;
+    cp_async8(Ps + rr * PS + c, a.W + (ok ? (lo + rr) * ldw + k0 + c : 0), ok);
   }
+  cp_commit();
+  cp_wait<0>();
   __syncthreads();
   Q2P(7);
 
+  // NB = 16 (the C4 shape, ~1500 rows per CTA): one sweep per column,
+  // thread per row (rows tid, tid + 512, ...: a whole
+  // row in one thread, no shuffles in the sweep): apply reflector jj
+  // (row[c] += v_r temp_c for c > jj, v_r = row[jj] scal below the pivot, 1
+  // on it) and accumulate the partial sums sum_{r > jj+1} a_{r,jj+1} a_{r,c}
+  // of the next column in registers; a reduce-scatter across the warp puts
+  // column c's warp sum in one lane (fixed order) -> red[warp][c].  Column
+  // jj's v values are written back at the next sweep (every thread of the
+  // CTA reads row[jj] in this one).  Only columns > jj are read or written.
+  const int nrow_iter = (h + QP_THREADS - 1) / QP_THREADS;
+  double vsave[QP_RPT];
+  int vcol = -1;
+  auto flush_v = [&]() {
+    if (vcol < 0) return;
+#pragma unroll
+    for (int k = 0; k < QP_RPT; ++k) {
+      const int r = tid + k * QP_THREADS;
+      if (k < nrow_iter && r < h && lo + r > k0 + vcol) Ps[r * PS + vcol] = vsave[k];
+    }
+    vcol = -1;
+  };
+  __shared__ double s_temp[32];  // temp_c of the current reflector (lanes of warp 0 write it)
+  auto sweep_t = [&](int jj, bool apply, double scal) {
+    const int jn = jj + 1;
+    const int jnc = jn < NB ? jn : 0;
+    flush_v();
+    double p[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) p[c] = 0.0;
+    const int64_t jg = k0 + jj;
+#pragma unroll
+    for (int k = 0; k < QP_RPT; ++k) {
+      const int r = tid + k * QP_THREADS;
+      if (k >= nrow_iter || r >= h) break;
+      const int64_t rg = lo + r;
+      if (rg < jg) continue;  // rows above the pivot: final rows of R
+      double* row = Ps + r * PS;
+      const bool part = rg > jg + 1;  // below the next pivot
+      double v = 1.0;
+      if (apply && rg > jg) {
+        v = row[jj] * scal;
+        vsave[k] = v;
+      }
+      double xn = 0.0;
+      if (jn < kb) {
+        xn = row[jnc];
+        if (apply) {
+          xn = fma(v, s_temp[jnc], xn);
+          row[jnc] = xn;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c < jn || c >= kb) continue;
+        double x = xn;
+        if (c != jn) {
+          x = row[c];
+          if (apply) {
+            x = fma(v, s_temp[c], x);
+            row[c] = x;
+          }
+        }
+        if (part) p[c] = fma(xn, x, p[c]);
+      }
+    }
+    if (apply) vcol = jj;
+    Q2P(0);
+    if (jn >= kb) return;  // last column: no record to exchange
+    // reduce-scatter of p[0..NB) over the warp: halving steps at lane offsets
+    // 16, 8, ... (NB = 32: lane l ends with column l; NB = 16: lanes 2c and
+    // 2c+1 with column c), one fixed order for every column
+    {
+#pragma unroll
+      for (int st = 0; (16 >> st) >= 32 / NB; ++st) {
+        const int o = 16 >> st, half = NB >> (st + 1);
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int i2 = 0; i2 < half; ++i2) {
+          const double keep = hi ? p[half + i2] : p[i2];
+          const double send = hi ? p[i2] : p[half + i2];
+          p[i2] = keep + __shfl_xor_sync(FULL, send, o);
+        }
+      }
+#pragma unroll
+      for (int o = 32 / NB / 2; o > 0; o >>= 1) p[0] += __shfl_xor_sync(FULL, p[0], o);
+      if ((lane & (32 / NB - 1)) == 0) red[warp * NB + lane / (32 / NB)] = p[0];
+    }
+    __syncthreads();
+    Q2P(1);
+    const int buf = jn & 1;
+    if (tid == 0)  // this CTA expects C records of (kb - jn) sums plus the owner's row
+      mbar_expect_tx(&mb[buf], static_cast<unsigned>((C + 1) * (kb - jn) * 8));
+    if (warp < C) {  // warp w delivers this CTA's record to CTA w
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (lane < kb) {
+#pragma unroll
+        for (int w = 0; w < QP_WARPS; w += 4) {
+          s0 += red[w * NB + cl_lane];
+          s1 += red[(w + 1) * NB + cl_lane];
+          s2 += red[(w + 2) * NB + cl_lane];
+          s3 += red[(w + 3) * NB + cl_lane];
+        }
+      }
+      const int64_t jrn = k0 + jn;
+      const bool own_next = jrn >= lo && jrn < hi;
+      if (lane >= jn && lane < kb) {
+        const uint32_t ib = mapa_u32(smem_u32(inbox + (buf * C + q) * REC + lane), warp);
+        const uint32_t rb = mapa_u32(smem_u32(&mb[buf]), warp);
+        st_async_f64(ib, (s0 + s1) + (s2 + s3), rb);
+        if (own_next) st_async_f64(ib + NB * 8, Ps[(jrn - lo) * PS + lane], rb);
+      }
+    }
+    Q2P(2);
+    mbar_wait_cluster(&mb[buf], static_cast<unsigned>((jn >> 1) & 1));
+    Q2P(3);
+  };
+
+  // NB = 32 (C2 / C3 shapes, <= ~600 rows per CTA): warp per row, lane per
+  // column — measured faster there than thread per row (a 32-wide row in one
+  // thread leaves half the threads idle and serialises the columns).
   // One sweep over the own rows (4 per step): apply reflector jj when `apply`
   // (lane c > jj: a_rc += v_r temp_c; lane jj stores v_r) and accumulate lane
   // c's partial sum_{r > j+1} a_{r,jj+1} a_{r,c} for the next column; then
   // every CTA's record goes to every inbox and the cluster synchronises.
-  auto sweep = [&](int jj, bool apply, double scal, double temp) {
+  auto sweep_w = [&](int jj, bool apply, double scal, double temp) {
     const int jn = jj + 1;
     const int jl = static_cast<int>(k0 + jj - lo);  // local index of row j (may be outside [0,h))
     const int jnl = jl + 1;
@@ -265,7 +391,8 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   };
 
   cl.sync();  // bnd, and every CTA's mbarriers initialised before any remote transaction
-  sweep(-1, false, 0.0, 0.0);  // partial sums of column 0
+  if constexpr (NB == 16) sweep_t(-1, false, 0.0);  // partial sums of column 0
+  else sweep_w(-1, false, 0.0, 0.0);
   int own = 0;
   for (int jj = 0; jj < kb; ++jj) {
     const int buf = jj & 1;
@@ -274,7 +401,6 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     // publishes tau, scal and temp_c; the other warps wait at the barrier
     // (sixteen redundant copies of the sqrt/divide chain were slower)
     __shared__ double s_coef[2];
-    __shared__ double s_temp[32];
     if (warp == 0) {
       double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
       const double* ib = inbox + buf * C * REC + cl_lane;
@@ -309,10 +435,11 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
     }
     __syncthreads();
     const double tau = s_coef[0], scal = s_coef[1];
-    const double temp = s_temp[lane];
     Q2P(4);
-    sweep(jj, tau != 0.0, scal, temp);
+    if constexpr (NB == 16) sweep_t(jj, tau != 0.0, scal);
+    else sweep_w(jj, tau != 0.0, scal, s_temp[lane]);
   }
+  flush_v();
   __syncthreads();
   Q2P(5);
   // write the panel back (R rows above the diagonal, v below), betas, taus
@@ -325,27 +452,46 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
       a.betas[k0 + c] = betl[c];
       a.taus[k0 + c] = taus[c];
     }
-  // G_q = V_own' V_own on DMMA tiles (one 8x8 tile per warp), to global
-  constexpr int GT = NB / 8;
-  const int g4 = lane >> 2, t4 = lane & 3;
-  if (warp < GT * GT) {
-    const int mt = warp / GT, nt = warp - mt * GT;
+  // G_q = V_own' V_own on DMMA tiles, to global: NT = (NB/8)^2 tiles, each
+  // over KS = 16 / NT row splits (every warp busy; 4 interleaved chains per
+  // warp), the splits summed in a fixed order through shared memory
+  {
+    constexpr int GT = NB / 8, NT = GT * GT, KS = QP_WARPS / NT;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int tile = warp % NT, ks = warp / NT;
+    const int mt = tile / GT, nt = tile - mt * GT;
     const int ci = mt * 8 + g4, ck = nt * 8 + g4;
-    // 4 interleaved DMMA chains (a dependent DMMA costs ~300 cycles)
+    const int groups = (h + 3) / 4;
+    const int gb0 = (ks * groups) / KS * 4, gb1 = min(h, ((ks + 1) * groups) / KS * 4);
     double e0[4] = {0.0, 0.0, 0.0, 0.0}, e1[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int r0 = 0; r0 < h; r0 += 16) {
+    for (int r0 = gb0; r0 < gb1; r0 += 16) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r0 + 4 * u + t4;
-        const bool ok = r < h;
+        const bool ok = r < gb1;
         const double av = ok ? vval(Ps[r * PS + ci], lo + r, k0, ci) : 0.0;
         const double bv = ok ? vval(Ps[r * PS + ck], lo + r, k0, ck) : 0.0;
         dmma(e0[u], e1[u], av, bv);
       }
     }
+    const double g0 = (e0[0] + e0[1]) + (e0[2] + e0[3]);
+    const double g1 = (e1[0] + e1[1]) + (e1[2] + e1[3]);
     double* gp = a.Gp + static_cast<int64_t>(q) * NB * NB;
-    gp[ci * NB + nt * 8 + 2 * t4] = (e0[0] + e0[1]) + (e0[2] + e0[3]);
-    gp[ci * NB + nt * 8 + 2 * t4 + 1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
+    if constexpr (KS == 1) {
+      gp[ci * NB + nt * 8 + 2 * t4] = g0;
+      gp[ci * NB + nt * 8 + 2 * t4 + 1] = g1;
+    } else {
+      double* gb = gbuf + ks * NB * NB;
+      gb[ci * NB + nt * 8 + 2 * t4] = g0;
+      gb[ci * NB + nt * 8 + 2 * t4 + 1] = g1;
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += QP_THREADS) {
+        double sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) sum += gbuf[k * NB * NB + e];
+        gp[e] = sum;
+      }
+    }
   }
   cl.sync();
   // G = sum_t G_t in rank order; element e summed by CTA e % C (all C
@@ -756,18 +902,26 @@ bool lookahead_enabled() {
   return on;
 }
 
-int side_stream(cudaStream_t* out) {
-  static cudaStream_t st[64] = {};
+// Side streams (per device, created once): 0 = the look-ahead's rest of the
+// trailing matrix, 1 = the far updates, 2 = the critical path (panels, their
+// block updates, the next block's far update) at the highest priority, so
+// the panel chain's CTAs are scheduled ahead of the overlapping far GEMMs.
+int side_stream(cudaStream_t* out, int which = 0) {
+  static cudaStream_t st[64][3] = {};
   int dev = 0;
   ITSK_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) return ITSK_EINVAL;
-  if (!st[dev]) ITSK_CUDA(cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking));
-  *out = st[dev];
+  if (dev < 0 || dev >= 64 || which < 0 || which > 2) return ITSK_EINVAL;
+  if (!st[dev][which]) {
+    int lo = 0, hi = 0;
+    ITSK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ITSK_CUDA(cudaStreamCreateWithPriority(&st[dev][which], cudaStreamNonBlocking, which == 2 ? hi : lo));
+  }
+  *out = st[dev][which];
   return ITSK_OK;
 }
 
 cudaError_t pooled_event(int which, cudaEvent_t* out) {
-  static cudaEvent_t ev[64][2] = {};
+  static cudaEvent_t ev[64][6] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -800,8 +954,9 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
   p.hmax = (d + p.C - 1) / p.C + 1;
   const int64_t N = n + 1;
   for (int nb : {32, 16}) {
-    const int64_t doubles = p.hmax * (nb + 1) + 2 * p.C * 2 * nb + QP_WARPS * nb + 2 * nb;
-    if (doubles * 8 <= 220 * 1024) {
+    const int ks = QP_WARPS / ((nb / 8) * (nb / 8));
+    const int64_t doubles = p.hmax * (nb + 1) + 2 * p.C * 2 * nb + QP_WARPS * nb + 2 * nb + (ks > 1 ? ks * nb * nb : 0);
+    if (doubles * 8 <= 225 * 1024 && p.hmax <= QP_RPT * QP_THREADS) {
       p.NB = nb;
       p.smem = static_cast<size_t>(doubles * 8);
       break;
@@ -812,11 +967,32 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
   // the side-stream update of panel k reads its G while panel k+1 writes its own)
   const int64_t npan = (n + 15) / 16;
   p.ws_doubles = static_cast<int64_t>(MAX_SPLIT + 1) * 32 * N + 2 * n + (MAX_C + npan) * 32 * 32 + 64;
+  // two-level blocking (n >= 3 outer blocks): per outer block its Gram matrix
+  // G_B (QR_OB^2), and two sets of far-update buffers (Yp, Z: the next
+  // block's columns on the main stream, the rest on a side stream)
+  p.two_level = n >= 3 * QR_OB;
+  if (p.two_level) {
+    const int64_t nblk = (n + QR_OB - 1) / QR_OB;
+    p.far_off = p.ws_doubles;
+    p.ws_doubles += nblk * QR_OB * QR_OB + 2 * (qr_far_yp_doubles() + static_cast<int64_t>(QR_OB) * N);
+  }
   return p;
 }
 
 int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
-                 int* singular, double* ws, const QrV2Plan& P, cudaStream_t s) {
+                 int* singular, double* ws, const QrV2Plan& P, cudaStream_t s_caller) {
+  // the factorisation runs on the high-priority stream, joined to the
+  // caller's stream at both ends
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  {
+    int rc = side_stream(&s, 2);
+    if (rc) return rc;
+    ITSK_CUDA(pooled_event(4, &ev_in));
+    ITSK_CUDA(pooled_event(5, &ev_out));
+    ITSK_CUDA(cudaEventRecord(ev_in, s_caller));
+    ITSK_CUDA(cudaStreamWaitEvent(s, ev_in, 0));
+  }
   double* Yp = ws;
   double* Z = Yp + static_cast<int64_t>(MAX_SPLIT) * 32 * N;
   double* betas = Z + 32 * N;
@@ -849,15 +1025,50 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     if (rc) return rc;
   }
   cudaEvent_t ev_main = nullptr, ev_side = nullptr;
-  if (ahead) {
+  if (ahead || P.two_level) {
     ITSK_CUDA(pooled_event(0, &ev_main));
     ITSK_CUDA(pooled_event(1, &ev_side));
-    ITSK_CUDA(cudaEventRecord(ev_main, s));  // the side stream starts after prior work on s
-    ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
+    ITSK_CUDA(cudaEventRecord(ev_main, s));  // the side streams start after prior work on s
+    if (ahead) ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
   }
   bool side_busy = false;
+  // Two-level blocking (P.two_level, n >= 3 QR_OB): the panels' updates stay
+  // inside their outer block of QR_OB columns; when a block is done, its
+  // reflectors update the far columns in one compact-WY step (qr_far.cu):
+  // the next block's columns on s (its panels need them), the rest on a
+  // second side stream, overlapping the next block's panels.  Ordering: the
+  // far update of block B+1's next block waits for block B's far rest.
+  const bool two = P.two_level;
+  cudaStream_t side_far = nullptr;
+  cudaEvent_t ev_g = nullptr, ev_far = nullptr;
+  bool far_busy = false;
+  double* Gfar = ws + P.far_off;
+  double* Ypf[2] = {nullptr, nullptr};
+  double* Zf[2] = {nullptr, nullptr};
+  if (two) {
+    int rc = side_stream(&side_far, 1);
+    if (rc) return rc;
+    ITSK_CUDA(pooled_event(2, &ev_g));
+    ITSK_CUDA(pooled_event(3, &ev_far));
+    ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_main, 0));
+    const int64_t nblk = (n + QR_OB - 1) / QR_OB;
+    Ypf[0] = Gfar + nblk * QR_OB * QR_OB;
+    Zf[0] = Ypf[0] + qr_far_yp_doubles();
+    Ypf[1] = Zf[0] + static_cast<int64_t>(QR_OB) * N;
+    Zf[1] = Ypf[1] + qr_far_yp_doubles();
+  }
   for (int64_t k0 = 0; k0 < n; k0 += P.NB) {
     const int kb = static_cast<int>(std::min<int64_t>(P.NB, n - k0));
+    // columns the panel's own update covers: its outer block (two-level; the
+    // last block also covers the rhs column) or all
+    const int64_t blk0 = two ? (k0 / QR_OB) * QR_OB : 0;
+    const int64_t horizon = (two && blk0 + QR_OB < n) ? blk0 + QR_OB : N;
+    if (two && k0 == blk0 && horizon == N && far_busy) {
+      // the last block's updates reach the rhs column, which the previous
+      // block's far rest may still be updating
+      ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));
+      far_busy = false;
+    }
     double* Gk = G + (k0 / P.NB) * 32 * 32;
     PanelArgs pa;
     pa.W = W;
@@ -884,7 +1095,30 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     cfg.numAttrs = 1;
     ITSK_CUDA(cudaLaunchKernelExC(&cfg, kp, args_of(pa)));
     count_launch();
-    const int64_t c0 = k0 + kb, Nt = N - c0;
+    const int64_t c0 = k0 + kb, Nt = horizon - c0;
+    if (two && c0 == horizon && horizon < N) {
+      // the outer block [blk0, horizon) is factored: its far update
+      const int ob = static_cast<int>(horizon - blk0);
+      double* Gb = Gfar + (blk0 / QR_OB) * QR_OB * QR_OB;
+      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, Ypf[0], Gb, s);
+      if (rc) return rc;
+      ITSK_CUDA(cudaEventRecord(ev_g, s));
+      if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));  // the previous block's far rest
+      const int64_t nn = std::min<int64_t>(QR_OB, N - horizon);
+      rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], s);
+      if (rc) return rc;
+      if (N - horizon > nn) {
+        ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_g, 0));
+        rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon + nn, N - horizon - nn, Gb, taus, Ypf[1], Zf[1],
+                                  side_far);
+        if (rc) return rc;
+        ITSK_CUDA(cudaEventRecord(ev_far, side_far));
+        far_busy = true;
+      } else {
+        far_busy = false;
+      }
+      continue;
+    }
     if (Nt <= 0) continue;
     UpdArgs ua;
     ua.W = W;
@@ -943,9 +1177,12 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     }
   }
   if (ahead && side_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
+  if (two && far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));
   k_qr_finish<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, s>>>(W, n, ldw, N, betas, R, z, singular);
   count_launch();
   ITSK_CHECK_LAUNCH();
+  ITSK_CUDA(cudaEventRecord(ev_out, s));
+  ITSK_CUDA(cudaStreamWaitEvent(s_caller, ev_out, 0));
   return ITSK_OK;
 }
 

@@ -1,0 +1,8 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "qr or solve_parity or c2_shape or trsv or estimates or condest" > gpurun_out/g9_pytest.txt 2>&1; echo "pytest rc=$?"
+tail -15 gpurun_out/g9_pytest.txt
+python scripts/micro_qr.py 24000 2000 5; python scripts/micro_qr.py 4000 200 20; python scripts/micro_qr.py 10000 500 10
+python scripts/qr_kernels.py 24000 2000 > gpurun_out/g9_qrk_c4.txt 2>&1; cat gpurun_out/g9_qrk_c4.txt
+python scripts/qr_kernels.py 10000 500 > gpurun_out/g9_qrk_c3.txt 2>&1; cat gpurun_out/g9_qrk_c3.txt
+python scripts/qr_compare.py > gpurun_out/g9_qr_compare.txt 2>&1; tail -20 gpurun_out/g9_qr_compare.txt
