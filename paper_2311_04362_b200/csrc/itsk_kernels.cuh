@@ -136,15 +136,17 @@ struct QrV2Plan {
   int64_t ws_doubles;
   bool two_level;    // outer blocks of QR_OB columns with a far update (qr_far.cu)
   int64_t far_off;   // offset (doubles) of the far-update buffers
+  int64_t next_off;  // offset of the next-panel update's Yp / Z (look-ahead without k_qr_next)
 };
 QrV2Plan qr_v2_plan(int64_t d, int64_t n);
-// Far update of the two-level blocked QR (qr_far.cu): G = V'V of an outer
-// block, and W_far -= V T' V' W_far for the far columns [c0, c0+Nf).
+// Far update of the two-level blocked QR (qr_far.cu): the compact-WY T of an
+// outer block (from G = V'V), and W_far -= V T' V' W_far for the far columns
+// [c0, c0+Nf) (G then holds T).
 constexpr int QR_OB = 128;          // outer block width
 constexpr int FAR_YP_TILES = 320;   // Yp capacity: splits x 64-column tiles
 int64_t qr_far_yp_doubles();
-int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, double* Yp, double* G,
-                       cudaStream_t s);
+int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, const double* taus, double* Yp,
+                       double* G, cudaStream_t s);
 int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, int64_t c0, int64_t Nf,
                          const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s);
 int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,

@@ -975,6 +975,10 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
     const int64_t nblk = (n + QR_OB - 1) / QR_OB;
     p.far_off = p.ws_doubles;
     p.ws_doubles += nblk * QR_OB * QR_OB + 2 * (qr_far_yp_doubles() + static_cast<int64_t>(QR_OB) * N);
+    // the look-ahead without k_qr_next: a second Yp / Z set for the next
+    // panel's update on the main stream
+    p.next_off = p.ws_doubles;
+    p.ws_doubles += static_cast<int64_t>(MAX_SPLIT + 1) * 32 * N;
   }
   return p;
 }
@@ -1018,7 +1022,11 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   // (k_qr_next, critical path); the rest of the trailing matrix on a side
   // stream, overlapping the next panel.  Ordering: rest(k) before next(k+1)
   // (which updates columns rest(k) covered), rest(k) after panel(k).
-  const bool ahead = nsmem <= 220 * 1024 && lookahead_enabled();
+  // k_qr_next (one cluster kernel) when its shared memory fits; else, in
+  // two-level mode, the next panel's columns through the regular update
+  // kernels on the critical path (own Yp / Z) and the rest beside them
+  const bool ahead_k = nsmem <= 220 * 1024 && lookahead_enabled();
+  const bool ahead = ahead_k || (P.two_level && lookahead_enabled());
   cudaStream_t side = nullptr;
   if (ahead) {
     int rc = side_stream(&side);
@@ -1031,6 +1039,25 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     ITSK_CUDA(cudaEventRecord(ev_main, s));  // the side streams start after prior work on s
     if (ahead) ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
   }
+  // Y = V'W2 (row splits), Z = T'Y, W2 -= V Z for the columns of `u`
+  auto launch_update = [&](UpdArgs u, int64_t rows, cudaStream_t st) {
+    const int64_t ncb = (u.Nt + UT - 1) / UT;
+    int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(MAX_SPLIT, (2 * nsm) / ncb)));
+    S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, rows / (2 * YRT))));
+    u.S = S;
+    dim3 gy(static_cast<unsigned>(ncb), static_cast<unsigned>(S));
+    dim3 ga(static_cast<unsigned>((rows + UT - 1) / UT), static_cast<unsigned>(ncb));
+    if (P.NB == 32) {
+      k_qr_y<32><<<gy, 256, ysm, st>>>(u);
+      k_qr_z<32><<<static_cast<unsigned>(ncb), 256, 0, st>>>(u);
+      k_qr_apply<32><<<ga, 256, 0, st>>>(u);
+    } else {
+      k_qr_y<16><<<gy, 256, ysm, st>>>(u);
+      k_qr_z<16><<<static_cast<unsigned>(ncb), 256, 0, st>>>(u);
+      k_qr_apply<16><<<ga, 256, 0, st>>>(u);
+    }
+    count_launch(3);
+  };
   bool side_busy = false;
   // Two-level blocking (P.two_level, n >= 3 QR_OB): the panels' updates stay
   // inside their outer block of QR_OB columns; when a block is done, its
@@ -1100,7 +1127,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
       // the outer block [blk0, horizon) is factored: its far update
       const int ob = static_cast<int>(horizon - blk0);
       double* Gb = Gfar + (blk0 / QR_OB) * QR_OB * QR_OB;
-      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, Ypf[0], Gb, s);
+      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, taus, Ypf[0], Gb, s);
       if (rc) return rc;
       ITSK_CUDA(cudaEventRecord(ev_g, s));
       if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));  // the previous block's far rest
@@ -1142,11 +1169,18 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
       UpdArgs un = ua;
       const int64_t nb2 = std::min<int64_t>(P.NB, Nt);
       un.Nt = nb2;
-      cudaLaunchConfig_t nc = cfg;
-      nc.dynamicSmemBytes = nsmem;
-      void* nargs[] = {&un, const_cast<int64_t*>(&P.hmax)};
-      ITSK_CUDA(cudaLaunchKernelExC(&nc, kn, nargs));
-      count_launch();
+      if (ahead_k) {
+        cudaLaunchConfig_t nc = cfg;
+        nc.dynamicSmemBytes = nsmem;
+        void* nargs[] = {&un, const_cast<int64_t*>(&P.hmax)};
+        ITSK_CUDA(cudaLaunchKernelExC(&nc, kn, nargs));
+        count_launch();
+      } else {
+        un.Yp = ws + P.next_off;
+        un.Z = un.Yp + static_cast<int64_t>(MAX_SPLIT) * 32 * N;
+        launch_update(un, rows, s);
+        ITSK_CHECK_LAUNCH();
+      }
       if (Nt == nb2) continue;
       ua.c0 = c0 + nb2;
       ua.Nt = Nt - nb2;
@@ -1154,22 +1188,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
       ITSK_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
       us = side;
     }
-    const int64_t ncb = (ua.Nt + UT - 1) / UT;
-    int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(MAX_SPLIT, (2 * nsm) / ncb)));
-    S = static_cast<int>(std::min<int64_t>(S, std::max<int64_t>(1, rows / (2 * YRT))));
-    ua.S = S;
-    dim3 gy(static_cast<unsigned>(ncb), static_cast<unsigned>(S));
-    dim3 ga(static_cast<unsigned>((rows + UT - 1) / UT), static_cast<unsigned>(ncb));
-    if (P.NB == 32) {
-      k_qr_y<32><<<gy, 256, ysm, us>>>(ua);
-      k_qr_z<32><<<static_cast<unsigned>(ncb), 256, 0, us>>>(ua);
-      k_qr_apply<32><<<ga, 256, 0, us>>>(ua);
-    } else {
-      k_qr_y<16><<<gy, 256, ysm, us>>>(ua);
-      k_qr_z<16><<<static_cast<unsigned>(ncb), 256, 0, us>>>(ua);
-      k_qr_apply<16><<<ga, 256, 0, us>>>(ua);
-    }
-    count_launch(3);
+    launch_update(ua, rows, us);
     ITSK_CHECK_LAUNCH();
     if (ahead) {
       ITSK_CUDA(cudaEventRecord(ev_side, side));

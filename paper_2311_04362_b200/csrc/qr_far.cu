@@ -5,9 +5,9 @@
 // tensor-core tiles:
 //
 //   Y = V' W_far          k_far_y   (split over row ranges, fixed-order sum)
-//   Z = T' Y              k_far_z   (z_i = tau_i (y_i - sum_{k<i} G_ki z_k),
-//                                    G = V'V: (T')^{-1} = diag(1/tau) +
-//                                    strict_lower(G'), no explicit T)
+//   G = V'V, T            k_far_y<true>, k_far_gsum, k_far_t (dlarft's
+//                                    recurrence T[0:i,i] = -tau_i T G[0:i,i])
+//   Z = T' Y              k_far_z   (a triangular mat-vec per column)
 //   W_far -= V Z          k_far_apply
 //
 // V (rows [b0, d), ob columns) is the unit lower trapezoid stored below the
@@ -64,7 +64,7 @@ struct FarArgs {
   double* Yp;          // S x Nf x FOB partials (k_far_y, column-major: a column's FOB values
                        // contiguous), summed by k_far_z
   int S;
-  const double* G;     // FOB x FOB: V'V of the block (k_far_z)
+  const double* G;     // FOB x FOB: the block's T (k_far_t), read by k_far_z
   const double* taus;  // global tau array, indexed b0 + i
   double* Z;           // Nf x FOB (column-major, like Yp)
 };
@@ -181,57 +181,92 @@ __global__ void k_far_gsum(const double* __restrict__ Gp, int S, int ob, double*
   G[e] = s;
 }
 
-// Z = T' Y for one column per warp: lane j carries t_j (j = lane + 32 q);
-// step i: z_i = tau_i t_i (lane i % 32), broadcast, lanes j > i subtract
-// G_ij z_i.  G (128 KB) is read through L1 (no shared memory: the kernel
-// fits beside the panel and GEMM kernels it overlaps); a column's partials
-// and its Z are contiguous (column-major).
+// T of the block (upper triangular, FOB x FOB, row stride FOB): dlarft's
+// forward column-wise recurrence T[i][i] = tau_i, T[0:i, i] = -tau_i
+// T[0:i, 0:i] G[0:i, i] (G = V'V), one CTA; each row's dot is split over 4
+// lanes and combined in a fixed order.  Z = T'Y then needs no sequential
+// substitution (k_far_z).
+constexpr int FT_THREADS = 512;
+__global__ void __launch_bounds__(FT_THREADS) k_far_t(const double* G, const double* __restrict__ taus,
+                                                      int64_t b0, int ob, double* T) {
+  extern __shared__ __align__(16) double tsm[];  // T: FOB x (FOB + 1) | G's strict upper triangle, packed
+  constexpr int TS = FOB + 1;
+  double* gu = tsm + FOB * TS;                   // column i of G above the diagonal at gu[i (i - 1) / 2 ...]
+  __shared__ double ts[FOB];
+  const int tid = threadIdx.x;
+  const int r = tid >> 2, part = tid & 3;
+  for (int e = tid; e < FOB * TS; e += FT_THREADS) tsm[e] = 0.0;
+  // every G element the recurrence reads, loaded up front (all in flight)
+  for (int e = tid; e < FOB * FOB; e += FT_THREADS) {
+    const int k = e / FOB, i = e - k * FOB;
+    if (k < i && i < ob) gu[i * (i - 1) / 2 + k] = G[e];
+  }
+  if (tid < FOB) ts[tid] = tid < ob ? taus[b0 + tid] : 0.0;
+  __syncthreads();
+  for (int i = 0; i < ob; ++i) {
+    const double* w = gu + i * (i - 1) / 2;
+    double sum = 0.0;
+    if (r < i)
+      for (int k = r + part; k < i; k += 4) sum = fma(tsm[r * TS + k], w[k], sum);
+    sum += __shfl_xor_sync(FULL, sum, 1);
+    sum += __shfl_xor_sync(FULL, sum, 2);
+    if (part == 0 && r < i) tsm[r * TS + i] = -ts[i] * sum;
+    if (tid == 0) tsm[i * TS + i] = ts[i];
+    __syncthreads();
+  }
+  for (int e = tid; e < FOB * FOB; e += FT_THREADS) {
+    const int rr = e / FOB, c = e - rr * FOB;
+    T[e] = (rr < ob && c < ob) ? tsm[rr * TS + c] : 0.0;
+  }
+}
+
+// Z = T'Y, one column per warp: lane j holds z_j for j = lane + 32 q; y_k is
+// the fixed-order sum of the split partials, broadcast by shuffle; z_j =
+// sum_{k <= j} T_kj y_k in ascending k.  Y partials and Z are column-major
+// (a column's FOB values contiguous); T is read through L1.
 constexpr int FZ_WARPS = 8;
 __global__ void __launch_bounds__(32 * FZ_WARPS) k_far_z(FarArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ob = a.ob;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * FZ_WARPS + warp;
   if (c >= a.Nf) return;
-  double t[4];
+  double y[4];
   {
     const double* yp = a.Yp + c * FOB + lane;
     const int64_t stride = static_cast<int64_t>(FOB) * a.Nf;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) t[q] = 0.0;
+    for (int q = 0; q < 4; ++q) y[q] = 0.0;
     for (int sp = 0; sp < a.S; ++sp) {
       double v[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[q] = lane + 32 * q < ob ? __ldcg(yp + sp * stride + 32 * q) : 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) t[q] += v[q];
+      for (int q = 0; q < 4; ++q) y[q] += v[q];
     }
   }
-  double tau[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) tau[q] = lane + 32 * q < ob ? __ldg(a.taus + a.b0 + lane + 32 * q) : 0.0;
+  double z[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* T = a.G;  // the block's T (k_far_t)
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (32 * q >= ob) break;
-#pragma unroll 4
-    for (int il = 0; il < 32; ++il) {
-      const int i = 32 * q + il;
-      if (i >= ob) break;
-      const double zi = __shfl_sync(FULL, tau[q] * t[q], il);
-      const double* gr = a.G + i * FOB + lane;
+#pragma unroll 8
+    for (int kl = 0; kl < 32; ++kl) {
+      const int k = 32 * q + kl;
+      if (k >= ob) break;
+      const double yk = __shfl_sync(FULL, y[q], kl);
+      const double* tr = T + k * FOB + lane;
 #pragma unroll
       for (int q2 = 0; q2 < 4; ++q2) {
         if (q2 < q) continue;
-        const int jj = lane + 32 * q2;
-        const double g = __ldg(gr + 32 * q2);
-        if (jj == i) t[q2] = zi;
-        else if (jj > i) t[q2] = fma(-g, zi, t[q2]);
+        const int j = lane + 32 * q2;
+        if (k <= j) z[q2] = fma(__ldg(tr + 32 * q2), yk, z[q2]);
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int jj = lane + 32 * q;
-    if (jj < ob) a.Z[c * FOB + jj] = t[q];
+    const int j = lane + 32 * q;
+    if (j < ob) a.Z[c * FOB + j] = z[q];
   }
 }
 
@@ -327,6 +362,7 @@ int far_attrs() {
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_y<false>)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_y<true>)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_apply)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_t)));
   return ITSK_OK;
 }
 
@@ -334,8 +370,8 @@ int far_attrs() {
 
 int64_t qr_far_yp_doubles() { return static_cast<int64_t>(FAR_YP_TILES) * FOB * 64; }
 
-int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, double* Yp, double* G,
-                       cudaStream_t s) {
+int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, const double* taus, double* Yp,
+                       double* G, cudaStream_t s) {
   int rc = far_attrs();
   if (rc) return rc;
   FarArgs a{};
@@ -354,7 +390,9 @@ int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, do
   a.S = std::max(1, S);
   k_far_y<true><<<dim3(ncb, a.S), FT, FY_SMEM, s>>>(a);
   k_far_gsum<<<(FOB * FOB + 255) / 256, 256, 0, s>>>(Yp, a.S, ob, G);
-  count_launch(2);
+  // T from G and tau, written over G (read completely before the first write)
+  k_far_t<<<1, FT_THREADS, (FOB * (FOB + 1) + FOB * (FOB - 1) / 2) * 8, s>>>(G, taus, b0, ob, G);
+  count_launch(3);
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
 }
