@@ -838,23 +838,32 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
     // row ((l / GW) % (RB / VPL)) * VPL + i
     constexpr int VPL = (GW * RB + 31) / 32;  // partials per lane
     constexpr int RPL = RB / VPL;              // row slots across the lanes
+    // column validity is loop-invariant: masks computed once
+    bool cok[CPP], cpad[CPP];
+#pragma unroll
+    for (int j = 0; j < CPP; ++j) {
+      cok[j] = col[j] < n;
+      cpad[j] = col[j] + 1 >= n;
+    }
+    // stage index and mbarrier phase advance by NG per batch (S is a multiple
+    // of NG): no integer division in the loop
+    int st = g;
+    unsigned ph = 0;
     for (int t = g, par = 0; t < ntiles; t += NG, par ^= 1) {
       double nb, np, nt;
       fetch(t + NG, nb, np, nt);
-      const int st = t % S;
       const int nu = min(RB, nrows - t * RB);
-      mbar_wait(full + st, static_cast<unsigned>((t / S) & 1));
+      mbar_wait(full + st, ph);
       const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(st) * sh.stage_bytes);
       double2 v[RB][CPP];
 #pragma unroll
       for (int u = 0; u < RB; ++u)
 #pragma unroll
         for (int j = 0; j < CPP; ++j) {
-          const int c = col[j];
           double2 w = make_double2(0.0, 0.0);
-          if (u < nu && c < n) {
-            w = *reinterpret_cast<const double2*>(base + u * lda + c);
-            if (c + 1 >= n) w.y = 0.0;  // the pad column of an odd n
+          if (cok[j] && u < nu) {
+            w = *reinterpret_cast<const double2*>(base + u * lda + col[j]);
+            if (cpad[j]) w.y = 0.0;  // the pad column of an odd n
           }
           v[u][j] = w;
         }
@@ -925,6 +934,11 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
         s_tt += tt * tt;
       }
       cb = nb; cp = np; ct = nt;
+      st += NG;
+      if (st >= S) {
+        st -= S;
+        ph ^= 1u;
+      }
     }
     if (gw == 0) {
       s_rr = warp_sum(s_rr);

@@ -43,6 +43,7 @@ constexpr int YRT = 32;       // row chunk of k_qr_y
 constexpr int MAX_SPLIT = 48; // row splits of k_qr_y (partials summed by k_qr_z)
 constexpr int MAX_C = 16;     // cluster size bound
 constexpr int QP_RPT = 4;     // panel rows per thread bound (rows per CTA <= QP_RPT * QP_THREADS)
+constexpr int NB_NEXT2 = 16;  // panel width of the streaming look-ahead (k_qr_next2)
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
 __device__ __forceinline__ int64_t lo_of(int q, int P, int64_t len) {
@@ -873,6 +874,201 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next(UpdArgs a, int64_t hm
   QNP(4);
 }
 
+// Streaming look-ahead (16-wide panels at C4 sizes, where k_qr_next's
+// whole-slice staging does not fit): the same update of the next panel's
+// nb2 <= NB columns by the panel just factored, in one cluster launch with
+// the panel's row split, but the CTA's rows pass through a double-buffered
+// cp.async ring of NX_RC-row chunks twice: pass 1 accumulates the partial
+// Y = V'B on DMMA tiles (16 warps = 4 tiles x 4 row slices, 4 interleaved
+// chains each, the slices summed in a fixed order), the partials are summed
+// over the cluster in rank order (DSMEM), Z = T'Y by substitution with G and
+// tau; pass 2 re-streams the chunks and stores B - V Z.  V and B are
+// L2-resident (just written by the panel and the previous updates).
+constexpr int NX_RC = 128;   // rows per chunk
+constexpr int NX_ST = 4;     // ring stages (3 chunks, ~120 KB, in flight per SM)
+constexpr int NX_S = NB_NEXT2 + 4;
+
+template <int NB>
+__global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next2(UpdArgs a) {
+  static_assert(NB == NB_NEXT2, "k_qr_next2 is instantiated for 16-wide panels");
+  extern __shared__ __align__(16) double sm[];
+#ifdef ITSK_QRNEXT_PROBE
+  long long _qt = clock64();
+#endif
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), q = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int64_t k0 = a.k0, ldw = a.ldw;
+  const int64_t len = a.d - k0;
+  const int64_t lo = k0 + lo_of(q, C, len), hi = k0 + lo_of(q + 1, C, len);
+  const int h = static_cast<int>(hi - lo);
+  const int nb2 = static_cast<int>(a.Nt);
+  const int kb = a.kb;
+  double* Vs = sm;                          // NX_ST x NX_RC x NX_S
+  double* Bs = Vs + NX_ST * NX_RC * NX_S;   // NX_ST x NX_RC x NX_S
+  double* Yk = Bs + NX_ST * NX_RC * NX_S;   // 4 slices x NB x NB
+  double* Yq = Yk + 4 * NB * NB;            // NB x NB: this CTA's partial
+  double* Ys = Yq + NB * NB;                // NB x NB: the sum, then Z
+  double* Yo = Ys + NB * NB;                // NB x NB: elements this CTA owns, summed
+  const int nch = (h + NX_RC - 1) / NX_RC;
+  auto load = [&](int ch) {
+    const int st = ch % NX_ST;
+    double* vs = Vs + st * NX_RC * NX_S;
+    double* bs = Bs + st * NX_RC * NX_S;
+    const int r0 = ch * NX_RC;
+    for (int idx = tid; idx < NX_RC * NB; idx += QP_THREADS) {
+      const int rr = idx / NB, c = idx - rr * NB;
+      const int64_t r = lo + r0 + rr;
+      const bool okv = r0 + rr < h && c < kb;
+      cp_async8(vs + rr * NX_S + c, a.W + (okv ? r * ldw + k0 + c : 0), okv);
+      const bool okb = r0 + rr < h && c < nb2;
+      cp_async8(bs + rr * NX_S + c, a.W + (okb ? r * ldw + a.c0 + c : 0), okb);
+    }
+  };
+  // V(r, c) with the unit-diagonal fix (rows of the panel's top triangle)
+  auto vfix = [&](double v, int64_t r, int c) { return vval(v, r, k0, c); };
+  // ---- pass 1: Y partial ----
+  const int tile = warp & 3, slice = warp >> 2;  // 4 tiles (NB/8)^2, 4 row slices of each chunk
+  const int mt = tile >> 1, nt = tile & 1;
+  double e0[4] = {0.0, 0.0, 0.0, 0.0}, e1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int ch = 0; ch < NX_ST - 1; ++ch) {
+    if (ch < nch) load(ch);
+    cp_commit();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_wait<NX_ST - 2>();
+    __syncthreads();
+    if (ch + NX_ST - 1 < nch) load(ch + NX_ST - 1);
+    cp_commit();
+    const int st = ch % NX_ST;
+    const double* vs = Vs + st * NX_RC * NX_S;
+    const double* bs = Bs + st * NX_RC * NX_S;
+    const int r0 = ch * NX_RC;
+    // slice `slice` takes rows [slice * 32, slice * 32 + 32) of the chunk
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 4) {
+        const int rr = slice * 32 + u * 8 + kk + t4;
+        const int64_t r = lo + r0 + rr;
+        const double av = vfix(vs[rr * NX_S + mt * 8 + g4], r, mt * 8 + g4);
+        const double bv = bs[rr * NX_S + nt * 8 + g4];
+        dmma(e0[u], e1[u], av, bv);
+      }
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+  QNP(0);
+  {
+    double* yk = Yk + slice * NB * NB;
+    yk[(mt * 8 + g4) * NB + nt * 8 + 2 * t4] = (e0[0] + e0[1]) + (e0[2] + e0[3]);
+    yk[(mt * 8 + g4) * NB + nt * 8 + 2 * t4 + 1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
+  }
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += QP_THREADS)
+    Yq[e] = (Yk[e] + Yk[NB * NB + e]) + (Yk[2 * NB * NB + e] + Yk[3 * NB * NB + e]);
+  cl.sync();
+  QNP(1);
+  // the C partials summed in rank order: CTA q sums the elements e = q mod C
+  // over all ranks, then every CTA gathers the owners' sums
+  for (int e = q + C * tid; e < NB * NB; e += C * QP_THREADS) {
+    const uint32_t la = smem_u32(Yq + e);
+    double v[MAX_C];
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t) {
+      v[t] = 0.0;
+      if (t < C) asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[t]) : "r"(mapa_u32(la, t)) : "memory");
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAX_C; ++t)
+      if (t < C) sum += v[t];
+    Yo[e] = sum;
+  }
+  cl.sync();
+  for (int e = tid; e < NB * NB; e += QP_THREADS) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(mapa_u32(smem_u32(Yo + e), e % C)) : "memory");
+    Ys[e] = v;
+  }
+  __syncthreads();
+  QNP(2);
+  // Z = T'Y: warp c < nb2 handles column c; lane j carries t_j
+  if (warp < nb2) {
+    const int c = warp;
+    const int jl = lane < NB ? lane : 0;
+    double t = lane < kb ? Ys[jl * NB + c] : 0.0;
+    const double mytau = lane < kb ? a.taus[k0 + jl] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (i >= kb) break;
+      const double g = a.G[i * NB + jl];
+      const double zi = __shfl_sync(FULL, mytau * t, i);
+      if (lane == i) t = zi;
+      else if (lane > i) t = fma(-g, zi, t);
+    }
+    __syncwarp();
+    if (lane < NB) Ys[jl * NB + c] = lane < kb ? t : 0.0;
+  }
+  __syncthreads();
+  QNP(3);
+  // ---- pass 2: B -= V Z, chunk by chunk ----
+#pragma unroll
+  for (int ch = 0; ch < NX_ST - 1; ++ch) {
+    if (ch < nch) load(ch);
+    cp_commit();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_wait<NX_ST - 2>();
+    __syncthreads();
+    if (ch + NX_ST - 1 < nch) load(ch + NX_ST - 1);
+    cp_commit();
+    const int st = ch % NX_ST;
+    const double* vs = Vs + st * NX_RC * NX_S;
+    const double* bs = Bs + st * NX_RC * NX_S;
+    const int r0 = ch * NX_RC;
+    // NX_RC x NB output = (NX_RC / 8) x 2 tiles of 8x8: one row tile per warp, both column tiles
+    {
+      const int rt = warp;  // 16 warps x 8 rows = NX_RC
+      const int rr = rt * 8 + g4;
+      const int64_t r = lo + r0 + rr;
+      double d[2][2];
+#pragma unroll
+      for (int ct = 0; ct < 2; ++ct) {
+        d[ct][0] = bs[rr * NX_S + ct * 8 + 2 * t4];
+        d[ct][1] = bs[rr * NX_S + ct * 8 + 2 * t4 + 1];
+      }
+#pragma unroll
+      for (int k = 0; k < NB; k += 4) {
+        const int rk = rt * 8 + g4;
+        const double av = -vfix(vs[rk * NX_S + k + t4], lo + r0 + rk, k + t4);
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) dmma(d[ct][0], d[ct][1], av, Ys[(k + t4) * NB + ct * 8 + g4]);
+      }
+      if (r0 + rr < h) {
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+          const int c = ct * 8 + 2 * t4;
+          double* wp = a.W + r * ldw + a.c0 + c;
+          if (c < nb2) wp[0] = d[ct][0];
+          if (c + 1 < nb2) wp[1] = d[ct][1];
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+  QNP(4);
+  cl.sync();  // no CTA exits while another may still read its Yo
+  QNP(5);
+}
+
+size_t next2_smem() {
+  return static_cast<size_t>(2 * NX_ST * NX_RC * NX_S + 4 * NB_NEXT2 * NB_NEXT2 + 3 * NB_NEXT2 * NB_NEXT2) * 8;
+}
+
 size_t next_smem(int64_t hmax, int nb) {
   return static_cast<size_t>((hmax + 16) * (nb + 4) + (hmax + 16) * 36 + 2 * 32 * 36 + nb * (nb + 4) + nb +
                              nb * 32) * 8;
@@ -1015,6 +1211,9 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   ITSK_CUDA(allow_max_smem(kn));
   ITSK_CUDA(func_attr_once(kp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   ITSK_CUDA(func_attr_once(kn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_qr_next2<NB_NEXT2>)));
+  ITSK_CUDA(func_attr_once(reinterpret_cast<const void*>(k_qr_next2<NB_NEXT2>),
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int nsm = num_sms();
   const size_t ysm = y_smem(P.NB);
   const size_t nsmem = next_smem(P.hmax, P.NB);
@@ -1174,6 +1373,12 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
         nc.dynamicSmemBytes = nsmem;
         void* nargs[] = {&un, const_cast<int64_t*>(&P.hmax)};
         ITSK_CUDA(cudaLaunchKernelExC(&nc, kn, nargs));
+        count_launch();
+      } else if (P.NB == NB_NEXT2) {
+        cudaLaunchConfig_t nc = cfg;
+        nc.dynamicSmemBytes = next2_smem();
+        void* nargs[] = {&un};
+        ITSK_CUDA(cudaLaunchKernelExC(&nc, reinterpret_cast<const void*>(k_qr_next2<NB_NEXT2>), nargs));
         count_launch();
       } else {
         un.Yp = ws + P.next_off;
