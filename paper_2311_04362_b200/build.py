@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libitsk_b200.so")
-SOURCES = ["capi.cu", "pattern.cu", "sketch.cu", "qr.cu", "qr2.cu", "qr_far.cu", "qr_tsqr.cu", "trsv.cu", "pass.cu", "loop.cu", "sparse.cu"]
+SOURCES = ["capi.cu", "pattern.cu", "sketch.cu", "qr.cu", "qr2.cu", "qr_far.cu", "trsv.cu", "pass.cu", "loop.cu", "sparse.cu"]
 HEADERS = ["itsk_common.cuh", "itsk_kernels.cuh", "itsk_dense.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -125,7 +125,6 @@ int launch_csr_pass(const CsrPlan* P, const double* b, double bscale, const doub
                     double* r_out, const double* r_true, double* cs, const LoopCtl* ctl, const double* xs,
                     double* rs, int mode, cudaStream_t s);
 
-// Communication-avoiding cluster QR (qr_tsqr.cu)
 // Panel / update split QR (qr2.cu), the default path of itsk_qr_aug.
 struct QrV2Plan {
   int C;             // cluster size of the panel kernel
@@ -152,8 +151,6 @@ int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, 
 int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
                  int* singular, double* ws, const QrV2Plan& P, cudaStream_t s);
 
-int qr_tsqr_plan(int64_t d, int64_t n, size_t* smem);
-int launch_qr_tsqr(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
-                   int* singular, int C, size_t smem, cudaStream_t s);
+
 
 }  // namespace itsk

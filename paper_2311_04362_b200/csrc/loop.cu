@@ -557,13 +557,7 @@ LoopPtrs make_ptrs(const itsk_loop_params* p) {
 // overlaps under programmatic dependent launch) and the deferred estimates
 // (condest's 2-CTA cluster, normest) running beside the first iterations.
 // A pass CTA that finds no free SM would wait for them.
-int loop_sm_reserve() {
-  static const int r = [] {
-    const char* e = getenv("ITSK_LOOP_SM_RESERVE");  // tuning knob
-    return e ? std::max(0, atoi(e)) : 4;
-  }();
-  return r;
-}
+int loop_sm_reserve() { return 4; }
 
 PassArgs pass_args(const itsk_loop_params* p, const LoopPtrs& q, int mode) {
   PassArgs a{};
@@ -632,13 +626,7 @@ int prepare_attrs(int64_t n) {
   return ITSK_OK;
 }
 
-int loop_unroll() {
-  static const int u = [] {
-    const char* e = getenv("ITSK_LOOP_UNROLL");  // tuning knob
-    return e ? std::max(1, std::min(8, atoi(e))) : 2;
-  }();
-  return u;
-}
+int loop_unroll() { return 2; }  // two iterations per graph body: every other boundary keeps PDL
 
 struct GraphHandle {
   cudaGraph_t graph = nullptr;

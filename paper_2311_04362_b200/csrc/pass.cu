@@ -148,7 +148,6 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(PassArgs a) {
 // then c update), so registers hold only c (and x when it fits) — this keeps
 // ~S*16 KB of HBM traffic in flight per SM independent of n.
 // ---------------------------------------------------------------------------
-constexpr int TMA_MAX_CONSUMERS = 16;
 
 struct TmaShape {
   int T;            // rows per tile (multiple of UNR)
@@ -487,211 +486,6 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
 #ifdef ITSK_TIMELINE
   if (tid == 0 && tl_slot >= 0 && tl_slot < TL_SLOTS) atomicMax(&g_pass_tl[tl_slot][2], gtime());
 #endif
-}
-
-// ---------------------------------------------------------------------------
-// Wide rows (n > 512): the same TMA ring, but the 16 consumer warps form 4
-// groups of 4; a group takes every 4th row and its 4 warps split the columns
-// (SW = 32 * CPLW each).  Per row: slice dot -> shuffle tree -> 4 partials
-// through shared memory + one 128-thread named barrier -> r -> c_slice += r *
-// row_slice.  c lives in CPLW registers per lane instead of 64, so the loads
-// of a row can be in flight together (the one-warp-per-row variant at n = 2000
-// needs 168 registers and serialises on shared-memory latency).
-// ---------------------------------------------------------------------------
-constexpr int WIDE_NCW = 16, WIDE_GW = 4, WIDE_NG = 4;
-
-template <int CPLW>
-__global__ void __launch_bounds__(32 * (WIDE_NCW + 1), 1) k_pass_wide(PassArgs a, TmaShape sh) {
-  constexpr int THREADS = 32 * (WIDE_NCW + 1);
-  constexpr int SW = 32 * CPLW;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* empty = full + 32;
-  int* stage_tile = reinterpret_cast<int*>(empty + 32);
-  // x for the 16-column variant (one copy per group, 4 * SW doubles each)
-  double* xsm_base = reinterpret_cast<double*>(smraw + 1024);
-  unsigned char* stages = smraw + 1024 + (CPLW > 8 ? WIDE_NG * WIDE_GW * SW * 8 : 0);
-  __shared__ double dpart[WIDE_NG][2][WIDE_GW];
-  __shared__ double ssm[WIDE_NCW][4];
-  __shared__ int s_done;
-
-  const double* r_true = a.r_true;
-  const double* b = a.b;
-  const double bscale = a.bscale;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n = a.n, lda = a.lda;
-  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
-  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
-  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
-  const int T = sh.T, S = sh.S;
-  const int ntiles = (nrows + T - 1) / T;
-  const int npre = min(S, ntiles);
-
-  if (tid == 0) {
-    for (int st = 0; st < S; ++st) {
-      mbar_init(full + st, 1);
-      mbar_init(empty + st, T * WIDE_GW);  // each row of a tile is read by one group of 4 warps
-      stage_tile[st] = -1;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_trigger();
-  if (warp == WIDE_NCW && lane == 0) {
-    const uint64_t pol = evict_first_policy();
-    for (int t = 0; t < npre; ++t) {
-      const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
-      const int rows = min(T, nrows - t * T);
-      const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
-      reinterpret_cast<volatile int*>(stage_tile)[t] = t;
-      mbar_expect_tx(full + t, bytes);
-      bulk_g2s(stages + static_cast<int64_t>(t) * sh.stage_bytes, a.A + row0 * lda, bytes, full + t, pol);
-    }
-  }
-  pdl_wait();
-
-  const double* x;
-  const double* r_prev;
-  double* r_out;
-  if (a.mode == 0) {
-    x = a.x;
-    r_prev = a.r_prev;
-    r_out = a.r_out;
-  } else {
-    const LoopCtl* ctl = a.ctl;
-    if (tid == 0) s_done = ctl->result.done;
-    __syncthreads();
-    if (s_done) {
-      if (warp == WIDE_NCW && lane == 0)
-        for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
-      return;
-    }
-    const int64_t SL = ctl->r_slots;
-    if (a.mode == 1) {
-      const int64_t it = ctl->it;
-      x = a.xs + (it + 1) * a.n;
-      r_prev = a.rs + (it % SL) * a.m;
-      r_out = a.rs + ((it + 1) % SL) * a.m;
-    } else {
-      x = a.xs;
-      r_prev = nullptr;
-      r_out = a.rs;
-    }
-  }
-
-  const int g = warp / WIDE_GW, gw = warp % WIDE_GW;
-  const int c0 = gw * SW;
-  double acc[CPLW];
-#pragma unroll
-  for (int q = 0; q < CPLW; ++q) acc[q] = 0.0;
-
-  if (warp == WIDE_NCW) {
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      for (int t = npre; t < ntiles; ++t) {
-        const int st = t % S;
-        mbar_wait(empty + st, static_cast<unsigned>(((t / S) - 1) & 1));
-        const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
-        const int rows = min(T, nrows - t * T);
-        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
-        reinterpret_cast<volatile int*>(stage_tile)[st] = t;
-        mbar_expect_tx(full + st, bytes);
-        bulk_g2s(stages + static_cast<int64_t>(st) * sh.stage_bytes, a.A + row0 * lda, bytes, full + st, pol);
-      }
-    }
-  } else {
-    // x slice: registers for CPLW <= 8, shared memory above (the 16-column
-    // variant would otherwise spill at the 544-thread register budget)
-    constexpr bool XR = CPLW <= 8;
-    double xv[XR ? CPLW : 1];
-    double* xs = xsm_base + g * WIDE_GW * SW + c0 + lane;
-#pragma unroll
-    for (int q = 0; q < CPLW; ++q) {
-      const int c = c0 + lane + 32 * q;
-      const double v = c < n ? x[c] : 0.0;
-      if (XR) xv[XR ? q : 0] = v; else xs[32 * q] = v;
-    }
-    __syncwarp();
-    double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
-    // b / r_prev / r_true of the group's next row, one row ahead
-    const bool lead = gw == 0 && lane == 0;
-    auto fetch = [&](int k, double& fb, double& fp, double& ft) {
-      const bool ok = k < nrows;
-      const int64_t gi = r_begin + k;
-      fb = ok ? b[gi] : 0.0;
-      fp = (ok && lead && r_prev) ? r_prev[gi] : 0.0;
-      ft = (ok && lead && r_true) ? r_true[gi] : 0.0;
-    };
-    double cb, cp, ct;
-    fetch(g, cb, cp, ct);
-    int par = 0;
-    for (int k = g; k < nrows; k += WIDE_NG, par ^= 1) {
-      double nb, np, nt;
-      fetch(k + WIDE_NG, nb, np, nt);
-      const int t = k / T;
-      const int st = t % S;
-      while (reinterpret_cast<volatile int*>(stage_tile)[st] != t) __nanosleep(20);
-      mbar_wait(full + st, static_cast<unsigned>((t / S) & 1));
-      const double* row = reinterpret_cast<const double*>(stages + static_cast<int64_t>(st) * sh.stage_bytes) +
-                          static_cast<int64_t>(k - t * T) * lda + c0 + lane;
-      double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < CPLW; q += 2) {
-        d0 = fma((c0 + lane + 32 * q < n) ? row[32 * q] : 0.0, XR ? xv[XR ? q : 0] : xs[32 * q], d0);
-        if (q + 1 < CPLW)
-          d1 = fma((c0 + lane + 32 * (q + 1) < n) ? row[32 * (q + 1)] : 0.0,
-                   XR ? xv[XR ? q + 1 : 0] : xs[32 * (q + 1)], d1);
-      }
-      double dp = warp_sum(d0 + d1);
-      if (lane == 0) dpart[g][par][gw] = dp;
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(32 * WIDE_GW) : "memory");
-      const double dot = (dpart[g][par][0] + dpart[g][par][1]) + (dpart[g][par][2] + dpart[g][par][3]);
-      const double r = bscale * cb - dot;
-      // the slice is read from shared memory again (holding it across the
-      // barrier would cost CPLW more registers per lane)
-#pragma unroll
-      for (int q = 0; q < CPLW; ++q) acc[q] = fma(r, (c0 + lane + 32 * q < n) ? row[32 * q] : 0.0, acc[q]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);
-      if (lead) {
-        if (r_out) r_out[r_begin + k] = r;
-        s_rr += r * r;
-        s_bb += cb * cb;
-        const double dd = r - cp;
-        s_dd += dd * dd;
-        const double tt = ct - r;
-        s_tt += tt * tt;
-      }
-      cb = nb; cp = np; ct = nt;
-    }
-    if (lane == 0) {
-      ssm[warp][0] = s_rr;
-      ssm[warp][1] = r_prev ? s_dd : 0.0;
-      ssm[warp][2] = r_true ? s_tt : 0.0;
-      ssm[warp][3] = s_bb;
-    }
-  }
-  __syncthreads();  // all tiles consumed: the ring is free for the reduction
-  double* csm = reinterpret_cast<double*>(stages);  // WIDE_NG x (4 * SW)
-  constexpr int NCOL = WIDE_GW * SW;
-  if (warp < WIDE_NCW) {
-#pragma unroll
-    for (int q = 0; q < CPLW; ++q) csm[g * NCOL + c0 + lane + 32 * q] = acc[q];
-  }
-  __syncthreads();
-  double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
-  for (int c = tid; c < n; c += THREADS) {
-    double sum = 0.0;
-#pragma unroll
-    for (int gg = 0; gg < WIDE_NG; ++gg) sum += csm[gg * NCOL + c];
-    out[c] = sum;
-  }
-  if (tid < 4) {
-    double sum = 0.0;
-    for (int w = 0; w < WIDE_NCW; ++w) sum += ssm[w][tid];
-    out[n + tid] = sum;
-  }
-  if (a.tickets) group_reduce(a, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -1095,20 +889,13 @@ TmaShape tma_shape(int64_t lda, int cpl, int unr, int ncw) {
   TmaShape sh;
   const int64_t row_bytes = lda * 8;
   // ~16 KB (at least UNR rows) per bulk copy
-  static const int64_t tile_target = [] {
-    const char* e = getenv("ITSK_PASS_TILE_BYTES");  // tuning knob
-    return e ? std::max(1024L, atol(e)) : 16384L;
-  }();
+  constexpr int64_t tile_target = 16384;
   int64_t T = std::max<int64_t>(1, (tile_target + row_bytes - 1) / row_bytes);
   T = ((T + unr - 1) / unr) * unr;
   sh.T = static_cast<int>(T);
   sh.stage_bytes = static_cast<int>(align_up(T * row_bytes, 128));
   const int xbytes = cpl > 8 ? 32 * cpl * 8 : 0;
-  static const int budget = [] {
-    const char* e = getenv("ITSK_PASS_SMEM_KB");  // tuning knob
-    return e ? atoi(e) * 1024 : TMA_SMEM_BUDGET;
-  }();
-  sh.S = std::min(24, (budget - 1024 - xbytes) / sh.stage_bytes);
+  sh.S = std::min(24, (TMA_SMEM_BUDGET - 1024 - xbytes) / sh.stage_bytes);
   const int red = ncw * 32 * cpl * 8;  // final reduction reuses the ring
   while (sh.S * sh.stage_bytes < red) ++sh.S;
   return sh;
@@ -1134,27 +921,6 @@ int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
   return ITSK_OK;
 }
 
-// rows per consumer batch: 4 while a row is <= 16 columns per lane, then
-// fewer so c stays in registers
-template <int CPLW>
-int launch_wide(const PassArgs& a0, int grid, cudaStream_t s) {
-  PassArgs a = a0;
-  // tiles of whole rows (~16 KB), ring sized like the narrow variant; the
-  // final reduction needs 4 x (4 * SW) doubles of the ring
-  TmaShape sh = tma_shape(a.lda, 1, 1, 1);
-  const int xbytes = CPLW > 8 ? WIDE_NG * WIDE_GW * 32 * CPLW * 8 : 0;  // per-group x slices
-  const int red = WIDE_NG * WIDE_GW * 32 * CPLW * 8;
-  sh.S = std::max(2, (TMA_SMEM_BUDGET - 1024 - xbytes) / sh.stage_bytes);
-  while (sh.S * sh.stage_bytes < red) ++sh.S;
-  a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
-  const size_t smem = 1024 + xbytes + static_cast<size_t>(sh.S) * sh.stage_bytes;
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_wide<CPLW>)));
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_wide<CPLW>), dim3(grid), dim3(32 * (WIDE_NCW + 1)),
-                       smem, s, a, sh));
-  count_launch();
-  ITSK_CHECK_LAUNCH();
-  return ITSK_OK;
-}
 
 template <int GW>
 int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
@@ -1179,52 +945,26 @@ int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
   return ITSK_OK;
 }
 
-// development A/B: ITSK_PASS_ROWS=0 off, 1 every n > 128, k: only where the
-// group is >= k warps wide (16: n > 1024 only)
-int pass_rows_mode() {
-  static const int mode = [] {
-    const char* e = getenv("ITSK_PASS_ROWS");
-    return e ? atoi(e) : 1;
-  }();
-  return mode;
-}
-
-bool pass_wide_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ITSK_PASS_WIDE");  // tuning knob: 0 = one warp per row for all n
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
-
 template <int CPL>
 int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
   // row groups where the group's 128 GW columns are mostly used (measured:
-  // n = 500, 600, 1000, 2000 faster than the warp-per-row / warp-group
-  // kernels; n = 200, 300 slower, profiles/rd2_pass_rows_ab.txt)
-  if (pass_rows_mode() > 0 && a.n > 384) {
-    const int gw = a.n > 1024 ? 16 : a.n > 512 ? 8 : 4;
-    if (pass_rows_mode() == 1 || gw >= pass_rows_mode()) {
-      switch (gw) {
-        case 16: return launch_rows<16>(a, grid, s);
-        case 8: return launch_rows<8>(a, grid, s);
-        default: return launch_rows<4>(a, grid, s);
-      }
-    }
+  // n = 500, 600, 1000, 2000 faster than the warp-per-row kernel; n = 200,
+  // 300 slower, profiles/rd2_pass_rows_ab.txt)
+  if (a.n > 384) {
+    if (a.n > 1024) return launch_rows<16>(a, grid, s);
+    if (a.n > 512) return launch_rows<8>(a, grid, s);
+    return launch_rows<4>(a, grid, s);
   }
-  if constexpr (CPL >= 32) {
-    if (pass_wide_enabled()) return CPL == 32 ? launch_wide<8>(a, grid, s) : launch_wide<16>(a, grid, s);
+  if constexpr (CPL <= 16) {
+    return launch_tma_u<CPL, 4, 16>(a, grid, s);  // n <= 384: CPL <= 16
+  } else {
+    set_error("fused pass: no TMA variant for n = %lld", (long long)a.n);
+    return ITSK_EINVAL;
   }
-  constexpr int UNR = CPL <= 16 ? 4 : (CPL <= 32 ? 2 : 1);
-  constexpr int NCW = CPL <= 16 ? 16 : 8;  // more consumer warps while c fits in registers
-  return launch_tma_u<CPL, UNR, NCW>(a, grid, s);
 }
 
 int tma_grid(int64_t m, int reserve = 0) {
-  static const int per_sm = [] {
-    const char* e = getenv("ITSK_PASS_CTAS_PER_SM");  // tuning knob
-    return e ? std::max(1, atoi(e)) : 1;
-  }();
+  constexpr int per_sm = 1;
   int64_t g = static_cast<int64_t>(std::max(1, num_sms() - reserve)) * per_sm;
   const int64_t cap = (m + 7) / 8;
   if (g > cap) g = cap;

@@ -174,7 +174,6 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
   double* taus = betas + n;        // NB, current panel
   double* tile = taus + NB;        // RT x CBP: staged W tile / Y staging
   double* Zs = tile + RT * CBP;    // NB x CBP: staged Z chunk
-  __shared__ double s_coef[2];
   int owner = 0;  // owner CTA of row j, advanced monotonically
 
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
@@ -511,12 +510,7 @@ QrPlan qr_plan(void* ws, int64_t d, int64_t n, int has_rhs) {
   const int64_t zld = (N + C - 1) / C + 1;
   const size_t smem_cl = (common_doubles(hmax_c, n) + 2 * C * REC + NB * (NB + N) + NB * zld) * 8;
   L.cluster = smem_cl <= QR_SMEM_MAX;
-  // tuning override: ITSK_QR_MODE=grid|cluster
-  if (const char* e = getenv("ITSK_QR_MODE")) {
-    if (!strcmp(e, "grid")) L.cluster = false;
-  }
-  int grid_cap = num_sms();
-  if (const char* e = getenv("ITSK_QR_GRID")) grid_cap = std::max(1, std::min(grid_cap, atoi(e)));
+  const int grid_cap = num_sms();
   if (L.cluster) {
     L.P = C;
     L.hmax = hmax_c;
@@ -570,9 +564,11 @@ int qr_aug_core(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double*
   ITSK_REQUIRE(L.smem <= QR_SMEM_MAX, "qr: too many rows per CTA (d=%lld, n=%lld)", (long long)d,
                (long long)n);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const char* mode = getenv("ITSK_QR_MODE");
+  // the panel / update split (qr2.cu) wherever its panel fits in a cluster's
+  // shared memory; beyond (more than ~25600 rows at 16-wide panels) the
+  // single-kernel QR below: one cluster, or the whole grid with barriers
   const QrV2Plan V2 = qr_v2_plan(d, n);
-  if (V2.NB > 0 && !(mode && (!strcmp(mode, "v1") || !strcmp(mode, "grid") || !strcmp(mode, "tsqr")))) {
+  if (V2.NB > 0) {
     ITSK_REQUIRE(V2_WS_OFFSET + 8 * V2.ws_doubles <= ws_bytes, "qr workspace too small");
     int* sing = reinterpret_cast<int*>(static_cast<char*>(ws) + 512);
     double* wsd = reinterpret_cast<double*>(static_cast<char*>(ws) + V2_WS_OFFSET);
@@ -582,17 +578,6 @@ int qr_aug_core(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double*
     return ITSK_OK;
   }
   ITSK_CUDA(cudaMemsetAsync(L.bar, 0, 512, s));
-  // Communication-avoiding cluster path (qr_tsqr.cu): correct, but its
-  // 64x32 tree QRs are not yet faster than one exchange per column, so it is
-  // opt-in (ITSK_QR_MODE=tsqr) until the small-QR primitive is tuned.
-  size_t tsqr_smem = 0;
-  const int tsqr_c = (mode && !strcmp(mode, "tsqr")) ? qr_tsqr_plan(d, n, &tsqr_smem) : 0;
-  if (tsqr_c > 0) {
-    int rc = launch_qr_tsqr(W, d, n, ldw, n + has_rhs, R, z, L.singular, tsqr_c, tsqr_smem, s);
-    if (rc) return rc;
-    *flag = L.singular;
-    return ITSK_OK;
-  }
   QrArgs a;
   a.W = W;
   a.d = d;

@@ -1090,13 +1090,7 @@ __global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, 
 }
 
 // Side stream and events of the look-ahead (per device, created once).
-bool lookahead_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ITSK_QR_LOOKAHEAD");  // tuning knob: 0 = update all columns on the main stream
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
+bool lookahead_enabled() { return true; }
 
 // Side streams (per device, created once): 0 = the look-ahead's rest of the
 // trailing matrix, 1 = the far updates, 2 = the critical path (panels, their

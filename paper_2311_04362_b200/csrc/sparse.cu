@@ -37,7 +37,6 @@ namespace {
 
 constexpr int CSR_THREADS = 256;
 constexpr int CHUNK = 1024;      // CSC entries per warp chunk
-constexpr int SK_PREF = 4;       // entries of a source row prefetched per lane
 
 __global__ void k_entry_rows(const int64_t* __restrict__ row_ptr, int64_t m, uint32_t* __restrict__ erow) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

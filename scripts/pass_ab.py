@@ -1,5 +1,5 @@
 """Fused-pass timing and agreement over shapes (CUDA events, 30 launches):
-    ITSK_PASS_ROWS=0|1|16|8|4 python scripts/pass_ab.py [m,n ...]"""
+    python scripts/pass_ab.py [m,n ...]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -13,7 +13,7 @@ for m, n in shapes:
     b = torch.randn(m, dtype=torch.float64, device="cuda", generator=g)
     x = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     ms = fused_pass_timing(lib, A, b, x, 30 if m * n < 4e9 else 10)
-    print(f"rows={os.environ.get("ITSK_PASS_ROWS", "1")} pass m={m} n={n}: {ms * 1e3:9.1f} us  "
+    print(f"pass m={m} n={n}: {ms * 1e3:9.1f} us  "
           f"{8 * m * n / ms / 1e6:7.0f} GB/s", flush=True)
     del A
     torch.cuda.empty_cache()

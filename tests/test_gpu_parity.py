@@ -176,14 +176,12 @@ def test_qr_matches_lapack(pkg, orc, m, n, seed):
     assert np.linalg.norm(f.z - z_ref) <= 100 * n * U * np.linalg.norm(rhs)
 
 
-@pytest.mark.parametrize("mode", ["v1", "grid", "tsqr"])
-@pytest.mark.parametrize("m,n,seed", [(200, 40, 2), (4000, 201, 4), (5000, 500, 7)])
-def test_qr_alternate_paths_match_lapack(pkg, orc, monkeypatch, mode, m, n, seed):
-    """The QR paths selected by ITSK_QR_MODE (the round-1 cluster kernel, its
-    grid-barrier form, the communication-avoiding cluster TSQR) against LAPACK
-    with the default path's bar; the default (panel / update split) is
-    covered by test_qr_matches_lapack."""
-    monkeypatch.setenv("ITSK_QR_MODE", mode)
+@pytest.mark.parametrize("m,n,seed", [(40000, 64, 2), (30000, 130, 4)])
+def test_qr_large_d_fallback_matches_lapack(pkg, orc, m, n, seed):
+    """Beyond the panel kernel's shared memory (more than ~25600 rows at
+    16-wide panels) itsk_qr_aug runs the single-kernel QR (qr.cu: one
+    cluster, or the whole grid with barriers); held to the same bar as the
+    panel / update path."""
     rng = np.random.default_rng(seed)
     a = rng.standard_normal((m, n))
     rhs = rng.standard_normal(m)
