@@ -128,6 +128,15 @@ int itsk_trsv(const double* R, int64_t n, const double* c, double* y, int trans,
  * tail's arithmetic).  Used for x0 = R^-1 z and LSQR's solves. */
 int itsk_trsv_rp(const double* R, const double* Rp, int64_t n, const double* c, double* y, int trans,
                  itsk_stream_t stream);
+/* The loop's solve pair d = R^{-1} R^{-T} c (solvers.py:339-340) on a
+ * 16-CTA thread-block cluster: 32-row blocks owned round robin, each
+ * block's chain warp waits for its predecessor's values (pushed through
+ * distributed shared memory), helper warps add the older terms; fixed-order
+ * sums (reproducible).  n <= 4096.  Rp: itsk_pack_upper's layout (its
+ * diagonal-block inverses) or NULL.  The loop tail uses the same code when
+ * R's triangle does not fit one CTA's shared memory. */
+int itsk_trsv_pair_cl(const double* R, const double* Rp, int64_t n, const double* c, double* d,
+                      itsk_stream_t stream);
 int itsk_trsv_pair(const double* R, int64_t n, const double* c, double* y, double* tmp,
                    itsk_stream_t stream);
 

@@ -90,6 +90,7 @@ _SIGS = {
     "itsk_qr_aug_async": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_dp, c_dp]),
     "itsk_trsv": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, ctypes.c_int, c_dp]),
     "itsk_trsv_rp": (ctypes.c_int, [c_dp, c_dp, c_i64, c_dp, c_dp, ctypes.c_int, c_dp]),
+    "itsk_trsv_pair_cl": (ctypes.c_int, [c_dp, c_dp, c_i64, c_dp, c_dp, c_dp]),
     "itsk_trsv_pair": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, c_dp, c_dp]),
     "itsk_normest": (ctypes.c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_dp, c_dp]),
     "itsk_pack_upper_doubles": (ctypes.c_int, [c_i64, ctypes.POINTER(c_i64)]),

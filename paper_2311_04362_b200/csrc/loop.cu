@@ -20,6 +20,7 @@
 
 #include "itsk_common.cuh"
 #include "itsk_dense.cuh"
+#include "itsk_trsv_cluster.cuh"
 #include "itsk_kernels.cuh"
 
 namespace itsk {
@@ -453,6 +454,92 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_tail(LoopPtrs p, int flags, i
   TL(5);
 }
 
+// Large n (R's triangle beyond shared memory, n <= TCL_NMAX): the tail on a
+// cluster of TCL_NC CTAs.  CTA 0 runs the control step exactly as k_tail
+// (the same 512-thread block sums, so a replayed stopping rule sees the same
+// bits); after a cluster barrier every CTA takes its share of the
+// triangular-solve pair (itsk_trsv_cluster.cuh) and the owner of each
+// 32-row block writes that block of x_{it+1} in the reference's operation
+// order.
+__global__ void __launch_bounds__(DENSE_THREADS, 1) k_tail_cl(LoopPtrs p, int flags,
+                                                             cudaGraphConditionalHandle h, int use_cond) {
+  namespace cg = cooperative_groups;
+  pdl_trigger();
+  extern __shared__ __align__(16) double sm_cl[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = static_cast<int>(cl.block_rank());
+  pdl_wait();
+  constexpr int CTL_WORDS = sizeof(LoopCtl) / 8;
+  __shared__ LoopCtl s_ctl;
+  if (q == 0) {
+    if (threadIdx.x < CTL_WORDS)
+      reinterpret_cast<uint64_t*>(&s_ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(p.ctl)[threadIdx.x];
+    __syncthreads();
+    LoopCtl* ctl = &s_ctl;
+    if (!ctl->result.done) {
+      if (p.ng > 0) tail_group_sum(p);
+      if (p.peer.size > 0) peer_gather(p, ctl->epoch_base, (flags & TAIL_BEGIN) ? 0 : ctl->it + 1);
+      int done = 0;
+      if (flags & TAIL_CONTROL) {
+        done = control_step(p, ctl, (flags & TAIL_BEGIN) ? 1 : 0);
+        if (threadIdx.x < CTL_WORDS)
+          reinterpret_cast<uint64_t*>(p.ctl)[threadIdx.x] = reinterpret_cast<const uint64_t*>(&s_ctl)[threadIdx.x];
+      }
+      if (done && use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+    } else if (use_cond && threadIdx.x == 0) {
+      cudaGraphSetConditional(h, 0);
+    }
+    __threadfence();
+  }
+  cl.sync();  // the loop state CTA 0 wrote is visible to the cluster
+  const LoopCtl* g = p.ctl;
+  if (__ldcg(&g->result.done) || !(flags & TAIL_STEP)) return;
+  const int64_t n = p.n;
+  const int64_t it = __ldcg(&g->it);
+  const double* x = p.xs + it * n;
+  const double* xp = p.xs + (it > 0 ? it - 1 : 0) * n;
+  double* xn = p.xs + (it + 1) * n;
+  const double alpha = __ldcg(&g->alpha), beta = __ldcg(&g->beta);
+  const bool basic = __ldcg(&g->variant) == ITSK_VARIANT_BASIC;
+  trsv_pair_cluster(p.R, p.Rp, static_cast<int>(n), p.cs, sm_cl, [&](int b, int lane, double di) {
+    const int64_t i = 32 * b + lane;
+    const double xi = x[i];
+    if (basic) {
+      xn[i] = __dadd_rn(xi, di);
+    } else {
+      const double t = __dadd_rn(xi, __dmul_rn(alpha, di));
+      xn[i] = __dadd_rn(t, __dmul_rn(beta, __dsub_rn(xi, xp[i])));
+    }
+  });
+}
+
+// The cluster pair alone: d = R^{-1} R^{-T} c (itsk_trsv_pair_cl, tests).
+__global__ void __launch_bounds__(DENSE_THREADS, 1) k_trsv_pair_cl(const double* R, const double* Rp, int64_t n,
+                                                                  const double* c, double* d) {
+  extern __shared__ __align__(16) double sm_cl[];
+  trsv_pair_cluster(R, Rp, static_cast<int>(n), c, sm_cl, [&](int b, int lane, double v) { d[32 * b + lane] = v; });
+}
+
+bool tail_on_cluster(int64_t n) { return !use_packed(n, n + 32) && n <= TCL_NMAX; }
+
+cudaError_t launch_cluster_pdl(const void* func, int64_t n, cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(TCL_NC);
+  cfg.blockDim = dim3(DENSE_THREADS);
+  cfg.dynamicSmemBytes = tcl_smem_bytes(n);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = TCL_NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelExC(&cfg, func, args);
+}
+
 struct LoopLayout {
   LoopCtl* ctl;
   double* step;
@@ -610,6 +697,15 @@ size_t trsv_smem(int64_t n) {
 
 int enqueue_tail(const itsk_loop_params* p, const LoopPtrs& q, int flags, int grid, cudaStream_t s,
                  cudaGraphConditionalHandle cond = cudaGraphConditionalHandle{}, int use_cond = 0) {
+  if (tail_on_cluster(p->n)) {
+    (void)grid;
+    LoopPtrs qq = q;
+    void* args[] = {&qq, &flags, &cond, &use_cond};
+    ITSK_CUDA(launch_cluster_pdl(reinterpret_cast<const void*>(k_tail_cl), p->n, s, args));
+    count_launch();
+    ITSK_CHECK_LAUNCH();
+    return ITSK_OK;
+  }
   const size_t smem = (flags & TAIL_STEP) ? trsv_smem(p->n) : 0;
   const void* fn = trsv_packed(p->n) ? reinterpret_cast<const void*>(k_tail<true>)
                                      : reinterpret_cast<const void*>(k_tail<false>);
@@ -623,6 +719,8 @@ int prepare_attrs(int64_t n) {
   (void)n;
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_tail<true>)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_tail<false>)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_tail_cl)));
+  ITSK_CUDA(func_attr_once(reinterpret_cast<const void*>(k_tail_cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   return ITSK_OK;
 }
 
@@ -802,6 +900,31 @@ extern "C" int itsk_loop_finish(const itsk_loop_params* p, itsk_stream_t stream)
   if (!p->est_ready) return ITSK_OK;
   LoopPtrs q = make_ptrs(p);
   k_loop_finish<<<1, DENSE_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(q);
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+extern "C" int itsk_trsv_pair_cl(const double* R, const double* Rp, int64_t n, const double* c, double* d,
+                                 itsk_stream_t stream) {
+  ITSK_REQUIRE(R && c && d && n >= 1 && n <= TCL_NMAX, "cluster TRSV pair: bad arguments (n <= %d)", TCL_NMAX);
+  const void* fn = reinterpret_cast<const void*>(k_trsv_pair_cl);
+  ITSK_CUDA(allow_max_smem(fn));
+  ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(TCL_NC);
+  cfg.blockDim = dim3(DENSE_THREADS);
+  cfg.dynamicSmemBytes = tcl_smem_bytes(n);
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = TCL_NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&R, &Rp, &n, &c, &d};
+  ITSK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;

@@ -728,3 +728,50 @@ def test_c3_full_size_parity(pkg, orc, seed):
     assert tr.fe[-1] <= 2 * tr_ref.fe[-1], (tr.fe[-1], tr_ref.fe[-1])
     assert tr.re[-1] <= 2 * tr_ref.re[-1], (tr.re[-1], tr_ref.re[-1])
     assert dev_x <= 10 * 1e15 * U + tr_ref.fe[-1]
+
+
+@pytest.mark.parametrize("n,kappa,illblock", [(500, 1e8, False), (1000, 1e10, False), (2000, 1e8, False),
+                                              (2047, 1e6, True), (4096, 1e4, False), (777, 1e12, True)])
+def test_trsv_pair_cluster(pkg, n, kappa, illblock):
+    """The cluster solve pair (itsk_trsv_pair_cl, the loop tail's solves for
+    large n) against a float64 reference solve: residual-based bar as the
+    single-CTA TRSV tests; with `illblock` some diagonal blocks are made
+    ill conditioned so the register substitution path runs instead of the
+    stored inverse.  Bitwise reproducible across runs."""
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = kappa ** (-np.arange(n) / (n - 1))
+    r = np.linalg.qr((q * s) @ np.linalg.qr(rng.standard_normal((n, n)))[0].T, mode="r")
+    r = r * np.sign(np.diag(r))[:, None]
+    if illblock:
+        # two diagonal blocks made ill conditioned (kappa_1 past the inverse's
+        # threshold): their solves take the register substitution chain
+        for b0 in (64, 32 * (n // 64)):
+            r[b0 + 5, b0 + 5] *= 1e-6
+    c = rng.standard_normal(n)
+    dev = torch.device("cuda")
+    R = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
+    nb = ctypes.c_int64()
+    lib = dv.lib(dev)
+    _lib.check(lib.itsk_pack_upper_doubles(n, ctypes.byref(nb)))
+    Rp = torch.empty(nb.value, dtype=torch.float64, device=dev)
+    _lib.check(lib.itsk_pack_upper(dv.ptr(R), n, dv.ptr(Rp), dv.stream_ptr()))
+    ct = torch.from_numpy(c).to(dev)
+    outs = []
+    for rep in range(3):
+        d = torch.full((n,), float("nan"), dtype=torch.float64, device=dev)
+        _lib.check(lib.itsk_trsv_pair_cl(dv.ptr(R), dv.ptr(Rp), n, dv.ptr(ct), dv.ptr(d), dv.stream_ptr()))
+        outs.append(d.cpu().numpy())
+    assert all(np.array_equal(o, outs[0]) for o in outs[1:])
+    d = outs[0]
+    assert np.isfinite(d).all()
+    # backward-error form: R' R d = c to ~ n u ||R||^2 ||d||
+    res = r.T @ (r @ d) - c
+    assert np.linalg.norm(res) <= 100 * n * U * np.linalg.norm(r, 2) ** 2 * np.linalg.norm(d) + 100 * n * U * np.linalg.norm(c)
+    import scipy.linalg as sl
+    ref = sl.solve_triangular(r, sl.solve_triangular(r, c, trans="T"))
+    cond = np.linalg.cond(r)
+    assert np.linalg.norm(d - ref) <= 1e3 * n * U * cond ** 2 * np.linalg.norm(ref) + 1e-300
