@@ -510,14 +510,13 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
 // on a stage always follows that group's own previous batch there (no
 // mbarrier phase aliasing without a stage-tag check).
 // ---------------------------------------------------------------------------
-constexpr int RW_NCW = 16, RW_RB = 4, RW_CPP = 2;
+constexpr int RW_NCW = 16, RW_RB = 4;
 
-template <int GW>
-__global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, TmaShape sh) {
-  constexpr int NG = RW_NCW / GW, GT = 32 * GW, RB = RW_RB, CPP = RW_CPP;
+template <int GW, int CPP>
+__global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaShape sh) {
+  constexpr int NG = RW_NCW / GW, GT = 32 * GW, RB = RW_RB;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* empty = full + 32;
   unsigned char* stages = smraw + 1024;
   __shared__ double dpart[NG][2][GW][RB];
   __shared__ double ssm[NG][4];
@@ -537,16 +536,16 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
   const int npre = min(S, ntiles);
 
   if (tid == 0) {
-    for (int st = 0; st < S; ++st) {
-      mbar_init(full + st, 1);
-      mbar_init(empty + st, GW);  // one arrival per warp of the consuming group
-    }
+    for (int st = 0; st < S; ++st) mbar_init(full + st, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   pdl_trigger();
-  if (warp == RW_NCW && lane == 0) {
-    const uint64_t pol = evict_first_policy();
+  // the ring's first S batches; batch t + S is issued into stage t % S by
+  // the consuming group once all its warps passed the group barrier of
+  // batch t (their values of the stage are in registers by then)
+  const uint64_t pol = evict_first_policy();
+  if (tid == 0) {
     for (int t = 0; t < npre; ++t) {
       const int rows = min(RB, nrows - t * RB);
       const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
@@ -569,7 +568,7 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
     if (tid == 0) s_done = ctl->result.done;
     __syncthreads();
     if (s_done) {
-      if (warp == RW_NCW && lane == 0)
+      if (tid == 0)
         for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
       return;
     }
@@ -594,20 +593,7 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
     col[j] = 2 * gt + 2 * GT * j;
   }
 
-  if (warp == RW_NCW) {
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      for (int t = npre; t < ntiles; ++t) {
-        const int st = t % S;
-        mbar_wait(empty + st, static_cast<unsigned>(((t / S) - 1) & 1));
-        const int rows = min(RB, nrows - t * RB);
-        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
-        mbar_expect_tx(full + st, bytes);
-        bulk_g2s(stages + static_cast<int64_t>(st) * sh.stage_bytes, a.A + (r_begin + t * RB) * lda, bytes,
-                 full + st, pol);
-      }
-    }
-  } else {
+  {
     double2 xv[CPP];
 #pragma unroll
     for (int j = 0; j < CPP; ++j) {
@@ -661,8 +647,6 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
           }
           v[u][j] = w;
         }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);  // the stage is in registers: release it
       double d[RB];
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
@@ -689,6 +673,15 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
         if ((lane & 7) == 0) dpart[g][par][gw][lane >> 3] = kk;
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GT) : "memory");
+      // every warp of the group has its values of stage st: refill it
+      if (gw == 0 && lane == 0 && t + S < ntiles) {
+        const int tn = t + S;
+        const int rows = min(RB, nrows - tn * RB);
+        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+        mbar_expect_tx(full + st, bytes);
+        bulk_g2s(stages + static_cast<int64_t>(st) * sh.stage_bytes, a.A + (r_begin + tn * RB) * lda, bytes,
+                 full + st, pol);
+      }
       // the group's GW partials per row, summed in a fixed tree (the same
       // bits in every warp of the group)
       double q[VPL];
@@ -769,7 +762,7 @@ __global__ void __launch_bounds__(32 * (RW_NCW + 1), 1) k_pass_rows(PassArgs a, 
       }
     }
     __syncthreads();
-    for (int c = tid; c < n; c += 32 * (RW_NCW + 1)) {
+    for (int c = tid; c < n; c += 32 * RW_NCW) {
       double sum = 0.0;
 #pragma unroll
       for (int gg = 0; gg < NG; ++gg) sum += csm[gg * W + c];
@@ -922,7 +915,7 @@ int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
 }
 
 
-template <int GW>
+template <int GW, int CPP>
 int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
   constexpr int NG = RW_NCW / GW;
   PassArgs a = a0;
@@ -932,13 +925,13 @@ int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
   // a multiple of NG stages (see the kernel), <= 32 mbarriers, and room for
   // the groups' c partials at the end
   int S = std::min(32, (TMA_SMEM_BUDGET - 1024) / sh.stage_bytes) / NG * NG;
-  const int red = NG > 1 ? NG * 2 * 32 * GW * RW_CPP * 8 : 0;
+  const int red = NG > 1 ? NG * 2 * 32 * GW * CPP * 8 : 0;
   while (S * sh.stage_bytes < red) S += NG;
   sh.S = std::max(NG, S);
   a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
   const size_t smem = 1024 + static_cast<size_t>(sh.S) * sh.stage_bytes;
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rows<GW>)));
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rows<GW>), dim3(grid), dim3(32 * (RW_NCW + 1)),
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rows<GW, CPP>)));
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rows<GW, CPP>), dim3(grid), dim3(32 * RW_NCW),
                        smem, s, a, sh));
   count_launch();
   ITSK_CHECK_LAUNCH();
@@ -951,9 +944,9 @@ int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
   // n = 500, 600, 1000, 2000 faster than the warp-per-row kernel; n = 200,
   // 300 slower, profiles/rd2_pass_rows_ab.txt)
   if (a.n > 384) {
-    if (a.n > 1024) return launch_rows<16>(a, grid, s);
-    if (a.n > 512) return launch_rows<8>(a, grid, s);
-    return launch_rows<4>(a, grid, s);
+    if (a.n > 1024) return launch_rows<16, 2>(a, grid, s);
+    if (a.n > 512) return launch_rows<8, 2>(a, grid, s);
+    return launch_rows<4, 2>(a, grid, s);
   }
   if constexpr (CPL <= 16) {
     return launch_tma_u<CPL, 4, 16>(a, grid, s);  // n <= 384: CPL <= 16
