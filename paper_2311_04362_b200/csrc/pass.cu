@@ -251,8 +251,8 @@ __device__ unsigned long long g_pass_tl[TL_SLOTS][4];
 #endif
 
 template <int CPL, int UNR, int NCW>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaShape sh) {
-  constexpr int THREADS = 32 * (NCW + 1);
+__global__ void __launch_bounds__(32 * NCW, 1) k_pass_tma(PassArgs a, TmaShape sh) {
+  constexpr int THREADS = 32 * NCW;
 #ifdef ITSK_TIMELINE
   const unsigned long long tl_t0 = gtime();
   int tl_slot = -1;
@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
   constexpr int NC = 32 * CPL;
   constexpr bool XREG = CPL <= 8;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* empty = full + 32;
-  int* stage_tile = reinterpret_cast<int*>(empty + 32);
+  unsigned* consumed = reinterpret_cast<unsigned*>(full + 32);  // batches of a stage's tile read so far
+  int* stage_tile = reinterpret_cast<int*>(consumed + 32);
   double* xsm = reinterpret_cast<double*>(smraw + 1024);
   unsigned char* stages = smraw + 1024 + (XREG ? 0 : NC * 8);
   __shared__ double ssm[NCW][4];
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, T / UNR);  // one arrival per consumed batch
+      consumed[s] = 0u;
       stage_tile[s] = -1;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -294,8 +294,12 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
   // runs; everything the previous kernel writes (x, the loop state) is read
   // after griddepcontrol.wait.
   pdl_trigger();
-  if (warp == NCW && lane == 0) {
-    const uint64_t pol = evict_first_policy();
+  // no producer warp: the consumer that reads the last batch of a stage's
+  // tile refills the stage with tile t + S (a per-stage counter; the bulk
+  // copy is ordered after every warp's reads of the stage by the counter's
+  // acquire-release and a proxy fence)
+  const uint64_t pol = evict_first_policy();
+  if (tid == 0) {
     for (int t = 0; t < npre; ++t) {
       const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
       const int rows = min(T, nrows - t * T);
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
     __syncthreads();
     if (s_done) {
       // loop finished: drain the prefetched copies before the CTA exits
-      if (warp == NCW && lane == 0)
+      if (tid == 0)
         for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
       return;
     }
@@ -347,22 +351,7 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
 #pragma unroll
   for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
 
-  if (warp == NCW) {
-    // ---------------- producer: one elected lane, one bulk copy per tile ---
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      for (int t = npre; t < ntiles; ++t) {
-        const int s = t % S;
-        if (t >= S) mbar_wait(empty + s, static_cast<unsigned>(((t / S) - 1) & 1));
-        const int64_t row0 = r_begin + static_cast<int64_t>(t) * T;
-        const int rows = min(T, nrows - t * T);
-        const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
-        reinterpret_cast<volatile int*>(stage_tile)[s] = t;
-        mbar_expect_tx(full + s, bytes);
-        bulk_g2s(stages + static_cast<int64_t>(s) * sh.stage_bytes, a.A + row0 * lda, bytes, full + s, pol);
-      }
-    }
-  } else {
+  {
     // ---------------- consumers ----------------
     double xv[XREG ? CPL : 1];
     if (XREG) {
@@ -428,7 +417,25 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassArgs a, TmaS
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);  // release after every read of the stage
+      if (lane == 0) {
+        // the last of the tile's T / UNR batches read: refill the stage
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(consumed + s)) : "memory");
+        if (old == static_cast<unsigned>(T / UNR - 1)) {
+          consumed[s] = 0u;
+          const int tn = t + S;
+          if (tn < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int rows = min(T, nrows - tn * T);
+            const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
+            reinterpret_cast<volatile int*>(stage_tile)[s] = tn;
+            mbar_expect_tx(full + s, bytes);
+            bulk_g2s(stages + static_cast<int64_t>(s) * sh.stage_bytes, a.A + (r_begin + static_cast<int64_t>(tn) * T) * lda,
+                     bytes, full + s, pol);
+          }
+        }
+      }
       if (lane < nu) {
         double rl = r[0];
 #pragma unroll
@@ -907,7 +914,7 @@ int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
   a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
   const size_t smem = tma_smem(sh, CPL);
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>)));
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>), dim3(grid), dim3(32 * (NCW + 1)),
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_tma<CPL, UNR, NCW>), dim3(grid), dim3(32 * NCW),
                        smem, s, a, sh));
   count_launch();
   ITSK_CHECK_LAUNCH();

@@ -62,6 +62,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   const int nbytes = valid ? 8 : 0;  // 0: zero-fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(nbytes) : "memory");
 }
+// 16 bytes, the first `src_bytes` (0, 8 or 16) from global, the rest zero
+__device__ __forceinline__ void cp_async16z(double* dst, const double* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -912,11 +917,26 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next2(UpdArgs a) {
   double* Ys = Yq + NB * NB;                // NB x NB: the sum, then Z
   double* Yo = Ys + NB * NB;                // NB x NB: elements this CTA owns, summed
   const int nch = (h + NX_RC - 1) / NX_RC;
+  // 16-byte copies where W's rows are 16-byte aligned (even ldw; k0, c0 are
+  // multiples of 16), a partial pair zero-filled by the source size
+  const bool vec16 = (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(a.W) & 15) == 0;
   auto load = [&](int ch) {
     const int st = ch % NX_ST;
     double* vs = Vs + st * NX_RC * NX_S;
     double* bs = Bs + st * NX_RC * NX_S;
     const int r0 = ch * NX_RC;
+    if (vec16) {
+      for (int idx = tid; idx < NX_RC * (NB / 2); idx += QP_THREADS) {
+        const int rr = idx / (NB / 2), c = 2 * (idx - rr * (NB / 2));
+        const int64_t r = lo + r0 + rr;
+        const bool rok = r0 + rr < h;
+        const int sv = rok ? 8 * max(0, min(2, kb - c)) : 0;
+        const int sb = rok ? 8 * max(0, min(2, nb2 - c)) : 0;
+        cp_async16z(vs + rr * NX_S + c, a.W + (sv ? r * ldw + k0 + c : 0), sv);
+        cp_async16z(bs + rr * NX_S + c, a.W + (sb ? r * ldw + a.c0 + c : 0), sb);
+      }
+      return;
+    }
     for (int idx = tid; idx < NX_RC * NB; idx += QP_THREADS) {
       const int rr = idx / NB, c = idx - rr * NB;
       const int64_t r = lo + r0 + rr;
@@ -1002,10 +1022,14 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_next2(UpdArgs a) {
     const int jl = lane < NB ? lane : 0;
     double t = lane < kb ? Ys[jl * NB + c] : 0.0;
     const double mytau = lane < kb ? a.taus[k0 + jl] : 0.0;
+    // lane j's column of G in registers, all loads in flight before the chain
+    double gcol[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) gcol[i] = a.G[i * NB + jl];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       if (i >= kb) break;
-      const double g = a.G[i * NB + jl];
+      const double g = gcol[i];
       const double zi = __shfl_sync(FULL, mytau * t, i);
       if (lane == i) t = zi;
       else if (lane > i) t = fma(-g, zi, t);

@@ -230,10 +230,10 @@ def _shard_prepare(a_local, b_local, cfg: SolverConfig, m_total: int, row0: int,
         _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), _dev.ptr(ws.pat_ws), ws.pat_ws.numel(), stream))
     if csr is not None:
         _lib.check(lib.itsk_csr_sketch(csr.plan, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), cfg.d,
-                                       cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
+                                       cfg.zeta, _dev.ptr(ws.W), ws.ldw, stream))
     else:
         _lib.check(lib.itsk_sketch(_dev.ptr(at), m_loc, n, lda, _dev.ptr(ws.b), _dev.ptr(ws.sk_ptr),
-                                   _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), n + 1, stream))
+                                   _dev.ptr(ws.sk_src), cfg.d, cfg.zeta, _dev.ptr(ws.W), ws.ldw, stream))
     return ws, at, lda, csr
 
 
@@ -246,7 +246,7 @@ def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange
     lib = _dev.lib(ws.dev)
     n = ws.n
     stream = _dev.stream_ptr()
-    _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
+    _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, ws.ldw, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     if cfg.init == "zero":
@@ -319,7 +319,7 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     def allreduce(t: torch.Tensor):
         tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=group)
 
-    allreduce(ws.W)
+    allreduce(ws.Wbuf)  # the whole padded buffer (contiguous; the pad column is zero)
     if peer == "require" and csr is not None:
         raise ValueError("peer='require': the peer exchange carries dense loops only")
     px = peer_exchange(n, ws.dev, group, require=peer == "require") if (peer != "nccl" and csr is None) else None

@@ -204,7 +204,11 @@ class _Workspace:
         nb = ctypes.c_int64()
         _lib.check(lib.itsk_pattern_workspace(d, m, zeta, ctypes.byref(nb)))
         self.pat_ws = _dev.workspace(nb.value, dev)
-        self.W = torch.empty((d, n + 1), **f64)
+        # W = [SA | Sb] at an even leading dimension (16-byte aligned rows for
+        # the QR's vector copies); the pad column stays zero
+        self.ldw = (n + 2) // 2 * 2
+        self.Wbuf = torch.zeros((d, self.ldw), **f64)
+        self.W = self.Wbuf[:, :n + 1]
         _lib.check(lib.itsk_qr_workspace(d, n, ctypes.byref(nb)))
         self.qr_ws = _dev.workspace(nb.value, dev)
         self.R = torch.empty((n, n), **f64)
@@ -386,16 +390,16 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
                 copy_chunk(r0, r1)
             compute.wait_event(events[k])
             _lib.check(lib.itsk_sketch_rows(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
-                                            _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, r0, r1,
+                                            _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), ws.ldw, r0, r1,
                                             1 if k else 0, stream))
     elif csr is not None:
         _lib.check(lib.itsk_csr_sketch(csr.plan, _dev.ptr(bt), _dev.ptr(ws.sk_ptr), _dev.ptr(ws.sk_src), d, zeta,
-                                       _dev.ptr(ws.W), n + 1, stream))
+                                       _dev.ptr(ws.W), ws.ldw, stream))
     else:
         _lib.check(lib.itsk_sketch(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
-                                   _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), n + 1, stream))
+                                   _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), ws.ldw, stream))
     # no host round trip: the zero-pivot flag is read with the results
-    _lib.check(lib.itsk_qr_aug_async(_dev.ptr(ws.W), d, n, n + 1, _dev.ptr(ws.R), _dev.ptr(ws.z),
+    _lib.check(lib.itsk_qr_aug_async(_dev.ptr(ws.W), d, n, ws.ldw, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                      _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), _dev.ptr(ws.sing), stream))
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     # condest (a 2-CTA cluster, the longest of the three) runs beside x0 and

@@ -36,11 +36,11 @@ def T(fn, reps=5):
 words, h, pend = pcg_state(0)
 out = {}
 out["pattern"] = T(lambda: _lib.check(lib.itsk_sparse_sign_pattern(d, m, zeta, words, h, pend, dv.ptr(ws.rows), dv.ptr(ws.neg), dv.ptr(ws.sk_ptr), dv.ptr(ws.sk_src), dv.ptr(ws.pat_ws), ws.pat_ws.numel(), s)))
-out["sketch"] = T(lambda: _lib.check(lib.itsk_sketch(dv.ptr(at), m, n, n, dv.ptr(bt), dv.ptr(ws.sk_ptr), dv.ptr(ws.sk_src), d, zeta, dv.ptr(ws.W), n+1, s)))
+out["sketch"] = T(lambda: _lib.check(lib.itsk_sketch(dv.ptr(at), m, n, n, dv.ptr(bt), dv.ptr(ws.sk_ptr), dv.ptr(ws.sk_src), d, zeta, dv.ptr(ws.W), ws.ldw, s)))
 W0 = ws.W.clone()
 def qr():
     ws.W.copy_(W0)
-    _lib.check(lib.itsk_qr_aug(dv.ptr(ws.W), d, n, n+1, dv.ptr(ws.R), dv.ptr(ws.z), dv.ptr(ws.qr_ws), ws.qr_ws.numel(), s))
+    _lib.check(lib.itsk_qr_aug(dv.ptr(ws.W), d, n, ws.ldw, dv.ptr(ws.R), dv.ptr(ws.z), dv.ptr(ws.qr_ws), ws.qr_ws.numel(), s))
 out["qr(+copy)"] = T(qr)
 out["copyW"] = T(lambda: ws.W.copy_(W0))
 out["trsv_x0"] = T(lambda: _lib.check(lib.itsk_trsv(dv.ptr(ws.R), n, dv.ptr(ws.z), dv.ptr(ws.xs[0]), 0, s)))
