@@ -104,6 +104,197 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   }
 }
 
+// Window sweep for a large A (the gather above re-reads A zeta times from
+// HBM: at C4 504 GB of DRAM reads for 64 GB of A, L2 hit rate 2%,
+// profiles/rd2_sketch_window_deadend.txt).  One persistent launch, one CTA
+// per SM: a warp owns up to SW_RPW sketch rows (i = warp, warp + NW, ...),
+// and the grid sweeps the source rows in windows of R rows, 64 columns (a
+// panel) at a time: every warp adds the sources of its rows that fall in the
+// current window, in ascending order, then counts itself done with the
+// window.  A warp may start window g only when every warp has finished
+// window g - SW_DRIFT (a per-window arrival counter; it orders nothing, A is
+// read-only — it only bounds the L2 working set), so all zeta readers of a
+// source row find its 512-byte panel segment in L2 and A is read from HBM
+// about once.
+// The window's (row, source) pairs of a warp are walked as ONE flattened list
+// in chunks of SW_U sources (one 16-byte load per lane each, SW_U in flight,
+// the next chunk's source words loaded under them), so the latency paid per
+// window is ~(pairs / SW_U), not (rows x rounds); each row's running sum
+// lives in shared memory between its window segments.  Every output is the
+// same sum in the same order as k_sketch_gather: bitwise scipy's.
+constexpr int SW_WARPS = 16, SW_RPW = 12, SW_DRIFT = 2;
+// CL adjacent columns per lane (a panel of 32 CL), U sources per chunk
+template <int CL>
+constexpr size_t sw_smem_bytes() { return sizeof(double) * SW_WARPS * SW_RPW * 32 * CL; }
+
+template <int CL, int U>
+__global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
+    const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
+    const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
+    double* __restrict__ W, int64_t ldw, uint32_t m, uint32_t R, int nwin, int npanel, unsigned* wdone,
+    uint32_t* __restrict__ bnd, int flags) {
+  const int vec = flags & 1;
+  static_assert(CL == 2 || CL == 4, "columns per lane");
+  constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
+  extern __shared__ __align__(16) double sw_sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t NW = static_cast<int64_t>(gridDim.x) * SW_WARPS;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * SW_WARPS + warp;
+  const int64_t ncol = n + (b ? 1 : 0);
+  double2* acc_sm = reinterpret_cast<double2*>(sw_sm + static_cast<int64_t>(warp) * SW_RPW * PANEL);
+  // lane k < SW_RPW holds row k = gw + NW * k (an empty range past d)
+  const int64_t myrow = gw + NW * lane;
+  const bool rowok = lane < SW_RPW && myrow < d;
+  const uint32_t r0 = rowok ? ptr[myrow] : 0u, r1 = rowok ? ptr[myrow + 1] : 0u;
+  // prologue: the end of every window's segment of every own row, from one
+  // coalesced pass over the rows' (ascending) sources: positions p-1, p in
+  // windows wp < wc end windows [wp, wc) at p; the row end is a sentinel in
+  // window nwin.
+  uint32_t* wb = bnd + gw * SW_RPW * static_cast<int64_t>(nwin);
+  for (int k = 0; k < SW_RPW; ++k) {
+    const uint32_t a0 = __shfl_sync(FULL, r0, k), a1 = __shfl_sync(FULL, r1, k);
+    int carry = 0;
+    for (uint32_t q = a0; q <= a1; q += 32) {
+      const uint32_t p = q + lane;
+      const int wc = p < a1 ? static_cast<int>((src[p] & 0x7fffffffu) / R) : nwin;
+      int wp = __shfl_up_sync(FULL, wc, 1);
+      if (lane == 0) wp = carry;
+      if (p <= a1)
+        for (int w = wp; w < wc; ++w) wb[k * nwin + w] = p;
+      carry = __shfl_sync(FULL, wc, 31);
+    }
+  }
+  __syncwarp();
+  const unsigned arrivals = gridDim.x * SW_WARPS;
+  for (int p = 0; p < npanel; ++p) {
+    // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
+    // warp is one contiguous 512-byte segment)
+    const int64_t cA = static_cast<int64_t>(p) * PANEL + 2 * lane;
+    const bool allv = __all_sync(FULL, vec && cA + 64 * (NV - 1) + 1 < n);
+    int kind[CL];
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+      const int64_t col = cA + 64 * (c >> 1) + (c & 1);
+      kind[c] = col < n ? 0 : (col == n && b ? 1 : 2);
+    }
+    const double* Ap = A + static_cast<int64_t>(p) * PANEL;
+    const double* Ac = Ap + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < SW_RPW; ++k)
+#pragma unroll
+      for (int h = 0; h < NV; ++h) acc_sm[k * 16 * CL + 32 * h + lane] = make_double2(0.0, 0.0);
+    __syncwarp();
+    uint32_t sk = r0;  // lane k: row k's first source in the current window
+    for (int w = 0; w < nwin; ++w) {
+      const int g = p * nwin + w;
+      if (g >= SW_DRIFT) {
+        if (lane == 0)
+          while (*reinterpret_cast<volatile unsigned*>(wdone + g - SW_DRIFT) < arrivals) __nanosleep(32);
+        __syncwarp();
+      }
+      const uint32_t tk = lane < SW_RPW ? wb[lane * nwin + w] : 0u;
+      const uint32_t cnt = lane < SW_RPW ? tk - sk : 0u;
+      uint32_t incl = cnt;  // inclusive scan: row k covers flattened positions [incl - cnt, incl)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(FULL, incl, 31);
+      const uint32_t base = sk - (incl - cnt);  // source index = base_k + position
+      // lane u: position P + u (clamped into the window's list, so every
+      // lane's row pointer is valid; positions past the end are not added):
+      // its row and sign packed in ku, its source row's panel segment in pu
+      auto locate = [&](uint32_t P, int& ku, uint32_t& sv, const double*& pu) {
+        const uint32_t pos = min(P + static_cast<uint32_t>(lane & (U - 1)), total - 1);
+        int k = 0;
+#pragma unroll
+        for (int kk = 0; kk < SW_RPW - 1; ++kk) k += pos >= __shfl_sync(FULL, incl, kk) ? 1 : 0;
+        const uint32_t bk = __shfl_sync(FULL, base, k);
+        sv = __ldg(src + bk + pos);
+        ku = (k << 1) | static_cast<int>(sv >> 31);
+        pu = Ap + static_cast<int64_t>(sv & 0x7fffffffu) * lda;  // the panel's start: lane-independent
+      };
+      int ku = 0, kcur = -1;
+      uint32_t sv = 0;
+      const double* pu = Ap;
+      double2 acc[NV];
+      if (total > 0) locate(0, ku, sv, pu);
+      for (uint32_t P = 0; P < total; P += U) {
+        int kn = 0;
+        uint32_t svn = 0;
+        const double* pn = Ap;
+        if (P + U < total) locate(P + U, kn, svn, pn);
+        const int nu = static_cast<int>(min(total - P, static_cast<uint32_t>(U)));
+        double2 v[U][NV];
+        if (allv) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const double2* q = reinterpret_cast<const double2*>(
+                                   __shfl_sync(FULL, reinterpret_cast<uintptr_t>(pu), u)) + lane;
+#pragma unroll
+            for (int h = 0; h < NV; ++h) v[u][h] = __ldg(q + 32 * h);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t j = __shfl_sync(FULL, sv, u) & 0x7fffffffu;
+            const double* arow = Ac + j * lda;
+#pragma unroll
+            for (int h = 0; h < NV; ++h) {
+              const int c0 = 2 * h, c1 = 2 * h + 1;
+              v[u][h].x = kind[c0] == 0 ? arow[64 * h] : (kind[c0] == 1 ? b[j] : 0.0);
+              v[u][h].y = kind[c1] == 0 ? arow[64 * h + 1] : (kind[c1] == 1 ? b[j] : 0.0);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kk = __shfl_sync(FULL, ku, u);
+          if (u < nu) {
+            const int k = kk >> 1;
+            if (k != kcur) {
+              if (kcur >= 0)
+#pragma unroll
+                for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
+#pragma unroll
+              for (int h = 0; h < NV; ++h) acc[h] = acc_sm[k * 16 * CL + 32 * h + lane];
+              kcur = k;
+            }
+            const double sg = (kk & 1) ? -scale : scale;
+#pragma unroll
+            for (int h = 0; h < NV; ++h) {
+              acc[h].x = __dadd_rn(acc[h].x, __dmul_rn(sg, v[u][h].x));
+              acc[h].y = __dadd_rn(acc[h].y, __dmul_rn(sg, v[u][h].y));
+            }
+          }
+        }
+        sv = svn;
+        ku = kn;
+        pu = pn;
+      }
+      if (kcur >= 0)
+#pragma unroll
+        for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
+      sk = tk;
+      __syncwarp();
+      if (lane == 0) atomicAdd(wdone + g, 1u);
+    }
+#pragma unroll
+    for (int k = 0; k < SW_RPW; ++k) {
+      const int64_t i = gw + NW * k;
+      if (i >= d) continue;
+#pragma unroll
+      for (int h = 0; h < NV; ++h) {
+        const double2 a = acc_sm[k * 16 * CL + 32 * h + lane];
+        if (cA + 64 * h < ncol) W[i * ldw + cA + 64 * h] = a.x;
+        if (cA + 64 * h + 1 < ncol) W[i * ldw + cA + 64 * h + 1] = a.y;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Ring variant: warp per (sketch row, 32-column block), one column per lane,
 // each lane streaming its element of the next RG_DEPTH source rows into a
 // per-warp shared-memory ring with cp.async (8 bytes per lane per source,
@@ -235,7 +426,11 @@ struct SketchTune {
   int ring = -1;      // 1: cp.async ring variant, 0: register gather, -1: by shape
   int gcpl = 0;       // register gather: cap on columns-per-lane (more column blocks)
   int unr = 0;        // register gather: sources per unrolled group (0 = heuristic)
+  int swcl = 0;      // window sweep columns per lane (2 or 4; A/B, same bits)
+  int sweep = -1;     // window sweep: -1 auto (large A), 0 off, 1 on, > 1 on with that many window rows (same bits)
   SketchTune() {
+    if (const char* e = getenv("ITSK_SKETCH_SWEEP")) sweep = atoi(e);
+    if (const char* e = getenv("ITSK_SKETCH_SWCL")) swcl = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_RING")) ring = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_UNR")) unr = atoi(e);
@@ -299,6 +494,44 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   const bool ring = tu.ring >= 0 ? tu.ring == 1
                                  : (tu.gcpl == 0 && tu.unr == 0 && d * ((ncol + 31) / 32) <= 2048);
   if (ring) return launch_ring(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
+  // the window sweep: a whole-source call (not an upload window, no
+  // accumulation) on an A several times the L2, with every sketch row of the
+  // grid's warps in registers
+  {
+    const int nsm = num_sms();
+    const int64_t nw = static_cast<int64_t>(nsm) * SW_WARPS;
+    // auto from 16 GB of [A|b] (C4, 64 GB: 59 vs 72 ms; C3, 4 GB: 5.3 vs
+    // 4.0 ms, where the gather still finds part of A in L2)
+    const bool big = m * ncol * 8 >= (16ll << 30);
+    if ((tu.sweep > 0 || (tu.sweep < 0 && big)) && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
+        rg.j1 == 0xffffffffu && !rg.accum && d <= nw * SW_RPW && m < (1ll << 31)) {
+      const int cl = tu.swcl == 2 ? 2 : 4;
+      const uint32_t R = tu.sweep > 1 ? static_cast<uint32_t>(tu.sweep) : (cl == 2 ? 40000u : 20000u);
+      const int nwin = static_cast<int>((m + R - 1) / R);
+      const int npanel = static_cast<int>((ncol + 32 * cl - 1) / (32 * cl));
+      unsigned* wdone = nullptr;
+      uint32_t* bnd = nullptr;
+      const size_t cbytes = sizeof(unsigned) * static_cast<size_t>(nwin) * npanel;
+      const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * SW_RPW * nwin;
+      ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wdone), cbytes, s));
+      ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bnd), bbytes, s));
+      ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
+      int flags = (lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
+      const void* fn = cl == 2 ? reinterpret_cast<const void*>(k_sketch_sweep<2, 16>)
+                               : reinterpret_cast<const void*>(k_sketch_sweep<4, 8>);
+      const size_t smem = cl == 2 ? sw_smem_bytes<2>() : sw_smem_bytes<4>();
+      ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      const uint32_t mm = static_cast<uint32_t>(m);
+      void* args[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
+                      const_cast<uint32_t*>(&mm), const_cast<uint32_t*>(&R), const_cast<int*>(&nwin),
+                      const_cast<int*>(&npanel), &wdone, &bnd, &flags};
+      ITSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(32 * SW_WARPS), args, smem, s));
+      count_launch();
+      ITSK_CUDA(cudaFreeAsync(bnd, s));
+      ITSK_CUDA(cudaFreeAsync(wdone, s));
+      return ITSK_OK;
+    }
+  }
   int64_t need = (ncol + 31) / 32;
   int64_t cap = 4;
   while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 6000) cap >>= 1;

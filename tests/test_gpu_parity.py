@@ -143,6 +143,34 @@ def test_sketch_kernel_variants_bitwise(pkg, orc, monkeypatch, variant):
         assert np.array_equal(s.apply_dense(a), ref[:, :n]), (variant, d, m, n, zeta)
 
 
+@pytest.mark.parametrize("m,n,d,lda,withb", [(700000, 300, 6000, 300, True), (600000, 511, 2000, 512, True),
+                                              (450000, 1000, 12000, 1000, True), (250001, 129, 700, 131, True),
+                                              (300000, 256, 3000, 256, False), (90000, 40, 27000, 40, True)])
+def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
+    """The window sweep (automatic from 16 GB of [A|b]: one persistent
+    launch, the grid sweeping 20000-row source windows of one 128-column
+    panel at a time with a bounded drift, each warp's sketch rows walked as
+    one flattened (row, source) list) against the register gather
+    (ITSK_SKETCH_SWEEP=0, itself bitwise scipy's order in the tests above):
+    bitwise equal, including the fused b column, for both lane widths; odd
+    leading dimension (the unvectorised loads), no b, a ragged last window,
+    d beyond the grid's warps (up to 12 rows per warp, 27000 here)."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(m)
+    buf = torch.randn(m, lda, dtype=torch.float64, device=dev, generator=g)
+    a = buf[:, :n]
+    b = torch.randn(m, dtype=torch.float64, device=dev, generator=g) if withb else None
+    s = pkg.sparse_sign_new(d, m, 8, 5)
+    monkeypatch.setenv("ITSK_SKETCH_SWEEP", "1")  # on below its automatic 16 GB threshold
+    got = s.apply_dense(a, b)
+    monkeypatch.setenv("ITSK_SKETCH_SWCL", "2")
+    got2 = s.apply_dense(a, b)
+    monkeypatch.setenv("ITSK_SKETCH_SWEEP", "0")
+    ref = s.apply_dense(a, b)
+    assert torch.equal(got, ref)
+    assert torch.equal(got2, ref)
+
+
 def test_pattern_argument_errors(pkg):
     with pytest.raises(ValueError):
         pkg.sparse_sign_new(3, 5, 4, 0)
