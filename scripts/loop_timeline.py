@@ -27,7 +27,7 @@ from bench import CONFIGS, make_problem  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 variant = sys.argv[2] if len(sys.argv) > 2 else "basic"
 m, n, kappa, beta, d, zeta = CONFIGS[name]
-p, _, _ = make_problem(name, 0, None)
+p, _, _ = make_problem(name, 0)
 dev = torch.device("cuda")
 at = p.a if isinstance(p.a, torch.Tensor) else torch.from_numpy(p.a).to(dev)
 bt = p.b if isinstance(p.b, torch.Tensor) else torch.from_numpy(p.b).to(dev)

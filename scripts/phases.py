@@ -14,7 +14,7 @@ gen = sys.argv[3] if len(sys.argv) > 3 else None
 from bench import CONFIGS, make_problem
 m, n, kappa, beta, d, zeta = CONFIGS[cfgname]
 t0 = time.perf_counter()
-p, _, _ = make_problem(cfgname, 0, gen)
+p, _, _ = make_problem(cfgname, 0)
 torch.cuda.synchronize()
 print(f"generate {time.perf_counter() - t0:.1f} s", flush=True)
 dev = torch.device("cuda")
