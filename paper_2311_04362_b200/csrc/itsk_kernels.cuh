@@ -144,8 +144,9 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n);
 constexpr int QR_OB = 128;          // outer block width
 constexpr int FAR_YP_TILES = 320;   // Yp capacity: splits x 64-column tiles
 int64_t qr_far_yp_doubles();
+// G = V'V on s; T (one CTA) on t_stream (nullptr: s), after s through ev_handoff
 int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, const double* taus, double* Yp,
-                       double* G, cudaStream_t s);
+                       double* G, cudaStream_t s, cudaStream_t t_stream = nullptr, cudaEvent_t ev_handoff = nullptr);
 int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, int64_t c0, int64_t Nf,
                          const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s);
 int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,

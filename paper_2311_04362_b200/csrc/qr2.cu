@@ -23,6 +23,7 @@
 //
 // Every cross-CTA sum runs in a fixed order: R is bitwise reproducible.
 #include <cooperative_groups.h>
+#include <cuda.h>  // green-context types (entry points fetched through the runtime)
 
 #include <algorithm>
 #include <cstdlib>
@@ -1134,8 +1135,94 @@ int side_stream(cudaStream_t* out, int which = 0) {
   return ITSK_OK;
 }
 
+// SM partition of the two-level QR (green contexts): the panel chain (one
+// 16-CTA cluster at a time, ~200 KB of shared memory per CTA, and the
+// one-CTA T recurrence) on a partition of QG_SMS SMs, every GEMM-shaped
+// update on the rest.  Sharing all SMs, the chain's big-CTA kernels waited
+// for SMs to drain of the far GEMMs' CTAs (up to ~0.5 ms per outer block).
+// The partition changes no operation order (splits follow the device's SM
+// count): results are bitwise the same with it or without (ITSK_QR_GREEN=0).
+constexpr unsigned QG_SMS = 16;
+struct QrGreen {
+  bool ok = false;
+  cudaStream_t chain = nullptr;  // the panel chain (highest priority)
+  cudaStream_t upd = nullptr;    // the outer block's Gram / near update (highest priority)
+  cudaStream_t side = nullptr;   // the look-ahead's rest of the block (highest priority: the next
+                                 // panel's look-ahead waits for it)
+  cudaStream_t far = nullptr;    // the far rest (lowest priority: due a block later)
+};
+
+QrGreen make_qr_green(int dev) {
+  QrGreen g;
+  auto entry = [](const char* name, void** fn) {
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPointByVersion(name, fn, CUDART_VERSION, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess && *fn != nullptr;
+  };
+  decltype(&cuDeviceGet) p_dev_get = nullptr;
+  decltype(&cuDeviceGetDevResource) p_get_res = nullptr;
+  decltype(&cuDevSmResourceSplitByCount) p_split = nullptr;
+  decltype(&cuDevResourceGenerateDesc) p_desc = nullptr;
+  decltype(&cuGreenCtxCreate) p_create = nullptr;
+  decltype(&cuGreenCtxStreamCreate) p_stream = nullptr;
+  if (!entry("cuDeviceGet", reinterpret_cast<void**>(&p_dev_get)) ||
+      !entry("cuDeviceGetDevResource", reinterpret_cast<void**>(&p_get_res)) ||
+      !entry("cuDevSmResourceSplitByCount", reinterpret_cast<void**>(&p_split)) ||
+      !entry("cuDevResourceGenerateDesc", reinterpret_cast<void**>(&p_desc)) ||
+      !entry("cuGreenCtxCreate", reinterpret_cast<void**>(&p_create)) ||
+      !entry("cuGreenCtxStreamCreate", reinterpret_cast<void**>(&p_stream)))
+    return g;
+  CUdevice cd;
+  if (p_dev_get(&cd, dev) != CUDA_SUCCESS) return g;
+  CUdevResource all, part, rest;
+  if (p_get_res(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return g;
+  unsigned np = 1;
+  if (p_split(&part, &np, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, QG_SMS) != CUDA_SUCCESS ||
+      np != 1 || part.sm.smCount < QG_SMS || rest.sm.smCount < 64)
+    return g;
+  CUdevResourceDesc da, db;
+  CUgreenCtx ga, gb;
+  if (p_desc(&da, &part, 1) != CUDA_SUCCESS || p_desc(&db, &rest, 1) != CUDA_SUCCESS) return g;
+  if (p_create(&ga, da, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      p_create(&gb, db, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return g;
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return g;
+  CUstream c0, c1, c2, c3;
+  if (p_stream(&c0, ga, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+      p_stream(&c1, gb, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+      p_stream(&c2, gb, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+      p_stream(&c3, gb, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS)
+    return g;
+  g.chain = reinterpret_cast<cudaStream_t>(c0);
+  g.upd = reinterpret_cast<cudaStream_t>(c1);
+  g.side = reinterpret_cast<cudaStream_t>(c2);
+  g.far = reinterpret_cast<cudaStream_t>(c3);
+  g.ok = true;
+  return g;
+}
+
+// per device, created once (nullptr streams when green contexts are
+// unavailable or ITSK_QR_GREEN=0: the shared-SM path)
+QrGreen qr_green() {
+  static QrGreen g[64];
+  static bool tried[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return QrGreen{};
+  if (const char* e = getenv("ITSK_QR_GREEN"))
+    if (atoi(e) == 0) return QrGreen{};
+  if (!tried[dev]) {
+    tried[dev] = true;
+    g[dev] = make_qr_green(dev);
+    cudaGetLastError();  // a failed probe leaves no sticky error behind
+    if (getenv("ITSK_QR_GREEN_VERBOSE"))
+      fprintf(stderr, "itsk: QR SM partition on device %d: %s\n", dev, g[dev].ok ? "on" : "unavailable");
+  }
+  return g[dev];
+}
+
 cudaError_t pooled_event(int which, cudaEvent_t* out) {
-  static cudaEvent_t ev[64][6] = {};
+  static cudaEvent_t ev[64][10] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -1203,9 +1290,11 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   // caller's stream at both ends
   cudaStream_t s = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  const QrGreen gr = P.two_level ? qr_green() : QrGreen{};
   {
-    int rc = side_stream(&s, 2);
+    int rc = gr.ok ? ITSK_OK : side_stream(&s, 2);
     if (rc) return rc;
+    if (gr.ok) s = gr.chain;
     ITSK_CUDA(pooled_event(4, &ev_in));
     ITSK_CUDA(pooled_event(5, &ev_out));
     ITSK_CUDA(cudaEventRecord(ev_in, s_caller));
@@ -1246,8 +1335,9 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   const bool ahead = ahead_k || (P.two_level && lookahead_enabled());
   cudaStream_t side = nullptr;
   if (ahead) {
-    int rc = side_stream(&side);
+    int rc = gr.ok ? ITSK_OK : side_stream(&side);
     if (rc) return rc;
+    if (gr.ok) side = gr.side;
   }
   cudaEvent_t ev_main = nullptr, ev_side = nullptr;
   if (ahead || P.two_level) {
@@ -1284,16 +1374,29 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   // far update of block B+1's next block waits for block B's far rest.
   const bool two = P.two_level;
   cudaStream_t side_far = nullptr;
-  cudaEvent_t ev_g = nullptr, ev_far = nullptr;
+  // ev_far: the previous block's far update of the NEXT block's columns (the
+  // near update waits only for those); ev_far_all: all of its far work
+  cudaEvent_t ev_g = nullptr, ev_far = nullptr, ev_far_all = nullptr;
   bool far_busy = false;
   double* Gfar = ws + P.far_off;
   double* Ypf[2] = {nullptr, nullptr};
   double* Zf[2] = {nullptr, nullptr};
+  // green partition: the Gram and near update on `upd` (GEMM partition),
+  // handed over to and from the chain through ev_s2u / ev_u2s
+  cudaStream_t upd = nullptr;
+  cudaEvent_t ev_s2u = nullptr, ev_u2s = nullptr;
   if (two) {
-    int rc = side_stream(&side_far, 1);
+    int rc = gr.ok ? ITSK_OK : side_stream(&side_far, 1);
     if (rc) return rc;
+    if (gr.ok) {
+      side_far = gr.far;
+      upd = gr.upd;
+      ITSK_CUDA(pooled_event(7, &ev_s2u));
+      ITSK_CUDA(pooled_event(8, &ev_u2s));
+    }
     ITSK_CUDA(pooled_event(2, &ev_g));
     ITSK_CUDA(pooled_event(3, &ev_far));
+    ITSK_CUDA(pooled_event(6, &ev_far_all));
     ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_main, 0));
     const int64_t nblk = (n + QR_OB - 1) / QR_OB;
     Ypf[0] = Gfar + nblk * QR_OB * QR_OB;
@@ -1310,7 +1413,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     if (two && k0 == blk0 && horizon == N && far_busy) {
       // the last block's updates reach the rhs column, which the previous
       // block's far rest may still be updating
-      ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));
+      ITSK_CUDA(cudaStreamWaitEvent(s, ev_far_all, 0));
       far_busy = false;
     }
     double* Gk = G + (k0 / P.NB) * 32 * 32;
@@ -1344,19 +1447,38 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
       // the outer block [blk0, horizon) is factored: its far update
       const int ob = static_cast<int>(horizon - blk0);
       double* Gb = Gfar + (blk0 / QR_OB) * QR_OB * QR_OB;
-      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, taus, Ypf[0], Gb, s);
+      // Gram on u (the GEMM partition when green), T on the chain stream
+      const cudaStream_t u = upd ? upd : s;
+      if (upd) {
+        ITSK_CUDA(cudaEventRecord(ev_s2u, s));
+        ITSK_CUDA(cudaStreamWaitEvent(u, ev_s2u, 0));
+      }
+      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, taus, Ypf[0], Gb, u, s, ev_u2s);
       if (rc) return rc;
       ITSK_CUDA(cudaEventRecord(ev_g, s));
-      if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));  // the previous block's far rest
+      if (upd) ITSK_CUDA(cudaStreamWaitEvent(u, ev_g, 0));
+      if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(u, ev_far, 0));  // the previous block's far update of these columns
       const int64_t nn = std::min<int64_t>(QR_OB, N - horizon);
-      rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], s);
+      rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], u);
       if (rc) return rc;
+      if (upd) {  // the next block's panels need it
+        ITSK_CUDA(cudaEventRecord(ev_u2s, u));
+        ITSK_CUDA(cudaStreamWaitEvent(s, ev_u2s, 0));
+      }
       if (N - horizon > nn) {
+        // the far rest on the side stream, the block after next first: the
+        // next block's own near update waits only for that part (stream order
+        // keeps every later column's updates in block order)
         ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_g, 0));
-        rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon + nn, N - horizon - nn, Gb, taus, Ypf[1], Zf[1],
-                                  side_far);
+        const int64_t f0 = horizon + nn, nf = N - f0, n1 = std::min<int64_t>(QR_OB, nf);
+        rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0, n1, Gb, taus, Ypf[1], Zf[1], side_far);
         if (rc) return rc;
         ITSK_CUDA(cudaEventRecord(ev_far, side_far));
+        if (nf > n1) {
+          rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0 + n1, nf - n1, Gb, taus, Ypf[1], Zf[1], side_far);
+          if (rc) return rc;
+        }
+        ITSK_CUDA(cudaEventRecord(ev_far_all, side_far));
         far_busy = true;
       } else {
         far_busy = false;
@@ -1419,11 +1541,18 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     }
   }
   if (ahead && side_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
-  if (two && far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far, 0));
-  k_qr_finish<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, s>>>(W, n, ldw, N, betas, R, z, singular);
+  if (two && far_busy) ITSK_CUDA(cudaStreamWaitEvent(s, ev_far_all, 0));
+  // the finish is n^2 elementwise work: on the GEMM partition when green
+  cudaStream_t fs = s;
+  if (upd) {
+    ITSK_CUDA(cudaEventRecord(ev_s2u, s));
+    ITSK_CUDA(cudaStreamWaitEvent(upd, ev_s2u, 0));
+    fs = upd;
+  }
+  k_qr_finish<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, fs>>>(W, n, ldw, N, betas, R, z, singular);
   count_launch();
   ITSK_CHECK_LAUNCH();
-  ITSK_CUDA(cudaEventRecord(ev_out, s));
+  ITSK_CUDA(cudaEventRecord(ev_out, fs));
   ITSK_CUDA(cudaStreamWaitEvent(s_caller, ev_out, 0));
   return ITSK_OK;
 }

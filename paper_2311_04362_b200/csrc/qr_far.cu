@@ -30,8 +30,6 @@ constexpr int FY_ST = 4;         // stages
 constexpr int FY_VS = FOB + 8;   // [k][i] tiles: stride = 8 (mod 16) doubles -> conflict-free fragments
 constexpr int FY_BS = 64 + 8;
 constexpr int FA_KC = 32;        // k per stage in k_far_apply
-constexpr int FA_VS = FA_KC + 4; // [row][k] tile: stride = 4 (mod 16)
-constexpr int FA_ZS = 64 + 8;    // [k][col] tile
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -41,6 +39,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+// 16 bytes, the first `src_bytes` (0, 8 or 16) from global, the rest zero
+__device__ __forceinline__ void cp_async16z(double* dst, const double* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -66,7 +69,8 @@ struct FarArgs {
   int S;
   const double* G;     // FOB x FOB: the block's T (k_far_t), read by k_far_z
   const double* taus;  // global tau array, indexed b0 + i
-  double* Z;           // Nf x FOB (column-major, like Yp)
+  double* Z;           // Nf x FOB (column-major, like Yp), stored NEGATED (-T'Y) for k_far_apply
+  int vec16;           // W 16-byte aligned, even ldw, b0 and c0 even: 16-byte copies
 };
 
 // Y_s = V_s' B_s over the rows of split s; B = the far columns of W, or V
@@ -91,6 +95,21 @@ __global__ void __launch_bounds__(FT) k_far_y(FarArgs a) {
     const int64_t r0 = rlo + static_cast<int64_t>(ch) * FY_KC;
     double* vs = Vs + st * FY_KC * FY_VS;
     double* bs = Bs + st * FY_KC * FY_BS;
+    if (a.vec16) {
+      for (int idx = tid; idx < FY_KC * (FOB / 2); idx += FT) {
+        const int rr = idx / (FOB / 2), i = 2 * (idx - rr * (FOB / 2));
+        const int64_t r = r0 + rr;
+        const int sv = r < rhi ? 8 * max(0, min(2, ob - i)) : 0;
+        cp_async16z(vs + rr * FY_VS + i, a.W + (sv ? r * a.ldw + a.b0 + i : 0), sv);
+      }
+      for (int idx = tid; idx < FY_KC * 32; idx += FT) {
+        const int rr = idx >> 5, c = 2 * (idx & 31);
+        const int64_t r = r0 + rr;
+        const int sb = r < rhi ? 8 * max(0, min(2, cw - c)) : 0;
+        cp_async16z(bs + rr * FY_BS + c, a.W + (sb ? r * a.ldw + a.c0 + cb + c : 0), sb);
+      }
+      return;
+    }
     for (int idx = tid; idx < FY_KC * FOB; idx += FT) {
       const int rr = idx / FOB, i = idx - rr * FOB;
       const int64_t r = r0 + rr;
@@ -123,28 +142,34 @@ __global__ void __launch_bounds__(FT) k_far_y(FarArgs a) {
     const double* vs = Vs + st * FY_KC * FY_VS;
     const double* bs = Bs + st * FY_KC * FY_BS;
     const int64_t r0 = rlo + static_cast<int64_t>(ch) * FY_KC;
-    const bool tri = r0 < a.b0 + ob;  // chunk meets the unit-diagonal triangle of V
+    // chunks meeting V's unit-diagonal triangle select per element; the
+    // others (all but the first few of split 0) use the stored values as is
+    auto step = [&](auto tri_c) {
+      constexpr bool TRI = decltype(tri_c)::value;
 #pragma unroll
-    for (int k = 0; k < FY_KC; k += 4) {
-      const int64_t r = r0 + k + t4;
-      double af[4], bf[4];
+      for (int k = 0; k < FY_KC; k += 4) {
+        const int64_t r = r0 + k + t4;
+        double af[4], bf[4];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int i = mw * 32 + mt * 8 + g4;
-        const double v = vs[(k + t4) * FY_VS + i];
-        af[mt] = tri ? vv(v, r, a.b0, i) : v;
+        for (int mt = 0; mt < 4; ++mt) {
+          const int i = mw * 32 + mt * 8 + g4;
+          const double v = vs[(k + t4) * FY_VS + i];
+          af[mt] = TRI ? vv(v, r, a.b0, i) : v;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int c = nw * 32 + nt * 8 + g4;
+          const double v = bs[(k + t4) * FY_BS + c];
+          bf[nt] = (BV && TRI) ? vv(v, r, a.b0, static_cast<int>(cb) + c) : v;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
       }
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int c = nw * 32 + nt * 8 + g4;
-        const double v = bs[(k + t4) * FY_BS + c];
-        bf[nt] = (BV && tri) ? vv(v, r, a.b0, static_cast<int>(cb) + c) : v;
-      }
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
+    };
+    if (r0 < a.b0 + ob) step(std::true_type{});
+    else step(std::false_type{});
   }
   cp_wait<0>();
   double* Y = a.Yp + static_cast<int64_t>(blockIdx.y) * FOB * a.Nf;
@@ -183,15 +208,23 @@ __global__ void k_far_gsum(const double* __restrict__ Gp, int S, int ob, double*
 
 // T of the block (upper triangular, FOB x FOB, row stride FOB): dlarft's
 // forward column-wise recurrence T[i][i] = tau_i, T[0:i, i] = -tau_i
-// T[0:i, 0:i] G[0:i, i] (G = V'V), one CTA; each row's dot is split over 4
-// lanes and combined in a fixed order.  Z = T'Y then needs no sequential
-// substitution (k_far_z).
+// T[0:i, 0:i] G[0:i, i] (G = V'V), one CTA, blocked by FT_BLK columns: for a
+// block J the part of every column's mat-vec over the finished blocks,
+// P = T[0:j0, 0:j0] G[0:j0, J] (j0 = J's first column), is one parallel
+// product; the sequential steps then add only the terms inside J (each row's
+// dot split over 4 lanes, combined in a fixed order).  Z = T'Y then needs no
+// sequential substitution (k_far_z).
 constexpr int FT_THREADS = 512;
+constexpr int FT_BLK = 16;
+constexpr size_t ft_smem() {
+  return static_cast<size_t>(FOB * (FOB + 1) + FOB * (FOB - 1) / 2 + FOB * FT_BLK) * 8;
+}
 __global__ void __launch_bounds__(FT_THREADS) k_far_t(const double* G, const double* __restrict__ taus,
                                                       int64_t b0, int ob, double* T) {
-  extern __shared__ __align__(16) double tsm[];  // T: FOB x (FOB + 1) | G's strict upper triangle, packed
+  extern __shared__ __align__(16) double tsm[];  // T: FOB x (FOB + 1) | G's strict upper triangle | P
   constexpr int TS = FOB + 1;
   double* gu = tsm + FOB * TS;                   // column i of G above the diagonal at gu[i (i - 1) / 2 ...]
+  double* P = gu + FOB * (FOB - 1) / 2;          // P[r * FT_BLK + c]
   __shared__ double ts[FOB];
   const int tid = threadIdx.x;
   const int r = tid >> 2, part = tid & 3;
@@ -203,16 +236,36 @@ __global__ void __launch_bounds__(FT_THREADS) k_far_t(const double* G, const dou
   }
   if (tid < FOB) ts[tid] = tid < ob ? taus[b0 + tid] : 0.0;
   __syncthreads();
-  for (int i = 0; i < ob; ++i) {
-    const double* w = gu + i * (i - 1) / 2;
-    double sum = 0.0;
-    if (r < i)
-      for (int k = r + part; k < i; k += 4) sum = fma(tsm[r * TS + k], w[k], sum);
-    sum += __shfl_xor_sync(FULL, sum, 1);
-    sum += __shfl_xor_sync(FULL, sum, 2);
-    if (part == 0 && r < i) tsm[r * TS + i] = -ts[i] * sum;
-    if (tid == 0) tsm[i * TS + i] = ts[i];
+  for (int j0 = 0; j0 < ob; j0 += FT_BLK) {
+    const int j1 = min(ob, j0 + FT_BLK);
+    // P[rr][c] = sum_{rr <= k < j0} T[rr][k] G[k][j0 + c], rows rr < j0
+    for (int e = tid; e < j0 * FT_BLK; e += FT_THREADS) {
+      const int rr = e / FT_BLK, c = e - rr * FT_BLK;
+      double s0 = 0.0, s1 = 0.0;
+      if (j0 + c < j1) {
+        const double* w = gu + (j0 + c) * (j0 + c - 1) / 2;
+        const double* tr = tsm + rr * TS;
+        int k = rr;
+        for (; k + 1 < j0; k += 2) {
+          s0 = fma(tr[k], w[k], s0);
+          s1 = fma(tr[k + 1], w[k + 1], s1);
+        }
+        if (k < j0) s0 = fma(tr[k], w[k], s0);
+      }
+      P[e] = s0 + s1;
+    }
     __syncthreads();
+    for (int i = j0; i < j1; ++i) {
+      const double* w = gu + i * (i - 1) / 2;
+      double sum = 0.0;
+      if (r < i)
+        for (int k = max(r, j0) + part; k < i; k += 4) sum = fma(tsm[r * TS + k], w[k], sum);
+      sum += __shfl_xor_sync(FULL, sum, 1);
+      sum += __shfl_xor_sync(FULL, sum, 2);
+      if (part == 0 && r < i) tsm[r * TS + i] = -ts[i] * (r < j0 ? P[r * FT_BLK + (i - j0)] + sum : sum);
+      if (tid == 0) tsm[i * TS + i] = ts[i];
+      __syncthreads();
+    }
   }
   for (int e = tid; e < FOB * FOB; e += FT_THREADS) {
     const int rr = e / FOB, c = e - rr * FOB;
@@ -225,58 +278,102 @@ __global__ void __launch_bounds__(FT_THREADS) k_far_t(const double* G, const dou
 // sum_{k <= j} T_kj y_k in ascending k.  Y partials and Z are column-major
 // (a column's FOB values contiguous); T is read through L1.
 constexpr int FZ_WARPS = 8;
+constexpr int FZ_CPW = 2;  // columns per warp, both at once (independent chains)
+constexpr size_t FZ_SMEM = static_cast<size_t>(FOB) * FOB * 8;
 __global__ void __launch_bounds__(32 * FZ_WARPS) k_far_z(FarArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(16) double Ts[];  // the block's T (k_far_t), FOB x FOB
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ob = a.ob;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * FZ_WARPS + warp;
-  if (c >= a.Nf) return;
-  double y[4];
-  {
-    const double* yp = a.Yp + c * FOB + lane;
-    const int64_t stride = static_cast<int64_t>(FOB) * a.Nf;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) y[q] = 0.0;
-    for (int sp = 0; sp < a.S; ++sp) {
-      double v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = lane + 32 * q < ob ? __ldcg(yp + sp * stride + 32 * q) : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) y[q] += v[q];
-    }
+  // T into shared memory first: the substitution-free mat-vec then reads it
+  // at shared-memory latency (from L2 each of its ob steps waited ~1 us)
+  if ((reinterpret_cast<uintptr_t>(a.G) & 15) == 0) {
+    for (int e = 2 * tid; e < FOB * FOB; e += 2 * 32 * FZ_WARPS) cp_async16z(Ts + e, a.G + e, 16);
+  } else {
+    for (int e = tid; e < FOB * FOB; e += 32 * FZ_WARPS) cp_async8(Ts + e, a.G + e, true);
   }
-  double z[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* T = a.G;  // the block's T (k_far_t)
+  cp_commit();
+  const int64_t stride = static_cast<int64_t>(FOB) * a.Nf;
+  // y of columns c0, c1 (c1 < 0: none): the split partials in ascending
+  // split order, 8 splits of both columns in flight per round
+  auto ysum2 = [&](int64_t c0, int64_t c1, double (&y0)[4], double (&y1)[4]) {
+    const double* yp0 = a.Yp + c0 * FOB + lane;
+    const double* yp1 = a.Yp + (c1 >= 0 ? c1 : c0) * FOB + lane;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (32 * q >= ob) break;
+    for (int q = 0; q < 4; ++q) y0[q] = y1[q] = 0.0;
+    for (int s0 = 0; s0 < a.S; s0 += 8) {
+      double v0[8][4], v1[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool ok = s0 + u < a.S && lane + 32 * q < ob;
+          v0[u][q] = ok ? __ldcg(yp0 + (s0 + u) * stride + 32 * q) : 0.0;
+          v1[u][q] = ok && c1 >= 0 ? __ldcg(yp1 + (s0 + u) * stride + 32 * q) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < a.S)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            y0[q] += v0[u][q];
+            y1[q] += v1[u][q];
+          }
+    }
+  };
+  cp_wait<0>();
+  __syncthreads();
+  for (int cc = 0; cc < FZ_CPW; cc += 2) {
+    const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * FZ_WARPS + warp) * FZ_CPW + cc;
+    if (c0 >= a.Nf) break;
+    const bool two = c0 + 1 < a.Nf;
+    double y0[4], y1[4];
+    ysum2(c0, two ? c0 + 1 : -1, y0, y1);
+    double z0[4] = {0.0, 0.0, 0.0, 0.0}, z1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (32 * q >= ob) break;
 #pragma unroll 8
-    for (int kl = 0; kl < 32; ++kl) {
-      const int k = 32 * q + kl;
-      if (k >= ob) break;
-      const double yk = __shfl_sync(FULL, y[q], kl);
-      const double* tr = T + k * FOB + lane;
+      for (int kl = 0; kl < 32; ++kl) {
+        const int k = 32 * q + kl;
+        if (k >= ob) break;
+        const double yk0 = __shfl_sync(FULL, y0[q], kl), yk1 = __shfl_sync(FULL, y1[q], kl);
+        const double* tr = Ts + k * FOB + lane;
 #pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-        if (q2 < q) continue;
-        const int j = lane + 32 * q2;
-        if (k <= j) z[q2] = fma(__ldg(tr + 32 * q2), yk, z[q2]);
+        for (int q2 = 0; q2 < 4; ++q2) {
+          if (q2 < q) continue;
+          const int j = lane + 32 * q2;
+          if (k <= j) {
+            const double t = tr[32 * q2];
+            z0[q2] = fma(t, yk0, z0[q2]);
+            z1[q2] = fma(t, yk1, z1[q2]);
+          }
+        }
       }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = lane + 32 * q;
-    if (j < ob) a.Z[c * FOB + j] = z[q];
+    for (int q = 0; q < 4; ++q) {
+      const int j = lane + 32 * q;
+      if (j < ob) {
+        a.Z[c0 * FOB + j] = -z0[q];  // negated: k_far_apply accumulates W + V (-Z)
+        if (two) a.Z[(c0 + 1) * FOB + j] = -z1[q];
+      }
+    }
   }
 }
 
 // W_far -= V Z on a 128-row x 64-column tile: 8 warps of 32 x 32, the
-// accumulators start from W and take the products with -V, k in chunks of
-// FA_KC through a double-buffered cp.async ring.
-__global__ void __launch_bounds__(FT) k_far_apply(FarArgs a) {
-  extern __shared__ __align__(16) double fsm[];
-  double* Vs = fsm;                      // 2 x 128 x FA_VS
-  double* Zs = Vs + 2 * 128 * FA_VS;     // 2 x FA_KC x FA_ZS
+// accumulators start from W and take the products V (-Z) (k_far_z stores Z
+// negated), k in chunks of FA_KC through a double-buffered cp.async ring.
+// Shared tiles [row][k] for V and [col][k] for Z, 32 doubles per row with the
+// 16-byte column index XOR-swizzled by the row's parity: each thread reads
+// the k pair (2 t4, 2 t4 + 1) of its fragment row with ONE 16-byte load and
+// feeds two DMMAs (the k = 8-step splits into the even and the odd k of the
+// pairs), and the 8 lanes of every quarter-warp hit 8 distinct 16-byte bank
+// groups.
+__device__ __forceinline__ int fa_sw(int row, int k) { return row * FA_KC + (((k >> 1) ^ ((row & 1) << 2)) << 1); }
+
+template <bool TRI>
+__device__ __forceinline__ void far_apply_body(const FarArgs& a, double* Vs, double* Zs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g4 = lane >> 2, t4 = lane & 3;
   const int mw = warp >> 1, nw = warp & 1;
@@ -286,21 +383,33 @@ __global__ void __launch_bounds__(FT) k_far_apply(FarArgs a) {
   const int cw = static_cast<int>(min(static_cast<int64_t>(64), a.Nf - cb));
   const int ob = a.ob;
   const int nch = (ob + FA_KC - 1) / FA_KC;
-  const bool tri = blockIdx.x == 0;  // rows [b0, b0 + 128) hold V's unit-diagonal triangle
   auto load = [&](int ch) {
     const int st = ch & 1;
     const int k0 = ch * FA_KC;
-    double* vs = Vs + st * 128 * FA_VS;
-    double* zs = Zs + st * FA_KC * FA_ZS;
+    double* vs = Vs + st * 128 * FA_KC;
+    double* zs = Zs + st * 64 * FA_KC;
+    if (a.vec16) {
+      for (int idx = tid; idx < 128 * (FA_KC / 2); idx += FT) {
+        const int rr = idx / (FA_KC / 2), k = 2 * (idx - rr * (FA_KC / 2));
+        const int sv = rr < rh ? 8 * max(0, min(2, ob - k0 - k)) : 0;
+        cp_async16z(vs + fa_sw(rr, k), a.W + (sv ? (r0 + rr) * a.ldw + a.b0 + k0 + k : 0), sv);
+      }
+      for (int idx = tid; idx < 64 * (FA_KC / 2); idx += FT) {
+        const int c = idx / (FA_KC / 2), k = 2 * (idx - c * (FA_KC / 2));
+        const int sz = c < cw ? 8 * max(0, min(2, ob - k0 - k)) : 0;
+        cp_async16z(zs + fa_sw(c, k), a.Z + (sz ? (cb + c) * FOB + k0 + k : 0), sz);
+      }
+      return;
+    }
     for (int idx = tid; idx < 128 * FA_KC; idx += FT) {
       const int rr = idx / FA_KC, k = idx - rr * FA_KC;
       const bool ok = rr < rh && k0 + k < ob;
-      cp_async8(vs + rr * FA_VS + k, a.W + (ok ? (r0 + rr) * a.ldw + a.b0 + k0 + k : 0), ok);
+      cp_async8(vs + fa_sw(rr, k) + (k & 1), a.W + (ok ? (r0 + rr) * a.ldw + a.b0 + k0 + k : 0), ok);
     }
-    for (int idx = tid; idx < FA_KC * 64; idx += FT) {
-      const int k = idx >> 6, c = idx & 63;
+    for (int idx = tid; idx < 64 * FA_KC; idx += FT) {
+      const int c = idx / FA_KC, k = idx - c * FA_KC;
       const bool ok = k0 + k < ob && c < cw;
-      cp_async8(zs + k * FA_ZS + c, a.Z + (ok ? (cb + c) * FOB + k0 + k : 0), ok);
+      cp_async8(zs + fa_sw(c, k) + (k & 1), a.Z + (ok ? (cb + c) * FOB + k0 + k : 0), ok);
     }
   };
   load(0);
@@ -321,24 +430,32 @@ __global__ void __launch_bounds__(FT) k_far_apply(FarArgs a) {
     cp_wait<1>();
     __syncthreads();
     const int st = ch & 1;
-    const double* vs = Vs + st * 128 * FA_VS;
-    const double* zs = Zs + st * FA_KC * FA_ZS;
+    const double* vs = Vs + st * 128 * FA_KC;
+    const double* zs = Zs + st * 64 * FA_KC;
     const int k0 = ch * FA_KC;
 #pragma unroll
-    for (int k = 0; k < FA_KC; k += 4) {
-      double af[4], bf[4];
+    for (int k = 0; k < FA_KC; k += 8) {
+      double2 af[4], bf[4];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
         const int rr = mw * 32 + mt * 8 + g4;
-        const double v = vs[rr * FA_VS + k + t4];
-        af[mt] = -(tri ? vv(v, r0 + rr, a.b0, k0 + k + t4) : v);
+        af[mt] = *reinterpret_cast<const double2*>(vs + fa_sw(rr, k + 2 * t4));
+        if (TRI) {
+          af[mt].x = vv(af[mt].x, r0 + rr, a.b0, k0 + k + 2 * t4);
+          af[mt].y = vv(af[mt].y, r0 + rr, a.b0, k0 + k + 2 * t4 + 1);
+        }
       }
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = zs[(k + t4) * FA_ZS + nw * 32 + nt * 8 + g4];
+      for (int nt = 0; nt < 4; ++nt)
+        bf[nt] = *reinterpret_cast<const double2*>(zs + fa_sw(nw * 32 + nt * 8 + g4, k + 2 * t4));
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt].x, bf[nt].x);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt].y, bf[nt].y);
     }
     __syncthreads();  // stage st is refilled by the next iteration's load
   }
@@ -355,14 +472,24 @@ __global__ void __launch_bounds__(FT) k_far_apply(FarArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(FT, 2) k_far_apply(FarArgs a) {
+  extern __shared__ __align__(16) double fsm[];
+  double* Vs = fsm;                   // 2 x 128 x FA_KC
+  double* Zs = Vs + 2 * 128 * FA_KC;  // 2 x 64 x FA_KC
+  // rows [b0, b0 + 128) hold V's unit-diagonal triangle
+  if (blockIdx.x == 0) far_apply_body<true>(a, Vs, Zs);
+  else far_apply_body<false>(a, Vs, Zs);
+}
+
 constexpr size_t FY_SMEM = static_cast<size_t>(FY_ST) * FY_KC * (FY_VS + FY_BS) * 8;
-constexpr size_t FA_SMEM = static_cast<size_t>(2) * (128 * FA_VS + FA_KC * FA_ZS) * 8;
+constexpr size_t FA_SMEM = static_cast<size_t>(2) * (128 + 64) * FA_KC * 8;
 
 int far_attrs() {
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_y<false>)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_y<true>)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_apply)));
   ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_t)));
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_far_z)));
   return ITSK_OK;
 }
 
@@ -371,7 +498,7 @@ int far_attrs() {
 int64_t qr_far_yp_doubles() { return static_cast<int64_t>(FAR_YP_TILES) * FOB * 64; }
 
 int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, const double* taus, double* Yp,
-                       double* G, cudaStream_t s) {
+                       double* G, cudaStream_t s, cudaStream_t t_stream, cudaEvent_t ev_handoff) {
   int rc = far_attrs();
   if (rc) return rc;
   FarArgs a{};
@@ -383,6 +510,7 @@ int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, co
   a.c0 = b0;
   a.Nf = ob;
   a.Yp = Yp;
+  a.vec16 = ((ldw | b0) & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   const int64_t len = d - b0;
   const int ncb = static_cast<int>((ob + 63) / 64);
   int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(FAR_YP_TILES / ncb, len / 64)));
@@ -390,9 +518,15 @@ int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, co
   a.S = std::max(1, S);
   k_far_y<true><<<dim3(ncb, a.S), FT, FY_SMEM, s>>>(a);
   k_far_gsum<<<(FOB * FOB + 255) / 256, 256, 0, s>>>(Yp, a.S, ob, G);
+  count_launch(2);
+  if (t_stream == nullptr) t_stream = s;
+  else if (t_stream != s) {
+    ITSK_CUDA(cudaEventRecord(ev_handoff, s));
+    ITSK_CUDA(cudaStreamWaitEvent(t_stream, ev_handoff, 0));
+  }
   // T from G and tau, written over G (read completely before the first write)
-  k_far_t<<<1, FT_THREADS, (FOB * (FOB + 1) + FOB * (FOB - 1) / 2) * 8, s>>>(G, taus, b0, ob, G);
-  count_launch(3);
+  k_far_t<<<1, FT_THREADS, ft_smem(), t_stream>>>(G, taus, b0, ob, G);
+  count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
 }
@@ -414,6 +548,7 @@ int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, 
   a.G = G;
   a.taus = taus;
   a.Z = Z;
+  a.vec16 = ((ldw | b0 | c0) & 1) == 0 && ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(Z)) & 15) == 0;
   const int64_t len = d - b0;
   const int ncb = static_cast<int>((Nf + 63) / 64);
   // splits: ~2 CTAs per SM, Yp capacity, >= 64 rows each
@@ -422,7 +557,7 @@ int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, 
   S = std::min<int64_t>(S, std::max<int64_t>(1, len / 64));
   a.S = static_cast<int>(S);
   k_far_y<false><<<dim3(ncb, a.S), FT, FY_SMEM, s>>>(a);
-  k_far_z<<<static_cast<unsigned>((Nf + FZ_WARPS - 1) / FZ_WARPS), 32 * FZ_WARPS, 0, s>>>(a);
+  k_far_z<<<static_cast<unsigned>((Nf + FZ_WARPS * FZ_CPW - 1) / (FZ_WARPS * FZ_CPW)), 32 * FZ_WARPS, FZ_SMEM, s>>>(a);
   k_far_apply<<<dim3(static_cast<unsigned>((len + 127) / 128), ncb), FT, FA_SMEM, s>>>(a);
   count_launch(3);
   ITSK_CHECK_LAUNCH();

@@ -11,7 +11,8 @@ from paper_2311_04362_b200.linalg import qr_workspace
 d, n = int(sys.argv[1]), int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 lib = _lib.lib_for_device(0)
-W0 = torch.randn(d, n + 1, dtype=torch.float64, device="cuda")
+ldw = (n + 2) // 2 * 2  # the solver's even leading dimension
+W0 = torch.randn(d, ldw, dtype=torch.float64, device="cuda")
 W = W0.clone()
 R = torch.empty(n, n, dtype=torch.float64, device="cuda")
 z = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -21,12 +22,18 @@ s = dv.stream_ptr()
 
 def run():
     W.copy_(W0)
-    _lib.check(lib.itsk_qr_aug(dv.ptr(W), d, n, n + 1, dv.ptr(R), dv.ptr(z), dv.ptr(ws), ws.numel(), s))
+    _lib.check(lib.itsk_qr_aug(dv.ptr(W), d, n, ldw, dv.ptr(R), dv.ptr(z), dv.ptr(ws), ws.numel(), s))
 
 
 for _ in range(2):
     run()
 torch.cuda.synchronize()
+ts = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); run(); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print(f"QR d={d} n={n} ldw={ldw}: wall (CUDA events, incl. the W copy) " + " ".join(f"{t:.2f}" for t in ts) + " ms")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(reps):
         run()

@@ -204,6 +204,23 @@ def test_qr_matches_lapack(pkg, orc, m, n, seed):
     assert np.linalg.norm(f.z - z_ref) <= 100 * n * U * np.linalg.norm(rhs)
 
 
+@pytest.mark.parametrize("m,n,seed", [(14000, 1000, 10), (4100, 641, 9)])
+def test_qr_sm_partition_bitwise(pkg, monkeypatch, m, n, seed):
+    """The two-level QR's SM partition (green contexts: the panel chain on
+    16 SMs, the GEMM-shaped updates on the rest) changes no operation order:
+    R and z bitwise equal to the shared-SM run (ITSK_QR_GREEN=0), and the
+    same on a repeat."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    rhs = rng.standard_normal(m)
+    f1 = pkg.householder_qr_econ(a, rhs)
+    f2 = pkg.householder_qr_econ(a, rhs)
+    monkeypatch.setenv("ITSK_QR_GREEN", "0")
+    f0 = pkg.householder_qr_econ(a, rhs)
+    assert np.array_equal(f1.r, f2.r) and np.array_equal(f1.z, f2.z)
+    assert np.array_equal(f1.r, f0.r) and np.array_equal(f1.z, f0.z)
+
+
 @pytest.mark.parametrize("m,n,seed", [(40000, 64, 2), (30000, 130, 4)])
 def test_qr_large_d_fallback_matches_lapack(pkg, orc, m, n, seed):
     """Beyond the panel kernel's shared memory (more than ~25600 rows at
