@@ -147,8 +147,11 @@ int64_t qr_far_yp_doubles();
 // G = V'V on s; T (one CTA) on t_stream (nullptr: s), after s through ev_handoff
 int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, const double* taus, double* Yp,
                        double* G, cudaStream_t s, cudaStream_t t_stream = nullptr, cudaEvent_t ev_handoff = nullptr);
+// parts: 1 = Y = V'W_far only (needs V, not T), 2 = Z = T'Y and W_far -= V Z
+// (after part 1 on the same buffers), 3 = both
 int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, int64_t c0, int64_t Nf,
-                         const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s);
+                         const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s,
+                         int parts = 3);
 int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double* R, double* z,
                  int* singular, double* ws, const QrV2Plan& P, cudaStream_t s);
 

@@ -118,7 +118,7 @@ struct PanelArgs {
 };
 
 #ifdef ITSK_QR2_PROFILE
-__device__ unsigned long long g_qr2_prof[8];
+__device__ unsigned long long g_qr2_prof[12];
 #define Q2P(i) do { if (threadIdx.x == 0 && q == 0) { long long _t = clock64(); _qa[i] += _t - _qt; _qt = _t; } } while (0)
 #else
 #define Q2P(i) do { } while (0)
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   const int C = static_cast<int>(cl.num_blocks()), q = static_cast<int>(cl.block_rank());
 #ifdef ITSK_QR2_PROFILE
   long long _qt = clock64();
-  long long _qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long _qa[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k0 = a.k0, ldw = a.ldw;
@@ -459,6 +459,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
       a.betas[k0 + c] = betl[c];
       a.taus[k0 + c] = taus[c];
     }
+  Q2P(8);
   // G_q = V_own' V_own on DMMA tiles, to global: NT = (NB/8)^2 tiles, each
   // over KS = 16 / NT row splits (every warp busy; 4 interleaved chains per
   // warp), the splits summed in a fixed order through shared memory
@@ -500,7 +501,9 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
       }
     }
   }
+  Q2P(9);
   cl.sync();
+  Q2P(10);
   // G = sum_t G_t in rank order; element e summed by CTA e % C (all C
   // partial loads in flight before the adds: one L2 round trip, not C)
   for (int e = q + C * tid; e < NB * NB; e += C * QP_THREADS) {
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) k_qr_panel(PanelArgs a) {
   Q2P(6);
 #ifdef ITSK_QR2_PROFILE
   if (threadIdx.x == 0 && q == 0)
-    for (int i = 0; i < 8; ++i) atomicAdd(&g_qr2_prof[i], static_cast<unsigned long long>(_qa[i]));
+    for (int i = 0; i < 12; ++i) atomicAdd(&g_qr2_prof[i], static_cast<unsigned long long>(_qa[i]));
 #endif
 }
 
@@ -1150,6 +1153,7 @@ struct QrGreen {
   cudaStream_t side = nullptr;   // the look-ahead's rest of the block (highest priority: the next
                                  // panel's look-ahead waits for it)
   cudaStream_t far = nullptr;    // the far rest (lowest priority: due a block later)
+  cudaStream_t nearY = nullptr;  // the near update's Y = V'W, beside the Gram and T (highest priority)
 };
 
 QrGreen make_qr_green(int dev) {
@@ -1188,12 +1192,14 @@ QrGreen make_qr_green(int dev) {
     return g;
   int lo = 0, hi = 0;
   if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return g;
-  CUstream c0, c1, c2, c3;
+  CUstream c0, c1, c2, c3, c4;
   if (p_stream(&c0, ga, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
       p_stream(&c1, gb, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
       p_stream(&c2, gb, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
-      p_stream(&c3, gb, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS)
+      p_stream(&c3, gb, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
+      p_stream(&c4, gb, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS)
     return g;
+  g.nearY = reinterpret_cast<cudaStream_t>(c4);
   g.chain = reinterpret_cast<cudaStream_t>(c0);
   g.upd = reinterpret_cast<cudaStream_t>(c1);
   g.side = reinterpret_cast<cudaStream_t>(c2);
@@ -1222,7 +1228,7 @@ QrGreen qr_green() {
 }
 
 cudaError_t pooled_event(int which, cudaEvent_t* out) {
-  static cudaEvent_t ev[64][10] = {};
+  static cudaEvent_t ev[64][12] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -1275,7 +1281,8 @@ QrV2Plan qr_v2_plan(int64_t d, int64_t n) {
   if (p.two_level) {
     const int64_t nblk = (n + QR_OB - 1) / QR_OB;
     p.far_off = p.ws_doubles;
-    p.ws_doubles += nblk * QR_OB * QR_OB + 2 * (qr_far_yp_doubles() + static_cast<int64_t>(QR_OB) * N);
+    p.ws_doubles += nblk * QR_OB * QR_OB + 2 * (qr_far_yp_doubles() + static_cast<int64_t>(QR_OB) * N) +
+                    qr_far_yp_doubles();
     // the look-ahead without k_qr_next: a second Yp / Z set for the next
     // panel's update on the main stream
     p.next_off = p.ws_doubles;
@@ -1379,20 +1386,22 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
   cudaEvent_t ev_g = nullptr, ev_far = nullptr, ev_far_all = nullptr;
   bool far_busy = false;
   double* Gfar = ws + P.far_off;
-  double* Ypf[2] = {nullptr, nullptr};
+  double* Ypf[3] = {nullptr, nullptr, nullptr};
   double* Zf[2] = {nullptr, nullptr};
   // green partition: the Gram and near update on `upd` (GEMM partition),
   // handed over to and from the chain through ev_s2u / ev_u2s
-  cudaStream_t upd = nullptr;
-  cudaEvent_t ev_s2u = nullptr, ev_u2s = nullptr;
+  cudaStream_t upd = nullptr, upy = nullptr;
+  cudaEvent_t ev_s2u = nullptr, ev_u2s = nullptr, ev_y = nullptr;
   if (two) {
     int rc = gr.ok ? ITSK_OK : side_stream(&side_far, 1);
     if (rc) return rc;
     if (gr.ok) {
       side_far = gr.far;
       upd = gr.upd;
+      upy = gr.nearY;
       ITSK_CUDA(pooled_event(7, &ev_s2u));
       ITSK_CUDA(pooled_event(8, &ev_u2s));
+      ITSK_CUDA(pooled_event(9, &ev_y));
     }
     ITSK_CUDA(pooled_event(2, &ev_g));
     ITSK_CUDA(pooled_event(3, &ev_far));
@@ -1403,6 +1412,7 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
     Zf[0] = Ypf[0] + qr_far_yp_doubles();
     Ypf[1] = Zf[0] + static_cast<int64_t>(QR_OB) * N;
     Zf[1] = Ypf[1] + qr_far_yp_doubles();
+    Ypf[2] = Zf[1] + static_cast<int64_t>(QR_OB) * N;  // the Gram's partials (beside the near Y)
   }
   for (int64_t k0 = 0; k0 < n; k0 += P.NB) {
     const int kb = static_cast<int>(std::min<int64_t>(P.NB, n - k0));
@@ -1447,19 +1457,30 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
       // the outer block [blk0, horizon) is factored: its far update
       const int ob = static_cast<int>(horizon - blk0);
       double* Gb = Gfar + (blk0 / QR_OB) * QR_OB * QR_OB;
-      // Gram on u (the GEMM partition when green), T on the chain stream
+      // green: the Gram on u and the near update's Y on upy (both need only
+      // V), T on the chain stream; then Z and the apply on u
       const cudaStream_t u = upd ? upd : s;
+      const int64_t nn = std::min<int64_t>(QR_OB, N - horizon);
       if (upd) {
         ITSK_CUDA(cudaEventRecord(ev_s2u, s));
         ITSK_CUDA(cudaStreamWaitEvent(u, ev_s2u, 0));
+        ITSK_CUDA(cudaStreamWaitEvent(upy, ev_s2u, 0));
+        if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(upy, ev_far, 0));  // the previous block's update of these columns
+        int rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], upy, 1);
+        if (rc) return rc;
+        ITSK_CUDA(cudaEventRecord(ev_y, upy));
       }
-      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, taus, Ypf[0], Gb, u, s, ev_u2s);
+      int rc = launch_qr_far_gram(W, d, ldw, blk0, ob, taus, Ypf[upd ? 2 : 0], Gb, u, s, ev_u2s);
       if (rc) return rc;
       ITSK_CUDA(cudaEventRecord(ev_g, s));
-      if (upd) ITSK_CUDA(cudaStreamWaitEvent(u, ev_g, 0));
-      if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(u, ev_far, 0));  // the previous block's far update of these columns
-      const int64_t nn = std::min<int64_t>(QR_OB, N - horizon);
-      rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], u);
+      if (upd) {
+        ITSK_CUDA(cudaStreamWaitEvent(u, ev_g, 0));
+        ITSK_CUDA(cudaStreamWaitEvent(u, ev_y, 0));
+        rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], u, 2);
+      } else {
+        if (far_busy) ITSK_CUDA(cudaStreamWaitEvent(u, ev_far, 0));  // the previous block's update of these columns
+        rc = launch_qr_far_update(W, d, ldw, blk0, ob, horizon, nn, Gb, taus, Ypf[0], Zf[0], u);
+      }
       if (rc) return rc;
       if (upd) {  // the next block's panels need it
         ITSK_CUDA(cudaEventRecord(ev_u2s, u));
@@ -1469,9 +1490,17 @@ int launch_qr_v2(double* W, int64_t d, int64_t n, int64_t ldw, int64_t N, double
         // the far rest on the side stream, the block after next first: the
         // next block's own near update waits only for that part (stream order
         // keeps every later column's updates in block order)
-        ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_g, 0));
         const int64_t f0 = horizon + nn, nf = N - f0, n1 = std::min<int64_t>(QR_OB, nf);
-        rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0, n1, Gb, taus, Ypf[1], Zf[1], side_far);
+        if (upd) {  // its Y needs only V: started before T
+          ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_s2u, 0));
+          rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0, n1, Gb, taus, Ypf[1], Zf[1], side_far, 1);
+          if (rc) return rc;
+          ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_g, 0));
+          rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0, n1, Gb, taus, Ypf[1], Zf[1], side_far, 2);
+        } else {
+          ITSK_CUDA(cudaStreamWaitEvent(side_far, ev_g, 0));
+          rc = launch_qr_far_update(W, d, ldw, blk0, ob, f0, n1, Gb, taus, Ypf[1], Zf[1], side_far);
+        }
         if (rc) return rc;
         ITSK_CUDA(cudaEventRecord(ev_far, side_far));
         if (nf > n1) {
@@ -1567,8 +1596,8 @@ extern "C" void itsk_qrnext_profile_read(unsigned long long* out) {
 
 #ifdef ITSK_QR2_PROFILE
 extern "C" void itsk_qr2_profile_read(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, itsk::g_qr2_prof, sizeof(unsigned long long) * 8);
-  unsigned long long z[8] = {0};
+  cudaMemcpyFromSymbol(out, itsk::g_qr2_prof, sizeof(unsigned long long) * 12);
+  unsigned long long z[12] = {0};
   cudaMemcpyToSymbol(itsk::g_qr2_prof, z, sizeof(z));
 }
 #endif

@@ -21,6 +21,22 @@
 #include "itsk_kernels.cuh"
 
 namespace itsk {
+#ifdef ITSK_FARPROBE
+__device__ unsigned long long g_far_prof[8];
+#define FP(i)                                                     \
+  do {                                                            \
+    __syncthreads();                                              \
+    if (threadIdx.x == 0) {                                       \
+      const long long _t = clock64();                             \
+      atomicAdd(&g_far_prof[i], static_cast<unsigned long long>(_t - _fp0)); \
+      _fp0 = _t;                                                  \
+    }                                                             \
+  } while (0)
+#else
+#define FP(i) \
+  do {        \
+  } while (0)
+#endif
 namespace {
 
 constexpr int FT = 256;          // threads per CTA
@@ -206,71 +222,124 @@ __global__ void k_far_gsum(const double* __restrict__ Gp, int S, int ob, double*
   G[e] = s;
 }
 
-// T of the block (upper triangular, FOB x FOB, row stride FOB): dlarft's
-// forward column-wise recurrence T[i][i] = tau_i, T[0:i, i] = -tau_i
-// T[0:i, 0:i] G[0:i, i] (G = V'V), one CTA, blocked by FT_BLK columns: for a
-// block J the part of every column's mat-vec over the finished blocks,
-// P = T[0:j0, 0:j0] G[0:j0, J] (j0 = J's first column), is one parallel
-// product; the sequential steps then add only the terms inside J (each row's
-// dot split over 4 lanes, combined in a fixed order).  Z = T'Y then needs no
-// sequential substitution (k_far_z).
+// T of the block (upper triangular, FOB x FOB, row stride FOB), dlarft's T
+// for V = [V_1 .. V_8] (16-column blocks), one CTA, by blocks: with T1 the
+// finished leading j0 x j0 part and T_JJ the diagonal block of the next 16
+// columns J,
+//   T_JJ            dlarft's column recurrence on the 16 x 16 block alone
+//                   (T[i][i] = tau_i, T[a][b] = -tau_b sum_{a<=k<b} T[a][k] G[k][b]);
+//                   each lane owns a row and needs only its own row's
+//                   earlier entries: one warp per block, all 8 at once
+//   T[0:j0, J]    = -(T1 G[0:j0, J]) T_JJ     two parallel products, J = 1..7
+// (T = [T1, -T1 V1'V2 T2; 0, T2], the recursive form of dlarft).  A zero
+// tau gives a zero column (T_JJ's column b and so T[0:j0, b]), as dlarft.
+// Z = T'Y then needs no sequential substitution (k_far_z).
 constexpr int FT_THREADS = 512;
 constexpr int FT_BLK = 16;
+constexpr int FT_NB = FOB / FT_BLK;                        // diagonal blocks
+constexpr int FT_GC = FT_BLK * FT_BLK * FT_NB * (FT_NB - 1) / 2;  // G[0:j0, J] for all J, [k][c]
 constexpr size_t ft_smem() {
-  return static_cast<size_t>(FOB * (FOB + 1) + FOB * (FOB - 1) / 2 + FOB * FT_BLK) * 8;
+  return static_cast<size_t>(FOB * (FOB + 1) + FT_GC + FT_NB * FT_BLK * FT_BLK + FOB * FT_BLK) * 8;
 }
 __global__ void __launch_bounds__(FT_THREADS) k_far_t(const double* G, const double* __restrict__ taus,
                                                       int64_t b0, int ob, double* T) {
-  extern __shared__ __align__(16) double tsm[];  // T: FOB x (FOB + 1) | G's strict upper triangle | P
+  extern __shared__ __align__(16) double tsm[];  // T: FOB x (FOB + 1) | Gc | Gd | P
   constexpr int TS = FOB + 1;
-  double* gu = tsm + FOB * TS;                   // column i of G above the diagonal at gu[i (i - 1) / 2 ...]
-  double* P = gu + FOB * (FOB - 1) / 2;          // P[r * FT_BLK + c]
+  double* Gc = tsm + FOB * TS;                   // block J's G[0:j0, J] at Gc + 256 J (J - 1) / 2, [k][c]
+  double* Gd = Gc + FT_GC;                       // G's diagonal blocks, Gd[J][k][c]
+  double* P = Gd + FT_NB * FT_BLK * FT_BLK;      // P[r * FT_BLK + c] = (T1 G[0:j0, J])[r][c]
   __shared__ double ts[FOB];
-  const int tid = threadIdx.x;
-  const int r = tid >> 2, part = tid & 3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef ITSK_FARPROBE
+  long long _fp0 = clock64();
+#endif
+  const int nbk = (ob + FT_BLK - 1) / FT_BLK;
   for (int e = tid; e < FOB * TS; e += FT_THREADS) tsm[e] = 0.0;
-  // every G element the recurrence reads, loaded up front (all in flight)
-  for (int e = tid; e < FOB * FOB; e += FT_THREADS) {
-    const int k = e / FOB, i = e - k * FOB;
-    if (k < i && i < ob) gu[i * (i - 1) / 2 + k] = G[e];
+  // every G element the recurrence reads, loaded up front (all in flight):
+  // the diagonal blocks and, per block J, the rows above it
+  for (int e = tid; e < FT_NB * FT_BLK * FT_BLK; e += FT_THREADS) {
+    const int J = e >> 8, k = (e >> 4) & 15, c = e & 15;
+    const int gk = J * FT_BLK + k, gc = J * FT_BLK + c;
+    Gd[e] = (gk < ob && gc < ob) ? __ldcg(G + gk * FOB + gc) : 0.0;
+  }
+  for (int e = tid; e < FT_GC; e += FT_THREADS) {
+    // e = 256 J (J - 1) / 2 + k * 16 + c with k < 16 J
+    int J = 1;
+    while (J + 1 < FT_NB && FT_BLK * FT_BLK * (J + 1) * J / 2 <= e) ++J;
+    const int off = e - FT_BLK * FT_BLK * J * (J - 1) / 2;
+    const int k = off >> 4, c = off & 15, gc = J * FT_BLK + c;
+    Gc[e] = gc < ob ? __ldcg(G + k * FOB + gc) : 0.0;
   }
   if (tid < FOB) ts[tid] = tid < ob ? taus[b0 + tid] : 0.0;
   __syncthreads();
-  for (int j0 = 0; j0 < ob; j0 += FT_BLK) {
-    const int j1 = min(ob, j0 + FT_BLK);
-    // P[rr][c] = sum_{rr <= k < j0} T[rr][k] G[k][j0 + c], rows rr < j0
-    for (int e = tid; e < j0 * FT_BLK; e += FT_THREADS) {
-      const int rr = e / FT_BLK, c = e - rr * FT_BLK;
-      double s0 = 0.0, s1 = 0.0;
-      if (j0 + c < j1) {
-        const double* w = gu + (j0 + c) * (j0 + c - 1) / 2;
-        const double* tr = tsm + rr * TS;
-        int k = rr;
-        for (; k + 1 < j0; k += 2) {
-          s0 = fma(tr[k], w[k], s0);
-          s1 = fma(tr[k + 1], w[k + 1], s1);
+  FP(0);
+  // (a) every diagonal block T_JJ (they depend on G_JJ and tau only): warp
+  // J, lane a owns row a of the block and needs only its own row's earlier
+  // entries (dlarft's recurrence T[a][b] = -tau_b sum_{a<=k<b} T[a][k] G[k][b])
+  if (warp < nbk && lane < FT_BLK) {
+    const int j0 = warp * FT_BLK, bw = min(FT_BLK, ob - j0);
+    const double* gd = Gd + warp * FT_BLK * FT_BLK;
+    double row[FT_BLK];
+#pragma unroll
+    for (int b = 0; b < FT_BLK; ++b) row[b] = 0.0;
+#pragma unroll
+    for (int b = 0; b < FT_BLK; ++b) {
+      const double tb = b < bw ? ts[j0 + b] : 0.0;
+      if (b == lane) {
+        row[b] = tb;
+      } else if (b > lane) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < FT_BLK; k += 2) {
+          if (k >= lane && k < b) s0 = fma(row[k], gd[k * FT_BLK + b], s0);
+          if (k + 1 >= lane && k + 1 < b) s1 = fma(row[k + 1], gd[(k + 1) * FT_BLK + b], s1);
         }
-        if (k < j0) s0 = fma(tr[k], w[k], s0);
+        row[b] = -tb * (s0 + s1);
       }
-      P[e] = s0 + s1;
+    }
+    if (lane < bw)
+#pragma unroll
+      for (int b = 0; b < FT_BLK; ++b)
+        if (b < bw) tsm[(j0 + lane) * TS + j0 + b] = row[b];
+  }
+  __syncthreads();
+  FP(2);
+  // (b) T[0:j0, J] = -(T1 G[0:j0, J]) T_JJ, block after block
+  for (int J = 1; J < nbk; ++J) {
+    const int j0 = J * FT_BLK, bw = min(FT_BLK, ob - j0);
+    const double* gc = Gc + FT_BLK * FT_BLK * J * (J - 1) / 2;
+    // P: thread (r, c), 4 independent chains over k; 16 lanes share row r
+    for (int e = tid; e < j0 * FT_BLK; e += FT_THREADS) {
+      const int r = e / FT_BLK, c = e - r * FT_BLK;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* tr = tsm + r * TS;
+      int k = r;
+      for (; k + 3 < j0; k += 4) {
+        a0 = fma(tr[k], gc[k * FT_BLK + c], a0);
+        a1 = fma(tr[k + 1], gc[(k + 1) * FT_BLK + c], a1);
+        a2 = fma(tr[k + 2], gc[(k + 2) * FT_BLK + c], a2);
+        a3 = fma(tr[k + 3], gc[(k + 3) * FT_BLK + c], a3);
+      }
+      for (; k < j0; ++k) a0 = fma(tr[k], gc[k * FT_BLK + c], a0);
+      P[e] = (a0 + a1) + (a2 + a3);
     }
     __syncthreads();
-    for (int i = j0; i < j1; ++i) {
-      const double* w = gu + i * (i - 1) / 2;
+    FP(1);
+    for (int e = tid; e < j0 * FT_BLK; e += FT_THREADS) {
+      const int r = e / FT_BLK, c = e - r * FT_BLK;
+      if (c >= bw) continue;
       double sum = 0.0;
-      if (r < i)
-        for (int k = max(r, j0) + part; k < i; k += 4) sum = fma(tsm[r * TS + k], w[k], sum);
-      sum += __shfl_xor_sync(FULL, sum, 1);
-      sum += __shfl_xor_sync(FULL, sum, 2);
-      if (part == 0 && r < i) tsm[r * TS + i] = -ts[i] * (r < j0 ? P[r * FT_BLK + (i - j0)] + sum : sum);
-      if (tid == 0) tsm[i * TS + i] = ts[i];
-      __syncthreads();
+      for (int k = 0; k <= c; ++k) sum = fma(P[r * FT_BLK + k], tsm[(j0 + k) * TS + j0 + c], sum);
+      tsm[r * TS + j0 + c] = -sum;
     }
+    __syncthreads();
+    FP(3);
   }
   for (int e = tid; e < FOB * FOB; e += FT_THREADS) {
     const int rr = e / FOB, c = e - rr * FOB;
     T[e] = (rr < ob && c < ob) ? tsm[rr * TS + c] : 0.0;
   }
+  FP(4);
 }
 
 // Z = T'Y, one column per warp: lane j holds z_j for j = lane + 32 q; y_k is
@@ -532,7 +601,7 @@ int launch_qr_far_gram(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, co
 }
 
 int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, int64_t c0, int64_t Nf,
-                         const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s) {
+                         const double* G, const double* taus, double* Yp, double* Z, cudaStream_t s, int parts) {
   if (Nf <= 0) return ITSK_OK;
   int rc = far_attrs();
   if (rc) return rc;
@@ -556,12 +625,24 @@ int launch_qr_far_update(double* W, int64_t d, int64_t ldw, int64_t b0, int ob, 
   S = std::min<int64_t>(S, std::max<int64_t>(1, FAR_YP_TILES / ncb));
   S = std::min<int64_t>(S, std::max<int64_t>(1, len / 64));
   a.S = static_cast<int>(S);
-  k_far_y<false><<<dim3(ncb, a.S), FT, FY_SMEM, s>>>(a);
-  k_far_z<<<static_cast<unsigned>((Nf + FZ_WARPS * FZ_CPW - 1) / (FZ_WARPS * FZ_CPW)), 32 * FZ_WARPS, FZ_SMEM, s>>>(a);
-  k_far_apply<<<dim3(static_cast<unsigned>((len + 127) / 128), ncb), FT, FA_SMEM, s>>>(a);
-  count_launch(3);
+  if (parts & 1) {
+    k_far_y<false><<<dim3(ncb, a.S), FT, FY_SMEM, s>>>(a);
+    count_launch();
+  }
+  if (parts & 2) {
+    k_far_z<<<static_cast<unsigned>((Nf + FZ_WARPS * FZ_CPW - 1) / (FZ_WARPS * FZ_CPW)), 32 * FZ_WARPS, FZ_SMEM,
+              s>>>(a);
+    k_far_apply<<<dim3(static_cast<unsigned>((len + 127) / 128), ncb), FT, FA_SMEM, s>>>(a);
+    count_launch(2);
+  }
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
 }
 
 }  // namespace itsk
+
+#ifdef ITSK_FARPROBE
+extern "C" void itsk_farprobe_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, itsk::g_far_prof, sizeof(unsigned long long) * 8);
+}
+#endif
