@@ -65,6 +65,26 @@ cudaError_t allow_max_smem(const void* func) {
   return e;
 }
 
+// The device's default memory pool gives freed blocks back to the driver at
+// the next synchronisation unless a release threshold is set: the sketch's
+// stream-ordered scratch would then be re-mapped on every solve (measured at
+// C4: ~9 ms of host time per itsk_sketch call).  Once per device.
+cudaError_t keep_async_pool() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_tuple(dev, static_cast<const void*>(nullptr), -2);
+  if (g_attr_done.count(key)) return cudaSuccess;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e == cudaSuccess) g_attr_done.insert(key);
+  return e;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("ITSK_NO_PDL");

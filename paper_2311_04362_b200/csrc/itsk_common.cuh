@@ -43,6 +43,7 @@ int num_sms();
 cudaError_t allow_max_smem(const void* func);
 // cudaFuncSetAttribute once per (device, function, attribute)
 cudaError_t func_attr_once(const void* func, cudaFuncAttribute attr, int value);
+cudaError_t keep_async_pool();  // default mempool keeps its freed blocks (once per device)
 
 constexpr unsigned FULL = 0xffffffffu;
 

@@ -513,6 +513,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
       uint32_t* bnd = nullptr;
       const size_t cbytes = sizeof(unsigned) * static_cast<size_t>(nwin) * npanel;
       const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * SW_RPW * nwin;
+      ITSK_CUDA(keep_async_pool());
       ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wdone), cbytes, s));
       ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bnd), bbytes, s));
       ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
