@@ -122,18 +122,19 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
 // window is ~(pairs / SW_U), not (rows x rounds); each row's running sum
 // lives in shared memory between its window segments.  Every output is the
 // same sum in the same order as k_sketch_gather: bitwise scipy's.
-constexpr int SW_WARPS = 16, SW_RPW = 12, SW_DRIFT = 2;
-// CL adjacent columns per lane (a panel of 32 CL), U sources per chunk
-template <int CL>
-constexpr size_t sw_smem_bytes() { return sizeof(double) * SW_WARPS * SW_RPW * 32 * CL; }
+// CL adjacent columns per lane (a panel of 32 CL), U sources per chunk,
+// NWARP warps per CTA with RPW sketch rows each
+template <int CL, int NWARP, int RPW>
+constexpr size_t sw_smem_bytes() { return sizeof(double) * NWARP * RPW * 32 * CL; }
 
-template <int CL, int U>
+template <int CL, int U, int SW_WARPS, int SW_RPW>
 __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
     const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
     const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
     double* __restrict__ W, int64_t ldw, uint32_t m, uint32_t R, int nwin, int npanel, unsigned* wdone,
     uint32_t* __restrict__ bnd, int flags) {
   const int vec = flags & 1;
+  const int SW_DRIFT = flags >> 8;  // windows a warp may run ahead of the slowest
   static_assert(CL == 2 || CL == 4, "columns per lane");
   constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
   extern __shared__ __align__(16) double sw_sm[];
@@ -165,7 +166,16 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
     }
   }
   __syncwarp();
-  const unsigned arrivals = gridDim.x * SW_WARPS;
+  // Window arrivals are counted per CTA in shared memory; the CTA's last warp
+  // adds one to the window's global counter, and the grid's last CTA writes
+  // the window's epoch (g + 1) into every CTA's own flag line — so a warp
+  // polls a line only its CTA reads (2368 warps polling and incrementing one
+  // counter made a hot spot worth ~7 us per window step).
+  __shared__ unsigned cta_cnt[8];
+  if (threadIdx.x < 8) cta_cnt[threadIdx.x] = 0u;
+  __syncthreads();
+  unsigned* wflag = wdone + static_cast<int64_t>(nwin) * npanel;           // gridDim.x lines of 32 words
+  const volatile unsigned* myflag = wflag + 32 * static_cast<int64_t>(blockIdx.x);
   for (int p = 0; p < npanel; ++p) {
     // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
     // warp is one contiguous 512-byte segment)
@@ -188,8 +198,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
     for (int w = 0; w < nwin; ++w) {
       const int g = p * nwin + w;
       if (g >= SW_DRIFT) {
-        if (lane == 0)
-          while (*reinterpret_cast<volatile unsigned*>(wdone + g - SW_DRIFT) < arrivals) __nanosleep(32);
+        if (lane == 0) {
+          const unsigned q = static_cast<unsigned>(g - SW_DRIFT);
+          while (myflag[q & 7u] < q + 1u) __nanosleep(32);  // slot values only grow (q + 1, q + 9, ...)
+        }
         __syncwarp();
       }
       const uint32_t tk = lane < SW_RPW ? wb[lane * nwin + w] : 0u;
@@ -205,26 +217,32 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
       // lane u: position P + u (clamped into the window's list, so every
       // lane's row pointer is valid; positions past the end are not added):
       // its row and sign packed in ku, its source row's panel segment in pu
-      auto locate = [&](uint32_t P, int& ku, uint32_t& sv, const double*& pu) {
+      auto locate = [&](uint32_t P, int& ku, uint32_t& sv) {
         const uint32_t pos = min(P + static_cast<uint32_t>(lane & (U - 1)), total - 1);
         int k = 0;
 #pragma unroll
         for (int kk = 0; kk < SW_RPW - 1; ++kk) k += pos >= __shfl_sync(FULL, incl, kk) ? 1 : 0;
         const uint32_t bk = __shfl_sync(FULL, base, k);
         sv = __ldg(src + bk + pos);
-        ku = (k << 1) | static_cast<int>(sv >> 31);
-        pu = Ap + static_cast<int64_t>(sv & 0x7fffffffu) * lda;  // the panel's start: lane-independent
+        ku = k;  // the sign joins it (ku << 1 | sign) once sv has landed
       };
+      // the source row's panel segment (lane-independent start)
+      auto rowptr = [&](uint32_t w) { return Ap + static_cast<int64_t>(w & 0x7fffffffu) * lda; };
       int ku = 0, kcur = -1;
       uint32_t sv = 0;
       const double* pu = Ap;
       double2 acc[NV];
-      if (total > 0) locate(0, ku, sv, pu);
+      if (total > 0) {
+        locate(0, ku, sv);
+        ku = (ku << 1) | static_cast<int>(sv >> 31);
+        pu = rowptr(sv);
+      }
       for (uint32_t P = 0; P < total; P += U) {
         int kn = 0;
         uint32_t svn = 0;
-        const double* pn = Ap;
-        if (P + U < total) locate(P + U, kn, svn, pn);
+        // the next chunk's source words are in flight under this chunk's
+        // loads and adds: nothing below depends on svn before the chunk ends
+        if (P + U < total) locate(P + U, kn, svn);
         const int nu = static_cast<int>(min(total - P, static_cast<uint32_t>(U)));
         double2 v[U][NV];
         if (allv) {
@@ -270,20 +288,265 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
           }
         }
         sv = svn;
-        ku = kn;
-        pu = pn;
+        ku = (kn << 1) | static_cast<int>(svn >> 31);
+        pu = rowptr(svn);
       }
       if (kcur >= 0)
 #pragma unroll
         for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
       sk = tk;
       __syncwarp();
-      if (lane == 0) atomicAdd(wdone + g, 1u);
+      int bcast = 0;
+      if (lane == 0) {
+        if (atomicAdd(&cta_cnt[g & 7], 1u) == SW_WARPS - 1) {
+          // every warp of the CTA has arrived: the slot is next used 8 windows
+          // on, which no warp reaches before window g + 8 - drift > g is
+          // complete everywhere (drift < 8)
+          cta_cnt[g & 7] = 0u;
+          __threadfence_block();
+          bcast = atomicAdd(wdone + g, 1u) == gridDim.x - 1 ? 1 : 0;
+        }
+      }
+      if (__shfl_sync(FULL, bcast, 0))
+        for (unsigned c = lane; c < gridDim.x; c += 32)
+          *reinterpret_cast<volatile unsigned*>(wflag + 32 * static_cast<int64_t>(c) + (g & 7)) =
+              static_cast<unsigned>(g) + 1u;
     }
 #pragma unroll
     for (int k = 0; k < SW_RPW; ++k) {
       const int64_t i = gw + NW * k;
       if (i >= d) continue;
+#pragma unroll
+      for (int h = 0; h < NV; ++h) {
+        const double2 a = acc_sm[k * 16 * CL + 32 * h + lane];
+        if (cA + 64 * h < ncol) W[i * ldw + cA + 64 * h] = a.x;
+        if (cA + 64 * h + 1 < ncol) W[i * ldw + cA + 64 * h + 1] = a.y;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Streamed window sweep: the same schedule with no per-window pipeline
+// drain.  k_sketch_sweep pays, per (panel, window) step and warp, a boundary
+// load, a scan, a dependent source-word load and a partly filled last chunk
+// (~2.4 us of the ~17 us a 20000-row window step takes at C4).  Here the
+// prologue writes each warp's (row, source) pairs ONCE in processing order
+// (window-major, rows ascending inside a window, sources ascending inside a
+// row) as 8-byte entries {source word, local row}; a panel is then one
+// uninterrupted stream of U-entry chunks: the entries of the next chunk are
+// loaded under the current chunk's 16-byte row loads, windows only gate the
+// issue (a chunk whose last entry lies in window w waits for window
+// w - drift to be complete everywhere) and are counted as the stream passes
+// them.  A warp owns a contiguous block of sketch rows, so its entries occupy
+// the index range of its rows in the pattern's CSR.  Same sums in the same
+// order: bitwise scipy's.
+__host__ __device__ __forceinline__ uint32_t sw_win(uint32_t j, double inv_r) {
+  // monotone in j; used wherever a source row is mapped to its window
+  return static_cast<uint32_t>(static_cast<double>(j) * inv_r);
+}
+
+template <int CL, int U, int SW_WARPS, int SW_RPW>
+__global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
+    const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
+    const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
+    double* __restrict__ W, int64_t ldw, double inv_r, int nwin, int npanel, unsigned* wdone,
+    uint32_t* __restrict__ bnd, uint2* ord, int flags) {
+  const int vec = flags & 1;
+  const int drift = flags >> 8;  // windows a warp may run ahead of the slowest
+  static_assert(CL == 2 || CL == 4, "columns per lane");
+  static_assert(U <= 32 && (U & (U - 1)) == 0 && SW_RPW <= 32, "chunk / row shape");
+  constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
+  extern __shared__ __align__(16) double sw_sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t NW = static_cast<int64_t>(gridDim.x) * SW_WARPS;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * SW_WARPS + warp;
+  const int64_t ncol = n + (b ? 1 : 0);
+  double2* acc_sm = reinterpret_cast<double2*>(sw_sm + static_cast<int64_t>(warp) * SW_RPW * PANEL);
+  // rows [row0, row0 + nrows) (d = q NW + rem: the first rem warps own q + 1)
+  const int64_t qr = d / NW, rem = d % NW;
+  const int64_t row0 = gw * qr + (gw < rem ? gw : rem);
+  const int nrows = static_cast<int>(qr + (gw < rem ? 1 : 0));
+  const bool rowok = lane < nrows;
+  const uint32_t r0 = rowok ? ptr[row0 + lane] : 0u, r1 = rowok ? ptr[row0 + lane + 1] : 0u;
+  const uint32_t e0 = ptr[row0];
+  const uint32_t etot = ptr[row0 + nrows] - e0;
+  // prologue 1: the end of every window's segment of every own row (positions
+  // p-1, p in windows wp < wc end windows [wp, wc) at p; the row end is a
+  // sentinel in window nwin)
+  uint32_t* wb = bnd + gw * SW_RPW * static_cast<int64_t>(nwin);
+  for (int k = 0; k < nrows; ++k) {
+    const uint32_t a0 = __shfl_sync(FULL, r0, k), a1 = __shfl_sync(FULL, r1, k);
+    int carry = 0;
+    for (uint32_t q = a0; q <= a1; q += 32) {
+      const uint32_t p = q + lane;
+      const int wc = p < a1 ? static_cast<int>(sw_win(src[p] & 0x7fffffffu, inv_r)) : nwin;
+      int wp = __shfl_up_sync(FULL, wc, 1);
+      if (lane == 0) wp = carry;
+      if (p <= a1)
+        for (int w = wp; w < wc; ++w) wb[k * nwin + w] = p;
+      carry = __shfl_sync(FULL, wc, 31);
+    }
+  }
+  __syncwarp();
+  // prologue 2: the entries in processing order
+  {
+    uint32_t sk = r0, o = e0;
+    for (int w = 0; w < nwin; ++w) {
+      const uint32_t tk = rowok ? wb[lane * nwin + w] : 0u;
+      const uint32_t cnt = rowok ? tk - sk : 0u;
+      uint32_t incl = cnt;  // inclusive scan: row k covers flattened positions [incl - cnt, incl)
+#pragma unroll
+      for (int q = 1; q < 32; q <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, q);
+        if (lane >= q) incl += t;
+      }
+      const uint32_t total = __shfl_sync(FULL, incl, 31);
+      const uint32_t base = sk - (incl - cnt);  // source index = base_k + position
+      for (uint32_t P = 0; P < total; P += 32) {
+        const uint32_t pos = min(P + lane, total - 1);
+        int k = 0;
+#pragma unroll
+        for (int kk = 0; kk < SW_RPW - 1; ++kk) k += pos >= __shfl_sync(FULL, incl, kk) ? 1 : 0;
+        const uint32_t bk = __shfl_sync(FULL, base, k);
+        if (P + lane < total) ord[o + pos] = make_uint2(src[bk + pos], static_cast<uint32_t>(k));
+      }
+      o += total;
+      sk = tk;
+    }
+  }
+  __syncwarp();
+  // Window arrivals are counted per CTA in shared memory; the CTA's last warp
+  // adds one to the window's global counter, and the grid's last CTA writes
+  // the window's epoch (g + 1) into every CTA's own flag line, the only line
+  // the CTA's warps poll.
+  __shared__ unsigned cta_cnt[8];
+  if (threadIdx.x < 8) cta_cnt[threadIdx.x] = 0u;
+  __syncthreads();
+  unsigned* wflag = wdone + static_cast<int64_t>(nwin) * npanel;  // gridDim.x lines of 32 words
+  const volatile unsigned* myflag = wflag + 32 * static_cast<int64_t>(blockIdx.x);
+  int known = -1;  // highest global window step known complete
+  auto wait_for = [&](int gq) {
+    if (gq > known) {
+      if (lane == 0)
+        while (myflag[gq & 7] < static_cast<unsigned>(gq) + 1u) __nanosleep(32);
+      __syncwarp();
+      known = gq;
+    }
+  };
+  auto arrive = [&](int g) {
+    // the CTA's counter slot g & 7 last counted window g - 8: a warp with few
+    // or no entries must not run more than a slot ring ahead of the grid
+    wait_for(g - 7);
+    int bcast = 0;
+    if (lane == 0) {
+      if (atomicAdd(&cta_cnt[g & 7], 1u) == SW_WARPS - 1) {
+        // the slot is next used 8 windows on, which no warp reaches before
+        // window g + 8 - drift > g is complete everywhere (drift < 8)
+        cta_cnt[g & 7] = 0u;
+        __threadfence();
+        bcast = atomicAdd(wdone + g, 1u) == gridDim.x - 1 ? 1 : 0;
+      }
+    }
+    if (__shfl_sync(FULL, bcast, 0))
+      for (unsigned c = lane; c < gridDim.x; c += 32)
+        *reinterpret_cast<volatile unsigned*>(wflag + 32 * static_cast<int64_t>(c) + (g & 7)) =
+            static_cast<unsigned>(g) + 1u;
+  };
+  const uint2* my = ord + e0;
+  for (int p = 0; p < npanel; ++p) {
+    // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
+    // warp is one contiguous 512-byte segment)
+    const int64_t cA = static_cast<int64_t>(p) * PANEL + 2 * lane;
+    const bool allv = __all_sync(FULL, vec && cA + 64 * (NV - 1) + 1 < n);
+    int kind[CL];
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+      const int64_t col = cA + 64 * (c >> 1) + (c & 1);
+      kind[c] = col < n ? 0 : (col == n && b ? 1 : 2);
+    }
+    const double* Ap = A + static_cast<int64_t>(p) * PANEL;
+    const double* Ac = Ap + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < SW_RPW; ++k)
+#pragma unroll
+      for (int h = 0; h < NV; ++h) acc_sm[k * 16 * CL + 32 * h + lane] = make_double2(0.0, 0.0);
+    __syncwarp();
+    const int g0 = p * nwin;
+    int arrived = 0;  // windows of this panel this warp has counted itself done with
+    int kcur = -1;
+    double2 acc[NV];
+    // lane u (mod U): entry P + u, clamped into the list
+    uint2 ent = make_uint2(0u, 0u);
+    if (etot > 0) ent = my[min(static_cast<uint32_t>(lane & (U - 1)), etot - 1)];
+    for (uint32_t P = 0; P < etot; P += U) {
+      uint2 entn = make_uint2(0u, 0u);
+      if (P + U < etot) entn = my[min(P + U + static_cast<uint32_t>(lane & (U - 1)), etot - 1)];
+      const int nu = static_cast<int>(min(etot - P, static_cast<uint32_t>(U)));
+      const uint32_t sv = ent.x;
+      const int wf = static_cast<int>(sw_win(__shfl_sync(FULL, sv, 0) & 0x7fffffffu, inv_r));
+      const int wl = static_cast<int>(sw_win(__shfl_sync(FULL, sv, nu - 1) & 0x7fffffffu, inv_r));
+      // everything before this chunk is added: windows below its first are done
+      while (arrived < wf) arrive(g0 + arrived++);
+      // gate: window wl - drift complete everywhere (never one this warp has
+      // not counted itself done with: a chunk may span more than `drift`)
+      wait_for(g0 + min(wl - drift, wf - 1));
+      const double* pu = Ap + static_cast<int64_t>(sv & 0x7fffffffu) * lda;  // lane-independent start
+      double2 v[U][NV];
+      if (allv) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double2* q = reinterpret_cast<const double2*>(
+                                 __shfl_sync(FULL, reinterpret_cast<uintptr_t>(pu), u)) + lane;
+#pragma unroll
+          for (int h = 0; h < NV; ++h) v[u][h] = __ldg(q + 32 * h);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = __shfl_sync(FULL, sv, u) & 0x7fffffffu;
+          const double* arow = Ac + j * lda;
+#pragma unroll
+          for (int h = 0; h < NV; ++h) {
+            const int c0 = 2 * h, c1 = 2 * h + 1;
+            v[u][h].x = kind[c0] == 0 ? arow[64 * h] : (kind[c0] == 1 ? b[j] : 0.0);
+            v[u][h].y = kind[c1] == 0 ? arow[64 * h + 1] : (kind[c1] == 1 ? b[j] : 0.0);
+          }
+        }
+      }
+      const int ku = static_cast<int>(ent.y << 1) | static_cast<int>(sv >> 31);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = __shfl_sync(FULL, ku, u);
+        if (u < nu) {
+          const int k = kk >> 1;
+          if (k != kcur) {
+            if (kcur >= 0)
+#pragma unroll
+              for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
+#pragma unroll
+            for (int h = 0; h < NV; ++h) acc[h] = acc_sm[k * 16 * CL + 32 * h + lane];
+            kcur = k;
+          }
+          const double sg = (kk & 1) ? -scale : scale;
+#pragma unroll
+          for (int h = 0; h < NV; ++h) {
+            acc[h].x = __dadd_rn(acc[h].x, __dmul_rn(sg, v[u][h].x));
+            acc[h].y = __dadd_rn(acc[h].y, __dmul_rn(sg, v[u][h].y));
+          }
+        }
+      }
+      ent = entn;
+    }
+    if (kcur >= 0)
+#pragma unroll
+      for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
+    __syncwarp();
+    while (arrived < nwin) arrive(g0 + arrived++);
+#pragma unroll
+    for (int k = 0; k < SW_RPW; ++k) {
+      const int64_t i = row0 + k;
+      if (k >= nrows) continue;
 #pragma unroll
       for (int h = 0; h < NV; ++h) {
         const double2 a = acc_sm[k * 16 * CL + 32 * h + lane];
@@ -427,10 +690,14 @@ struct SketchTune {
   int gcpl = 0;       // register gather: cap on columns-per-lane (more column blocks)
   int unr = 0;        // register gather: sources per unrolled group (0 = heuristic)
   int swcl = 0;      // window sweep columns per lane (2 or 4; A/B, same bits)
+  int stream = 1;     // window sweep: entries materialised in processing order (0: per-window walk; same bits)
+  int drift = 2;      // window sweep: windows a warp may run ahead (L2 working set; same bits)
   int sweep = -1;     // window sweep: -1 auto (large A), 0 off, 1 on, > 1 on with that many window rows (same bits)
   SketchTune() {
     if (const char* e = getenv("ITSK_SKETCH_SWEEP")) sweep = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_SWCL")) swcl = atoi(e);
+    if (const char* e = getenv("ITSK_SKETCH_STREAM")) stream = atoi(e);
+    if (const char* e = getenv("ITSK_SKETCH_DRIFT")) drift = std::min(7, std::max(1, atoi(e)));
     if (const char* e = getenv("ITSK_SKETCH_RING")) ring = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_UNR")) unr = atoi(e);
@@ -499,34 +766,52 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   // grid's warps in registers
   {
     const int nsm = num_sms();
-    const int64_t nw = static_cast<int64_t>(nsm) * SW_WARPS;
+    // kernel shapes (all the same bits): columns per lane, sources per chunk,
+    // warps per CTA, sketch rows per warp
+    struct SwShape { const void* fn; const void* fn_stream; int cl, warps, rpw; size_t smem; };
+#define ITSK_SW(CLV, UV, WV, RV)                                          \
+  {reinterpret_cast<const void*>(k_sketch_sweep<CLV, UV, WV, RV>),        \
+   reinterpret_cast<const void*>(k_sketch_stream<CLV, UV, WV, RV>), CLV, WV, RV, sw_smem_bytes<CLV, WV, RV>()}
+    static const SwShape shapes[] = {ITSK_SW(4, 8, 16, 12), ITSK_SW(2, 16, 16, 12), ITSK_SW(4, 4, 24, 8),
+                                     ITSK_SW(4, 16, 8, 24)};
+#undef ITSK_SW
+    const SwShape& sh = shapes[tu.swcl == 2 ? 1 : (tu.swcl == 6 ? 2 : (tu.swcl == 7 ? 3 : 0))];
+    const int64_t nw = static_cast<int64_t>(nsm) * sh.warps;
     // auto from 16 GB of [A|b] (C4, 64 GB: 59 vs 72 ms; C3, 4 GB: 5.3 vs
     // 4.0 ms, where the gather still finds part of A in L2)
     const bool big = m * ncol * 8 >= (16ll << 30);
     if ((tu.sweep > 0 || (tu.sweep < 0 && big)) && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
-        rg.j1 == 0xffffffffu && !rg.accum && d <= nw * SW_RPW && m < (1ll << 31)) {
-      const int cl = tu.swcl == 2 ? 2 : 4;
+        rg.j1 == 0xffffffffu && !rg.accum && d <= nw * sh.rpw && m < (1ll << 31)) {
+      const int cl = sh.cl;
       const uint32_t R = tu.sweep > 1 ? static_cast<uint32_t>(tu.sweep) : (cl == 2 ? 40000u : 20000u);
-      const int nwin = static_cast<int>((m + R - 1) / R);
+      const double inv_r = 1.0 / static_cast<double>(R);
+      const int nwin = tu.stream ? static_cast<int>(sw_win(static_cast<uint32_t>(m - 1), inv_r)) + 1
+                                 : static_cast<int>((m + R - 1) / R);
       const int npanel = static_cast<int>((ncol + 32 * cl - 1) / (32 * cl));
       unsigned* wdone = nullptr;
       uint32_t* bnd = nullptr;
-      const size_t cbytes = sizeof(unsigned) * static_cast<size_t>(nwin) * npanel;
-      const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * SW_RPW * nwin;
+      // per-window counters, then one 128-byte flag line per CTA
+      const size_t cbytes = sizeof(unsigned) * (static_cast<size_t>(nwin) * npanel + 32 * static_cast<size_t>(nsm));
+      const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * sh.rpw * nwin;
       ITSK_CUDA(keep_async_pool());
       ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wdone), cbytes, s));
       ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bnd), bbytes, s));
       ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
-      int flags = (lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0;
-      const void* fn = cl == 2 ? reinterpret_cast<const void*>(k_sketch_sweep<2, 16>)
-                               : reinterpret_cast<const void*>(k_sketch_sweep<4, 8>);
-      const size_t smem = cl == 2 ? sw_smem_bytes<2>() : sw_smem_bytes<4>();
+      uint2* ord = nullptr;  // the streamed sweep's entries in processing order
+      if (tu.stream) ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ord), sizeof(uint2) * static_cast<size_t>(m) * zeta, s));
+      int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8);
+      const void* fn = tu.stream ? sh.fn_stream : sh.fn;
+      const size_t smem = sh.smem;
       ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       const uint32_t mm = static_cast<uint32_t>(m);
       void* args[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
                       const_cast<uint32_t*>(&mm), const_cast<uint32_t*>(&R), const_cast<int*>(&nwin),
                       const_cast<int*>(&npanel), &wdone, &bnd, &flags};
-      ITSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(32 * SW_WARPS), args, smem, s));
+      void* args_st[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
+                         const_cast<double*>(&inv_r), const_cast<int*>(&nwin), const_cast<int*>(&npanel),
+                         &wdone, &bnd, &ord, &flags};
+      ITSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(32 * sh.warps), tu.stream ? args_st : args, smem, s));
+      if (ord) ITSK_CUDA(cudaFreeAsync(ord, s));
       count_launch();
       ITSK_CUDA(cudaFreeAsync(bnd, s));
       ITSK_CUDA(cudaFreeAsync(wdone, s));

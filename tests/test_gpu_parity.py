@@ -161,14 +161,22 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     a = buf[:, :n]
     b = torch.randn(m, dtype=torch.float64, device=dev, generator=g) if withb else None
     s = pkg.sparse_sign_new(d, m, 8, 5)
-    monkeypatch.setenv("ITSK_SKETCH_SWEEP", "1")  # on below its automatic 16 GB threshold
-    got = s.apply_dense(a, b)
-    monkeypatch.setenv("ITSK_SKETCH_SWCL", "2")
-    got2 = s.apply_dense(a, b)
     monkeypatch.setenv("ITSK_SKETCH_SWEEP", "0")
     ref = s.apply_dense(a, b)
-    assert torch.equal(got, ref)
-    assert torch.equal(got2, ref)
+    # the streamed sweep (entries materialised in processing order) and the
+    # per-window walk; window rows: default, small (many windows per chunk: a
+    # chunk spanning more than `drift` windows must not wait for itself)
+    for stream in ("1", "0"):
+        monkeypatch.setenv("ITSK_SKETCH_STREAM", stream)
+        for sweep, swcl, drift in (("1", "0", "2"), ("1", "2", "2"), ("7000", "0", "3"), ("7000", "7", "1"),
+                                   ("97", "6", "1")):
+            if sweep == "97" and (stream == "0" or m > 300000):
+                continue  # thousands of windows: the streamed kernel on the smaller shapes only
+            monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 16 GB threshold
+            monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
+            monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
+            got = s.apply_dense(a, b)
+            assert torch.equal(got, ref), (stream, sweep, swcl, drift)
 
 
 def test_pattern_argument_errors(pkg):
