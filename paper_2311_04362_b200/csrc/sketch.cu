@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
           const double2* q = reinterpret_cast<const double2*>(
                                  __shfl_sync(FULL, reinterpret_cast<uintptr_t>(pu), u)) + lane;
 #pragma unroll
-          for (int h = 0; h < NV; ++h) v[u][h] = __ldg(q + 32 * h);
+          for (int h = 0; h < NV; ++h) v[u][h] = u < nu ? __ldg(q + 32 * h) : make_double2(0.0, 0.0);
         }
       } else {
 #pragma unroll
@@ -509,31 +509,36 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
 #pragma unroll
           for (int h = 0; h < NV; ++h) {
             const int c0 = 2 * h, c1 = 2 * h + 1;
-            v[u][h].x = kind[c0] == 0 ? arow[64 * h] : (kind[c0] == 1 ? b[j] : 0.0);
-            v[u][h].y = kind[c1] == 0 ? arow[64 * h + 1] : (kind[c1] == 1 ? b[j] : 0.0);
+            v[u][h].x = u >= nu ? 0.0 : (kind[c0] == 0 ? arow[64 * h] : (kind[c0] == 1 ? b[j] : 0.0));
+            v[u][h].y = u >= nu ? 0.0 : (kind[c1] == 0 ? arow[64 * h + 1] : (kind[c1] == 1 ? b[j] : 0.0));
           }
         }
       }
-      const int ku = static_cast<int>(ent.y << 1) | static_cast<int>(sv >> 31);
+      // the chunk's row switches and signs as ballots (warp-uniform masks:
+      // the per-source tests below are uniform branches); slots past the end
+      // of the list hold zeros and add +0.0, which changes no sum (a sum that
+      // starts at +0.0 is never -0.0)
+      const int kme = static_cast<int>(ent.y);
+      int kprev = __shfl_up_sync(FULL, kme, 1);
+      if (lane == 0) kprev = kcur;
+      const unsigned swm = __ballot_sync(FULL, lane < nu && kme != kprev);
+      const unsigned sgm = __ballot_sync(FULL, lane < nu && (sv >> 31) != 0u);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int kk = __shfl_sync(FULL, ku, u);
-        if (u < nu) {
-          const int k = kk >> 1;
-          if (k != kcur) {
-            if (kcur >= 0)
+        if ((swm >> u) & 1u) {
+          const int k = __shfl_sync(FULL, kme, u);
+          if (kcur >= 0)
 #pragma unroll
-              for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
+            for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
 #pragma unroll
-            for (int h = 0; h < NV; ++h) acc[h] = acc_sm[k * 16 * CL + 32 * h + lane];
-            kcur = k;
-          }
-          const double sg = (kk & 1) ? -scale : scale;
+          for (int h = 0; h < NV; ++h) acc[h] = acc_sm[k * 16 * CL + 32 * h + lane];
+          kcur = k;
+        }
+        const double sg = ((sgm >> u) & 1u) ? -scale : scale;
 #pragma unroll
-          for (int h = 0; h < NV; ++h) {
-            acc[h].x = __dadd_rn(acc[h].x, __dmul_rn(sg, v[u][h].x));
-            acc[h].y = __dadd_rn(acc[h].y, __dmul_rn(sg, v[u][h].y));
-          }
+        for (int h = 0; h < NV; ++h) {
+          acc[h].x = __dadd_rn(acc[h].x, __dmul_rn(sg, v[u][h].x));
+          acc[h].y = __dadd_rn(acc[h].y, __dmul_rn(sg, v[u][h].y));
         }
       }
       ent = entn;
