@@ -782,9 +782,10 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
 #undef ITSK_SW
     const SwShape& sh = shapes[tu.swcl == 2 ? 1 : (tu.swcl == 6 ? 2 : (tu.swcl == 7 ? 3 : 0))];
     const int64_t nw = static_cast<int64_t>(nsm) * sh.warps;
-    // auto from 16 GB of [A|b] (C4, 64 GB: 59 vs 72 ms; C3, 4 GB: 5.3 vs
-    // 4.0 ms, where the gather still finds part of A in L2)
-    const bool big = m * ncol * 8 >= (16ll << 30);
+    // auto from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
+    // 32 GB 24.1 / 35.5; 16 GB 12.4 / 17.3; 8 GB 6.1 / 8.3; C3 4 GB 3.7 / 4.1;
+    // C2 0.3 GB 0.50 / 0.27, where the gather finds A in L2)
+    const bool big = m * ncol * 8 >= (2ll << 30);
     if ((tu.sweep > 0 || (tu.sweep < 0 && big)) && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
         rg.j1 == 0xffffffffu && !rg.accum && d <= nw * sh.rpw && m < (1ll << 31)) {
       const int cl = sh.cl;

@@ -147,7 +147,7 @@ def test_sketch_kernel_variants_bitwise(pkg, orc, monkeypatch, variant):
                                               (450000, 1000, 12000, 1000, True), (250001, 129, 700, 131, True),
                                               (300000, 256, 3000, 256, False), (90000, 40, 27000, 40, True)])
 def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
-    """The window sweep (automatic from 16 GB of [A|b]: one persistent
+    """The window sweep (automatic from 2 GB of [A|b]: one persistent
     launch, the grid sweeping 20000-row source windows of one 128-column
     panel at a time with a bounded drift, each warp's sketch rows walked as
     one flattened (row, source) list) against the register gather
@@ -172,7 +172,7 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
                                    ("97", "6", "1")):
             if sweep == "97" and (stream == "0" or m > 300000):
                 continue  # thousands of windows: the streamed kernel on the smaller shapes only
-            monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 16 GB threshold
+            monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 2 GB threshold
             monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
             monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
             got = s.apply_dense(a, b)
