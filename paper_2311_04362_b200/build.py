@@ -13,7 +13,6 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libitsk_b200.so")
 SOURCES = ["capi.cu", "pattern.cu", "sketch.cu", "qr.cu", "qr2.cu", "qr_far.cu", "trsv.cu", "pass.cu", "loop.cu", "sparse.cu"]
-HEADERS = ["itsk_common.cuh", "itsk_kernels.cuh", "itsk_dense.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
@@ -35,7 +34,9 @@ def build(verbose: bool = False, jobs: int | None = None, probe: str | None = No
     lib_out = LIB if probe is None else os.path.join(HERE, f"libitsk_b200_{probe}.so")
     extra = [] if probe is None else [f"-DITSK_{probe.upper()}"]
     os.makedirs(objdir, exist_ok=True)
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "itsk_b200.h")]
+    # every header under csrc/ (a header missing from a hand-kept list left stale objects behind)
+    hdrs = sorted(os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h")))
+    hdrs.append(os.path.join(ROOT, "include", "itsk_b200.h"))
     objs, procs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)

@@ -10,8 +10,10 @@
 // waits for y_{b-1}, adds that term to the helper warps' partial sums of the
 // terms j <= b-2, solves the diagonal block (its stored inverse, or a
 // register substitution chain when the block is ill conditioned), and
-// pushes y_b into every CTA's shared memory (remote stores, then a release
-// store of the block's flag).  Helper warps take the terms j <= b-2 of every
+// pushes y_b into every CTA's shared memory: every lane sends its value to
+// each CTA with st.async, which completes 8 bytes of the block's mbarrier
+// there — the waiters' try_wait wakes when all 256 bytes have landed (no
+// release fence behind 32 remote stores, no polled flag).  Helper warps take the terms j <= b-2 of every
 // owned block, j = h, h + NH, ... ascending: the R block is loaded before
 // y_j arrives, so a term is added ~a hundred cycles after its y_j lands.
 // Backward substitution R x = y mirrors it from the last block down.  Every
@@ -37,8 +39,8 @@ __host__ __device__ __forceinline__ int tcl_ko(int64_t n) {
 // dynamic shared memory of the cluster pair (doubles, then words)
 __host__ __device__ __forceinline__ size_t tcl_smem_bytes(int64_t n) {
   const int64_t nb = nblocks32(n), ko = tcl_ko(n), nh = 16 - ko;
-  const int64_t dbl = 2 * nb * 32 + nh * ko * 32 * 2 + ko * 32 * TCL_DS;
-  const int64_t words = 2 * nb + 2 * ko + ko;
+  const int64_t dbl = 2 * nb * 32 + nh * ko * 32 * 2 + ko * 32 * TCL_DS + 2 * nb /* mbarriers */;
+  const int64_t words = 2 * ko + ko;
   return static_cast<size_t>(dbl * 8 + words * 4 + 64);
 }
 
@@ -47,19 +49,11 @@ __device__ __forceinline__ uint32_t tcl_mapa(uint32_t a, int rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void tcl_st_remote(uint32_t a, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __forceinline__ void tcl_release_flag(uint32_t a, unsigned v) {
-  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned tcl_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void tcl_wait_flag(const unsigned* p) {
-  while (tcl_acquire(p) == 0u) __nanosleep(20);
+// 8 bytes into a CTA of the cluster, counted on that CTA's mbarrier when they land
+__device__ __forceinline__ void tcl_st_async(uint32_t a, double v, uint32_t bar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(a),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
 }
 __device__ __forceinline__ void tcl_wait_count(const unsigned* p, unsigned target) {
   while (*reinterpret_cast<const volatile unsigned*>(p) < target) __nanosleep(20);
@@ -71,8 +65,8 @@ struct TclShared {
   double* xv;       // n: x of every block
   double* acc;      // NH x KO x 2 x 32: helper partials (forward, backward)
   double* dinv;     // KO x 32 x TCL_DS: the owned blocks' diagonal inverses (dense)
-  unsigned* rdyF;   // nb: y_b landed here
-  unsigned* rdyB;   // nb: x_b landed here
+  uint64_t* rdyF;   // nb mbarriers: y_b landed here (256 bytes each, phase 0)
+  uint64_t* rdyB;   // nb mbarriers: x_b landed here
   unsigned* cntF;   // KO: helper terms added (forward)
   unsigned* cntB;   // KO: helper terms added (backward)
   int* dok;         // KO: the stored inverse is usable
@@ -86,10 +80,10 @@ __device__ __forceinline__ TclShared tcl_carve(void* base, int64_t n) {
   s.xv = s.yv + nb * 32;
   s.acc = s.xv + nb * 32;
   s.dinv = s.acc + nh * ko * 64;
-  unsigned* w = reinterpret_cast<unsigned*>(s.dinv + ko * 32 * TCL_DS);
-  s.rdyF = w;
+  s.rdyF = reinterpret_cast<uint64_t*>(s.dinv + ko * 32 * TCL_DS);
   s.rdyB = s.rdyF + nb;
-  s.cntF = s.rdyB + nb;
+  unsigned* w = reinterpret_cast<unsigned*>(s.rdyB + nb);
+  s.cntF = w;
   s.cntB = s.cntF + ko;
   s.dok = reinterpret_cast<int*>(s.cntB + ko);
   return s;
@@ -110,8 +104,13 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
   TclShared S = tcl_carve(smem, n);
   // ---- setup: flags / counters zero, the owned diagonal inverses staged ----
   for (int i = tid; i < nb; i += blockDim.x) {
-    S.rdyF[i] = 0u;
-    S.rdyB[i] = 0u;
+    // one arrival (this thread's, with the 256 bytes every block publishes:
+    // lanes past a short last block send zeros) arms phase 0 of each barrier
+    mbar_init(&S.rdyF[i], 1);
+    mbar_init(&S.rdyB[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&S.rdyF[i], 256);
+    mbar_expect_tx(&S.rdyB[i], 256);
   }
   if (tid < ko) {
     S.cntF[tid] = 0u;
@@ -137,21 +136,16 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
       }
     }
   }
-  cl.sync();  // every CTA's flags zero before any remote store
+  cl.sync();  // every CTA's barriers armed before any remote store
   const uint32_t yv_a = smem_u32(S.yv), xv_a = smem_u32(S.xv);
   const uint32_t rf_a = smem_u32(S.rdyF), rb_a = smem_u32(S.rdyB);
 
-  // publish the 32 values of block b (val in lane i) into every CTA's vec,
-  // then its flag: lane r < NC writes CTA r (data and flag from one thread,
-  // ordered by the release)
-  auto publish = [&](int b, double val, uint32_t vec_a, uint32_t flag_a) {
-    const uint32_t vbase = tcl_mapa(vec_a + static_cast<uint32_t>(32 * b) * 8u, lane < TCL_NC ? lane : 0);
+  // publish the 32 values of block b (val in lane i) into every CTA's vec:
+  // lane i sends its value to each CTA and counts it on that CTA's barrier b
+  auto publish = [&](int b, double val, uint32_t vec_a, uint32_t bar_a) {
+    const uint32_t va = vec_a + static_cast<uint32_t>(32 * b + lane) * 8u, ba = bar_a + 8u * b;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const double v = __shfl_sync(FULL, val, k);
-      if (lane < TCL_NC) tcl_st_remote(vbase + 8u * k, v);
-    }
-    if (lane < TCL_NC) tcl_release_flag(tcl_mapa(flag_a + 4u * b, lane), 1u);
+    for (int r = 0; r < TCL_NC; ++r) tcl_st_async(tcl_mapa(va, r), val, tcl_mapa(ba, r));
   };
 
   // ================= forward: R^T y = c =================
@@ -172,7 +166,7 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
       double s = 0.0;
       for (int h = 0; h < nh; ++h) s += S.acc[(h * ko + k) * 64 + lane];
       if (b >= 1) {
-        tcl_wait_flag(&S.rdyF[b - 1]);
+        mbar_wait(&S.rdyF[b - 1], 0);
         const double* yp = S.yv + b0 - 32;
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -223,7 +217,7 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
         double rv[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) rv[t] = R[static_cast<int64_t>(32 * j + t) * n + col];
-        tcl_wait_flag(&S.rdyF[j]);
+        mbar_wait(&S.rdyF[j], 0);
         const double* yp = S.yv + 32 * j;
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -252,13 +246,14 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
       const int nb1 = b + 1 < nb ? min(32, n - b0 - 32) : 0;
 #pragma unroll
       for (int t = 0; t < 32; ++t) rb[t] = t < nb1 ? R[static_cast<int64_t>(row) * n + b0 + 32 + t] : 0.0;
+      mbar_wait(&S.rdyF[b], 0);  // this CTA's own copy of y_b (sent like the others)
       const double yb = S.yv[row];
       const int after = nb - 2 - b;  // helper terms j >= b+2
       if (after > 0) tcl_wait_count(&S.cntB[k], static_cast<unsigned>(after));
       double s = 0.0;
       for (int hh = 0; hh < nh; ++hh) s += S.acc[(hh * ko + k) * 64 + 32 + lane];
       if (nb1 > 0) {
-        tcl_wait_flag(&S.rdyB[b + 1]);
+        mbar_wait(&S.rdyB[b + 1], 0);
         const double* xp = S.xv + b0 + 32;
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -310,7 +305,7 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
         double rv[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) rv[t] = t < js ? R[static_cast<int64_t>(row) * n + 32 * j + t] : 0.0;
-        tcl_wait_flag(&S.rdyB[j]);
+        mbar_wait(&S.rdyB[j], 0);
         const double* xp = S.xv + 32 * j;
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -326,7 +321,10 @@ __device__ void trsv_pair_cluster(const double* __restrict__ R, const double* __
       }
     }
   }
-  cl.sync();  // no CTA exits while another may still store into its shared memory
+  // every block's values have landed here (asynchronous stores complete only
+  // on the barriers), then: no CTA exits while another may still store into it
+  for (int i = tid; i < 2 * nb; i += blockDim.x) mbar_wait(&S.rdyF[i], 0);  // rdyB follows rdyF
+  cl.sync();
 }
 
 }  // namespace itsk
