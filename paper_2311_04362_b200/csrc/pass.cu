@@ -519,13 +519,14 @@ __global__ void __launch_bounds__(32 * NCW, 1) k_pass_tma(PassArgs a, TmaShape s
 // ---------------------------------------------------------------------------
 constexpr int RW_NCW = 16, RW_RB = 4;
 
-template <int GW, int CPP>
+template <int GW, int CPP, bool ODD>
 __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaShape sh) {
   constexpr int NG = RW_NCW / GW, GT = 32 * GW, RB = RW_RB;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   unsigned char* stages = smraw + 1024;
   __shared__ double dpart[NG][2][GW][RB];
+  __shared__ __align__(16) double rsm[NG][2][RB];  // the batch's residuals, from the group's first warp
   __shared__ double ssm[NG][4];
   __shared__ int s_done;
 
@@ -627,11 +628,14 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
     constexpr int RPL = RB / VPL;              // row slots across the lanes
     // column validity is loop-invariant: masks computed once
     bool cok[CPP], cpad[CPP];
+    int off[CPP];  // byte offset of the pair in a staged row (the first pair's when past n)
 #pragma unroll
     for (int j = 0; j < CPP; ++j) {
       cok[j] = col[j] < n;
       cpad[j] = col[j] + 1 >= n;
+      off[j] = 8 * (cok[j] ? col[j] : col[0]);
     }
+    const int row_bytes = static_cast<int>(lda) * 8;
     // stage index and mbarrier phase advance by NG per batch (S is a multiple
     // of NG): no integer division in the loop
     int st = g;
@@ -643,17 +647,33 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
       mbar_wait(full + st, ph);
       const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(st) * sh.stage_bytes);
       double2 v[RB][CPP];
+      if (nu == RB) {
+        // a full batch: unconditional loads at per-thread byte offsets (a pair
+        // past n re-reads the thread's first pair: its x is 0 and its c is
+        // never written); only an odd n needs its pad column zeroed
 #pragma unroll
-      for (int u = 0; u < RB; ++u)
+        for (int u = 0; u < RB; ++u) {
+          const unsigned char* rp = reinterpret_cast<const unsigned char*>(base) + u * row_bytes;
 #pragma unroll
-        for (int j = 0; j < CPP; ++j) {
-          double2 w = make_double2(0.0, 0.0);
-          if (cok[j] && u < nu) {
-            w = *reinterpret_cast<const double2*>(base + u * lda + col[j]);
-            if (cpad[j]) w.y = 0.0;  // the pad column of an odd n
+          for (int j = 0; j < CPP; ++j) {
+            double2 w = *reinterpret_cast<const double2*>(rp + off[j]);
+            if (ODD && cpad[j]) w.y = 0.0;
+            v[u][j] = w;
           }
-          v[u][j] = w;
         }
+      } else {
+#pragma unroll
+        for (int u = 0; u < RB; ++u)
+#pragma unroll
+          for (int j = 0; j < CPP; ++j) {
+            double2 w = make_double2(0.0, 0.0);
+            if (cok[j] && u < nu) {
+              w = *reinterpret_cast<const double2*>(base + u * lda + col[j]);
+              if (cpad[j]) w.y = 0.0;  // the pad column of an odd n
+            }
+            v[u][j] = w;
+          }
+      }
       double d[RB];
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
@@ -680,8 +700,12 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
         if ((lane & 7) == 0) dpart[g][par][gw][lane >> 3] = kk;
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(GT) : "memory");
-      // every warp of the group has its values of stage st: refill it
-      if (gw == 0 && lane == 0 && t + S < ntiles) {
+      // every warp of the group has its values of stage st: refill it.  By
+      // the group's LAST warp: issued from lane 0 of the first warp, the
+      // compiler merged this thread test with the first warp's branch below
+      // and left lane 0 unreconverged, so every shuffle of the tree ran twice
+      // on its divergent path (34 ms per C4 pass instead of 9)
+      if (gw == GW - 1 && lane == 0 && t + S < ntiles) {
         const int tn = t + S;
         const int rows = min(RB, nrows - tn * RB);
         const unsigned bytes = static_cast<unsigned>(rows * lda * 8);
@@ -689,23 +713,45 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
         bulk_g2s(stages + static_cast<int64_t>(st) * sh.stage_bytes, a.A + (r_begin + tn * RB) * lda, bytes,
                  full + st, pol);
       }
-      // the group's GW partials per row, summed in a fixed tree (the same
-      // bits in every warp of the group)
-      double q[VPL];
-      {
-        const int w = lane % GW, r0 = ((lane / GW) % RPL) * VPL;
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) q[i] = dpart[g][par][w][r0 + i];
-      }
-#pragma unroll
-      for (int o = GW / 2; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) q[i] += __shfl_xor_sync(FULL, q[i], o);
+      // the group's GW partials per row, summed in a fixed tree by the
+      // group's first warp, which hands r = b - dot of the 4 rows to the other
+      // warps through shared memory (they wait on a second named barrier it
+      // only arrives at; sixteen redundant copies of the tree were 2 of the
+      // pass's ~19 instructions per element)
       double rv[RB];
+      if (gw == 0) {
+        double q[VPL];
+        {
+          const int w = lane % GW, r0 = ((lane / GW) % RPL) * VPL;
 #pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        const double dot = __shfl_sync(FULL, q[u % VPL], (u / VPL) * GW);
-        rv[u] = u < nu ? bscale * __shfl_sync(FULL, cb, u) - dot : 0.0;
+          for (int i = 0; i < VPL; ++i) q[i] = dpart[g][par][w][r0 + i];
+        }
+#pragma unroll
+        for (int o = GW / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) q[i] += __shfl_xor_sync(FULL, q[i], o);
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+          const double dot = __shfl_sync(FULL, q[u % VPL], (u / VPL) * GW);
+          rv[u] = u < nu ? bscale * __shfl_sync(FULL, cb, u) - dot : 0.0;
+        }
+        if constexpr (GW > 1) {
+          if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < RB; u += 2)
+              *reinterpret_cast<double2*>(&rsm[g][par][u]) = make_double2(rv[u], rv[u + 1]);
+          }
+          __syncwarp();
+          asm volatile("bar.arrive %0, %1;" ::"r"(1 + NG + g), "r"(GT) : "memory");
+        }
+      } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + NG + g), "r"(GT) : "memory");
+#pragma unroll
+        for (int u = 0; u < RB; u += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(&rsm[g][par][u]);
+          rv[u] = t2.x;
+          rv[u + 1] = t2.y;
+        }
       }
 #pragma unroll
       for (int u = 0; u < RB; ++u)
@@ -922,8 +968,8 @@ int launch_tma_u(const PassArgs& a0, int grid, cudaStream_t s) {
 }
 
 
-template <int GW, int CPP>
-int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
+template <int GW, int CPP, bool ODD>
+int launch_rows_p(const PassArgs& a0, int grid, cudaStream_t s) {
   constexpr int NG = RW_NCW / GW;
   PassArgs a = a0;
   TmaShape sh;
@@ -937,12 +983,17 @@ int launch_rows(const PassArgs& a0, int grid, cudaStream_t s) {
   sh.S = std::max(NG, S);
   a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
   const size_t smem = 1024 + static_cast<size_t>(sh.S) * sh.stage_bytes;
-  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rows<GW, CPP>)));
-  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rows<GW, CPP>), dim3(grid), dim3(32 * RW_NCW),
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_rows<GW, CPP, ODD>)));
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_rows<GW, CPP, ODD>), dim3(grid), dim3(32 * RW_NCW),
                        smem, s, a, sh));
   count_launch();
   ITSK_CHECK_LAUNCH();
   return ITSK_OK;
+}
+
+template <int GW, int CPP>
+int launch_rows(const PassArgs& a, int grid, cudaStream_t s) {
+  return (a.n & 1) ? launch_rows_p<GW, CPP, true>(a, grid, s) : launch_rows_p<GW, CPP, false>(a, grid, s);
 }
 
 template <int CPL>
