@@ -620,8 +620,8 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
       ft = (ok && gw == 0 && r_true) ? r_true[gi] : 0.0;
     };
     double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
-    double cb, cp, ct;
-    fetch(g, cb, cp, ct);
+    double cb = 0.0, cp = 0.0, ct = 0.0;  // used by the group's first warp only (it forms r)
+    if (gw == 0) fetch(g, cb, cp, ct);
     // second-stage lane map: value i of lane l is warp (l % GW)'s partial of
     // row ((l / GW) % (RB / VPL)) * VPL + i
     constexpr int VPL = (GW * RB + 31) / 32;  // partials per lane
@@ -636,13 +636,21 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
       off[j] = 8 * (cok[j] ? col[j] : col[0]);
     }
     const int row_bytes = static_cast<int>(lda) * 8;
+    uint32_t doff[CPP];
+#pragma unroll
+    for (int j = 0; j < CPP; ++j) doff[j] = static_cast<uint32_t>(off[j] - off[0]);
+    // shared address of the thread's first pair in the group's current stage
+    const uint32_t sa_stride = static_cast<uint32_t>(NG) * static_cast<uint32_t>(sh.stage_bytes);
+    const uint32_t sa_wrap = static_cast<uint32_t>(S) * static_cast<uint32_t>(sh.stage_bytes);
+    uint32_t sa = smem_u32(stages) + static_cast<uint32_t>(g) * static_cast<uint32_t>(sh.stage_bytes) +
+                  static_cast<uint32_t>(off[0]);
     // stage index and mbarrier phase advance by NG per batch (S is a multiple
     // of NG): no integer division in the loop
     int st = g;
     unsigned ph = 0;
     for (int t = g, par = 0; t < ntiles; t += NG, par ^= 1) {
-      double nb, np, nt;
-      fetch(t + NG, nb, np, nt);
+      double nb = 0.0, np = 0.0, nt = 0.0;
+      if (gw == 0) fetch(t + NG, nb, np, nt);
       const int nu = min(RB, nrows - t * RB);
       mbar_wait(full + st, ph);
       const double* base = reinterpret_cast<const double*>(stages + static_cast<int64_t>(st) * sh.stage_bytes);
@@ -651,12 +659,15 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
         // a full batch: unconditional loads at per-thread byte offsets (a pair
         // past n re-reads the thread's first pair: its x is 0 and its c is
         // never written); only an odd n needs its pad column zeroed
+        // 32-bit shared addresses: the thread's first pair in this stage (sa)
+        // + row + pair offset — 7 adds per batch
 #pragma unroll
         for (int u = 0; u < RB; ++u) {
-          const unsigned char* rp = reinterpret_cast<const unsigned char*>(base) + u * row_bytes;
+          const uint32_t ra = sa + static_cast<uint32_t>(u) * static_cast<uint32_t>(row_bytes);
 #pragma unroll
           for (int j = 0; j < CPP; ++j) {
-            double2 w = *reinterpret_cast<const double2*>(rp + off[j]);
+            double2 w;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "r"(ra + doff[j]));
             if (ODD && cpad[j]) w.y = 0.0;
             v[u][j] = w;
           }
@@ -775,8 +786,10 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
       }
       cb = nb; cp = np; ct = nt;
       st += NG;
+      sa += sa_stride;
       if (st >= S) {
         st -= S;
+        sa -= sa_wrap;
         ph ^= 1u;
       }
     }
