@@ -107,231 +107,26 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
 // Window sweep for a large A (the gather above re-reads A zeta times from
 // HBM: at C4 504 GB of DRAM reads for 64 GB of A, L2 hit rate 2%,
 // profiles/rd2_sketch_window_deadend.txt).  One persistent launch, one CTA
-// per SM: a warp owns up to SW_RPW sketch rows (i = warp, warp + NW, ...),
-// and the grid sweeps the source rows in windows of R rows, 64 columns (a
-// panel) at a time: every warp adds the sources of its rows that fall in the
-// current window, in ascending order, then counts itself done with the
-// window.  A warp may start window g only when every warp has finished
-// window g - SW_DRIFT (a per-window arrival counter; it orders nothing, A is
-// read-only — it only bounds the L2 working set), so all zeta readers of a
-// source row find its 512-byte panel segment in L2 and A is read from HBM
-// about once.
-// The window's (row, source) pairs of a warp are walked as ONE flattened list
-// in chunks of SW_U sources (one 16-byte load per lane each, SW_U in flight,
-// the next chunk's source words loaded under them), so the latency paid per
-// window is ~(pairs / SW_U), not (rows x rounds); each row's running sum
-// lives in shared memory between its window segments.  Every output is the
-// same sum in the same order as k_sketch_gather: bitwise scipy's.
+// per SM: a warp owns up to RPW sketch rows, and the grid sweeps the source
+// rows in windows of R rows, 128 columns (a panel) at a time: every warp
+// adds the sources of its rows that fall in the current window, in ascending
+// order, then counts itself done with the window.  A warp may start window g
+// only when every warp has finished window g - drift (arrival counters; they
+// order nothing, A is read-only — they only bound the L2 working set), so
+// all zeta readers of a source row find its panel segment in L2 and A is
+// read from HBM about once.  Each row's running sum lives in shared memory
+// between its window segments.  Every output is the same sum in the same
+// order as k_sketch_gather: bitwise scipy's.
 // CL adjacent columns per lane (a panel of 32 CL), U sources per chunk,
 // NWARP warps per CTA with RPW sketch rows each
 template <int CL, int NWARP, int RPW>
 constexpr size_t sw_smem_bytes() { return sizeof(double) * NWARP * RPW * 32 * CL; }
 
-template <int CL, int U, int SW_WARPS, int SW_RPW>
-__global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_sweep(
-    const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
-    const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
-    double* __restrict__ W, int64_t ldw, uint32_t m, uint32_t R, int nwin, int npanel, unsigned* wdone,
-    uint32_t* __restrict__ bnd, int flags) {
-  const int vec = flags & 1;
-  const int SW_DRIFT = flags >> 8;  // windows a warp may run ahead of the slowest
-  static_assert(CL == 2 || CL == 4, "columns per lane");
-  constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
-  extern __shared__ __align__(16) double sw_sm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t NW = static_cast<int64_t>(gridDim.x) * SW_WARPS;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * SW_WARPS + warp;
-  const int64_t ncol = n + (b ? 1 : 0);
-  double2* acc_sm = reinterpret_cast<double2*>(sw_sm + static_cast<int64_t>(warp) * SW_RPW * PANEL);
-  // lane k < SW_RPW holds row k = gw + NW * k (an empty range past d)
-  const int64_t myrow = gw + NW * lane;
-  const bool rowok = lane < SW_RPW && myrow < d;
-  const uint32_t r0 = rowok ? ptr[myrow] : 0u, r1 = rowok ? ptr[myrow + 1] : 0u;
-  // prologue: the end of every window's segment of every own row, from one
-  // coalesced pass over the rows' (ascending) sources: positions p-1, p in
-  // windows wp < wc end windows [wp, wc) at p; the row end is a sentinel in
-  // window nwin.
-  uint32_t* wb = bnd + gw * SW_RPW * static_cast<int64_t>(nwin);
-  for (int k = 0; k < SW_RPW; ++k) {
-    const uint32_t a0 = __shfl_sync(FULL, r0, k), a1 = __shfl_sync(FULL, r1, k);
-    int carry = 0;
-    for (uint32_t q = a0; q <= a1; q += 32) {
-      const uint32_t p = q + lane;
-      const int wc = p < a1 ? static_cast<int>((src[p] & 0x7fffffffu) / R) : nwin;
-      int wp = __shfl_up_sync(FULL, wc, 1);
-      if (lane == 0) wp = carry;
-      if (p <= a1)
-        for (int w = wp; w < wc; ++w) wb[k * nwin + w] = p;
-      carry = __shfl_sync(FULL, wc, 31);
-    }
-  }
-  __syncwarp();
-  // Window arrivals are counted per CTA in shared memory; the CTA's last warp
-  // adds one to the window's global counter, and the grid's last CTA writes
-  // the window's epoch (g + 1) into every CTA's own flag line — so a warp
-  // polls a line only its CTA reads (2368 warps polling and incrementing one
-  // counter made a hot spot worth ~7 us per window step).
-  __shared__ unsigned cta_cnt[8];
-  if (threadIdx.x < 8) cta_cnt[threadIdx.x] = 0u;
-  __syncthreads();
-  unsigned* wflag = wdone + static_cast<int64_t>(nwin) * npanel;           // gridDim.x lines of 32 words
-  const volatile unsigned* myflag = wflag + 32 * static_cast<int64_t>(blockIdx.x);
-  for (int p = 0; p < npanel; ++p) {
-    // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
-    // warp is one contiguous 512-byte segment)
-    const int64_t cA = static_cast<int64_t>(p) * PANEL + 2 * lane;
-    const bool allv = __all_sync(FULL, vec && cA + 64 * (NV - 1) + 1 < n);
-    int kind[CL];
-#pragma unroll
-    for (int c = 0; c < CL; ++c) {
-      const int64_t col = cA + 64 * (c >> 1) + (c & 1);
-      kind[c] = col < n ? 0 : (col == n && b ? 1 : 2);
-    }
-    const double* Ap = A + static_cast<int64_t>(p) * PANEL;
-    const double* Ac = Ap + 2 * lane;
-#pragma unroll
-    for (int k = 0; k < SW_RPW; ++k)
-#pragma unroll
-      for (int h = 0; h < NV; ++h) acc_sm[k * 16 * CL + 32 * h + lane] = make_double2(0.0, 0.0);
-    __syncwarp();
-    uint32_t sk = r0;  // lane k: row k's first source in the current window
-    for (int w = 0; w < nwin; ++w) {
-      const int g = p * nwin + w;
-      if (g >= SW_DRIFT) {
-        if (lane == 0) {
-          const unsigned q = static_cast<unsigned>(g - SW_DRIFT);
-          while (myflag[q & 7u] < q + 1u) __nanosleep(32);  // slot values only grow (q + 1, q + 9, ...)
-        }
-        __syncwarp();
-      }
-      const uint32_t tk = lane < SW_RPW ? wb[lane * nwin + w] : 0u;
-      const uint32_t cnt = lane < SW_RPW ? tk - sk : 0u;
-      uint32_t incl = cnt;  // inclusive scan: row k covers flattened positions [incl - cnt, incl)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t total = __shfl_sync(FULL, incl, 31);
-      const uint32_t base = sk - (incl - cnt);  // source index = base_k + position
-      // lane u: position P + u (clamped into the window's list, so every
-      // lane's row pointer is valid; positions past the end are not added):
-      // its row and sign packed in ku, its source row's panel segment in pu
-      auto locate = [&](uint32_t P, int& ku, uint32_t& sv) {
-        const uint32_t pos = min(P + static_cast<uint32_t>(lane & (U - 1)), total - 1);
-        int k = 0;
-#pragma unroll
-        for (int kk = 0; kk < SW_RPW - 1; ++kk) k += pos >= __shfl_sync(FULL, incl, kk) ? 1 : 0;
-        const uint32_t bk = __shfl_sync(FULL, base, k);
-        sv = __ldg(src + bk + pos);
-        ku = k;  // the sign joins it (ku << 1 | sign) once sv has landed
-      };
-      // the source row's panel segment (lane-independent start)
-      auto rowptr = [&](uint32_t w) { return Ap + static_cast<int64_t>(w & 0x7fffffffu) * lda; };
-      int ku = 0, kcur = -1;
-      uint32_t sv = 0;
-      const double* pu = Ap;
-      double2 acc[NV];
-      if (total > 0) {
-        locate(0, ku, sv);
-        ku = (ku << 1) | static_cast<int>(sv >> 31);
-        pu = rowptr(sv);
-      }
-      for (uint32_t P = 0; P < total; P += U) {
-        int kn = 0;
-        uint32_t svn = 0;
-        // the next chunk's source words are in flight under this chunk's
-        // loads and adds: nothing below depends on svn before the chunk ends
-        if (P + U < total) locate(P + U, kn, svn);
-        const int nu = static_cast<int>(min(total - P, static_cast<uint32_t>(U)));
-        double2 v[U][NV];
-        if (allv) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const double2* q = reinterpret_cast<const double2*>(
-                                   __shfl_sync(FULL, reinterpret_cast<uintptr_t>(pu), u)) + lane;
-#pragma unroll
-            for (int h = 0; h < NV; ++h) v[u][h] = __ldg(q + 32 * h);
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int64_t j = __shfl_sync(FULL, sv, u) & 0x7fffffffu;
-            const double* arow = Ac + j * lda;
-#pragma unroll
-            for (int h = 0; h < NV; ++h) {
-              const int c0 = 2 * h, c1 = 2 * h + 1;
-              v[u][h].x = kind[c0] == 0 ? arow[64 * h] : (kind[c0] == 1 ? b[j] : 0.0);
-              v[u][h].y = kind[c1] == 0 ? arow[64 * h + 1] : (kind[c1] == 1 ? b[j] : 0.0);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int kk = __shfl_sync(FULL, ku, u);
-          if (u < nu) {
-            const int k = kk >> 1;
-            if (k != kcur) {
-              if (kcur >= 0)
-#pragma unroll
-                for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
-#pragma unroll
-              for (int h = 0; h < NV; ++h) acc[h] = acc_sm[k * 16 * CL + 32 * h + lane];
-              kcur = k;
-            }
-            const double sg = (kk & 1) ? -scale : scale;
-#pragma unroll
-            for (int h = 0; h < NV; ++h) {
-              acc[h].x = __dadd_rn(acc[h].x, __dmul_rn(sg, v[u][h].x));
-              acc[h].y = __dadd_rn(acc[h].y, __dmul_rn(sg, v[u][h].y));
-            }
-          }
-        }
-        sv = svn;
-        ku = (kn << 1) | static_cast<int>(svn >> 31);
-        pu = rowptr(svn);
-      }
-      if (kcur >= 0)
-#pragma unroll
-        for (int h = 0; h < NV; ++h) acc_sm[kcur * 16 * CL + 32 * h + lane] = acc[h];
-      sk = tk;
-      __syncwarp();
-      int bcast = 0;
-      if (lane == 0) {
-        if (atomicAdd(&cta_cnt[g & 7], 1u) == SW_WARPS - 1) {
-          // every warp of the CTA has arrived: the slot is next used 8 windows
-          // on, which no warp reaches before window g + 8 - drift > g is
-          // complete everywhere (drift < 8)
-          cta_cnt[g & 7] = 0u;
-          __threadfence_block();
-          bcast = atomicAdd(wdone + g, 1u) == gridDim.x - 1 ? 1 : 0;
-        }
-      }
-      if (__shfl_sync(FULL, bcast, 0))
-        for (unsigned c = lane; c < gridDim.x; c += 32)
-          *reinterpret_cast<volatile unsigned*>(wflag + 32 * static_cast<int64_t>(c) + (g & 7)) =
-              static_cast<unsigned>(g) + 1u;
-    }
-#pragma unroll
-    for (int k = 0; k < SW_RPW; ++k) {
-      const int64_t i = gw + NW * k;
-      if (i >= d) continue;
-#pragma unroll
-      for (int h = 0; h < NV; ++h) {
-        const double2 a = acc_sm[k * 16 * CL + 32 * h + lane];
-        if (cA + 64 * h < ncol) W[i * ldw + cA + 64 * h] = a.x;
-        if (cA + 64 * h + 1 < ncol) W[i * ldw + cA + 64 * h + 1] = a.y;
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// Streamed window sweep: the same schedule with no per-window pipeline
-// drain.  k_sketch_sweep pays, per (panel, window) step and warp, a boundary
-// load, a scan, a dependent source-word load and a partly filled last chunk
-// (~2.4 us of the ~17 us a 20000-row window step takes at C4).  Here the
-// prologue writes each warp's (row, source) pairs ONCE in processing order
+// The stream: walking the windows one by one costs, per (panel, window) step
+// and warp, a boundary load, a scan, a dependent source-word load and a
+// partly filled last chunk (~2.4 us of the ~17 us a 20000-row window step
+// takes at C4; that version ran 53-59 ms, profiles/rd2_sketch_sweep.txt).
+// Here the prologue writes each warp's (row, source) pairs ONCE in processing order
 // (window-major, rows ascending inside a window, sources ascending inside a
 // row) as 8-byte entries {source word, local row}; a panel is then one
 // uninterrupted stream of U-entry chunks: the entries of the next chunk are
@@ -694,14 +489,12 @@ struct SketchTune {
   int ring = -1;      // 1: cp.async ring variant, 0: register gather, -1: by shape
   int gcpl = 0;       // register gather: cap on columns-per-lane (more column blocks)
   int unr = 0;        // register gather: sources per unrolled group (0 = heuristic)
-  int swcl = 0;      // window sweep columns per lane (2 or 4; A/B, same bits)
-  int stream = 1;     // window sweep: entries materialised in processing order (0: per-window walk; same bits)
+  int swcl = 0;      // window sweep columns per lane (2: 64-column panels, else 128; same bits)
   int drift = 2;      // window sweep: windows a warp may run ahead (L2 working set; same bits)
   int sweep = -1;     // window sweep: -1 auto (large A), 0 off, 1 on, > 1 on with that many window rows (same bits)
   SketchTune() {
     if (const char* e = getenv("ITSK_SKETCH_SWEEP")) sweep = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_SWCL")) swcl = atoi(e);
-    if (const char* e = getenv("ITSK_SKETCH_STREAM")) stream = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_DRIFT")) drift = std::min(7, std::max(1, atoi(e)));
     if (const char* e = getenv("ITSK_SKETCH_RING")) ring = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
@@ -773,14 +566,12 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
     const int nsm = num_sms();
     // kernel shapes (all the same bits): columns per lane, sources per chunk,
     // warps per CTA, sketch rows per warp
-    struct SwShape { const void* fn; const void* fn_stream; int cl, warps, rpw; size_t smem; };
-#define ITSK_SW(CLV, UV, WV, RV)                                          \
-  {reinterpret_cast<const void*>(k_sketch_sweep<CLV, UV, WV, RV>),        \
-   reinterpret_cast<const void*>(k_sketch_stream<CLV, UV, WV, RV>), CLV, WV, RV, sw_smem_bytes<CLV, WV, RV>()}
-    static const SwShape shapes[] = {ITSK_SW(4, 8, 16, 12), ITSK_SW(2, 16, 16, 12), ITSK_SW(4, 4, 24, 8),
-                                     ITSK_SW(4, 16, 8, 24)};
-#undef ITSK_SW
-    const SwShape& sh = shapes[tu.swcl == 2 ? 1 : (tu.swcl == 6 ? 2 : (tu.swcl == 7 ? 3 : 0))];
+    struct SwShape { const void* fn; int cl, warps, rpw; size_t smem; };
+    // 128-column panels; the 64-column shape is kept for the tests (same bits)
+    static const SwShape shapes[] = {
+        {reinterpret_cast<const void*>(k_sketch_stream<4, 8, 16, 12>), 4, 16, 12, sw_smem_bytes<4, 16, 12>()},
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()}};
+    const SwShape& sh = shapes[tu.swcl == 2 ? 1 : 0];
     const int64_t nw = static_cast<int64_t>(nsm) * sh.warps;
     // auto from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
     // 32 GB 24.1 / 35.5; 16 GB 12.4 / 17.3; 8 GB 6.1 / 8.3; C3 4 GB 3.7 / 4.1;
@@ -791,8 +582,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
       const int cl = sh.cl;
       const uint32_t R = tu.sweep > 1 ? static_cast<uint32_t>(tu.sweep) : (cl == 2 ? 40000u : 20000u);
       const double inv_r = 1.0 / static_cast<double>(R);
-      const int nwin = tu.stream ? static_cast<int>(sw_win(static_cast<uint32_t>(m - 1), inv_r)) + 1
-                                 : static_cast<int>((m + R - 1) / R);
+      const int nwin = static_cast<int>(sw_win(static_cast<uint32_t>(m - 1), inv_r)) + 1;
       const int npanel = static_cast<int>((ncol + 32 * cl - 1) / (32 * cl));
       unsigned* wdone = nullptr;
       uint32_t* bnd = nullptr;
@@ -800,28 +590,33 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
       const size_t cbytes = sizeof(unsigned) * (static_cast<size_t>(nwin) * npanel + 32 * static_cast<size_t>(nsm));
       const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * sh.rpw * nwin;
       ITSK_CUDA(keep_async_pool());
-      ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wdone), cbytes, s));
-      ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bnd), bbytes, s));
-      ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
-      uint2* ord = nullptr;  // the streamed sweep's entries in processing order
-      if (tu.stream) ITSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ord), sizeof(uint2) * static_cast<size_t>(m) * zeta, s));
-      int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8);
-      const void* fn = tu.stream ? sh.fn_stream : sh.fn;
-      const size_t smem = sh.smem;
-      ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      const uint32_t mm = static_cast<uint32_t>(m);
-      void* args[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
-                      const_cast<uint32_t*>(&mm), const_cast<uint32_t*>(&R), const_cast<int*>(&nwin),
-                      const_cast<int*>(&npanel), &wdone, &bnd, &flags};
-      void* args_st[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
-                         const_cast<double*>(&inv_r), const_cast<int*>(&nwin), const_cast<int*>(&npanel),
-                         &wdone, &bnd, &ord, &flags};
-      ITSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(32 * sh.warps), tu.stream ? args_st : args, smem, s));
-      if (ord) ITSK_CUDA(cudaFreeAsync(ord, s));
-      count_launch();
-      ITSK_CUDA(cudaFreeAsync(bnd, s));
-      ITSK_CUDA(cudaFreeAsync(wdone, s));
-      return ITSK_OK;
+      // one scratch block: counters and flag lines | window boundaries | the
+      // entries in processing order (8 m zeta bytes: 256 MB at C4).  Without
+      // room for it the gather below does the job (same bits).
+      const size_t obytes = sizeof(uint2) * static_cast<size_t>(m) * zeta;
+      const size_t c_al = (cbytes + 255) / 256 * 256, b_al = (bbytes + 255) / 256 * 256;
+      unsigned char* scratch = nullptr;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), c_al + b_al + obytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        scratch = nullptr;
+      }
+      if (scratch) {
+        wdone = reinterpret_cast<unsigned*>(scratch);
+        bnd = reinterpret_cast<uint32_t*>(scratch + c_al);
+        uint2* ord = reinterpret_cast<uint2*>(scratch + c_al + b_al);
+        ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
+        int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8);
+        const void* fn = sh.fn;
+        const size_t smem = sh.smem;
+        ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        void* args[] = {&A, &lda, &n, &b, &sk_ptr, &sk_src, &d, const_cast<double*>(&scale), &SAb, &ldw,
+                        const_cast<double*>(&inv_r), const_cast<int*>(&nwin), const_cast<int*>(&npanel),
+                        &wdone, &bnd, &ord, &flags};
+        ITSK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(32 * sh.warps), args, smem, s));
+        count_launch();
+        ITSK_CUDA(cudaFreeAsync(scratch, s));
+        return ITSK_OK;
+      }
     }
   }
   int64_t need = (ncol + 31) / 32;

@@ -149,8 +149,8 @@ def test_sketch_kernel_variants_bitwise(pkg, orc, monkeypatch, variant):
 def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     """The window sweep (automatic from 2 GB of [A|b]: one persistent
     launch, the grid sweeping 20000-row source windows of one 128-column
-    panel at a time with a bounded drift, each warp's sketch rows walked as
-    one flattened (row, source) list) against the register gather
+    panel at a time with a bounded drift, each warp's (row, source) pairs
+    materialised once in processing order and streamed) against the register gather
     (ITSK_SKETCH_SWEEP=0, itself bitwise scipy's order in the tests above):
     bitwise equal, including the fused b column, for both lane widths; odd
     leading dimension (the unvectorised loads), no b, a ragged last window,
@@ -163,20 +163,18 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     s = pkg.sparse_sign_new(d, m, 8, 5)
     monkeypatch.setenv("ITSK_SKETCH_SWEEP", "0")
     ref = s.apply_dense(a, b)
-    # the streamed sweep (entries materialised in processing order) and the
-    # per-window walk; window rows: default, small (many windows per chunk: a
-    # chunk spanning more than `drift` windows must not wait for itself)
-    for stream in ("1", "0"):
-        monkeypatch.setenv("ITSK_SKETCH_STREAM", stream)
-        for sweep, swcl, drift in (("1", "0", "2"), ("1", "2", "2"), ("7000", "0", "3"), ("7000", "7", "1"),
-                                   ("97", "6", "1")):
-            if sweep == "97" and (stream == "0" or m > 300000):
-                continue  # thousands of windows: the streamed kernel on the smaller shapes only
-            monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 2 GB threshold
-            monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
-            monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
-            got = s.apply_dense(a, b)
-            assert torch.equal(got, ref), (stream, sweep, swcl, drift)
+    # window rows: default, small (many windows per chunk: a chunk spanning
+    # more than `drift` windows must not wait for itself; warps without rows
+    # must not run a counter ring ahead), 128- and 64-column panels
+    for sweep, swcl, drift in (("1", "0", "2"), ("1", "2", "2"), ("7000", "0", "3"), ("7000", "2", "1"),
+                               ("97", "0", "1")):
+        if sweep == "97" and m > 300000:
+            continue  # thousands of windows: on the smaller shapes only
+        monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 2 GB threshold
+        monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
+        monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
+        got = s.apply_dense(a, b)
+        assert torch.equal(got, ref), (sweep, swcl, drift)
 
 
 def test_pattern_argument_errors(pkg):
