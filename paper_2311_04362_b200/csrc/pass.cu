@@ -844,6 +844,246 @@ __global__ void __launch_bounds__(32 * RW_NCW, 1) k_pass_rows(PassArgs a, TmaSha
   if (a.tickets) group_reduce(a, n);
 }
 
+// ---------------------------------------------------------------------------
+// Row slots (1408 < n <= 2048; the C4 shape).  The pass is HBM-bound, but the
+// whole solve runs under the board's power cap and its time follows the SM
+// clock: instructions per byte are what is left to save.  The row-group
+// kernel above spends ~11.6 thread instructions per element at GW = 16
+// (every thread holds 4 columns of 4 rows: 4 partial dots per thread to
+// reduce-scatter, per-batch address arithmetic).  Here the 512 threads form 4
+// slots of 128: a slot owns ONE row of the 4-row batch, a thread 8 column
+// pairs {t + 128 k} of it — one partial dot per thread, a plain butterfly,
+// 16-byte loads at immediate offsets from one address.  Rows are staged at a
+// fixed 16 KB stride (one bulk copy per row, only the n columns: a wider lda
+// costs no bandwidth); the ring is zeroed once, so the columns past n read
+// zeros (their x is 0 and their c is never written).  Per batch: dot
+// butterfly -> 16 warp partials -> barrier -> warp 0's lane u sums row u's 4
+// partials in a fixed order, forms r = b - dot and hands it over through
+// shared memory (a second barrier it only arrives at) -> c += r * row in the
+// slot's registers.  The 4 slots' c partials are summed in slot order at the
+// end.  10.5 thread instructions per element executed (ncu), 3 % faster than
+// the row groups over sustained C4 passes (scripts/pass_sustained_ab.py).
+// ---------------------------------------------------------------------------
+constexpr int SL_T = 512, SL_RB = 4, SL_KP = 8, SL_ROW = 2048;  // threads, rows per batch, pairs per thread, staged row (doubles)
+constexpr int SL_STAGE = SL_RB * SL_ROW * 8;                    // bytes per stage
+
+template <bool ODD>
+__global__ void __launch_bounds__(SL_T, 1) k_pass_slots(PassArgs a, TmaShape sh) {
+  constexpr int RB = SL_RB, KP = SL_KP;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  unsigned char* stages = smraw + 1024;
+  __shared__ __align__(16) double dpart[2][16];  // [batch parity][warp]: warp w holds row w / 4
+  __shared__ __align__(16) double rsm[2][RB];    // the batch's residuals
+  __shared__ double ssm[4];
+  __shared__ int s_done;
+
+  const double* r_true = a.r_true;
+  const double* b = a.b;
+  const double bscale = a.bscale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = tid >> 7, ts = tid & 127;
+  const int64_t n = a.n, lda = a.lda;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const int nrows = r_end > r_begin ? static_cast<int>(r_end - r_begin) : 0;
+  const int S = sh.S;
+  const int ntiles = (nrows + RB - 1) / RB;
+  const int npre = min(S, ntiles);
+
+  // zero the ring (generic proxy) before the copies (async proxy) land in it
+  {
+    double2* z = reinterpret_cast<double2*>(stages);
+    const int nz = S * (SL_STAGE / 16);
+    for (int i = tid; i < nz; i += SL_T) z[i] = make_double2(0.0, 0.0);
+  }
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(full + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  pdl_trigger();
+  const uint64_t pol = evict_first_policy();
+  const unsigned rowbytes = static_cast<unsigned>(((n + 1) & ~static_cast<int64_t>(1)) * 8);  // 16-byte multiple <= 8 lda
+  auto issue = [&](int t, int st) {  // one thread: the rows of batch t into stage st
+    const int rows = min(RB, nrows - t * RB);
+    mbar_expect_tx(full + st, static_cast<unsigned>(rows) * rowbytes);
+    for (int u = 0; u < rows; ++u)
+      bulk_g2s(stages + static_cast<int64_t>(st) * SL_STAGE + u * (SL_ROW * 8), a.A + (r_begin + t * RB + u) * lda,
+               rowbytes, full + st, pol);
+  };
+  if (tid == 0)
+    for (int t = 0; t < npre; ++t) issue(t, t);
+  pdl_wait();
+
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  if (a.mode == 0) {
+    x = a.x;
+    r_prev = a.r_prev;
+    r_out = a.r_out;
+  } else {
+    const LoopCtl* ctl = a.ctl;
+    if (tid == 0) s_done = ctl->result.done;
+    __syncthreads();
+    if (s_done) {
+      if (tid == 0)
+        for (int t = 0; t < npre; ++t) mbar_wait(full + t, 0u);
+      return;
+    }
+    const int64_t SLOTS = ctl->r_slots;
+    if (a.mode == 1) {
+      const int64_t it = ctl->it;
+      x = a.xs + (it + 1) * a.n;
+      r_prev = a.rs + (it % SLOTS) * a.m;
+      r_out = a.rs + ((it + 1) % SLOTS) * a.m;
+    } else {
+      x = a.xs;
+      r_prev = nullptr;
+      r_out = a.rs;
+    }
+  }
+
+  // x (zero past n) in shared memory: with x, c and the row's values all in
+  // registers the kernel spills at 512 threads; a second 16-byte shared load
+  // per pair is cheaper than local memory
+  double* xs = reinterpret_cast<double*>(stages + static_cast<int64_t>(S) * SL_STAGE);
+  for (int c = tid; c < SL_ROW; c += SL_T) xs[c] = c < n ? x[c] : 0.0;
+  __syncthreads();
+  const uint32_t xa = smem_u32(xs) + static_cast<uint32_t>(ts) * 16u;
+  double2 acc[KP];
+  int padk = -1;  // the pair whose second column is the pad column of an odd n
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int c = 2 * (ts + 128 * k);
+    acc[k] = make_double2(0.0, 0.0);
+    if (ODD && c + 1 == n) padk = k;
+  }
+  // b / r_prev / r_true of the next batch, in warp 0 (lane u <-> row u)
+  auto fetch = [&](int t, double& fb, double& fp, double& ft) {
+    const int k = t * RB + lane;
+    const bool ok = lane < RB && t < ntiles && k < nrows;
+    const int64_t gi = r_begin + k;
+    fb = ok ? b[gi] : 0.0;
+    fp = (ok && r_prev) ? r_prev[gi] : 0.0;
+    ft = (ok && r_true) ? r_true[gi] : 0.0;
+  };
+  double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
+  double cb = 0.0, cp = 0.0, ct = 0.0;
+  if (warp == 0) fetch(0, cb, cp, ct);
+  // shared address of the thread's first pair in the current stage
+  uint32_t sa = smem_u32(stages) + static_cast<uint32_t>(slot) * (SL_ROW * 8) + static_cast<uint32_t>(ts) * 16u;
+  int st = 0;
+  unsigned ph = 0;
+  for (int t = 0, par = 0; t < ntiles; ++t, par ^= 1) {
+    double nb = 0.0, np = 0.0, nt = 0.0;
+    if (warp == 0) fetch(t + 1, nb, np, nt);
+    const int nu = min(RB, nrows - t * RB);
+    mbar_wait(full + st, ph);
+    double2 v[KP];
+#define ITSK_SL_LD(K) \
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v[K].x), "=d"(v[K].y) : "r"(sa), "n"(2048 * K));
+    ITSK_SL_LD(0) ITSK_SL_LD(1) ITSK_SL_LD(2) ITSK_SL_LD(3) ITSK_SL_LD(4) ITSK_SL_LD(5) ITSK_SL_LD(6) ITSK_SL_LD(7)
+#undef ITSK_SL_LD
+    static_assert(KP == 8, "eight pairs per thread");
+    if (ODD) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k)
+        if (k == padk) v[k].y = 0.0;
+    }
+    // the thread's partial dot of its row: 4 chains, one fixed order
+    double e[4] = {0.0, 0.0, 0.0, 0.0};
+    {
+      double2 xv[KP];
+#define ITSK_SL_LDX(K) \
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(xv[K].x), "=d"(xv[K].y) : "r"(xa), "n"(2048 * K));
+      ITSK_SL_LDX(0) ITSK_SL_LDX(1) ITSK_SL_LDX(2) ITSK_SL_LDX(3) ITSK_SL_LDX(4) ITSK_SL_LDX(5) ITSK_SL_LDX(6)
+      ITSK_SL_LDX(7)
+#undef ITSK_SL_LDX
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        e[k & 3] = fma(v[k].x, xv[k].x, e[k & 3]);
+        e[k & 3] = fma(v[k].y, xv[k].y, e[k & 3]);
+      }
+    }
+    double d = (e[0] + e[1]) + (e[2] + e[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+    if (lane == 0) dpart[par][warp] = d;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    // every thread has its values of stage st in registers: refill it (from the
+    // last warp: see the note at the row-group kernel's refill)
+    if (tid == SL_T - 32 && t + S < ntiles) issue(t + S, st);
+    if (warp == 0) {
+      if (lane < RB) {
+        const double2 q0 = *reinterpret_cast<const double2*>(&dpart[par][4 * lane]);
+        const double2 q1 = *reinterpret_cast<const double2*>(&dpart[par][4 * lane + 2]);
+        const double dot = (q0.x + q0.y) + (q1.x + q1.y);
+        const double rl = lane < nu ? bscale * cb - dot : 0.0;
+        rsm[par][lane] = rl;
+        if (lane < nu) {
+          if (r_out) r_out[r_begin + t * RB + lane] = rl;
+          s_rr += rl * rl;
+          s_bb += cb * cb;
+          const double dd = rl - cp;
+          s_dd += dd * dd;
+          const double tt = ct - rl;
+          s_tt += tt * tt;
+        }
+      }
+      cb = nb; cp = np; ct = nt;
+      __syncwarp();
+      asm volatile("bar.arrive 2, 512;" ::: "memory");
+    } else {
+      asm volatile("bar.sync 2, 512;" ::: "memory");
+    }
+    if (slot < nu) {  // (a slot past the last row holds an older batch's row)
+      const double rv = rsm[par][slot];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        acc[k].x = fma(rv, v[k].x, acc[k].x);
+        acc[k].y = fma(rv, v[k].y, acc[k].y);
+      }
+    }
+    ++st;
+    sa += SL_STAGE;
+    if (st == S) {
+      st = 0;
+      sa -= static_cast<uint32_t>(S) * SL_STAGE;
+      ph ^= 1u;
+    }
+  }
+  if (warp == 0) {
+    s_rr = warp_sum(s_rr);
+    s_dd = warp_sum(s_dd);
+    s_tt = warp_sum(s_tt);
+    s_bb = warp_sum(s_bb);
+    if (lane == 0) {
+      ssm[0] = s_rr;
+      ssm[1] = r_prev ? s_dd : 0.0;
+      ssm[2] = r_true ? s_tt : 0.0;
+      ssm[3] = s_bb;
+    }
+  }
+  __syncthreads();  // all stages consumed: the ring holds the slots' c partials
+  double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
+  double* csm = reinterpret_cast<double*>(stages);  // RB x SL_ROW
+#pragma unroll
+  for (int k = 0; k < KP; ++k)
+    *reinterpret_cast<double2*>(csm + slot * SL_ROW + 2 * (ts + 128 * k)) = acc[k];
+  __syncthreads();
+  for (int c = tid; c < n; c += SL_T) {
+    double sum = 0.0;
+#pragma unroll
+    for (int g = 0; g < RB; ++g) sum += csm[g * SL_ROW + c];
+    out[c] = sum;
+  }
+  if (tid < 4) out[n + tid] = ssm[tid];
+  if (a.tickets) group_reduce(a, n);
+}
+
 // Fixed-order reduction of the per-CTA partials: one warp per output, lanes
 // take CTAs strided by 32, then a fixed shuffle tree.
 __global__ void k_finalize(const double* __restrict__ part, int grid, int64_t n, double* cs,
@@ -1009,12 +1249,35 @@ int launch_rows(const PassArgs& a, int grid, cudaStream_t s) {
   return (a.n & 1) ? launch_rows_p<GW, CPP, true>(a, grid, s) : launch_rows_p<GW, CPP, false>(a, grid, s);
 }
 
+template <bool ODD>
+int launch_slots_p(const PassArgs& a0, int grid, cudaStream_t s) {
+  PassArgs a = a0;
+  TmaShape sh;
+  sh.T = SL_RB;
+  sh.stage_bytes = SL_STAGE;
+  sh.S = (TMA_SMEM_BUDGET - 1024 - SL_ROW * 8) / SL_STAGE;  // 3; a stage also holds the slots' c partials at the end
+  a.rows_per_cta = align_up((a.m + grid - 1) / grid, 4);
+  const size_t smem = 1024 + static_cast<size_t>(sh.S) * SL_STAGE + SL_ROW * 8;  // barriers | ring | x
+  ITSK_CUDA(allow_max_smem(reinterpret_cast<const void*>(k_pass_slots<ODD>)));
+  ITSK_CUDA(launch_pdl(reinterpret_cast<const void*>(k_pass_slots<ODD>), dim3(grid), dim3(SL_T), smem, s, a, sh));
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
+int launch_slots(const PassArgs& a, int grid, cudaStream_t s) {
+  return (a.n & 1) ? launch_slots_p<true>(a, grid, s) : launch_slots_p<false>(a, grid, s);
+}
+
 template <int CPL>
 int launch_tma(const PassArgs& a, int grid, cudaStream_t s) {
   // row groups where the group's 128 GW columns are mostly used (measured:
   // n = 500, 600, 1000, 2000 faster than the warp-per-row kernel; n = 200,
   // 300 slower, profiles/rd2_pass_rows_ab.txt)
   if (a.n > 384) {
+    // row slots from n ~ 1400 (short runs, GB/s rows / slots: n = 1280 5024 / 4724, 1536 5223 / 5469,
+    // 1792 5915 / 5971, 1920 5982 / 6157; sustained C4 passes under the power cap 10.40 / 10.07 ms)
+    if (a.n > 1408) return launch_slots(a, grid, s);
     if (a.n > 1024) return launch_rows<16, 2>(a, grid, s);
     if (a.n > 512) return launch_rows<8, 2>(a, grid, s);
     return launch_rows<4, 2>(a, grid, s);
