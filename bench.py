@@ -560,8 +560,8 @@ def run_b200(args):
                               "host_memory": "pageable numpy"} if ms_e2e_pg is not None else None),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-                         "kernel": "fused r=b-Ax, c=A'r pass (k_pass_rows for n > 384, k_pass_tma below; the "
-                                   "norms and the in-kernel partial reduction ride along)",
+                         "kernel": "fused r=b-Ax, c=A'r pass (k_pass_slots for n > 1408, k_pass_rows for n > 384, "
+                                   "k_pass_tma below; the norms and the in-kernel partial reduction ride along)",
                          "bytes_per_launch": alg_bytes, "ms_per_launch": pass_ms},
             "gpu_launches": int(launches),
             "iterations": iters, "stop_reason": res.trace.stop_reason, "fe": fe,
