@@ -396,19 +396,22 @@ def test_fused_pass_matches_numpy(pkg, m, n):
     assert got[n + 3] == pytest.approx(b @ b, rel=1e-12)
 
 
-@pytest.mark.parametrize("m,n", [(5003, 513), (4099, 1025), (6001, 2047), (777, 1500), (9, 2000)])
-def test_fused_pass_wide_padded_rows(pkg, m, n):
-    """Wide rows (512 < n <= 2048: the CTA-wide-row kernel) with an odd n
-    stored at an even leading dimension whose pad column holds NaN: the pad
-    must never enter r, c or the norms; batches of 4 rows with a ragged
-    last batch (m not a multiple of 4 per CTA)."""
+@pytest.mark.parametrize("m,n,lda", [(5003, 513, 514), (4099, 1025, 1026), (6001, 2047, 2048), (777, 1500, 1500),
+                                     (9, 2000, 2000), (3001, 1800, 2300), (1000, 2048, 2048), (2500, 1409, 1410),
+                                     (2500, 1408, 1500), (1203, 1999, 2600)])
+def test_fused_pass_wide_padded_rows(pkg, m, n, lda):
+    """Wide rows (512 < n <= 2048: the row-group kernel up to n = 1408, the
+    row-slot kernel above) with NaN in every pad column (an odd n stored at an
+    even leading dimension; a leading dimension well beyond n, which the
+    row-slot kernel's per-row copies do not stage): the pads must never enter
+    r, c or the norms; batches of 4 rows with a ragged last batch (m not a
+    multiple of 4 per CTA)."""
     import ctypes
 
     from paper_2311_04362_b200 import _lib
     from paper_2311_04362_b200 import device as dv
 
     rng = np.random.default_rng(m * n)
-    lda = n + (n & 1)
     a = rng.standard_normal((m, n))
     b = rng.standard_normal(m)
     x = rng.standard_normal(n)
