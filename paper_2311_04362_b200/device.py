@@ -27,6 +27,43 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else int(t.data_ptr())
 
 
+# Pageable host memory -> device.  cudaMemcpy from pageable memory is staged by
+# the driver on one thread (11.5 GB/s measured on the GPU box); here the rows
+# go through two pinned 64 MB buffers filled by torch's multi-threaded host copy
+# (61 GB/s on 16 cores) while the previous buffer's copy to the device is in
+# flight: 46 GB/s end to end (scripts/h2d_pageable_probe.py).
+STAGE_BYTES = 64 << 20
+STAGE_MIN_BYTES = 32 << 20   # smaller pageable inputs take the plain copy
+_STAGE: dict = {"bufs": None, "evs": [None, None], "next": 0}
+
+
+def upload_rows_staged(dst: torch.Tensor, src: torch.Tensor, r0: int, r1: int,
+                       stream: torch.cuda.Stream) -> torch.cuda.Event | None:
+    """dst[r0:r1] (device, row-major fp64) <- src[r0:r1] (pageable CPU fp64
+    matrix) through the pinned staging buffers, the device copies on
+    `stream`; returns the event of the last one."""
+    if _STAGE["bufs"] is None:
+        _STAGE["bufs"] = [torch.empty(STAGE_BYTES // 8, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    bufs, evs = _STAGE["bufs"], _STAGE["evs"]
+    n = int(src.shape[1])
+    rows = max(1, (STAGE_BYTES // 8) // max(n, 1))
+    ev = None
+    for s0 in range(r0, r1, rows):
+        s1 = min(r1, s0 + rows)
+        i = _STAGE["next"] & 1
+        _STAGE["next"] += 1
+        if evs[i] is not None:
+            evs[i].synchronize()  # the buffer's previous copy to the device
+        hb = bufs[i][: (s1 - s0) * n].view(s1 - s0, n)
+        hb.copy_(src[s0:s1])
+        with torch.cuda.stream(stream):
+            dst[s0:s1].copy_(hb, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        evs[i] = ev
+    return ev
+
+
 def as_device_matrix(a, dev: torch.device, non_blocking: bool = True) -> tuple[torch.Tensor, int]:
     """Row-major fp64 matrix on `dev` and its leading dimension (elements).
     numpy / CPU inputs are copied (asynchronously when the host memory is
@@ -41,7 +78,12 @@ def as_device_matrix(a, dev: torch.device, non_blocking: bool = True) -> tuple[t
         arr = np.asarray(a, dtype=np.float64)
         if arr.ndim != 2:
             raise ValueError(f"expected a matrix, got ndim={arr.ndim}")
-        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev, non_blocking=non_blocking)
+        h = torch.from_numpy(np.ascontiguousarray(arr))
+        if h.numel() * 8 >= STAGE_MIN_BYTES and not h.is_pinned():
+            t = torch.empty(tuple(h.shape), dtype=torch.float64, device=dev)
+            upload_rows_staged(t, h, 0, int(h.shape[0]), torch.cuda.current_stream(dev))
+        else:
+            t = h.to(dev, non_blocking=non_blocking)
     if t.ndim != 2:
         raise ValueError(f"expected a matrix, got ndim={t.ndim}")
     if t.stride(1) != 1 or t.stride(0) < t.shape[1]:

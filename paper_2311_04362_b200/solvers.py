@@ -372,10 +372,14 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
             ev.record(ws.copy_stream)
         events.append(ev)
 
+    def copy_chunk_staged(r0, r1):  # pageable host memory: through pinned staging buffers
+        events.append(_dev.upload_rows_staged(at, upload, r0, r1, ws.copy_stream))
+
     chunks = _upload_chunks(m, n) if upload is not None else []
     # pinned host memory: every chunk copy is queued before the pattern (whose
-    # redraw rounds wait on the host), so the copy engine never idles; a
-    # pageable copy blocks the host, so those are interleaved with the sketches
+    # redraw rounds wait on the host), so the copy engine never idles; pageable
+    # memory is staged through pinned buffers by the host (which that blocks),
+    # so those copies are interleaved with the sketches
     early = upload is not None and upload.is_pinned()
     if early:
         for r0, r1 in chunks:
@@ -387,7 +391,7 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
     if upload is not None:
         for k, (r0, r1) in enumerate(chunks):
             if not early:
-                copy_chunk(r0, r1)
+                copy_chunk_staged(r0, r1)
             compute.wait_event(events[k])
             _lib.check(lib.itsk_sketch_rows(_dev.ptr(at), m, n, lda, _dev.ptr(bt), _dev.ptr(ws.sk_ptr),
                                             _dev.ptr(ws.sk_src), d, zeta, _dev.ptr(ws.W), ws.ldw, r0, r1,

@@ -711,6 +711,24 @@ def test_chunked_upload_and_sketch_windows_bitwise(pkg, orc):
     del ctypes
 
 
+def test_pageable_upload_staging_is_exact(pkg):
+    """A pageable host matrix >= 32 MB goes through two pinned 64 MB staging
+    buffers (device.upload_rows_staged); several pieces per call and two
+    calls back to back (the buffers and their events are reused): the device
+    copy equals the plain one bit for bit, also for a strided source."""
+    from paper_2311_04362_b200 import device as dv
+
+    dev = dv.current_device()
+    rng = np.random.default_rng(3)
+    big = rng.standard_normal((70000, 401))          # 224 MB: 4 pieces
+    strided = rng.standard_normal((30000, 500))[:, :333]  # rows of a wider array
+    for arr in (big, strided, big[:12345]):
+        t, lda = dv.as_device_matrix(arr, dev)
+        torch.cuda.synchronize()
+        assert lda == arr.shape[1]
+        assert torch.equal(t.cpu(), torch.from_numpy(np.ascontiguousarray(arr)))
+
+
 def test_edge_configs(pkg, orc):
     # zeta == d, zeta == 1, odd n, residuals="last", extra_iters
     for (m, n, d, zeta) in [(300, 7, 10, 10), (500, 9, 40, 1), (2001, 33, 300, 3)]:
