@@ -79,11 +79,17 @@ def as_device_matrix(a, dev: torch.device, non_blocking: bool = True) -> tuple[t
         if arr.ndim != 2:
             raise ValueError(f"expected a matrix, got ndim={arr.ndim}")
         h = torch.from_numpy(np.ascontiguousarray(arr))
-        if h.numel() * 8 >= STAGE_MIN_BYTES and not h.is_pinned():
+        try:
             t = torch.empty(tuple(h.shape), dtype=torch.float64, device=dev)
+        except torch.OutOfMemoryError:
+            # a cached block of almost the right size (a previous upload of the
+            # same matrix) can neither be reused nor leaves room for a new one
+            torch.cuda.empty_cache()
+            t = torch.empty(tuple(h.shape), dtype=torch.float64, device=dev)
+        if h.numel() * 8 >= STAGE_MIN_BYTES and not h.is_pinned():
             upload_rows_staged(t, h, 0, int(h.shape[0]), torch.cuda.current_stream(dev))
         else:
-            t = h.to(dev, non_blocking=non_blocking)
+            t.copy_(h, non_blocking=non_blocking)
     if t.ndim != 2:
         raise ValueError(f"expected a matrix, got ndim={t.ndim}")
     if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
