@@ -567,16 +567,26 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
     // kernel shapes (all the same bits): columns per lane, sources per chunk,
     // warps per CTA, sketch rows per warp
     struct SwShape { const void* fn; int cl, warps, rpw; size_t smem; };
-    // 128-column panels; the 64-column shape is kept for the tests (same bits)
+    // 128-column panels with up to 12 sketch rows per warp; 64-column panels
+    // with up to 24 for a d beyond that (and, 12 rows, for the tests: same bits)
     static const SwShape shapes[] = {
         {reinterpret_cast<const void*>(k_sketch_stream<4, 8, 16, 12>), 4, 16, 12, sw_smem_bytes<4, 16, 12>()},
-        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()}};
-    const SwShape& sh = shapes[tu.swcl == 2 ? 1 : 0];
-    const int64_t nw = static_cast<int64_t>(nsm) * sh.warps;
-    // auto from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()},
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 24>), 2, 16, 24, sw_smem_bytes<2, 16, 24>()}};
+    const int64_t nw = static_cast<int64_t>(nsm) * 16;
+    const SwShape& sh = shapes[d > nw * 12 ? 2 : (tu.swcl == 2 ? 1 : 0)];
+    // automatic from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
     // 32 GB 24.1 / 35.5; 16 GB 12.4 / 17.3; 8 GB 6.1 / 8.3; C3 4 GB 3.7 / 4.1;
-    // C2 0.3 GB 0.50 / 0.27, where the gather finds A in L2)
-    const bool big = m * ncol * 8 >= (2ll << 30);
+    // C2 0.3 GB 0.50 / 0.27, where the gather finds A in L2) when the grid's
+    // warps have rows to own (C5 cells, profiles/rd2_final_sketch_sweep_c5.txt):
+    // d >= 2 rows per warp, and below 16 GB only with zeta >= 8 (the re-reads
+    // it saves) or d >= 4 rows per warp; from 16 GB also a d of one row for
+    // most warps when the rows are at least two panels wide
+    const int64_t bytes = m * ncol * 8;
+    const bool big =
+        bytes >= (2ll << 30) &&
+        ((d >= 2 * nw && (zeta >= 8 || d >= 4 * nw || bytes >= (16ll << 30))) ||
+         (4 * d >= 3 * nw && ncol >= 256 && bytes >= (16ll << 30) && zeta >= 8));
     if ((tu.sweep > 0 || (tu.sweep < 0 && big)) && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
         rg.j1 == 0xffffffffu && !rg.accum && d <= nw * sh.rpw && m < (1ll << 31)) {
       const int cl = sh.cl;

@@ -145,7 +145,8 @@ def test_sketch_kernel_variants_bitwise(pkg, orc, monkeypatch, variant):
 
 @pytest.mark.parametrize("m,n,d,lda,withb", [(700000, 300, 6000, 300, True), (600000, 511, 2000, 512, True),
                                               (450000, 1000, 12000, 1000, True), (250001, 129, 700, 131, True),
-                                              (300000, 256, 3000, 256, False), (90000, 40, 27000, 40, True)])
+                                              (300000, 256, 3000, 256, False), (90000, 40, 27000, 40, True),
+                                              (120000, 70, 41000, 70, True)])
 def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     """The window sweep (automatic from 2 GB of [A|b]: one persistent
     launch, the grid sweeping 20000-row source windows of one 128-column
@@ -154,7 +155,8 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     (ITSK_SKETCH_SWEEP=0, itself bitwise scipy's order in the tests above):
     bitwise equal, including the fused b column, for both lane widths; odd
     leading dimension (the unvectorised loads), no b, a ragged last window,
-    d beyond the grid's warps (up to 12 rows per warp, 27000 here)."""
+    d beyond the grid's warps (up to 12 rows per warp, 27000 here; 41000: the
+    64-column shape with up to 24 rows per warp)."""
     dev = torch.device("cuda")
     g = torch.Generator(device=dev).manual_seed(m)
     buf = torch.randn(m, lda, dtype=torch.float64, device=dev, generator=g)
