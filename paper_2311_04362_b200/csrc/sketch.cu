@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
     double* __restrict__ W, int64_t ldw, double inv_r, int nwin, int npanel, unsigned* wdone,
     uint32_t* __restrict__ bnd, uint2* ord, int flags) {
   const int vec = flags & 1;
-  const int drift = flags >> 8;  // windows a warp may run ahead of the slowest
+  const int direct = (flags >> 1) & 1;
+  const int drift = (flags >> 8) & 0xff;  // windows a warp may run ahead of the slowest
   static_assert(CL == 2 || CL == 4, "columns per lane");
   static_assert(U <= 32 && (U & (U - 1)) == 0 && SW_RPW <= 32, "chunk / row shape");
   constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
@@ -158,10 +159,23 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * SW_WARPS + warp;
   const int64_t ncol = n + (b ? 1 : 0);
   double2* acc_sm = reinterpret_cast<double2*>(sw_sm + static_cast<int64_t>(warp) * SW_RPW * PANEL);
-  // rows [row0, row0 + nrows) (d = q NW + rem: the first rem warps own q + 1)
-  const int64_t qr = d / NW, rem = d % NW;
-  const int64_t row0 = gw * qr + (gw < rem ? gw : rem);
-  const int nrows = static_cast<int>(qr + (gw < rem ? 1 : 0));
+  // rows [row0, row0 + nrows) (d = q NW + rem: the first rem warps own q + 1).
+  // Direct mode (no more sketch rows than the grid has warps): a warp owns at
+  // most ONE sketch row — its processing order is the row's own CSR order, so
+  // the entries are read straight from the pattern (no prologue, no scratch)
+  // — and the owners are dealt warp-major, so that every SM gets its share of
+  // the rows.
+  int64_t row0;
+  int nrows;
+  if (direct) {
+    const int64_t gwp = static_cast<int64_t>(warp) * gridDim.x + blockIdx.x;
+    row0 = gwp < d ? gwp : 0;
+    nrows = gwp < d ? 1 : 0;
+  } else {
+    const int64_t qr = d / NW, rem = d % NW;
+    row0 = gw * qr + (gw < rem ? gw : rem);
+    nrows = static_cast<int>(qr + (gw < rem ? 1 : 0));
+  }
   const bool rowok = lane < nrows;
   const uint32_t r0 = rowok ? ptr[row0 + lane] : 0u, r1 = rowok ? ptr[row0 + lane + 1] : 0u;
   const uint32_t e0 = ptr[row0];
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   // p-1, p in windows wp < wc end windows [wp, wc) at p; the row end is a
   // sentinel in window nwin)
   uint32_t* wb = bnd + gw * SW_RPW * static_cast<int64_t>(nwin);
-  for (int k = 0; k < nrows; ++k) {
+  for (int k = 0; k < (direct ? 0 : nrows); ++k) {
     const uint32_t a0 = __shfl_sync(FULL, r0, k), a1 = __shfl_sync(FULL, r1, k);
     int carry = 0;
     for (uint32_t q = a0; q <= a1; q += 32) {
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   }
   __syncwarp();
   // prologue 2: the entries in processing order
-  {
+  if (!direct) {
     uint32_t sk = r0, o = e0;
     for (int w = 0; w < nwin; ++w) {
       const uint32_t tk = rowok ? wb[lane * nwin + w] : 0u;
@@ -249,6 +263,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
             static_cast<unsigned>(g) + 1u;
   };
   const uint2* my = ord + e0;
+  const uint32_t* mysrc = src + e0;
+  auto entry = [&](uint32_t idx) { return direct ? make_uint2(__ldg(mysrc + idx), 0u) : my[idx]; };
   for (int p = 0; p < npanel; ++p) {
     // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
     // warp is one contiguous 512-byte segment)
@@ -273,10 +289,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
     double2 acc[NV];
     // lane u (mod U): entry P + u, clamped into the list
     uint2 ent = make_uint2(0u, 0u);
-    if (etot > 0) ent = my[min(static_cast<uint32_t>(lane & (U - 1)), etot - 1)];
+    if (etot > 0) ent = entry(min(static_cast<uint32_t>(lane & (U - 1)), etot - 1));
     for (uint32_t P = 0; P < etot; P += U) {
       uint2 entn = make_uint2(0u, 0u);
-      if (P + U < etot) entn = my[min(P + U + static_cast<uint32_t>(lane & (U - 1)), etot - 1)];
+      if (P + U < etot) entn = entry(min(P + U + static_cast<uint32_t>(lane & (U - 1)), etot - 1));
       const int nu = static_cast<int>(min(etot - P, static_cast<uint32_t>(U)));
       const uint32_t sv = ent.x;
       const int wf = static_cast<int>(sw_win(__shfl_sync(FULL, sv, 0) & 0x7fffffffu, inv_r));
@@ -492,9 +508,11 @@ struct SketchTune {
   int swcl = 0;      // window sweep columns per lane (2: 64-column panels, else 128; same bits)
   int drift = 2;      // window sweep: windows a warp may run ahead (L2 working set; same bits)
   int sweep = -1;     // window sweep: -1 auto (large A), 0 off, 1 on, > 1 on with that many window rows (same bits)
+  int direct = -1;    // window sweep, one row per warp read straight from the pattern: -1 auto, 0 off, 1 on (same bits)
   SketchTune() {
     if (const char* e = getenv("ITSK_SKETCH_SWEEP")) sweep = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_SWCL")) swcl = atoi(e);
+    if (const char* e = getenv("ITSK_SKETCH_DIRECT")) direct = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_DRIFT")) drift = std::min(7, std::max(1, atoi(e)));
     if (const char* e = getenv("ITSK_SKETCH_RING")) ring = atoi(e);
     if (const char* e = getenv("ITSK_SKETCH_GCPL")) gcpl = atoi(e);
@@ -558,7 +576,6 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   // 5000 up the gather wins, profiles/r04_sketch_ring_vs_gather.txt)
   const bool ring = tu.ring >= 0 ? tu.ring == 1
                                  : (tu.gcpl == 0 && tu.unr == 0 && d * ((ncol + 31) / 32) <= 2048);
-  if (ring) return launch_ring(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
   // the window sweep: a whole-source call (not an upload window, no
   // accumulation) on an A several times the L2, with every sketch row of the
   // grid's warps in registers
@@ -574,7 +591,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
         {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()},
         {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 24>), 2, 16, 24, sw_smem_bytes<2, 16, 24>()}};
     const int64_t nw = static_cast<int64_t>(nsm) * 16;
-    const SwShape& sh = shapes[d > nw * 12 ? 2 : (tu.swcl == 2 ? 1 : 0)];
+    const SwShape& sh0 = shapes[d > nw * 12 ? 2 : (tu.swcl == 2 ? 1 : 0)];
     // automatic from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
     // 32 GB 24.1 / 35.5; 16 GB 12.4 / 17.3; 8 GB 6.1 / 8.3; C3 4 GB 3.7 / 4.1;
     // C2 0.3 GB 0.50 / 0.27, where the gather finds A in L2) when the grid's
@@ -587,10 +604,20 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
         bytes >= (2ll << 30) &&
         ((d >= 2 * nw && (zeta >= 8 || d >= 4 * nw || bytes >= (16ll << 30))) ||
          (4 * d >= 3 * nw && ncol >= 256 && bytes >= (16ll << 30) && zeta >= 8));
-    if ((tu.sweep > 0 || (tu.sweep < 0 && big)) && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
+    // direct mode (no more sketch rows than warps: a warp owns one row and
+    // reads its entries straight from the pattern, no prologue and no scratch):
+    // wide rows of a large A (16.7M x 500, d = 2000, zeta = 8: 71.5 -> 65.5 ms);
+    // on C5's narrow cells (n = 100) one 8 KB chunk in flight per warp is too
+    // little and the ring / gather stay ahead (profiles/rd2_sketch_direct_ab.txt)
+    const bool can_direct = d <= nw && tu.direct != 0;
+    const bool direct = can_direct && (tu.direct == 1 || (ncol >= 256 && bytes >= (16ll << 30)));
+    const SwShape& sh = direct ? shapes[tu.swcl == 2 ? 1 : 0] : sh0;
+    if ((tu.sweep > 0 || (tu.sweep < 0 && (big || direct))) && tu.ring != 1 && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
         rg.j1 == 0xffffffffu && !rg.accum && d <= nw * sh.rpw && m < (1ll << 31)) {
       const int cl = sh.cl;
-      const uint32_t R = tu.sweep > 1 ? static_cast<uint32_t>(tu.sweep) : (cl == 2 ? 40000u : 20000u);
+      // a window holds ~20 MB of A: 20000 rows of a 128-column panel, 40000 of a 64-column one
+      const uint32_t R = tu.sweep > 1 ? static_cast<uint32_t>(tu.sweep)
+                                      : (cl == 2 ? 40000u : 20000u);
       const double inv_r = 1.0 / static_cast<double>(R);
       const int nwin = static_cast<int>(sw_win(static_cast<uint32_t>(m - 1), inv_r)) + 1;
       const int npanel = static_cast<int>((ncol + 32 * cl - 1) / (32 * cl));
@@ -598,12 +625,12 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
       uint32_t* bnd = nullptr;
       // per-window counters, then one 128-byte flag line per CTA
       const size_t cbytes = sizeof(unsigned) * (static_cast<size_t>(nwin) * npanel + 32 * static_cast<size_t>(nsm));
-      const size_t bbytes = sizeof(uint32_t) * static_cast<size_t>(nw) * sh.rpw * nwin;
+      const size_t bbytes = direct ? 0 : sizeof(uint32_t) * static_cast<size_t>(nw) * sh.rpw * nwin;
       ITSK_CUDA(keep_async_pool());
       // one scratch block: counters and flag lines | window boundaries | the
       // entries in processing order (8 m zeta bytes: 256 MB at C4).  Without
       // room for it the gather below does the job (same bits).
-      const size_t obytes = sizeof(uint2) * static_cast<size_t>(m) * zeta;
+      const size_t obytes = direct ? 0 : sizeof(uint2) * static_cast<size_t>(m) * zeta;
       const size_t c_al = (cbytes + 255) / 256 * 256, b_al = (bbytes + 255) / 256 * 256;
       unsigned char* scratch = nullptr;
       if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), c_al + b_al + obytes, s) != cudaSuccess) {
@@ -615,7 +642,8 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
         bnd = reinterpret_cast<uint32_t*>(scratch + c_al);
         uint2* ord = reinterpret_cast<uint2*>(scratch + c_al + b_al);
         ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
-        int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8);
+        int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8) |
+                    (direct ? 2 : 0);
         const void* fn = sh.fn;
         const size_t smem = sh.smem;
         ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -629,6 +657,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
       }
     }
   }
+  if (ring) return launch_ring(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
   int64_t need = (ncol + 31) / 32;
   int64_t cap = 4;
   while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 6000) cap >>= 1;

@@ -165,6 +165,7 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
     s = pkg.sparse_sign_new(d, m, 8, 5)
     monkeypatch.setenv("ITSK_SKETCH_SWEEP", "0")
     ref = s.apply_dense(a, b)
+    monkeypatch.setenv("ITSK_SKETCH_DIRECT", "0")  # the materialised-order path (the direct mode has its own test)
     # window rows: default, small (many windows per chunk: a chunk spanning
     # more than `drift` windows must not wait for itself; warps without rows
     # must not run a counter ring ahead), 128- and 64-column panels
@@ -173,6 +174,37 @@ def test_sketch_window_sweep_bitwise(pkg, monkeypatch, m, n, d, lda, withb):
         if sweep == "97" and m > 300000:
             continue  # thousands of windows: on the smaller shapes only
         monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)  # on below its automatic 2 GB threshold
+        monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
+        monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
+        got = s.apply_dense(a, b)
+        assert torch.equal(got, ref), (sweep, swcl, drift)
+
+
+@pytest.mark.parametrize("m,n,d,zeta,lda,withb", [(400000, 100, 400, 8, 100, True), (300000, 100, 1200, 16, 102, True),
+                                                   (250000, 37, 2000, 4, 37, True), (200000, 300, 500, 8, 300, False),
+                                                   (150000, 511, 2368, 8, 512, True), (100000, 64, 90, 8, 64, True),
+                                                   (50000, 200, 3, 2, 200, True)])
+def test_sketch_direct_sweep_bitwise(pkg, monkeypatch, m, n, d, zeta, lda, withb):
+    """The sweep's direct mode (no more sketch rows than the grid has warps: a
+    warp owns one row and streams its entries straight from the pattern;
+    chosen for wide rows of an A from 16 GB) against the register gather:
+    bitwise equal for both lane widths, odd leading dimensions, no b, rows on
+    only some of the warps, d equal to the number of warps, and windows of a
+    few hundred rows."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(m + d)
+    buf = torch.randn(m, lda, dtype=torch.float64, device=dev, generator=g)
+    a = buf[:, :n]
+    b = torch.randn(m, dtype=torch.float64, device=dev, generator=g) if withb else None
+    s = pkg.sparse_sign_new(d, m, zeta, 7)
+    monkeypatch.setenv("ITSK_SKETCH_SWEEP", "0")
+    monkeypatch.setenv("ITSK_SKETCH_RING", "0")
+    ref = s.apply_dense(a, b)
+    monkeypatch.delenv("ITSK_SKETCH_RING")
+    monkeypatch.setenv("ITSK_SKETCH_DIRECT", "1")
+    for sweep, swcl, drift in (("1", "0", "2"), ("1", "2", "2"), ("3000", "0", "3"), ("3000", "2", "1"),
+                               ("211", "0", "1"), ("211", "2", "2")):
+        monkeypatch.setenv("ITSK_SKETCH_SWEEP", sweep)
         monkeypatch.setenv("ITSK_SKETCH_SWCL", swcl)
         monkeypatch.setenv("ITSK_SKETCH_DRIFT", drift)
         got = s.apply_dense(a, b)
