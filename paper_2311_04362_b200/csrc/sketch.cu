@@ -608,7 +608,9 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
     // reads its entries straight from the pattern, no prologue and no scratch):
     // wide rows of a large A (16.7M x 500, d = 2000, zeta = 8: 71.5 -> 65.5 ms);
     // on C5's narrow cells (n = 100) one 8 KB chunk in flight per warp is too
-    // little and the ring / gather stay ahead (profiles/rd2_sketch_direct_ab.txt)
+    // little and the ring / gather stay ahead; so did a gated cp.async ring with up to
+    // 64 segments in flight per owner: with one warp per row the warp's own
+    // instruction stream is the limit (profiles/rd2_sketch_direct_ab.txt)
     const bool can_direct = d <= nw && tu.direct != 0;
     const bool direct = can_direct && (tu.direct == 1 || (ncol >= 256 && bytes >= (16ll << 30)));
     const SwShape& sh = direct ? shapes[tu.swcl == 2 ? 1 : 0] : sh0;
