@@ -141,15 +141,14 @@ __host__ __device__ __forceinline__ uint32_t sw_win(uint32_t j, double inv_r) {
   return static_cast<uint32_t>(static_cast<double>(j) * inv_r);
 }
 
-template <int CL, int U, int SW_WARPS, int SW_RPW>
+template <int CL, int U, int SW_WARPS, int SW_RPW, bool DIRECT>
 __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
     const double* __restrict__ A, int64_t lda, int64_t n, const double* __restrict__ b,
     const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ src, int64_t d, double scale,
     double* __restrict__ W, int64_t ldw, double inv_r, int nwin, int npanel, unsigned* wdone,
     uint32_t* __restrict__ bnd, uint2* ord, int flags) {
   const int vec = flags & 1;
-  const int direct = (flags >> 1) & 1;
-  const int drift = (flags >> 8) & 0xff;  // windows a warp may run ahead of the slowest
+  const int drift = flags >> 8;  // windows a warp may run ahead of the slowest
   static_assert(CL == 2 || CL == 4, "columns per lane");
   static_assert(U <= 32 && (U & (U - 1)) == 0 && SW_RPW <= 32, "chunk / row shape");
   constexpr int PANEL = 32 * CL, NV = CL / 2;  // NV double2 per lane per source
@@ -165,17 +164,12 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   // the entries are read straight from the pattern (no prologue, no scratch)
   // — and the owners are dealt warp-major, so that every SM gets its share of
   // the rows.
-  int64_t row0;
-  int nrows;
-  if (direct) {
-    const int64_t gwp = static_cast<int64_t>(warp) * gridDim.x + blockIdx.x;
-    row0 = gwp < d ? gwp : 0;
-    nrows = gwp < d ? 1 : 0;
-  } else {
-    const int64_t qr = d / NW, rem = d % NW;
-    row0 = gw * qr + (gw < rem ? gw : rem);
-    nrows = static_cast<int>(qr + (gw < rem ? 1 : 0));
-  }
+  // (a template parameter: the materialised-order kernel's code is untouched —
+  // as a run-time branch the direct path cost the C4 sketch 46.3 -> 53.2 ms)
+  const int64_t qr = d / NW, rem = d % NW;
+  const int64_t gwp = static_cast<int64_t>(warp) * gridDim.x + blockIdx.x;
+  const int64_t row0 = DIRECT ? (gwp < d ? gwp : 0) : gw * qr + (gw < rem ? gw : rem);
+  const int nrows = DIRECT ? (gwp < d ? 1 : 0) : static_cast<int>(qr + (gw < rem ? 1 : 0));
   const bool rowok = lane < nrows;
   const uint32_t r0 = rowok ? ptr[row0 + lane] : 0u, r1 = rowok ? ptr[row0 + lane + 1] : 0u;
   const uint32_t e0 = ptr[row0];
@@ -184,7 +178,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   // p-1, p in windows wp < wc end windows [wp, wc) at p; the row end is a
   // sentinel in window nwin)
   uint32_t* wb = bnd + gw * SW_RPW * static_cast<int64_t>(nwin);
-  for (int k = 0; k < (direct ? 0 : nrows); ++k) {
+  for (int k = 0; k < (DIRECT ? 0 : nrows); ++k) {
     const uint32_t a0 = __shfl_sync(FULL, r0, k), a1 = __shfl_sync(FULL, r1, k);
     int carry = 0;
     for (uint32_t q = a0; q <= a1; q += 32) {
@@ -199,7 +193,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   }
   __syncwarp();
   // prologue 2: the entries in processing order
-  if (!direct) {
+  if constexpr (!DIRECT) {
     uint32_t sk = r0, o = e0;
     for (int w = 0; w < nwin; ++w) {
       const uint32_t tk = rowok ? wb[lane * nwin + w] : 0u;
@@ -264,7 +258,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   };
   const uint2* my = ord + e0;
   const uint32_t* mysrc = src + e0;
-  auto entry = [&](uint32_t idx) { return direct ? make_uint2(__ldg(mysrc + idx), 0u) : my[idx]; };
+  auto entry = [&](uint32_t idx) {
+    if constexpr (DIRECT) return make_uint2(__ldg(mysrc + idx), 0u);
+    else return my[idx];
+  };
   for (int p = 0; p < npanel; ++p) {
     // this lane's columns: cA + 64 h + {0, 1}, h < NV (each 16-byte load of a
     // warp is one contiguous 512-byte segment)
@@ -566,8 +563,12 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   // columns per lane: at most 4 (4 columns x 4 sources = 16 loads in flight
   // per lane at ~70 registers; 8 columns needs ~110 registers and halves the
   // resident warps — 25% slower at C2), fewer when d is small so that the grid
-  // still has >= ~6000 warps (the chains are sequential per output, so
-  // parallelism comes only from d x column blocks).  A TMA-staged variant
+  // still has >= ~2400 warps (the chains are sequential per output, so
+  // parallelism comes only from d x column blocks; but these shapes are bound
+  // by warp instructions per (source, column block), and two columns per lane
+  // halve them: 16.7M x 100, d = 2000: 22.8 ms with 8000 one-column warps, 15.8
+  // with 4000 two-column warps, 18.5 with 2000 four-column warps;
+  // profiles/rd2_sketch_gather_ab.txt).  A TMA-staged variant
   // (per-warp ring of bulk-copied row segments) measured 1.8-5x slower: the
   // per-copy cost of 0.25-2 KB bulk copies dominates.
   // few (sketch row x 32-column) chains — about one wave or less — leave the
@@ -587,9 +588,12 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
     // 128-column panels with up to 12 sketch rows per warp; 64-column panels
     // with up to 24 for a d beyond that (and, 12 rows, for the tests: same bits)
     static const SwShape shapes[] = {
-        {reinterpret_cast<const void*>(k_sketch_stream<4, 8, 16, 12>), 4, 16, 12, sw_smem_bytes<4, 16, 12>()},
-        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()},
-        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 24>), 2, 16, 24, sw_smem_bytes<2, 16, 24>()}};
+        {reinterpret_cast<const void*>(k_sketch_stream<4, 8, 16, 12, false>), 4, 16, 12, sw_smem_bytes<4, 16, 12>()},
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 12, false>), 2, 16, 12, sw_smem_bytes<2, 16, 12>()},
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 24, false>), 2, 16, 24, sw_smem_bytes<2, 16, 24>()},
+        // direct mode: one row per warp (one row's running sums in shared memory)
+        {reinterpret_cast<const void*>(k_sketch_stream<4, 8, 16, 1, true>), 4, 16, 1, sw_smem_bytes<4, 16, 1>()},
+        {reinterpret_cast<const void*>(k_sketch_stream<2, 16, 16, 1, true>), 2, 16, 1, sw_smem_bytes<2, 16, 1>()}};
     const int64_t nw = static_cast<int64_t>(nsm) * 16;
     const SwShape& sh0 = shapes[d > nw * 12 ? 2 : (tu.swcl == 2 ? 1 : 0)];
     // automatic from 2 GB of [A|b] (streamed sweep vs gather, ms: C4 64 GB 46.6 / 72;
@@ -613,7 +617,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
     // instruction stream is the limit (profiles/rd2_sketch_direct_ab.txt)
     const bool can_direct = d <= nw && tu.direct != 0;
     const bool direct = can_direct && (tu.direct == 1 || (ncol >= 256 && bytes >= (16ll << 30)));
-    const SwShape& sh = direct ? shapes[tu.swcl == 2 ? 1 : 0] : sh0;
+    const SwShape& sh = direct ? shapes[tu.swcl == 2 ? 4 : 3] : sh0;
     if ((tu.sweep > 0 || (tu.sweep < 0 && (big || direct))) && tu.ring != 1 && tu.gcpl == 0 && tu.unr == 0 && rg.j0 == 0 &&
         rg.j1 == 0xffffffffu && !rg.accum && d <= nw * sh.rpw && m < (1ll << 31)) {
       const int cl = sh.cl;
@@ -644,8 +648,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
         bnd = reinterpret_cast<uint32_t*>(scratch + c_al);
         uint2* ord = reinterpret_cast<uint2*>(scratch + c_al + b_al);
         ITSK_CUDA(cudaMemsetAsync(wdone, 0, cbytes, s));
-        int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8) |
-                    (direct ? 2 : 0);
+        int flags = ((lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) ? 1 : 0) | (tu.drift << 8);
         const void* fn = sh.fn;
         const size_t smem = sh.smem;
         ITSK_CUDA(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -662,7 +665,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   if (ring) return launch_ring(A, lda, n, b, sk_ptr, sk_src, d, scale, SAb, ldw, rg, s);
   int64_t need = (ncol + 31) / 32;
   int64_t cap = 4;
-  while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 6000) cap >>= 1;
+  while (cap > 1 && d * ((ncol + 32 * cap - 1) / (32 * cap)) < 2400) cap >>= 1;
   if (tu.gcpl > 0) cap = tu.gcpl;
   if (need > cap) need = cap;
   const int unr = tu.unr > 0 ? tu.unr : (need <= 2 ? 8 : 4);
