@@ -7,9 +7,10 @@
     cond_est             linalg.py:108-113  -> device Lanczos extremes of R'R, R^-1 R^-T
 
 Differences from the reference, by design:
-  * the QR never forms Q (dorgqr); it applies the reflectors to an extra
-    right-hand-side column instead, returning R and z = Q'rhs.  Reading
-    QrFactors.q raises an AttributeError explaining this.
+  * the QR does not form Q (dorgqr) on the solver path; it applies the
+    reflectors to an extra right-hand-side column instead, returning R and
+    z = Q'rhs.  QrFactors.q forms Q on first access from the Householder
+    vectors (householder_qr_econ keeps them).
   * cond_est uses Lanczos (<= 96 steps, stopped when the extreme Ritz values
     are stable to rounding) instead of a full SVD; for the spectra on this
     path it agrees with dgesdd's ratio to ~1e-14 relative (tests/).
@@ -19,7 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -34,21 +35,61 @@ __all__ = ["QrFactors", "SingularMatrixError", "householder_qr_econ", "qr_aug", 
 
 @dataclass(frozen=True)
 class QrFactors:
-    """R (n x n, upper, diag >= 0) and z = Q' rhs (None without a rhs).
+    """R (n x n, upper, diag >= 0), z = Q' rhs (None without a rhs), and Q.
 
-    The reference's QrFactors (linalg.py:21-27) carries an explicit Q; this
-    path never forms it (the reflectors are applied to the rhs column
-    instead, solvers.py:209 only needs Q'Sb).  Reading `q` raises an
-    AttributeError that says so, rather than returning None
-    (INTEGRATION.md §4)."""
+    The reference's QrFactors (linalg.py:21-27) carries an explicit Q from
+    dorgqr.  The solver path never needs it (the reflectors are applied to the
+    rhs column instead, solvers.py:209 only needs Q'Sb), so `q` is formed on
+    first access from the Householder vectors the device QR leaves below the
+    diagonal (`_form_q`; float64 GEMMs through torch, off the solver path)."""
 
     r: object
     z: object = None
+    _v: object = field(default=None, repr=False, compare=False)   # the factored [V \ R | .] (device)
+    _a: object = field(default=None, repr=False, compare=False)   # the input (device), for the sign of diag(R)
+    _host: bool = field(default=False, repr=False, compare=False)
 
     @property
     def q(self):
-        raise AttributeError("QrFactors.q: the B200 QR does not form Q (dorgqr); use "
-                             "householder_qr_econ(a, rhs=b).z for Q'b, as sketch_and_solve does")
+        """Q (m x n, orthonormal columns, Q R = A) as linalg.py:42-46 returns it."""
+        cached = self.__dict__.get("_q")
+        if cached is None:
+            if self._v is None:
+                raise AttributeError("QrFactors.q: built without the Householder vectors; use "
+                                     "householder_qr_econ(a) to get a QrFactors that can form Q")
+            qd = _form_q(self._v, self.r.shape[0], self._a)
+            cached = _dev.to_numpy(qd) if self._host else qd
+            object.__setattr__(self, "_q", cached)
+        return cached
+
+
+def _form_q(w: torch.Tensor, n: int, a: torch.Tensor, nb: int = 128) -> torch.Tensor:
+    """Q = H_1 ... H_n [I; 0] (dorgqr) from the factored matrix: column j of
+    `w` holds v_j below the diagonal (unit diagonal implied).  tau_j =
+    2 / v_j'v_j (dlarfg's (beta - alpha) / beta), 0 for an exactly zero tail
+    (H_j = I); blocks of nb reflectors are applied last block first as
+    I - V T V' with T^-1 = diag(1/tau) + striu(V'V) (dlarft).  The columns are
+    then signed like R's rows (diag(R) >= 0, linalg.py:43-46)."""
+    d = w.shape[0]
+    dev = w.device
+    q = torch.zeros((d, n), dtype=torch.float64, device=dev)
+    q.diagonal().fill_(1.0)
+    for k1 in range(n, 0, -nb):
+        k0 = max(0, k1 - nb)
+        v = torch.tril(w[k0:, k0:k1], -1)
+        live = (v != 0).any(0)                 # reflectors with a non-zero tail
+        v.diagonal().copy_(live.to(torch.float64))
+        g = v.T @ v
+        tinv = torch.triu(g, 1)
+        tinv.diagonal().copy_(torch.where(live, 0.5 * g.diagonal(), torch.ones_like(g.diagonal())))
+        qs = q[k0:, :]
+        y = v.T @ qs
+        zt = torch.linalg.solve_triangular(tinv, y, upper=True)
+        qs.sub_(v @ zt)
+    sgn = torch.sign((q * a).sum(0))
+    sgn = torch.where(sgn == 0, torch.ones_like(sgn), sgn)
+    q.mul_(sgn)
+    return q
 
 
 def qr_workspace(d: int, n: int, dev) -> torch.Tensor:
@@ -94,9 +135,11 @@ def householder_qr_econ(a, rhs=None) -> QrFactors:
     if rhs is not None:
         w[:, n] = _dev.as_device_vector(rhs, dev)
     r, z = qr_aug(w, n)
+    # w (the Householder vectors) and the input stay on the device behind the
+    # result so that .q can be formed on request
     if host:
-        return QrFactors(r=_dev.to_numpy(r), z=None if z is None else _dev.to_numpy(z))
-    return QrFactors(r=r, z=z)
+        return QrFactors(r=_dev.to_numpy(r), z=None if z is None else _dev.to_numpy(z), _v=w, _a=at, _host=True)
+    return QrFactors(r=r, z=z, _v=w, _a=at)
 
 
 def _solve(r, c, trans: int):

@@ -301,6 +301,35 @@ def test_qr_deterministic(pkg):
     assert np.array_equal(f1.r, f2.r)
 
 
+@pytest.mark.parametrize("m,n,seed,kappa", [(20, 5, 1, 1e2), (7, 7, 2, 1e1), (4000, 201, 4, 1e8), (14000, 1000, 10, 1e10),
+                                             (40000, 64, 2, 1e4), (3000, 130, 6, 1e12)])
+def test_qr_explicit_q(pkg, m, n, seed, kappa):
+    """QrFactors.q (linalg.py:42-46: dorgqr's Q with the columns signed like
+    R's rows), formed from the device QR's Householder vectors: orthonormal,
+    Q R = A, Q'b = z, and equal to LAPACK's Q up to rounding times kappa —
+    over the single-kernel, panel, two-level and large-d fallback paths."""
+    rng = np.random.default_rng(seed)
+    u0, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v0, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u0 * np.logspace(0, -np.log10(kappa), n)) @ v0.T
+    b = rng.standard_normal(m)
+    f = pkg.householder_qr_econ(a, rhs=b)
+    q, r = f.q, f.r
+    u = np.finfo(float).eps
+    assert q.shape == (m, n) and f.q is q
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 100 * n * u
+    assert np.linalg.norm(q @ r - a) <= 100 * n * u * np.linalg.norm(a)
+    assert np.linalg.norm(q.T @ b - f.z) <= 100 * n * u * np.linalg.norm(b)
+    ql, rl = np.linalg.qr(a)
+    sg = np.sign(np.diag(rl))
+    ql = ql * sg
+    if kappa <= 1e4:
+        assert np.linalg.norm(q - ql) <= 100 * n * u * kappa
+    # device input -> device Q
+    ft = pkg.householder_qr_econ(torch.from_numpy(a).cuda())
+    assert isinstance(ft.q, torch.Tensor) and np.array_equal(ft.q.cpu().numpy(), q)
+
+
 def test_trsv_and_estimates_vs_reference(pkg, golden):
     g = golden("linalg.npz")
     import scipy.linalg as sl

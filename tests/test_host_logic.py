@@ -70,14 +70,15 @@ def test_gen_randsvd_matches_oracle_bitwise():
     assert math.isclose(np.linalg.norm(p.truth.r), 1e-4, rel_tol=1e-12)
 
 
-def test_qrfactors_q_raises_clearly():
-    """The B200 QR never forms Q: reading .q says so
-    instead of returning None."""
+def test_qrfactors_q_without_vectors_raises_clearly():
+    """A QrFactors built by hand (no Householder vectors behind it) cannot
+    form Q: reading .q says so instead of returning None (ADVICE r1);
+    householder_qr_econ's result forms Q on request (tests/test_gpu_parity.py)."""
     import pytest
 
     from paper_2311_04362_b200.linalg import QrFactors
 
     f = QrFactors(r=np.eye(2), z=np.zeros(2))
-    with pytest.raises(AttributeError, match="does not form Q"):
+    with pytest.raises(AttributeError, match="without the Householder vectors"):
         f.q
     assert not hasattr(f, "q")
