@@ -624,7 +624,8 @@ def iterative_sketching(a, b, cfg: SolverConfig, truth: Truth | None = None, *,
 
 def sketch_and_solve(a, b, s: SparseSignEmbedding):
     """Sketch-and-solve start (solvers.py:199-210): x0 = R^-1 (Q'Sb)[:n] with
-    R from the QR of S·A.  Returns (x0, QrFactors(r, z)); Q is not formed."""
+    R from the QR of S·A.  Returns (x0, QrFactors(r, z)); the factors' Q (of
+    S·A, linalg.py:42) is formed only if `.q` is read."""
     from .linalg import QrFactors, qr_aug
 
     host = not isinstance(a, torch.Tensor)
@@ -633,9 +634,10 @@ def sketch_and_solve(a, b, s: SparseSignEmbedding):
     m, n = at.shape
     bt = _dev.as_device_vector(b, dev)
     w = s.apply_dense(at, bt)
+    sa = w[:, :n].clone()  # S·A before the QR overwrites it (the sign reference of QrFactors.q)
     r, z = qr_aug(w, n)
     x0 = torch.empty(n, dtype=torch.float64, device=dev)
     _lib.check(_dev.lib(dev).itsk_trsv(_dev.ptr(r), n, _dev.ptr(z), _dev.ptr(x0), 0, _dev.stream_ptr()))
     if host:
-        return _dev.to_numpy(x0), QrFactors(r=_dev.to_numpy(r), z=_dev.to_numpy(z))
-    return x0, QrFactors(r=r, z=z)
+        return _dev.to_numpy(x0), QrFactors(r=_dev.to_numpy(r), z=_dev.to_numpy(z), _v=w, _a=sa, _host=True)
+    return x0, QrFactors(r=r, z=z, _v=w, _a=sa)

@@ -7,7 +7,9 @@ tests/test_oracle_pin.py (tests/golden/theory.npz).
 
   C01  test_acceptance.py:58-74    FE/RE within 10x of QR on the 12-case grid
   C02  test_acceptance.py:77-95    geometric rate <= g_IS(eps) + 0.05, Thm bound
+  C03  test_acceptance.py:98-114   sketch-and-solve quality (Fact 2.4), 100 seeds
   C08  test_acceptance.py:219-240  damped / momentum rates and final FE
+  test_solvers.py:158-175 (sketch_and_solve: consistent system, quality bounds)
   test_solvers.py:173-182 (consistent system), :189-195, :197-207, :209-221,
   :235-246 (extra_iters plateau), :248-256 (bitwise determinism), :258-264
 """
@@ -184,3 +186,68 @@ def test_damped_and_momentum_converge(pkg):
         res = _solve(pkg, p, d=400, variant=variant, max_iters=60, rng_seed=6)
         assert res.trace.stop_reason != "diverged"
         assert res.trace.fe[-1] <= 1e-10, (variant, res.trace.fe[-1])
+
+
+def _pattern_of(orc, s):
+    """The device-generated pattern as the oracle's Pattern (bit-equal to the
+    oracle's own, tests/test_gpu_parity.py; taken from the device here so the
+    distortion is measured for the embedding sketch_and_solve uses)."""
+    return orc.Pattern(d=s.d, m=s.m, zeta=s.zeta, rows=np.asarray(s.rows).astype(np.int64),
+                       signs=np.asarray(s.signs).astype(np.float64), scale=s.scale)
+
+
+def test_sketch_and_solve_consistent_system(pkg):
+    """test_solvers.py:159-163: beta = 0 -> the sketched solve is exact."""
+    p = pkg.gen_randsvd(400, 15, 1e4, 0.0, 0)
+    s = pkg.sparse_sign_new(200, 400, 8, 0)
+    x0, _ = pkg.sketch_and_solve(p.a, p.b, s)
+    assert np.linalg.norm(p.b - p.a @ x0) <= 1e-12 * np.linalg.norm(p.b)
+
+
+def test_sketch_and_solve_quality_bounds_and_factors(pkg, orc):
+    """test_solvers.py:165-175: Fact 2.4's residual and forward-error bounds
+    with the measured distortion of the same embedding; and the returned
+    factors are those of S·A (linalg.py:42-46): Q R = S A, Q'Sb = z,
+    R x0 = z, equal to the oracle's x0 to rounding."""
+    p = pkg.gen_randsvd(1000, 20, 1e4, 1e-2, 1)
+    s = pkg.sparse_sign_new(500, 1000, 8, 1)
+    pat = orc.sparse_sign_pattern(500, 1000, 8, 1)
+    q = np.linalg.qr(p.a, mode="reduced")[0]
+    eps = orc.measure_distortion(pat, q)
+    x0, f = pkg.sketch_and_solve(p.a, p.b, s)
+    beta = p.truth.beta
+    assert np.linalg.norm(p.b - p.a @ x0) <= (1 + eps) / (1 - eps) * beta * (1 + 1e-10)
+    norm_a = np.linalg.norm(p.a, 2)
+    fe_bound = 2 * math.sqrt(eps) / (1 - eps) * p.truth.kappa / norm_a * beta
+    assert np.linalg.norm(p.truth.x - x0) <= fe_bound * (1 + 1e-10)
+    sa, sb = orc.sketch_apply(pat, p.a), orc.sketch_apply(pat, p.b[:, None])[:, 0]
+    n = 20
+    assert np.linalg.norm(f.q @ f.r - sa) <= 100 * n * U * np.linalg.norm(sa)
+    assert np.linalg.norm(f.q.T @ f.q - np.eye(n)) <= 100 * n * U
+    assert np.linalg.norm(f.q.T @ sb - f.z) <= 100 * n * U * np.linalg.norm(sb)
+    qo, ro = orc.householder_qr_econ(sa)
+    x_ref = orc.tri_solve_upper(ro, qo.T @ sb)
+    assert np.linalg.norm(x0 - x_ref) <= 100 * n * U * np.linalg.cond(sa) * np.linalg.norm(x_ref)
+
+
+def test_c03_sketch_and_solve_quality(pkg, orc):
+    """test_acceptance.py:98-114: over 100 seeds (1000 x 25, kappa 1e4, beta
+    1e-3, d = 500) the sketch-and-solve residual and forward error stay
+    within Fact 2.4's bounds at the embedding's measured distortion of
+    range([A b]): 0 violations."""
+    violations = 0
+    for seed in range(100):
+        p = pkg.gen_randsvd(1000, 25, 1e4, 1e-3, seed)
+        s = pkg.sparse_sign_new(500, 1000, 8, seed)
+        basis = np.linalg.qr(np.column_stack([p.a, p.b]), mode="reduced")[0]
+        eps = orc.measure_distortion(_pattern_of(orc, s), basis)
+        x0, _ = pkg.sketch_and_solve(p.a, p.b, s)
+        slack = 1 + 1e-8
+        if np.linalg.norm(p.b - p.a @ x0) / p.truth.beta > (1 + eps) / (1 - eps) * slack:
+            violations += 1
+        norm_a = np.linalg.norm(p.a, 2)
+        fe_lim = 2 * math.sqrt(eps) / (1 - eps) * p.truth.kappa / norm_a * p.truth.beta
+        if np.linalg.norm(p.truth.x - x0) > fe_lim * slack:
+            violations += 1
+    print(f"[C03] {violations} violations over 100 seeds (limit 0)")
+    assert violations == 0
