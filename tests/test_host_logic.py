@@ -50,6 +50,14 @@ def test_param_formulas():
     assert momentum_params(0.5) == (pytest.approx(0.5625), pytest.approx(0.25))
     grid = np.linspace(0.0, 0.9, 91)
     assert np.all(np.diff([damping_params(e)[0] for e in grid]) < 0)
+    # test_solvers.py:59-71: momentum at 0, beta < 1 on [0, 1), the domain errors
+    assert momentum_params(0.0) == (1.0, 0.0) and damping_params(0.5)[1] == 0.0
+    assert all(momentum_params(e)[1] < 1.0 for e in np.linspace(0.0, 0.999, 50))
+    for fn in (damping_params, momentum_params):
+        with pytest.raises(ValueError):
+            fn(1.0)
+        with pytest.raises(ValueError):
+            fn(-0.1)
 
 
 def test_should_stop_inclusive_boundary():
