@@ -251,3 +251,51 @@ def test_c03_sketch_and_solve_quality(pkg, orc):
             violations += 1
     print(f"[C03] {violations} violations over 100 seeds (limit 0)")
     assert violations == 0
+
+
+def test_c07_backward_error_dichotomy(pkg, orc):
+    """test_acceptance.py:203-216: iterative sketching is backward stable
+    when the residual is small (beta = 1e-12: BE <= 100u) and only forward
+    stable when it is not (beta = 1e-3: BE >= 100u while Householder QR's is
+    <= 100u).  The trace's BE (cfg.track_be: the device restatement of
+    metrics.py:99-129) agrees with the oracle's on the same solution."""
+    bes = {}
+    for beta in (1e-12, 1e-3):
+        p = pkg.gen_randsvd(4000, 50, 1e10, beta, 0)
+        res = _solve(pkg, p, d=1000, max_iters=100, track_be=True)
+        be_ref = orc.backward_error(p.a, p.b, res.solution)
+        be_dev = res.trace.be[-1]
+        assert abs(be_dev - be_ref) <= 1e-6 * be_ref + 50 * U, (beta, be_dev, be_ref)
+        bes[beta] = be_ref
+        if beta == 1e-3:
+            be_qr = orc.backward_error(p.a, p.b, orc.qr_solve(p.a, p.b))
+    print(f"[C07] BE(IS) {bes[1e-12]:.2g} / {bes[1e-3]:.2g}, BE(QR) {be_qr:.2g}, 100u = {100 * U:.2g}")
+    assert bes[1e-12] <= 100 * U and bes[1e-3] >= 100 * U and be_qr <= 100 * U
+
+
+def test_backward_error_device_matches_oracle(pkg, orc):
+    """metrics.py:99-129 on the device against the oracle (test_metrics.py:
+    101-137): both branches (m <= 400 literal SVD, m > 400 reduced form) over
+    random scalings, the zero-residual, zero-x and size-cap cases."""
+    from paper_2311_04362_b200.metrics import backward_error_device as be_dev
+
+    def dev(a, b, x, **kw):
+        return be_dev(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(x).cuda(), **kw)
+
+    rng = np.random.default_rng(2)
+    for trial in range(12):
+        m = int(rng.integers(500, 700)) if trial % 2 else int(rng.integers(30, 400))
+        n = int(rng.integers(2, 12))
+        a = rng.standard_normal((m, n)) * 10.0 ** rng.integers(-2, 2)
+        x = rng.standard_normal(n)
+        b = a @ x + 10.0 ** rng.integers(-10, -1) * rng.standard_normal(m)
+        x_hat = np.linalg.lstsq(a, b, rcond=None)[0] + 10.0 ** rng.integers(-12, -3) * rng.standard_normal(n)
+        ref = orc.backward_error(a, b, x_hat)
+        assert abs(dev(a, b, x_hat) - ref) <= 1e-6 * ref + 50 * U, (trial, m, n)
+    a = np.eye(3)
+    x = np.array([1.0, 2.0, 3.0])
+    assert dev(a, a @ x, x) == 0.0
+    with pytest.raises(ValueError):
+        dev(np.eye(3), np.ones(3), np.zeros(3))
+    with pytest.raises(ValueError):
+        dev(np.ones((11, 2)), np.ones(11), np.ones(2), max_m=10)
