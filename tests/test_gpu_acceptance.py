@@ -8,7 +8,9 @@ tests/test_oracle_pin.py (tests/golden/theory.npz).
   C01  test_acceptance.py:58-74    FE/RE within 10x of QR on the 12-case grid
   C02  test_acceptance.py:77-95    geometric rate <= g_IS(eps) + 0.05, Thm bound
   C03  test_acceptance.py:98-114   sketch-and-solve quality (Fact 2.4), 100 seeds
+  C07  test_acceptance.py:203-216  backward-error dichotomy (and the device BE vs the oracle's)
   C08  test_acceptance.py:219-240  damped / momentum rates and final FE
+  C09  test_acceptance.py:243-274  stopping rule: the same corners fire, same reasons / iterations as the oracle
   test_solvers.py:158-175 (sketch_and_solve: consistent system, quality bounds)
   test_solvers.py:173-182 (consistent system), :189-195, :197-207, :209-221,
   :235-246 (extra_iters plateau), :248-256 (bitwise determinism), :258-264
@@ -299,3 +301,30 @@ def test_backward_error_device_matches_oracle(pkg, orc):
         dev(np.eye(3), np.ones(3), np.zeros(3))
     with pytest.raises(ValueError):
         dev(np.ones((11, 2)), np.ones(11), np.ones(2), max_m=10)
+
+
+def test_c09_stopping_rule_agrees_with_reference(pkg, orc):
+    """test_acceptance.py:243-274 (a known red of the reference: at kappa =
+    1e1, beta = 1e-3 the rule needs more than 50 iterations): on the 12-case
+    grid the device path stops for the same reason as the oracle, within
+    max(3, 15 %) iterations of it, the same corners fire within 50 iterations,
+    and where the rule fired the final FE is within 2x the oracle's."""
+    red = []
+    for kappa in (1e1, 1e10):
+        for beta in (1e-12, 1e-3):
+            for seed in SEEDS:
+                p = pkg.gen_randsvd(4000, 50, kappa, beta, seed)
+                res = _solve(pkg, p, d=1000, max_iters=100, rng_seed=seed)
+                _, tr = orc.iterative_sketching(p.a, p.b, orc.Config(d=1000, max_iters=100, rng_seed=seed), p.truth)
+                it_ref = len(tr.iterates) - 1
+                assert res.trace.stop_reason == tr.stop_reason, (kappa, beta, seed)
+                assert abs(res.iterations - it_ref) <= max(3, 0.15 * it_ref), (kappa, beta, seed, res.iterations, it_ref)
+                within = res.trace.stop_reason == "stopped_by_rule" and res.iterations <= 50
+                within_ref = tr.stop_reason == "stopped_by_rule" and it_ref <= 50
+                assert within == within_ref, (kappa, beta, seed, res.iterations, it_ref)
+                if not within:
+                    red.append((kappa, beta, seed, res.iterations, it_ref))
+                if res.trace.stop_reason == "stopped_by_rule":
+                    assert res.trace.fe[-1] <= 2 * tr.fe[-1], (kappa, beta, seed, res.trace.fe[-1], tr.fe[-1])
+    print(f"[C09] corners past 50 iterations (device, oracle): {red}")
+    assert all(k == 1e1 and b == 1e-3 for k, b, *_ in red)
