@@ -8,6 +8,7 @@ tests/test_oracle_pin.py (tests/golden/theory.npz).
   C01  test_acceptance.py:58-74    FE/RE within 10x of QR on the 12-case grid
   C02  test_acceptance.py:77-95    geometric rate <= g_IS(eps) + 0.05, Thm bound
   C03  test_acceptance.py:98-114   sketch-and-solve quality (Fact 2.4), 100 seeds
+  C06  test_acceptance.py:164-200  sketch-and-precondition vs iterative sketching (start vector, iterations to the QR level)
   C07  test_acceptance.py:203-216  backward-error dichotomy (and the device BE vs the oracle's)
   C08  test_acceptance.py:219-240  damped / momentum rates and final FE
   C09  test_acceptance.py:243-274  stopping rule: the same corners fire, same reasons / iterations as the oracle
@@ -328,3 +329,28 @@ def test_c09_stopping_rule_agrees_with_reference(pkg, orc):
                     assert res.trace.fe[-1] <= 2 * tr.fe[-1], (kappa, beta, seed, res.trace.fe[-1], tr.fe[-1])
     print(f"[C09] corners past 50 iterations (device, oracle): {red}")
     assert all(k == 1e1 and b == 1e-3 for k, b, *_ in red)
+
+
+def test_c06_sketch_and_precondition(pkg, orc):
+    """test_acceptance.py:164-200: with a zero start sketch-and-precondition
+    stalls above 10x the QR forward error, with the sketch-and-solve start it
+    reaches it; momentum and S&P reach the QR level at least 1.5x sooner than
+    basic iterative sketching (4000 x 50, kappa 1e10, beta 1e-6, d = 1000)."""
+    p = pkg.gen_randsvd(4000, 50, 1e10, 1e-6, 0)
+    t = pkg.Truth(x=p.truth.x, r=p.truth.r, kappa=p.truth.kappa, beta=p.truth.beta)
+    fe_qr, _ = _rel_errors(p, orc.qr_solve(p.a, p.b))
+    d = 20 * 50
+    zero = pkg.sketch_and_precondition(p.a, p.b, pkg.SolverConfig(d=d, init="zero", max_iters=120), t)
+    ss = pkg.sketch_and_precondition(p.a, p.b, pkg.SolverConfig(d=d, init="sketch_and_solve", max_iters=120), t)
+    basic = pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=d, max_iters=120), t)
+    mom = pkg.iterative_sketching(p.a, p.b, pkg.SolverConfig(d=d, variant="momentum", max_iters=120), t)
+
+    def first_at_qr_level(trace):
+        return next((i for i, fe in enumerate(trace.fe) if fe <= 10 * fe_qr), None)
+
+    it_basic, it_mom, it_sp = (first_at_qr_level(r.trace) for r in (basic, mom, ss))
+    print(f"[C06] zero-init FE {zero.trace.fe[-1]:.2g} vs 10*QR {10 * fe_qr:.2g}; ss-init FE {ss.trace.fe[-1]:.2g}; "
+          f"iterations to the QR level: basic {it_basic}, momentum {it_mom}, S&P {it_sp}")
+    assert zero.trace.fe[-1] >= 10 * fe_qr and ss.trace.fe[-1] <= 10 * fe_qr
+    assert None not in (it_basic, it_mom, it_sp)
+    assert it_basic >= 1.5 * it_mom and it_basic >= 1.5 * it_sp
