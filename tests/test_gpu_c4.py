@@ -101,6 +101,17 @@ def test_c4_full_size_parity(pkg):
     b_h, r_h = p.b.cpu().numpy(), p.truth.r.cpu().numpy()
     torch.cuda.synchronize()
     x_true = p.truth.x
+    # S·[A | b] of the full instance (the streamed window sweep at its headline
+    # size): a column subset, b included, bitwise equal to the oracle's
+    # sequential sum over the same 4e6 rows
+    s = pkg.sparse_sign_new(D, M, 8, 0)
+    w = s.apply_dense(p.a, p.b)
+    cols = [0, 1, 999, 1000, N - 1]
+    sub = np.column_stack([a_h.numpy()[:, cols], b_h])
+    pat = orc.Pattern(d=D, m=M, zeta=8, rows=np.asarray(s.rows).astype(np.int64),
+                      signs=np.asarray(s.signs).astype(np.float64), scale=s.scale)
+    assert np.array_equal(w[:, cols + [N]].cpu().numpy(), orc.sketch_apply(pat, sub))
+    del s, w, pat, sub
     del p
     torch.cuda.empty_cache()
     otruth = orc.Truth(x=x_true, r=r_h, kappa=KAPPA, beta=BETA)
