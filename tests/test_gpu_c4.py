@@ -138,3 +138,65 @@ def test_c4_full_size_parity(pkg):
     assert tr.stop_reason == "stopped_by_rule" and 15 <= res.iterations <= 22, (tr.stop_reason, res.iterations)
     assert (tr_ref.stop_reason == "max_iters" and ref_iters == 50) or (
         tr_ref.stop_reason == "stopped_by_rule" and ref_iters >= res.iterations - 2), (tr_ref.stop_reason, ref_iters)
+
+
+def test_c4_pass_full_size(pkg):
+    """The fused pass (itsk_fused_pass: r = b - A x, c = A'r, the four norms)
+    at the C4 shape, 4e6 x 2000 = 64 GB, against a float64 row-block
+    computation on the same device bytes (torch addmv), and the exact
+    property of a zero iterate: r == b bitwise, c = A'b, ||r||^2 = ||b||^2."""
+    import ctypes
+
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    dev = dv.current_device()
+    g = torch.Generator(device=dev).manual_seed(4)
+    a = torch.randn(M, N, dtype=torch.float64, device=dev, generator=g)
+    b = torch.randn(M, dtype=torch.float64, device=dev, generator=g)
+    x = torch.randn(N, dtype=torch.float64, device=dev, generator=g)
+    r_prev = torch.randn(M, dtype=torch.float64, device=dev, generator=g)
+    r_true = torch.randn(M, dtype=torch.float64, device=dev, generator=g)
+    lib = dv.lib(dev)
+    nb = ctypes.c_int64()
+    _lib.check(lib.itsk_pass_workspace(M, N, ctypes.byref(nb)))
+    ws = dv.workspace(nb.value, dev)
+    r_out = torch.empty(M, dtype=torch.float64, device=dev)
+    cs = torch.empty(N + 8, dtype=torch.float64, device=dev)
+
+    def run(xv):
+        _lib.check(lib.itsk_fused_pass(dv.ptr(a), M, N, N, dv.ptr(b), dv.ptr(xv), dv.ptr(r_prev), dv.ptr(r_out),
+                                       dv.ptr(r_true), dv.ptr(cs), dv.ptr(ws), ws.numel(), dv.stream_ptr()))
+        torch.cuda.synchronize()
+        return r_out.clone(), cs.clone()
+
+    def blocked(rv_from_x):
+        blk = 1 << 18
+        r = torch.empty(M, dtype=torch.float64, device=dev)
+        c = torch.zeros(N, dtype=torch.float64, device=dev)
+        cabs = torch.zeros(N, dtype=torch.float64, device=dev)
+        for i in range(0, M, blk):
+            torch.addmv(b[i:i + blk], a[i:i + blk], rv_from_x, alpha=-1.0, out=r[i:i + blk])
+            c.addmv_(a[i:i + blk].T, r[i:i + blk])
+            cabs.addmv_(a[i:i + blk].abs().T, r[i:i + blk].abs())
+        return r, c, cabs
+
+    r, got = run(x)
+    r_ref, c_ref, cabs = blocked(x)
+    # |r - r_ref| <= ~ n u |a|'|x| per row: normwise over the 4e6 rows
+    xa = float(torch.linalg.vector_norm(x)) * (N ** 0.5)
+    assert float((r - r_ref).abs().max()) <= 50 * N * U * xa
+    assert float(torch.linalg.vector_norm(got[:N] - c_ref)) <= 1e-12 * float(torch.linalg.vector_norm(cabs))
+    assert float(got[N]) == pytest.approx(float(r_ref @ r_ref), rel=1e-12)
+    assert float(got[N + 1]) == pytest.approx(float((r_ref - r_prev) @ (r_ref - r_prev)), rel=1e-12)
+    assert float(got[N + 2]) == pytest.approx(float((r_true - r_ref) @ (r_true - r_ref)), rel=1e-12)
+    assert float(got[N + 3]) == pytest.approx(float(b @ b), rel=1e-12)
+    # zero iterate: every dot is exactly zero
+    r0, got0 = run(torch.zeros(N, dtype=torch.float64, device=dev))
+    assert torch.equal(r0, b)
+    _, c0, cabs0 = blocked(torch.zeros(N, dtype=torch.float64, device=dev))
+    assert float(torch.linalg.vector_norm(got0[:N] - c0)) <= 1e-12 * float(torch.linalg.vector_norm(cabs0))
+    assert float(got0[N]) == pytest.approx(float(b @ b), rel=1e-12)
+    # bitwise repeatable (fixed reduction order)
+    r1, got1 = run(x)
+    assert torch.equal(r1, r) and torch.equal(got1[:N + 4], got[:N + 4])
