@@ -229,7 +229,9 @@ def test_pattern_argument_errors(pkg):
                                       (300, 33, 5), (64, 64, 6), (5000, 500, 7),
                                       # two-level blocking (n >= 384: outer blocks of 128 with a far
                                       # update): block-aligned, ragged last block, the C4 panel width
-                                      (3000, 384, 8), (4100, 641, 9), (14000, 1000, 10), (16500, 1100, 11)])
+                                      (3000, 384, 8), (4100, 641, 9), (14000, 1000, 10), (16500, 1100, 11),
+                                      # the C4 sketch's own shape (d = 24000, n = 2000)
+                                      (24000, 2000, 12)])
 def test_qr_matches_lapack(pkg, orc, m, n, seed):
     rng = np.random.default_rng(seed)
     a = rng.standard_normal((m, n))
