@@ -11,6 +11,7 @@
 // column n of the output (apply_vec is the same sum, solvers.py:208).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "itsk_common.cuh"
 
@@ -63,40 +64,50 @@ __global__ void __launch_bounds__(128) k_sketch_gather(
   uint32_t e0 = ptr[i], e1 = ptr[i + 1];
   if (rg.j0 > 0) e0 = lower_src(src, e0, e1, rg.j0);
   if (rg.j1 != 0xffffffffu) e1 = lower_src(src, e0, e1, rg.j1);
-  for (uint32_t e = e0; e < e1; e += 32) {
-    const uint32_t mine = (e + lane < e1) ? src[e + lane] : 0u;
-    const int cnt = static_cast<int>(min(32u, e1 - e));
-    int k = 0;
-    for (; k + UNR <= cnt; k += UNR) {
-      double v[UNR][CPL];
-      double sv[UNR];
+  // source row x leading dimension as one 32 x 32 -> 64 multiply-add (the
+  // entry point requires lda < 2^31); a block of columns that lies inside A
+  // (block-uniform) loads without the per-column kind tests
+  const uint32_t lda32 = static_cast<uint32_t>(lda);
+  const bool interior = c0 + 32 * CPL <= n;
+  auto sweep = [&](auto inner) {
+    constexpr bool IN = decltype(inner)::value;
+    for (uint32_t e = e0; e < e1; e += 32) {
+      const uint32_t mine = (e + lane < e1) ? src[e + lane] : 0u;
+      const int cnt = static_cast<int>(min(32u, e1 - e));
+      int k = 0;
+      for (; k + UNR <= cnt; k += UNR) {
+        double v[UNR][CPL];
+        double sv[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const uint32_t s = __shfl_sync(FULL, mine, k + u);
-        const int64_t j = s & 0x7fffffffu;
-        sv[u] = (s >> 31) ? -scale : scale;
-        const double* arow = Ac + j * lda;
+        for (int u = 0; u < UNR; ++u) {
+          const uint32_t s = __shfl_sync(FULL, mine, k + u);
+          const uint32_t j = s & 0x7fffffffu;
+          sv[u] = (s >> 31) ? -scale : scale;
+          const double* arow = Ac + static_cast<uint64_t>(j) * lda32;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
-          v[u][q] = kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0);
+          for (int q = 0; q < CPL; ++q)
+            v[u][q] = IN ? arow[32 * q] : (kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0));
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], v[u][q]));
       }
+      for (; k < cnt; ++k) {
+        const uint32_t s = __shfl_sync(FULL, mine, k);
+        const uint32_t j = s & 0x7fffffffu;
+        const double svk = (s >> 31) ? -scale : scale;
+        const double* arow = Ac + static_cast<uint64_t>(j) * lda32;
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], v[u][q]));
-    }
-    for (; k < cnt; ++k) {
-      const uint32_t s = __shfl_sync(FULL, mine, k);
-      const int64_t j = s & 0x7fffffffu;
-      const double svk = (s >> 31) ? -scale : scale;
-      const double* arow = Ac + j * lda;
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        const double a = kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0);
-        acc[q] = __dadd_rn(acc[q], __dmul_rn(svk, a));
+        for (int q = 0; q < CPL; ++q) {
+          const double a = IN ? arow[32 * q] : (kind[q] == 0 ? arow[32 * q] : (kind[q] == 1 ? b[j] : 0.0));
+          acc[q] = __dadd_rn(acc[q], __dmul_rn(svk, a));
+        }
       }
     }
-  }
+  };
+  if (interior) sweep(std::true_type{});
+  else sweep(std::false_type{});
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
     const int64_t col = c0 + lane + 32 * q;
@@ -427,7 +438,9 @@ __global__ void __launch_bounds__(32 * RG_WARPS) k_sketch_ring(
   const int64_t col = static_cast<int64_t>(blockIdx.y) * 32 + lane;
   const int kind = col < n ? 0 : (col == n && b ? 1 : 2);
   const double* base = kind == 0 ? A + col : (kind == 1 ? b : A);
-  const int64_t stride = kind == 0 ? lda : (kind == 1 ? 1 : 0);
+  // 32-bit stride (the entry point requires lda < 2^31): source row x stride
+  // is one wide multiply-add instead of a 64 x 64 product
+  const uint32_t stride = kind == 0 ? static_cast<uint32_t>(lda) : (kind == 1 ? 1u : 0u);
   double acc = (rg.accum && col < ncol) ? W[i * ldw + col] : 0.0;
   uint32_t e0 = ptr[i], e1 = ptr[i + 1];
   if (rg.j0 > 0) e0 = lower_src(src, e0, e1, rg.j0);
@@ -435,6 +448,7 @@ __global__ void __launch_bounds__(32 * RG_WARPS) k_sketch_ring(
   const uint32_t total = e1 - e0;
   const uint32_t ngroups = (total + RG_G - 1) / RG_G;
   double* my = ring + lane;
+  const uint32_t my_s = smem_u32(my);
   // issue side: src words of the 32-block holding the next group, and the block after
   uint32_t blk = 0;
   uint32_t wcur = lane < total ? __ldg(src + e0 + lane) : 0u;
@@ -447,12 +461,26 @@ __global__ void __launch_bounds__(32 * RG_WARPS) k_sketch_ring(
       const uint32_t qn = (blk + 1) * 32 + lane;
       wnxt = qn < total ? __ldg(src + e0 + qn) : 0u;
     }
+    // (a group never straddles a ring wrap or a 32-block: RG_G divides both)
+    const uint32_t dst0 = my_s + (q0 % RG_DEPTH) * 256u;
+    const int nbytes = kind != 2 ? 8 : 0;  // 0: zero-fill
+    if (q0 + RG_G <= total) {  // full group (uniform): no per-source predicates
 #pragma unroll
-    for (int u = 0; u < RG_G; ++u) {
-      const uint32_t q = q0 + u;
-      const uint32_t w = __shfl_sync(FULL, wcur, (q0 & 31) + u);
-      if (q < total) cp_async8_ring(my + (q % RG_DEPTH) * 32, base + static_cast<int64_t>(w & 0x7fffffffu) * stride,
-                                    kind != 2);
+      for (int u = 0; u < RG_G; ++u) {
+        const uint32_t w = __shfl_sync(FULL, wcur, (q0 & 31) + u);
+        const double* sp = base + static_cast<uint64_t>(w & 0x7fffffffu) * stride;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst0 + 256u * u), "l"(sp), "r"(nbytes)
+                     : "memory");
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RG_G; ++u) {
+        const uint32_t w = __shfl_sync(FULL, wcur, (q0 & 31) + u);
+        const double* sp = base + static_cast<uint64_t>(w & 0x7fffffffu) * stride;
+        if (q0 + u < total)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst0 + 256u * u), "l"(sp), "r"(nbytes)
+                       : "memory");
+      }
     }
     const uint32_t wv = __shfl_sync(FULL, wcur, (q0 & 31) + (lane & (RG_G - 1)));
     if (lane < RG_G) rsrc[(q0 + lane) % RG_DEPTH] = wv;
@@ -466,16 +494,28 @@ __global__ void __launch_bounds__(32 * RG_WARPS) k_sketch_ring(
     __syncwarp();  // rsrc entries written by other lanes
     double v[RG_G];
     uint32_t sw[RG_G];
+    const uint32_t s0 = (g * RG_G) % RG_DEPTH;
 #pragma unroll
     for (int u = 0; u < RG_G; ++u) {
-      const uint32_t q = g * RG_G + u;
-      sw[u] = rsrc[q % RG_DEPTH];
-      v[u] = my[(q % RG_DEPTH) * 32];
+      sw[u] = rsrc[s0 + u];
+      v[u] = my[(s0 + u) * 32];
     }
+    // fl(-scale * v) = fl(scale * -v): the sign goes into the operand's sign
+    // bit (one logic op) instead of selecting +-scale
+    if ((g + 1) * RG_G <= total) {
 #pragma unroll
-    for (int u = 0; u < RG_G; ++u) {
-      const uint32_t q = g * RG_G + u;
-      if (q < total) acc = __dadd_rn(acc, __dmul_rn((sw[u] >> 31) ? -scale : scale, v[u]));
+      for (int u = 0; u < RG_G; ++u) {
+        const double vs = __hiloint2double(__double2hiint(v[u]) ^ static_cast<int>(sw[u] & 0x80000000u),
+                                           __double2loint(v[u]));
+        acc = __dadd_rn(acc, __dmul_rn(scale, vs));
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RG_G; ++u) {
+        const double vs = __hiloint2double(__double2hiint(v[u]) ^ static_cast<int>(sw[u] & 0x80000000u),
+                                           __double2loint(v[u]));
+        if (g * RG_G + u < total) acc = __dadd_rn(acc, __dmul_rn(scale, vs));
+      }
     }
     __syncwarp();  // every lane has read the group's rsrc slots before they are rewritten
     // the slots just read are free: refill them with group g + RG_NG
@@ -553,7 +593,7 @@ extern "C" int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t l
   rg.j0 = static_cast<uint32_t>(row0);
   rg.j1 = row1 >= m ? 0xffffffffu : static_cast<uint32_t>(row1);
   rg.accum = accumulate ? 1 : 0;
-  ITSK_REQUIRE(lda >= n && ldw >= n + (b ? 1 : 0), "bad leading dimension");
+  ITSK_REQUIRE(lda >= n && ldw >= n + (b ? 1 : 0) && lda < (1ll << 31), "bad leading dimension");
   ITSK_REQUIRE(sk_ptr && sk_src && SAb && (A || n == 0), "null pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // scale = 1/sqrt(zeta) exactly as embed.py:92 (correctly rounded sqrt, div)
