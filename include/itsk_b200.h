@@ -87,6 +87,7 @@ int itsk_pattern_csr(const uint32_t* rows, const uint8_t* neg, int64_t m, int64_
  * rounded before the add), so SAb is bitwise identical to scipy's.
  * For a row shard (multi-GPU) pass the shard's rows and its own CSR
  * (itsk_pattern_csr); the per-rank partial sketches are then summed.
+ * m < 2^31 and n <= lda < 2^31 (ITSK_EINVAL otherwise).
  * -------------------------------------------------------------------- */
 int itsk_sketch(const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                 const uint32_t* sk_ptr, const uint32_t* sk_src, int64_t d, int64_t zeta,
