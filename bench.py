@@ -604,7 +604,7 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--variant", default=None, choices=["basic", "damped", "momentum"])
     ap.add_argument("--sharded", action="store_true",
-                    help="run the row-sharded (multi-GPU) path even with one rank (under torchrun)")
+                    help="run the row-sharded (multi-GPU) path even with one rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-numpy e2e measurement")
     ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
@@ -615,8 +615,8 @@ def main():
         ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args)
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return relaunch_under_torchrun(args)
+    if (args.gpus > 1 or args.sharded) and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)  # --sharded with one rank also needs the rendezvous environment
     if args.probe_launch:
         return probe_launch(args)
     return run_b200(args)

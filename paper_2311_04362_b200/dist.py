@@ -125,6 +125,18 @@ class PeerExchange:
 
 
 _PEERS: dict = {}
+# the process groups behind _PEERS' keys, kept referenced: a key holds the
+# group's id(), which must not be reused by a later group with other members
+# (a re-initialised default group is a new object and gets its own exchange)
+_PEER_GROUPS: dict = {}
+
+
+def _peer_key(group, dev, n: int, world: int) -> tuple:
+    import torch.distributed as tdist
+
+    g = group if group is not None else tdist.group.WORLD
+    _PEER_GROUPS[id(g)] = g
+    return (id(g), dev.index, n, world)
 # why the peer exchange is unavailable, per _PEERS key (reported by the
 # result's `peer_fallback` and by bench.py's `loop_exchange`)
 PEER_FALLBACK: dict = {}
@@ -139,7 +151,7 @@ def peer_exchange(n: int, dev, group=None, require: bool = False) -> PeerExchang
 
     world = tdist.get_world_size(group)
     rank = tdist.get_rank(group)
-    key = (id(group), dev.index, n, world)
+    key = _peer_key(group, dev, n, world)
     if key in _PEERS:
         if _PEERS[key] is None and require:
             raise RuntimeError(f"peer exchange unavailable: {PEER_FALLBACK.get(key)}")
@@ -326,7 +338,7 @@ def iterative_sketching_sharded(a_local, b_local, cfg: SolverConfig, m_total: in
     fallback = None
     if px is None:
         fallback = ("peer='nccl'" if peer == "nccl" else "sparse block" if csr is not None else
-                    PEER_FALLBACK.get((id(group), ws.dev.index, n, tdist.get_world_size(group)), "unavailable"))
+                    PEER_FALLBACK.get(_peer_key(group, ws.dev, n, tdist.get_world_size(group)), "unavailable"))
     # deferred estimates: with the peer exchange the ready bits travel with
     # the partials (every rank evaluates the rule at the same iteration); the
     # host-collective loop polls `done` between collectives, so over several

@@ -53,3 +53,16 @@ def test_world_size_must_match_gpus():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c1"],
                          capture_output=True, text=True, env=env, cwd=ROOT, timeout=300)
     assert out.returncode != 0 and "WORLD_SIZE=1" in (out.stderr + out.stdout)
+
+
+def test_sharded_one_rank_gets_the_rendezvous_environment():
+    """--sharded with one GPU outside torchrun re-launches itself as one rank
+    (the sharded path needs RANK / WORLD_SIZE / MASTER_* for its process group)."""
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--sharded", "--probe-launch"],
+                         capture_output=True, text=True, env=env, cwd=ROOT, timeout=300)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert lines == [{"probe": "launch", "world": 1, "gpus": 1, "rank_sum": 1.0}]
