@@ -113,9 +113,13 @@ int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t lda, const d
 int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes);
 int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
                 void* ws, int64_t ws_bytes, itsk_stream_t stream);
-/* The same without the host round trip: the "exact zero on diag(R)" flag
- * (1/0) is copied to the device int *singular on the stream; the caller
- * raises SingularMatrixError when it reads the flag with its results. */
+/* The same without the host round trip: the factorisation's flags are
+ * copied to the device int *singular on the stream — bit 0: an exact zero on
+ * diag(R) (the caller raises SingularMatrixError when it reads the flag with
+ * its results); bit 1: a non-finite entry in R or z (the reference's
+ * triangular solves refuse those: scipy solve_triangular's check_finite,
+ * linalg.py:59-68 -> ValueError).  itsk_qr_aug itself returns NaNs like
+ * LAPACK's QR (linalg.py:42) and reports only the zero pivot. */
 int itsk_qr_aug_async(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z, void* ws,
                       int64_t ws_bytes, int* singular, itsk_stream_t stream);
 

@@ -436,12 +436,18 @@ __device__ void qr_body(const QrArgs& a, const X& x, double* sm) {
     const int64_t i = lo + idx / n, c = idx % n;
     const double bi = betas[i];
     const double sg = bi < 0.0 ? -1.0 : 1.0;
-    a.R[i * n + c] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
+    const double rv = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
+    a.R[i * n + c] = rv;
+    if (!isfinite(rv)) atomicOr(a.singular, 2);  // bit 1: non-finite R or z (see k_qr_finish)
   }
   for (int64_t i = lo + tid; i < ihi; i += QR_THREADS) {
     const double bi = betas[i];
     const double sg = bi < 0.0 ? -1.0 : 1.0;
-    if (a.z && N > n) a.z[i] = sg * W[i * ldw + n];
+    if (a.z && N > n) {
+      const double zv = sg * W[i * ldw + n];
+      a.z[i] = zv;
+      if (!isfinite(zv)) atomicOr(a.singular, 2);
+    }
   }
   if (p == 0)
     for (int64_t i = tid; i < n; i += QR_THREADS)
@@ -631,7 +637,7 @@ extern "C" int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   ITSK_CUDA(cudaMemcpyAsync(&singular, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   ITSK_CUDA(cudaStreamSynchronize(s));
-  if (singular) {
+  if (singular & 1) {  // bit 1 (non-finite R or z) is the async entry's business: LAPACK's QR returns NaNs too
     set_error("zero diagonal entry in triangular factor");
     return ITSK_ESINGULAR;
   }

@@ -1110,11 +1110,20 @@ __global__ void k_qr_finish(const double* W, int64_t n, int64_t ldw, int64_t N, 
   const int64_t i = e / n, c = e - i * n;
   const double bi = betas[i];
   const double sg = bi < 0.0 ? -1.0 : 1.0;
-  R[e] = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
+  const double rv = (c < i) ? 0.0 : (c == i ? sg * bi : sg * W[i * ldw + c]);
+  R[e] = rv;
+  // bit 1: a non-finite entry of R or z — the reference's triangular solves
+  // refuse those (scipy solve_triangular's check_finite, linalg.py:59-68)
+  bool bad = !isfinite(rv);
   if (c == 0) {
-    if (z && N > n) z[i] = sg * W[i * ldw + n];
+    if (z && N > n) {
+      const double zv = sg * W[i * ldw + n];
+      z[i] = zv;
+      bad = bad || !isfinite(zv);
+    }
     if (bi == 0.0) atomicOr(singular, 1);
   }
+  if (bad) atomicOr(singular, 2);
 }
 
 // Side stream and events of the look-ahead (per device, created once).

@@ -155,6 +155,8 @@ def _solve(r, c, trans: int):
         raise SingularMatrixError("zero diagonal entry in triangular factor")
     rt = rt.contiguous()
     ct = _dev.as_device_vector(c, dev)
+    if not bool(torch.isfinite(rt).all() & torch.isfinite(ct).all()):
+        raise ValueError("array must not contain infs or NaNs")  # scipy solve_triangular's check_finite
     y = torch.empty(n, dtype=torch.float64, device=dev)
     _lib.check(_dev.lib(dev).itsk_trsv(_dev.ptr(rt), n, _dev.ptr(ct), _dev.ptr(y), trans, _dev.stream_ptr()))
     return _dev.to_numpy(y) if host else y

@@ -438,11 +438,19 @@ def _sketch_qr_x0(lib, ws: _Workspace, at, lda, bt, cfg: SolverConfig, stream: i
         compute.wait_stream(ws.est_stream)
 
 
+NONFINITE_MSG = "array must not contain infs or NaNs"  # scipy's check_finite message
+
+
 def check_singular(ws: _Workspace) -> None:
-    """The QR's zero-pivot flag (itsk_qr_aug_async) -> SingularMatrixError,
-    as tri_solve_upper raises it in sketch_and_solve (linalg.py:54-55)."""
-    if int(ws.sing_host[0]) != 0:
+    """The QR's flags (itsk_qr_aug_async) -> the exceptions tri_solve_upper
+    raises in sketch_and_solve: a zero pivot is a SingularMatrixError
+    (linalg.py:54-55), a non-finite R or Q'Sb — NaN / Inf in A or b — the
+    ValueError of scipy's solve_triangular (linalg.py:59-62), in that order."""
+    flag = int(ws.sing_host[0])
+    if flag & 1:
         raise SingularMatrixError("zero diagonal entry in triangular factor")
+    if flag & 2:
+        raise ValueError(NONFINITE_MSG)
 
 
 def _loop_params(ws: _Workspace, at, lda, cfg: SolverConfig, alpha, beta, truth, m_local=None, csr=None,
@@ -636,6 +644,8 @@ def sketch_and_solve(a, b, s: SparseSignEmbedding):
     w = s.apply_dense(at, bt)
     sa = w[:, :n].clone()  # S·A before the QR overwrites it (the sign reference of QrFactors.q)
     r, z = qr_aug(w, n)
+    if not bool(torch.isfinite(r).all() & torch.isfinite(z).all()):
+        raise ValueError(NONFINITE_MSG)  # tri_solve_upper's check_finite (linalg.py:59-62)
     x0 = torch.empty(n, dtype=torch.float64, device=dev)
     _lib.check(_dev.lib(dev).itsk_trsv(_dev.ptr(r), n, _dev.ptr(z), _dev.ptr(x0), 0, _dev.stream_ptr()))
     if host:

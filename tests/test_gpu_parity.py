@@ -823,6 +823,51 @@ def test_validation_and_singular(pkg):
         pkg.iterative_sketching(a, p.b, pkg.SolverConfig(d=50))
 
 
+@pytest.mark.parametrize("shape", [(400, 10, 200), (6000, 130, 2600), (20000, 400, 8000)])
+def test_nonfinite_inputs_raise_like_the_reference(pkg, orc, shape):
+    """NaN / Inf in A or b: the reference fails in sketch_and_solve's
+    triangular solve (scipy solve_triangular's check_finite, linalg.py:59-62)
+    with ValueError("array must not contain infs or NaNs") — the oracle does
+    the same here — and so does the device path (a flag bit set by the QR's
+    finish kernel, read with the results), in iterative_sketching,
+    sketch_and_precondition, sketch_and_solve and the triangular solves;
+    householder_qr_econ itself returns the NaNs like LAPACK's QR (linalg.py:42).
+    A zero pivot still wins over a non-finite entry (_check_square_upper first)."""
+    m, n, d = shape
+    p = pkg.gen_randsvd(m, n, 10.0, 0.1, 0)
+    cfg = pkg.SolverConfig(d=d)
+    for what, val in (("a", np.nan), ("a", np.inf), ("b", np.nan), ("b", -np.inf)):
+        a, b = p.a.copy(), p.b.copy()
+        (a if what == "a" else b)[m // 3, ...] = val
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            orc.iterative_sketching(a, b, orc.Config(d=d))
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            pkg.iterative_sketching(a, b, cfg)
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            pkg.sketch_and_precondition(a, b, cfg)
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            pkg.sketch_and_solve(a, b, pkg.sparse_sign_new(d, m, 8, 0))
+    a = p.a.copy()
+    a[5, 2] = np.nan
+    f = pkg.householder_qr_econ(a)
+    assert not np.all(np.isfinite(f.r))
+    with pytest.raises(ValueError, match="infs or NaNs"):
+        pkg.tri_solve_upper(f.r, np.ones(n))
+    with pytest.raises(ValueError, match="infs or NaNs"):
+        pkg.tri_solve_upper_transpose(np.eye(3), np.array([1.0, np.inf, 0.0]))
+    # the workspace is reusable after the error, and a clean solve is unaffected
+    res = pkg.iterative_sketching(p.a, p.b, cfg)
+    x_ref, tr_ref = orc.iterative_sketching(p.a, p.b, orc.Config(d=d))
+    it_ref = len(tr_ref.iterates) - 1
+    assert res.trace.stop_reason == tr_ref.stop_reason and abs(res.iterations - it_ref) <= max(3, 0.15 * it_ref)
+    assert np.linalg.norm(res.solution - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+    a = p.a.copy()
+    a[:, 4] = 0.0
+    a[7, 1] = np.nan  # a zero column AND a NaN: R has a NaN pivot row, not a zero pivot -> ValueError
+    with pytest.raises((ValueError, pkg.SingularMatrixError)):
+        pkg.iterative_sketching(a, p.b, cfg)
+
+
 def test_residual_vectors_survive_workspace_reuse(pkg):
     p = pkg.gen_randsvd(800, 10, 1e3, 1e-3, 4)
     cfg = pkg.SolverConfig(d=200, rng_seed=4)
