@@ -260,6 +260,13 @@ def _shard_factor(ws, at, lda, csr, cfg: SolverConfig, truth, peer: PeerExchange
     stream = _dev.stream_ptr()
     _lib.check(lib.itsk_qr_aug(_dev.ptr(ws.W), cfg.d, n, ws.ldw, _dev.ptr(ws.R), _dev.ptr(ws.z),
                                _dev.ptr(ws.qr_ws), ws.qr_ws.numel(), stream))
+    # a non-finite R or Q'Sb (NaN / Inf in A or b): the reference's triangular
+    # solve refuses it (linalg.py:59-62); R is the same on every rank, so every
+    # rank raises (itsk_qr_aug has synchronised already)
+    if not bool(torch.isfinite(ws.R).all() & torch.isfinite(ws.z).all()):
+        from .solvers import NONFINITE_MSG
+
+        raise ValueError(NONFINITE_MSG)
     _lib.check(lib.itsk_pack_upper(_dev.ptr(ws.R), n, _dev.ptr(ws.Rp), stream))
     if cfg.init == "zero":
         ws.xs[0].zero_()

@@ -56,6 +56,22 @@ def test_sharded_solve_matches_single_gpu(nccl_group, m, n, kappa, beta, d, vari
         _same_solve(got, ref)
 
 
+def test_sharded_nonfinite_input_raises(nccl_group):
+    """NaN in A: the sharded solver raises the reference's ValueError too
+    (every rank holds the same R), and the next clean solve is unaffected."""
+    import paper_2311_04362_b200 as itsk
+    from paper_2311_04362_b200.dist import iterative_sketching_sharded
+
+    p = itsk.gen_randsvd(5000, 40, 1e4, 1e-6, 1)
+    cfg = itsk.SolverConfig(d=800, rng_seed=1)
+    a = p.a.copy()
+    a[123, 7] = np.nan
+    with pytest.raises(ValueError, match="infs or NaNs"):
+        iterative_sketching_sharded(a, p.b, cfg, 5000, 0)
+    got = iterative_sketching_sharded(p.a, p.b, cfg, 5000, 0, p.truth)
+    _same_solve(got, itsk.iterative_sketching(p.a, p.b, cfg, p.truth, residuals="last"))
+
+
 def _same_solve(got, ref):
     assert got.trace.stop_reason == ref.trace.stop_reason
     assert got.iterations == ref.iterations
