@@ -1,14 +1,15 @@
-"""A/B of the window-sweep kernel shapes at the C4 sketch shape (same bits):
-    python scripts/sketch_sweep_ab.py [m n d zeta reps] [shape ...]
-shape = ITSK_SKETCH_SWCL value (0: 16 warps x 12 rows, 8 sources/chunk; 2: 64-column
-panels; 5: 32 warps x 6 rows, 4 sources/chunk; 6: 24 warps x 8 rows)."""
+"""A/B of sketch kernel variants at one shape (same bits; the first variant is the bitwise reference):
+    python scripts/sketch_sweep_ab.py [m n d zeta reps] [variant ...]
+variant = an ITSK_SKETCH_SWCL value (0: 128-column panels, 2: 64-column panels) or a comma-separated list of
+NAME=value pairs setting ITSK_SKETCH_<NAME> (SWEEP, SWCL, DRIFT, DIRECT, RING, GCPL, UNR), e.g. "DIRECT=0,SWCL=0".
+Settings persist from one variant to the next: name every knob a comparison depends on."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2311_04362_b200 as itsk
 m, n, d, zeta = (int(v) for v in sys.argv[1:5]) if len(sys.argv) > 4 else (4000000, 2000, 24000, 8)
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 4
-shapes = [v for v in sys.argv[6:]] or ["0", "5", "6"]
+shapes = [v for v in sys.argv[6:]] or ["0", "2"]
 g = torch.Generator(device="cuda").manual_seed(0)
 A = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
 b = torch.randn(m, dtype=torch.float64, device="cuda", generator=g)
