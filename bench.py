@@ -41,6 +41,7 @@ from HBM.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import platform
@@ -471,7 +472,13 @@ def run_b200(args):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+            # outside the timed region: the solution's bytes (every solve of the
+            # same inputs must give the same bits — fixed reduction orders)
+            digests.setdefault(variant, set()).add(
+                hashlib.sha256(np.ascontiguousarray(res.solution).tobytes()).hexdigest())
         return times, res
+
+    digests = {}  # variant -> the distinct solutions seen
 
     for _ in range(args.warmup):
         solve(a_dev, b_dev)
@@ -572,6 +579,8 @@ def run_b200(args):
             "gpu_launches": int(launches),
             "iterations": iters, "stop_reason": res.trace.stop_reason, "fe": fe,
             "passes_per_solve": iters + 1, "instance_s": round(t_gen, 2),
+            # device-resident, pinned and pageable inputs, every timed step: one set of solution bits
+            "solutions_bitwise_equal": all(len(v) == 1 for v in digests.values()),
             "clocks": clk.summary(),
         }
         if variants:
