@@ -179,6 +179,16 @@ def peer_exchange(n: int, dev, group=None, require: bool = False) -> PeerExchang
             raise
         PEER_FALLBACK[key] = f"{type(exc).__name__}: {exc}"[:300]
         px = None
+    # every rank must take the same path: a rank whose setup failed while the
+    # others' succeeded would wait in NCCL for ranks that wait on peer flags
+    if world > 1:
+        ok = torch.tensor([1 if px is not None else 0], dtype=torch.int32, device=dev)
+        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0 and px is not None:
+            PEER_FALLBACK[key] = "the peer exchange could not be set up on another rank"
+            px = None
+            if require:
+                raise RuntimeError(f"peer exchange unavailable: {PEER_FALLBACK[key]}")
     _PEERS[key] = px
     return px
 
