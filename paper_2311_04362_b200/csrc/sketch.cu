@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
   };
   const uint2* my = ord + e0;
   const uint32_t* mysrc = src + e0;
+  const uint32_t lda32 = static_cast<uint32_t>(lda);  // lda < 2^31 (entry point)
   auto entry = [&](uint32_t idx) {
     if constexpr (DIRECT) return make_uint2(__ldg(mysrc + idx), 0u);
     else return my[idx];
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, 1) k_sketch_stream(
       // gate: window wl - drift complete everywhere (never one this warp has
       // not counted itself done with: a chunk may span more than `drift`)
       wait_for(g0 + min(wl - drift, wf - 1));
-      const double* pu = Ap + static_cast<int64_t>(sv & 0x7fffffffu) * lda;  // lane-independent start
+      const double* pu = Ap + static_cast<uint64_t>(sv & 0x7fffffffu) * lda32;  // lane-independent start
       double2 v[U][NV];
       if (allv) {
 #pragma unroll
