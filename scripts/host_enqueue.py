@@ -8,7 +8,7 @@ import paper_2311_04362_b200 as itsk
 from bench import CONFIGS, make_problem
 
 m, n, kappa, beta, d, zeta = CONFIGS["c2"]
-p, _, _ = make_problem("c2", 0, None)
+p, _, _ = make_problem("c2", 0)
 dev = torch.device("cuda")
 at = torch.from_numpy(p.a).to(dev); bt = torch.from_numpy(p.b).to(dev)
 cfg = itsk.SolverConfig(d=d, zeta=zeta)
