@@ -1,3 +1,6 @@
+"""Probe of input forms on the GPU box: Fortran-ordered / strided / row-sliced / float32 / integer A, list b,
+non-contiguous device tensors (all must give the contiguous float64 result bit for bit or to rounding),
+and malformed inputs (wrong length, 1-D A, m < n, NaN).  python scripts/edge_inputs.py"""
 import numpy as np, torch, sys
 sys.path.insert(0, "/root/repo")
 import paper_2311_04362_b200 as itsk
