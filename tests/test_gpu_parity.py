@@ -868,6 +868,36 @@ def test_nonfinite_inputs_raise_like_the_reference(pkg, orc, shape):
         pkg.iterative_sketching(a, p.b, cfg)
 
 
+def test_input_forms(pkg, orc):
+    """np.asarray(a, dtype=float) semantics of the reference's entry point
+    (solvers.py:323-329): Fortran-ordered, column-strided, row-sliced and
+    non-contiguous device inputs and a list b give the contiguous float64
+    solve bit for bit; float32 / integer A are converted like the reference
+    converts them; a wrong-length b and a 1-D A raise ValueError."""
+    a, b, _ = orc.gen_randsvd(4000, 50, 1e6, 1e-6, 0)
+    cfg = pkg.SolverConfig(d=1000)
+    ref = pkg.iterative_sketching(a, b, cfg).solution
+    forms = {
+        "fortran": (np.asfortranarray(a), b),
+        "column-strided": (np.ascontiguousarray(np.hstack([a, a]))[:, :50], b),
+        "row-sliced": (np.vstack([a, a])[:4000], b),
+        "list b": (a, list(b)),
+        "device, non-contiguous": (torch.from_numpy(np.asfortranarray(a)).cuda(), torch.from_numpy(b).cuda()),
+    }
+    for name, (aa, bb) in forms.items():
+        x = pkg.iterative_sketching(aa, bb, cfg).solution
+        x = x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+        assert np.array_equal(x, ref), name
+    for aa in (a.astype(np.float32), np.round(a * 1e3).astype(np.int64)):
+        x = pkg.iterative_sketching(aa, b, cfg).solution
+        x_ref, _ = orc.iterative_sketching(np.asarray(aa, dtype=float), b, orc.Config(d=1000))
+        assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref), aa.dtype
+    with pytest.raises(ValueError):
+        pkg.iterative_sketching(a, b[:-1], cfg)
+    with pytest.raises(ValueError):
+        pkg.iterative_sketching(a[:, 0], b, cfg)
+
+
 def test_residual_vectors_survive_workspace_reuse(pkg):
     p = pkg.gen_randsvd(800, 10, 1e3, 1e-3, 4)
     cfg = pkg.SolverConfig(d=200, rng_seed=4)
