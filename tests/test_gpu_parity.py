@@ -222,6 +222,35 @@ def test_pattern_argument_errors(pkg):
     assert np.all(s.apply_dense(np.zeros((20, 4))) == 0)
 
 
+def test_sketch_c_abi_argument_errors(pkg):
+    """itsk_sketch / itsk_sketch_rows refuse bad arguments with ITSK_EINVAL
+    (-> ValueError) before touching memory: leading dimensions below n or
+    from 2^31, a source-row window outside [0, m], null pointers, m from 2^31."""
+    from paper_2311_04362_b200 import _lib
+    from paper_2311_04362_b200 import device as dv
+
+    dev = dv.current_device()
+    lib = dv.lib(dev)
+    s = pkg.sparse_sign_new(50, 200, 4, 0)
+    a = torch.zeros((200, 8), dtype=torch.float64, device=dev)
+    w = torch.zeros((50, 8), dtype=torch.float64, device=dev)
+    st = dv.stream_ptr()
+    P, S = dv.ptr(s.ptr_dev), dv.ptr(s.src_dev)
+
+    def sketch(m=200, n=8, lda=8, ldw=8, A=dv.ptr(a), W=dv.ptr(w), ptr=P):
+        return lib.itsk_sketch(A, m, n, lda, None, ptr, S, 50, 4, W, ldw, st)
+
+    assert sketch() == _lib.ITSK_OK
+    for kw in ({"lda": 7}, {"lda": 1 << 31}, {"ldw": 7}, {"A": None}, {"W": None}, {"ptr": None}, {"m": 1 << 31},
+               {"m": 0}):
+        with pytest.raises(ValueError):
+            _lib.check(sketch(**kw))
+    for r0, r1 in ((-1, 10), (10, 5), (0, 201)):
+        with pytest.raises(ValueError):
+            _lib.check(lib.itsk_sketch_rows(dv.ptr(a), 200, 8, 8, None, P, S, 50, 4, dv.ptr(w), 8, r0, r1, 0, st))
+    torch.cuda.synchronize()
+
+
 # --------------------------------------------------------------------------
 # QR, triangular solves, estimates
 # --------------------------------------------------------------------------
