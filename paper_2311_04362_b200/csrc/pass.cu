@@ -141,6 +141,116 @@ __global__ void __launch_bounds__(PASS_THREADS) k_pass(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Wide rows (n beyond the staged kernels' 2048 columns, or beyond 1024 at an
+// odd leading dimension): the whole CTA takes one row at a time.  A thread
+// owns the columns tid, tid + 512, ... (coalesced 8-byte loads, the next row
+// in flight under the current one), so the row's elements stay in registers
+// between the dot product and the c update — A is read once — and every
+// column of c has exactly one owner (no CTA-level reduction of c).  One
+// barrier per row (double-buffered warp partials, summed in warp order by
+// every thread).  The per-CTA partials go through k_finalize like k_pass's.
+// ---------------------------------------------------------------------------
+constexpr int WIDE_THREADS = 512;
+constexpr int WIDE_WARPS = WIDE_THREADS / 32;
+
+template <int CPT>
+__global__ void __launch_bounds__(WIDE_THREADS, 1) k_pass_wide(PassArgs a) {
+  __shared__ double red[2][WIDE_WARPS];
+  const double* x;
+  const double* r_prev;
+  double* r_out;
+  if (a.mode == 0) {
+    x = a.x;
+    r_prev = a.r_prev;
+    r_out = a.r_out;
+  } else {
+    const LoopCtl* ctl = a.ctl;
+    if (ctl->result.done) return;
+    const int64_t S = ctl->r_slots;
+    if (a.mode == 1) {
+      const int64_t it = ctl->it;
+      x = a.xs + (it + 1) * a.n;
+      r_prev = a.rs + (it % S) * a.m;
+      r_out = a.rs + ((it + 1) % S) * a.m;
+    } else {
+      x = a.xs;
+      r_prev = nullptr;
+      r_out = a.rs;
+    }
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n, lda = a.lda;
+  double xv[CPT], acc[CPT], av[CPT], an[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int64_t c = tid + WIDE_THREADS * q;
+    xv[q] = c < n ? x[c] : 0.0;
+    acc[q] = 0.0;
+  }
+  double s_rr = 0.0, s_dd = 0.0, s_tt = 0.0, s_bb = 0.0;
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * a.rows_per_cta;
+  const int64_t r_end = min(a.m, r_begin + a.rows_per_cta);
+  const double* b = a.b;
+  const double* r_true = a.r_true;
+  const uint64_t pol = evict_first_policy();
+  auto load_row = [&](int64_t row, double (&v)[CPT]) {
+    const double* arow = a.A + row * lda;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int64_t c = tid + WIDE_THREADS * q;
+      v[q] = (row < r_end && c < n) ? ldg_stream(arow + c, pol) : 0.0;
+    }
+  };
+  load_row(r_begin, av);
+  int buf = 0;
+  for (int64_t row = r_begin; row < r_end; ++row) {
+    load_row(row + 1, an);
+    double dot = 0.0;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) dot = fma(av[q], xv[q], dot);
+    dot = warp_sum(dot);
+    if (lane == 0) red[buf][warp] = dot;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < WIDE_WARPS; ++w) tot += red[buf][w];
+    buf ^= 1;
+    const double bj = b[row];
+    const double r = (a.bscale == 1.0 ? bj : a.bscale * bj) - tot;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      acc[q] = fma(r, av[q], acc[q]);
+      av[q] = an[q];
+    }
+    if (tid == 0) {
+      if (r_out) r_out[row] = r;
+      s_rr += r * r;
+      s_bb += bj * bj;
+      if (r_prev) {
+        const double dd = r - r_prev[row];
+        s_dd += dd * dd;
+      }
+      if (r_true) {
+        const double tt = r_true[row] - r;
+        s_tt += tt * tt;
+      }
+    }
+  }
+  double* out = a.part + static_cast<int64_t>(blockIdx.x) * (n + 4);
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int64_t c = tid + WIDE_THREADS * q;
+    if (c < n) out[c] = acc[q];
+  }
+  if (tid == 0) {
+    out[n] = s_rr;
+    out[n + 1] = s_dd;
+    out[n + 2] = s_tt;
+    out[n + 3] = s_bb;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // TMA-staged variant (sm_100a): one producer warp streams contiguous tiles of
 // T rows (T*lda*8 bytes, one cp.async.bulk each, L2 evict-first) into an
 // S-stage shared-memory ring guarded by mbarriers; 8 consumer warps take rows
@@ -1315,6 +1425,26 @@ int64_t pass_part_doubles(int64_t m, int64_t n) {
   return static_cast<int64_t>(pass_grid(m, n)) * (n + 4);
 }
 
+// rows of more than 1024 columns outside the staged kernels (k_pass_wide)
+int launch_wide(PassArgs a, cudaStream_t s, int* grid_used) {
+  int grid = num_sms() - a.sm_reserve;
+  if (grid < 1) grid = 1;
+  if (grid > a.m) grid = static_cast<int>(a.m);
+  grid = std::min(grid, pass_grid(a.m, a.n));  // the partials buffer is sized for pass_grid CTAs
+  *grid_used = grid;
+  a.rows_per_cta = (a.m + grid - 1) / grid;
+  if (a.n <= 4 * WIDE_THREADS) k_pass_wide<4><<<grid, WIDE_THREADS, 0, s>>>(a);
+  else if (a.n <= 8 * WIDE_THREADS) k_pass_wide<8><<<grid, WIDE_THREADS, 0, s>>>(a);
+  else if (a.n <= 16 * WIDE_THREADS) k_pass_wide<16><<<grid, WIDE_THREADS, 0, s>>>(a);
+  else {
+    set_error("fused pass: n=%lld is beyond the widest row kernel (8192 columns)", (long long)a.n);
+    return ITSK_EINVAL;
+  }
+  count_launch();
+  ITSK_CHECK_LAUNCH();
+  return ITSK_OK;
+}
+
 int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
   if (tma_eligible(a0)) {
     const int grid = tma_grid(a0.m, a0.sm_reserve);
@@ -1347,11 +1477,12 @@ int launch_pass(const PassArgs& a0, cudaStream_t s, int* grid_used) {
     case 16: rc = launch_cpl<16>(a, grid, s); break;
     case 32: rc = launch_cpl<32>(a, grid, s); break;
     default:
-      set_error("fused pass: n=%lld with an odd leading dimension exceeds the register-resident "
-                "row limit (1024)", (long long)a.n);
-      return ITSK_EINVAL;
+      rc = launch_wide(a, s, grid_used);
+      break;
   }
-  if (rc == ITSK_OK && a0.tickets) rc = launch_finalize(a0.part, grid, a0.n, a0.cs, a0.ctl, s);
+  if (rc != ITSK_OK) return rc;
+  const int grid_fin = *grid_used;
+  if (rc == ITSK_OK && a0.tickets) rc = launch_finalize(a0.part, grid_fin, a0.n, a0.cs, a0.ctl, s);
   if (rc == ITSK_OK && a0.peer.size > 0 && a0.ctl) {
     k_peer_send<<<1, 256, 0, s>>>(a0.cs, a0.n, a0.ctl, a0.mode, a0.peer);
     count_launch();

@@ -453,7 +453,9 @@ def test_condest_on_sketch_factor(pkg, orc):
 # fused pass
 # --------------------------------------------------------------------------
 @pytest.mark.parametrize("m,n", [(1000, 1), (999, 7), (5000, 50), (20000, 200), (3001, 257), (4096, 500),
-                                 (2000, 1000), (3000, 2000), (7, 4), (150, 64)])
+                                 (2000, 1000), (3000, 2000), (7, 4), (150, 64),
+                                 # beyond the staged kernels' 2048 columns: the CTA-per-row kernel
+                                 (1500, 2049), (1201, 3000), (700, 4097), (300, 6000), (5, 8192)])
 def test_fused_pass_matches_numpy(pkg, m, n):
     import ctypes
 
@@ -895,6 +897,29 @@ def test_nonfinite_inputs_raise_like_the_reference(pkg, orc, shape):
     a[7, 1] = np.nan  # a zero column AND a NaN: R has a NaN pivot row, not a zero pivot -> ValueError
     with pytest.raises((ValueError, pkg.SingularMatrixError)):
         pkg.iterative_sketching(a, p.b, cfg)
+
+
+def test_wide_problem_parity(pkg, orc):
+    """n beyond the staged pass kernels' 2048 columns (the CTA-per-row pass,
+    the cluster tail and the global-R estimates): 15000 x 2100, momentum,
+    against the oracle on the same bytes — FE / RE within 2x, the stated
+    bound on x, the estimates to rounding."""
+    m, n, kappa, beta, d = 15000, 2100, 1e6, 1e-8, 16800
+    a, b, t = orc.gen_randsvd(m, n, kappa, beta, 0)
+    x_ref, tr = orc.iterative_sketching(a, b, orc.Config(d=d, variant="momentum"), t)
+    truth = pkg.Truth(x=t.x, r=t.r, kappa=t.kappa, beta=t.beta)
+    res = pkg.iterative_sketching(a, b, pkg.SolverConfig(d=d, variant="momentum"), truth)
+    it_ref = len(tr.iterates) - 1
+    # as at C4 (tests/test_gpu_c4.py): with 2100-term dots the rule's threshold
+    # lies under OpenBLAS's dgemv noise, so the oracle may run to max_iters where
+    # the device path stops by the rule; never the other way round
+    assert res.trace.stop_reason == "stopped_by_rule", res.trace.stop_reason
+    assert tr.stop_reason == "max_iters" or abs(res.iterations - it_ref) <= max(3, 0.15 * it_ref), (
+        res.iterations, it_ref, tr.stop_reason)
+    assert res.trace.fe[-1] <= 2 * tr.fe[-1] and res.trace.re[-1] <= 2 * tr.re[-1]
+    assert np.linalg.norm(res.solution - x_ref) / np.linalg.norm(x_ref) <= 10 * kappa * U + tr.fe[-1]
+    assert res.trace.normest == pytest.approx(tr.normest, rel=1e-10)
+    assert res.trace.condest == pytest.approx(tr.condest, rel=1e-8)
 
 
 def test_input_forms(pkg, orc):
