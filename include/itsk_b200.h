@@ -111,6 +111,12 @@ int itsk_sketch_rows(const double* A, int64_t m, int64_t n, int64_t lda, const d
  * synchronising) if some R_kk == 0, like _check_square_upper.
  * -------------------------------------------------------------------- */
 int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes);
+/* Row blocks of the factorisation: 1 = one Householder QR (W then holds the
+ * reflectors below the diagonal); more for a d beyond one factorisation's
+ * range (~50000 rows): TSQR over blocks of <= 24000 rows — each block with
+ * its share of the rhs column, then the stacked [R_i | z_i] — which returns
+ * the R and z of the whole matrix and leaves no single set of reflectors. */
+int itsk_qr_row_blocks(int64_t d, int64_t n, int64_t* blocks);
 int itsk_qr_aug(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double* z,
                 void* ws, int64_t ws_bytes, itsk_stream_t stream);
 /* The same without the host round trip: the factorisation's flags are

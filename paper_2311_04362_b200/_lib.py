@@ -86,6 +86,7 @@ _SIGS = {
     "itsk_sketch_rows": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_i64, c_dp,
                                         c_i64, c_i64, c_i64, ctypes.c_int, c_dp]),
     "itsk_qr_workspace": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
+    "itsk_qr_row_blocks": (ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(c_i64)]),
     "itsk_qr_aug": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_dp]),
     "itsk_qr_aug_async": (ctypes.c_int, [c_dp, c_i64, c_i64, c_i64, c_dp, c_dp, c_dp, c_i64, c_dp, c_dp]),
     "itsk_trsv": (ctypes.c_int, [c_dp, c_i64, c_dp, c_dp, ctypes.c_int, c_dp]),

@@ -548,10 +548,59 @@ using namespace itsk;
 
 constexpr int64_t V2_WS_OFFSET = 1024;  // bytes: [0,512) barrier, [512,1024) singular flag
 
+namespace {
+// A factorisation in one piece: the panel / update split (qr2.cu), or the
+// single-kernel QR while its rows fit a CTA's shared memory (~50000 rows).
+bool qr_direct_ok(int64_t d, int64_t n) {
+  if (qr_v2_plan(d, n).NB > 0) return true;
+  return qr_plan(nullptr, d, n, 1).smem <= QR_SMEM_MAX;
+}
+int64_t qr_direct_ws(int64_t d, int64_t n) {
+  int64_t b = std::max(qr_plan(nullptr, d, n, 1).ws_bytes, qr_plan(nullptr, d, n, 0).ws_bytes);
+  return std::max<int64_t>(b, V2_WS_OFFSET + 8 * qr_v2_plan(d, n).ws_doubles);
+}
+// Taller matrices: TSQR over row blocks (as stable as one Householder QR) —
+// each block of <= QR_BLOCK_ROWS rows is factored with its share of the rhs
+// column, the k stacked [R_i | z_i] (k n x (n+1)) are factored again; the
+// final R and z are those of the whole [A | b].
+constexpr int64_t QR_BLOCK_ROWS = 24000;
+struct QrBlocks {
+  int64_t k, hb;  // k blocks of hb rows (the last one shorter)
+};
+QrBlocks qr_blocks(int64_t d, int64_t n) {
+  if (qr_direct_ok(d, n)) return {1, d};
+  const int64_t k = (d + QR_BLOCK_ROWS - 1) / QR_BLOCK_ROWS;
+  return {k, (d + k - 1) / k};
+}
+struct QrBlockWs {
+  int64_t sub, total;           // bytes: the sub-factorisations' workspace, everything
+  int64_t s_off, r_off, z_off;  // byte offsets of the stack, the block's R and z
+};
+int64_t qr_total_ws(int64_t d, int64_t n);
+QrBlockWs qr_block_ws(int64_t d, int64_t n) {
+  const QrBlocks B = qr_blocks(d, n);
+  QrBlockWs w{};
+  w.sub = align_up(std::max(qr_direct_ws(B.hb, n), qr_total_ws(B.k * n, n)), 256);
+  w.s_off = w.sub;
+  w.r_off = align_up(w.s_off + B.k * n * (n + 1) * 8, 256);
+  w.z_off = align_up(w.r_off + n * n * 8, 256);
+  w.total = align_up(w.z_off + n * 8, 256) + 256;
+  return w;
+}
+int64_t qr_total_ws(int64_t d, int64_t n) {
+  return qr_blocks(d, n).k == 1 ? qr_direct_ws(d, n) : qr_block_ws(d, n).total;
+}
+}  // namespace
+
 extern "C" int itsk_qr_workspace(int64_t d, int64_t n, int64_t* bytes) {
   ITSK_REQUIRE(bytes && d >= n && n >= 1, "need d >= n >= 1");
-  *bytes = std::max(qr_plan(nullptr, d, n, 1).ws_bytes, qr_plan(nullptr, d, n, 0).ws_bytes);
-  *bytes = std::max<int64_t>(*bytes, V2_WS_OFFSET + 8 * qr_v2_plan(d, n).ws_doubles);
+  *bytes = qr_total_ws(d, n);
+  return ITSK_OK;
+}
+
+extern "C" int itsk_qr_row_blocks(int64_t d, int64_t n, int64_t* blocks) {
+  ITSK_REQUIRE(blocks && d >= n && n >= 1, "need d >= n >= 1");
+  *blocks = qr_blocks(d, n).k;
   return ITSK_OK;
 }
 
@@ -564,6 +613,31 @@ int qr_aug_core(double* W, int64_t d, int64_t n, int64_t ldw, double* R, double*
   ITSK_REQUIRE(n >= 1 && d >= n, "need m >= n, got %lld x %lld", (long long)d, (long long)n);
   const int has_rhs = z != nullptr;
   ITSK_REQUIRE(ldw >= n + has_rhs, "bad leading dimension");
+  const QrBlocks B = qr_blocks(d, n);
+  if (B.k > 1) {
+    ITSK_REQUIRE(2 * n <= B.hb, "qr: n=%lld is too wide for the row-blocked factorisation of %lld rows",
+                 (long long)n, (long long)d);
+    const QrBlockWs bw = qr_block_ws(d, n);
+    ITSK_REQUIRE(bw.total <= ws_bytes, "qr workspace too small (%lld < %lld)", (long long)ws_bytes,
+                 (long long)bw.total);
+    cudaStream_t bs = reinterpret_cast<cudaStream_t>(stream);
+    char* base = static_cast<char*>(ws);
+    double* S = reinterpret_cast<double*>(base + bw.s_off);
+    double* Rt = reinterpret_cast<double*>(base + bw.r_off);
+    double* zt = reinterpret_cast<double*>(base + bw.z_off);
+    const int64_t N = n + has_rhs;
+    for (int64_t i = 0; i < B.k; ++i) {
+      const int64_t r0 = i * B.hb, rows = std::min(B.hb, d - r0);
+      int* f = nullptr;
+      int rc = qr_aug_core(W + r0 * ldw, rows, n, ldw, Rt, has_rhs ? zt : nullptr, ws, bw.sub, stream, &f);
+      if (rc) return rc;
+      ITSK_CUDA(cudaMemcpy2DAsync(S + i * n * N, N * 8, Rt, n * 8, n * 8, n, cudaMemcpyDeviceToDevice, bs));
+      if (has_rhs)
+        ITSK_CUDA(cudaMemcpy2DAsync(S + i * n * N + n, N * 8, zt, 8, 8, n, cudaMemcpyDeviceToDevice, bs));
+    }
+    // (a block's own zero pivot is not the matrix's: only the last factorisation's flags count)
+    return qr_aug_core(S, B.k * n, n, N, R, z, ws, bw.sub, stream, flag);
+  }
   QrPlan L = qr_plan(ws, d, n, has_rhs);
   ITSK_REQUIRE(L.ws_bytes <= ws_bytes, "qr workspace too small (%lld < %lld)", (long long)ws_bytes,
                (long long)L.ws_bytes);

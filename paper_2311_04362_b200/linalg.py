@@ -55,8 +55,9 @@ class QrFactors:
         cached = self.__dict__.get("_q")
         if cached is None:
             if self._v is None:
-                raise AttributeError("QrFactors.q: built without the Householder vectors; use "
-                                     "householder_qr_econ(a) to get a QrFactors that can form Q")
+                raise AttributeError("QrFactors.q: built without the Householder vectors (by hand, or by the "
+                                     "row-blocked QR of more than ~50000 rows); householder_qr_econ(a) of a "
+                                     "shorter matrix returns a QrFactors that can form Q")
             qd = _form_q(self._v, self.r.shape[0], self._a)
             cached = _dev.to_numpy(qd) if self._host else qd
             object.__setattr__(self, "_q", cached)
@@ -90,6 +91,13 @@ def _form_q(w: torch.Tensor, n: int, a: torch.Tensor, nb: int = 128) -> torch.Te
     sgn = torch.where(sgn == 0, torch.ones_like(sgn), sgn)
     q.mul_(sgn)
     return q
+
+
+def qr_row_blocks(d: int, n: int, dev) -> int:
+    """Row blocks of the device QR of a d x n matrix (itsk_qr_row_blocks)."""
+    k = ctypes.c_int64()
+    _lib.check(_dev.lib(dev).itsk_qr_row_blocks(d, n, ctypes.byref(k)))
+    return int(k.value)
 
 
 def qr_workspace(d: int, n: int, dev) -> torch.Tensor:
@@ -136,7 +144,10 @@ def householder_qr_econ(a, rhs=None) -> QrFactors:
         w[:, n] = _dev.as_device_vector(rhs, dev)
     r, z = qr_aug(w, n)
     # w (the Householder vectors) and the input stay on the device behind the
-    # result so that .q can be formed on request
+    # result so that .q can be formed on request — unless the factorisation
+    # ran over row blocks (TSQR beyond ~50000 rows: no single set of reflectors)
+    if qr_row_blocks(d, n, dev) > 1:
+        w = at = None
     if host:
         return QrFactors(r=_dev.to_numpy(r), z=None if z is None else _dev.to_numpy(z), _v=w, _a=at, _host=True)
     return QrFactors(r=r, z=z, _v=w, _a=at)

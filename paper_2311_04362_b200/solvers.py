@@ -634,7 +634,7 @@ def sketch_and_solve(a, b, s: SparseSignEmbedding):
     """Sketch-and-solve start (solvers.py:199-210): x0 = R^-1 (Q'Sb)[:n] with
     R from the QR of S·A.  Returns (x0, QrFactors(r, z)); the factors' Q (of
     S·A, linalg.py:42) is formed only if `.q` is read."""
-    from .linalg import QrFactors, qr_aug
+    from .linalg import QrFactors, qr_aug, qr_row_blocks
 
     host = not isinstance(a, torch.Tensor)
     dev = s.rows_dev.device
@@ -644,6 +644,8 @@ def sketch_and_solve(a, b, s: SparseSignEmbedding):
     w = s.apply_dense(at, bt)
     sa = w[:, :n].clone()  # S·A before the QR overwrites it (the sign reference of QrFactors.q)
     r, z = qr_aug(w, n)
+    if qr_row_blocks(w.shape[0], n, dev) > 1:
+        w = sa = None  # row-blocked QR: no single set of reflectors to form Q from
     if not bool(torch.isfinite(r).all() & torch.isfinite(z).all()):
         raise ValueError(NONFINITE_MSG)  # tri_solve_upper's check_finite (linalg.py:59-62)
     x0 = torch.empty(n, dtype=torch.float64, device=dev)

@@ -308,6 +308,29 @@ def test_qr_large_d_fallback_matches_lapack(pkg, orc, m, n, seed):
     assert np.linalg.norm(f.z - q_ref.T @ rhs) <= 100 * n * U * np.linalg.norm(rhs)
 
 
+@pytest.mark.parametrize("m,n,seed", [(100000, 200, 3), (120001, 700, 5), (260000, 64, 7), (104000, 1000, 8)])
+def test_qr_row_blocked_matches_lapack(pkg, orc, m, n, seed):
+    """Beyond one factorisation's range (~50000 rows): TSQR over row blocks of
+    <= 24000 rows, each with its share of the rhs column, then the stacked
+    [R_i | z_i] — the same R (diag >= 0) and z = Q'b as LAPACK's single QR to
+    the usual bar; no single set of reflectors, so .q says it is unavailable."""
+    from paper_2311_04362_b200.linalg import qr_row_blocks
+
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    rhs = rng.standard_normal(m)
+    assert qr_row_blocks(m, n, torch.device("cuda", 0)) >= 2
+    f = pkg.householder_qr_econ(a, rhs)
+    q_ref, r_ref = orc.householder_qr_econ(a)
+    assert np.all(np.diag(f.r) >= 0) and np.array_equal(f.r, np.triu(f.r))
+    assert np.linalg.norm(f.r - r_ref) <= 100 * n * U * np.linalg.norm(r_ref)
+    assert np.linalg.norm(f.z - q_ref.T @ rhs) <= 100 * n * U * np.linalg.norm(rhs)
+    with pytest.raises(AttributeError, match="row-blocked"):
+        f.q
+    f2 = pkg.householder_qr_econ(a, rhs)
+    assert np.array_equal(f.r, f2.r) and np.array_equal(f.z, f2.z)
+
+
 def test_qr_hand_cases(pkg):
     f = pkg.householder_qr_econ(np.array([[3.0], [4.0]]))
     np.testing.assert_allclose(f.r, [[5.0]], rtol=1e-15)
